@@ -1,0 +1,310 @@
+"""ctypes binding of the CPU oracle (oracle/liboracle.so).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs, where it is the checker or the
+timed CPU baseline -- never the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+ERRORS = {2: "ConfigError", 3: "DataError", 4: "NumericError", 1: "Error"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+        self.kind = ERRORS.get(code, "Error")
+
+
+class Params(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("sigma2", "sigma1_2", "a", "c", "alpha", "nu", "beta", "delta")]
+
+
+class Model(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int), ("policy", C.c_int), ("n", C.c_int),
+        ("x", C.c_void_p), ("y", C.c_void_p), ("t", C.c_void_p),
+        ("nbr", C.c_void_p), ("m_v", C.c_int), ("M", C.c_int),
+        ("zx", C.c_void_p), ("zy", C.c_void_p), ("zt", C.c_void_p),
+        ("theta", Params),
+    ]
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB):
+            build()
+        _lib = C.CDLL(_LIB)
+        _lib.orc_last_error.restype = C.c_char_p
+        _lib.orc_exp.restype = C.c_double
+        _lib.orc_exp.argtypes = [C.c_double]
+        _lib.orc_kernel_eval.restype = C.c_double
+        _lib.orc_kernel_eval.argtypes = [C.POINTER(Params), C.c_double, C.c_double]
+        _lib.orc_dc_pair.restype = C.c_double
+        _lib.orc_dc_pair.argtypes = [C.POINTER(Params)] + [C.c_double] * 6
+        _lib.orc_mix_seed.restype = C.c_uint64
+        _lib.orc_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _chk(rc: int):
+    if rc != 0:
+        raise OracleError(rc, lib().orc_last_error().decode())
+
+
+def params(theta) -> Params:
+    if isinstance(theta, Params):
+        return theta
+    if isinstance(theta, dict):
+        return Params(**theta)
+    if hasattr(theta, "as_tuple"):
+        return Params(*theta.as_tuple())
+    return Params(*theta)
+
+
+def set_threads(n: int) -> int:
+    return lib().orc_set_threads(int(n))
+
+
+def set_prune(on: bool):
+    lib().orc_set_prune(int(bool(on)))
+
+
+def kernel_eval(theta, h, u) -> float:
+    return lib().orc_kernel_eval(C.byref(params(theta)), float(h), float(u))
+
+
+def kernel_grad(theta, h, u) -> np.ndarray:
+    g = np.zeros(6)
+    _chk(lib().orc_kernel_grad(C.byref(params(theta)), C.c_double(h), C.c_double(u), _p(g)))
+    return g
+
+
+def effective_ranges(theta):
+    tr, sr = C.c_double(), C.c_double()
+    _chk(lib().orc_effective_ranges(C.byref(params(theta)), C.byref(tr), C.byref(sr)))
+    return tr.value, sr.value
+
+
+def mix_seed(seed: int, stream: int) -> int:
+    return int(lib().orc_mix_seed(seed, stream))
+
+
+def exp(x: float) -> float:
+    return lib().orc_exp(float(x))
+
+
+def order_observations(t, seed: int) -> np.ndarray:
+    t = _f64(t)
+    perm = np.zeros(len(t), dtype=np.int32)
+    _chk(lib().orc_order_observations(C.c_int(len(t)), _p(t), C.c_uint64(seed), _p(perm)))
+    return perm
+
+
+def test_dataset(kind: int, n: int, seed: int, n_times: int = 10, p: int = 0):
+    """Reference test-suite datasets (see orc_test_dataset)."""
+    nn = n * n_times if kind == 2 else n
+    x, y, t, yv = (np.zeros(nn) for _ in range(4))
+    X = np.zeros((nn, max(p, 0)), order="F")
+    _chk(lib().orc_test_dataset(kind, n, C.c_uint64(seed), n_times, p, _p(x), _p(y), _p(t), _p(yv),
+                                _p(X) if p > 0 else None))
+    return x, y, t, yv, X
+
+
+def dc_pair(theta, a, b) -> float:
+    return lib().orc_dc_pair(C.byref(params(theta)), *map(float, a), *map(float, b))
+
+
+def dc_neighbors(x, y, t, theta, m_v: int, with_dist: bool = False):
+    x, y, t = _f64(x), _f64(y), _f64(t)
+    n = len(x)
+    out = np.zeros((n, m_v), dtype=np.int32)
+    dist = np.zeros((n, m_v)) if with_dist else None
+    _chk(lib().orc_dc_neighbors(n, _p(x), _p(y), _p(t), C.byref(params(theta)), m_v, _p(out), _p(dist)))
+    return (out, dist) if with_dist else out
+
+
+def dc_neighbors_range(x, y, t, theta, m_v: int, q0: int, q1: int):
+    x, y, t = _f64(x), _f64(y), _f64(t)
+    out = np.zeros((q1 - q0, m_v), dtype=np.int32)
+    _chk(lib().orc_dc_neighbors_range(len(x), _p(x), _p(y), _p(t), C.byref(params(theta)), m_v, q0, q1, _p(out)))
+    return out
+
+
+def dr_neighbors(x, y, t, theta, Z, m_v: int, with_dist: bool = False, with_w: bool = False):
+    x, y, t = _f64(x), _f64(y), _f64(t)
+    Z = np.asarray(Z, dtype=np.float64).reshape(-1, 3)
+    zx, zy, zt = _f64(Z[:, 0]), _f64(Z[:, 1]), _f64(Z[:, 2])
+    n, M = len(x), len(Z)
+    out = np.zeros((n, m_v), dtype=np.int32)
+    dist = np.zeros((n, m_v)) if with_dist else None
+    W = np.zeros((n, M)) if with_w else None  # column-major M x n == row-major n x M
+    resid = np.zeros(n) if with_w else None
+    _chk(lib().orc_dr_neighbors(n, _p(x), _p(y), _p(t), C.byref(params(theta)), M, _p(zx), _p(zy), _p(zt),
+                                m_v, _p(out), _p(dist), _p(W), _p(resid)))
+    res = [out]
+    if with_dist:
+        res.append(dist)
+    if with_w:
+        res += [W, resid]
+    return res[0] if len(res) == 1 else tuple(res)
+
+
+def euclid_neighbors(x, y, t, m_v: int, ss: float, ts: float):
+    x, y, t = _f64(x), _f64(y), _f64(t)
+    n = len(x)
+    out = np.zeros((n, m_v), dtype=np.int32)
+    _chk(lib().orc_euclid_neighbors(n, _p(x), _p(y), _p(t), m_v, C.c_double(ss), C.c_double(ts), _p(out)))
+    return out
+
+
+def kmeanspp(points, k: int, seed: int) -> np.ndarray:
+    P = np.asfortranarray(np.asarray(points, dtype=np.float64).reshape(len(points), -1))
+    n, d = P.shape
+    out = np.zeros((k, d), order="F")
+    _chk(lib().orc_kmeanspp(_p(P), n, d, k, C.c_uint64(seed), _p(out)))
+    return np.ascontiguousarray(out)
+
+
+def sts_kmeanspp(x, y, t, m: int, seed: int):
+    x, y, t = _f64(x), _f64(y), _f64(t)
+    cap = max(m, 1) * 4 + 16
+    out = np.zeros((cap, 3))
+    ms, mt = C.c_int(), C.c_int()
+    _chk(lib().orc_sts_kmeanspp(len(x), _p(x), _p(y), _p(t), m, C.c_uint64(seed), C.byref(ms), C.byref(mt), _p(out), cap))
+    return out[: ms.value * mt.value].copy(), ms.value, mt.value
+
+
+def joint_kmeanspp(x, y, t, m: int, ss: float, ts: float, seed: int):
+    x, y, t = _f64(x), _f64(y), _f64(t)
+    out = np.zeros((m, 3))
+    k = C.c_int()
+    _chk(lib().orc_joint_kmeanspp(len(x), _p(x), _p(y), _p(t), m, C.c_double(ss), C.c_double(ts), C.c_uint64(seed),
+                                  C.byref(k), _p(out), m))
+    return out[: k.value].copy()
+
+
+KIND = {"vecchia": 0, "fitc": 1, "vif": 2}
+
+
+class OracleModel:
+    """A model description for the oracle's structure functions."""
+
+    def __init__(self, kind, x, y, t, theta, nbr=None, Z=None, policy="observation"):
+        self._keep = []
+        self.x, self.y, self.t = _f64(x), _f64(y), _f64(t)
+        self.n = len(self.x)
+        self.nbr = None if nbr is None else np.ascontiguousarray(nbr, dtype=np.int32)
+        m_v = 0 if self.nbr is None else self.nbr.shape[1]
+        if self.nbr is None:
+            self.nbr = np.zeros((self.n, 1), dtype=np.int32) - 1
+            m_v = 1
+        Z = np.zeros((0, 3)) if Z is None else np.asarray(Z, dtype=np.float64).reshape(-1, 3)
+        self.zx, self.zy, self.zt = _f64(Z[:, 0]), _f64(Z[:, 1]), _f64(Z[:, 2])
+        self.m = Model(KIND[kind] if isinstance(kind, str) else kind,
+                       1 if policy in ("observation", 1) else 0, self.n,
+                       _p(self.x), _p(self.y), _p(self.t), _p(self.nbr), m_v, len(Z),
+                       _p(self.zx), _p(self.zy), _p(self.zt), params(theta))
+
+    @staticmethod
+    def _xb(n, X, beta):
+        if X is None or beta is None or np.size(beta) == 0:
+            return 0, None, None
+        X = np.asfortranarray(np.asarray(X, dtype=np.float64).reshape(n, -1))
+        return X.shape[1], X, _f64(beta)
+
+    def rows(self):
+        D = np.zeros(self.n)
+        A = np.zeros(self.nbr.shape)
+        _chk(lib().orc_build_rows(C.byref(self.m), _p(D), _p(A)))
+        return D, A
+
+    def fitc_diag(self):
+        d = np.zeros(self.n)
+        _chk(lib().orc_fitc_diag(C.byref(self.m), _p(d)))
+        return d
+
+    def nll(self, yv, X=None, beta=None) -> float:
+        p, Xf, b = self._xb(self.n, X, beta)
+        yv = _f64(yv)
+        out = C.c_double()
+        _chk(lib().orc_nll(C.byref(self.m), _p(yv), p, _p(Xf), _p(b), C.byref(out)))
+        return out.value
+
+    def nll_grad(self, yv, X=None, beta=None) -> np.ndarray:
+        p, Xf, b = self._xb(self.n, X, beta)
+        yv = _f64(yv)
+        g = np.zeros(7)
+        _chk(lib().orc_nll_grad(C.byref(self.m), _p(yv), p, _p(Xf), _p(b), _p(g)))
+        return g
+
+    def gls_beta(self, yv, X) -> np.ndarray:
+        X = np.asfortranarray(np.asarray(X, dtype=np.float64).reshape(self.n, -1))
+        yv = _f64(yv)
+        out = np.zeros(X.shape[1])
+        _chk(lib().orc_gls_beta(C.byref(self.m), _p(yv), X.shape[1], _p(X), _p(out)))
+        return out
+
+    def predict(self, yv, targets, pred_m_v: int, X=None, beta=None, Xp=None):
+        p, Xf, b = self._xb(self.n, X, beta)
+        T = np.asarray(targets, dtype=np.float64).reshape(-1, 3)
+        qx, qy, qt = _f64(T[:, 0]), _f64(T[:, 1]), _f64(T[:, 2])
+        npred = len(T)
+        Xpf = None if Xp is None or p == 0 else np.asfortranarray(np.asarray(Xp, dtype=np.float64).reshape(npred, -1))
+        mu, var = np.zeros(npred), np.zeros(npred)
+        yv = _f64(yv)
+        _chk(lib().orc_predict(C.byref(self.m), _p(yv), p, _p(Xf), _p(b), npred, _p(qx), _p(qy), _p(qt), _p(Xpf),
+                               pred_m_v, _p(mu), _p(var)))
+        return mu, var
+
+
+def dense_nll(x, y, t, theta, yv, X=None, beta=None) -> float:
+    x, y, t, yv = _f64(x), _f64(y), _f64(t), _f64(yv)
+    p, Xf, b = OracleModel._xb(len(x), X, beta)
+    out = C.c_double()
+    _chk(lib().orc_dense_nll(len(x), _p(x), _p(y), _p(t), C.byref(params(theta)), _p(yv), p, _p(Xf), _p(b), C.byref(out)))
+    return out.value
+
+
+def dense_predict(x, y, t, theta, yv, targets):
+    x, y, t, yv = _f64(x), _f64(y), _f64(t), _f64(yv)
+    T = np.asarray(targets, dtype=np.float64).reshape(-1, 3)
+    qx, qy, qt = _f64(T[:, 0]), _f64(T[:, 1]), _f64(T[:, 2])
+    mu, var = np.zeros(len(T)), np.zeros(len(T))
+    _chk(lib().orc_dense_predict(len(x), _p(x), _p(y), _p(t), C.byref(params(theta)), _p(yv), len(T), _p(qx), _p(qy),
+                                 _p(qt), _p(mu), _p(var)))
+    return mu, var
+
+
+def full_conditioning(n: int) -> np.ndarray:
+    """test_approximations.cpp:34-43: N(i) = {0..i-1}."""
+    nb = np.full((n, max(n - 1, 1)), -1, dtype=np.int32)
+    for i in range(1, n):
+        nb[i, :i] = np.arange(i)
+    return nb
