@@ -1,0 +1,296 @@
+"""Benchmark: NLL+gradient evaluations per second of the Vecchia/VIF likelihood at
+n = 1.1M, m = 30 (BASELINE.json metric), on synthetic NOAA-shaped station x day data.
+
+One "step" = one optimizer evaluation: rebuild the structure at theta and
+compute the NLL and its 7-component gradient (estimation.cpp:277-325), over all
+n observations.  Neighbour search and inducing-point seeding are setup (their
+wall time is reported separately as nn_search_s / seeding_s).
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+        [--workload vecchia|vif] [--stations S] [--days D]
+For N > 1 launch under torch.distributed.run (one process per GPU); observations
+are sharded by contiguous index ranges and partial sums all-reduced with NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "VIF/Vecchia NLL+grad evals/sec at n=1.1M, m=30 (1/2/4/8 B200); NN-search s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="vecchia", choices=["vecchia", "vif"])
+    ap.add_argument("--stations", type=int, default=10000)
+    ap.add_argument("--days", type=int, default=110)
+    ap.add_argument("--m_v", type=int, default=30)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 3 + k and r[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_data(stations, days, seed=20260203):
+    import paper_2602_03609_b200 as S
+    theta = S.synth.THETA_T3 if stations >= 2000 else S.synth.THETA_SEC4
+    box = (4.6e6, 2.9e6) if stations >= 2000 else (1.0, 1.0)
+    x, y, t, resp = S.synth.station_day(stations, days, box=box, theta=theta, seed=seed)
+    perm = S.order_observations_perm(t, seed)
+    return x[perm], y[perm], t[perm], resp[perm], theta
+
+
+# canonical algorithmic FP64 work per row: FMA = k^3/6 + 3 k^2 (Cholesky,
+# two triangular solves per RHS, products), plus c_k kernel evaluations and c_k kernel
+# gradients; KE = 30 flop, KG = 50 flop (device instruction counts of gneiting_eval /
+# gneiting_grad incl. the exp port).
+KE_FLOP, KG_FLOP = 30.0, 50.0
+
+
+def vecchia_flops(nbr_counts):
+    k = nbr_counts.astype(np.float64)
+    ck = (k + 1) * (k + 2) / 2
+    return float(np.sum(2 * (k ** 3 / 6 + 3 * k ** 2) + ck * (KE_FLOP + KG_FLOP)))
+
+
+def cpu_sample_vecchia(x, y, t, resp, theta, nbr, target_s=10.0):
+    """Time the oracle (reference algorithm restated: build + nll + build + nll_grad,
+    i.e. Objective::value + Objective::gradient) on a prefix of the ordered rows; a
+    prefix with its own neighbour rows is a self-contained Vecchia model."""
+    from oracle import oracle as O
+    cores = O.set_threads(os.cpu_count() or 1)
+    n = len(x)
+    ns = min(n, 20000)
+    while True:
+        om = O.OracleModel("vecchia", x[:ns], y[:ns], t[:ns], theta, nbr=nbr[:ns])
+        t0 = time.perf_counter()
+        om.nll(resp[:ns])
+        om.nll_grad(resp[:ns])
+        dt = time.perf_counter() - t0
+        if dt >= 2.0 or ns >= n:
+            break
+        ns = min(n, int(ns * max(2.0, min(target_s / max(dt, 1e-3), 20.0))))
+    per_eval_full = dt * n / ns
+    return {"value": 1.0 / per_eval_full, "unit": "evals/s", "cores": cores, "kind": "port",
+            "sample": f"oracle build+nll+build+nll_grad on the first {ns} of {n} ordered rows "
+                      f"({dt:.2f} s), scaled linearly to n"}
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm's CPU path (oracle port; the reference
+    itself cannot be built here) on all host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    import paper_2602_03609_b200.synth as synth
+    x, y, t, resp, theta = make_data(args.stations, args.days)
+    n = len(x)
+    m_v = args.m_v
+    cores = O.set_threads(os.cpu_count() or 1)
+    # neighbour rows for the sample prefix (the oracle's own exact search)
+    ns = min(n, 30000)
+    nbr = O.dc_neighbors(x[:ns], y[:ns], t[:ns], theta, m_v)
+    times = []
+    for step in range(args.warmup + args.steps):
+        om = O.OracleModel("vecchia", x[:ns], y[:ns], t[:ns], theta, nbr=nbr)
+        t0 = time.perf_counter()
+        om.nll(resp[:ns])
+        om.nll_grad(resp[:ns])
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt * n / ns)
+    per = statistics.median(times)
+    val = 1.0 / per
+    line = {"metric": METRIC, "value": val, "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg4-{args.workload}-dc" if args.workload == "vecchia" else "cfg4-vif",
+                       "n": n, "m_v": m_v, "stations": args.stations, "days": args.days},
+            "impl": "reference",
+            "cpu_baseline": {"value": val, "unit": "evals/s", "cores": cores, "kind": "port",
+                             "sample": f"oracle build+nll+build+nll_grad on the first {ns} of {n} ordered rows per "
+                                       "step, scaled linearly to n"},
+            "e2e": {"value": val, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import paper_2602_03609_b200 as S
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("gloo")
+    ctx = S.Context(local)
+    if dist:
+        uid = [S.Context.nccl_unique_id() if rank == 0 else None]
+        tdist.broadcast_object_list(uid, src=0)
+        ctx.init_nccl(uid[0], rank, world)
+        ctx.set_shard(rank, world)
+
+    x, y, t, resp, theta = make_data(args.stations, args.days)
+    n = len(x)
+    ds = S.SpaceTimeDataset(x, y, t, resp, ctx=ctx)
+    ctx.profile(True)
+    t0 = time.perf_counter()
+    nb = S.correlation_neighbors(ds, theta, args.m_v)
+    nn_s = time.perf_counter() - t0
+    knn_ms, _ = ctx.profile_get("knn_dc")
+    nbr = nb.indices()
+    counts = (nbr >= 0).sum(axis=1)
+    s = S.build_vecchia(ds, theta, nb, S.OBSERVATION)
+
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
+    thetas = [tuple(v * (1.0 + 0.01 * ((i % 5) - 2)) if j in (1, 2, 3) else v for j, v in enumerate(theta))
+              for i in range(args.warmup + args.steps)]
+    for i in range(args.warmup):
+        S.evaluate(s, thetas[i])
+    ctx.profile_reset()
+    launches0 = ctx.kernel_launches()
+    if dist:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for i in range(args.steps):
+            v, g = S.evaluate(s, thetas[args.warmup + i])
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms_total = e0.elapsed_time(e1)
+    launches = ctx.kernel_launches() - launches0
+    rows_ms, rows_cnt = ctx.profile_get("rows")
+    ms_step = ms_total / args.steps
+    if dist:
+        tt = torch.tensor([ms_step], dtype=torch.float64)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        ms_step = float(tt[0])
+
+    # e2e: the public API with host buffers (pinned y uploaded each step, nll+grad read back)
+    pinned = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    pinned[:] = resp
+    S.evaluate(s, thetas[0], pinned)
+    if dist:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        v2, g2 = S.evaluate(s, thetas[args.warmup + i], pinned)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    if dist:
+        tt = torch.tensor([e2e_s], dtype=torch.float64)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        e2e_s = float(tt[0])
+
+    # roofline of the dominant kernel (per-row fused build + NLL + gradient)
+    lo, hi = int(n * rank / world), int(n * (rank + 1) / world)
+    flops_launch = vecchia_flops(counts[lo:hi])
+    rows_avg_ms = rows_ms / max(rows_cnt, 1)
+    fp64_peak = ctx.fp64_peak_tflops()
+    achieved = flops_launch / (rows_avg_ms * 1e-3) / 1e12
+    roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+            "frac": achieved / fp64_peak, "traffic": None, "kernel": "vecchia_rows_kernel<grad>",
+            "kernel_ms": rows_avg_ms, "kernel_share": rows_avg_ms / ms_step,
+            "peak_source": "measured in-run: DFMA throughput microbenchmark (MEASURED_PEAKS.json has no FP64 entry)",
+            "flop_per_launch": flops_launch}
+
+    line = {"metric": METRIC, "value": 1e3 / ms_step, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (station x day layout of simulate.cpp, random-feature field + nugget)",
+            "config": {"workload": "cfg4-vecchia-dc", "n": n, "m_v": args.m_v, "stations": args.stations,
+                       "days": args.days, "theta": "PAPER.md Table 3 (NOAA temperature)",
+                       "neighbors": "d_c exact kNN (correlation_neighbors)", "parallelism": f"index-shard x{world}",
+                       "l2": "inputs larger than L2 (nbr 132 MB + A 264 MB per eval)"},
+            "nn_search_s": nn_s, "nn_search_kernel_ms": knn_ms, "nll": v, "grad": list(g),
+            "e2e": {"value": 1.0 / e2e_s, "unit": "evals/s", "h2d_bytes_per_step": n * 8 + 64,
+                    "d2h_bytes_per_step": 64},
+            "gpu_launches": launches, "roofline": roof, "clocks": clk.summary()}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_sample_vecchia(x, y, t, resp, theta, nbr)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

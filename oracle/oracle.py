@@ -120,6 +120,14 @@ def exp(x: float) -> float:
     return lib().orc_exp(float(x))
 
 
+def exp_array(x) -> np.ndarray:
+    """host glibc exp, element-wise (numpy's exp is not glibc's)."""
+    x = _f64(x)
+    out = np.zeros_like(x)
+    lib().orc_exp_array(C.c_long(len(x)), _p(x), _p(out))
+    return out
+
+
 def order_observations(t, seed: int) -> np.ndarray:
     t = _f64(t)
     perm = np.zeros(len(t), dtype=np.int32)

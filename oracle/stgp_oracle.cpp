@@ -1406,6 +1406,10 @@ extern "C" {
 
 const char* orc_last_error(void) { return g_err.c_str(); }
 double orc_exp(double x) { return std::exp(x); }
+void orc_exp_array(long n, const double* x, double* out) {
+#pragma omp parallel for schedule(static)
+  for (long i = 0; i < n; ++i) out[i] = std::exp(x[i]);
+}
 uint64_t orc_mix_seed(uint64_t seed, uint64_t stream) { return mix_seed(seed, stream); }
 int orc_set_threads(int n) {
 #ifdef _OPENMP

@@ -49,6 +49,7 @@ typedef struct {
 
 const char* orc_last_error(void);
 double orc_exp(double x);
+void orc_exp_array(long n, const double* x, double* out);
 uint64_t orc_mix_seed(uint64_t seed, uint64_t stream);
 double orc_kernel_eval(const orc_params* p, double h, double u);
 int orc_kernel_grad(const orc_params* p, double h, double u, double* g6);

@@ -1,0 +1,78 @@
+// Multi-GPU plumbing: one process per GPU, observations sharded by contiguous
+// index ranges; partial sums are all-reduced with NCCL over
+// NVLink/NVSwitch.  Without a communicator a context returns its shard's
+// partials (used by the single-GPU shard emulation tests).
+#include <nccl.h>
+
+#include <cstring>
+
+#include "comm.hpp"
+#include "structure.hpp"
+#include "../../include/stgp_b200.h"
+
+namespace stgp {
+
+void allreduce_sum(stgp_ctx* ctx, double* dev, size_t count) {
+  if (!ctx->comm || ctx->world == 1) return;
+  const ncclResult_t r = ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, reinterpret_cast<ncclComm_t>(ctx->comm),
+                                       ctx->stream);
+  if (r != ncclSuccess) throw Error(kInternal, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+}
+
+void allreduce_host(stgp_ctx* ctx, std::vector<double>& v) {
+  if (!ctx->comm || ctx->world == 1) return;
+  DevBuf<double> d;
+  d.upload(v.data(), v.size(), ctx->stream);
+  allreduce_sum(ctx, d.get(), v.size());
+  d.download(v.data(), v.size(), ctx->stream);
+  STGP_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void shard_rows(const stgp_ctx* ctx, int n, int& begin, int& end) {
+  begin = static_cast<int>(static_cast<long long>(n) * ctx->rank / ctx->world);
+  end = static_cast<int>(static_cast<long long>(n) * (ctx->rank + 1) / ctx->world);
+}
+
+}  // namespace stgp
+
+extern "C" {
+
+int stgp_nccl_unique_id(void* out128) {
+  ncclUniqueId id;
+  const ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) {
+    stgp::g_last_error = std::string("ncclGetUniqueId: ") + ncclGetErrorString(r);
+    return STGP_ERR_INTERNAL;
+  }
+  std::memcpy(out128, &id, sizeof(id));
+  return STGP_OK;
+}
+
+int stgp_ctx_init_nccl(stgp_ctx* ctx, const void* uid, int rank, int world) {
+  if (!ctx || !uid || world < 1 || rank < 0 || rank >= world) {
+    stgp::g_last_error = "stgp_ctx_init_nccl: bad argument";
+    return STGP_ERR_CONFIG;
+  }
+  cudaSetDevice(ctx->device);
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof(id));
+  ncclComm_t comm;
+  const ncclResult_t r = ncclCommInitRank(&comm, world, id, rank);
+  if (r != ncclSuccess) {
+    stgp::g_last_error = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+    return STGP_ERR_INTERNAL;
+  }
+  ctx->comm = reinterpret_cast<ncclComm*>(comm);
+  ctx->rank = rank;
+  ctx->world = world;
+  return STGP_OK;
+}
+
+void stgp_ctx_release_comm(stgp_ctx* ctx) {
+  if (ctx && ctx->comm) {
+    ncclCommDestroy(reinterpret_cast<ncclComm_t>(ctx->comm));
+    ctx->comm = nullptr;
+  }
+}
+
+}  // extern "C"

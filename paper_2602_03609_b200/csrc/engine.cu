@@ -1,0 +1,815 @@
+// Host orchestration of the stgp B200 engine and the C ABI (include/stgp_b200.h).
+//
+// Host code here only sequences device work, tabulates per-lag temporal factors
+// with glibc (bit-identical to the reference's pow/log) and moves O(1)-sized
+// results.  Every O(n) loop of the hot path runs in a CUDA kernel.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <numeric>
+#include <random>
+#include <set>
+
+#include "engine.hpp"
+#include "rows.cuh"
+#include "rows_serial.cuh"
+#include "search.cuh"
+#include "structure.hpp"
+#include "../../include/stgp_b200.h"
+
+namespace stgp {
+
+thread_local std::string g_last_error;
+
+void validate_params(const Params& p) {
+  auto fail = [](const char* w) { config_error(std::string("CovarianceParams: ") + w); };
+  if (!(p.sigma2 >= 0.0) || !std::isfinite(p.sigma2)) fail("sigma2 must be >= 0");
+  if (!(p.sigma1_2 > 0.0) || !std::isfinite(p.sigma1_2)) fail("sigma1_2 must be > 0");
+  if (!(p.a > 0.0) || !std::isfinite(p.a)) fail("a must be > 0");
+  if (!(p.c > 0.0) || !std::isfinite(p.c)) fail("c must be > 0");
+  if (!(p.alpha > 0.0 && p.alpha <= 1.0)) fail("alpha must be in (0, 1]");
+  if (!(p.nu > 0.0) || !std::isfinite(p.nu)) fail("nu must be > 0");
+  if (!(p.beta >= 0.0 && p.beta <= 1.0)) fail("beta must be in [0, 1]");
+  if (!(p.delta >= 0.0) || !std::isfinite(p.delta)) fail("delta must be >= 0");
+}
+
+static double exponent_E(const Params& p) { return p.delta + p.beta * 2 / 2.0; }
+
+TF host_factors(const Params& p, double u) {
+  TF f;
+  if (u == 0.0) {
+    f.u2a = 0.0;
+    f.u2a_logu = 0.0;
+    f.pow_mE = 1.0;
+    f.pow_mbh = 1.0;
+    f.inv_T = 1.0;
+    f.log_T = 0.0;
+    return f;
+  }
+  f.u2a = std::pow(u, 2.0 * p.alpha);
+  f.u2a_logu = f.u2a * std::log(u);
+  const double T = p.a * f.u2a + 1.0;
+  f.inv_T = 1.0 / T;
+  f.log_T = std::log(T);
+  f.pow_mE = std::pow(T, -exponent_E(p));
+  f.pow_mbh = std::pow(T, -p.beta / 2.0);
+  return f;
+}
+
+void host_grad00(const Params& p, double g[6]) {
+  // GneitingKernel::grad(0, 0): x = 0, M = 1, M' = matern_corr_deriv(0)
+  const double x = 0.0;
+  const double M = 1.0;
+  const double Mp = p.nu == 0.5 ? -1.0 : (p.nu == 1.5 ? -x * 1.0 : -(x * (1.0 + x) / 3.0) * 1.0);
+  const double base = p.sigma1_2 * 1.0;
+  const double E = exponent_E(p);
+  g[0] = 1.0 * M;
+  const double dC_dT = base * 1.0 * (-E * M - 0.5 * p.beta * x * Mp);
+  g[1] = dC_dT * 0.0;
+  g[3] = dC_dT * 2.0 * p.a * 0.0;
+  g[2] = base * Mp * x / p.c;
+  g[4] = -0.0 * base * (M + 0.5 * x * Mp);
+  g[5] = -0.0 * base * M;
+}
+
+DevKernel dev_kernel(const Params& p) {
+  DevKernel k;
+  k.s1 = p.sigma1_2;
+  k.c = p.c;
+  k.a = p.a;
+  k.beta = p.beta;
+  k.E = exponent_E(p);
+  k.nu_code = nu_code_of(p.nu);
+  if (k.nu_code < 0)
+    config_error("device kernels support nu in {0.5, 1.5, 2.5} (Matern closed forms, covariance.cpp:66-71)");
+  return k;
+}
+
+uint64_t mix_seed(uint64_t seed, uint64_t stream) {
+  uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (stream + 1);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+void TimeIndex::build() {
+  const int nt = nT();
+  if (nt > 4096)
+    config_error("more than 4096 distinct time values: the device lag tables need a discrete time axis");
+  std::vector<double> all;
+  all.reserve(static_cast<size_t>(nt) * (nt + 1) / 2);
+  for (int a = 0; a < nt; ++a)
+    for (int b = 0; b <= a; ++b) all.push_back(std::abs(T[static_cast<size_t>(a)] - T[static_cast<size_t>(b)]));
+  std::sort(all.begin(), all.end());
+  all.erase(std::unique(all.begin(), all.end()), all.end());
+  lags = all;
+  lagid.assign(static_cast<size_t>(nt) * nt, 0);
+  for (int a = 0; a < nt; ++a)
+    for (int b = 0; b <= a; ++b) {
+      const double u = std::abs(T[static_cast<size_t>(a)] - T[static_cast<size_t>(b)]);
+      const int id = static_cast<int>(std::lower_bound(lags.begin(), lags.end(), u) - lags.begin());
+      lagid[static_cast<size_t>(a) * nt + b] = id;
+      lagid[static_cast<size_t>(b) * nt + a] = id;
+    }
+}
+
+std::vector<TF> tabulate(const Params& p, const std::vector<double>& lags, const LagPolicy& pol) {
+  std::vector<TF> out(lags.size());
+  for (size_t i = 0; i < lags.size(); ++i) {
+    const double u = lags[i];
+    if (pol.table) {  // covariance.cpp:127-146 snap rule
+      const double r = std::nearbyint(u);
+      if (std::abs(u - r) < 1e-9 && r >= 0.0 && static_cast<int>(r) < pol.size) {
+        out[i] = host_factors(p, static_cast<double>(static_cast<int>(r)));
+        continue;
+      }
+    }
+    out[i] = host_factors(p, u);
+  }
+  return out;
+}
+
+void upload_lag_table(DevLagTable& d, const TimeIndex& ti, const Params& p, const LagPolicy& pol,
+                      cudaStream_t s, bool index_changed) {
+  if (index_changed || d.nT != ti.nT()) {
+    d.lagid.upload(ti.lagid.data(), ti.lagid.size(), s);
+    d.nT = ti.nT();
+  }
+  d.host_tf = tabulate(p, ti.lags, pol);
+  d.tf.upload(d.host_tf.data(), d.host_tf.size(), s);
+}
+
+LagTable lag_view(const DevLagTable& d) { return LagTable{d.lagid.get(), d.tf.get(), d.nT}; }
+
+ProfRegion::ProfRegion(stgp_ctx* c, const char* n) : ctx(c), name(n) {
+  if (!ctx->prof) return;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, ctx->stream);
+}
+ProfRegion::~ProfRegion() {
+  if (!e0) return;
+  cudaEventRecord(e1, ctx->stream);
+  ctx->prof_pending.push_back({name, {e0, e1}});
+}
+void prof_collect(stgp_ctx* ctx) {
+  for (auto& p : ctx->prof_pending) {
+    cudaEventSynchronize(p.second.second);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+    auto& acc = ctx->prof_acc[p.first];
+    acc.first += ms;
+    acc.second += 1;
+    cudaEventDestroy(p.second.first);
+    cudaEventDestroy(p.second.second);
+  }
+  ctx->prof_pending.clear();
+}
+
+// ---------------------------------------------------------------------------
+// small kernels
+// ---------------------------------------------------------------------------
+__global__ void residual_kernel(int n, const double* y, const double* X, int p, const double* beta, double* r) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double xb = 0.0;
+    for (int j = 0; j < p; ++j) xb += X[static_cast<size_t>(i) + static_cast<size_t>(j) * n] * beta[j];
+    r[i] = y[i] - xb;
+  }
+}
+
+// u_i = (B r)_i from stored A; NLL terms log D + u^2 / D (approximations.cpp:336-347)
+__global__ void __launch_bounds__(256) vecchia_nll_stored_kernel(int row_begin, int row_end, int m_v,
+                                                                  const int32_t* nbr, const double* A,
+                                                                  const double* D, const double* r,
+                                                                  double* u_out, double* part) {
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (int i = row_begin + blockIdx.x * blockDim.x + threadIdx.x; i < row_end; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int a = 0; a < m_v; ++a) {
+      const int j = nbr[static_cast<size_t>(i) * m_v + a];
+      if (j < 0) break;
+      s += -A[static_cast<size_t>(i) * m_v + a] * r[j];
+    }
+    const double u = s + r[i];
+    if (u_out) u_out[i] = u;
+    acc += log(D[i]) + u * u / D[i];
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+// 16 independent DFMA chains per thread
+__global__ void fp64_peak_kernel(int iters, double* out) {
+  double a[16];
+  const double m = 1.0000001, c = 1e-9;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) a[q] = threadIdx.x * 1e-3 + q;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) a[q] = fma(a[q], m, c);
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) s += a[q];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void debug_exp_kernel(int n, const double* x, double* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = glibc_exp(x[i]);
+}
+
+__global__ void debug_kernel_kernel(int n, DevKernel k, const TF* tf, const double* h, double* cov, double* g6) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double g[6];
+    const TF f = tf[i];
+    cov[i] = gneiting_eval(k, h[i], f);
+    gneiting_grad(k, h[i], f, g);
+    for (int q = 0; q < 6; ++q) g6[static_cast<size_t>(i) * 6 + q] = g[q];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// reductions
+// ---------------------------------------------------------------------------
+void Reducer::ensure(int blocks, int width) {
+  part.ensure(static_cast<size_t>(blocks) * width);
+  out.ensure(static_cast<size_t>(width));
+}
+std::vector<double> Reducer::finish(stgp_ctx* ctx, int blocks, int width) {
+  reduce_parts_kernel<<<1, 32, 0, ctx->stream>>>(part.get(), blocks, width, out.get());
+  ++ctx->launches;
+  STGP_LAUNCH_CHECK();
+  std::vector<double> h(static_cast<size_t>(width));
+  out.download(h.data(), h.size(), ctx->stream);
+  STGP_CUDA(cudaStreamSynchronize(ctx->stream));
+  return h;
+}
+
+int row_blocks(stgp_ctx* ctx, int rows) {
+  const int need = ceil_div(std::max(rows, 1), kRowWarps);
+  return std::max(1, std::min(need, ctx->num_sms * 16));
+}
+
+}  // namespace stgp
+
+using namespace stgp;
+
+// ===========================================================================
+// structure internals shared with the other translation units
+// ===========================================================================
+namespace stgp {
+
+void compute_residual(stgp_structure* s, const double* y_host, const double* X_host, int p,
+                      const double* beta) {
+  stgp_ctx* ctx = s->ds->ctx;
+  const int n = s->n;
+  s->r.ensure(static_cast<size_t>(n));
+  const double* yd;
+  const double* Xd = nullptr;
+  int pp = 0;
+  if (y_host) {
+    s->ywork.upload(y_host, static_cast<size_t>(n), ctx->stream);
+    yd = s->ywork.get();
+    if (p > 0 && beta) {
+      s->Xwork.upload(X_host, static_cast<size_t>(n) * p, ctx->stream);
+      Xd = s->Xwork.get();
+      pp = p;
+    }
+  } else {
+    if (!s->ds->has_resp) config_error("no response: pass y or call stgp_dataset_set_response");
+    yd = s->ds->resp.get();
+    if (p > 0 && beta) {
+      if (p != s->ds->p) config_error("beta length does not match X");
+      Xd = s->ds->X.get();
+      pp = p;
+    }
+  }
+  if (pp > 0) s->betaw.upload(beta, static_cast<size_t>(pp), ctx->stream);
+  residual_kernel<<<std::min(ceil_div(n, 256), 1024), 256, 0, ctx->stream>>>(n, yd, Xd, pp, s->betaw.get(), s->r.get());
+  ++ctx->launches;
+  STGP_LAUNCH_CHECK();
+}
+
+RowArgs row_args(stgp_structure* s, const double* W, int ldw, double nugget) {
+  RowArgs a{};
+  a.n = s->n;
+  a.m_v = s->m_v;
+  a.row_begin = s->row_begin;
+  a.row_end = s->row_end;
+  a.nbr = s->nbr.get();
+  a.x = s->ds->x.get();
+  a.y = s->ds->y.get();
+  a.tid = s->ds->tid.get();
+  a.k = dev_kernel(s->th);
+  a.lt = lag_view(s->lt);
+  a.s1 = s->th.sigma1_2;
+  a.nugget = nugget;
+  a.W = W;
+  a.ldw = ldw;
+  a.r = s->r.get();
+  a.A_out = s->A.get();
+  a.D_out = s->D.get();
+  a.fail_row = s->fail.get();
+  host_grad00(s->th, a.g00);
+  return a;
+}
+
+// Launch the per-row kernel in the given mode; returns the 8 reduced partials.
+std::vector<double> run_rows(stgp_structure* s, int mode, const double* W, int ldw, double nugget) {
+  stgp_ctx* ctx = s->ds->ctx;
+  RowArgs a = row_args(s, W, ldw, nugget);
+  const int rows = s->row_end - s->row_begin;
+  int fail_init = INT_MAX;
+  s->fail.upload(&fail_init, 1, ctx->stream);
+  int blocks;
+  {
+  ProfRegion pr(ctx, "rows");
+  if (s->m_v <= kKmax - 1) {
+    blocks = row_blocks(ctx, rows);
+    s->red.ensure(blocks, 8);
+    a.part = s->red.part.get();
+    const bool hw = W != nullptr;
+#define STGP_ROWS(M, HW) vecchia_rows_kernel<M, HW><<<blocks, kRowWarps * 32, 0, ctx->stream>>>(a)
+    if (mode == kModeBuild) { if (hw) STGP_ROWS(kModeBuild, true); else STGP_ROWS(kModeBuild, false); }
+    else if (mode == kModeNll) { if (hw) STGP_ROWS(kModeNll, true); else STGP_ROWS(kModeNll, false); }
+    else { if (hw) STGP_ROWS(kModeGrad, true); else STGP_ROWS(kModeGrad, false); }
+#undef STGP_ROWS
+  } else {
+    const int threads = 64;
+    blocks = std::max(1, std::min(ceil_div(rows, threads), 64));
+    const size_t K = static_cast<size_t>(s->m_v);
+    const size_t slab = K * K + 8 * K + 16;
+    s->scratch.ensure(slab * threads * blocks);
+    s->red.ensure(blocks, 8);
+    a.part = s->red.part.get();
+    const bool hw = W != nullptr;
+#define STGP_ROWS(M, HW) vecchia_rows_serial_kernel<M, HW><<<blocks, threads, 0, ctx->stream>>>(a, s->scratch.get())
+    if (mode == kModeBuild) { if (hw) STGP_ROWS(kModeBuild, true); else STGP_ROWS(kModeBuild, false); }
+    else if (mode == kModeNll) { if (hw) STGP_ROWS(kModeNll, true); else STGP_ROWS(kModeNll, false); }
+    else { if (hw) STGP_ROWS(kModeGrad, true); else STGP_ROWS(kModeGrad, false); }
+#undef STGP_ROWS
+  }
+  }
+  ++ctx->launches;
+  STGP_LAUNCH_CHECK();
+  std::vector<double> tot = s->red.finish(ctx, blocks, 8);
+  prof_collect(ctx);
+  int fail = 0;
+  s->fail.download(&fail, 1, ctx->stream);
+  STGP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (fail != INT_MAX)
+    numeric_error("vecchia row " + std::to_string(fail) +
+                  ": conditioning block is not positive definite or non-positive conditional variance");
+  return tot;
+}
+
+void prepare_tables(stgp_structure* s) {
+  // structure kernel: integer-lag table per maybe_precompute_lags
+  upload_lag_table(s->lt, s->ti, s->th, s->ds->lagpol, s->ds->ctx->stream, s->ti_dirty);
+  s->ti_dirty = false;
+}
+
+double nll_const(int n) { return n * 1.8378770664093453; }
+
+void launch_nll_stored(stgp_structure* s, int blocks, double* u_out) {
+  stgp_ctx* ctx = s->ds->ctx;
+  vecchia_nll_stored_kernel<<<blocks, 256, 0, ctx->stream>>>(s->row_begin, s->row_end, s->m_v, s->nbr.get(), s->A.get(),
+                                                             s->D.get(), s->r.get(), u_out, s->red.part.get());
+  ++ctx->launches;
+  STGP_LAUNCH_CHECK();
+}
+
+}  // namespace stgp
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return STGP_OK;
+  } catch (const stgp::Error& e) {
+    stgp::g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    stgp::g_last_error = "out of host memory";
+    return STGP_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    stgp::g_last_error = e.what();
+    return STGP_ERR_INTERNAL;
+  }
+}
+
+void require(bool c, const char* m) {
+  if (!c) config_error(m);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* stgp_last_error(void) { return stgp::g_last_error.c_str(); }
+int stgp_version(void) { return 1; }
+
+int stgp_ctx_create(int device, stgp_ctx** out) {
+  return guarded([&] {
+    require(out != nullptr, "stgp_ctx_create: null out");
+    int count = 0;
+    STGP_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) config_error("stgp_ctx_create: no such CUDA device");
+    STGP_CUDA(cudaSetDevice(device));
+    auto ctx = std::make_unique<stgp_ctx>();
+    ctx->device = device;
+    STGP_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    cudaDeviceProp prop{};
+    STGP_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+      config_error("stgp_b200 is built for sm_100a (B200); found compute capability " +
+                   std::to_string(prop.major) + "." + std::to_string(prop.minor));
+    ctx->num_sms = prop.multiProcessorCount;
+    if (cublasCreate(&ctx->cublas) != CUBLAS_STATUS_SUCCESS) throw Error(kInternal, "cublasCreate failed");
+    cublasSetStream(ctx->cublas, ctx->stream);
+    *out = ctx.release();
+  });
+}
+
+void stgp_ctx_destroy(stgp_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  stgp_ctx_release_comm(ctx);
+  if (ctx->cublas) cublasDestroy(ctx->cublas);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int stgp_ctx_synchronize(stgp_ctx* ctx) {
+  return guarded([&] { STGP_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int stgp_ctx_set_shard(stgp_ctx* ctx, int rank, int world) {
+  return guarded([&] {
+    if (world < 1 || rank < 0 || rank >= world) config_error("stgp_ctx_set_shard: bad rank/world");
+    ctx->rank = rank;
+    ctx->world = world;
+  });
+}
+
+int64_t stgp_ctx_kernel_launches(const stgp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+void* stgp_ctx_stream(stgp_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int stgp_ctx_profile(stgp_ctx* ctx, int enable) {
+  return guarded([&] {
+    require(ctx, "null context");
+    ctx->prof = enable != 0;
+  });
+}
+int stgp_ctx_profile_get(stgp_ctx* ctx, const char* region, double* total_ms, int64_t* count) {
+  return guarded([&] {
+    require(ctx && region, "null argument");
+    prof_collect(ctx);
+    auto it = ctx->prof_acc.find(region);
+    *total_ms = it == ctx->prof_acc.end() ? 0.0 : it->second.first;
+    *count = it == ctx->prof_acc.end() ? 0 : it->second.second;
+  });
+}
+int stgp_ctx_profile_reset(stgp_ctx* ctx) {
+  return guarded([&] {
+    prof_collect(ctx);
+    ctx->prof_acc.clear();
+  });
+}
+
+int stgp_debug_fp64_peak(stgp_ctx* ctx, double* tflops) {
+  return guarded([&] {
+    const int blocks = ctx->num_sms * 4, threads = 256, iters = 4096;
+    DevBuf<double> out(static_cast<size_t>(blocks) * threads);
+    cudaEvent_t e0, e1;
+    STGP_CUDA(cudaEventCreate(&e0));
+    STGP_CUDA(cudaEventCreate(&e1));
+    fp64_peak_kernel<<<blocks, threads, 0, ctx->stream>>>(iters, out.get());  // warm-up
+    STGP_CUDA(cudaEventRecord(e0, ctx->stream));
+    for (int r = 0; r < 5; ++r) fp64_peak_kernel<<<blocks, threads, 0, ctx->stream>>>(iters, out.get());
+    STGP_CUDA(cudaEventRecord(e1, ctx->stream));
+    ctx->launches += 6;
+    STGP_LAUNCH_CHECK();
+    STGP_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    STGP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flops = 5.0 * blocks * threads * static_cast<double>(iters) * 16 * 2;
+    *tflops = flops / (ms * 1e-3) / 1e12;
+  });
+}
+
+int stgp_order_observations(int n, const double* t, uint64_t seed, int32_t* perm_out) {
+  return guarded([&] {
+    if (n <= 0) data_error("SpaceTimeDataset: empty dataset");
+    std::vector<int> perm(static_cast<size_t>(n));
+    std::iota(perm.begin(), perm.end(), 0);
+    std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return t[a] < t[b]; });
+    std::mt19937_64 rng(mix_seed(seed, 0x0bde11));
+    size_t bs = 0;
+    for (size_t k = 1; k <= perm.size(); ++k) {
+      const bool end = k == perm.size() || t[perm[k]] != t[perm[bs]];
+      if (end) {
+        for (size_t j = k - 1; j > bs; --j) {
+          std::uniform_int_distribution<size_t> pick(bs, j);
+          std::swap(perm[j], perm[pick(rng)]);
+        }
+        bs = k;
+      }
+    }
+    std::copy(perm.begin(), perm.end(), perm_out);
+  });
+}
+
+int stgp_effective_ranges(const stgp_params* theta, double* tr, double* sr) {
+  return guarded([&] {
+    Params p;
+    std::memcpy(&p, theta, sizeof(p));
+    validate_params(p);
+    const double e = p.delta + p.beta;
+    if (e <= 0.0 || p.a <= 0.0) {
+      *tr = std::numeric_limits<double>::infinity();
+    } else {
+      const double T = std::pow(20.0, 1.0 / e);
+      *tr = std::pow((T - 1.0) / p.a, 1.0 / (2.0 * p.alpha));
+    }
+    auto matern = [&](double x) {
+      if (x == 0.0) return 1.0;
+      if (p.nu == 0.5) return std::exp(-x);
+      if (p.nu == 1.5) return (1.0 + x) * std::exp(-x);
+      if (p.nu == 2.5) return (1.0 + x + x * x / 3.0) * std::exp(-x);
+      const double v = std::pow(2.0, 1.0 - p.nu) / std::tgamma(p.nu) * std::pow(x, p.nu) * std::cyl_bessel_k(p.nu, x);
+      return std::isfinite(v) ? v : 0.0;
+    };
+    double lo = 0.0, hi = 1.0;
+    while (matern(hi) > 0.05) hi *= 2.0;
+    while ((hi - lo) > 1e-10 * hi) {
+      const double mid = 0.5 * (lo + hi);
+      if (matern(mid) > 0.05) lo = mid;
+      else hi = mid;
+    }
+    *sr = 0.5 * (lo + hi) / p.c;
+  });
+}
+
+uint64_t stgp_mix_seed(uint64_t seed, uint64_t stream) { return mix_seed(seed, stream); }
+
+int stgp_dataset_create(stgp_ctx* ctx, int n, const double* x, const double* y, const double* t,
+                        stgp_dataset** out) {
+  return guarded([&] {
+    require(ctx && out, "stgp_dataset_create: null argument");
+    if (n <= 0) data_error("SpaceTimeDataset: empty dataset");
+    auto ds = std::make_unique<stgp_dataset>();
+    ds->ctx = ctx;
+    ds->n = n;
+    ds->hx.assign(x, x + n);
+    ds->hy.assign(y, y + n);
+    ds->ht.assign(t, t + n);
+    for (int i = 0; i < n; ++i)
+      if (!std::isfinite(x[i]) || !std::isfinite(y[i]) || !std::isfinite(t[i]))
+        data_error("SpaceTimeDataset: non-finite coordinates");
+    std::set<double> ts(t, t + n);
+    ds->Tdata.assign(ts.begin(), ts.end());
+    ds->htid.resize(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i)
+      ds->htid[static_cast<size_t>(i)] =
+          static_cast<int32_t>(std::lower_bound(ds->Tdata.begin(), ds->Tdata.end(), t[i]) - ds->Tdata.begin());
+    ds->time_sorted = true;
+    for (int i = 1; i < n; ++i)
+      if (t[i] < t[i - 1]) ds->time_sorted = false;
+    // maybe_precompute_lags (approximations.cpp:26-38)
+    bool integral = true;
+    double tmin = t[0], tmax = t[0];
+    for (int i = 0; i < n; ++i) {
+      if (std::abs(t[i] - std::nearbyint(t[i])) >= 1e-9) {
+        integral = false;
+        break;
+      }
+      tmin = std::min(tmin, t[i]);
+      tmax = std::max(tmax, t[i]);
+    }
+    const double range = tmax - tmin;
+    if (integral && range >= 0.0 && range <= 200000.0) {
+      ds->lagpol.table = true;
+      ds->lagpol.size = static_cast<int>(range) + 2;
+    }
+    cudaStream_t s = ctx->stream;
+    ds->x.upload(x, n, s);
+    ds->y.upload(y, n, s);
+    ds->t.upload(t, n, s);
+    ds->tid.upload(ds->htid.data(), n, s);
+    if (ds->time_sorted) {
+      std::vector<int32_t> bs(ds->Tdata.size() + 1, 0);
+      for (int i = n - 1; i >= 0; --i) bs[static_cast<size_t>(ds->htid[static_cast<size_t>(i)])] = i;
+      bs.back() = n;
+      ds->blk_start.upload(bs.data(), bs.size(), s);
+    }
+    STGP_CUDA(cudaStreamSynchronize(s));
+    *out = ds.release();
+  });
+}
+
+int stgp_dataset_set_response(stgp_dataset* ds, const double* resp, int p, const double* X) {
+  return guarded([&] {
+    require(ds && resp, "stgp_dataset_set_response: null argument");
+    for (int i = 0; i < ds->n; ++i)
+      if (!std::isfinite(resp[i])) data_error("SpaceTimeDataset: non-finite response or covariates");
+    ds->resp.upload(resp, ds->n, ds->ctx->stream);
+    ds->p = std::max(p, 0);
+    if (ds->p > 0) ds->X.upload(X, static_cast<size_t>(ds->n) * ds->p, ds->ctx->stream);
+    ds->has_resp = true;
+    STGP_CUDA(cudaStreamSynchronize(ds->ctx->stream));
+  });
+}
+
+void stgp_dataset_destroy(stgp_dataset* ds) { delete ds; }
+
+// ---- neighbour searches ----
+static stgp_neighbors* run_search(stgp_dataset* ds, int metric, const Params* th, int m_v, double ss,
+                                  double ts) {
+  stgp_ctx* ctx = ds->ctx;
+  if (m_v < 0) config_error("m_v must be >= 0");
+  if (m_v > 32) config_error("neighbour search supports m_v <= 32 on the device");
+  auto nb = std::make_unique<stgp_neighbors>();
+  nb->ctx = ctx;
+  nb->n = ds->n;
+  nb->m_v = std::max(m_v, 1);
+  nb->kind = metric;
+  nb->ss = ss;
+  nb->ts = ts;
+  const size_t total = static_cast<size_t>(ds->n) * nb->m_v;
+  nb->idx.alloc(total);
+  nb->dist.alloc(total);
+  nb->has_dist = true;
+  SearchArgs a{};
+  a.n = ds->n;
+  a.m_v = m_v == 0 ? 1 : m_v;
+  a.q_begin = 0;
+  a.q_end = ds->n;
+  a.x = ds->x.get();
+  a.y = ds->y.get();
+  a.t = ds->t.get();
+  a.tid = ds->tid.get();
+  a.ss = ss;
+  a.ts = ts;
+  a.out = nb->idx.get();
+  a.dist = nb->dist.get();
+  DevLagTable dl;
+  TimeIndex ti;
+  if (ds->time_sorted) {
+    a.blk_of = ds->tid.get();
+    a.blk_start = ds->blk_start.get();
+    a.nblk = static_cast<int>(ds->Tdata.size());
+    a.blk_tid = nullptr;
+  }
+  DevBuf<int32_t> blk_tid;
+  if (ds->time_sorted) {
+    std::vector<int32_t> bt(ds->Tdata.size());
+    std::iota(bt.begin(), bt.end(), 0);
+    blk_tid.upload(bt.data(), bt.size(), ctx->stream);
+    a.blk_tid = blk_tid.get();
+  }
+  if (metric == STGP_METRIC_DC) {
+    a.k = dev_kernel(*th);
+    ti.T = ds->Tdata;
+    ti.build();
+    LagPolicy live;  // selection kernel has no lag table (estimation.cpp:200)
+    upload_lag_table(dl, ti, *th, live, ctx->stream, true);
+    a.lt = lag_view(dl);
+  }
+  const int blocks = std::max(1, std::min(ceil_div(ds->n, 8), ctx->num_sms * 8));
+  if (m_v == 0) {
+    std::vector<int32_t> neg(total, -1);
+    nb->idx.upload(neg.data(), total, ctx->stream);
+  } else if (metric == STGP_METRIC_DC) {
+    ProfRegion pr(ctx, "knn_dc");
+    knn_kernel<0><<<blocks, 256, 0, ctx->stream>>>(a);
+    ++ctx->launches;
+  } else {
+    ProfRegion pr(ctx, "knn_euclid");
+    knn_kernel<1><<<blocks, 256, 0, ctx->stream>>>(a);
+    ++ctx->launches;
+  }
+  STGP_LAUNCH_CHECK();
+  STGP_CUDA(cudaStreamSynchronize(ctx->stream));
+  prof_collect(ctx);
+  return nb.release();
+}
+
+int stgp_euclidean_neighbors(stgp_dataset* ds, int m_v, double ss, double ts, stgp_neighbors** out) {
+  return guarded([&] {
+    require(ds && out, "null argument");
+    if (!(ss > 0.0) || !(ts > 0.0)) config_error("euclidean_neighbors: scales must be positive");
+    if (!ds->time_sorted) config_error("euclidean_neighbors: dataset must be time-ordered");
+    *out = run_search(ds, STGP_METRIC_EUCLID, nullptr, m_v, ss, ts);
+  });
+}
+
+int stgp_correlation_neighbors(stgp_dataset* ds, const stgp_params* theta, int m_v, stgp_neighbors** out) {
+  return guarded([&] {
+    require(ds && theta && out, "null argument");
+    Params p;
+    std::memcpy(&p, theta, sizeof(p));
+    validate_params(p);
+    *out = run_search(ds, STGP_METRIC_DC, &p, m_v, 1.0, 1.0);
+  });
+}
+
+int stgp_neighbors_from_host(stgp_dataset* ds, int m_v, const int32_t* idx, int kind, stgp_neighbors** out) {
+  return guarded([&] {
+    require(ds && idx && out && m_v >= 1, "stgp_neighbors_from_host: bad argument");
+    for (int i = 0; i < ds->n; ++i) {
+      int prev = -1;
+      bool ended = false;
+      for (int a = 0; a < m_v; ++a) {
+        const int j = idx[static_cast<size_t>(i) * m_v + a];
+        if (j < 0) {
+          ended = true;
+          continue;
+        }
+        if (ended || j <= prev || j >= ds->n) config_error("neighbour rows must be ascending, in range, -1 padded");
+        prev = j;
+      }
+    }
+    auto nb = std::make_unique<stgp_neighbors>();
+    nb->ctx = ds->ctx;
+    nb->n = ds->n;
+    nb->m_v = m_v;
+    nb->kind = kind;
+    nb->idx.upload(idx, static_cast<size_t>(ds->n) * m_v, ds->ctx->stream);
+    STGP_CUDA(cudaStreamSynchronize(ds->ctx->stream));
+    *out = nb.release();
+  });
+}
+
+int stgp_neighbors_shape(const stgp_neighbors* nb, int* n, int* m_v, int* kind) {
+  return guarded([&] {
+    require(nb, "null neighbours");
+    if (n) *n = nb->n;
+    if (m_v) *m_v = nb->m_v;
+    if (kind) *kind = nb->kind;
+  });
+}
+
+int stgp_neighbors_download(const stgp_neighbors* nb, int32_t* idx, double* dist) {
+  return guarded([&] {
+    require(nb, "null neighbours");
+    const size_t total = static_cast<size_t>(nb->n) * nb->m_v;
+    if (idx) nb->idx.download(idx, total, nb->ctx->stream);
+    if (dist) {
+      if (!nb->has_dist) config_error("these neighbour sets carry no distances");
+      nb->dist.download(dist, total, nb->ctx->stream);
+    }
+    STGP_CUDA(cudaStreamSynchronize(nb->ctx->stream));
+  });
+}
+
+void stgp_neighbors_destroy(stgp_neighbors* nb) { delete nb; }
+
+int stgp_debug_exp(stgp_ctx* ctx, int n, const double* x, double* out) {
+  return guarded([&] {
+    DevBuf<double> dx, dy(static_cast<size_t>(n));
+    dx.upload(x, n, ctx->stream);
+    debug_exp_kernel<<<std::max(1, std::min(ceil_div(n, 256), 4096)), 256, 0, ctx->stream>>>(n, dx.get(), dy.get());
+    ++ctx->launches;
+    STGP_LAUNCH_CHECK();
+    dy.download(out, n, ctx->stream);
+    STGP_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int stgp_debug_kernel(stgp_ctx* ctx, const stgp_params* theta, int n, const double* h, const double* u,
+                      double* cov, double* g6) {
+  return guarded([&] {
+    Params p;
+    std::memcpy(&p, theta, sizeof(p));
+    validate_params(p);
+    std::vector<TF> tf(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) tf[static_cast<size_t>(i)] = host_factors(p, u[i]);
+    DevBuf<TF> dtf;
+    DevBuf<double> dh, dc(static_cast<size_t>(n)), dg(static_cast<size_t>(n) * 6);
+    dtf.upload(tf.data(), n, ctx->stream);
+    dh.upload(h, n, ctx->stream);
+    debug_kernel_kernel<<<std::max(1, ceil_div(n, 128)), 128, 0, ctx->stream>>>(n, dev_kernel(p), dtf.get(), dh.get(),
+                                                                               dc.get(), dg.get());
+    ++ctx->launches;
+    STGP_LAUNCH_CHECK();
+    dc.download(cov, n, ctx->stream);
+    if (g6) dg.download(g6, static_cast<size_t>(n) * 6, ctx->stream);
+    STGP_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+}  // extern "C"

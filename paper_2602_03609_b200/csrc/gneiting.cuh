@@ -1,0 +1,161 @@
+// Device Gneiting space-time kernel (reference covariance.cpp:62-181).
+//
+// Bit-exactness contract: every operation below is an explicit IEEE
+// round-to-nearest intrinsic in the reference's evaluation order, so a device
+// covariance equals the host `GneitingKernel::eval` bit-for-bit given the same
+// temporal factors.  Temporal factors (pow/log of the time lag) are computed on
+// the host with glibc and tabulated per time-id pair; the only transcendental
+// left on the device is exp, ported from glibc 2.39's FMA variant
+// (sysdeps/ieee754/dbl-64/e_exp.c, compiled by glibc with -mfma -mavx2).
+#pragma once
+
+#include <cstdint>
+
+#include "common.cuh"
+#include "glibc_exp_table.h"
+
+namespace stgp {
+
+// global table (per translation unit): divergent indexed loads, constant memory would serialise them
+static __device__ uint64_t kExpTab[256] = STGP_EXP_TABLE_INIT;
+
+// glibc exp, specialcase(): k > 0 keeps the contracted form; k < 0 shares the
+// product scale*tmp (GCC CSE), so nothing there is contracted.
+static __device__ __noinline__ double glibc_exp_special(double tmp, uint64_t sbits, uint64_t ki) {
+  if ((ki & 0x80000000ULL) == 0) {
+    sbits -= 1009ULL << 52;
+    const double scale = __longlong_as_double(static_cast<long long>(sbits));
+    return __dmul_rn(0x1p1009, __fma_rn(scale, tmp, scale));
+  }
+  sbits += 1022ULL << 52;
+  const double scale = __longlong_as_double(static_cast<long long>(sbits));
+  const double st = __dmul_rn(scale, tmp);
+  double y = __dadd_rn(scale, st);
+  if (y < 1.0) {
+    double lo = __dadd_rn(__dsub_rn(scale, y), st);
+    const double hi = __dadd_rn(1.0, y);
+    lo = __dadd_rn(__dadd_rn(__dsub_rn(1.0, hi), y), lo);
+    y = __dsub_rn(__dadd_rn(hi, lo), 1.0);
+    if (y == 0.0) y = 0.0;
+  }
+  return __dmul_rn(0x1p-1022, y);
+}
+
+__device__ __forceinline__ double glibc_exp(double x) {
+  const uint64_t ux = static_cast<uint64_t>(__double_as_longlong(x));
+  uint32_t abstop = static_cast<uint32_t>(ux >> 52) & 0x7ffu;
+  if (abstop - 0x3c9u >= 0x408u - 0x3c9u) {
+    if (abstop - 0x3c9u >= 0x80000000u) return __dadd_rn(1.0, x);  // |x| < 2^-54
+    if (abstop >= 0x409u) {
+      if (ux == 0xfff0000000000000ULL) return 0.0;
+      if (abstop >= 0x7ffu) return __dadd_rn(1.0, x);
+      return (ux >> 63) ? 0.0 : __longlong_as_double(0x7ff0000000000000LL);
+    }
+    abstop = 0;  // large |x|: special case below
+  }
+  double kd = __fma_rn(STGP_EXP_invln2N, x, STGP_EXP_shift);
+  const uint64_t ki = static_cast<uint64_t>(__double_as_longlong(kd));
+  kd = __dsub_rn(kd, STGP_EXP_shift);
+  const double r = __fma_rn(kd, STGP_EXP_negln2loN, __fma_rn(kd, STGP_EXP_negln2hiN, x));
+  const uint32_t idx = 2u * static_cast<uint32_t>(ki & 127u);
+  const uint64_t top = ki << 45;
+  const double tail = __longlong_as_double(static_cast<long long>(__ldg(&kExpTab[idx])));
+  const uint64_t sbits = __ldg(&kExpTab[idx + 1]) + top;
+  const double r2 = __dmul_rn(r, r);
+  const double tmp =
+      __fma_rn(__dmul_rn(r2, r2), __fma_rn(r, STGP_EXP_C5, STGP_EXP_C4),
+               __fma_rn(r2, __fma_rn(r, STGP_EXP_C3, STGP_EXP_C2), __dadd_rn(tail, r)));
+  if (abstop == 0) return glibc_exp_special(tmp, sbits, ki);
+  const double scale = __longlong_as_double(static_cast<long long>(sbits));
+  return __fma_rn(scale, tmp, scale);
+}
+
+// spatial distance, types.hpp:53-56
+__device__ __forceinline__ double spatial_dist(double xa, double ya, double xb, double yb) {
+  const double dx = __dsub_rn(xa, xb), dy = __dsub_rn(ya, yb);
+  return __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+}
+
+// Matern correlation for nu in {0.5, 1.5, 2.5} (covariance.cpp:66-71), given e = exp(-x)
+__device__ __forceinline__ double matern_from_exp(double x, double e, int nu_code) {
+  if (x == 0.0) return 1.0;
+  if (nu_code == 0) return e;
+  if (nu_code == 1) return __dmul_rn(__dadd_rn(1.0, x), e);
+  return __dmul_rn(__dadd_rn(__dadd_rn(1.0, x), __ddiv_rn(__dmul_rn(x, x), 3.0)), e);
+}
+// derivative (covariance.cpp:79-87)
+__device__ __forceinline__ double matern_deriv_from_exp(double x, double e, int nu_code) {
+  if (nu_code == 0) return -e;
+  if (nu_code == 1) return __dmul_rn(-x, e);
+  return __dmul_rn(-__ddiv_rn(__dmul_rn(x, __dadd_rn(1.0, x)), 3.0), e);
+}
+
+struct DevKernel {
+  double s1, c, a, beta, E;  // sigma1_2, spatial decay, temporal scale, beta, delta+beta
+  int nu_code;               // 0: 0.5, 1: 1.5, 2: 2.5
+};
+
+inline int nu_code_of(double nu) {
+  if (nu == 0.5) return 0;
+  if (nu == 1.5) return 1;
+  if (nu == 2.5) return 2;
+  return -1;
+}
+
+// GneitingKernel::eval (covariance.cpp:138-149)
+__device__ __forceinline__ double gneiting_eval(const DevKernel& k, double h, const TF& f) {
+  const double x = __dmul_rn(__dmul_rn(k.c, h), f.pow_mbh);
+  const double e = (x == 0.0) ? 1.0 : glibc_exp(-x);
+  return __dmul_rn(__dmul_rn(k.s1, f.pow_mE), matern_from_exp(x, e, k.nu_code));
+}
+
+// GneitingKernel::grad (covariance.cpp:151-181); g order (sigma1_2, a, c, alpha, beta, delta).
+// Also returns the covariance value.
+__device__ __forceinline__ double gneiting_grad(const DevKernel& k, double h, const TF& f, double g[6]) {
+  const double x = __dmul_rn(__dmul_rn(k.c, h), f.pow_mbh);
+  const double e = glibc_exp(-x);
+  const double M = matern_from_exp(x, e, k.nu_code);
+  const double Mp = matern_deriv_from_exp(x, e, k.nu_code);
+  const double base = __dmul_rn(k.s1, f.pow_mE);
+  g[0] = __dmul_rn(f.pow_mE, M);
+  const double dC_dT = __dmul_rn(__dmul_rn(base, f.inv_T),
+                                 __dsub_rn(__dmul_rn(-k.E, M), __dmul_rn(__dmul_rn(__dmul_rn(0.5, k.beta), x), Mp)));
+  g[1] = __dmul_rn(dC_dT, f.u2a);
+  g[3] = __dmul_rn(__dmul_rn(__dmul_rn(dC_dT, 2.0), k.a), f.u2a_logu);
+  g[2] = __ddiv_rn(__dmul_rn(__dmul_rn(base, Mp), x), k.c);
+  g[4] = __dmul_rn(__dmul_rn(-f.log_T, base), __dadd_rn(M, __dmul_rn(__dmul_rn(0.5, x), Mp)));
+  g[5] = __dmul_rn(__dmul_rn(-f.log_T, base), M);
+  return __dmul_rn(base, M);
+}
+
+// Temporal-factor table indexed by time-id pairs (host-computed with glibc).
+struct TFTable {
+  const TF* tab;  // nT * nT
+  int nT;
+  __device__ __forceinline__ TF get(int ta, int tb) const {
+    const TF* p = tab + static_cast<size_t>(ta) * nT + tb;
+    TF f;
+    f.pow_mE = __ldg(&p->pow_mE);
+    f.pow_mbh = __ldg(&p->pow_mbh);
+    f.inv_T = __ldg(&p->inv_T);
+    f.log_T = __ldg(&p->log_T);
+    f.u2a = __ldg(&p->u2a);
+    f.u2a_logu = __ldg(&p->u2a_logu);
+    return f;
+  }
+  __device__ __forceinline__ void get2(int ta, int tb, double& pow_mE, double& pow_mbh) const {
+    const TF* p = tab + static_cast<size_t>(ta) * nT + tb;
+    pow_mE = __ldg(&p->pow_mE);
+    pow_mbh = __ldg(&p->pow_mbh);
+  }
+};
+
+// Covariance between two points given their time ids.
+__device__ __forceinline__ double cov_pts(const DevKernel& k, const TFTable& T, double xa, double ya,
+                                          int ta, double xb, double yb, int tb) {
+  TF f;
+  T.get2(ta, tb, f.pow_mE, f.pow_mbh);
+  return gneiting_eval(k, spatial_dist(xa, ya, xb, yb), f);
+}
+
+}  // namespace stgp

@@ -1,0 +1,72 @@
+// Built approximation structures (approximations.hpp:33-75) and the helpers
+// shared by the Vecchia / FITC / VIF translation units.
+#pragma once
+
+#include <vector>
+
+#include "engine.hpp"
+#include "rows.cuh"
+
+namespace stgp {
+
+struct Reducer {
+  DevBuf<double> part, out;
+  void ensure(int blocks, int width);
+  std::vector<double> finish(stgp_ctx* ctx, int blocks, int width);
+};
+
+// Low-rank state of FITC / VIF structures (all device, column-major).
+struct LowRank {
+  int M = 0, ldm = 0;            // inducing count, padded leading dimension (multiple of 4)
+  std::vector<double> zxyt;      // host M x 3
+  DevBuf<double> zx, zy, zt;     // device inducing coordinates
+  DevBuf<int32_t> ztid;          // time ids of inducing points
+  DevBuf<double> Lm;             // Cholesky of jittered Sigma_m (ldm x ldm, lower)
+  double logdet_m = 0.0;
+  DevBuf<double> U, W;           // ldm x n : cross covariance, whitened L_m^{-1} U
+  DevBuf<double> Mc;             // Woodbury core (ldm x ldm), Cholesky in place
+  double logdet_M = 0.0;
+  DevBuf<double> fitc_diag, lambda;  // FITC
+  DevBuf<double> work1, work2, work3, work4, vecM, vecM2, vecN, vecN2;
+};
+
+}  // namespace stgp
+
+struct stgp_structure {
+  stgp_dataset* ds = nullptr;
+  int kind = 0, policy = 0;
+  stgp::Params th{};
+  int n = 0, m_v = 1;
+  int row_begin = 0, row_end = 0;
+  stgp::DevBuf<int32_t> nbr;
+  int nbr_kind = 0;
+  stgp::DevBuf<double> A, D;
+  stgp::TimeIndex ti;
+  bool ti_dirty = true;
+  stgp::DevLagTable lt;
+  stgp::Reducer red;
+  stgp::DevBuf<int> fail;
+  stgp::DevBuf<double> r, ywork, Xwork, betaw, u, scratch;
+  stgp::LowRank lr;
+  bool built = false;
+};
+
+namespace stgp {
+
+extern thread_local std::string g_last_error;
+
+void compute_residual(stgp_structure* s, const double* y_host, const double* X_host, int p,
+                      const double* beta);
+RowArgs row_args(stgp_structure* s, const double* W, int ldw, double nugget);
+std::vector<double> run_rows(stgp_structure* s, int mode, const double* W, int ldw, double nugget);
+void prepare_tables(stgp_structure* s);
+double nll_const(int n);
+void launch_nll_stored(stgp_structure* s, int blocks, double* u_out);
+int row_blocks(stgp_ctx* ctx, int rows);
+void upload_lag_table(DevLagTable& d, const TimeIndex& ti, const Params& p, const LagPolicy& pol,
+                      cudaStream_t s, bool index_changed);
+LagTable lag_view(const DevLagTable& d);
+
+}  // namespace stgp
+
+extern "C" void stgp_ctx_release_comm(stgp_ctx* ctx);

@@ -1,0 +1,310 @@
+// Structure builders and likelihood entry points (approximations.cpp:198-744).
+// Vecchia lives here; the low-rank FITC/VIF algebra is in lowrank.cu.
+#include <climits>
+#include <cstring>
+
+#include "comm.hpp"
+#include "structure.hpp"
+#include "../../include/stgp_b200.h"
+
+namespace stgp {
+
+Params params_of(const stgp_params* th) {
+  if (!th) config_error("null parameters");
+  Params p;
+  std::memcpy(&p, th, sizeof(p));
+  validate_params(p);
+  return p;
+}
+
+stgp_structure* new_structure(stgp_dataset* ds, int kind, const Params& th, const stgp_neighbors* nb, int policy) {
+  if (!ds) config_error("null dataset");
+  auto s = std::make_unique<stgp_structure>();
+  s->ds = ds;
+  s->kind = kind;
+  s->policy = policy;
+  s->th = th;
+  s->n = ds->n;
+  shard_rows(ds->ctx, s->n, s->row_begin, s->row_end);
+  cudaStream_t st = ds->ctx->stream;
+  if (nb) {
+    if (nb->n != ds->n) config_error("build: neighbor sets inconsistent with the dataset");
+    s->m_v = nb->m_v;
+    s->nbr_kind = nb->kind;
+    s->nbr.alloc(static_cast<size_t>(s->n) * s->m_v);
+    STGP_CUDA(cudaMemcpyAsync(s->nbr.get(), nb->idx.get(), static_cast<size_t>(s->n) * s->m_v * sizeof(int32_t),
+                              cudaMemcpyDeviceToDevice, st));
+  } else {
+    s->m_v = 1;
+    std::vector<int32_t> none(static_cast<size_t>(s->n), -1);
+    s->nbr.upload(none.data(), none.size(), st);
+  }
+  s->A.alloc(static_cast<size_t>(s->n) * s->m_v);
+  s->D.alloc(static_cast<size_t>(s->n));
+  s->A.zero(st);
+  s->D.zero(st);
+  s->ti.T = ds->Tdata;
+  s->fail.alloc(1);
+  return s.release();
+}
+
+static void require_obs(const stgp_structure* s, const char* what) {
+  if (s->policy != STGP_OBSERVATION)
+    numeric_error(std::string(what) +
+                  ": analytic gradient is defined for the observation-policy structure driven by the optimizer");
+}
+
+// ---- Vecchia ----
+void vecchia_build(stgp_structure* s) {
+  prepare_tables(s);
+  const double nug = s->policy == STGP_OBSERVATION ? s->th.sigma2 : 0.0;
+  run_rows(s, kModeBuild, nullptr, 0, nug);
+  s->built = true;
+}
+
+double vecchia_nll(stgp_structure* s) {
+  if (s->policy != STGP_OBSERVATION)
+    config_error("nll: latent-policy likelihood goes through the Laplace algebra (out of scope, SURVEY.md §8(f) f3)");
+  stgp_ctx* ctx = s->ds->ctx;
+  const int rows = s->row_end - s->row_begin;
+  const int blocks = std::max(1, std::min(ceil_div(rows, 256), ctx->num_sms * 4));
+  s->red.ensure(blocks, 1);
+  launch_nll_stored(s, blocks, nullptr);
+  std::vector<double> tot = s->red.finish(ctx, blocks, 1);
+  allreduce_host(ctx, tot);
+  return 0.5 * (tot[0] + nll_const(s->n));
+}
+
+void vecchia_nll_grad(stgp_structure* s, double* nll, double* grad) {
+  require_obs(s, "nll_grad");
+  prepare_tables(s);
+  std::vector<double> tot = run_rows(s, kModeGrad, nullptr, 0, s->th.sigma2);
+  allreduce_host(s->ds->ctx, tot);
+  if (nll) *nll = 0.5 * (tot[0] + nll_const(s->n));
+  if (grad)
+    for (int q = 0; q < 7; ++q) grad[q] = tot[1 + q];
+  s->built = true;
+}
+
+}  // namespace stgp
+
+using namespace stgp;
+
+namespace {
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return STGP_OK;
+  } catch (const stgp::Error& e) {
+    stgp::g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    stgp::g_last_error = e.what();
+    return STGP_ERR_INTERNAL;
+  }
+}
+}  // namespace
+
+// declared in lowrank.cu
+namespace stgp {
+void lowrank_setup(stgp_structure* s, const stgp_inducing* ind);
+void fitc_build(stgp_structure* s);
+void vif_build(stgp_structure* s);
+double lowrank_nll(stgp_structure* s);
+void lowrank_nll_grad(stgp_structure* s, double* nll, double* grad);
+void lowrank_predict(stgp_structure* s, int n_p, const double* txyt, int pred_m_v, double* mu, double* var);
+void vecchia_predict(stgp_structure* s, int n_p, const double* txyt, int pred_m_v, double* mu, double* var);
+std::vector<double> sigma_inv_apply_host(stgp_structure* s, const double* v_dev);
+}  // namespace stgp
+
+extern "C" {
+
+int stgp_build_vecchia(stgp_dataset* ds, const stgp_params* theta, const stgp_neighbors* nb, int policy,
+                       stgp_structure** out) {
+  return guarded([&] {
+    if (!out || !nb) config_error("stgp_build_vecchia: null argument");
+    std::unique_ptr<stgp_structure> s(new_structure(ds, STGP_VECCHIA, params_of(theta), nb, policy));
+    vecchia_build(s.get());
+    *out = s.release();
+  });
+}
+
+int stgp_build_fitc(stgp_dataset* ds, const stgp_params* theta, const stgp_inducing* ind, stgp_structure** out) {
+  return guarded([&] {
+    if (!out || !ind) config_error("stgp_build_fitc: null argument");
+    if (ind->M() < 1) config_error("build_fitc: need at least one inducing point");
+    std::unique_ptr<stgp_structure> s(new_structure(ds, STGP_FITC, params_of(theta), nullptr, STGP_OBSERVATION));
+    lowrank_setup(s.get(), ind);
+    fitc_build(s.get());
+    *out = s.release();
+  });
+}
+
+int stgp_build_vif(stgp_dataset* ds, const stgp_params* theta, const stgp_inducing* ind, const stgp_neighbors* nb,
+                   int policy, stgp_structure** out) {
+  return guarded([&] {
+    if (!out || !ind || !nb) config_error("stgp_build_vif: null argument");
+    std::unique_ptr<stgp_structure> s(new_structure(ds, STGP_VIF, params_of(theta), nb, policy));
+    lowrank_setup(s.get(), ind);
+    vif_build(s.get());
+    *out = s.release();
+  });
+}
+
+void stgp_structure_destroy(stgp_structure* s) { delete s; }
+
+int stgp_structure_download_D(const stgp_structure* s, double* D) {
+  return guarded([&] {
+    if (s->kind == STGP_FITC) config_error("FITC structures have no Vecchia factor D");
+    s->D.download(D, static_cast<size_t>(s->n), s->ds->ctx->stream);
+    STGP_CUDA(cudaStreamSynchronize(s->ds->ctx->stream));
+  });
+}
+
+int stgp_structure_download_A(const stgp_structure* s, double* A) {
+  return guarded([&] {
+    if (s->kind == STGP_FITC) config_error("FITC structures have no Vecchia factor B");
+    s->A.download(A, static_cast<size_t>(s->n) * s->m_v, s->ds->ctx->stream);
+    STGP_CUDA(cudaStreamSynchronize(s->ds->ctx->stream));
+  });
+}
+
+int stgp_structure_download_fitc_diag(const stgp_structure* s, double* out) {
+  return guarded([&] {
+    if (s->kind != STGP_FITC) config_error("only FITC structures carry fitc_diag");
+    s->lr.fitc_diag.download(out, static_cast<size_t>(s->n), s->ds->ctx->stream);
+    STGP_CUDA(cudaStreamSynchronize(s->ds->ctx->stream));
+  });
+}
+
+int stgp_nll(stgp_structure* s, const double* y, const double* X, int p, const double* beta, double* out) {
+  return guarded([&] {
+    if (!s || !out) config_error("stgp_nll: null argument");
+    compute_residual(s, y, X, p, beta);
+    if (s->kind == STGP_VECCHIA) *out = vecchia_nll(s);
+    else *out = lowrank_nll(s);
+  });
+}
+
+int stgp_nll_grad(stgp_structure* s, const double* y, const double* X, int p, const double* beta, double* grad) {
+  return guarded([&] {
+    if (!s || !grad) config_error("stgp_nll_grad: null argument");
+    compute_residual(s, y, X, p, beta);
+    if (s->kind == STGP_VECCHIA) vecchia_nll_grad(s, nullptr, grad);
+    else lowrank_nll_grad(s, nullptr, grad);
+  });
+}
+
+int stgp_nll_and_grad(stgp_structure* s, const double* y, const double* X, int p, const double* beta, double* nll,
+                      double* grad) {
+  return guarded([&] {
+    if (!s) config_error("stgp_nll_and_grad: null argument");
+    compute_residual(s, y, X, p, beta);
+    if (s->kind == STGP_VECCHIA) vecchia_nll_grad(s, nll, grad);
+    else lowrank_nll_grad(s, nll, grad);
+  });
+}
+
+int stgp_eval(stgp_structure* s, const stgp_params* theta, const double* y, const double* X, int p,
+              const double* beta, double* nll, double* grad) {
+  return guarded([&] {
+    if (!s) config_error("stgp_eval: null structure");
+    s->th = params_of(theta);
+    compute_residual(s, y, X, p, beta);
+    if (s->kind == STGP_VECCHIA) {
+      vecchia_nll_grad(s, nll, grad);
+    } else {
+      if (s->kind == STGP_FITC) fitc_build(s);
+      else vif_build(s);
+      lowrank_nll_grad(s, nll, grad);
+    }
+  });
+}
+
+int stgp_gls_beta(stgp_structure* s, const double* y, const double* X, int p, double* beta_out) {
+  return guarded([&] {
+    if (!s || !beta_out) config_error("stgp_gls_beta: null argument");
+    if (s->kind != STGP_FITC && s->policy != STGP_OBSERVATION)
+      numeric_error("gls_beta: requires the observation-policy structure");
+    if (p <= 0) return;
+    const int n = s->n;
+    const double* Xd;
+    const double* yd;
+    if (y) {
+      s->Xwork.upload(X, static_cast<size_t>(n) * p, s->ds->ctx->stream);
+      s->ywork.upload(y, static_cast<size_t>(n), s->ds->ctx->stream);
+      Xd = s->Xwork.get();
+      yd = s->ywork.get();
+    } else {
+      if (!s->ds->has_resp || s->ds->p != p) config_error("gls_beta: resident covariates do not match p");
+      Xd = s->ds->X.get();
+      yd = s->ds->resp.get();
+    }
+    // SX_j = Sigma~^{-1} X_j;  XtSX = X^T SX;  Xty = SX^T y  (approximations.cpp:752-765)
+    std::vector<double> XtSX(static_cast<size_t>(p) * p), Xty(static_cast<size_t>(p));
+    std::vector<double> hX(static_cast<size_t>(n) * p), hy(static_cast<size_t>(n));
+    DevBuf<double> tmpX;
+    tmpX.alloc(static_cast<size_t>(n) * p);
+    STGP_CUDA(cudaMemcpyAsync(hX.data(), Xd, sizeof(double) * n * p, cudaMemcpyDeviceToHost, s->ds->ctx->stream));
+    STGP_CUDA(cudaMemcpyAsync(hy.data(), yd, sizeof(double) * n, cudaMemcpyDeviceToHost, s->ds->ctx->stream));
+    STGP_CUDA(cudaStreamSynchronize(s->ds->ctx->stream));
+    for (int j = 0; j < p; ++j) {
+      const std::vector<double> sx = sigma_inv_apply_host(s, Xd + static_cast<size_t>(j) * n);
+      for (int a = 0; a < p; ++a) {
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) acc += hX[static_cast<size_t>(i) + static_cast<size_t>(a) * n] * sx[static_cast<size_t>(i)];
+        XtSX[static_cast<size_t>(a) + static_cast<size_t>(j) * p] = acc;
+      }
+      double acc = 0.0;
+      for (int i = 0; i < n; ++i) acc += sx[static_cast<size_t>(i)] * hy[static_cast<size_t>(i)];
+      Xty[static_cast<size_t>(j)] = acc;
+    }
+    // p x p SPD solve (the reference uses LDLT)
+    std::vector<double> L(XtSX);
+    for (int j = 0; j < p; ++j) {
+      double d = L[static_cast<size_t>(j) * p + j];
+      for (int k = 0; k < j; ++k) d -= L[static_cast<size_t>(j) + static_cast<size_t>(k) * p] * L[static_cast<size_t>(j) + static_cast<size_t>(k) * p];
+      if (!(d > 0.0)) numeric_error("gls_beta: normal equations are singular");
+      d = std::sqrt(d);
+      L[static_cast<size_t>(j) + static_cast<size_t>(j) * p] = d;
+      for (int r = j + 1; r < p; ++r) {
+        double v = L[static_cast<size_t>(r) + static_cast<size_t>(j) * p];
+        for (int k = 0; k < j; ++k) v -= L[static_cast<size_t>(r) + static_cast<size_t>(k) * p] * L[static_cast<size_t>(j) + static_cast<size_t>(k) * p];
+        L[static_cast<size_t>(r) + static_cast<size_t>(j) * p] = v / d;
+      }
+    }
+    std::vector<double> z(Xty);
+    for (int r = 0; r < p; ++r) {
+      for (int k = 0; k < r; ++k) z[static_cast<size_t>(r)] -= L[static_cast<size_t>(r) + static_cast<size_t>(k) * p] * z[static_cast<size_t>(k)];
+      z[static_cast<size_t>(r)] /= L[static_cast<size_t>(r) + static_cast<size_t>(r) * p];
+    }
+    for (int r = p - 1; r >= 0; --r) {
+      for (int k = r + 1; k < p; ++k) z[static_cast<size_t>(r)] -= L[static_cast<size_t>(k) + static_cast<size_t>(r) * p] * z[static_cast<size_t>(k)];
+      z[static_cast<size_t>(r)] /= L[static_cast<size_t>(r) + static_cast<size_t>(r) * p];
+    }
+    std::copy(z.begin(), z.end(), beta_out);
+  });
+}
+
+int stgp_predict(stgp_structure* s, const double* y, const double* X, int p, const double* beta, int n_p,
+                 const double* txyt, const double* Xp, int pred_m_v, double* mu, double* var) {
+  return guarded([&] {
+    if (!s || !mu || !var) config_error("stgp_predict: null argument");
+    if (s->kind != STGP_FITC && s->policy != STGP_OBSERVATION)
+      numeric_error("predict: requires the observation-policy structure");
+    compute_residual(s, y, X, p, beta);
+    if (n_p <= 0) return;
+    if (s->kind == STGP_VECCHIA) vecchia_predict(s, n_p, txyt, pred_m_v, mu, var);
+    else lowrank_predict(s, n_p, txyt, pred_m_v, mu, var);
+    // fixed effect X_p beta (approximations.cpp:806-812)
+    if (p > 0 && beta && Xp)
+      for (int k = 0; k < n_p; ++k) {
+        double fe = 0.0;
+        for (int j = 0; j < p; ++j) fe += Xp[static_cast<size_t>(k) + static_cast<size_t>(j) * n_p] * beta[j];
+        mu[k] += fe;
+      }
+  });
+}
+
+}  // extern "C"
