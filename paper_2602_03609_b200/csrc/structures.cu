@@ -44,6 +44,8 @@ stgp_structure* new_structure(stgp_dataset* ds, int kind, const Params& th, cons
   s->A.zero(st);
   s->D.zero(st);
   s->ti.T = ds->Tdata;
+  s->ti.build();
+  s->ti_dirty = true;
   s->fail.alloc(1);
   return s.release();
 }
