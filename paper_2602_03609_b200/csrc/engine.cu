@@ -315,6 +315,8 @@ RowArgs row_args(stgp_structure* s, const double* W, int ldw, double nugget) {
   a.A_out = s->A.get();
   a.D_out = s->D.get();
   a.fail_row = s->fail.get();
+  a.u_out = nullptr;
+  a.inv_c = 1.0 / s->th.c;
   host_grad00(s->th, a.g00);
   return a;
 }
@@ -334,10 +336,19 @@ std::vector<double> run_rows(stgp_structure* s, int mode, const double* W, int l
     s->red.ensure(blocks, 8);
     a.part = s->red.part.get();
     const bool hw = W != nullptr;
-#define STGP_ROWS(M, HW) vecchia_rows_kernel<M, HW><<<blocks, kRowWarps * 32, 0, ctx->stream>>>(a)
-    if (mode == kModeBuild) { if (hw) STGP_ROWS(kModeBuild, true); else STGP_ROWS(kModeBuild, false); }
-    else if (mode == kModeNll) { if (hw) STGP_ROWS(kModeNll, true); else STGP_ROWS(kModeNll, false); }
-    else { if (hw) STGP_ROWS(kModeGrad, true); else STGP_ROWS(kModeGrad, false); }
+    const int ks = s->m_v <= 8 ? 8 : (s->m_v <= 16 ? 16 : (s->m_v <= 24 ? 24 : 31));
+#define STGP_ROWS(M, HW, KS) vecchia_rows_kernel<M, HW, KS><<<blocks, kRowWarps * 32, 0, ctx->stream>>>(a)
+#define STGP_ROWS_KS(M, HW)              \
+  switch (ks) {                          \
+    case 8: STGP_ROWS(M, HW, 8); break;   \
+    case 16: STGP_ROWS(M, HW, 16); break; \
+    case 24: STGP_ROWS(M, HW, 24); break; \
+    default: STGP_ROWS(M, HW, 31); break; \
+  }
+    if (mode == kModeBuild) { if (hw) { STGP_ROWS_KS(kModeBuild, true) } else { STGP_ROWS_KS(kModeBuild, false) } }
+    else if (mode == kModeNll) { if (hw) { STGP_ROWS_KS(kModeNll, true) } else { STGP_ROWS_KS(kModeNll, false) } }
+    else { if (hw) { STGP_ROWS_KS(kModeGrad, true) } else { STGP_ROWS_KS(kModeGrad, false) } }
+#undef STGP_ROWS_KS
 #undef STGP_ROWS
   } else {
     const int threads = 64;

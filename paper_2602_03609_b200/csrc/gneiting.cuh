@@ -128,6 +128,34 @@ __device__ __forceinline__ double gneiting_grad(const DevKernel& k, double h, co
   return __dmul_rn(base, M);
 }
 
+// Gradient with the divisions replaced by precomputed reciprocals (inv_c = 1/c);
+// used where only the 1e-8 tolerance applies (likelihood gradients).
+__device__ __forceinline__ void gneiting_grad_fast(const DevKernel& k, double inv_c, double h, const TF& f,
+                                                   double g[6]) {
+  const double x = k.c * h * f.pow_mbh;
+  const double e = glibc_exp(-x);
+  double M, Mp;
+  if (k.nu_code == 0) {
+    M = e;
+    Mp = -e;
+  } else if (k.nu_code == 1) {
+    M = (1.0 + x) * e;
+    Mp = -x * e;
+  } else {
+    M = (1.0 + x + x * x * (1.0 / 3.0)) * e;
+    Mp = -(x * (1.0 + x) * (1.0 / 3.0)) * e;
+  }
+  if (x == 0.0) M = 1.0;
+  const double base = k.s1 * f.pow_mE;
+  g[0] = f.pow_mE * M;
+  const double dC_dT = base * f.inv_T * (-k.E * M - 0.5 * k.beta * x * Mp);
+  g[1] = dC_dT * f.u2a;
+  g[3] = dC_dT * 2.0 * k.a * f.u2a_logu;
+  g[2] = base * Mp * x * inv_c;
+  g[4] = -f.log_T * base * (M + 0.5 * x * Mp);
+  g[5] = -f.log_T * base * M;
+}
+
 // Temporal-factor table indexed by time-id pairs (host-computed with glibc).
 struct TFTable {
   const TF* tab;  // nT * nT

@@ -1,17 +1,19 @@
 // Per-observation Vecchia/VIF row kernels (K1, K1g, K3 of SURVEY.md §2.4).
 //
-// One warp per row i.  The closure cl(i) = [N_0 .. N_{k-1}, i] (k <= 31) lives in
-// lanes 0..k; lane r owns row r of the k x k conditioning block in registers.
-//   phase A  pairwise Gneiting covariances of the closure (lane-strided over the
-//            k(k+1)/2 off-diagonal pairs) -> shared memory;
-//            VIF: minus the closure Gram W_cl^T W_cl computed with FP64 DMMA
-//            (mma.sync m8n8k4 f64) straight from the column-major W in HBM/L2;
-//   phase B  in-register right-looking Cholesky with the reference's jitter
-//            ladder (approximations.cpp:91-103), forward/back solves;
-//   phase C  A_i, D_i (approximations.cpp:104-110), u_i = (B r)_i and the NLL
-//            term log D_i + u_i^2/D_i (approximations.cpp:340-346);
-//   phase D  (gradient) kernel gradients over the closure pairs weighted by
-//            c_d * a~a~' - c_u * sym(w~ a~') (approximations.cpp:419-483).
+// One warp per row i.  Closure slots: 0..k-1 hold N(i) (ascending), k..KS-1 are
+// identity padding, slot KS holds i itself (KS >= m_v is a compile-time size,
+// KS <= 31).  Lane r owns row r of the KS x KS conditioning block in registers.
+//   phase A  pairwise Gneiting covariances of the closure, lane-strided over a
+//            shared pair table, into shared memory; VIF: minus the closure Gram
+//            W_cl^T W_cl computed with FP64 DMMA (mma.sync m8n8k4 f64) straight
+//            from the column-major W in HBM/L2;
+//   phase B  right-looking Cholesky in registers: pivot broadcast by shuffle,
+//            1/sqrt once per column, L column broadcast through shared memory;
+//            the reference's jitter ladder (approximations.cpp:91-103);
+//   phase C  A_i = C^{-1} c, D_i = d_ii - A.c (approximations.cpp:104-110),
+//            u_i = (B r)_i, NLL term log D_i + u_i^2 / D_i (approximations.cpp:340-346);
+//   phase D  (gradient) kernel gradients over closure pairs weighted by
+//            c_d a~a~' - c_u sym(w~ a~') (approximations.cpp:419-483).
 // Per-row results are reduced per block in a fixed order (deterministic).
 #pragma once
 
@@ -65,21 +67,14 @@ struct RowArgs {
   const double* r;  // residual y - X beta (NLL / gradient modes)
   double* A_out;    // n * m_v (optional)
   double* D_out;    // n (optional)
+  double* u_out;    // n (optional): u_i = (B r)_i
   double* part;     // per-block partial sums [gridDim.x][8]
   int* fail_row;    // min failing row index (init INT_MAX)
   double g00[6];    // kernel gradient at (h, u) = (0, 0)
+  double inv_c;     // 1 / c
 };
 
 enum RowMode { kModeBuild = 0, kModeNll = 1, kModeGrad = 2 };
-
-__device__ __forceinline__ void unrank_pair(int p, int& a, int& b) {
-  // p -> (a, b), b < a, enumerating a = 1.. : p = a(a-1)/2 + b
-  int aa = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * static_cast<float>(p))) * 0.5f);
-  while (aa * (aa - 1) / 2 > p) --aa;
-  while ((aa + 1) * aa / 2 <= p) ++aa;
-  a = aa;
-  b = p - aa * (aa - 1) / 2;
-}
 
 __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -87,10 +82,11 @@ __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, doubl
                : "d"(a), "d"(b));
 }
 
-// Closure Gram G = W_cl^T W_cl (32 x 32, lower 8x8 tiles) with DMMA; result into sG (row-major, ld 33).
-// col[c] = column index of closure slot c (or -1 for empty slots).
+// Closure Gram G = W_cl^T W_cl over 32 slots (lower 8x8 tiles, mirrored) with
+// DMMA; scol[c] = column of slot c or -1.  Result into sG (row stride LD).
+template <int LD>
 __device__ __forceinline__ void closure_gram_dmma(const double* __restrict__ W, int ldw, const int* scol,
-                                                  double (*sG)[33], int lane) {
+                                                  double* sG, int lane) {
   const int grp = lane >> 2, tig = lane & 3;
   double acc[10][2];
 #pragma unroll
@@ -99,12 +95,12 @@ __device__ __forceinline__ void closure_gram_dmma(const double* __restrict__ W, 
 #pragma unroll
   for (int I = 0; I < 4; ++I) {
     const int c = scol[8 * I + grp];
-    colp[I] = c >= 0 ? W + static_cast<size_t>(c) * ldw : nullptr;
+    colp[I] = c >= 0 ? W + static_cast<size_t>(c) * ldw + tig : nullptr;
   }
   for (int kb = 0; kb < ldw; kb += 4) {
     double f[4];
 #pragma unroll
-    for (int I = 0; I < 4; ++I) f[I] = colp[I] ? __ldg(colp[I] + kb + tig) : 0.0;
+    for (int I = 0; I < 4; ++I) f[I] = colp[I] ? __ldg(colp[I] + kb) : 0.0;
     int t = 0;
 #pragma unroll
     for (int I = 0; I < 4; ++I)
@@ -120,34 +116,48 @@ __device__ __forceinline__ void closure_gram_dmma(const double* __restrict__ W, 
 #pragma unroll
     for (int J = 0; J <= I; ++J) {
       const int r = 8 * I + grp, c = 8 * J + 2 * tig;
-      sG[r][c] = acc[t][0];
-      sG[r][c + 1] = acc[t][1];
-      sG[c][r] = acc[t][0];
-      sG[c + 1][r] = acc[t][1];
+      sG[r * LD + c] = acc[t][0];
+      sG[r * LD + c + 1] = acc[t][1];
+      sG[c * LD + r] = acc[t][0];
+      sG[(c + 1) * LD + r] = acc[t][1];
       ++t;
     }
 }
 
-template <int MODE, bool HAS_W>
-__global__ void __launch_bounds__(kRowWarps * 32) vecchia_rows_kernel(RowArgs a) {
-  __shared__ double sC[kRowWarps][kKmax][33];
-  __shared__ double sx[kRowWarps][kKmax], sy[kRowWarps][kKmax], sAw[kRowWarps][2][kKmax];
-  __shared__ int st[kRowWarps][kKmax], scol[kRowWarps][kKmax];
+template <int MODE, bool HAS_W, int KS>
+__global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs a) {
+  static_assert(KS >= 1 && KS <= 31, "closure must fit a warp");
+  constexpr int NS = KS + 1;           // closure slots
+  constexpr int LD = 33;               // smem row stride (doubles)
+  constexpr int NP = NS * (NS - 1) / 2;
+  __shared__ uint16_t sPair[NP];
+  __shared__ double sC[kRowWarps][32 * LD];
+  __shared__ double sx[kRowWarps][32], sy[kRowWarps][32], sAw[kRowWarps][2][32];
+  __shared__ double sCol[kRowWarps][2][32];
+  __shared__ int st[kRowWarps][32], scol[kRowWarps][32];
   __shared__ double sred[kRowWarps][8];
 
+  for (int p = threadIdx.x; p < NP; p += blockDim.x) {
+    int aa = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * static_cast<float>(p))) * 0.5f);
+    while (aa * (aa - 1) / 2 > p) --aa;
+    while ((aa + 1) * aa / 2 <= p) ++aa;
+    sPair[p] = static_cast<uint16_t>(aa | ((p - aa * (aa - 1) / 2) << 8));
+  }
+  __syncthreads();
+
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* C = sC[w];
   double tot[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) tot[q] = 0.0;
 
   const int gw = blockIdx.x * kRowWarps + w, nw = gridDim.x * kRowWarps;
   for (int i = a.row_begin + gw; i < a.row_end; i += nw) {
-    // ---- closure ----
+    // ---- closure slots ----
     int nb = -1;
     if (lane < a.m_v) nb = __ldg(&a.nbr[static_cast<size_t>(i) * a.m_v + lane]);
-    const unsigned vmask = __ballot_sync(kFull, nb >= 0);
-    const int k = __popc(vmask);  // neighbours are packed at the front
-    const int pt = lane < k ? nb : (lane == k ? i : -1);
+    const int k = __popc(__ballot_sync(kFull, nb >= 0));  // neighbours packed at the front
+    const int pt = lane < k ? nb : (lane == KS ? i : -1);
     double rp = 0.0;
     if (pt >= 0) {
       sx[w][lane] = __ldg(&a.x[pt]);
@@ -157,115 +167,101 @@ __global__ void __launch_bounds__(kRowWarps * 32) vecchia_rows_kernel(RowArgs a)
     }
     scol[w][lane] = pt;
     __syncwarp();
-    if (HAS_W) closure_gram_dmma(a.W, a.ldw, scol[w], sC[w], lane);  // Gram staged in sC
+    if (HAS_W) closure_gram_dmma<LD>(a.W, a.ldw, scol[w], C, lane);  // Gram staged in C
     __syncwarp();
-    // ---- phase A: covariances over the closure ----
+    // ---- phase A: covariances over the closure (compact slot k maps to KS) ----
     const int P = (k + 1) * k / 2;
     for (int p = lane; p < P; p += 32) {
-      int ai, bi;
-      unrank_pair(p, ai, bi);
+      const int pr = sPair[p];
+      const int ca = pr & 0xff, sb = pr >> 8;
+      const int sa = ca == k ? KS : ca;
       double pe, pb;
-      a.lt.get2(st[w][ai], st[w][bi], pe, pb);
+      a.lt.get2(st[w][sa], st[w][sb], pe, pb);
       TF f;
       f.pow_mE = pe;
       f.pow_mbh = pb;
-      double v = gneiting_eval(a.k, spatial_dist(sx[w][ai], sy[w][ai], sx[w][bi], sy[w][bi]), f);
-      if (HAS_W) v = __dsub_rn(v, sC[w][ai][bi]);  // each pair slot is owned by one lane
-      sC[w][ai][bi] = v;  // ai == k: cross covariance c_iN stored in row k
-      sC[w][bi][ai] = v;
+      double v = gneiting_eval(a.k, spatial_dist(sx[w][sa], sy[w][sa], sx[w][sb], sy[w][sb]), f);
+      if (HAS_W) v = __dsub_rn(v, C[sa * LD + sb]);  // each pair slot is owned by one lane
+      C[sa * LD + sb] = v;
+      C[sb * LD + sa] = v;
     }
-    {
+    if (lane < k || lane == KS) {
       // diagonal: k(p,p) = sigma1_2 exactly; minus |w_p|^2 for VIF; plus nugget
       double v = a.s1;
-      if (HAS_W && lane <= k) v = __dsub_rn(v, sC[w][lane][lane]);
-      if (lane <= k) sC[w][lane][lane] = __dadd_rn(v, a.nugget);
+      if (HAS_W) v = __dsub_rn(v, C[lane * LD + lane]);
+      C[lane * LD + lane] = __dadd_rn(v, a.nugget);
     }
     __syncwarp();
-    const double dii = sC[w][k][k];
-    // ---- phase B: Cholesky of the k x k block in registers ----
-    double R[kKmax];
-    double jit = 0.0;
+    const double dii = C[KS * LD + KS];
+    const double cval = lane < k ? C[KS * LD + lane] : 0.0;
+    // ---- phase B: Cholesky of the KS x KS block (identity-padded) in registers ----
+    double R[KS];
+    double dinv = 0.0;  // lane j keeps 1 / L_jj
     bool ok = false;
     for (int attempt = 0; attempt < 3 && !ok; ++attempt) {
-      if (attempt == 1) jit = 1e-10 * a.s1;
-      if (attempt == 2) jit = 9.0 * (1e-10 * a.s1);
 #pragma unroll
-      for (int c = 0; c < kKmax; ++c) R[c] = (lane < k && c < k) ? sC[w][lane][c] : (c == lane ? 1.0 : 0.0);
+      for (int c = 0; c < KS; ++c) R[c] = (lane < k && c < k) ? C[lane * LD + c] : (c == lane ? 1.0 : 0.0);
       if (attempt >= 1 && lane < k) {
         // cumulative ladder: (C + j) then (C + j) + 9j, as the reference mutates C_N in place
-        double d = __dadd_rn(sC[w][lane][lane], 1e-10 * a.s1);
-        if (attempt == 2) d = __dadd_rn(d, jit);
+        double d = __dadd_rn(C[lane * LD + lane], 1e-10 * a.s1);
+        if (attempt == 2) d = __dadd_rn(d, 9.0 * (1e-10 * a.s1));
 #pragma unroll
-        for (int c = 0; c < kKmax; ++c)
+        for (int c = 0; c < KS; ++c)
           if (c == lane) R[c] = d;
       }
       bool good = true;
 #pragma unroll
-      for (int j = 0; j < kKmax; ++j) {
-        if (j < k && good) {
-          const double piv = __shfl_sync(kFull, R[j], j);
-          if (!(piv > 0.0)) {
-            if (piv <= 0.0) good = false;
-          }
-          if (good) {
-            const double ljj = sqrt(piv);
-            if (lane == j) R[j] = ljj;
-            else if (lane > j) R[j] = R[j] / ljj;
+      for (int j = 0; j < KS; ++j) {
+        const double piv = __shfl_sync(kFull, R[j], j);
+        good = good && (piv > 0.0);
+        const double inv = rsqrt(piv);
+        R[j] = lane == j ? piv * inv : R[j] * inv;
+        if (lane == j) dinv = inv;
+        double* col = sCol[w][j & 1];
+        col[lane] = R[j];
+        __syncwarp();
 #pragma unroll
-            for (int c = j + 1; c < kKmax; ++c) {
-              if (c < k) {
-                const double lcj = __shfl_sync(kFull, R[j], c);
-                if (lane >= c) R[c] = fma(-R[j], lcj, R[c]);
-              }
-            }
-          }
-        }
+        for (int c = j + 1; c < KS; ++c) R[c] = fma(-R[j], col[c], R[c]);  // upper entries: unused garbage
       }
-      ok = good;
+      ok = __all_sync(kFull, good);
     }
     if (!ok) {
       if (lane == 0) atomicMin(a.fail_row, i);
       continue;
     }
-    // L rows to smem for the back substitution
-    __syncwarp();
-    const double cval = lane < k ? sC[w][k][lane] : 0.0;
+    // L rows to smem for the back substitution (C no longer needed)
     __syncwarp();
 #pragma unroll
-    for (int c = 0; c < kKmax; ++c)
-      if (c <= lane && lane < k) sC[w][lane][c] = R[c];
+    for (int c = 0; c < KS; ++c)
+      if (c <= lane) C[lane * LD + c] = R[c];
     __syncwarp();
     // ---- solves: b1 = C^{-1} c (A), b2 = C^{-1} r_N (gradient) ----
     double b1 = cval, b2 = (MODE == kModeGrad && lane < k) ? rp : 0.0;
 #pragma unroll
-    for (int j = 0; j < kKmax; ++j) {
-      if (j < k) {
-        if (lane == j) {
-          b1 = b1 / R[j];
-          if (MODE == kModeGrad) b2 = b2 / R[j];
-        }
-        const double y1 = __shfl_sync(kFull, b1, j);
-        const double y2 = MODE == kModeGrad ? __shfl_sync(kFull, b2, j) : 0.0;
-        if (lane > j) {
-          b1 = fma(-R[j], y1, b1);
-          if (MODE == kModeGrad) b2 = fma(-R[j], y2, b2);
-        }
+    for (int j = 0; j < KS; ++j) {
+      if (lane == j) {
+        b1 *= dinv;
+        if (MODE == kModeGrad) b2 *= dinv;
+      }
+      const double y1 = __shfl_sync(kFull, b1, j);
+      const double y2 = MODE == kModeGrad ? __shfl_sync(kFull, b2, j) : 0.0;
+      if (lane > j) {
+        b1 = fma(-R[j], y1, b1);
+        if (MODE == kModeGrad) b2 = fma(-R[j], y2, b2);
       }
     }
 #pragma unroll
-    for (int j = kKmax - 1; j >= 0; --j) {
-      if (j < k) {
-        if (lane == j) {
-          b1 = b1 / R[j];
-          if (MODE == kModeGrad) b2 = b2 / R[j];
-        }
-        const double x1 = __shfl_sync(kFull, b1, j);
-        const double x2 = MODE == kModeGrad ? __shfl_sync(kFull, b2, j) : 0.0;
-        if (lane < j) {
-          const double ljl = sC[w][j][lane];
-          b1 = fma(-ljl, x1, b1);
-          if (MODE == kModeGrad) b2 = fma(-ljl, x2, b2);
-        }
+    for (int j = KS - 1; j >= 0; --j) {
+      if (lane == j) {
+        b1 *= dinv;
+        if (MODE == kModeGrad) b2 *= dinv;
+      }
+      const double x1 = __shfl_sync(kFull, b1, j);
+      const double x2 = MODE == kModeGrad ? __shfl_sync(kFull, b2, j) : 0.0;
+      if (lane < j) {
+        const double ljl = C[j * LD + lane];
+        b1 = fma(-ljl, x1, b1);
+        if (MODE == kModeGrad) b2 = fma(-ljl, x2, b2);
       }
     }
     const double Aval = lane < k ? b1 : 0.0;
@@ -275,9 +271,11 @@ __global__ void __launch_bounds__(kRowWarps * 32) vecchia_rows_kernel(RowArgs a)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       ac += __shfl_xor_sync(kFull, ac, o);
-      ar += __shfl_xor_sync(kFull, ar, o);
-      aa += __shfl_xor_sync(kFull, aa, o);
-      aw += __shfl_xor_sync(kFull, aw, o);
+      if (MODE != kModeBuild) ar += __shfl_xor_sync(kFull, ar, o);
+      if (MODE == kModeGrad) {
+        aa += __shfl_xor_sync(kFull, aa, o);
+        aw += __shfl_xor_sync(kFull, aw, o);
+      }
     }
     const double D = dii - ac;
     if (!(D > 0.0)) {
@@ -287,24 +285,26 @@ __global__ void __launch_bounds__(kRowWarps * 32) vecchia_rows_kernel(RowArgs a)
     if (a.A_out && lane < a.m_v) a.A_out[static_cast<size_t>(i) * a.m_v + lane] = Aval;
     if (a.D_out && lane == 0) a.D_out[i] = D;
     if (MODE == kModeBuild) continue;
-    const double ri = __shfl_sync(kFull, rp, k);
+    const double ri = __shfl_sync(kFull, rp, KS);
     const double u = ri - ar;
+    if (a.u_out && lane == 0) a.u_out[i] = u;
     if (lane == 0) tot[0] += log(D) + u * u / D;
     if (MODE != kModeGrad) continue;
     // ---- phase D: gradient over closure pairs ----
-    sAw[w][0][lane] = lane < k ? -Aval : (lane == k ? 1.0 : 0.0);  // a~
-    sAw[w][1][lane] = wval;                                         // w~ (0 at i)
+    sAw[w][0][lane] = lane < k ? -Aval : (lane == KS ? 1.0 : 0.0);  // a~
+    sAw[w][1][lane] = wval;                                          // w~ (0 at i)
     __syncwarp();
     const double cd = 0.5 * (1.0 / D - u * u / (D * D));
     const double cu = u / D;
     double g[6] = {0, 0, 0, 0, 0, 0};
     for (int p = lane; p < P; p += 32) {
-      int ai, bi;
-      unrank_pair(p, ai, bi);
-      const TF f = a.lt.get(st[w][ai], st[w][bi]);
+      const int pr = sPair[p];
+      const int ca = pr & 0xff, sb = pr >> 8;
+      const int sa = ca == k ? KS : ca;
+      const TF f = a.lt.get(st[w][sa], st[w][sb]);
       double kg[6];
-      gneiting_grad(a.k, spatial_dist(sx[w][ai], sy[w][ai], sx[w][bi], sy[w][bi]), f, kg);
-      const double ta = sAw[w][0][ai], tb = sAw[w][0][bi], wa = sAw[w][1][ai], wb = sAw[w][1][bi];
+      gneiting_grad_fast(a.k, a.inv_c, spatial_dist(sx[w][sa], sy[w][sa], sx[w][sb], sy[w][sb]), f, kg);
+      const double ta = sAw[w][0][sa], tb = sAw[w][0][sb], wa = sAw[w][1][sa], wb = sAw[w][1][sb];
       const double wt = cd * (2.0 * ta * tb) - cu * (wa * tb + wb * ta);
 #pragma unroll
       for (int q = 0; q < 6; ++q) g[q] = fma(wt, kg[q], g[q]);
@@ -335,12 +335,11 @@ __global__ void __launch_bounds__(kRowWarps * 32) vecchia_rows_kernel(RowArgs a)
   }
 }
 
-// Sum per-block partials in a fixed order: out[q] = sum_b part[b][q].
+// Sum per-block partials in a fixed order: out[q] = sum_b part[b][q] (compensated).
 static __global__ void reduce_parts_kernel(const double* part, int nblocks, int width, double* out) {
   const int q = threadIdx.x;
   if (q >= width) return;
-  // pairwise tree over blocks for accuracy, fixed shape
-  double s = 0.0, c = 0.0;  // Kahan-compensated running sum
+  double s = 0.0, c = 0.0;
   for (int b = 0; b < nblocks; ++b) {
     const double y = part[static_cast<size_t>(b) * width + q] - c;
     const double t = s + y;
