@@ -1,0 +1,38 @@
+// Dense FP64 linear algebra on the device for the M x M / M x n low-rank pieces.
+// Large contractions (TRSM, SYRK, GEMM over n columns) are plain library
+// products (cuBLAS, FP64 tensor cores); the blocked Cholesky drives them with a
+// hand-written diagonal-block factorization that reports failure instead of
+// producing NaNs (Eigen's LLT info() semantics, used by the jitter ladders).
+#pragma once
+
+#include <cublas_v2.h>
+
+#include "common.cuh"
+
+struct stgp_ctx;
+
+namespace stgp {
+
+void cublas_check(cublasStatus_t s, const char* what);
+
+// In-place lower Cholesky of the leading n x n block of A (column-major, ld).
+// Returns false when a pivot is not positive (the factor is then unusable).
+bool dev_cholesky(stgp_ctx* ctx, double* A, int ld, int n);
+// 2 * sum log diag(L)
+double dev_logdet_chol(stgp_ctx* ctx, const double* L, int ld, int n);
+// B <- op(L)^{-1} B for lower-triangular L (n x n), B n x ncols (ldb).
+void dev_trsm_left(stgp_ctx* ctx, const double* L, int ldl, int n, double* B, int ldb, long long ncols,
+                   bool transpose);
+// C (n x n, lower) = alpha * A A^T + beta * C, A n x k (lda)
+void dev_syrk(stgp_ctx* ctx, int n, long long k, double alpha, const double* A, int lda, double beta, double* C,
+              int ldc);
+// C = alpha op(A) op(B) + beta C
+void dev_gemm(stgp_ctx* ctx, bool ta, bool tb, int m, int n, long long k, double alpha, const double* A, int lda,
+              const double* B, int ldb, double beta, double* C, int ldc);
+// y = alpha op(A) x + beta y
+void dev_gemv(stgp_ctx* ctx, bool ta, int m, long long n, double alpha, const double* A, int lda, const double* x,
+              double beta, double* y);
+// copy the lower triangle into the upper triangle
+void dev_symmetrize_lower(stgp_ctx* ctx, double* A, int ld, int n);
+
+}  // namespace stgp

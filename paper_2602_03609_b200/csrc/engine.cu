@@ -323,20 +323,24 @@ RowArgs row_args(stgp_structure* s, const double* W, int ldw, double nugget) {
 
 // Launch the per-row kernel in the given mode; returns the 8 reduced partials.
 std::vector<double> run_rows(stgp_structure* s, int mode, const double* W, int ldw, double nugget) {
-  stgp_ctx* ctx = s->ds->ctx;
   RowArgs a = row_args(s, W, ldw, nugget);
+  return run_rows_args(s, mode, a);
+}
+
+std::vector<double> run_rows_args(stgp_structure* s, int mode, RowArgs& a) {
+  stgp_ctx* ctx = s->ds->ctx;
   const int rows = s->row_end - s->row_begin;
   int fail_init = INT_MAX;
   s->fail.upload(&fail_init, 1, ctx->stream);
+  const bool hw = a.W != nullptr;
   int blocks;
   {
-  ProfRegion pr(ctx, "rows");
-  if (s->m_v <= kKmax - 1) {
-    blocks = row_blocks(ctx, rows);
-    s->red.ensure(blocks, 8);
-    a.part = s->red.part.get();
-    const bool hw = W != nullptr;
-    const int ks = s->m_v <= 8 ? 8 : (s->m_v <= 16 ? 16 : (s->m_v <= 24 ? 24 : 31));
+    ProfRegion pr(ctx, mode == kModeVifGrad ? "rows_vifgrad" : "rows");
+    if (s->m_v <= kKmax - 1) {
+      blocks = row_blocks(ctx, rows);
+      s->red.ensure(blocks, 8);
+      a.part = s->red.part.get();
+      const int ks = s->m_v <= 8 ? 8 : (s->m_v <= 16 ? 16 : (s->m_v <= 24 ? 24 : 31));
 #define STGP_ROWS(M, HW, KS) vecchia_rows_kernel<M, HW, KS><<<blocks, kRowWarps * 32, 0, ctx->stream>>>(a)
 #define STGP_ROWS_KS(M, HW)              \
   switch (ks) {                          \
@@ -345,26 +349,28 @@ std::vector<double> run_rows(stgp_structure* s, int mode, const double* W, int l
     case 24: STGP_ROWS(M, HW, 24); break; \
     default: STGP_ROWS(M, HW, 31); break; \
   }
-    if (mode == kModeBuild) { if (hw) { STGP_ROWS_KS(kModeBuild, true) } else { STGP_ROWS_KS(kModeBuild, false) } }
-    else if (mode == kModeNll) { if (hw) { STGP_ROWS_KS(kModeNll, true) } else { STGP_ROWS_KS(kModeNll, false) } }
-    else { if (hw) { STGP_ROWS_KS(kModeGrad, true) } else { STGP_ROWS_KS(kModeGrad, false) } }
+      if (mode == kModeBuild) { if (hw) { STGP_ROWS_KS(kModeBuild, true) } else { STGP_ROWS_KS(kModeBuild, false) } }
+      else if (mode == kModeNll) { if (hw) { STGP_ROWS_KS(kModeNll, true) } else { STGP_ROWS_KS(kModeNll, false) } }
+      else if (mode == kModeGrad) { if (hw) { STGP_ROWS_KS(kModeGrad, true) } else { STGP_ROWS_KS(kModeGrad, false) } }
+      else { STGP_ROWS_KS(kModeVifGrad, true) }
 #undef STGP_ROWS_KS
 #undef STGP_ROWS
-  } else {
-    const int threads = 64;
-    blocks = std::max(1, std::min(ceil_div(rows, threads), 64));
-    const size_t K = static_cast<size_t>(s->m_v);
-    const size_t slab = K * K + 8 * K + 16;
-    s->scratch.ensure(slab * threads * blocks);
-    s->red.ensure(blocks, 8);
-    a.part = s->red.part.get();
-    const bool hw = W != nullptr;
+    } else {
+      if (mode == kModeVifGrad)
+        config_error("VIF gradient supports neighbour sets of size <= 31 (warp-per-row kernel)");
+      const int threads = 64;
+      blocks = std::max(1, std::min(ceil_div(rows, threads), 64));
+      const size_t K = static_cast<size_t>(s->m_v);
+      const size_t slab = K * K + 8 * K + 16;
+      s->scratch.ensure(slab * threads * blocks);
+      s->red.ensure(blocks, 8);
+      a.part = s->red.part.get();
 #define STGP_ROWS(M, HW) vecchia_rows_serial_kernel<M, HW><<<blocks, threads, 0, ctx->stream>>>(a, s->scratch.get())
-    if (mode == kModeBuild) { if (hw) STGP_ROWS(kModeBuild, true); else STGP_ROWS(kModeBuild, false); }
-    else if (mode == kModeNll) { if (hw) STGP_ROWS(kModeNll, true); else STGP_ROWS(kModeNll, false); }
-    else { if (hw) STGP_ROWS(kModeGrad, true); else STGP_ROWS(kModeGrad, false); }
+      if (mode == kModeBuild) { if (hw) STGP_ROWS(kModeBuild, true); else STGP_ROWS(kModeBuild, false); }
+      else if (mode == kModeNll) { if (hw) STGP_ROWS(kModeNll, true); else STGP_ROWS(kModeNll, false); }
+      else { if (hw) STGP_ROWS(kModeGrad, true); else STGP_ROWS(kModeGrad, false); }
 #undef STGP_ROWS
-  }
+    }
   }
   ++ctx->launches;
   STGP_LAUNCH_CHECK();

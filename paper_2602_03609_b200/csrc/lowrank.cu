@@ -1,50 +1,791 @@
-// FITC / VIF low-rank algebra (approximations.cpp:217-312, 352-384, 495-744, 923-1080).
+// FITC / VIF low-rank algebra (approximations.cpp:217-312, 352-384, 495-744).
+//
+// Everything is carried in the whitened basis of the inducing Cholesky factor
+// L_m (Sigma_m + jitter = L_m L_m^T, inducing.cpp:237-262):
+//   W = L_m^{-1} U            (U_ji = k(z_j, p_i), M x n)
+//   VIF:  V' = W B^T,  K = I + V' D^{-1} V'^T  so that M_core = L_m K L_m^T and
+//         log|M_core| - log|Sigma_m| = log|K|, w' M^{-1} w = (W ur)' K^{-1} (W ur)
+//   FITC: K = I + W Lambda^{-1} W^T
+// The reference's M x n temporaries (P = Sigma_m^{-1} U, N1, Hhat, omega, ...)
+// become L_m^{-T} times whitened quantities; the only dense n x M^2 work left is
+// the TRSM for W, one SYRK for K, two TRSMs for X = K^{-1} V', one GEMM for the
+// Sigma_m-pair weights and one TRSM for omega -- the canonical 3.5 n M^2 of
+// SURVEY.md §8(d).  All sparse B / B^T products are deterministic gathers (a
+// CSC of B's pattern is built once per structure).
+#include <climits>
+#include <cstring>
+#include <numeric>
+#include <set>
+
+#include <cub/device/device_scan.cuh>
+
 #include "comm.hpp"
+#include "dense.cuh"
+#include "lowrank_common.cuh"
+#include "rows.cuh"
 #include "structure.hpp"
 #include "../../include/stgp_b200.h"
 
 namespace stgp {
-void lowrank_setup(stgp_structure*, const stgp_inducing*) { config_error("FITC/VIF: not built yet"); }
-void fitc_build(stgp_structure*) { config_error("FITC: not built yet"); }
-void vif_build(stgp_structure*) { config_error("VIF: not built yet"); }
-double lowrank_nll(stgp_structure*) { config_error("FITC/VIF: not built yet"); }
-void lowrank_nll_grad(stgp_structure*, double*, double*) { config_error("FITC/VIF: not built yet"); }
-void lowrank_predict(stgp_structure*, int, const double*, int, double*, double*) { config_error("predict: not built yet"); }
-void vecchia_predict(stgp_structure*, int, const double*, int, double*, double*) { config_error("predict: not built yet"); }
-std::vector<double> sigma_inv_apply_host(stgp_structure*, const double*) { config_error("gls: not built yet"); }
+
+namespace {
+
+constexpr int kT = kLrThreads;
+
+struct ZPts {
+  const double *zx, *zy;
+  const int32_t* ztid;
+};
+
+// Sigma_m(i, j) = k(z_i, z_j) (inducing.cpp:242-249) + diagonal jitter; padded part = identity
+__global__ void sigma_m_kernel(ZPts z, int M, int ldm, DevKernel k, LagTable lt, double jit1, double jit2,
+                               double* S) {
+  const long long total = static_cast<long long>(ldm) * ldm;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e % ldm), c = static_cast<int>(e / ldm);
+    double v;
+    if (r >= M || c >= M) {
+      v = r == c ? 1.0 : 0.0;
+    } else {
+      const int a = r >= c ? r : c, b = r >= c ? c : r;  // evaluate k(z_a, z_b), a >= b (loop order of the reference)
+      double pe, pb;
+      lt.get2(z.ztid[a], z.ztid[b], pe, pb);
+      TF f;
+      f.pow_mE = pe;
+      f.pow_mbh = pb;
+      v = gneiting_eval(k, spatial_dist(z.zx[a], z.zy[a], z.zx[b], z.zy[b]), f);
+      if (r == c) {
+        v = __dadd_rn(v, jit1);
+        if (jit2 != 0.0) v = __dadd_rn(v, jit2);
+      }
+    }
+    S[static_cast<size_t>(c) * ldm + r] = v;
+  }
+}
+
+// U(j, i) = k(z_j, p_i) (approximations.cpp:226-232), columns [c0, c1)
+__global__ void cross_cov_kernel(ZPts z, int M, int ldm, const double* x, const double* y, const int32_t* tid,
+                                 int c0, int c1, DevKernel k, LagTable lt, double* U) {
+  for (int i = c0 + blockIdx.x; i < c1; i += gridDim.x) {
+    const double xi = x[i], yi = y[i];
+    const int ti = tid[i];
+    double* col = U + static_cast<size_t>(i) * ldm;
+    for (int j = threadIdx.x; j < ldm; j += blockDim.x) {
+      double v = 0.0;
+      if (j < M) {
+        double pe, pb;
+        lt.get2(z.ztid[j], ti, pe, pb);
+        TF f;
+        f.pow_mE = pe;
+        f.pow_mbh = pb;
+        v = gneiting_eval(k, spatial_dist(z.zx[j], z.zy[j], xi, yi), f);
+      }
+      col[j] = v;
+    }
+  }
+}
+
+// V'(:, r) = (W B^T)(:, r) = W(:, r) - sum_a A(r, a) W(:, N_a)   (approximations.cpp:298-305)
+__global__ void vprime_kernel(const double* W, int ldm, const int32_t* nbr, int m_v, const double* A, int r0, int r1,
+                              double* Vp) {
+  __shared__ int sN[32];
+  __shared__ double sA[32];
+  for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
+    __syncthreads();
+    if (threadIdx.x < m_v) {
+      sN[threadIdx.x] = nbr[static_cast<size_t>(r) * m_v + threadIdx.x];
+      sA[threadIdx.x] = A[static_cast<size_t>(r) * m_v + threadIdx.x];
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < ldm; j += blockDim.x) {
+      double acc = 0.0;
+      for (int a = 0; a < m_v; ++a) {
+        const int c = sN[a];
+        if (c < 0) break;
+        acc += -sA[a] * W[static_cast<size_t>(c) * ldm + j];
+      }
+      acc += W[static_cast<size_t>(r) * ldm + j];
+      Vp[static_cast<size_t>(r) * ldm + j] = acc;
+    }
+  }
+}
+
+// out(:, i) = in(:, i) * s_i
+__global__ void scale_cols_kernel(const double* in, int ldm, long long ncols, const double* s, bool rsqrt_of,
+                                  double* out) {
+  const long long total = static_cast<long long>(ldm) * ncols;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = e / ldm;
+    const double f = rsqrt_of ? 1.0 / sqrt(s[i]) : s[i];
+    out[e] = in[e] * f;
+  }
+}
+
+__global__ void set_identity_kernel(double* A, int ld, int n) {
+  const long long total = static_cast<long long>(ld) * n;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x)
+    A[e] = (e % ld == e / ld) ? 1.0 : 0.0;
+}
+
+// y = a * x (+ b * z) elementwise helpers
+__global__ void axpby_kernel(int n, double a, const double* x, double b, const double* z, double* y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = a * x[i] + (z ? b * z[i] : 0.0);
+}
+__global__ void div_kernel(int n, const double* x, const double* d, double* y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] = x[i] / d[i];
+}
+
+// (B v)_i = v_i - sum_a A(i, a) v_{N_a}
+__global__ void b_apply_kernel(int r0, int r1, int m_v, const int32_t* nbr, const double* A, const double* v,
+                               double* out) {
+  for (int i = r0 + blockIdx.x * blockDim.x + threadIdx.x; i < r1; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int a = 0; a < m_v; ++a) {
+      const int j = nbr[static_cast<size_t>(i) * m_v + a];
+      if (j < 0) break;
+      s += -A[static_cast<size_t>(i) * m_v + a] * v[j];
+    }
+    out[i] = s + v[i];
+  }
+}
+
+// CSC of B's pattern: column j lists (row r, slot) with N_r[slot] == j, plus (j, -1) for the diagonal.
+__global__ void csc_count_kernel(int n, int m_v, const int32_t* nbr, int32_t* cnt) {
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < static_cast<long long>(n) * m_v;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int j = nbr[e];
+    if (j >= 0) atomicAdd(&cnt[j], 1);
+  }
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) atomicAdd(&cnt[j], 1);
+}
+__global__ void csc_fill_kernel(int n, int m_v, const int32_t* nbr, const int32_t* ptr, int32_t* fillc, int32_t* erow,
+                                int16_t* eslot) {
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+       e < static_cast<long long>(n) * (m_v + 1); e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e / (m_v + 1));
+    const int a = static_cast<int>(e % (m_v + 1));
+    int j;
+    if (a == m_v) {
+      j = r;
+    } else {
+      j = nbr[static_cast<size_t>(r) * m_v + a];
+      if (j < 0) continue;
+    }
+    const int pos = ptr[j] + atomicAdd(&fillc[j], 1);
+    erow[pos] = r;
+    eslot[pos] = static_cast<int16_t>(a == m_v ? -1 : a);
+  }
+}
+// sort each column's entries by row (insertion sort; columns hold ~m_v + 1 entries)
+__global__ void csc_sort_kernel(int n, const int32_t* ptr, int32_t* erow, int16_t* eslot) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int b = ptr[j], e = ptr[j + 1];
+    for (int p = b + 1; p < e; ++p) {
+      const int r = erow[p];
+      const int16_t s = eslot[p];
+      int q = p - 1;
+      while (q >= b && erow[q] > r) {
+        erow[q + 1] = erow[q];
+        eslot[q + 1] = eslot[q];
+        --q;
+      }
+      erow[q + 1] = r;
+      eslot[q + 1] = s;
+    }
+  }
+}
+
+// (B^T v)_j = sum over column j entries of B(r, j) v_r (deterministic, rows ascending)
+__global__ void bt_apply_kernel(int c0, int c1, int m_v, const int32_t* ptr, const int32_t* erow, const int16_t* eslot,
+                                const double* A, const double* v, double* out) {
+  for (int j = c0 + blockIdx.x * blockDim.x + threadIdx.x; j < c1; j += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int p = ptr[j]; p < ptr[j + 1]; ++p) {
+      const int r = erow[p];
+      const int sl = eslot[p];
+      const double b = sl < 0 ? 1.0 : -A[static_cast<size_t>(r) * m_v + sl];
+      s += b * v[r];
+    }
+    out[j] = s;
+  }
+}
+
+// E_r = X_r / D_r - 2 c0_r V'_r + Zr_r and F_r = c0_r V'_r - Zr_r with Zr_r = sum_a Rv_r[a] W_{N_a}
+// (E overwrites X in place: column r of X is read only here).
+__global__ void ef_kernel(int r0, int r1, int ldm, int m_v, const int32_t* nbr, const double* Rv, const double* c0,
+                          const double* D, const double* W, const double* Vp, double* X_E, double* F) {
+  __shared__ int sN[32];
+  __shared__ double sR[32];
+  for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
+    __syncthreads();
+    if (threadIdx.x < m_v) {
+      sN[threadIdx.x] = nbr[static_cast<size_t>(r) * m_v + threadIdx.x];
+      sR[threadIdx.x] = Rv[static_cast<size_t>(r) * m_v + threadIdx.x];
+    }
+    __syncthreads();
+    const double cr = c0[r], inv = 1.0 / D[r];
+    for (int j = threadIdx.x; j < ldm; j += blockDim.x) {
+      double zr = 0.0;
+      for (int a = 0; a < m_v; ++a) {
+        const int c = sN[a];
+        if (c < 0) break;
+        zr = fma(sR[a], W[static_cast<size_t>(c) * ldm + j], zr);
+      }
+      const size_t o = static_cast<size_t>(r) * ldm + j;
+      const double v = Vp[o];
+      X_E[o] = X_E[o] * inv - 2.0 * cr * v + zr;
+      F[o] = cr * v - zr;
+    }
+  }
+}
+
+// omega'(:, b) = -yhat q_b + sum_{(r, a) in col b} ( B(r, b) E_r + Rv_r[a] V'_r )
+__global__ void omega_prime_kernel(int c0, int c1, int ldm, int m_v, const int32_t* ptr, const int32_t* erow,
+                                   const int16_t* eslot, const double* A, const double* Rv, const double* E,
+                                   const double* Vp, const double* yhat, const double* q, double* Om) {
+  __shared__ int sr[64];
+  __shared__ double sb[64], sv[64];
+  for (int b = c0 + blockIdx.x; b < c1; b += gridDim.x) {
+    const int p0 = ptr[b], p1 = ptr[b + 1];
+    const double qb = q[b];
+    for (int j = threadIdx.x; j < ldm; j += blockDim.x) Om[static_cast<size_t>(b) * ldm + j] = -yhat[j] * qb;
+    for (int pb = p0; pb < p1; pb += 64) {
+      __syncthreads();
+      if (threadIdx.x < 64 && pb + static_cast<int>(threadIdx.x) < p1) {
+        const int p = pb + threadIdx.x;
+        const int r = erow[p];
+        const int sl = eslot[p];
+        sr[threadIdx.x] = r;
+        sb[threadIdx.x] = sl < 0 ? 1.0 : -A[static_cast<size_t>(r) * m_v + sl];
+        sv[threadIdx.x] = sl < 0 ? 0.0 : Rv[static_cast<size_t>(r) * m_v + sl];
+      }
+      __syncthreads();
+      const int cnt = min(64, p1 - pb);
+      for (int j = threadIdx.x; j < ldm; j += blockDim.x) {
+        double acc = Om[static_cast<size_t>(b) * ldm + j];
+        for (int e = 0; e < cnt; ++e) {
+          const size_t o = static_cast<size_t>(sr[e]) * ldm + j;
+          acc = fma(sb[e], E[o], acc);
+          acc = fma(sv[e], Vp[o], acc);
+        }
+        Om[static_cast<size_t>(b) * ldm + j] = acc;
+      }
+    }
+  }
+}
+
+// sum_{j, i} Om(j, i) dk(z_j, p_i) over columns [c0, c1): per-block partials (6)
+__global__ void __launch_bounds__(256) upair_grad_kernel(int c0, int c1, int M, int ldm, ZPts z, const double* x,
+                                                         const double* y, const int32_t* tid, DevKernel k, double inv_c,
+                                                         LagTable lt, const double* Om, double* part) {
+  double g[6] = {0, 0, 0, 0, 0, 0};
+  for (int i = c0 + blockIdx.x; i < c1; i += gridDim.x) {
+    const double xi = x[i], yi = y[i];
+    const int ti = tid[i];
+    for (int j = threadIdx.x; j < M; j += blockDim.x) {
+      const TF f = lt.get(z.ztid[j], ti);
+      double kg[6];
+      gneiting_grad_fast(k, inv_c, spatial_dist(z.zx[j], z.zy[j], xi, yi), f, kg);
+      const double wgt = Om[static_cast<size_t>(i) * ldm + j];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) g[q] = fma(wgt, kg[q], g[q]);
+    }
+  }
+  __shared__ double red[6][256];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) red[q][threadIdx.x] = g[q];
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+#pragma unroll
+      for (int q = 0; q < 6; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) part[static_cast<size_t>(blockIdx.x) * 6 + threadIdx.x] = red[threadIdx.x][0];
+}
+
+// Sigma_m pairs: sum_{j1 >= j2} w(j1, j2) dk(z_j1, z_j2), w = wsig(j1,j1) or wsig(j1,j2) + wsig(j2,j1)
+__global__ void __launch_bounds__(256) sigma_pair_grad_kernel(int M, int ldm, ZPts z, DevKernel k, double inv_c,
+                                                              LagTable lt, const double* Ws, double* part) {
+  double g[6] = {0, 0, 0, 0, 0, 0};
+  const long long total = static_cast<long long>(M) * M;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int j1 = static_cast<int>(e / M), j2 = static_cast<int>(e % M);
+    if (j2 > j1) continue;
+    const double wgt = j1 == j2 ? Ws[static_cast<size_t>(j1) * ldm + j1]
+                                : Ws[static_cast<size_t>(j2) * ldm + j1] + Ws[static_cast<size_t>(j1) * ldm + j2];
+    const TF f = lt.get(z.ztid[j1], z.ztid[j2]);
+    double kg[6];
+    gneiting_grad_fast(k, inv_c, spatial_dist(z.zx[j1], z.zy[j1], z.zx[j2], z.zy[j2]), f, kg);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) g[q] = fma(wgt, kg[q], g[q]);
+  }
+  __shared__ double red[6][256];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) red[q][threadIdx.x] = g[q];
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+#pragma unroll
+      for (int q = 0; q < 6; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) part[static_cast<size_t>(blockIdx.x) * 6 + threadIdx.x] = red[threadIdx.x][0];
+}
+
+// M x M helper: C = 0.5 * y y^T + S + 0.5 * (Kinv - I)   (lower+upper)
+__global__ void wsig_assemble_kernel(int M, int ldm, const double* yhat, const double* S, const double* Kinv,
+                                     double* out) {
+  const long long total = static_cast<long long>(ldm) * ldm;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e % ldm), c = static_cast<int>(e / ldm);
+    double v = 0.0;
+    if (r < M && c < M) {
+      // sym(S): S holds V' F^T, both triangles
+      const double s = 0.5 * (S[static_cast<size_t>(c) * ldm + r] + S[static_cast<size_t>(r) * ldm + c]);
+      v = 0.5 * yhat[r] * yhat[c] + s + 0.5 * (Kinv[e] - (r == c ? 1.0 : 0.0));
+    }
+    out[e] = v;
+  }
+}
+
+__global__ void block_sum_kernel(const double* v, long long n, double* part) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    s += v[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void block_sumlog_kernel(const double* v, long long n, double* part) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    s += log(v[i]);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+// deterministic dot product partials
+__global__ void dot_kernel(const double* a, const double* b, long long n, double* part) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    s = fma(a[i], b[i], s);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------------
+double dev_dot(stgp_ctx* ctx, const double* a, const double* b, long long n, Reducer& red) {
+  const int blocks = grid_for(n, kT, 1024);
+  red.ensure(blocks, 1);
+  dot_kernel<<<blocks, kT, 0, ctx->stream>>>(a, b, n, red.part.get());
+  launched(ctx);
+  return red.finish(ctx, blocks, 1)[0];
+}
+
+ZPts zpts(const stgp_structure* s) { return ZPts{s->lr.zx.get(), s->lr.zy.get(), s->lr.ztid.get()}; }
+
+void lowrank_setup(stgp_structure* s, const stgp_inducing* ind) {
+  LowRank& L = s->lr;
+  L.M = ind->M();
+  L.zxyt = ind->xyt;
+  L.ldm = std::max(8, (L.M + 7) / 8 * 8);
+  std::vector<double> zx(L.M), zy(L.M), zt(L.M);
+  for (int j = 0; j < L.M; ++j) {
+    zx[j] = ind->xyt[3 * j];
+    zy[j] = ind->xyt[3 * j + 1];
+    zt[j] = ind->xyt[3 * j + 2];
+    if (!std::isfinite(zx[j]) || !std::isfinite(zy[j]) || !std::isfinite(zt[j]))
+      data_error("SpaceTimePoint: coordinates and time must be finite");
+  }
+  // time groups: data times, then distinct inducing times
+  std::set<double> it(zt.begin(), zt.end());
+  std::vector<double> Ti(it.begin(), it.end());
+  std::vector<int32_t> ztid(L.M);
+  const int nD = static_cast<int>(s->ds->Tdata.size());
+  for (int j = 0; j < L.M; ++j)
+    ztid[j] = nD + static_cast<int>(std::lower_bound(Ti.begin(), Ti.end(), zt[j]) - Ti.begin());
+  s->ti.T = s->ds->Tdata;
+  s->ti.T.insert(s->ti.T.end(), Ti.begin(), Ti.end());
+  s->ti.build();
+  s->ti_dirty = true;
+  cudaStream_t st = s->ds->ctx->stream;
+  L.zx.upload(zx.data(), L.M, st);
+  L.zy.upload(zy.data(), L.M, st);
+  L.zt.upload(zt.data(), L.M, st);
+  L.ztid.upload(ztid.data(), L.M, st);
+}
+
+// Sigma_m Cholesky with the jitter ladder (inducing.cpp:250-261)
+void build_basis(stgp_structure* s) {
+  stgp_ctx* ctx = s->ds->ctx;
+  LowRank& L = s->lr;
+  const DevKernel k = dev_kernel(s->th);
+  const LagTable lt = lag_view(s->lt);
+  const double jitter = 1e-8 * s->th.sigma1_2;
+  L.Lm.ensure(static_cast<size_t>(L.ldm) * L.ldm);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    sigma_m_kernel<<<grid_for(static_cast<long long>(L.ldm) * L.ldm), kT, 0, ctx->stream>>>(
+        zpts(s), L.M, L.ldm, k, lt, jitter, attempt == 0 ? 0.0 : 9.0 * jitter, L.Lm.get());
+    launched(ctx);
+    if (dev_cholesky(ctx, L.Lm.get(), L.ldm, L.ldm)) {
+      L.logdet_m = dev_logdet_chol(ctx, L.Lm.get(), L.ldm, L.M);
+      return;
+    }
+  }
+  numeric_error("InducingBasis: inducing covariance is not positive definite");
+}
+
+// U and W = L_m^{-1} U for columns [c0, c1)
+void build_cross(stgp_structure* s, int c0, int c1, bool keep_U) {
+  stgp_ctx* ctx = s->ds->ctx;
+  LowRank& L = s->lr;
+  const size_t total = static_cast<size_t>(L.ldm) * s->n;
+  L.W.ensure(total);
+  cross_cov_kernel<<<std::max(1, std::min(c1 - c0, ctx->num_sms * 16)), 128, 0, ctx->stream>>>(
+      zpts(s), L.M, L.ldm, s->ds->x.get(), s->ds->y.get(), s->ds->tid.get(), c0, c1, dev_kernel(s->th),
+      lag_view(s->lt), L.W.get());
+  launched(ctx);
+  if (keep_U) {
+    L.U.ensure(total);
+    STGP_CUDA(cudaMemcpyAsync(L.U.get() + static_cast<size_t>(c0) * L.ldm, L.W.get() + static_cast<size_t>(c0) * L.ldm,
+                              sizeof(double) * L.ldm * (c1 - c0), cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  dev_trsm_left(ctx, L.Lm.get(), L.ldm, L.ldm, L.W.get() + static_cast<size_t>(c0) * L.ldm, L.ldm, c1 - c0, false);
+}
+
+void ensure_csc(stgp_structure* s) {
+  if (s->csc_built) return;
+  stgp_ctx* ctx = s->ds->ctx;
+  const int n = s->n, m_v = s->m_v;
+  DevBuf<int32_t> cnt(static_cast<size_t>(n) + 1), fillc(static_cast<size_t>(n));
+  cnt.zero(ctx->stream);
+  fillc.zero(ctx->stream);
+  csc_count_kernel<<<grid_for(static_cast<long long>(n) * m_v), kT, 0, ctx->stream>>>(n, m_v, s->nbr.get(), cnt.get());
+  launched(ctx);
+  s->csc_ptr.ensure(static_cast<size_t>(n) + 1);
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt.get(), s->csc_ptr.get(), n + 1, ctx->stream);
+  DevBuf<unsigned char> tmp(tmp_bytes);
+  cub::DeviceScan::ExclusiveSum(tmp.get(), tmp_bytes, cnt.get(), s->csc_ptr.get(), n + 1, ctx->stream);
+  launched(ctx);
+  int nnz = 0;
+  STGP_CUDA(cudaMemcpyAsync(&nnz, s->csc_ptr.get() + n, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  STGP_CUDA(cudaStreamSynchronize(ctx->stream));
+  s->csc_row.ensure(static_cast<size_t>(nnz));
+  s->csc_slot.ensure(static_cast<size_t>(nnz));
+  csc_fill_kernel<<<grid_for(static_cast<long long>(n) * (m_v + 1)), kT, 0, ctx->stream>>>(
+      n, m_v, s->nbr.get(), s->csc_ptr.get(), fillc.get(), s->csc_row.get(), s->csc_slot.get());
+  launched(ctx);
+  csc_sort_kernel<<<grid_for(n), kT, 0, ctx->stream>>>(n, s->csc_ptr.get(), s->csc_row.get(), s->csc_slot.get());
+  launched(ctx);
+  s->csc_built = true;
+}
+
+void b_apply(stgp_structure* s, const double* v, double* out) {
+  stgp_ctx* ctx = s->ds->ctx;
+  b_apply_kernel<<<grid_for(s->n), kT, 0, ctx->stream>>>(0, s->n, s->m_v, s->nbr.get(), s->A.get(), v, out);
+  launched(ctx);
+}
+void bt_apply(stgp_structure* s, const double* v, double* out) {
+  stgp_ctx* ctx = s->ds->ctx;
+  ensure_csc(s);
+  bt_apply_kernel<<<grid_for(s->n), kT, 0, ctx->stream>>>(0, s->n, s->m_v, s->csc_ptr.get(), s->csc_row.get(),
+                                                          s->csc_slot.get(), s->A.get(), v, out);
+  launched(ctx);
+}
+
+void scale_cols(stgp_ctx* ctx, const double* in, int ldm, long long ncols, const double* sc, bool rsqrt_of, double* out) {
+  scale_cols_kernel<<<grid_for(static_cast<long long>(ldm) * ncols), kT, 0, ctx->stream>>>(in, ldm, ncols, sc, rsqrt_of,
+                                                                                          out);
+  launched(ctx);
+}
+void set_identity(stgp_ctx* ctx, double* A, int ld) {
+  set_identity_kernel<<<grid_for(static_cast<long long>(ld) * ld), kT, 0, ctx->stream>>>(A, ld, ld);
+  launched(ctx);
+}
+void div_vec(stgp_ctx* ctx, int n, const double* x, const double* d, double* y) {
+  div_kernel<<<grid_for(n), kT, 0, ctx->stream>>>(n, x, d, y);
+  launched(ctx);
+}
+double dev_sum(stgp_ctx* ctx, const double* v, long long n, Reducer& red) {
+  const int blocks = grid_for(n, kT, 1024);
+  red.ensure(blocks, 1);
+  block_sum_kernel<<<blocks, kT, 0, ctx->stream>>>(v, n, red.part.get());
+  launched(ctx);
+  return red.finish(ctx, blocks, 1)[0];
+}
+double dev_sum_log(stgp_ctx* ctx, const double* v, long long n, Reducer& red) {
+  const int blocks = grid_for(n, kT, 1024);
+  red.ensure(blocks, 1);
+  block_sumlog_kernel<<<blocks, kT, 0, ctx->stream>>>(v, n, red.part.get());
+  launched(ctx);
+  return red.finish(ctx, blocks, 1)[0];
+}
+void transform_wsig(stgp_ctx* ctx, const double* Lm, int ldm, double* Ws) {
+  dev_trsm_left(ctx, Lm, ldm, ldm, Ws, ldm, ldm, true);
+  const double one = 1.0;
+  cublas_check(cublasDtrsm(ctx->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, ldm,
+                           ldm, &one, Lm, ldm, Ws, ldm),
+               "trsm(wsig)");
+}
+std::vector<double> upair_grad(stgp_structure* s, const double* Om) {
+  stgp_ctx* ctx = s->ds->ctx;
+  const int ub = std::max(1, std::min(s->n, ctx->num_sms * 8));
+  Reducer r;
+  r.ensure(ub, 6);
+  upair_grad_kernel<<<ub, 256, 0, ctx->stream>>>(0, s->n, s->lr.M, s->lr.ldm, zpts(s), s->ds->x.get(), s->ds->y.get(),
+                                                 s->ds->tid.get(), dev_kernel(s->th), 1.0 / s->th.c, lag_view(s->lt), Om,
+                                                 r.part.get());
+  launched(ctx);
+  return r.finish(ctx, ub, 6);
+}
+std::vector<double> sigma_pair_grad(stgp_structure* s, const double* Ws) {
+  stgp_ctx* ctx = s->ds->ctx;
+  const int M = s->lr.M;
+  const int sb = grid_for(static_cast<long long>(M) * M, 256, 1024);
+  Reducer r;
+  r.ensure(sb, 6);
+  sigma_pair_grad_kernel<<<sb, 256, 0, ctx->stream>>>(M, s->lr.ldm, zpts(s), dev_kernel(s->th), 1.0 / s->th.c,
+                                                      lag_view(s->lt), Ws, r.part.get());
+  launched(ctx);
+  return r.finish(ctx, sb, 6);
+}
+
+// ---------------------------------------------------------------------------
+// builds
+// ---------------------------------------------------------------------------
+void vif_build(stgp_structure* s) {
+  stgp_ctx* ctx = s->ds->ctx;
+  LowRank& L = s->lr;
+  prepare_tables(s);
+  const double nug = s->policy == STGP_OBSERVATION ? s->th.sigma2 : 0.0;
+  if (L.M == 0) {
+    run_rows(s, kModeBuild, nullptr, 0, nug);
+    s->built = true;
+    return;
+  }
+  build_basis(s);
+  build_cross(s, 0, s->n, false);
+  run_rows(s, kModeBuild, L.W.get(), L.ldm, nug);
+  // V' = W B^T and K = I + V' D^{-1} V'^T
+  const size_t total = static_cast<size_t>(L.ldm) * s->n;
+  L.Vp.ensure(total);
+  vprime_kernel<<<std::min(s->n, ctx->num_sms * 16), 128, 0, ctx->stream>>>(L.W.get(), L.ldm, s->nbr.get(), s->m_v,
+                                                                           s->A.get(), 0, s->n, L.Vp.get());
+  launched(ctx);
+  L.work1.ensure(total);
+  scale_cols_kernel<<<grid_for(static_cast<long long>(total)), kT, 0, ctx->stream>>>(L.Vp.get(), L.ldm, s->n, s->D.get(),
+                                                                                     true, L.work1.get());
+  launched(ctx);
+  L.Mc.ensure(static_cast<size_t>(L.ldm) * L.ldm);
+  set_identity_kernel<<<grid_for(static_cast<long long>(L.ldm) * L.ldm), kT, 0, ctx->stream>>>(L.Mc.get(), L.ldm,
+                                                                                               L.ldm);
+  launched(ctx);
+  dev_syrk(ctx, L.ldm, s->n, 1.0, L.work1.get(), L.ldm, 1.0, L.Mc.get(), L.ldm);
+  if (!dev_cholesky(ctx, L.Mc.get(), L.ldm, L.ldm)) numeric_error("build_vif: Woodbury core factorization failed");
+  L.logdet_M = dev_logdet_chol(ctx, L.Mc.get(), L.ldm, L.ldm);  // = log|M_core| - log|Sigma_m|
+  s->built = true;
+}
+
+// ---------------------------------------------------------------------------
+// NLL (approximations.cpp:352-384)
+// ---------------------------------------------------------------------------
+static double vif_nll_given_u(stgp_structure* s, double rows_sum) {
+  stgp_ctx* ctx = s->ds->ctx;
+  LowRank& L = s->lr;
+  double quad_lr = 0.0, logdet_lr = 0.0;
+  if (L.M > 0) {
+    // W ur = V' D^{-1} u;  quad -= (W ur)' K^{-1} (W ur)
+    s->u.ensure(s->n);
+    L.vecN.ensure(s->n);
+    div_kernel<<<grid_for(s->n), kT, 0, ctx->stream>>>(s->n, s->u.get(), s->D.get(), L.vecN.get());
+    launched(ctx);
+    L.vecM.ensure(L.ldm);
+    L.vecM2.ensure(L.ldm);
+    dev_gemv(ctx, false, L.ldm, s->n, 1.0, L.Vp.get(), L.ldm, L.vecN.get(), 0.0, L.vecM.get());
+    STGP_CUDA(cudaMemcpyAsync(L.vecM2.get(), L.vecM.get(), sizeof(double) * L.ldm, cudaMemcpyDeviceToDevice, ctx->stream));
+    dev_trsm_left(ctx, L.Mc.get(), L.ldm, L.ldm, L.vecM2.get(), L.ldm, 1, false);  // L_K^{-1} (W ur)
+    quad_lr = dev_dot(ctx, L.vecM2.get(), L.vecM2.get(), L.ldm, s->red);
+    logdet_lr = L.logdet_M;
+  }
+  return 0.5 * (rows_sum - quad_lr + logdet_lr + nll_const(s->n));
+}
+
+double lowrank_nll(stgp_structure* s) {
+  stgp_ctx* ctx = s->ds->ctx;
+  if (s->kind == STGP_FITC) return fitc_nll(s);
+  if (s->policy != STGP_OBSERVATION)
+    config_error("nll: latent-policy likelihood goes through the Laplace algebra (out of scope, SURVEY.md §8(f) f3)");
+  const int blocks = std::max(1, std::min(ceil_div(s->n, 256), ctx->num_sms * 4));
+  s->red.ensure(blocks, 1);
+  s->u.ensure(s->n);
+  launch_nll_stored(s, blocks, s->u.get());
+  const double rows_sum = s->red.finish(ctx, blocks, 1)[0];
+  return vif_nll_given_u(s, rows_sum);
+}
+
+// ---------------------------------------------------------------------------
+// VIF gradient (approximations.cpp:573-744), whitened (file header)
+// ---------------------------------------------------------------------------
+static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
+  if (s->policy != STGP_OBSERVATION)
+    numeric_error("nll_grad: analytic gradient is defined for the observation-policy structure driven by the optimizer");
+  stgp_ctx* ctx = s->ds->ctx;
+  LowRank& L = s->lr;
+  const int n = s->n, M = L.M, ldm = L.ldm;
+  if (M == 0) {  // plain Vecchia gradient on the residual structure
+    std::vector<double> tot = run_rows(s, kModeGrad, nullptr, 0, s->th.sigma2);
+    if (nll_out) *nll_out = 0.5 * (tot[0] + nll_const(n));
+    for (int q = 0; q < 7; ++q) grad[q] = tot[1 + q];
+    return;
+  }
+  const size_t total = static_cast<size_t>(ldm) * n;
+  cudaStream_t st = ctx->stream;
+  // u = B r, NLL rows part
+  const int nb = std::max(1, std::min(ceil_div(n, 256), ctx->num_sms * 4));
+  s->red.ensure(nb, 1);
+  s->u.ensure(n);
+  launch_nll_stored(s, nb, s->u.get());
+  const double rows_sum = s->red.finish(ctx, nb, 1)[0];
+  if (nll_out) *nll_out = vif_nll_given_u(s, rows_sum);
+  // g1 = D^{-1} u, ur = B^T g1, W ur = V' g1, yhat = K^{-1} W ur, t = W^T yhat
+  DevBuf<double> g1(n), ur(n), t(n), z(n), Bz(n), q(n), tmp(n), c0(n), Rv(static_cast<size_t>(n) * s->m_v);
+  div_kernel<<<grid_for(n), kT, 0, st>>>(n, s->u.get(), s->D.get(), g1.get());
+  launched(ctx);
+  bt_apply(s, g1.get(), ur.get());
+  DevBuf<double> yhat(ldm);
+  dev_gemv(ctx, false, ldm, n, 1.0, L.Vp.get(), ldm, g1.get(), 0.0, yhat.get());
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, yhat.get(), ldm, 1, false);
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, yhat.get(), ldm, 1, true);
+  dev_gemv(ctx, true, ldm, n, 1.0, L.W.get(), ldm, yhat.get(), 0.0, t.get());
+  axpby_kernel<<<grid_for(n), kT, 0, st>>>(n, 1.0, s->r.get(), -1.0, t.get(), z.get());
+  launched(ctx);
+  b_apply(s, z.get(), Bz.get());
+  // X = K^{-1} V'
+  L.work1.ensure(total);
+  STGP_CUDA(cudaMemcpyAsync(L.work1.get(), L.Vp.get(), sizeof(double) * total, cudaMemcpyDeviceToDevice, st));
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.work1.get(), ldm, n, false);
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.work1.get(), ldm, n, true);
+  // per-row Phi_i: direct pass + c0, Rv
+  RowArgs a = row_args(s, L.W.get(), ldm, s->th.sigma2);
+  a.X = L.work1.get();
+  a.Vp = L.Vp.get();
+  a.z = z.get();
+  a.Bz = Bz.get();
+  a.D_in = s->D.get();
+  a.c0_out = c0.get();
+  a.Rv_out = Rv.get();
+  a.A_out = nullptr;
+  a.D_out = nullptr;
+  std::vector<double> rows = run_rows_args(s, kModeVifGrad, a);
+  for (int qd = 0; qd < 7; ++qd) grad[qd] = rows[1 + qd];
+  // E (in place of X) and F
+  L.work2.ensure(total);
+  ef_kernel<<<std::min(n, ctx->num_sms * 16), 128, 0, st>>>(0, n, ldm, s->m_v, s->nbr.get(), Rv.get(), c0.get(),
+                                                           s->D.get(), L.W.get(), L.Vp.get(), L.work1.get(),
+                                                           L.work2.get());
+  launched(ctx);
+  // WPhiW^T = sym(V' F^T)  -> wsig' = 0.5 yhat yhat^T + sym(V'F^T) + 0.5 (K^{-1} - I)
+  DevBuf<double> S(static_cast<size_t>(ldm) * ldm), Kinv(static_cast<size_t>(ldm) * ldm), Ws(static_cast<size_t>(ldm) * ldm);
+  dev_gemm(ctx, false, true, ldm, ldm, n, 1.0, L.Vp.get(), ldm, L.work2.get(), ldm, 0.0, S.get(), ldm);
+  set_identity_kernel<<<grid_for(static_cast<long long>(ldm) * ldm), kT, 0, st>>>(Kinv.get(), ldm, ldm);
+  launched(ctx);
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, Kinv.get(), ldm, ldm, false);
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, Kinv.get(), ldm, ldm, true);
+  wsig_assemble_kernel<<<grid_for(static_cast<long long>(ldm) * ldm), kT, 0, st>>>(M, ldm, yhat.get(), S.get(), Kinv.get(),
+                                                                                    Ws.get());
+  launched(ctx);
+  // wsig = L_m^{-T} wsig' L_m^{-1}
+  transform_wsig(ctx, L.Lm.get(), ldm, Ws.get());
+  // q = ur - Q t
+  b_apply(s, t.get(), tmp.get());
+  div_kernel<<<grid_for(n), kT, 0, st>>>(n, tmp.get(), s->D.get(), tmp.get());
+  launched(ctx);
+  bt_apply(s, tmp.get(), q.get());
+  axpby_kernel<<<grid_for(n), kT, 0, st>>>(n, 1.0, ur.get(), -1.0, q.get(), q.get());
+  launched(ctx);
+  // omega' then omega = L_m^{-T} omega' (reuse the W-sized buffer F after the GEMM)
+  ensure_csc(s);
+  omega_prime_kernel<<<std::min(n, ctx->num_sms * 16), 128, 0, st>>>(0, n, ldm, s->m_v, s->csc_ptr.get(), s->csc_row.get(),
+                                                                     s->csc_slot.get(), s->A.get(), Rv.get(),
+                                                                     L.work1.get(), L.Vp.get(), yhat.get(), q.get(),
+                                                                     L.work2.get());
+  launched(ctx);
+  dev_trsm_left(ctx, L.Lm.get(), ldm, ldm, L.work2.get(), ldm, n, true);
+  // U-pair and Sigma_m-pair kernel gradients
+  std::vector<double> gu = upair_grad(s, L.work2.get());
+  std::vector<double> gs = sigma_pair_grad(s, Ws.get());
+  for (int qd = 0; qd < 6; ++qd) grad[1 + qd] += gu[qd] + gs[qd];
+}
+
+void lowrank_nll_grad(stgp_structure* s, double* nll, double* grad) {
+  if (s->kind == STGP_FITC) {
+    fitc_nll_grad(s, nll, grad);
+    return;
+  }
+  vif_grad(s, nll, grad);
+}
+
 }  // namespace stgp
 
 extern "C" {
-int stgp_residual_neighbors(stgp_dataset*, const stgp_params*, const stgp_inducing*, int, stgp_neighbors**) {
-  stgp::g_last_error = "residual_neighbors: not built yet";
-  return STGP_ERR_CONFIG;
-}
 int stgp_inducing_create(stgp_ctx* ctx, int M, const double* xyt, stgp_inducing** out) {
+  if (!ctx || !out || M < 0 || (M > 0 && !xyt)) {
+    stgp::g_last_error = "stgp_inducing_create: bad argument";
+    return STGP_ERR_CONFIG;
+  }
+  for (int i = 0; i < 3 * M; ++i)
+    if (!std::isfinite(xyt[i])) {
+      stgp::g_last_error = "SpaceTimePoint: coordinates and time must be finite";
+      return STGP_ERR_DATA;
+    }
   auto* ind = new stgp_inducing();
   ind->ctx = ctx;
   ind->xyt.assign(xyt, xyt + 3 * static_cast<size_t>(M));
   *out = ind;
   return STGP_OK;
 }
-int stgp_sts_kmeanspp(stgp_dataset*, int, uint64_t, stgp_inducing**) {
-  stgp::g_last_error = "sts_kmeanspp: not built yet";
-  return STGP_ERR_CONFIG;
-}
-int stgp_joint_kmeanspp_inducing(stgp_dataset*, int, double, double, uint64_t, stgp_inducing**) {
-  stgp::g_last_error = "joint_kmeanspp: not built yet";
-  return STGP_ERR_CONFIG;
-}
-int stgp_kmeanspp(stgp_ctx*, const double*, int, int, int, uint64_t, double*) {
-  stgp::g_last_error = "kmeanspp: not built yet";
-  return STGP_ERR_CONFIG;
-}
 int stgp_inducing_size(const stgp_inducing* ind, int* M, int* m_s, int* m_t) {
+  if (!ind) return STGP_ERR_CONFIG;
   if (M) *M = ind->M();
   if (m_s) *m_s = ind->m_s;
   if (m_t) *m_t = ind->m_t;
   return STGP_OK;
 }
 int stgp_inducing_download(const stgp_inducing* ind, double* xyt) {
+  if (!ind) return STGP_ERR_CONFIG;
   std::copy(ind->xyt.begin(), ind->xyt.end(), xyt);
   return STGP_OK;
 }

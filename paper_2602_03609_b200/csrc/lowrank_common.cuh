@@ -1,0 +1,37 @@
+// Host helpers shared by the low-rank translation units (lowrank.cu, fitc.cu, predict.cu).
+#pragma once
+#include <vector>
+
+#include "structure.hpp"
+
+namespace stgp {
+
+constexpr int kLrThreads = 256;
+inline int grid_for(long long work, int per = kLrThreads, int cap = 148 * 32) {
+  return static_cast<int>(std::max<long long>(1, std::min<long long>((work + per - 1) / per, cap)));
+}
+inline void launched(stgp_ctx* ctx) {
+  ++ctx->launches;
+  STGP_LAUNCH_CHECK();
+}
+
+void build_basis(stgp_structure* s);                               // Sigma_m Cholesky + jitter ladder
+void build_cross(stgp_structure* s, int c0, int c1, bool keep_U);  // U, W = L_m^{-1} U
+void ensure_csc(stgp_structure* s);
+void b_apply(stgp_structure* s, const double* v, double* out);     // B v
+void bt_apply(stgp_structure* s, const double* v, double* out);    // B^T v
+void scale_cols(stgp_ctx* ctx, const double* in, int ldm, long long ncols, const double* s, bool rsqrt_of, double* out);
+void set_identity(stgp_ctx* ctx, double* A, int ld);
+void div_vec(stgp_ctx* ctx, int n, const double* x, const double* d, double* y);
+double dev_dot(stgp_ctx* ctx, const double* a, const double* b, long long n, Reducer& red);
+double dev_sum(stgp_ctx* ctx, const double* v, long long n, Reducer& red);
+double dev_sum_log(stgp_ctx* ctx, const double* v, long long n, Reducer& red);
+// wsig = L_m^{-T} wsig' L_m^{-1} in place
+void transform_wsig(stgp_ctx* ctx, const double* Lm, int ldm, double* Ws);
+// sum_{j,i} Om(j,i) dk(z_j, p_i) and the Sigma_m-pair sum (6 components each)
+std::vector<double> upair_grad(stgp_structure* s, const double* Om);
+std::vector<double> sigma_pair_grad(stgp_structure* s, const double* Ws);
+double fitc_nll(stgp_structure* s);
+void fitc_nll_grad(stgp_structure* s, double* nll, double* grad);
+
+}  // namespace stgp

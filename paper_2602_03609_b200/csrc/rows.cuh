@@ -72,9 +72,18 @@ struct RowArgs {
   int* fail_row;    // min failing row index (init INT_MAX)
   double g00[6];    // kernel gradient at (h, u) = (0, 0)
   double inv_c;     // 1 / c
+  // VIF gradient mode (approximations.cpp:616-661): X = K^{-1} V' (ldw x n),
+  // Vp = V' = W B^T, z = r - t, Bz = B z, D from the build; outputs c0, Rv.
+  const double* X;
+  const double* Vp;
+  const double* z;
+  const double* Bz;
+  const double* D_in;
+  double* c0_out;  // n
+  double* Rv_out;  // n * m_v
 };
 
-enum RowMode { kModeBuild = 0, kModeNll = 1, kModeGrad = 2 };
+enum RowMode { kModeBuild = 0, kModeNll = 1, kModeGrad = 2, kModeVifGrad = 3 };
 
 __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -158,17 +167,32 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
     if (lane < a.m_v) nb = __ldg(&a.nbr[static_cast<size_t>(i) * a.m_v + lane]);
     const int k = __popc(__ballot_sync(kFull, nb >= 0));  // neighbours packed at the front
     const int pt = lane < k ? nb : (lane == KS ? i : -1);
-    double rp = 0.0;
+    double rp = 0.0, zp = 0.0;
     if (pt >= 0) {
       sx[w][lane] = __ldg(&a.x[pt]);
       sy[w][lane] = __ldg(&a.y[pt]);
       st[w][lane] = __ldg(&a.tid[pt]);
       if (MODE != kModeBuild) rp = __ldg(&a.r[pt]);
+      if (MODE == kModeVifGrad) zp = __ldg(&a.z[pt]);
     }
     scol[w][lane] = pt;
     __syncwarp();
     if (HAS_W) closure_gram_dmma<LD>(a.W, a.ldw, scol[w], C, lane);  // Gram staged in C
     __syncwarp();
+    // VIF gradient: Ga[s] = W_{cl_s} . X_i (= U_{cl_s} . Hhat_i), aGa = V'_i . X_i
+    double Ga = 0.0, aGa = 0.0;
+    if (MODE == kModeVifGrad) {
+      const double* xi = a.X + static_cast<size_t>(i) * a.ldw;
+      if (pt >= 0) {
+        const double* wc = a.W + static_cast<size_t>(pt) * a.ldw;
+#pragma unroll 4
+        for (int j = 0; j < a.ldw; ++j) Ga = fma(__ldg(&wc[j]), __ldg(&xi[j]), Ga);
+      }
+      const double* vi = a.Vp + static_cast<size_t>(i) * a.ldw;
+      for (int j = lane; j < a.ldw; j += 32) aGa = fma(__ldg(&vi[j]), __ldg(&xi[j]), aGa);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) aGa += __shfl_xor_sync(kFull, aGa, o);
+    }
     // ---- phase A: covariances over the closure (compact slot k maps to KS) ----
     const int P = (k + 1) * k / 2;
     for (int p = lane; p < P; p += 32) {
@@ -236,43 +260,52 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
       if (c <= lane) C[lane * LD + c] = R[c];
     __syncwarp();
     // ---- solves: b1 = C^{-1} c (A), b2 = C^{-1} r_N (gradient) ----
-    double b1 = cval, b2 = (MODE == kModeGrad && lane < k) ? rp : 0.0;
+    constexpr bool TWO = (MODE == kModeGrad || MODE == kModeVifGrad);
+    double Dst = 0.0, uz = 0.0;
+    if (MODE == kModeVifGrad) {
+      Dst = __ldg(&a.D_in[i]);
+      uz = __ldg(&a.Bz[i]);
+    }
+    double b1 = cval;
+    double b2 = 0.0;
+    if (MODE == kModeGrad && lane < k) b2 = rp;
+    if (MODE == kModeVifGrad && lane < k) b2 = (Ga + uz * zp) / Dst;  // vrow_N
 #pragma unroll
     for (int j = 0; j < KS; ++j) {
       if (lane == j) {
         b1 *= dinv;
-        if (MODE == kModeGrad) b2 *= dinv;
+        if (TWO) b2 *= dinv;
       }
       const double y1 = __shfl_sync(kFull, b1, j);
-      const double y2 = MODE == kModeGrad ? __shfl_sync(kFull, b2, j) : 0.0;
+      const double y2 = TWO ? __shfl_sync(kFull, b2, j) : 0.0;
       if (lane > j) {
         b1 = fma(-R[j], y1, b1);
-        if (MODE == kModeGrad) b2 = fma(-R[j], y2, b2);
+        if (TWO) b2 = fma(-R[j], y2, b2);
       }
     }
 #pragma unroll
     for (int j = KS - 1; j >= 0; --j) {
       if (lane == j) {
         b1 *= dinv;
-        if (MODE == kModeGrad) b2 *= dinv;
+        if (TWO) b2 *= dinv;
       }
       const double x1 = __shfl_sync(kFull, b1, j);
-      const double x2 = MODE == kModeGrad ? __shfl_sync(kFull, b2, j) : 0.0;
+      const double x2 = TWO ? __shfl_sync(kFull, b2, j) : 0.0;
       if (lane < j) {
         const double ljl = C[j * LD + lane];
         b1 = fma(-ljl, x1, b1);
-        if (MODE == kModeGrad) b2 = fma(-ljl, x2, b2);
+        if (TWO) b2 = fma(-ljl, x2, b2);
       }
     }
     const double Aval = lane < k ? b1 : 0.0;
-    const double wval = (MODE == kModeGrad && lane < k) ? b2 : 0.0;
+    const double wval = (TWO && lane < k) ? b2 : 0.0;  // C^{-1} r_N (Vecchia) or Rv (VIF)
     // ---- phase C: D, u ----
     double ac = Aval * cval, ar = Aval * (lane < k ? rp : 0.0), aa = Aval * Aval, aw = Aval * wval;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       ac += __shfl_xor_sync(kFull, ac, o);
       if (MODE != kModeBuild) ar += __shfl_xor_sync(kFull, ar, o);
-      if (MODE == kModeGrad) {
+      if (TWO) {
         aa += __shfl_xor_sync(kFull, aa, o);
         aw += __shfl_xor_sync(kFull, aw, o);
       }
@@ -289,13 +322,22 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
     const double u = ri - ar;
     if (a.u_out && lane == 0) a.u_out[i] = u;
     if (lane == 0) tot[0] += log(D) + u * u / D;
-    if (MODE != kModeGrad) continue;
+    if (!TWO) continue;
     // ---- phase D: gradient over closure pairs ----
     sAw[w][0][lane] = lane < k ? -Aval : (lane == KS ? 1.0 : 0.0);  // a~
-    sAw[w][1][lane] = wval;                                          // w~ (0 at i)
+    sAw[w][1][lane] = wval;                                          // w~ or Rv (0 at i)
     __syncwarp();
-    const double cd = 0.5 * (1.0 / D - u * u / (D * D));
-    const double cu = u / D;
+    double cd, cu;
+    if (MODE == kModeVifGrad) {
+      // Phi_i = c0 a~a~' - sym(a~ Rv')   (approximations.cpp:646-661)
+      cd = 0.5 * (1.0 / Dst - (aGa + uz * uz) / (Dst * Dst));
+      cu = 1.0;
+      if (lane == 0) a.c0_out[i] = cd;
+      if (lane < a.m_v) a.Rv_out[static_cast<size_t>(i) * a.m_v + lane] = wval;
+    } else {
+      cd = 0.5 * (1.0 / D - u * u / (D * D));
+      cu = u / D;
+    }
     double g[6] = {0, 0, 0, 0, 0, 0};
     for (int p = lane; p < P; p += 32) {
       const int pr = sPair[p];

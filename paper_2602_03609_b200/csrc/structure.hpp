@@ -24,6 +24,7 @@ struct LowRank {
   DevBuf<double> Lm;             // Cholesky of jittered Sigma_m (ldm x ldm, lower)
   double logdet_m = 0.0;
   DevBuf<double> U, W;           // ldm x n : cross covariance, whitened L_m^{-1} U
+  DevBuf<double> Vp;             // VIF: V' = W B^T (ldm x n)
   DevBuf<double> Mc;             // Woodbury core (ldm x ldm), Cholesky in place
   double logdet_M = 0.0;
   DevBuf<double> fitc_diag, lambda;  // FITC
@@ -49,6 +50,10 @@ struct stgp_structure {
   stgp::DevBuf<double> r, ywork, Xwork, betaw, u, scratch;
   stgp::LowRank lr;
   bool built = false;
+  // CSC of B's pattern for deterministic B^T products
+  bool csc_built = false;
+  stgp::DevBuf<int32_t> csc_ptr, csc_row;
+  stgp::DevBuf<int16_t> csc_slot;
 };
 
 namespace stgp {
@@ -59,6 +64,7 @@ void compute_residual(stgp_structure* s, const double* y_host, const double* X_h
                       const double* beta);
 RowArgs row_args(stgp_structure* s, const double* W, int ldw, double nugget);
 std::vector<double> run_rows(stgp_structure* s, int mode, const double* W, int ldw, double nugget);
+std::vector<double> run_rows_args(stgp_structure* s, int mode, RowArgs& a);
 void prepare_tables(stgp_structure* s);
 double nll_const(int n);
 void launch_nll_stored(stgp_structure* s, int blocks, double* u_out);
