@@ -31,6 +31,7 @@ namespace stgp {
 namespace {
 
 constexpr int kT = kLrThreads;
+constexpr int kMaxGatherM = 512;  // neighbour-set width supported by the column gathers
 
 struct ZPts {
   const double *zx, *zy;
@@ -89,13 +90,13 @@ __global__ void cross_cov_kernel(ZPts z, int M, int ldm, const double* x, const 
 // V'(:, r) = (W B^T)(:, r) = W(:, r) - sum_a A(r, a) W(:, N_a)   (approximations.cpp:298-305)
 __global__ void vprime_kernel(const double* W, int ldm, const int32_t* nbr, int m_v, const double* A, int r0, int r1,
                               double* Vp) {
-  __shared__ int sN[32];
-  __shared__ double sA[32];
+  __shared__ int sN[kMaxGatherM];
+  __shared__ double sA[kMaxGatherM];
   for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
     __syncthreads();
-    if (threadIdx.x < m_v) {
-      sN[threadIdx.x] = nbr[static_cast<size_t>(r) * m_v + threadIdx.x];
-      sA[threadIdx.x] = A[static_cast<size_t>(r) * m_v + threadIdx.x];
+    for (int a = threadIdx.x; a < m_v; a += blockDim.x) {
+      sN[a] = nbr[static_cast<size_t>(r) * m_v + a];
+      sA[a] = A[static_cast<size_t>(r) * m_v + a];
     }
     __syncthreads();
     for (int j = threadIdx.x; j < ldm; j += blockDim.x) {
@@ -218,13 +219,13 @@ __global__ void bt_apply_kernel(int c0, int c1, int m_v, const int32_t* ptr, con
 // (E overwrites X in place: column r of X is read only here).
 __global__ void ef_kernel(int r0, int r1, int ldm, int m_v, const int32_t* nbr, const double* Rv, const double* c0,
                           const double* D, const double* W, const double* Vp, double* X_E, double* F) {
-  __shared__ int sN[32];
-  __shared__ double sR[32];
+  __shared__ int sN[kMaxGatherM];
+  __shared__ double sR[kMaxGatherM];
   for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
     __syncthreads();
-    if (threadIdx.x < m_v) {
-      sN[threadIdx.x] = nbr[static_cast<size_t>(r) * m_v + threadIdx.x];
-      sR[threadIdx.x] = Rv[static_cast<size_t>(r) * m_v + threadIdx.x];
+    for (int a = threadIdx.x; a < m_v; a += blockDim.x) {
+      sN[a] = nbr[static_cast<size_t>(r) * m_v + a];
+      sR[a] = Rv[static_cast<size_t>(r) * m_v + a];
     }
     __syncthreads();
     const double cr = c0[r], inv = 1.0 / D[r];
@@ -417,6 +418,7 @@ double dev_dot(stgp_ctx* ctx, const double* a, const double* b, long long n, Red
 ZPts zpts(const stgp_structure* s) { return ZPts{s->lr.zx.get(), s->lr.zy.get(), s->lr.ztid.get()}; }
 
 void lowrank_setup(stgp_structure* s, const stgp_inducing* ind) {
+  if (s->m_v > kMaxGatherM) config_error("VIF: neighbour sets wider than 512 are not supported");
   LowRank& L = s->lr;
   L.M = ind->M();
   L.zxyt = ind->xyt;
