@@ -1,23 +1,459 @@
-// Residual-correlation (d_r) neighbour search and space-time kMeans++ seeding.
+// Residual-correlation (d_r) neighbour search (neighbors.cpp:51-83, 324-329), bit-exact.
+//
+// d_r(i, j) = sqrt(max(1 - |k(p_i,p_j) - w_i.w_j| / sqrt(r_i r_j), 0)), w_i = L^{-1} k_m(p_i),
+// r_i = sigma1_2 - |w_i|^2, degenerate (r <= 1e-7 sigma1_2) -> 1.  The selection
+// kernel has no lag table (estimation.cpp:200,225).  Every reduction feeding d_r
+// follows the oracle's order (sequential fused multiply-add chains in increasing
+// index), so distances -- and hence index sets -- are bit-identical:
+//   * Sigma_m Cholesky: left-looking, one column per step (single CTA);
+//   * W: forward substitution as a column wavefront (each accumulator receives
+//     its terms in increasing column order, the same sequence as the oracle);
+//   * w_i.w_j: register-tiled Gram whose K loop runs sequentially per element.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <set>
+
 #include "comm.hpp"
+#include "lowrank_common.cuh"
+#include "search.cuh"
 #include "structure.hpp"
 #include "../../include/stgp_b200.h"
 
+namespace stgp {
+
+namespace {
+
+// Sigma_m (live factors) + diagonal jitter, row-major M x M
+__global__ void sel_sigma_kernel(const double* zx, const double* zy, const int32_t* ztid, int M, DevKernel k,
+                                 LagTable lt, double jit1, double jit2, double* A) {
+  const long long total = static_cast<long long>(M) * M;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e / M), c = static_cast<int>(e % M);
+    const int a = r >= c ? r : c, b = r >= c ? c : r;
+    double pe, pb;
+    lt.get2(ztid[a], ztid[b], pe, pb);
+    TF f;
+    f.pow_mE = pe;
+    f.pow_mbh = pb;
+    double v = gneiting_eval(k, spatial_dist(zx[a], zy[a], zx[b], zy[b]), f);
+    if (r == c) {
+      v = __dadd_rn(v, jit1);
+      if (jit2 != 0.0) v = __dadd_rn(v, jit2);
+    }
+    A[e] = v;
+  }
+}
+
+// Left-looking Cholesky in the oracle's order (chol_seq); A row-major in, L row-major out.
+__global__ void __launch_bounds__(1024) chol_seq_kernel(const double* A, int M, double* L, int* fail) {
+  __shared__ double diag;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  for (int j = 0; j < M; ++j) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double* Lj = L + static_cast<size_t>(j) * M;
+      double acc = A[static_cast<size_t>(j) * M + j];
+      for (int k = 0; k < j; ++k) acc = __fma_rn(-Lj[k], Lj[k], acc);
+      if (acc <= 0.0) bad = 1;
+      diag = __dsqrt_rn(acc);
+      L[static_cast<size_t>(j) * M + j] = diag;
+    }
+    __syncthreads();
+    if (bad) break;
+    const double d = diag;
+    const double* Lj = L + static_cast<size_t>(j) * M;
+    for (int r = j + 1 + threadIdx.x; r < M; r += blockDim.x) {
+      const double* Lr = L + static_cast<size_t>(r) * M;
+      double s = A[static_cast<size_t>(r) * M + j];
+      for (int k = 0; k < j; ++k) s = __fma_rn(-Lr[k], Lj[k], s);
+      L[static_cast<size_t>(r) * M + j] = __ddiv_rn(s, d);
+    }
+  }
+  if (threadIdx.x == 0 && bad) *fail = 1;
+}
+
+constexpr int kWB = 64;      // rows per block and columns per CTA
+constexpr int kWKC = 16;     // K chunk of the off-diagonal update
+constexpr int kWthreads = 256;
+constexpr size_t kWsmem = sizeof(double) * (64 * 17 + 16 * 65 + 64 * 65 + 2 * 64 + 2 * 64) + sizeof(int) * 64;
+
+// W(:, i) = L^{-1} k_m(p_i) for 64 columns per CTA.  Row blocks of 64: the
+// off-diagonal part is a register-tiled update whose K loop runs in increasing
+// c, the diagonal block is a column wavefront, so every accumulator receives
+// -L[r][c] w_c for c = 0, 1, ... in order -- the oracle's fwd_seq sequence.
+__global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx, const double* zy, const int32_t* ztid,
+                                                              int M, int ldm, const double* x, const double* y,
+                                                              const int32_t* tid, int n, DevKernel k, LagTable lt,
+                                                              const double* L, double* W) {
+  extern __shared__ double sm[];
+  double* sL = sm;               // [64][17]
+  double* sWt = sL + 64 * 17;    // [16][65]
+  double* sD = sWt + 16 * 65;    // [64][65]
+  double* wrow = sD + 64 * 65;   // [2][64]
+  double* sx = wrow + 2 * 64;    // [64]
+  double* sy = sx + 64;          // [64]
+  int* st = reinterpret_cast<int*>(sy + 64);
+  const int i0 = blockIdx.x * kWB;
+  const int nc = min(kWB, n - i0);
+  const int t = threadIdx.x;
+  if (t < kWB) {
+    const int i = i0 + (t < nc ? t : 0);
+    sx[t] = x[i];
+    sy[t] = y[i];
+    st[t] = tid[i];
+  }
+  const int tr = (t / 16) * 4, tc = (t % 16) * 4;
+  __syncthreads();
+  for (int r0 = 0; r0 < M; r0 += kWB) {
+    const int rb = min(kWB, M - r0);
+    double acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int r = r0 + tr + u, c = tc + v;
+        double val = 0.0;
+        if (r < M && c < nc) {
+          double pe, pb;
+          lt.get2(ztid[r], st[c], pe, pb);
+          TF f;
+          f.pow_mE = pe;
+          f.pow_mbh = pb;
+          val = gneiting_eval(k, spatial_dist(zx[r], zy[r], sx[c], sy[c]), f);  // k(z_r, p_i)
+        }
+        acc[u][v] = val;
+      }
+    for (int c0 = 0; c0 < r0; c0 += kWKC) {
+      __syncthreads();
+      for (int e = t; e < 64 * kWKC; e += kWthreads) {
+        const int rr = e / kWKC, kk = e % kWKC;
+        sL[rr * 17 + kk] = r0 + rr < M ? L[static_cast<size_t>(r0 + rr) * M + c0 + kk] : 0.0;
+        const int cc = e / kWKC;
+        sWt[kk * 65 + cc] = cc < nc ? W[static_cast<size_t>(i0 + cc) * ldm + c0 + kk] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < kWKC; ++kk) {
+        double lr[4], wv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) lr[u] = -sL[(tr + u) * 17 + kk];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) wv[v] = sWt[kk * 65 + tc + v];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = __fma_rn(lr[u], wv[v], acc[u][v]);
+      }
+    }
+    __syncthreads();
+    for (int e = t; e < 64 * 64; e += kWthreads) {
+      const int rr = e / 64, cc = e % 64;
+      sD[rr * 65 + cc] = (rr < rb && cc <= rr) ? L[static_cast<size_t>(r0 + rr) * M + r0 + cc] : 0.0;
+    }
+    __syncthreads();
+    for (int cl = 0; cl < rb; ++cl) {
+      double* buf = wrow + (cl & 1) * 64;
+      if (cl >= tr && cl < tr + 4) {
+        const double d = sD[cl * 65 + cl];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u == cl - tr)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const double wv = __ddiv_rn(acc[u][v], d);
+              buf[tc + v] = wv;
+              if (tc + v < nc) W[static_cast<size_t>(i0 + tc + v) * ldm + r0 + cl] = wv;
+            }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rr = tr + u;
+        if (rr > cl && rr < rb) {
+          const double l = -sD[rr * 65 + cl];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = __fma_rn(l, buf[tc + v], acc[u][v]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// r_i = sigma1_2 - |w_i|^2 (sequential fma from 0); degenerate flag
+__global__ void resid_kernel(const double* W, int M, int ldm, int n, double s1, double* resid, int* degen) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double* w = W + static_cast<size_t>(i) * ldm;
+    double acc = 0.0;
+    for (int k2 = 0; k2 < M; ++k2) acc = __fma_rn(w[k2], w[k2], acc);
+    const double r = M > 0 ? __dsub_rn(s1, acc) : s1;
+    resid[i] = r;
+    degen[i] = r <= 1e-7 * s1 ? 1 : 0;
+  }
+}
+
+constexpr int kQT = 64;   // queries per CTA
+constexpr int kCT = 64;   // candidates per tile
+constexpr int kKC = 16;   // K chunk
+constexpr int kDrThreads = 256;
+
+struct DrArgs {
+  int n, m_v, M, ldm;
+  const double *x, *y, *W, *resid;
+  const int32_t *tid, *degen;
+  DevKernel k;
+  LagTable lt;
+  int32_t* out;
+  double* dist;
+};
+
+// Tiled exact d_r top-m over predecessors.  CTA = 64 consecutive queries; each
+// 64-candidate tile's Gram W_Q^T W_C is computed with a sequential fma chain per
+// element (4 x 4 register tile per thread), the epilogue forms d_r and the warps
+// merge the tile into per-query top-m lists kept in shared memory.
+constexpr size_t kDrSmem = sizeof(double) * (kQT * (kCT + 1) + kQT * 32) + sizeof(int) * kQT * 32;
+
+__global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
+  extern __shared__ double sm[];
+  // the Gram staging tiles and the distance tile are never live together
+  double (*sWq)[kQT + 1] = reinterpret_cast<double (*)[kQT + 1]>(sm);
+  double (*sWc)[kCT + 1] = reinterpret_cast<double (*)[kCT + 1]>(sm + kKC * (kQT + 1));
+  double (*sd)[kCT + 1] = reinterpret_cast<double (*)[kCT + 1]>(sm);
+  double (*topd)[32] = reinterpret_cast<double (*)[32]>(sm + kQT * (kCT + 1));
+  int (*topj)[32] = reinterpret_cast<int (*)[32]>(sm + kQT * (kCT + 1) + kQT * 32);
+  const int q0 = blockIdx.x * kQT;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int tq = (tid / 16) * 4, tc = (tid % 16) * 4;  // thread tile origin
+  for (int e = tid; e < kQT * 32; e += kDrThreads) {
+    topd[e / 32][e % 32] = __longlong_as_double(0x7ff0000000000000LL);
+    topj[e / 32][e % 32] = INT_MAX;
+  }
+  const int qmax = min(q0 + kQT, a.n);
+  for (int c0 = 0; c0 < qmax - 1; c0 += kCT) {
+    double g[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) g[u][v] = 0.0;
+    for (int k0 = 0; k0 < a.M; k0 += kKC) {
+      __syncthreads();
+      for (int e = tid; e < kKC * kQT; e += kDrThreads) {
+        const int kk = e % kKC, qq = e / kKC;
+        const int i = min(q0 + qq, a.n - 1), j = min(c0 + qq, a.n - 1);
+        const bool in = k0 + kk < a.M;
+        sWq[kk][qq] = in ? a.W[static_cast<size_t>(i) * a.ldm + k0 + kk] : 0.0;
+        sWc[kk][qq] = in ? a.W[static_cast<size_t>(j) * a.ldm + k0 + kk] : 0.0;
+      }
+      __syncthreads();
+      const int kn = min(kKC, a.M - k0);
+      for (int kk = 0; kk < kn; ++kk) {
+        double wq[4], wc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) wq[u] = sWq[kk][tq + u];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) wc[v] = sWc[kk][tc + v];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) g[u][v] = __fma_rn(wq[u], wc[v], g[u][v]);
+      }
+    }
+    // epilogue: d_r for the thread's 4 x 4 pairs (sd aliases the staging tiles)
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int i = q0 + tq + u, j = c0 + tc + v;
+        double d = __longlong_as_double(0x7ff0000000000000LL);
+        if (i < a.n && j < i) {
+          if (a.degen[i] || a.degen[j]) {
+            d = 1.0;
+          } else {
+            double pe, pb;
+            a.lt.get2(a.tid[i], a.tid[j], pe, pb);
+            TF f;
+            f.pow_mE = pe;
+            f.pow_mbh = pb;
+            double rho = gneiting_eval(a.k, spatial_dist(a.x[i], a.y[i], a.x[j], a.y[j]), f);
+            if (a.M > 0) rho = __dsub_rn(rho, g[u][v]);
+            const double rad =
+                __dsub_rn(1.0, __ddiv_rn(fabs(rho), __dsqrt_rn(__dmul_rn(a.resid[i], a.resid[j]))));
+            d = __dsqrt_rn(rad < 0.0 ? 0.0 : rad);
+          }
+        }
+        sd[tq + u][tc + v] = d;
+      }
+    __syncthreads();
+    // merge: warp wid handles queries wid, wid + 8, ...
+    for (int qq = wid; qq < kQT; qq += kDrThreads / 32) {
+      const int i = q0 + qq;
+      if (i >= a.n) break;
+      const int m = min(a.m_v, i);
+      if (m <= 0) continue;
+      TopM e{topd[qq][lane], topj[qq][lane]};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cc = lane + 32 * h;
+        const int j = c0 + cc;
+        const double d = sd[qq][cc];
+        const double wd = __shfl_sync(kFull, e.d, m - 1);
+        const int wj = __shfl_sync(kFull, e.j, m - 1);
+        const unsigned acc = __ballot_sync(kFull, j < i && lex_less(d, j, wd, wj));
+        if (acc) topm_insert(e, m, acc, d, j, lane);
+      }
+      topd[qq][lane] = e.d;
+      topj[qq][lane] = e.j;
+    }
+  }
+  __syncthreads();
+  for (int qq = wid; qq < kQT; qq += kDrThreads / 32) {
+    const int i = q0 + qq;
+    if (i >= a.n) break;
+    const int m = min(a.m_v, i);
+    TopM e{topd[qq][lane], topj[qq][lane]};
+    topm_emit(e, a.m_v, m, lane, a.out + static_cast<size_t>(i) * a.m_v, a.dist ? a.dist + static_cast<size_t>(i) * a.m_v : nullptr);
+  }
+}
+
+}  // namespace
+
+}  // namespace stgp
+
+using namespace stgp;
+
+namespace {
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return STGP_OK;
+  } catch (const stgp::Error& e) {
+    stgp::g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    stgp::g_last_error = e.what();
+    return STGP_ERR_INTERNAL;
+  }
+}
+}  // namespace
+
 extern "C" {
-int stgp_residual_neighbors(stgp_dataset*, const stgp_params*, const stgp_inducing*, int, stgp_neighbors**) {
-  stgp::g_last_error = "residual_neighbors: not built yet";
-  return STGP_ERR_CONFIG;
+
+int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const stgp_inducing* ind, int m_v,
+                            stgp_neighbors** out) {
+  return guarded([&] {
+    if (!ds || !theta || !ind || !out) config_error("stgp_residual_neighbors: null argument");
+    if (m_v < 0) config_error("m_v must be >= 0");
+    if (m_v > 32) config_error("neighbour search supports m_v <= 32 on the device");
+    Params p;
+    std::memcpy(&p, theta, sizeof(p));
+    validate_params(p);
+    stgp_ctx* ctx = ds->ctx;
+    cudaStream_t st = ctx->stream;
+    const int n = ds->n, M = ind->M();
+    const DevKernel k = dev_kernel(p);
+    // time index over data + inducing times, live factors (no lag table in the selection kernel)
+    std::vector<double> zx(M), zy(M), zt(M);
+    for (int j = 0; j < M; ++j) {
+      zx[j] = ind->xyt[3 * j];
+      zy[j] = ind->xyt[3 * j + 1];
+      zt[j] = ind->xyt[3 * j + 2];
+    }
+    std::set<double> it(zt.begin(), zt.end());
+    std::vector<double> Ti(it.begin(), it.end());
+    TimeIndex ti;
+    ti.T = ds->Tdata;
+    ti.T.insert(ti.T.end(), Ti.begin(), Ti.end());
+    ti.build();
+    DevLagTable dl;
+    LagPolicy live;
+    upload_lag_table(dl, ti, p, live, st, true);
+    const LagTable lt = lag_view(dl);
+    std::vector<int32_t> ztid(M);
+    const int nD = static_cast<int>(ds->Tdata.size());
+    for (int j = 0; j < M; ++j)
+      ztid[j] = nD + static_cast<int>(std::lower_bound(Ti.begin(), Ti.end(), zt[j]) - Ti.begin());
+    DevBuf<double> dzx, dzy;
+    DevBuf<int32_t> dzt;
+    dzx.upload(zx.data(), M, st);
+    dzy.upload(zy.data(), M, st);
+    dzt.upload(ztid.data(), M, st);
+    const int ldm = std::max(1, M);
+    DevBuf<double> W(static_cast<size_t>(ldm) * n), resid(n);
+    DevBuf<int32_t> degen(n);
+    {
+      ProfRegion pr(ctx, "dr_whiten");
+      if (M > 0) {
+        // InducingBasis(set, selection kernel): jittered Sigma_m, one retry at 10x (inducing.cpp:250-261)
+        DevBuf<double> A(static_cast<size_t>(M) * M), L(static_cast<size_t>(M) * M);
+        DevBuf<int> fail(1);
+        const double jitter = 1e-8 * p.sigma1_2;
+        bool ok = false;
+        for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+          sel_sigma_kernel<<<grid_for(static_cast<long long>(M) * M), 256, 0, st>>>(
+              dzx.get(), dzy.get(), dzt.get(), M, k, lt, jitter, attempt == 0 ? 0.0 : 9.0 * jitter, A.get());
+          launched(ctx);
+          fail.zero(st);
+          chol_seq_kernel<<<1, 1024, 0, st>>>(A.get(), M, L.get(), fail.get());
+          launched(ctx);
+          int f = 0;
+          fail.download(&f, 1, st);
+          STGP_CUDA(cudaStreamSynchronize(st));
+          ok = f == 0;
+        }
+        if (!ok) numeric_error("InducingBasis: inducing covariance is not positive definite");
+        STGP_CUDA(cudaFuncSetAttribute(whiten_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kWsmem)));
+        whiten_seq_kernel<<<ceil_div(n, kWB), kWthreads, kWsmem, st>>>(dzx.get(), dzy.get(), dzt.get(), M, ldm,
+                                                                      ds->x.get(), ds->y.get(), ds->tid.get(), n, k, lt,
+                                                                      L.get(), W.get());
+        launched(ctx);
+      }
+      resid_kernel<<<grid_for(n), 256, 0, st>>>(W.get(), M, ldm, n, p.sigma1_2, resid.get(), degen.get());
+      launched(ctx);
+    }
+    auto nb = std::make_unique<stgp_neighbors>();
+    nb->ctx = ctx;
+    nb->n = n;
+    nb->m_v = std::max(m_v, 1);
+    nb->kind = STGP_METRIC_DR;
+    const size_t total = static_cast<size_t>(n) * nb->m_v;
+    nb->idx.alloc(total);
+    nb->dist.alloc(total);
+    nb->has_dist = true;
+    if (m_v == 0) {
+      std::vector<int32_t> neg(total, -1);
+      nb->idx.upload(neg.data(), total, st);
+    } else {
+      DrArgs a{};
+      a.n = n;
+      a.m_v = m_v;
+      a.M = M;
+      a.ldm = ldm;
+      a.x = ds->x.get();
+      a.y = ds->y.get();
+      a.W = W.get();
+      a.resid = resid.get();
+      a.tid = ds->tid.get();
+      a.degen = degen.get();
+      a.k = k;
+      a.lt = lt;
+      a.out = nb->idx.get();
+      a.dist = nb->dist.get();
+      ProfRegion pr(ctx, "knn_dr");
+      STGP_CUDA(cudaFuncSetAttribute(knn_dr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kDrSmem)));
+      knn_dr_kernel<<<ceil_div(n, kQT), kDrThreads, kDrSmem, st>>>(a);
+      launched(ctx);
+    }
+    STGP_CUDA(cudaStreamSynchronize(st));
+    prof_collect(ctx);
+    *out = nb.release();
+  });
 }
-int stgp_sts_kmeanspp(stgp_dataset*, int, uint64_t, stgp_inducing**) {
-  stgp::g_last_error = "sts_kmeanspp: not built yet";
-  return STGP_ERR_CONFIG;
-}
-int stgp_joint_kmeanspp_inducing(stgp_dataset*, int, double, double, uint64_t, stgp_inducing**) {
-  stgp::g_last_error = "joint_kmeanspp: not built yet";
-  return STGP_ERR_CONFIG;
-}
-int stgp_kmeanspp(stgp_ctx*, const double*, int, int, int, uint64_t, double*) {
-  stgp::g_last_error = "kmeanspp: not built yet";
-  return STGP_ERR_CONFIG;
-}
-}
+
+}  // extern "C"

@@ -1,0 +1,113 @@
+"""GPU parity for the selection path: kMeans++ / sts / joint seeding and the
+residual-correlation (d_r) neighbour search, bit-exact against the oracle
+(test_inducing.cpp, test_neighbors.cpp:111-131, 222-238)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+SEC4 = (0.01, 1.0, 0.5, 20.0, 0.4, 1.5, 0.4, 0.2)
+
+
+@pytest.fixture(scope="module")
+def S():
+    import paper_2602_03609_b200 as S
+    return S
+
+
+def _bits(a, b):
+    return (np.asarray(a).view(np.uint64) == np.asarray(b).view(np.uint64)).all()
+
+
+@pytest.mark.parametrize("n,d,k,seed", [(500, 2, 20, 1), (300, 1, 7, 2), (400, 3, 25, 3), (4, 2, 4, 7), (5, 1, 1, 3)])
+def test_kmeanspp_bit_exact(S, n, d, k, seed):
+    rng = np.random.default_rng(seed)
+    P = rng.random((n, d)) if n > 5 else (np.array([[0, 0], [1, 0], [0, 1], [1, 1]], float) if d == 2 else
+                                           np.array([[1.0], [2], [3], [4], [10]]))
+    c = S.kmeanspp(P, k, seed)
+    assert _bits(c, O.kmeanspp(P, k, seed))
+
+
+def test_kmeanspp_errors(S):
+    with pytest.raises(S.DataError):
+        S.kmeanspp(np.array([[1.0], [1], [2], [2]]), 3, 1)
+    with pytest.raises(S.ConfigError):
+        S.kmeanspp(np.array([[1.0], [2]]), 0, 1)
+
+
+def test_sts_counts_and_bits(S):
+    # test_inducing.cpp:101-110: 500 locations x 20 times, m = 500 -> 112 x 4
+    x, y, t, _, _ = O.test_dataset(2, 500, 5, n_times=20)
+    ds = S.SpaceTimeDataset(x, y, t)
+    ind = S.sts_kmeanspp(ds, 500, 1)
+    assert (ind.m_s, ind.m_t, ind.M) == (112, 4, 448)
+    Z, ms, mt = O.sts_kmeanspp(x, y, t, 500, 1)
+    assert _bits(ind.points, Z)
+
+
+def test_sts_cfg3_shape(S):
+    x, y, t, _ = S.synth.station_day(1000, 100, seed=11)
+    perm = O.order_observations(t, 11)
+    x, y, t = x[perm], y[perm], t[perm]
+    ds = S.SpaceTimeDataset(x, y, t)
+    ind = S.sts_kmeanspp(ds, 200, 20260203)
+    assert (ind.m_s, ind.m_t) == (45, 4)
+    Z, _, _ = O.sts_kmeanspp(x, y, t, 200, 20260203)
+    assert _bits(ind.points, Z)
+
+
+def test_joint_kmeanspp_bits(S):
+    x, y, t, _, _ = O.test_dataset(2, 60, 23, n_times=6)
+    ds = S.SpaceTimeDataset(x, y, t)
+    ind = S.joint_kmeanspp_inducing(ds, 25, 0.5, 2.0, 5)
+    assert ind.M == 25
+    assert _bits(ind.points, O.joint_kmeanspp(x, y, t, 25, 0.5, 2.0, 5))
+    with pytest.raises(S.ConfigError):
+        S.joint_kmeanspp_inducing(ds, 25, 0.0, 2.0, 5)
+
+
+def _check_dr(S, x, y, t, th, Z, m):
+    ds = S.SpaceTimeDataset(x, y, t)
+    nb = S.residual_neighbors(ds, th, S.InducingSet.from_points(Z), m)
+    idx, dist = nb.indices(), nb.distances()
+    ref, rdist = O.dr_neighbors(x, y, t, th, Z, m, with_dist=True)
+    assert (idx == ref).all(), np.argwhere(idx != ref)[:5]
+    ok = ~np.isnan(rdist)
+    assert _bits(dist[ok], rdist[ok])
+
+
+def test_dr_reference_case(S):
+    # test_neighbors.cpp:111-131: n = 600, m = 20, 25 random inducing points
+    x, y, t, _, _ = O.test_dataset(0, 600, 19)
+    rng = np.random.default_rng(5)
+    Z = np.column_stack([rng.random(25), rng.random(25), 1 + 9 * rng.random(25)])
+    _check_dr(S, x, y, t, SEC4, Z, 20)
+
+
+def test_dr_station_day_sts(S):
+    x, y, t, _ = S.synth.station_day(200, 15, seed=4)
+    perm = O.order_observations(t, 4)
+    x, y, t = x[perm], y[perm], t[perm]
+    Z, _, _ = O.sts_kmeanspp(x, y, t, 100, 9)
+    _check_dr(S, x, y, t, SEC4, Z, 30)
+    _check_dr(S, x, y, t, SEC4, Z[:70], 7)
+
+
+def test_dr_degenerate(S):
+    # test_neighbors.cpp:222-238
+    pts = np.array([[0.5, 0.5, 1.0], [0.2, 0.8, 1.0], [0.9, 0.1, 2.0]])
+    ds = S.SpaceTimeDataset(pts[:, 0], pts[:, 1], pts[:, 2])
+    nb = S.residual_neighbors(ds, SEC4, S.InducingSet.from_points(pts[:1]), 2)
+    d = nb.distances()
+    assert d[1, 0] == 1.0 and d[2, 1] == 1.0 and d[2, 0] < 1.0
+    _check_dr(S, pts[:, 0], pts[:, 1], pts[:, 2], SEC4, pts[:1], 2)
+
+
+def test_dr_empty_inducing_equals_dc(S):
+    x, y, t, _, _ = O.test_dataset(0, 300, 3)
+    ds = S.SpaceTimeDataset(x, y, t)
+    a = S.correlation_neighbors(ds, SEC4, 8).indices()
+    b = S.residual_neighbors(ds, SEC4, S.InducingSet.from_points(np.zeros((0, 3))), 8).indices()
+    assert (a == b).all()
