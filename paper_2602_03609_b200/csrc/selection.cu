@@ -195,6 +195,52 @@ __global__ void resid_kernel(const double* W, int M, int ldm, int n, double s1, 
   }
 }
 
+// Per 64-row tile: time-id range, max |w| and min r over non-degenerate rows, degenerate flag.
+__global__ void tile_stats_kernel(const double* resid, const int32_t* degen, const int32_t* tid, int n, double s1,
+                                  int* tmin, int* tmax, double* wmax, double* rmin, int* hasdeg) {
+  const int tile = blockIdx.x;
+  const int i0 = tile * 64, i1 = min(n, i0 + 64);
+  __shared__ double sw[64], sr[64];
+  __shared__ int smn[64], smx[64], sdg[64];
+  const int t = threadIdx.x;
+  const int i = i0 + t;
+  double w = 0.0, r = __longlong_as_double(0x7ff0000000000000LL);
+  int mn = INT_MAX, mx = -1, dg = 0;
+  if (i < i1) {
+    mn = mx = tid[i];
+    if (degen[i]) {
+      dg = 1;
+    } else {
+      r = resid[i];
+      w = s1 - resid[i];
+    }
+  }
+  sw[t] = w;
+  sr[t] = r;
+  smn[t] = mn;
+  smx[t] = mx;
+  sdg[t] = dg;
+  __syncthreads();
+  for (int o = 32; o > 0; o >>= 1) {
+    if (t < o) {
+      sw[t] = fmax(sw[t], sw[t + o]);
+      sr[t] = fmin(sr[t], sr[t + o]);
+      smn[t] = min(smn[t], smn[t + o]);
+      smx[t] = max(smx[t], smx[t + o]);
+      sdg[t] = sdg[t] | sdg[t + o];
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    // |w|^2 = s1 - r up to one rounding of s1 (bounded by the 1e-11 factor of the prune test)
+    wmax[tile] = sqrt(fmax(sw[0], 0.0) + 1e-15 * s1);
+    rmin[tile] = sr[0];
+    tmin[tile] = smn[0];
+    tmax[tile] = smx[0];
+    hasdeg[tile] = sdg[0];
+  }
+}
+
 constexpr int kQT = 64;   // queries per CTA
 constexpr int kCT = 64;   // candidates per tile
 constexpr int kKC = 16;   // K chunk
@@ -208,6 +254,10 @@ struct DrArgs {
   LagTable lt;
   int32_t* out;
   double* dist;
+  // exact tile pruning
+  const int *tmin, *tmax, *hasdeg;
+  const double *wmax, *rmin;
+  double s1;
 };
 
 // Tiled exact d_r top-m over predecessors.  CTA = 64 consecutive queries; each
@@ -232,7 +282,44 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
     topj[e / 32][e % 32] = INT_MAX;
   }
   const int qmax = min(q0 + kQT, a.n);
-  for (int c0 = 0; c0 < qmax - 1; c0 += kCT) {
+  __shared__ double s_dmax[kDrThreads / 32];
+  __shared__ int s_prune;
+  const int qtile = q0 / kQT;
+  // candidate tiles nearest-first: tight thresholds early, then exact pruning of far tiles
+  for (int c0 = ((qmax - 2) / kCT) * kCT; c0 >= 0; c0 -= kCT) {
+    {
+      // current worst threshold over the tile's queries (inf while any list is short)
+      double dm = 0.0;
+      for (int qq = tid; qq < kQT; qq += kDrThreads) {
+        const int i = q0 + qq;
+        if (i >= a.n) continue;
+        const int m = min(a.m_v, i);
+        if (m > 0) dm = fmax(dm, topd[qq][m - 1]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(kFull, dm, o));
+      if (lane == 0) s_dmax[wid] = dm;
+      __syncthreads();
+      if (tid == 0) {
+        double d = 0.0;
+        for (int w2 = 0; w2 < kDrThreads / 32; ++w2) d = fmax(d, s_dmax[w2]);
+        const int ct = c0 / kCT;
+        int prune = 0;
+        if (a.tmin && d < 1.0 && ct != qtile && !a.hasdeg[qtile]) {
+          // rows are time sorted and C precedes Q, so the smallest lag is T(tmin_Q) - T(tmax_C).
+          // |rho_r| <= |k| + |w_i||w_j| <= s1 T(u_min)^{-(delta+beta)} + wmax_Q wmax_C (non-degenerate
+          // candidates; degenerate ones sit at d = 1 > d).  rmin_C = inf when all are degenerate.
+          double pe, pb;
+          a.lt.get2(a.tmin[qtile], a.tmax[ct], pe, pb);
+          const double cmax =
+              (a.s1 * pe + a.wmax[qtile] * a.wmax[ct]) * (1.0 + 1e-11) / sqrt(a.rmin[qtile] * a.rmin[ct]);
+          if (cmax < 1.0 && (1.0 - cmax) - 1e-12 > d * d) prune = 1;
+        }
+        s_prune = prune;
+      }
+      __syncthreads();
+      if (s_prune) continue;
+    }
     double g[4][4];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
@@ -444,6 +531,20 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
       a.lt = lt;
       a.out = nb->idx.get();
       a.dist = nb->dist.get();
+      const int ntile = ceil_div(n, 64);
+      DevBuf<int> tmn(ntile), tmx(ntile), hdg(ntile);
+      DevBuf<double> wmx(ntile), rmn(ntile);
+      tile_stats_kernel<<<ntile, 64, 0, st>>>(resid.get(), degen.get(), ds->tid.get(), n, p.sigma1_2, tmn.get(),
+                                              tmx.get(), wmx.get(), rmn.get(), hdg.get());
+      launched(ctx);
+      a.tmin = tmn.get();
+      a.tmax = tmx.get();
+      a.wmax = wmx.get();
+      a.rmin = rmn.get();
+      a.hasdeg = hdg.get();
+      a.s1 = p.sigma1_2;
+      // pruning needs time-sorted rows (tile time ranges); otherwise plain brute force
+      if (!ds->time_sorted) a.tmin = nullptr;
       ProfRegion pr(ctx, "knn_dr");
       STGP_CUDA(cudaFuncSetAttribute(knn_dr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kDrSmem)));
