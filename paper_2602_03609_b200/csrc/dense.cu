@@ -78,8 +78,9 @@ __global__ void symmetrize_kernel(double* A, int ld, int n) {
 }  // namespace
 
 bool dev_cholesky(stgp_ctx* ctx, double* A, int ld, int n) {
-  DevBuf<int> flag(1);
-  flag.zero(ctx->stream);
+  DevBuf<int>& flag = ctx->iscr;
+  flag.ensure(1);
+  STGP_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), ctx->stream));
   const double one = 1.0, mone = -1.0;
   for (int j0 = 0; j0 < n; j0 += kNB) {
     const int nb = std::min(kNB, n - j0);
@@ -107,7 +108,8 @@ bool dev_cholesky(stgp_ctx* ctx, double* A, int ld, int n) {
 }
 
 double dev_logdet_chol(stgp_ctx* ctx, const double* L, int ld, int n) {
-  DevBuf<double> out(1);
+  DevBuf<double>& out = ctx->dscr;
+  out.ensure(1);
   logdiag_kernel<<<1, 256, 0, ctx->stream>>>(L, ld, n, out.get());
   ++ctx->launches;
   STGP_LAUNCH_CHECK();
@@ -125,6 +127,34 @@ void dev_trsm_left(stgp_ctx* ctx, const double* L, int ldl, int n, double* B, in
     cublas_check(cublasDtrsm(ctx->cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, transpose ? CUBLAS_OP_T : CUBLAS_OP_N,
                              CUBLAS_DIAG_NON_UNIT, n, nc, &one, L, ldl, B + static_cast<size_t>(c0) * ldb, ldb),
                  "trsm");
+  }
+}
+
+static __global__ void identity_kernel(double* A, int ld, int n) {
+  const long long total = static_cast<long long>(ld) * n;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x)
+    A[e] = (e % ld == e / ld) ? 1.0 : 0.0;
+}
+
+void dev_tri_inverse(stgp_ctx* ctx, const double* L, int ld, int n, double* Linv) {
+  const long long total = static_cast<long long>(ld) * n;
+  identity_kernel<<<static_cast<int>(std::min<long long>((total + 255) / 256, 4096)), 256, 0, ctx->stream>>>(Linv, ld, n);
+  ++ctx->launches;
+  STGP_LAUNCH_CHECK();
+  dev_trsm_left(ctx, L, ld, n, Linv, ld, n, false);
+}
+
+void dev_trmm_left(stgp_ctx* ctx, const double* T, int ldt, int n, const double* B, int ldb, long long ncols,
+                   bool transpose, double* C, int ldc) {
+  const double one = 1.0;
+  const long long chunk = INT_MAX / 2;
+  for (long long c0 = 0; c0 < ncols; c0 += chunk) {
+    const int nc = static_cast<int>(std::min(chunk, ncols - c0));
+    cublas_check(cublasDtrmm(ctx->cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, transpose ? CUBLAS_OP_T : CUBLAS_OP_N,
+                             CUBLAS_DIAG_NON_UNIT, n, nc, &one, T, ldt, B + static_cast<size_t>(c0) * ldb, ldb,
+                             C + static_cast<size_t>(c0) * ldc, ldc),
+                 "trmm");
   }
 }
 

@@ -23,6 +23,11 @@ double dev_logdet_chol(stgp_ctx* ctx, const double* L, int ld, int n);
 // B <- op(L)^{-1} B for lower-triangular L (n x n), B n x ncols (ldb).
 void dev_trsm_left(stgp_ctx* ctx, const double* L, int ldl, int n, double* B, int ldb, long long ncols,
                    bool transpose);
+// Linv = L^{-1} (lower triangular, n x n, zero upper part); out-of-place
+void dev_tri_inverse(stgp_ctx* ctx, const double* L, int ld, int n, double* Linv);
+// C = op(T) B for lower-triangular T (n x n): out-of-place triangular multiply
+void dev_trmm_left(stgp_ctx* ctx, const double* T, int ldt, int n, const double* B, int ldb, long long ncols,
+                   bool transpose, double* C, int ldc);
 // C (n x n, lower) = alpha * A A^T + beta * C, A n x k (lda)
 void dev_syrk(stgp_ctx* ctx, int n, long long k, double alpha, const double* A, int lda, double beta, double* C,
               int ldc);

@@ -61,6 +61,8 @@ struct stgp_ctx {
   ncclComm* comm = nullptr;
   int64_t launches = 0;
   int num_sms = 148;
+  stgp::DevBuf<int> iscr;     // small persistent scratch (flags, scalars)
+  stgp::DevBuf<double> dscr;
   // live per-region kernel timing (stgp_ctx_profile)
   bool prof = false;
   std::map<std::string, std::pair<double, int64_t>> prof_acc;

@@ -463,28 +463,27 @@ void build_basis(stgp_structure* s) {
     launched(ctx);
     if (dev_cholesky(ctx, L.Lm.get(), L.ldm, L.ldm)) {
       L.logdet_m = dev_logdet_chol(ctx, L.Lm.get(), L.ldm, L.M);
+      L.Lminv.ensure(static_cast<size_t>(L.ldm) * L.ldm);
+      dev_tri_inverse(ctx, L.Lm.get(), L.ldm, L.ldm, L.Lminv.get());
       return;
     }
   }
   numeric_error("InducingBasis: inducing covariance is not positive definite");
 }
 
-// U and W = L_m^{-1} U for columns [c0, c1)
-void build_cross(stgp_structure* s, int c0, int c1, bool keep_U) {
+// U (kept) and W = L_m^{-1} U for columns [c0, c1): explicit triangular inverse + TRMM
+void build_cross(stgp_structure* s, int c0, int c1, bool /*keep_U*/) {
   stgp_ctx* ctx = s->ds->ctx;
   LowRank& L = s->lr;
   const size_t total = static_cast<size_t>(L.ldm) * s->n;
+  L.U.ensure(total);
   L.W.ensure(total);
   cross_cov_kernel<<<std::max(1, std::min(c1 - c0, ctx->num_sms * 16)), 128, 0, ctx->stream>>>(
       zpts(s), L.M, L.ldm, s->ds->x.get(), s->ds->y.get(), s->ds->tid.get(), c0, c1, dev_kernel(s->th),
-      lag_view(s->lt), L.W.get());
+      lag_view(s->lt), L.U.get());
   launched(ctx);
-  if (keep_U) {
-    L.U.ensure(total);
-    STGP_CUDA(cudaMemcpyAsync(L.U.get() + static_cast<size_t>(c0) * L.ldm, L.W.get() + static_cast<size_t>(c0) * L.ldm,
-                              sizeof(double) * L.ldm * (c1 - c0), cudaMemcpyDeviceToDevice, ctx->stream));
-  }
-  dev_trsm_left(ctx, L.Lm.get(), L.ldm, L.ldm, L.W.get() + static_cast<size_t>(c0) * L.ldm, L.ldm, c1 - c0, false);
+  dev_trmm_left(ctx, L.Lminv.get(), L.ldm, L.ldm, L.U.get() + static_cast<size_t>(c0) * L.ldm, L.ldm, c1 - c0, false,
+                L.W.get() + static_cast<size_t>(c0) * L.ldm, L.ldm);
 }
 
 void ensure_csc(stgp_structure* s) {
@@ -666,14 +665,15 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
     numeric_error("nll_grad: analytic gradient is defined for the observation-policy structure driven by the optimizer");
   stgp_ctx* ctx = s->ds->ctx;
   LowRank& L = s->lr;
-  const int n = s->n, M = L.M, ldm = L.ldm;
-  if (M == 0) {  // plain Vecchia gradient on the residual structure
+  const int n = s->n, ldm = L.ldm;
+  if (L.M == 0) {  // plain Vecchia gradient on the residual structure
     std::vector<double> tot = run_rows(s, kModeGrad, nullptr, 0, s->th.sigma2);
     if (nll_out) *nll_out = 0.5 * (tot[0] + nll_const(n));
     for (int q = 0; q < 7; ++q) grad[q] = tot[1 + q];
     return;
   }
   const size_t total = static_cast<size_t>(ldm) * n;
+  const size_t mm = static_cast<size_t>(ldm) * ldm;
   cudaStream_t st = ctx->stream;
   // u = B r, NLL rows part
   const int nb = std::max(1, std::min(ceil_div(n, 256), ctx->num_sms * 4));
@@ -682,73 +682,70 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
   launch_nll_stored(s, nb, s->u.get());
   const double rows_sum = s->red.finish(ctx, nb, 1)[0];
   if (nll_out) *nll_out = vif_nll_given_u(s, rows_sum);
+  double *g1 = L.tmp("g1", n), *ur = L.tmp("ur", n), *t = L.tmp("t", n), *z = L.tmp("z", n), *Bz = L.tmp("Bz", n),
+         *q = L.tmp("q", n), *tmpv = L.tmp("tmpv", n), *c0 = L.tmp("c0", n),
+         *Rv = L.tmp("Rv", static_cast<size_t>(n) * s->m_v), *yhat = L.tmp("yhat", ldm), *S = L.tmp("S", mm),
+         *Ws = L.tmp("Ws", mm);
   // g1 = D^{-1} u, ur = B^T g1, W ur = V' g1, yhat = K^{-1} W ur, t = W^T yhat
-  DevBuf<double> g1(n), ur(n), t(n), z(n), Bz(n), q(n), tmp(n), c0(n), Rv(static_cast<size_t>(n) * s->m_v);
-  div_kernel<<<grid_for(n), kT, 0, st>>>(n, s->u.get(), s->D.get(), g1.get());
+  div_kernel<<<grid_for(n), kT, 0, st>>>(n, s->u.get(), s->D.get(), g1);
   launched(ctx);
-  bt_apply(s, g1.get(), ur.get());
-  DevBuf<double> yhat(ldm);
-  dev_gemv(ctx, false, ldm, n, 1.0, L.Vp.get(), ldm, g1.get(), 0.0, yhat.get());
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, yhat.get(), ldm, 1, false);
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, yhat.get(), ldm, 1, true);
-  dev_gemv(ctx, true, ldm, n, 1.0, L.W.get(), ldm, yhat.get(), 0.0, t.get());
-  axpby_kernel<<<grid_for(n), kT, 0, st>>>(n, 1.0, s->r.get(), -1.0, t.get(), z.get());
+  bt_apply(s, g1, ur);
+  dev_gemv(ctx, false, ldm, n, 1.0, L.Vp.get(), ldm, g1, 0.0, yhat);
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, yhat, ldm, 1, false);
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, yhat, ldm, 1, true);
+  dev_gemv(ctx, true, ldm, n, 1.0, L.W.get(), ldm, yhat, 0.0, t);
+  axpby_kernel<<<grid_for(n), kT, 0, st>>>(n, 1.0, s->r.get(), -1.0, t, z);
   launched(ctx);
-  b_apply(s, z.get(), Bz.get());
-  // X = K^{-1} V'
+  b_apply(s, z, Bz);
+  // K^{-1} (explicit, M x M) and X = K^{-1} V' as one GEMM
+  L.Kinv.ensure(mm);
+  set_identity_kernel<<<grid_for(static_cast<long long>(mm)), kT, 0, st>>>(L.Kinv.get(), ldm, ldm);
+  launched(ctx);
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, false);
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, true);
   L.work1.ensure(total);
-  STGP_CUDA(cudaMemcpyAsync(L.work1.get(), L.Vp.get(), sizeof(double) * total, cudaMemcpyDeviceToDevice, st));
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.work1.get(), ldm, n, false);
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.work1.get(), ldm, n, true);
+  dev_gemm(ctx, false, false, ldm, n, ldm, 1.0, L.Kinv.get(), ldm, L.Vp.get(), ldm, 0.0, L.work1.get(), ldm);
   // per-row Phi_i: direct pass + c0, Rv
   RowArgs a = row_args(s, L.W.get(), ldm, s->th.sigma2);
   a.X = L.work1.get();
   a.Vp = L.Vp.get();
-  a.z = z.get();
-  a.Bz = Bz.get();
+  a.z = z;
+  a.Bz = Bz;
   a.D_in = s->D.get();
-  a.c0_out = c0.get();
-  a.Rv_out = Rv.get();
+  a.c0_out = c0;
+  a.Rv_out = Rv;
   a.A_out = nullptr;
   a.D_out = nullptr;
   std::vector<double> rows = run_rows_args(s, kModeVifGrad, a);
   for (int qd = 0; qd < 7; ++qd) grad[qd] = rows[1 + qd];
   // E (in place of X) and F
   L.work2.ensure(total);
-  ef_kernel<<<std::min(n, ctx->num_sms * 16), 128, 0, st>>>(0, n, ldm, s->m_v, s->nbr.get(), Rv.get(), c0.get(),
-                                                           s->D.get(), L.W.get(), L.Vp.get(), L.work1.get(),
-                                                           L.work2.get());
+  ef_kernel<<<std::min(n, ctx->num_sms * 16), 128, 0, st>>>(0, n, ldm, s->m_v, s->nbr.get(), Rv, c0, s->D.get(),
+                                                           L.W.get(), L.Vp.get(), L.work1.get(), L.work2.get());
   launched(ctx);
-  // WPhiW^T = sym(V' F^T)  -> wsig' = 0.5 yhat yhat^T + sym(V'F^T) + 0.5 (K^{-1} - I)
-  DevBuf<double> S(static_cast<size_t>(ldm) * ldm), Kinv(static_cast<size_t>(ldm) * ldm), Ws(static_cast<size_t>(ldm) * ldm);
-  dev_gemm(ctx, false, true, ldm, ldm, n, 1.0, L.Vp.get(), ldm, L.work2.get(), ldm, 0.0, S.get(), ldm);
-  set_identity_kernel<<<grid_for(static_cast<long long>(ldm) * ldm), kT, 0, st>>>(Kinv.get(), ldm, ldm);
+  // W Phi W^T = sym(V' F^T) -> wsig' = 0.5 yhat yhat^T + sym(V'F^T) + 0.5 (K^{-1} - I)
+  dev_gemm(ctx, false, true, ldm, ldm, n, 1.0, L.Vp.get(), ldm, L.work2.get(), ldm, 0.0, S, ldm);
+  wsig_assemble_kernel<<<grid_for(static_cast<long long>(mm)), kT, 0, st>>>(L.M, ldm, yhat, S, L.Kinv.get(), Ws);
   launched(ctx);
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, Kinv.get(), ldm, ldm, false);
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, Kinv.get(), ldm, ldm, true);
-  wsig_assemble_kernel<<<grid_for(static_cast<long long>(ldm) * ldm), kT, 0, st>>>(M, ldm, yhat.get(), S.get(), Kinv.get(),
-                                                                                    Ws.get());
-  launched(ctx);
-  // wsig = L_m^{-T} wsig' L_m^{-1}
-  transform_wsig(ctx, L.Lm.get(), ldm, Ws.get());
+  transform_wsig(ctx, L.Lm.get(), ldm, Ws);
   // q = ur - Q t
-  b_apply(s, t.get(), tmp.get());
-  div_kernel<<<grid_for(n), kT, 0, st>>>(n, tmp.get(), s->D.get(), tmp.get());
+  b_apply(s, t, tmpv);
+  div_kernel<<<grid_for(n), kT, 0, st>>>(n, tmpv, s->D.get(), tmpv);
   launched(ctx);
-  bt_apply(s, tmp.get(), q.get());
-  axpby_kernel<<<grid_for(n), kT, 0, st>>>(n, 1.0, ur.get(), -1.0, q.get(), q.get());
+  bt_apply(s, tmpv, q);
+  axpby_kernel<<<grid_for(n), kT, 0, st>>>(n, 1.0, ur, -1.0, q, q);
   launched(ctx);
-  // omega' then omega = L_m^{-T} omega' (reuse the W-sized buffer F after the GEMM)
+  // omega' (into work2, F no longer needed) then omega = L_m^{-T} omega' (into the U buffer's twin work3)
   ensure_csc(s);
   omega_prime_kernel<<<std::min(n, ctx->num_sms * 16), 128, 0, st>>>(0, n, ldm, s->m_v, s->csc_ptr.get(), s->csc_row.get(),
-                                                                     s->csc_slot.get(), s->A.get(), Rv.get(),
-                                                                     L.work1.get(), L.Vp.get(), yhat.get(), q.get(),
-                                                                     L.work2.get());
+                                                                     s->csc_slot.get(), s->A.get(), Rv, L.work1.get(),
+                                                                     L.Vp.get(), yhat, q, L.work2.get());
   launched(ctx);
-  dev_trsm_left(ctx, L.Lm.get(), ldm, ldm, L.work2.get(), ldm, n, true);
+  L.work3.ensure(total);
+  dev_trmm_left(ctx, L.Lminv.get(), ldm, ldm, L.work2.get(), ldm, n, true, L.work3.get(), ldm);
   // U-pair and Sigma_m-pair kernel gradients
-  std::vector<double> gu = upair_grad(s, L.work2.get());
-  std::vector<double> gs = sigma_pair_grad(s, Ws.get());
+  std::vector<double> gu = upair_grad(s, L.work3.get());
+  std::vector<double> gs = sigma_pair_grad(s, Ws);
   for (int qd = 0; qd < 6; ++qd) grad[1 + qd] += gu[qd] + gs[qd];
 }
 

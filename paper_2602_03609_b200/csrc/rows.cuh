@@ -93,13 +93,18 @@ __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, doubl
 
 // Closure Gram G = W_cl^T W_cl over 32 slots (lower 8x8 tiles, mirrored) with
 // DMMA; scol[c] = column of slot c or -1.  Result into sG (row stride LD).
-template <int LD>
+// WITH_X: also Ga[c] = W_{cl_c} . x (x = X(:, i)) as a fifth DMMA column block.
+template <int LD, bool WITH_X>
 __device__ __forceinline__ void closure_gram_dmma(const double* __restrict__ W, int ldw, const int* scol,
-                                                  double* sG, int lane) {
+                                                  double* sG, int lane, const double* __restrict__ xcol,
+                                                  double* sGa) {
   const int grp = lane >> 2, tig = lane & 3;
   double acc[10][2];
+  double accx[4][2];
 #pragma unroll
   for (int t = 0; t < 10; ++t) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) accx[t][0] = accx[t][1] = 0.0;
   const double* colp[4];
 #pragma unroll
   for (int I = 0; I < 4; ++I) {
@@ -110,6 +115,11 @@ __device__ __forceinline__ void closure_gram_dmma(const double* __restrict__ W, 
     double f[4];
 #pragma unroll
     for (int I = 0; I < 4; ++I) f[I] = colp[I] ? __ldg(colp[I] + kb) : 0.0;
+    if (WITH_X) {
+      const double bx = grp == 0 ? __ldg(xcol + kb + tig) : 0.0;
+#pragma unroll
+      for (int I = 0; I < 4; ++I) dmma_f64(accx[I][0], accx[I][1], f[I], bx);
+    }
     int t = 0;
 #pragma unroll
     for (int I = 0; I < 4; ++I)
@@ -131,6 +141,9 @@ __device__ __forceinline__ void closure_gram_dmma(const double* __restrict__ W, 
       sG[(c + 1) * LD + r] = acc[t][1];
       ++t;
     }
+  if (WITH_X && tig == 0)
+#pragma unroll
+    for (int I = 0; I < 4; ++I) sGa[8 * I + grp] = accx[I][0];
 }
 
 template <int MODE, bool HAS_W, int KS>
@@ -177,17 +190,16 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
     }
     scol[w][lane] = pt;
     __syncwarp();
-    if (HAS_W) closure_gram_dmma<LD>(a.W, a.ldw, scol[w], C, lane);  // Gram staged in C
+    // VIF gradient: Ga[s] = W_{cl_s} . X_i (= U_{cl_s} . Hhat_i) from the same DMMA pass
+    if (HAS_W)
+      closure_gram_dmma<LD, MODE == kModeVifGrad>(a.W, a.ldw, scol[w], C, lane,
+                                                 MODE == kModeVifGrad ? a.X + static_cast<size_t>(i) * a.ldw : nullptr,
+                                                 sAw[w][0]);  // Gram staged in C
     __syncwarp();
-    // VIF gradient: Ga[s] = W_{cl_s} . X_i (= U_{cl_s} . Hhat_i), aGa = V'_i . X_i
     double Ga = 0.0, aGa = 0.0;
     if (MODE == kModeVifGrad) {
       const double* xi = a.X + static_cast<size_t>(i) * a.ldw;
-      if (pt >= 0) {
-        const double* wc = a.W + static_cast<size_t>(pt) * a.ldw;
-#pragma unroll 4
-        for (int j = 0; j < a.ldw; ++j) Ga = fma(__ldg(&wc[j]), __ldg(&xi[j]), Ga);
-      }
+      Ga = pt >= 0 ? sAw[w][0][lane] : 0.0;
       const double* vi = a.Vp + static_cast<size_t>(i) * a.ldw;
       for (int j = lane; j < a.ldw; j += 32) aGa = fma(__ldg(&vi[j]), __ldg(&xi[j]), aGa);
 #pragma unroll

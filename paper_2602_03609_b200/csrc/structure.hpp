@@ -2,6 +2,8 @@
 // shared by the Vecchia / FITC / VIF translation units.
 #pragma once
 
+#include <map>
+#include <string>
 #include <vector>
 
 #include "engine.hpp"
@@ -28,7 +30,14 @@ struct LowRank {
   DevBuf<double> Mc;             // Woodbury core (ldm x ldm), Cholesky in place
   double logdet_M = 0.0;
   DevBuf<double> fitc_diag, lambda;  // FITC
+  DevBuf<double> Lminv, Kinv;        // explicit inverses of L_m and K (M x M)
   DevBuf<double> work1, work2, work3, work4, vecM, vecM2, vecN, vecN2;
+  std::map<std::string, DevBuf<double>> pool;  // persistent per-structure temporaries
+  double* tmp(const char* name, size_t count) {
+    DevBuf<double>& b = pool[name];
+    b.ensure(count);
+    return b.get();
+  }
 };
 
 }  // namespace stgp
