@@ -36,7 +36,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="vecchia", choices=["vecchia", "vif"])
+    ap.add_argument("--workload", default="vif", choices=["vecchia", "vif"])
+    ap.add_argument("--m", type=int, default=1000, help="sts kMeans++ inducing request (VIF)")
     ap.add_argument("--stations", type=int, default=10000)
     ap.add_argument("--days", type=int, default=110)
     ap.add_argument("--m_v", type=int, default=30)
@@ -142,24 +143,70 @@ def cpu_sample_vecchia(x, y, t, resp, theta, nbr, target_s=10.0):
                       f"({dt:.2f} s), scaled linearly to n"}
 
 
+def vif_flops(nbr_counts, M):
+    """canonical FP64 work of one VIF NLL+grad:
+    FMA = n [3.5 M^2 + (c_k + (k+1)^2 + k + 2) M + k^3/6 + k^2] + 2/3 M^3, plus n (M + c_k) KE and KG."""
+    k = nbr_counts.astype(np.float64)
+    ck = (k + 1) * (k + 2) / 2
+    fma = np.sum(3.5 * M * M + (ck + (k + 1) ** 2 + k + 2) * M + k ** 3 / 6 + k ** 2) + 2.0 / 3.0 * M ** 3
+    return float(2 * fma + np.sum((M + ck) * (KE_FLOP + KG_FLOP)))
+
+
+def vif_rows_flops(nbr_counts, M):
+    """canonical work of the fused VIF-gradient row kernel: closure Gram c_k M, Ga (k+1) M and
+    aGa M FMAs, Cholesky k^3/6 and two solves 2 k^2, c_k KE + KG."""
+    k = nbr_counts.astype(np.float64)
+    ck = (k + 1) * (k + 2) / 2
+    return float(np.sum(2 * ((ck + k + 2) * M + k ** 3 / 6 + 2 * k ** 2) + ck * (KE_FLOP + KG_FLOP)))
+
+
+def cpu_sample_vif(x, y, t, resp, theta, nbr, Z, target_s=10.0):
+    """Oracle VIF build + nll + build + nll_grad on a prefix of the ordered rows with the full
+    inducing set; the n M^2 and per-row terms are linear in n, so scale linearly."""
+    from oracle import oracle as O
+    cores = O.set_threads(os.cpu_count() or 1)
+    n = len(x)
+    ns = min(n, 1500)
+    while True:
+        om = O.OracleModel("vif", x[:ns], y[:ns], t[:ns], theta, nbr=nbr[:ns], Z=Z)
+        t0 = time.perf_counter()
+        om.nll(resp[:ns])
+        om.nll_grad(resp[:ns])
+        dt = time.perf_counter() - t0
+        if dt >= 3.0 or ns >= n or ns >= 40000:
+            break
+        ns = min(n, 40000, int(ns * max(2.0, min(target_s / max(dt, 1e-3), 8.0))))
+    per_eval_full = dt * n / ns
+    return {"value": 1.0 / per_eval_full, "unit": "evals/s", "cores": cores, "kind": "port",
+            "sample": f"oracle VIF build+nll+build+nll_grad on the first {ns} of {n} ordered rows with all "
+                      f"{len(Z)} inducing points ({dt:.2f} s), scaled linearly to n"}
+
+
 def run_reference(args):
     """--impl reference: the reference algorithm's CPU path (oracle port; the reference
-    itself cannot be built here) on all host cores."""
+    itself cannot be built here) on all host cores, one bounded prefix
+    sample of the workload per step, scaled to n."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle import oracle as O
-    import paper_2602_03609_b200.synth as synth
     x, y, t, resp, theta = make_data(args.stations, args.days)
     n = len(x)
-    m_v = args.m_v
     cores = O.set_threads(os.cpu_count() or 1)
-    # neighbour rows for the sample prefix (the oracle's own exact search)
-    ns = min(n, 30000)
-    nbr = O.dc_neighbors(x[:ns], y[:ns], t[:ns], theta, m_v)
+    if args.workload == "vif":
+        Z, _, _ = O.sts_kmeanspp(x, y, t, args.m, 20260203)
+        ns = min(n, 3000)
+        nbr = O.dr_neighbors(x[:ns], y[:ns], t[:ns], theta, Z, args.m_v)
+        kind, extra = "vif", {"Z": Z}
+        desc = f"oracle VIF build+nll+build+nll_grad on the first {ns} of {n} ordered rows ({len(Z)} inducing points)"
+    else:
+        ns = min(n, 30000)
+        nbr = O.dc_neighbors(x[:ns], y[:ns], t[:ns], theta, args.m_v)
+        kind, extra = "vecchia", {}
+        desc = f"oracle build+nll+build+nll_grad on the first {ns} of {n} ordered rows"
     times = []
     for step in range(args.warmup + args.steps):
-        om = O.OracleModel("vecchia", x[:ns], y[:ns], t[:ns], theta, nbr=nbr)
+        om = O.OracleModel(kind, x[:ns], y[:ns], t[:ns], theta, nbr=nbr, **extra)
         t0 = time.perf_counter()
         om.nll(resp[:ns])
         om.nll_grad(resp[:ns])
@@ -171,14 +218,17 @@ def run_reference(args):
     line = {"metric": METRIC, "value": val, "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg4-{args.workload}-dc" if args.workload == "vecchia" else "cfg4-vif",
-                       "n": n, "m_v": m_v, "stations": args.stations, "days": args.days},
+            "config": {"workload": workload_name(args), "n": n, "m_v": args.m_v, "stations": args.stations,
+                       "days": args.days},
             "impl": "reference",
             "cpu_baseline": {"value": val, "unit": "evals/s", "cores": cores, "kind": "port",
-                             "sample": f"oracle build+nll+build+nll_grad on the first {ns} of {n} ordered rows per "
-                                       "step, scaled linearly to n"},
+                             "sample": desc + " per step, scaled linearly to n"},
             "e2e": {"value": val, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def workload_name(args):
+    return "cfg4-vif-dr-sts" if args.workload == "vif" else "cfg4-vecchia-dc"
 
 
 def main():
@@ -208,13 +258,27 @@ def main():
     n = len(x)
     ds = S.SpaceTimeDataset(x, y, t, resp, ctx=ctx)
     ctx.profile(True)
-    t0 = time.perf_counter()
-    nb = S.correlation_neighbors(ds, theta, args.m_v)
-    nn_s = time.perf_counter() - t0
-    knn_ms, _ = ctx.profile_get("knn_dc")
+    extra = {}
+    if args.workload == "vif":
+        t0 = time.perf_counter()
+        ind = S.sts_kmeanspp(ds, args.m, 20260203)
+        extra["seeding_s"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        nb = S.residual_neighbors(ds, theta, ind, args.m_v)
+        nn_s = time.perf_counter() - t0
+        knn_ms = ctx.profile_get("knn_dr")[0] + ctx.profile_get("dr_whiten")[0]
+        s = S.build_vif(ds, theta, ind, nb, S.OBSERVATION)
+        M = ind.M
+        extra["inducing"] = {"m": args.m, "M": M, "m_s": ind.m_s, "m_t": ind.m_t}
+    else:
+        t0 = time.perf_counter()
+        nb = S.correlation_neighbors(ds, theta, args.m_v)
+        nn_s = time.perf_counter() - t0
+        knn_ms = ctx.profile_get("knn_dc")[0]
+        s = S.build_vecchia(ds, theta, nb, S.OBSERVATION)
+        M = 0
     nbr = nb.indices()
     counts = (nbr >= 0).sum(axis=1)
-    s = S.build_vecchia(ds, theta, nb, S.OBSERVATION)
 
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
     thetas = [tuple(v * (1.0 + 0.01 * ((i % 5) - 2)) if j in (1, 2, 3) else v for j, v in enumerate(theta))
@@ -235,7 +299,6 @@ def main():
         torch.cuda.synchronize()
     ms_total = e0.elapsed_time(e1)
     launches = ctx.kernel_launches() - launches0
-    rows_ms, rows_cnt = ctx.profile_get("rows")
     ms_step = ms_total / args.steps
     if dist:
         tt = torch.tensor([ms_step], dtype=torch.float64)
@@ -251,7 +314,7 @@ def main():
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for i in range(args.steps):
-        v2, g2 = S.evaluate(s, thetas[args.warmup + i], pinned)
+        S.evaluate(s, thetas[args.warmup + i], pinned)
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / args.steps
     if dist:
@@ -259,32 +322,47 @@ def main():
         tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
         e2e_s = float(tt[0])
 
-    # roofline of the dominant kernel (per-row fused build + NLL + gradient)
+    # roofline of the dominant kernel of this step, timed live with events on the context stream
     lo, hi = int(n * rank / world), int(n * (rank + 1) / world)
-    flops_launch = vecchia_flops(counts[lo:hi])
-    rows_avg_ms = rows_ms / max(rows_cnt, 1)
     fp64_peak = ctx.fp64_peak_tflops()
-    achieved = flops_launch / (rows_avg_ms * 1e-3) / 1e12
+    if args.workload == "vif":
+        kname, region = "vecchia_rows_kernel<vif-grad> (closure Gram + Ga by DMMA, Cholesky, Phi_i, KG)", "rows_vifgrad"
+        flops_launch = vif_rows_flops(counts[lo:hi], M)
+        step_flops = vif_flops(counts, M)
+    else:
+        kname, region = "vecchia_rows_kernel<grad>", "rows"
+        flops_launch = vecchia_flops(counts[lo:hi])
+        step_flops = vecchia_flops(counts)
+    k_ms, k_cnt = ctx.profile_get(region)
+    k_avg = k_ms / max(k_cnt, 1)
+    achieved = flops_launch / (k_avg * 1e-3) / 1e12
     roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-            "frac": achieved / fp64_peak, "traffic": None, "kernel": "vecchia_rows_kernel<grad>",
-            "kernel_ms": rows_avg_ms, "kernel_share": rows_avg_ms / ms_step,
+            "frac": achieved / fp64_peak, "traffic": None, "kernel": kname, "kernel_ms": k_avg,
+            "kernel_share": k_avg / ms_step, "flop_per_launch": flops_launch,
             "peak_source": "measured in-run: DFMA throughput microbenchmark (MEASURED_PEAKS.json has no FP64 entry)",
-            "flop_per_launch": flops_launch}
-
+            "step_canonical_flop": step_flops, "step_tflops": step_flops / (ms_step * 1e-3) / 1e12}
     line = {"metric": METRIC, "value": 1e3 / ms_step, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (station x day layout of simulate.cpp, random-feature field + nugget)",
-            "config": {"workload": "cfg4-vecchia-dc", "n": n, "m_v": args.m_v, "stations": args.stations,
-                       "days": args.days, "theta": "PAPER.md Table 3 (NOAA temperature)",
-                       "neighbors": "d_c exact kNN (correlation_neighbors)", "parallelism": f"index-shard x{world}",
-                       "l2": "inputs larger than L2 (nbr 132 MB + A 264 MB per eval)"},
+            "config": {"workload": workload_name(args), "n": n, "m_v": args.m_v, "stations": args.stations,
+                       "days": args.days, "theta": "PAPER.md Table 3 (NOAA temperature)" if args.stations >= 2000
+                       else "PAPER.md section 4",
+                       "neighbors": "d_r exact kNN (residual_neighbors)" if args.workload == "vif"
+                       else "d_c exact kNN (correlation_neighbors)",
+                       "parallelism": f"index-shard x{world}",
+                       "l2": "inputs larger than L2 (W, V' 8 GB each)" if args.workload == "vif"
+                       else "inputs larger than L2 (nbr 132 MB + A 264 MB)"},
             "nn_search_s": nn_s, "nn_search_kernel_ms": knn_ms, "nll": v, "grad": list(g),
             "e2e": {"value": 1.0 / e2e_s, "unit": "evals/s", "h2d_bytes_per_step": n * 8 + 64,
                     "d2h_bytes_per_step": 64},
             "gpu_launches": launches, "roofline": roof, "clocks": clk.summary()}
+    line.update(extra)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_sample_vecchia(x, y, t, resp, theta, nbr)
+        if args.workload == "vif":
+            line["cpu_baseline"] = cpu_sample_vif(x, y, t, resp, theta, nbr, ind.points)
+        else:
+            line["cpu_baseline"] = cpu_sample_vecchia(x, y, t, resp, theta, nbr)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
