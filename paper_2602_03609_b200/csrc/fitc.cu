@@ -124,6 +124,10 @@ void fitc_build(stgp_structure* s) {
   L.Mc.ensure(static_cast<size_t>(ldm) * ldm);
   set_identity(ctx, L.Mc.get(), ldm);
   dev_syrk(ctx, ldm, n, 1.0, L.work1.get(), ldm, 1.0, L.Mc.get(), ldm);
+  dev_symmetrize_lower(ctx, L.Mc.get(), ldm, ldm);
+  L.Kfull.ensure(static_cast<size_t>(ldm) * ldm);
+  STGP_CUDA(cudaMemcpyAsync(L.Kfull.get(), L.Mc.get(), sizeof(double) * ldm * ldm, cudaMemcpyDeviceToDevice,
+                            ctx->stream));
   if (!dev_cholesky(ctx, L.Mc.get(), ldm, ldm)) numeric_error("build_fitc: Woodbury core factorization failed");
   L.logdet_M = dev_logdet_chol(ctx, L.Mc.get(), ldm, ldm);
   s->built = true;

@@ -131,6 +131,17 @@ __global__ void set_identity_kernel(double* A, int ld, int n) {
     A[e] = (e % ld == e / ld) ? 1.0 : 0.0;
 }
 
+__global__ void vsub_kernel(long long n, const double* a, const double* b, double* out) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    out[i] = a[i] - b[i];
+}
+__global__ void vadd_kernel(long long n, const double* a, const double* b, double* out) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    out[i] = a[i] + b[i];
+}
+
 // y = a * x (+ b * z) elementwise helpers
 __global__ void axpby_kernel(int n, double a, const double* x, double b, const double* z, double* y) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -532,6 +543,14 @@ void scale_cols(stgp_ctx* ctx, const double* in, int ldm, long long ncols, const
                                                                                           out);
   launched(ctx);
 }
+void vsub(stgp_ctx* ctx, long long n, const double* a, const double* b, double* out) {
+  vsub_kernel<<<grid_for(n), kT, 0, ctx->stream>>>(n, a, b, out);
+  launched(ctx);
+}
+void vadd(stgp_ctx* ctx, long long n, const double* a, const double* b, double* out) {
+  vadd_kernel<<<grid_for(n), kT, 0, ctx->stream>>>(n, a, b, out);
+  launched(ctx);
+}
 void set_identity(stgp_ctx* ctx, double* A, int ld) {
   set_identity_kernel<<<grid_for(static_cast<long long>(ld) * ld), kT, 0, ctx->stream>>>(A, ld, ld);
   launched(ctx);
@@ -615,6 +634,10 @@ void vif_build(stgp_structure* s) {
                                                                                                L.ldm);
   launched(ctx);
   dev_syrk(ctx, L.ldm, s->n, 1.0, L.work1.get(), L.ldm, 1.0, L.Mc.get(), L.ldm);
+  dev_symmetrize_lower(ctx, L.Mc.get(), L.ldm, L.ldm);
+  L.Kfull.ensure(static_cast<size_t>(L.ldm) * L.ldm);
+  STGP_CUDA(cudaMemcpyAsync(L.Kfull.get(), L.Mc.get(), sizeof(double) * L.ldm * L.ldm, cudaMemcpyDeviceToDevice,
+                            ctx->stream));
   if (!dev_cholesky(ctx, L.Mc.get(), L.ldm, L.ldm)) numeric_error("build_vif: Woodbury core factorization failed");
   L.logdet_M = dev_logdet_chol(ctx, L.Mc.get(), L.ldm, L.ldm);  // = log|M_core| - log|Sigma_m|
   s->built = true;

@@ -23,6 +23,10 @@ void bt_apply(stgp_structure* s, const double* v, double* out);    // B^T v
 void scale_cols(stgp_ctx* ctx, const double* in, int ldm, long long ncols, const double* s, bool rsqrt_of, double* out);
 void set_identity(stgp_ctx* ctx, double* A, int ld);
 void div_vec(stgp_ctx* ctx, int n, const double* x, const double* d, double* y);
+void vsub(stgp_ctx* ctx, long long n, const double* a, const double* b, double* out);  // a - b
+void vadd(stgp_ctx* ctx, long long n, const double* a, const double* b, double* out);  // a + b
+void sigma_inv_apply_dev(stgp_structure* s, const double* v, double* out);
+void gls_beta_device(stgp_structure* s, const double* y_host, const double* X_host, int p, double* beta_out);
 double dev_dot(stgp_ctx* ctx, const double* a, const double* b, long long n, Reducer& red);
 double dev_sum(stgp_ctx* ctx, const double* v, long long n, Reducer& red);
 double dev_sum_log(stgp_ctx* ctx, const double* v, long long n, Reducer& red);

@@ -31,6 +31,7 @@ struct LowRank {
   double logdet_M = 0.0;
   DevBuf<double> fitc_diag, lambda;  // FITC
   DevBuf<double> Lminv, Kinv;        // explicit inverses of L_m and K (M x M)
+  DevBuf<double> Kfull;              // K itself (before its Cholesky), for prediction
   DevBuf<double> work1, work2, work3, work4, vecM, vecM2, vecN, vecN2;
   std::map<std::string, DevBuf<double>> pool;  // persistent per-structure temporaries
   double* tmp(const char* name, size_t count) {
@@ -50,6 +51,7 @@ struct stgp_structure {
   int row_begin = 0, row_end = 0;
   stgp::DevBuf<int32_t> nbr;
   int nbr_kind = 0;
+  double nbr_ss = 1.0, nbr_ts = 1.0;  // Euclidean scales of the neighbour sets (prediction metric)
   stgp::DevBuf<double> A, D;
   stgp::TimeIndex ti;
   bool ti_dirty = true;

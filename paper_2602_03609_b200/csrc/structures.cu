@@ -31,6 +31,8 @@ stgp_structure* new_structure(stgp_dataset* ds, int kind, const Params& th, cons
     if (nb->n != ds->n) config_error("build: neighbor sets inconsistent with the dataset");
     s->m_v = nb->m_v;
     s->nbr_kind = nb->kind;
+    s->nbr_ss = nb->ss;
+    s->nbr_ts = nb->ts;
     s->nbr.alloc(static_cast<size_t>(s->n) * s->m_v);
     STGP_CUDA(cudaMemcpyAsync(s->nbr.get(), nb->idx.get(), static_cast<size_t>(s->n) * s->m_v * sizeof(int32_t),
                               cudaMemcpyDeviceToDevice, st));
@@ -117,7 +119,7 @@ double lowrank_nll(stgp_structure* s);
 void lowrank_nll_grad(stgp_structure* s, double* nll, double* grad);
 void lowrank_predict(stgp_structure* s, int n_p, const double* txyt, int pred_m_v, double* mu, double* var);
 void vecchia_predict(stgp_structure* s, int n_p, const double* txyt, int pred_m_v, double* mu, double* var);
-std::vector<double> sigma_inv_apply_host(stgp_structure* s, const double* v_dev);
+void gls_beta_device(stgp_structure* s, const double* y_host, const double* X_host, int p, double* beta_out);
 }  // namespace stgp
 
 extern "C" {
@@ -230,62 +232,7 @@ int stgp_gls_beta(stgp_structure* s, const double* y, const double* X, int p, do
     if (s->kind != STGP_FITC && s->policy != STGP_OBSERVATION)
       numeric_error("gls_beta: requires the observation-policy structure");
     if (p <= 0) return;
-    const int n = s->n;
-    const double* Xd;
-    const double* yd;
-    if (y) {
-      s->Xwork.upload(X, static_cast<size_t>(n) * p, s->ds->ctx->stream);
-      s->ywork.upload(y, static_cast<size_t>(n), s->ds->ctx->stream);
-      Xd = s->Xwork.get();
-      yd = s->ywork.get();
-    } else {
-      if (!s->ds->has_resp || s->ds->p != p) config_error("gls_beta: resident covariates do not match p");
-      Xd = s->ds->X.get();
-      yd = s->ds->resp.get();
-    }
-    // SX_j = Sigma~^{-1} X_j;  XtSX = X^T SX;  Xty = SX^T y  (approximations.cpp:752-765)
-    std::vector<double> XtSX(static_cast<size_t>(p) * p), Xty(static_cast<size_t>(p));
-    std::vector<double> hX(static_cast<size_t>(n) * p), hy(static_cast<size_t>(n));
-    DevBuf<double> tmpX;
-    tmpX.alloc(static_cast<size_t>(n) * p);
-    STGP_CUDA(cudaMemcpyAsync(hX.data(), Xd, sizeof(double) * n * p, cudaMemcpyDeviceToHost, s->ds->ctx->stream));
-    STGP_CUDA(cudaMemcpyAsync(hy.data(), yd, sizeof(double) * n, cudaMemcpyDeviceToHost, s->ds->ctx->stream));
-    STGP_CUDA(cudaStreamSynchronize(s->ds->ctx->stream));
-    for (int j = 0; j < p; ++j) {
-      const std::vector<double> sx = sigma_inv_apply_host(s, Xd + static_cast<size_t>(j) * n);
-      for (int a = 0; a < p; ++a) {
-        double acc = 0.0;
-        for (int i = 0; i < n; ++i) acc += hX[static_cast<size_t>(i) + static_cast<size_t>(a) * n] * sx[static_cast<size_t>(i)];
-        XtSX[static_cast<size_t>(a) + static_cast<size_t>(j) * p] = acc;
-      }
-      double acc = 0.0;
-      for (int i = 0; i < n; ++i) acc += sx[static_cast<size_t>(i)] * hy[static_cast<size_t>(i)];
-      Xty[static_cast<size_t>(j)] = acc;
-    }
-    // p x p SPD solve (the reference uses LDLT)
-    std::vector<double> L(XtSX);
-    for (int j = 0; j < p; ++j) {
-      double d = L[static_cast<size_t>(j) * p + j];
-      for (int k = 0; k < j; ++k) d -= L[static_cast<size_t>(j) + static_cast<size_t>(k) * p] * L[static_cast<size_t>(j) + static_cast<size_t>(k) * p];
-      if (!(d > 0.0)) numeric_error("gls_beta: normal equations are singular");
-      d = std::sqrt(d);
-      L[static_cast<size_t>(j) + static_cast<size_t>(j) * p] = d;
-      for (int r = j + 1; r < p; ++r) {
-        double v = L[static_cast<size_t>(r) + static_cast<size_t>(j) * p];
-        for (int k = 0; k < j; ++k) v -= L[static_cast<size_t>(r) + static_cast<size_t>(k) * p] * L[static_cast<size_t>(j) + static_cast<size_t>(k) * p];
-        L[static_cast<size_t>(r) + static_cast<size_t>(j) * p] = v / d;
-      }
-    }
-    std::vector<double> z(Xty);
-    for (int r = 0; r < p; ++r) {
-      for (int k = 0; k < r; ++k) z[static_cast<size_t>(r)] -= L[static_cast<size_t>(r) + static_cast<size_t>(k) * p] * z[static_cast<size_t>(k)];
-      z[static_cast<size_t>(r)] /= L[static_cast<size_t>(r) + static_cast<size_t>(r) * p];
-    }
-    for (int r = p - 1; r >= 0; --r) {
-      for (int k = r + 1; k < p; ++k) z[static_cast<size_t>(r)] -= L[static_cast<size_t>(k) + static_cast<size_t>(r) * p] * z[static_cast<size_t>(k)];
-      z[static_cast<size_t>(r)] /= L[static_cast<size_t>(r) + static_cast<size_t>(r) * p];
-    }
-    std::copy(z.begin(), z.end(), beta_out);
+    gls_beta_device(s, y, X, p, beta_out);
   });
 }
 
