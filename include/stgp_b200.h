@@ -73,6 +73,10 @@ int stgp_ctx_synchronize(stgp_ctx* ctx);
 int stgp_ctx_set_shard(stgp_ctx* ctx, int rank, int world);
 int stgp_nccl_unique_id(void* out128);
 int stgp_ctx_init_nccl(stgp_ctx* ctx, const void* unique_id128, int rank, int world);
+/* Sum all-reduce over host buffers supplied by the caller instead of NCCL
+ * (in-process ranks on one device, test harnesses).  fn returns 0 on success. */
+typedef int (*stgp_allreduce_fn)(void* user, double* buf, int64_t count);
+int stgp_ctx_set_host_allreduce(stgp_ctx* ctx, stgp_allreduce_fn fn, void* user);
 /* the context's cudaStream_t (for event timing by the caller) */
 void* stgp_ctx_stream(stgp_ctx* ctx);
 /* live per-kernel timing with CUDA events on the context stream (off by default):

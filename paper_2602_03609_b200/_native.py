@@ -38,6 +38,7 @@ class Params(C.Structure):
 
 _P = C.c_void_p
 _D = C.POINTER(C.c_double)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
 
 # name -> argtypes (restype int unless noted)
 _SIGS = {
@@ -78,6 +79,7 @@ _SIGS = {
     "stgp_debug_exp": [_P, C.c_int, _P, _P],
     "stgp_debug_fp64_peak": [_P, _D],
     "stgp_ctx_profile": [_P, C.c_int],
+    "stgp_ctx_set_host_allreduce": [_P, _P, _P],
     "stgp_ctx_profile_get": [_P, C.c_char_p, _D, C.POINTER(C.c_int64)],
     "stgp_ctx_profile_reset": [_P],
     "stgp_debug_kernel": [_P, C.POINTER(Params), C.c_int, _P, _P, _P, _P],

@@ -79,6 +79,17 @@ class Context:
     def synchronize(self):
         N.call("stgp_ctx_synchronize", self.h)
 
+    def set_host_allreduce(self, fn):
+        """fn(buf: np.ndarray) sums buf across ranks in place (in-process ranks)."""
+        def _cb(user, buf, count):
+            try:
+                fn(np.ctypeslib.as_array(buf, shape=(count,)))
+                return 0
+            except Exception:  # noqa: BLE001 - reported to the engine as a failed all-reduce
+                return 1
+        self._allreduce_cb = N.ALLREDUCE_FN(_cb)
+        N.call("stgp_ctx_set_host_allreduce", self.h, C.cast(self._allreduce_cb, C.c_void_p), None)
+
     def stream_ptr(self) -> int:
         return int(N.lib().stgp_ctx_stream(self.h))
 
@@ -134,6 +145,27 @@ def effective_ranges(theta):
     p = as_params(theta).c_struct()
     N.call("stgp_effective_ranges", C.byref(p), C.byref(tr), C.byref(sr))
     return tr.value, sr.value
+
+
+class HostAllreduce:
+    """Sum all-reduce between in-process ranks (threads) through host buffers."""
+
+    def __init__(self, world: int, timeout: float = 300.0):
+        import threading
+        self.world = world
+        self.bufs = [None] * world
+        self.barrier = threading.Barrier(world, timeout=timeout)
+
+    def for_rank(self, rank: int):
+        def fn(buf):
+            self.bufs[rank] = buf.copy()
+            self.barrier.wait()
+            total = self.bufs[0].copy()
+            for r in range(1, self.world):  # fixed rank order: identical bits on every rank
+                total += self.bufs[r]
+            self.barrier.wait()
+            buf[:] = total
+        return fn
 
 
 class SpaceTimeDataset:

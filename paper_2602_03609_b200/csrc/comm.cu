@@ -13,14 +13,31 @@
 namespace stgp {
 
 void allreduce_sum(stgp_ctx* ctx, double* dev, size_t count) {
-  if (!ctx->comm || ctx->world == 1) return;
+  if (ctx->world == 1 || count == 0) return;
+  if (!ctx->comm && ctx->host_allreduce) {
+    std::vector<double> h(count);
+    STGP_CUDA(cudaMemcpyAsync(h.data(), dev, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
+    STGP_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->host_allreduce(ctx->host_allreduce_user, h.data(), static_cast<int64_t>(count)) != 0)
+      throw Error(kInternal, "host all-reduce callback failed");
+    STGP_CUDA(cudaMemcpyAsync(dev, h.data(), sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
+    STGP_CUDA(cudaStreamSynchronize(ctx->stream));
+    return;
+  }
+  if (!ctx->comm) return;
   const ncclResult_t r = ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, reinterpret_cast<ncclComm_t>(ctx->comm),
                                        ctx->stream);
   if (r != ncclSuccess) throw Error(kInternal, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
 }
 
 void allreduce_host(stgp_ctx* ctx, std::vector<double>& v) {
-  if (!ctx->comm || ctx->world == 1) return;
+  if (ctx->world == 1 || v.empty()) return;
+  if (!ctx->comm && ctx->host_allreduce) {
+    if (ctx->host_allreduce(ctx->host_allreduce_user, v.data(), static_cast<int64_t>(v.size())) != 0)
+      throw Error(kInternal, "host all-reduce callback failed");
+    return;
+  }
+  if (!ctx->comm) return;
   DevBuf<double> d;
   d.upload(v.data(), v.size(), ctx->stream);
   allreduce_sum(ctx, d.get(), v.size());
@@ -65,6 +82,16 @@ int stgp_ctx_init_nccl(stgp_ctx* ctx, const void* uid, int rank, int world) {
   ctx->comm = reinterpret_cast<ncclComm*>(comm);
   ctx->rank = rank;
   ctx->world = world;
+  return STGP_OK;
+}
+
+int stgp_ctx_set_host_allreduce(stgp_ctx* ctx, stgp_allreduce_fn fn, void* user) {
+  if (!ctx) {
+    stgp::g_last_error = "null context";
+    return STGP_ERR_CONFIG;
+  }
+  ctx->host_allreduce = fn;
+  ctx->host_allreduce_user = user;
   return STGP_OK;
 }
 

@@ -61,6 +61,8 @@ struct stgp_ctx {
   ncclComm* comm = nullptr;
   int64_t launches = 0;
   int num_sms = 148;
+  int (*host_allreduce)(void*, double*, int64_t) = nullptr;  // stgp_ctx_set_host_allreduce
+  void* host_allreduce_user = nullptr;
   stgp::DevBuf<int> iscr;     // small persistent scratch (flags, scalars)
   stgp::DevBuf<double> dscr;
   // live per-region kernel timing (stgp_ctx_profile)

@@ -32,13 +32,13 @@ __global__ void fitc_diag_kernel(int n, int M, int ldm, const double* W, double 
     if (lane == 0) {
       double d = s1 - acc;
       if (d < 0.0) {
-        if (d < -clamp_tol) atomicExch(fail, 1);
+        if (d < -clamp_tol) atomicOr(fail, 1);
         d = 0.0;
       }
       diag[i] = d;
       const double l = d + sigma2;
       lambda[i] = l;
-      if (l <= 0.0) atomicExch(fail, 2);
+      if (l <= 0.0) atomicOr(fail, 2);
     }
   }
 }
@@ -102,29 +102,42 @@ void fitc_build(stgp_structure* s) {
   LowRank& L = s->lr;
   prepare_tables(s);
   build_basis(s);
-  build_cross(s, 0, s->n, false);
-  const int n = s->n, ldm = L.ldm;
+  const int rb = s->row_begin, re = s->row_end, ldm = L.ldm, n = s->n;
+  build_cross(s, rb, re, false);
   L.fitc_diag.ensure(n);
   L.lambda.ensure(n);
   DevBuf<int> fail(1);
   fail.zero(ctx->stream);
-  fitc_diag_kernel<<<grid_for(static_cast<long long>(n) * 32), 256, 0, ctx->stream>>>(
-      n, L.M, ldm, L.W.get(), s->th.sigma1_2, s->th.sigma2, 1e-10 * std::max(1.0, s->th.sigma1_2), L.fitc_diag.get(),
-      L.lambda.get(), fail.get());
-  launched(ctx);
-  int f = 0;
-  fail.download(&f, 1, ctx->stream);
-  STGP_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (f == 1) numeric_error("build_fitc: diagonal correction went negative");
-  if (f == 2) numeric_error("build_fitc: zero observation diagonal; a positive nugget is required");
-  // K = I + W Lambda^{-1} W^T
+  const size_t own = static_cast<size_t>(rb) * ldm;
+  if (re > rb) {
+    fitc_diag_kernel<<<grid_for(static_cast<long long>(re - rb) * 32), 256, 0, ctx->stream>>>(
+        re - rb, L.M, ldm, L.W.get() + own, s->th.sigma1_2, s->th.sigma2, 1e-10 * std::max(1.0, s->th.sigma1_2),
+        L.fitc_diag.get() + rb, L.lambda.get() + rb, fail.get());
+    launched(ctx);
+  }
+  std::vector<double> f(2, 0.0);
+  {
+    int fi = 0;
+    fail.download(&fi, 1, ctx->stream);
+    STGP_CUDA(cudaStreamSynchronize(ctx->stream));
+    f[0] = (fi & 1) ? 1.0 : 0.0;
+    f[1] = (fi & 2) ? 1.0 : 0.0;
+  }
+  allreduce_host(ctx, f);  // every rank raises the same error
+  if (f[0] > 0.0) numeric_error("build_fitc: diagonal correction went negative");
+  if (f[1] > 0.0) numeric_error("build_fitc: zero observation diagonal; a positive nugget is required");
+  // K = I + sum_shards W Lambda^{-1} W^T
   const size_t total = static_cast<size_t>(ldm) * n;
   L.work1.ensure(total);
-  scale_cols(ctx, L.W.get(), ldm, n, L.lambda.get(), true, L.work1.get());
   L.Mc.ensure(static_cast<size_t>(ldm) * ldm);
-  set_identity(ctx, L.Mc.get(), ldm);
-  dev_syrk(ctx, ldm, n, 1.0, L.work1.get(), ldm, 1.0, L.Mc.get(), ldm);
+  STGP_CUDA(cudaMemsetAsync(L.Mc.get(), 0, sizeof(double) * ldm * ldm, ctx->stream));
+  if (re > rb) {
+    scale_cols(ctx, L.W.get() + own, ldm, re - rb, L.lambda.get() + rb, true, L.work1.get() + own);
+    dev_syrk(ctx, ldm, re - rb, 1.0, L.work1.get() + own, ldm, 0.0, L.Mc.get(), ldm);
+  }
   dev_symmetrize_lower(ctx, L.Mc.get(), ldm, ldm);
+  allreduce_sum(ctx, L.Mc.get(), static_cast<size_t>(ldm) * ldm);
+  add_identity(ctx, L.Mc.get(), ldm);
   L.Kfull.ensure(static_cast<size_t>(ldm) * ldm);
   STGP_CUDA(cudaMemcpyAsync(L.Kfull.get(), L.Mc.get(), sizeof(double) * ldm * ldm, cudaMemcpyDeviceToDevice,
                             ctx->stream));
@@ -133,80 +146,105 @@ void fitc_build(stgp_structure* s) {
   s->built = true;
 }
 
-// shared prefix of NLL and gradient: rl, v = W rl, K^{-1} v, t = W^T K^{-1} W rl
-static double fitc_core(stgp_structure* s, DevBuf<double>& rl, DevBuf<double>& kv, DevBuf<double>& t) {
+// shared prefix of NLL and gradient (own rows): rl, v = W rl (summed), kv = K^{-1} v, t = W^T kv
+static double fitc_core(stgp_structure* s, double*& rl, double*& kv, double*& t) {
   stgp_ctx* ctx = s->ds->ctx;
   LowRank& L = s->lr;
-  const int n = s->n, ldm = L.ldm;
-  rl.ensure(n);
-  div_vec(ctx, n, s->r.get(), L.lambda.get(), rl.get());
-  kv.ensure(ldm);
-  dev_gemv(ctx, false, ldm, n, 1.0, L.W.get(), ldm, rl.get(), 0.0, kv.get());
-  DevBuf<double> half(ldm);
-  STGP_CUDA(cudaMemcpyAsync(half.get(), kv.get(), sizeof(double) * ldm, cudaMemcpyDeviceToDevice, ctx->stream));
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, half.get(), ldm, 1, false);
-  const double vKv = dev_dot(ctx, half.get(), half.get(), ldm, s->red);
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, kv.get(), ldm, 1, false);
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, kv.get(), ldm, 1, true);
-  t.ensure(n);
-  dev_gemv(ctx, true, ldm, n, 1.0, L.W.get(), ldm, kv.get(), 0.0, t.get());
-  const double rrl = dev_dot(ctx, s->r.get(), rl.get(), n, s->red);
-  const double logl = dev_sum_log(ctx, L.lambda.get(), n, s->red);
-  return 0.5 * (logl + L.logdet_M + rrl - vKv + nll_const(n));
+  const int n = s->n, ldm = L.ldm, rb = s->row_begin, re = s->row_end;
+  const size_t own = static_cast<size_t>(rb) * ldm;
+  rl = L.tmp("f_rl", n);
+  kv = L.tmp("f_kv", ldm);
+  t = L.tmp("f_t", n);
+  double* half = L.tmp("f_half", ldm);
+  STGP_CUDA(cudaMemsetAsync(kv, 0, sizeof(double) * ldm, ctx->stream));
+  std::vector<double> parts(2, 0.0);
+  if (re > rb) {
+    div_vec(ctx, re - rb, s->r.get() + rb, L.lambda.get() + rb, rl + rb);
+    dev_gemv(ctx, false, ldm, re - rb, 1.0, L.W.get() + own, ldm, rl + rb, 0.0, kv);
+    parts[0] = dev_dot(ctx, s->r.get() + rb, rl + rb, re - rb, s->red);
+    parts[1] = dev_sum_log(ctx, L.lambda.get() + rb, re - rb, s->red);
+  }
+  allreduce_sum(ctx, kv, ldm);
+  allreduce_host(ctx, parts);
+  STGP_CUDA(cudaMemcpyAsync(half, kv, sizeof(double) * ldm, cudaMemcpyDeviceToDevice, ctx->stream));
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, half, ldm, 1, false);
+  const double vKv = dev_dot(ctx, half, half, ldm, s->red);
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, kv, ldm, 1, false);
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, kv, ldm, 1, true);
+  if (re > rb) dev_gemv(ctx, true, ldm, re - rb, 1.0, L.W.get() + own, ldm, kv, 0.0, t + rb);
+  return 0.5 * (parts[1] + L.logdet_M + parts[0] - vKv + nll_const(n));
 }
 
 double fitc_nll(stgp_structure* s) {
-  DevBuf<double> rl, kv, t;
+  double *rl, *kv, *t;
   return fitc_core(s, rl, kv, t);
 }
 
 void fitc_nll_grad(stgp_structure* s, double* nll, double* grad) {
   stgp_ctx* ctx = s->ds->ctx;
   LowRank& L = s->lr;
-  const int n = s->n, M = L.M, ldm = L.ldm;
+  const int n = s->n, M = L.M, ldm = L.ldm, rb = s->row_begin, re = s->row_end, nown = re - rb;
+  const size_t own = static_cast<size_t>(rb) * ldm, mm = static_cast<size_t>(ldm) * ldm;
   cudaStream_t st = ctx->stream;
-  DevBuf<double> rl, kv, t;
+  double *rl, *kv, *t;
   const double v = fitc_core(s, rl, kv, t);
   if (nll) *nll = v;
-  // Hw = L_K^{-1} W (|Hw_i|^2 -> diag of Sigma~^{-1}), KW = K^{-1} W
+  double *hsq = L.tmp("f_hsq", n), *alpha = L.tmp("f_alpha", n), *phi = L.tmp("f_phi", n), *wa = L.tmp("f_wa", ldm),
+         *S = L.tmp("f_S", mm), *Ws = L.tmp("f_Ws", mm);
   const size_t total = static_cast<size_t>(ldm) * n;
   L.work1.ensure(total);
-  STGP_CUDA(cudaMemcpyAsync(L.work1.get(), L.W.get(), sizeof(double) * total, cudaMemcpyDeviceToDevice, st));
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.work1.get(), ldm, n, false);
-  DevBuf<double> hsq(n), alpha(n), phi(n), wa(ldm);
-  col_sqnorm_kernel<<<grid_for(static_cast<long long>(n) * 32), 256, 0, st>>>(n, ldm, L.work1.get(), hsq.get());
-  launched(ctx);
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.work1.get(), ldm, n, true);
-  fitc_alpha_phi_kernel<<<grid_for(n), 256, 0, st>>>(n, s->r.get(), L.lambda.get(), t.get(), hsq.get(), alpha.get(),
-                                                     phi.get());
-  launched(ctx);
-  dev_gemv(ctx, false, ldm, n, 1.0, L.W.get(), ldm, alpha.get(), 0.0, wa.get());
-  // S = W diag(phi) W^T ; wsig'
   L.work2.ensure(total);
-  scale_cols(ctx, L.W.get(), ldm, n, phi.get(), false, L.work2.get());
-  DevBuf<double> S(static_cast<size_t>(ldm) * ldm), Kinv(static_cast<size_t>(ldm) * ldm), Ws(static_cast<size_t>(ldm) * ldm);
-  dev_gemm(ctx, false, true, ldm, ldm, n, 1.0, L.W.get(), ldm, L.work2.get(), ldm, 0.0, S.get(), ldm);
-  set_identity(ctx, Kinv.get(), ldm);
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, Kinv.get(), ldm, ldm, false);
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, Kinv.get(), ldm, ldm, true);
-  fitc_wsig_kernel<<<grid_for(static_cast<long long>(ldm) * ldm), 256, 0, st>>>(M, ldm, Kinv.get(), wa.get(), S.get(),
-                                                                                Ws.get());
+  STGP_CUDA(cudaMemsetAsync(wa, 0, sizeof(double) * ldm, st));
+  STGP_CUDA(cudaMemsetAsync(S, 0, sizeof(double) * mm, st));
+  std::vector<double> phisum(1, 0.0);
+  if (nown > 0) {
+    // Hw = L_K^{-1} W (|Hw_i|^2 -> diag of Sigma~^{-1}), then KW = K^{-1} W in place
+    STGP_CUDA(cudaMemcpyAsync(L.work1.get() + own, L.W.get() + own, sizeof(double) * ldm * nown,
+                              cudaMemcpyDeviceToDevice, st));
+    dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.work1.get() + own, ldm, nown, false);
+    col_sqnorm_kernel<<<grid_for(static_cast<long long>(nown) * 32), 256, 0, st>>>(nown, ldm, L.work1.get() + own,
+                                                                                  hsq + rb);
+    launched(ctx);
+    dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.work1.get() + own, ldm, nown, true);
+    fitc_alpha_phi_kernel<<<grid_for(nown), 256, 0, st>>>(nown, s->r.get() + rb, L.lambda.get() + rb, t + rb, hsq + rb,
+                                                          alpha + rb, phi + rb);
+    launched(ctx);
+    dev_gemv(ctx, false, ldm, nown, 1.0, L.W.get() + own, ldm, alpha + rb, 0.0, wa);
+    // S = W diag(phi) W^T
+    scale_cols(ctx, L.W.get() + own, ldm, nown, phi + rb, false, L.work2.get() + own);
+    dev_gemm(ctx, false, true, ldm, ldm, nown, 1.0, L.W.get() + own, ldm, L.work2.get() + own, ldm, 0.0, S, ldm);
+    Reducer rr;
+    phisum[0] = dev_sum(ctx, phi + rb, nown, rr);
+  }
+  allreduce_sum(ctx, wa, ldm);
+  allreduce_sum(ctx, S, mm);
+  allreduce_host(ctx, phisum);
+  L.Kinv.ensure(mm);
+  set_identity(ctx, L.Kinv.get(), ldm);
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, false);
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, true);
+  fitc_wsig_kernel<<<grid_for(static_cast<long long>(mm)), 256, 0, st>>>(M, ldm, L.Kinv.get(), wa, S, Ws);
   launched(ctx);
-  transform_wsig(ctx, L.Lm.get(), ldm, Ws.get());
-  // omega' (in place of KW), omega = L_m^{-T} omega'
-  fitc_omega_kernel<<<grid_for(static_cast<long long>(total)), 256, 0, st>>>(static_cast<long long>(total), ldm,
-                                                                             L.lambda.get(), alpha.get(), phi.get(),
-                                                                             wa.get(), L.W.get(), L.work1.get());
-  launched(ctx);
-  dev_trsm_left(ctx, L.Lm.get(), ldm, ldm, L.work1.get(), ldm, n, true);
-  for (int q = 0; q < 7; ++q) grad[q] = 0.0;
-  Reducer rr;
-  const double phisum = dev_sum(ctx, phi.get(), n, rr);
-  grad[0] += phisum;
-  grad[1] += phisum;
-  std::vector<double> gu = upair_grad(s, L.work1.get());
-  std::vector<double> gs = sigma_pair_grad(s, Ws.get());
-  for (int q = 0; q < 6; ++q) grad[1 + q] += gu[q] + gs[q];
+  transform_wsig(ctx, L.Lm.get(), ldm, Ws);
+  std::vector<double> g(7, 0.0);
+  if (nown > 0) {
+    // omega' (in place of KW), omega = L_m^{-T} omega'
+    fitc_omega_kernel<<<grid_for(static_cast<long long>(ldm) * nown), 256, 0, st>>>(
+        static_cast<long long>(ldm) * nown, ldm, L.lambda.get() + rb, alpha + rb, phi + rb, wa, L.W.get() + own,
+        L.work1.get() + own);
+    launched(ctx);
+    dev_trmm_left(ctx, L.Lminv.get(), ldm, ldm, L.work1.get() + own, ldm, nown, true, L.work2.get() + own, ldm);
+    std::vector<double> gu = upair_grad(s, L.work2.get(), rb, re);
+    for (int q = 0; q < 6; ++q) g[1 + q] += gu[q];
+  }
+  if (ctx->rank == 0) {
+    std::vector<double> gs = sigma_pair_grad(s, Ws);
+    for (int q = 0; q < 6; ++q) g[1 + q] += gs[q];
+  }
+  allreduce_host(ctx, g);
+  for (int q = 0; q < 7; ++q) grad[q] = g[q];
+  grad[0] += phisum[0];
+  grad[1] += phisum[0];
 }
 
 }  // namespace stgp

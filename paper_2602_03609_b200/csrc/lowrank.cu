@@ -226,10 +226,12 @@ __global__ void bt_apply_kernel(int c0, int c1, int m_v, const int32_t* ptr, con
   }
 }
 
-// E_r = X_r / D_r - 2 c0_r V'_r + Zr_r and F_r = c0_r V'_r - Zr_r with Zr_r = sum_a Rv_r[a] W_{N_a}
-// (E overwrites X in place: column r of X is read only here).
+// E_r = X_r / D_r - 2 c0_r V'_r + Zr_r - yhat (Bz)_r / D_r and F_r = c0_r V'_r - Zr_r with
+// Zr_r = sum_a Rv_r[a] W_{N_a} (E overwrites X in place: column r of X is read only here).
+// The yhat term folds yM (ur - Q t)^T of the reference row by row: ur - Q t = Q z = B^T D^{-1} B z.
 __global__ void ef_kernel(int r0, int r1, int ldm, int m_v, const int32_t* nbr, const double* Rv, const double* c0,
-                          const double* D, const double* W, const double* Vp, double* X_E, double* F) {
+                          const double* D, const double* W, const double* Vp, const double* yhat, const double* Bz,
+                          double* X_E, double* F) {
   __shared__ int sN[kMaxGatherM];
   __shared__ double sR[kMaxGatherM];
   for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
@@ -239,7 +241,7 @@ __global__ void ef_kernel(int r0, int r1, int ldm, int m_v, const int32_t* nbr, 
       sR[a] = Rv[static_cast<size_t>(r) * m_v + a];
     }
     __syncthreads();
-    const double cr = c0[r], inv = 1.0 / D[r];
+    const double cr = c0[r], inv = 1.0 / D[r], qr = Bz[r] * inv;
     for (int j = threadIdx.x; j < ldm; j += blockDim.x) {
       double zr = 0.0;
       for (int a = 0; a < m_v; ++a) {
@@ -249,45 +251,67 @@ __global__ void ef_kernel(int r0, int r1, int ldm, int m_v, const int32_t* nbr, 
       }
       const size_t o = static_cast<size_t>(r) * ldm + j;
       const double v = Vp[o];
-      X_E[o] = X_E[o] * inv - 2.0 * cr * v + zr;
+      X_E[o] = X_E[o] * inv - 2.0 * cr * v + zr - yhat[j] * qr;
       F[o] = cr * v - zr;
     }
   }
 }
 
-// omega'(:, b) = -yhat q_b + sum_{(r, a) in col b} ( B(r, b) E_r + Rv_r[a] V'_r )
-__global__ void omega_prime_kernel(int c0, int c1, int ldm, int m_v, const int32_t* ptr, const int32_t* erow,
-                                   const int16_t* eslot, const double* A, const double* Rv, const double* E,
-                                   const double* Vp, const double* yhat, const double* q, double* Om) {
+// omega'(:, b) = sum_{(r, a) in col b, r0 <= r < r1} ( B(r, b) E_r + Rv_r[a] V'_r ): the
+// contribution of this shard's rows (the gradient is linear in omega, so shard partials add).
+__global__ void omega_prime_kernel(int c0, int c1, int r0, int r1, int ldm, int m_v, const int32_t* ptr,
+                                   const int32_t* erow, const int16_t* eslot, const double* A, const double* Rv,
+                                   const double* E, const double* Vp, double* Om) {
   __shared__ int sr[64];
   __shared__ double sb[64], sv[64];
   for (int b = c0 + blockIdx.x; b < c1; b += gridDim.x) {
     const int p0 = ptr[b], p1 = ptr[b + 1];
-    const double qb = q[b];
-    for (int j = threadIdx.x; j < ldm; j += blockDim.x) Om[static_cast<size_t>(b) * ldm + j] = -yhat[j] * qb;
+    double* out = Om + static_cast<size_t>(b) * ldm;
+    for (int j = threadIdx.x; j < ldm; j += blockDim.x) out[j] = 0.0;
     for (int pb = p0; pb < p1; pb += 64) {
       __syncthreads();
-      if (threadIdx.x < 64 && pb + static_cast<int>(threadIdx.x) < p1) {
+      if (threadIdx.x < 64) {
         const int p = pb + threadIdx.x;
-        const int r = erow[p];
-        const int sl = eslot[p];
+        int r = -1;
+        double bb = 0.0, vv = 0.0;
+        if (p < p1) {
+          r = erow[p];
+          const int sl = eslot[p];
+          if (r >= r0 && r < r1) {
+            bb = sl < 0 ? 1.0 : -A[static_cast<size_t>(r) * m_v + sl];
+            vv = sl < 0 ? 0.0 : Rv[static_cast<size_t>(r) * m_v + sl];
+          } else {
+            r = -1;
+          }
+        }
         sr[threadIdx.x] = r;
-        sb[threadIdx.x] = sl < 0 ? 1.0 : -A[static_cast<size_t>(r) * m_v + sl];
-        sv[threadIdx.x] = sl < 0 ? 0.0 : Rv[static_cast<size_t>(r) * m_v + sl];
+        sb[threadIdx.x] = bb;
+        sv[threadIdx.x] = vv;
       }
       __syncthreads();
       const int cnt = min(64, p1 - pb);
       for (int j = threadIdx.x; j < ldm; j += blockDim.x) {
-        double acc = Om[static_cast<size_t>(b) * ldm + j];
+        double acc = out[j];
         for (int e = 0; e < cnt; ++e) {
+          if (sr[e] < 0) continue;
           const size_t o = static_cast<size_t>(sr[e]) * ldm + j;
           acc = fma(sb[e], E[o], acc);
           acc = fma(sv[e], Vp[o], acc);
         }
-        Om[static_cast<size_t>(b) * ldm + j] = acc;
+        out[j] = acc;
       }
     }
   }
+}
+
+// min over rows [r0, r1) of the first (smallest) neighbour index, and r0 itself
+__global__ void halo_kernel(int r0, int r1, int m_v, const int32_t* nbr, int* out) {
+  int mn = r0;
+  for (int i = r0 + blockIdx.x * blockDim.x + threadIdx.x; i < r1; i += gridDim.x * blockDim.x) {
+    const int j = nbr[static_cast<size_t>(i) * m_v];
+    if (j >= 0 && j < mn) mn = j;
+  }
+  atomicMin(out, mn);
 }
 
 // sum_{j, i} Om(j, i) dk(z_j, p_i) over columns [c0, c1): per-block partials (6)
@@ -453,6 +477,7 @@ void lowrank_setup(stgp_structure* s, const stgp_inducing* ind) {
   s->ti.T.insert(s->ti.T.end(), Ti.begin(), Ti.end());
   s->ti.build();
   s->ti_dirty = true;
+  compute_halo(s);
   cudaStream_t st = s->ds->ctx->stream;
   L.zx.upload(zx.data(), L.M, st);
   L.zy.upload(zy.data(), L.M, st);
@@ -495,6 +520,21 @@ void build_cross(stgp_structure* s, int c0, int c1, bool /*keep_U*/) {
   launched(ctx);
   dev_trmm_left(ctx, L.Lminv.get(), L.ldm, L.ldm, L.U.get() + static_cast<size_t>(c0) * L.ldm, L.ldm, c1 - c0, false,
                 L.W.get() + static_cast<size_t>(c0) * L.ldm, L.ldm);
+}
+
+void compute_halo(stgp_structure* s) {
+  stgp_ctx* ctx = s->ds->ctx;
+  int init = s->row_begin;
+  DevBuf<int>& d = ctx->iscr;
+  d.ensure(1);
+  d.upload(&init, 1, ctx->stream);
+  if (s->row_end > s->row_begin && s->kind != STGP_FITC) {
+    halo_kernel<<<grid_for(s->row_end - s->row_begin), kT, 0, ctx->stream>>>(s->row_begin, s->row_end, s->m_v,
+                                                                            s->nbr.get(), d.get());
+    launched(ctx);
+  }
+  d.download(&s->col_begin, 1, ctx->stream);
+  STGP_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 void ensure_csc(stgp_structure* s) {
@@ -543,6 +583,14 @@ void scale_cols(stgp_ctx* ctx, const double* in, int ldm, long long ncols, const
                                                                                           out);
   launched(ctx);
 }
+__global__ void add_identity_kernel(double* A, int ld) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ld; i += gridDim.x * blockDim.x)
+    A[static_cast<size_t>(i) * ld + i] += 1.0;
+}
+void add_identity(stgp_ctx* ctx, double* A, int ld) {
+  add_identity_kernel<<<grid_for(ld), kT, 0, ctx->stream>>>(A, ld);
+  launched(ctx);
+}
 void vsub(stgp_ctx* ctx, long long n, const double* a, const double* b, double* out) {
   vsub_kernel<<<grid_for(n), kT, 0, ctx->stream>>>(n, a, b, out);
   launched(ctx);
@@ -580,12 +628,12 @@ void transform_wsig(stgp_ctx* ctx, const double* Lm, int ldm, double* Ws) {
                            ldm, &one, Lm, ldm, Ws, ldm),
                "trsm(wsig)");
 }
-std::vector<double> upair_grad(stgp_structure* s, const double* Om) {
+std::vector<double> upair_grad(stgp_structure* s, const double* Om, int c0, int c1) {
   stgp_ctx* ctx = s->ds->ctx;
-  const int ub = std::max(1, std::min(s->n, ctx->num_sms * 8));
+  const int ub = std::max(1, std::min(c1 - c0, ctx->num_sms * 8));
   Reducer r;
   r.ensure(ub, 6);
-  upair_grad_kernel<<<ub, 256, 0, ctx->stream>>>(0, s->n, s->lr.M, s->lr.ldm, zpts(s), s->ds->x.get(), s->ds->y.get(),
+  upair_grad_kernel<<<ub, 256, 0, ctx->stream>>>(c0, c1, s->lr.M, s->lr.ldm, zpts(s), s->ds->x.get(), s->ds->y.get(),
                                                  s->ds->tid.get(), dev_kernel(s->th), 1.0 / s->th.c, lag_view(s->lt), Om,
                                                  r.part.get());
   launched(ctx);
@@ -616,55 +664,64 @@ void vif_build(stgp_structure* s) {
     s->built = true;
     return;
   }
+  const int rb = s->row_begin, re = s->row_end, hb = s->col_begin, ldm = L.ldm;
   build_basis(s);
-  build_cross(s, 0, s->n, false);
-  run_rows(s, kModeBuild, L.W.get(), L.ldm, nug);
-  // V' = W B^T and K = I + V' D^{-1} V'^T
-  const size_t total = static_cast<size_t>(L.ldm) * s->n;
+  build_cross(s, hb, re, false);  // W for this shard's rows and their halo
+  run_rows(s, kModeBuild, L.W.get(), ldm, nug);
+  // V' = W B^T (own columns) and K = I + sum_shards V' D^{-1} V'^T
+  const size_t total = static_cast<size_t>(ldm) * s->n;
   L.Vp.ensure(total);
-  vprime_kernel<<<std::min(s->n, ctx->num_sms * 16), 128, 0, ctx->stream>>>(L.W.get(), L.ldm, s->nbr.get(), s->m_v,
-                                                                           s->A.get(), 0, s->n, L.Vp.get());
-  launched(ctx);
+  if (re > rb) {
+    vprime_kernel<<<std::min(re - rb, ctx->num_sms * 16), 128, 0, ctx->stream>>>(L.W.get(), ldm, s->nbr.get(), s->m_v,
+                                                                                s->A.get(), rb, re, L.Vp.get());
+    launched(ctx);
+  }
   L.work1.ensure(total);
-  scale_cols_kernel<<<grid_for(static_cast<long long>(total)), kT, 0, ctx->stream>>>(L.Vp.get(), L.ldm, s->n, s->D.get(),
-                                                                                     true, L.work1.get());
-  launched(ctx);
-  L.Mc.ensure(static_cast<size_t>(L.ldm) * L.ldm);
-  set_identity_kernel<<<grid_for(static_cast<long long>(L.ldm) * L.ldm), kT, 0, ctx->stream>>>(L.Mc.get(), L.ldm,
-                                                                                               L.ldm);
-  launched(ctx);
-  dev_syrk(ctx, L.ldm, s->n, 1.0, L.work1.get(), L.ldm, 1.0, L.Mc.get(), L.ldm);
-  dev_symmetrize_lower(ctx, L.Mc.get(), L.ldm, L.ldm);
-  L.Kfull.ensure(static_cast<size_t>(L.ldm) * L.ldm);
-  STGP_CUDA(cudaMemcpyAsync(L.Kfull.get(), L.Mc.get(), sizeof(double) * L.ldm * L.ldm, cudaMemcpyDeviceToDevice,
+  const size_t off = static_cast<size_t>(rb) * ldm;
+  scale_cols(ctx, L.Vp.get() + off, ldm, re - rb, s->D.get() + rb, true, L.work1.get() + off);
+  L.Mc.ensure(static_cast<size_t>(ldm) * ldm);
+  STGP_CUDA(cudaMemsetAsync(L.Mc.get(), 0, sizeof(double) * ldm * ldm, ctx->stream));
+  if (re > rb) dev_syrk(ctx, ldm, re - rb, 1.0, L.work1.get() + off, ldm, 0.0, L.Mc.get(), ldm);
+  dev_symmetrize_lower(ctx, L.Mc.get(), ldm, ldm);
+  allreduce_sum(ctx, L.Mc.get(), static_cast<size_t>(ldm) * ldm);
+  add_identity(ctx, L.Mc.get(), ldm);
+  L.Kfull.ensure(static_cast<size_t>(ldm) * ldm);
+  STGP_CUDA(cudaMemcpyAsync(L.Kfull.get(), L.Mc.get(), sizeof(double) * ldm * ldm, cudaMemcpyDeviceToDevice,
                             ctx->stream));
-  if (!dev_cholesky(ctx, L.Mc.get(), L.ldm, L.ldm)) numeric_error("build_vif: Woodbury core factorization failed");
-  L.logdet_M = dev_logdet_chol(ctx, L.Mc.get(), L.ldm, L.ldm);  // = log|M_core| - log|Sigma_m|
+  if (!dev_cholesky(ctx, L.Mc.get(), ldm, ldm)) numeric_error("build_vif: Woodbury core factorization failed");
+  L.logdet_M = dev_logdet_chol(ctx, L.Mc.get(), ldm, ldm);  // = log|M_core| - log|Sigma_m|
   s->built = true;
 }
 
 // ---------------------------------------------------------------------------
 // NLL (approximations.cpp:352-384)
 // ---------------------------------------------------------------------------
+// rows_sum: this shard's sum of log D + u^2 / D.  Leaves W ur (all shards) in vecM.
 static double vif_nll_given_u(stgp_structure* s, double rows_sum) {
   stgp_ctx* ctx = s->ds->ctx;
   LowRank& L = s->lr;
+  const int rb = s->row_begin, re = s->row_end, ldm = L.ldm;
+  std::vector<double> parts{rows_sum};
+  allreduce_host(ctx, parts);
   double quad_lr = 0.0, logdet_lr = 0.0;
   if (L.M > 0) {
-    // W ur = V' D^{-1} u;  quad -= (W ur)' K^{-1} (W ur)
-    s->u.ensure(s->n);
+    // W ur = V' D^{-1} u (own columns, then summed over shards);  quad -= (W ur)' K^{-1} (W ur)
     L.vecN.ensure(s->n);
-    div_kernel<<<grid_for(s->n), kT, 0, ctx->stream>>>(s->n, s->u.get(), s->D.get(), L.vecN.get());
-    launched(ctx);
-    L.vecM.ensure(L.ldm);
-    L.vecM2.ensure(L.ldm);
-    dev_gemv(ctx, false, L.ldm, s->n, 1.0, L.Vp.get(), L.ldm, L.vecN.get(), 0.0, L.vecM.get());
-    STGP_CUDA(cudaMemcpyAsync(L.vecM2.get(), L.vecM.get(), sizeof(double) * L.ldm, cudaMemcpyDeviceToDevice, ctx->stream));
-    dev_trsm_left(ctx, L.Mc.get(), L.ldm, L.ldm, L.vecM2.get(), L.ldm, 1, false);  // L_K^{-1} (W ur)
-    quad_lr = dev_dot(ctx, L.vecM2.get(), L.vecM2.get(), L.ldm, s->red);
+    L.vecM.ensure(ldm);
+    L.vecM2.ensure(ldm);
+    STGP_CUDA(cudaMemsetAsync(L.vecM.get(), 0, sizeof(double) * ldm, ctx->stream));
+    if (re > rb) {
+      div_vec(ctx, re - rb, s->u.get() + rb, s->D.get() + rb, L.vecN.get() + rb);
+      dev_gemv(ctx, false, ldm, re - rb, 1.0, L.Vp.get() + static_cast<size_t>(rb) * ldm, ldm, L.vecN.get() + rb, 0.0,
+               L.vecM.get());
+    }
+    allreduce_sum(ctx, L.vecM.get(), ldm);
+    STGP_CUDA(cudaMemcpyAsync(L.vecM2.get(), L.vecM.get(), sizeof(double) * ldm, cudaMemcpyDeviceToDevice, ctx->stream));
+    dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.vecM2.get(), ldm, 1, false);  // L_K^{-1} (W ur)
+    quad_lr = dev_dot(ctx, L.vecM2.get(), L.vecM2.get(), ldm, s->red);
     logdet_lr = L.logdet_M;
   }
-  return 0.5 * (rows_sum - quad_lr + logdet_lr + nll_const(s->n));
+  return 0.5 * (parts[0] - quad_lr + logdet_lr + nll_const(s->n));
 }
 
 double lowrank_nll(stgp_structure* s) {
@@ -688,15 +745,17 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
     numeric_error("nll_grad: analytic gradient is defined for the observation-policy structure driven by the optimizer");
   stgp_ctx* ctx = s->ds->ctx;
   LowRank& L = s->lr;
-  const int n = s->n, ldm = L.ldm;
+  const int n = s->n, ldm = L.ldm, rb = s->row_begin, re = s->row_end, hb = s->col_begin;
   if (L.M == 0) {  // plain Vecchia gradient on the residual structure
     std::vector<double> tot = run_rows(s, kModeGrad, nullptr, 0, s->th.sigma2);
+    allreduce_host(ctx, tot);
     if (nll_out) *nll_out = 0.5 * (tot[0] + nll_const(n));
     for (int q = 0; q < 7; ++q) grad[q] = tot[1 + q];
     return;
   }
   const size_t total = static_cast<size_t>(ldm) * n;
   const size_t mm = static_cast<size_t>(ldm) * ldm;
+  const size_t own = static_cast<size_t>(rb) * ldm, halo = static_cast<size_t>(hb) * ldm;
   cudaStream_t st = ctx->stream;
   // u = B r, NLL rows part
   const int nb = std::max(1, std::min(ceil_div(n, 256), ctx->num_sms * 4));
@@ -704,31 +763,31 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
   s->u.ensure(n);
   launch_nll_stored(s, nb, s->u.get());
   const double rows_sum = s->red.finish(ctx, nb, 1)[0];
-  if (nll_out) *nll_out = vif_nll_given_u(s, rows_sum);
-  double *g1 = L.tmp("g1", n), *ur = L.tmp("ur", n), *t = L.tmp("t", n), *z = L.tmp("z", n), *Bz = L.tmp("Bz", n),
-         *q = L.tmp("q", n), *tmpv = L.tmp("tmpv", n), *c0 = L.tmp("c0", n),
+  const double nll_val = vif_nll_given_u(s, rows_sum);  // leaves W ur (all shards) in L.vecM
+  if (nll_out) *nll_out = nll_val;
+  double *t = L.tmp("t", n), *z = L.tmp("z", n), *Bz = L.tmp("Bz", n), *c0 = L.tmp("c0", n),
          *Rv = L.tmp("Rv", static_cast<size_t>(n) * s->m_v), *yhat = L.tmp("yhat", ldm), *S = L.tmp("S", mm),
          *Ws = L.tmp("Ws", mm);
-  // g1 = D^{-1} u, ur = B^T g1, W ur = V' g1, yhat = K^{-1} W ur, t = W^T yhat
-  div_kernel<<<grid_for(n), kT, 0, st>>>(n, s->u.get(), s->D.get(), g1);
-  launched(ctx);
-  bt_apply(s, g1, ur);
-  dev_gemv(ctx, false, ldm, n, 1.0, L.Vp.get(), ldm, g1, 0.0, yhat);
+  // yhat = K^{-1} W ur, t = W^T yhat, z = r - t (halo + own columns), Bz (own rows)
+  STGP_CUDA(cudaMemcpyAsync(yhat, L.vecM.get(), sizeof(double) * ldm, cudaMemcpyDeviceToDevice, st));
   dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, yhat, ldm, 1, false);
   dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, yhat, ldm, 1, true);
-  dev_gemv(ctx, true, ldm, n, 1.0, L.W.get(), ldm, yhat, 0.0, t);
-  axpby_kernel<<<grid_for(n), kT, 0, st>>>(n, 1.0, s->r.get(), -1.0, t, z);
+  dev_gemv(ctx, true, ldm, re - hb, 1.0, L.W.get() + halo, ldm, yhat, 0.0, t + hb);
+  axpby_kernel<<<grid_for(re - hb), kT, 0, st>>>(re - hb, 1.0, s->r.get() + hb, -1.0, t + hb, z + hb);
   launched(ctx);
-  b_apply(s, z, Bz);
-  // K^{-1} (explicit, M x M) and X = K^{-1} V' as one GEMM
+  b_apply_kernel<<<grid_for(re - rb), kT, 0, st>>>(rb, re, s->m_v, s->nbr.get(), s->A.get(), z, Bz);
+  launched(ctx);
+  // K^{-1} (explicit, M x M) and X = K^{-1} V' (own columns) as one GEMM
   L.Kinv.ensure(mm);
   set_identity_kernel<<<grid_for(static_cast<long long>(mm)), kT, 0, st>>>(L.Kinv.get(), ldm, ldm);
   launched(ctx);
   dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, false);
   dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, true);
   L.work1.ensure(total);
-  dev_gemm(ctx, false, false, ldm, n, ldm, 1.0, L.Kinv.get(), ldm, L.Vp.get(), ldm, 0.0, L.work1.get(), ldm);
-  // per-row Phi_i: direct pass + c0, Rv
+  if (re > rb)
+    dev_gemm(ctx, false, false, ldm, re - rb, ldm, 1.0, L.Kinv.get(), ldm, L.Vp.get() + own, ldm, 0.0,
+             L.work1.get() + own, ldm);
+  // per-row Phi_i: direct pass + c0, Rv (own rows)
   RowArgs a = row_args(s, L.W.get(), ldm, s->th.sigma2);
   a.X = L.work1.get();
   a.Vp = L.Vp.get();
@@ -740,36 +799,46 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
   a.A_out = nullptr;
   a.D_out = nullptr;
   std::vector<double> rows = run_rows_args(s, kModeVifGrad, a);
-  for (int qd = 0; qd < 7; ++qd) grad[qd] = rows[1 + qd];
-  // E (in place of X) and F
+  // E (in place of X) and F (own rows)
   L.work2.ensure(total);
-  ef_kernel<<<std::min(n, ctx->num_sms * 16), 128, 0, st>>>(0, n, ldm, s->m_v, s->nbr.get(), Rv, c0, s->D.get(),
-                                                           L.W.get(), L.Vp.get(), L.work1.get(), L.work2.get());
-  launched(ctx);
-  // W Phi W^T = sym(V' F^T) -> wsig' = 0.5 yhat yhat^T + sym(V'F^T) + 0.5 (K^{-1} - I)
-  dev_gemm(ctx, false, true, ldm, ldm, n, 1.0, L.Vp.get(), ldm, L.work2.get(), ldm, 0.0, S, ldm);
+  if (re > rb) {
+    ef_kernel<<<std::min(re - rb, ctx->num_sms * 16), 128, 0, st>>>(rb, re, ldm, s->m_v, s->nbr.get(), Rv, c0,
+                                                                    s->D.get(), L.W.get(), L.Vp.get(), yhat, Bz,
+                                                                    L.work1.get(), L.work2.get());
+    launched(ctx);
+  }
+  // W Phi W^T = sym(V' F^T) summed over shards -> wsig' = 0.5 yhat yhat^T + sym(V'F^T) + 0.5 (K^{-1} - I)
+  if (re > rb)
+    dev_gemm(ctx, false, true, ldm, ldm, re - rb, 1.0, L.Vp.get() + own, ldm, L.work2.get() + own, ldm, 0.0, S, ldm);
+  else
+    STGP_CUDA(cudaMemsetAsync(S, 0, sizeof(double) * mm, st));
+  allreduce_sum(ctx, S, mm);
   wsig_assemble_kernel<<<grid_for(static_cast<long long>(mm)), kT, 0, st>>>(L.M, ldm, yhat, S, L.Kinv.get(), Ws);
   launched(ctx);
   transform_wsig(ctx, L.Lm.get(), ldm, Ws);
-  // q = ur - Q t
-  b_apply(s, t, tmpv);
-  div_kernel<<<grid_for(n), kT, 0, st>>>(n, tmpv, s->D.get(), tmpv);
-  launched(ctx);
-  bt_apply(s, tmpv, q);
-  axpby_kernel<<<grid_for(n), kT, 0, st>>>(n, 1.0, ur, -1.0, q, q);
-  launched(ctx);
-  // omega' (into work2, F no longer needed) then omega = L_m^{-T} omega' (into the U buffer's twin work3)
+  // omega' over the columns this shard's rows touch, omega = L_m^{-T} omega'
   ensure_csc(s);
-  omega_prime_kernel<<<std::min(n, ctx->num_sms * 16), 128, 0, st>>>(0, n, ldm, s->m_v, s->csc_ptr.get(), s->csc_row.get(),
-                                                                     s->csc_slot.get(), s->A.get(), Rv, L.work1.get(),
-                                                                     L.Vp.get(), yhat, q, L.work2.get());
-  launched(ctx);
-  L.work3.ensure(total);
-  dev_trmm_left(ctx, L.Lminv.get(), ldm, ldm, L.work2.get(), ldm, n, true, L.work3.get(), ldm);
-  // U-pair and Sigma_m-pair kernel gradients
-  std::vector<double> gu = upair_grad(s, L.work3.get());
-  std::vector<double> gs = sigma_pair_grad(s, Ws);
-  for (int qd = 0; qd < 6; ++qd) grad[1 + qd] += gu[qd] + gs[qd];
+  if (re > hb) {
+    omega_prime_kernel<<<std::min(re - hb, ctx->num_sms * 16), 128, 0, st>>>(
+        hb, re, rb, re, ldm, s->m_v, s->csc_ptr.get(), s->csc_row.get(), s->csc_slot.get(), s->A.get(), Rv,
+        L.work1.get(), L.Vp.get(), L.work2.get());
+    launched(ctx);
+    L.work3.ensure(total);
+    dev_trmm_left(ctx, L.Lminv.get(), ldm, ldm, L.work2.get() + halo, ldm, re - hb, true, L.work3.get() + halo, ldm);
+  }
+  // U-pair (this shard's omega) and Sigma_m-pair (rank 0) kernel gradients, then one all-reduce
+  std::vector<double> g(7, 0.0);
+  for (int qd = 0; qd < 7; ++qd) g[qd] = rows[1 + qd];
+  if (re > hb) {
+    std::vector<double> gu = upair_grad(s, L.work3.get(), hb, re);
+    for (int qd = 0; qd < 6; ++qd) g[1 + qd] += gu[qd];
+  }
+  if (ctx->rank == 0) {
+    std::vector<double> gs = sigma_pair_grad(s, Ws);
+    for (int qd = 0; qd < 6; ++qd) g[1 + qd] += gs[qd];
+  }
+  allreduce_host(ctx, g);
+  for (int qd = 0; qd < 7; ++qd) grad[qd] = g[qd];
 }
 
 void lowrank_nll_grad(stgp_structure* s, double* nll, double* grad) {

@@ -33,7 +33,9 @@ double dev_sum_log(stgp_ctx* ctx, const double* v, long long n, Reducer& red);
 // wsig = L_m^{-T} wsig' L_m^{-1} in place
 void transform_wsig(stgp_ctx* ctx, const double* Lm, int ldm, double* Ws);
 // sum_{j,i} Om(j,i) dk(z_j, p_i) and the Sigma_m-pair sum (6 components each)
-std::vector<double> upair_grad(stgp_structure* s, const double* Om);
+std::vector<double> upair_grad(stgp_structure* s, const double* Om, int c0, int c1);
+void add_identity(stgp_ctx* ctx, double* A, int ld);
+void compute_halo(stgp_structure* s);  // col_begin = min neighbour index over this shard's rows
 std::vector<double> sigma_pair_grad(stgp_structure* s, const double* Ws);
 double fitc_nll(stgp_structure* s);
 void fitc_nll_grad(stgp_structure* s, double* nll, double* grad);

@@ -49,6 +49,7 @@ struct stgp_structure {
   stgp::Params th{};
   int n = 0, m_v = 1;
   int row_begin = 0, row_end = 0;
+  int col_begin = 0;  // first column this shard touches (halo of its neighbour sets)
   stgp::DevBuf<int32_t> nbr;
   int nbr_kind = 0;
   double nbr_ss = 1.0, nbr_ts = 1.0;  // Euclidean scales of the neighbour sets (prediction metric)

@@ -232,6 +232,7 @@ int stgp_gls_beta(stgp_structure* s, const double* y, const double* X, int p, do
     if (s->kind != STGP_FITC && s->policy != STGP_OBSERVATION)
       numeric_error("gls_beta: requires the observation-policy structure");
     if (p <= 0) return;
+    if (s->ds->ctx->world > 1) config_error("gls_beta: run on an unsharded context (stgp_ctx_set_shard(ctx, 0, 1))");
     gls_beta_device(s, y, X, p, beta_out);
   });
 }
@@ -244,6 +245,8 @@ int stgp_predict(stgp_structure* s, const double* y, const double* X, int p, con
       numeric_error("predict: requires the observation-policy structure");
     compute_residual(s, y, X, p, beta);
     if (n_p <= 0) return;
+    if (s->kind != STGP_VECCHIA && s->ds->ctx->world > 1)
+      config_error("predict: FITC/VIF prediction runs on an unsharded context (stgp_ctx_set_shard(ctx, 0, 1))");
     if (s->kind == STGP_VECCHIA) vecchia_predict(s, n_p, txyt, pred_m_v, mu, var);
     else lowrank_predict(s, n_p, txyt, pred_m_v, mu, var);
     // fixed effect X_p beta (approximations.cpp:806-812)

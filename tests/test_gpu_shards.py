@@ -1,0 +1,78 @@
+"""Sharded (multi-rank) evaluation emulated with two contexts on one GPU.
+
+Each rank owns a contiguous row range (stgp_ctx_set_shard) and exchanges its
+partial sums through a host all-reduce hook; the kernels of the two ranks never
+wait on each other on the device.  The sharded NLL and gradient must equal the
+single-context values."""
+import threading
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+SEC4 = (0.05, 1.0, 0.5, 20.0, 0.4, 1.5, 0.4, 0.2)
+
+
+@pytest.fixture(scope="module")
+def S():
+    import paper_2602_03609_b200 as S
+    return S
+
+
+def _run(S, world, build, x, y, t, yv, X=None, beta=None):
+    out = [None] * world
+    err = [None] * world
+    hub = S.api.HostAllreduce(world) if world > 1 else None
+
+    def work(rank):
+        try:
+            ctx = S.Context(0)
+            if world > 1:
+                ctx.set_shard(rank, world)
+                ctx.set_host_allreduce(hub.for_rank(rank))
+            ds = S.SpaceTimeDataset(x, y, t, ctx=ctx)
+            s = build(S, ds, ctx)
+            out[rank] = S.nll_and_grad(s, yv, X, beta)
+        except Exception as e:  # noqa: BLE001
+            err[rank] = e
+            if hub:
+                hub.barrier.abort()
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for h in th:
+        h.start()
+    for h in th:
+        h.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
+@pytest.mark.parametrize("kind", ["vecchia", "vif", "fitc"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_equals_single(S, kind, world):
+    x, y, t, yv, X = O.test_dataset(1, 1800, 53, n_times=9, p=1)
+    beta = np.array([0.2])
+    Z = np.column_stack([x, y, t])[::61]
+    nbr = O.dr_neighbors(x, y, t, SEC4, Z, 12) if kind == "vif" else O.dc_neighbors(x, y, t, SEC4, 12)
+
+    def build(S, ds, ctx):
+        nb = S.NeighborSets.from_sets(ds, nbr)
+        ind = S.InducingSet.from_points(Z, ctx=ctx)
+        if kind == "vecchia":
+            return S.build_vecchia(ds, SEC4, nb, S.OBSERVATION)
+        if kind == "vif":
+            return S.build_vif(ds, SEC4, ind, nb, S.OBSERVATION)
+        return S.build_fitc(ds, SEC4, ind)
+
+    (v1, g1), = _run(S, 1, build, x, y, t, yv, X, beta)
+    res = _run(S, world, build, x, y, t, yv, X, beta)
+    for v, g in res:
+        assert v == pytest.approx(v1, rel=1e-11)
+        assert np.allclose(g, g1, rtol=1e-10, atol=1e-10 * np.abs(g1).max())
+    # every rank holds identical bits
+    assert all(r[0] == res[0][0] and (r[1] == res[0][1]).all() for r in res)
