@@ -250,6 +250,11 @@ std::vector<double> Reducer::finish(stgp_ctx* ctx, int blocks, int width) {
   return h;
 }
 
+int lfac_stride_for(int m_v) {
+  const int ks = m_v <= 8 ? 8 : (m_v <= 16 ? 16 : (m_v <= 24 ? 24 : 31));
+  return ks * (ks + 1) / 2 + 32;
+}
+
 int row_blocks(stgp_ctx* ctx, int rows) {
   const int need = ceil_div(std::max(rows, 1), kRowWarps);
   return std::max(1, std::min(need, ctx->num_sms * 16));
@@ -316,6 +321,9 @@ RowArgs row_args(stgp_structure* s, const double* W, int ldw, double nugget) {
   a.D_out = s->D.get();
   a.fail_row = s->fail.get();
   a.u_out = nullptr;
+  a.Lfac_out = nullptr;
+  a.Lfac_in = nullptr;
+  a.A_in = nullptr;
   a.inv_c = 1.0 / s->th.c;
   host_grad00(s->th, a.g00);
   return a;
@@ -349,7 +357,14 @@ std::vector<double> run_rows_args(stgp_structure* s, int mode, RowArgs& a) {
     case 24: STGP_ROWS(M, HW, 24); break; \
     default: STGP_ROWS(M, HW, 31); break; \
   }
-      if (mode == kModeBuild) { if (hw) { STGP_ROWS_KS(kModeBuild, true) } else { STGP_ROWS_KS(kModeBuild, false) } }
+      if (mode == kModeVifGrad && a.Lfac_in) {
+        switch (ks) {
+          case 8: vif_grad_stored_kernel<8><<<blocks, kRowWarps * 32, 0, ctx->stream>>>(a); break;
+          case 16: vif_grad_stored_kernel<16><<<blocks, kRowWarps * 32, 0, ctx->stream>>>(a); break;
+          case 24: vif_grad_stored_kernel<24><<<blocks, kRowWarps * 32, 0, ctx->stream>>>(a); break;
+          default: vif_grad_stored_kernel<31><<<blocks, kRowWarps * 32, 0, ctx->stream>>>(a); break;
+        }
+      } else if (mode == kModeBuild) { if (hw) { STGP_ROWS_KS(kModeBuild, true) } else { STGP_ROWS_KS(kModeBuild, false) } }
       else if (mode == kModeNll) { if (hw) { STGP_ROWS_KS(kModeNll, true) } else { STGP_ROWS_KS(kModeNll, false) } }
       else if (mode == kModeGrad) { if (hw) { STGP_ROWS_KS(kModeGrad, true) } else { STGP_ROWS_KS(kModeGrad, false) } }
       else { STGP_ROWS_KS(kModeVifGrad, true) }

@@ -667,7 +667,14 @@ void vif_build(stgp_structure* s) {
   const int rb = s->row_begin, re = s->row_end, hb = s->col_begin, ldm = L.ldm;
   build_basis(s);
   build_cross(s, hb, re, false);  // W for this shard's rows and their halo
-  run_rows(s, kModeBuild, L.W.get(), ldm, nug);
+  {
+    RowArgs ra = row_args(s, L.W.get(), ldm, nug);
+    if (s->m_v <= kKmax - 1 && s->policy == STGP_OBSERVATION) {
+      L.Lfac.ensure(static_cast<size_t>(s->n) * lfac_stride_for(s->m_v));
+      ra.Lfac_out = L.Lfac.get();
+    }
+    run_rows_args(s, kModeBuild, ra);
+  }
   // V' = W B^T (own columns) and K = I + sum_shards V' D^{-1} V'^T
   const size_t total = static_cast<size_t>(ldm) * s->n;
   L.Vp.ensure(total);
@@ -681,8 +688,10 @@ void vif_build(stgp_structure* s) {
   scale_cols(ctx, L.Vp.get() + off, ldm, re - rb, s->D.get() + rb, true, L.work1.get() + off);
   L.Mc.ensure(static_cast<size_t>(ldm) * ldm);
   STGP_CUDA(cudaMemsetAsync(L.Mc.get(), 0, sizeof(double) * ldm * ldm, ctx->stream));
-  if (re > rb) dev_syrk(ctx, ldm, re - rb, 1.0, L.work1.get() + off, ldm, 0.0, L.Mc.get(), ldm);
-  dev_symmetrize_lower(ctx, L.Mc.get(), ldm, ldm);
+  // full S S^T by GEMM: cuBLAS SYRK tiles this small-output / long-K shape poorly
+  if (re > rb)
+    dev_gemm(ctx, false, true, ldm, ldm, re - rb, 1.0, L.work1.get() + off, ldm, L.work1.get() + off, ldm, 0.0,
+             L.Mc.get(), ldm);
   allreduce_sum(ctx, L.Mc.get(), static_cast<size_t>(ldm) * ldm);
   add_identity(ctx, L.Mc.get(), ldm);
   L.Kfull.ensure(static_cast<size_t>(ldm) * ldm);
@@ -798,6 +807,10 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
   a.Rv_out = Rv;
   a.A_out = nullptr;
   a.D_out = nullptr;
+  if (L.Lfac.get() && s->m_v <= kKmax - 1) {  // stored factors from the build at this theta
+    a.Lfac_in = L.Lfac.get();
+    a.A_in = s->A.get();
+  }
   std::vector<double> rows = run_rows_args(s, kModeVifGrad, a);
   // E (in place of X) and F (own rows)
   L.work2.ensure(total);

@@ -28,7 +28,6 @@ namespace stgp {
 
 namespace {
 
-constexpr int kMaxPredK = 512;
 
 struct PredArgs {
   int n, np, m;  // training rows, targets, pred_m_v

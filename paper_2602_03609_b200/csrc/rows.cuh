@@ -81,7 +81,17 @@ struct RowArgs {
   const double* D_in;
   double* c0_out;  // n
   double* Rv_out;  // n * m_v
+  // stored closure factors: build writes, the VIF gradient pass reads (per row:
+  // packed lower KS x KS factor, then 32 reciprocal pivots)
+  double* Lfac_out;
+  const double* Lfac_in;
+  const double* A_in;
 };
+
+template <int KS>
+constexpr int lfac_stride() {
+  return KS * (KS + 1) / 2 + 32;
+}
 
 enum RowMode { kModeBuild = 0, kModeNll = 1, kModeGrad = 2, kModeVifGrad = 3 };
 
@@ -270,6 +280,14 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
 #pragma unroll
     for (int c = 0; c < KS; ++c)
       if (c <= lane) C[lane * LD + c] = R[c];
+    if (MODE == kModeBuild && a.Lfac_out && lane < KS) {
+      double* dst = a.Lfac_out + static_cast<size_t>(i) * lfac_stride<KS>();
+      const int off = lane * (lane + 1) / 2;
+#pragma unroll
+      for (int c = 0; c < KS; ++c)
+        if (c <= lane) dst[off + c] = R[c];
+      dst[KS * (KS + 1) / 2 + lane] = dinv;
+    }
     __syncwarp();
     // ---- solves: b1 = C^{-1} c (A), b2 = C^{-1} r_N (gradient) ----
     constexpr bool TWO = (MODE == kModeGrad || MODE == kModeVifGrad);
@@ -386,6 +404,156 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
     double s = 0.0;
     for (int ww = 0; ww < kRowWarps; ++ww) s += sred[ww][threadIdx.x];
     a.part[static_cast<size_t>(blockIdx.x) * 8 + threadIdx.x] = s;
+  }
+}
+
+// Ga[s] = W_{cl_s} . x for the 32 closure slots (4 DMMA blocks per k-step).
+__device__ __forceinline__ void closure_x_dmma(const double* __restrict__ W, int ldw, const int* scol,
+                                               const double* __restrict__ xcol, double* sGa, int lane) {
+  const int grp = lane >> 2, tig = lane & 3;
+  double accx[4][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) accx[t][0] = accx[t][1] = 0.0;
+  const double* colp[4];
+#pragma unroll
+  for (int I = 0; I < 4; ++I) {
+    const int c = scol[8 * I + grp];
+    colp[I] = c >= 0 ? W + static_cast<size_t>(c) * ldw + tig : nullptr;
+  }
+  for (int kb = 0; kb < ldw; kb += 4) {
+    const double bx = grp == 0 ? __ldg(xcol + kb + tig) : 0.0;
+#pragma unroll
+    for (int I = 0; I < 4; ++I) {
+      const double f = colp[I] ? __ldg(colp[I] + kb) : 0.0;
+      dmma_f64(accx[I][0], accx[I][1], f, bx);
+    }
+  }
+  if (tig == 0)
+#pragma unroll
+    for (int I = 0; I < 4; ++I) sGa[8 * I + grp] = accx[I][0];
+}
+
+// VIF gradient rows from the build's stored factors (approximations.cpp:616-697):
+// Ga, aGa, vrow, Rv = C_N^{-1} vrow_N with the stored Cholesky factor, c0, Phi_i
+// weights and the direct-pass kernel gradients.  No Gram, assembly or factorisation.
+template <int KS>
+__global__ void __launch_bounds__(kRowWarps * 32) vif_grad_stored_kernel(RowArgs a) {
+  constexpr int NS = KS + 1;
+  constexpr int LD = 33;
+  constexpr int NP = NS * (NS - 1) / 2;
+  __shared__ uint16_t sPair[NP];
+  __shared__ double sL[kRowWarps][32 * LD];
+  __shared__ double sx[kRowWarps][32], sy[kRowWarps][32], sAw[kRowWarps][2][32], sGa[kRowWarps][32];
+  __shared__ int st[kRowWarps][32], scol[kRowWarps][32];
+  __shared__ double sred[kRowWarps][8];
+  for (int p = threadIdx.x; p < NP; p += blockDim.x) {
+    int aa = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * static_cast<float>(p))) * 0.5f);
+    while (aa * (aa - 1) / 2 > p) --aa;
+    while ((aa + 1) * aa / 2 <= p) ++aa;
+    sPair[p] = static_cast<uint16_t>(aa | ((p - aa * (aa - 1) / 2) << 8));
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* Lw = sL[w];
+  double tot[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) tot[q] = 0.0;
+  const int gw = blockIdx.x * kRowWarps + w, nw = gridDim.x * kRowWarps;
+  for (int i = a.row_begin + gw; i < a.row_end; i += nw) {
+    int nb = -1;
+    if (lane < a.m_v) nb = __ldg(&a.nbr[static_cast<size_t>(i) * a.m_v + lane]);
+    const int k = __popc(__ballot_sync(kFull, nb >= 0));
+    const int pt = lane < k ? nb : (lane == KS ? i : -1);
+    double zp = 0.0;
+    if (pt >= 0) {
+      sx[w][lane] = __ldg(&a.x[pt]);
+      sy[w][lane] = __ldg(&a.y[pt]);
+      st[w][lane] = __ldg(&a.tid[pt]);
+      zp = __ldg(&a.z[pt]);
+    }
+    scol[w][lane] = pt;
+    __syncwarp();
+    const double* xi = a.X + static_cast<size_t>(i) * a.ldw;
+    closure_x_dmma(a.W, a.ldw, scol[w], xi, sGa[w], lane);
+    double aGa = 0.0;
+    const double* vi = a.Vp + static_cast<size_t>(i) * a.ldw;
+    for (int j = lane; j < a.ldw; j += 32) aGa = fma(__ldg(&vi[j]), __ldg(&xi[j]), aGa);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) aGa += __shfl_xor_sync(kFull, aGa, o);
+    // stored factor: row `lane` of L into registers and shared memory
+    const double* src = a.Lfac_in + static_cast<size_t>(i) * lfac_stride<KS>();
+    double R[KS];
+    const int off = lane * (lane + 1) / 2;
+#pragma unroll
+    for (int c = 0; c < KS; ++c) R[c] = (lane < KS && c <= lane) ? __ldg(&src[off + c]) : 0.0;
+    const double dinv = lane < KS ? __ldg(&src[KS * (KS + 1) / 2 + lane]) : 0.0;
+#pragma unroll
+    for (int c = 0; c < KS; ++c)
+      if (c <= lane && lane < KS) Lw[lane * LD + c] = R[c];
+    __syncwarp();
+    const double Dst = __ldg(&a.D_in[i]), uz = __ldg(&a.Bz[i]);
+    const double Ga = pt >= 0 ? sGa[w][lane] : 0.0;
+    double b2 = lane < k ? (Ga + uz * zp) / Dst : 0.0;  // vrow_N
+#pragma unroll
+    for (int j = 0; j < KS; ++j) {
+      if (lane == j) b2 *= dinv;
+      const double y2 = __shfl_sync(kFull, b2, j);
+      if (lane > j) b2 = fma(-R[j], y2, b2);
+    }
+#pragma unroll
+    for (int j = KS - 1; j >= 0; --j) {
+      if (lane == j) b2 *= dinv;
+      const double x2 = __shfl_sync(kFull, b2, j);
+      if (lane < j) b2 = fma(-Lw[j * LD + lane], x2, b2);
+    }
+    const double Rv = lane < k ? b2 : 0.0;
+    const double Aval = lane < k ? __ldg(&a.A_in[static_cast<size_t>(i) * a.m_v + lane]) : 0.0;
+    double aa = Aval * Aval, aw = Aval * Rv;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      aa += __shfl_xor_sync(kFull, aa, o);
+      aw += __shfl_xor_sync(kFull, aw, o);
+    }
+    const double cd = 0.5 * (1.0 / Dst - (aGa + uz * uz) / (Dst * Dst));  // c0
+    if (lane == 0) a.c0_out[i] = cd;
+    if (lane < a.m_v) a.Rv_out[static_cast<size_t>(i) * a.m_v + lane] = Rv;
+    sAw[w][0][lane] = lane < k ? -Aval : (lane == KS ? 1.0 : 0.0);
+    sAw[w][1][lane] = Rv;
+    __syncwarp();
+    const int P = (k + 1) * k / 2;
+    double g[6] = {0, 0, 0, 0, 0, 0};
+    for (int p = lane; p < P; p += 32) {
+      const int pr = sPair[p];
+      const int ca = pr & 0xff, sb = pr >> 8;
+      const int sa = ca == k ? KS : ca;
+      const TF f = a.lt.get(st[w][sa], st[w][sb]);
+      double kg[6];
+      gneiting_grad_fast(a.k, a.inv_c, spatial_dist(sx[w][sa], sy[w][sa], sx[w][sb], sy[w][sb]), f, kg);
+      const double ta = sAw[w][0][sa], tb = sAw[w][0][sb], wa = sAw[w][1][sa], wb = sAw[w][1][sb];
+      const double wt = cd * (2.0 * ta * tb) - (wa * tb + wb * ta);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) g[q] = fma(wt, kg[q], g[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) g[q] += __shfl_xor_sync(kFull, g[q], o);
+    const double wd = cd * (1.0 + aa) - (-aw);
+    if (lane == 0) {
+      tot[1] += wd;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) tot[2 + q] += g[q] + wd * a.g00[q];
+    }
+    __syncwarp();
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sred[w][q] = tot[q];
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    double s2 = 0.0;
+    for (int ww = 0; ww < kRowWarps; ++ww) s2 += sred[ww][threadIdx.x];
+    a.part[static_cast<size_t>(blockIdx.x) * 8 + threadIdx.x] = s2;
   }
 }
 

@@ -32,6 +32,7 @@ struct LowRank {
   DevBuf<double> fitc_diag, lambda;  // FITC
   DevBuf<double> Lminv, Kinv;        // explicit inverses of L_m and K (M x M)
   DevBuf<double> Kfull;              // K itself (before its Cholesky), for prediction
+  DevBuf<double> Lfac;               // per-row closure Cholesky factors from the build (VIF)
   DevBuf<double> work1, work2, work3, work4, vecM, vecM2, vecN, vecN2;
   std::map<std::string, DevBuf<double>> pool;  // persistent per-structure temporaries
   double* tmp(const char* name, size_t count) {
@@ -81,6 +82,7 @@ void prepare_tables(stgp_structure* s);
 double nll_const(int n);
 void launch_nll_stored(stgp_structure* s, int blocks, double* u_out);
 int row_blocks(stgp_ctx* ctx, int rows);
+int lfac_stride_for(int m_v);  // per-row stored closure factor size (doubles)
 void upload_lag_table(DevLagTable& d, const TimeIndex& ti, const Params& p, const LagPolicy& pol,
                       cudaStream_t s, bool index_changed);
 LagTable lag_view(const DevLagTable& d);
