@@ -169,6 +169,10 @@ int stgp_eval(stgp_structure* s, const stgp_params* theta, const double* y_host,
 int stgp_debug_exp(stgp_ctx* ctx, int n, const double* x_host, double* out);
 /* FP64 FMA throughput microbenchmark: returns achieved TFLOP/s (2 flops / DFMA) */
 int stgp_debug_fp64_peak(stgp_ctx* ctx, double* tflops);
+/* Measured FP64 tensor-core (mma.sync m8n8k4 f64, DMMA) throughput in TFLOP/s. */
+int stgp_debug_dmma_peak(stgp_ctx* ctx, double* tflops);
+/* Names of the profiled regions recorded so far, newline separated (truncated to cap-1 bytes). */
+int stgp_ctx_profile_names(stgp_ctx* ctx, char* buf, int cap);
 /* device Gneiting covariance / kernel gradient of (h, u) pairs with live factors */
 int stgp_debug_kernel(stgp_ctx* ctx, const stgp_params* theta, int n, const double* h_host,
                       const double* u_host, double* cov_out, double* grad6_out);

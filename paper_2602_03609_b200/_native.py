@@ -78,6 +78,8 @@ _SIGS = {
     "stgp_eval": [_P, C.POINTER(Params), _P, _P, C.c_int, _P, _D, _P],
     "stgp_debug_exp": [_P, C.c_int, _P, _P],
     "stgp_debug_fp64_peak": [_P, _D],
+    "stgp_debug_dmma_peak": [_P, _D],
+    "stgp_ctx_profile_names": [_P, C.c_char_p, C.c_int],
     "stgp_ctx_profile": [_P, C.c_int],
     "stgp_ctx_set_host_allreduce": [_P, _P, _P],
     "stgp_ctx_profile_get": [_P, C.c_char_p, _D, C.POINTER(C.c_int64)],

@@ -98,6 +98,19 @@ class Context:
         N.call("stgp_debug_fp64_peak", self.h, C.byref(out))
         return out.value
 
+    def profile_all(self) -> dict:
+        """{region: (ms, count)} for every profiled region recorded so far."""
+        buf = C.create_string_buffer(1 << 14)
+        N.call("stgp_ctx_profile_names", self.h, buf, len(buf))
+        names = [n for n in buf.value.decode().split("\n") if n]
+        return {n: self.profile_get(n) for n in names}
+
+    def dmma_peak_tflops(self) -> float:
+        """Measured FP64 tensor-core (DMMA m8n8k4) throughput, TFLOP/s."""
+        out = C.c_double()
+        N.call("stgp_debug_dmma_peak", self.h, C.byref(out))
+        return out.value
+
     def profile(self, enable: bool = True):
         N.call("stgp_ctx_profile", self.h, int(enable))
 

@@ -219,6 +219,24 @@ __global__ void fp64_peak_kernel(int iters, double* out) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// 8 independent m8n8k4 f64 MMA chains per warp (512 flop each)
+__global__ void dmma_peak_kernel(int iters, double* out) {
+  double d[8][2];
+  const double a = 1.0 + threadIdx.x * 1e-7, b = 0.999999;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) d[q][0] = d[q][1] = q * 1e-3;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(d[q][0]), "+d"(d[q][1])
+                   : "d"(a), "d"(b));
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += d[q][0] + d[q][1];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 __global__ void debug_exp_kernel(int n, const double* x, double* out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = glibc_exp(x[i]);
 }
@@ -306,6 +324,7 @@ RowArgs row_args(stgp_structure* s, const double* W, int ldw, double nugget) {
   a.m_v = s->m_v;
   a.row_begin = s->row_begin;
   a.row_end = s->row_end;
+  a.order = s->order_rows ? s->rorder.get() : nullptr;
   a.nbr = s->nbr.get();
   a.x = s->ds->x.get();
   a.y = s->ds->y.get();
@@ -329,6 +348,28 @@ RowArgs row_args(stgp_structure* s, const double* W, int ldw, double nugget) {
   return a;
 }
 
+// zeroed work counter for kernels that claim their items in order
+unsigned long long* claim_counter(stgp_ctx* ctx) {
+  DevBuf<int>& ctr = ctx->iscr;
+  ctr.ensure(2);
+  STGP_CUDA(cudaMemsetAsync(ctr.get(), 0, sizeof(unsigned long long), ctx->stream));
+  return reinterpret_cast<unsigned long long*>(ctr.get());
+}
+
+// Launch a warp-per-row kernel: the static grid, or (a.next set) one resident wave whose warps
+// claim rows in schedule order.
+template <typename K>
+static int launch_row_kernel(stgp_ctx* ctx, K kern, int static_blocks, RowArgs& a) {
+  int blocks = static_blocks;
+  if (a.next) {
+    int per_sm = 0;
+    STGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowWarps * 32, 0));
+    blocks = std::max(1, std::min(per_sm, 16)) * ctx->num_sms;
+  }
+  kern<<<blocks, kRowWarps * 32, 0, ctx->stream>>>(a);
+  return blocks;
+}
+
 // Launch the per-row kernel in the given mode; returns the 8 reduced partials.
 std::vector<double> run_rows(stgp_structure* s, int mode, const double* W, int ldw, double nugget) {
   RowArgs a = row_args(s, W, ldw, nugget);
@@ -346,10 +387,19 @@ std::vector<double> run_rows_args(stgp_structure* s, int mode, RowArgs& a) {
     ProfRegion pr(ctx, mode == kModeVifGrad ? "rows_vifgrad" : "rows");
     if (s->m_v <= kKmax - 1) {
       blocks = row_blocks(ctx, rows);
-      s->red.ensure(blocks, 8);
+      s->red.ensure(ctx->num_sms * 16, 8);
       a.part = s->red.part.get();
+      // low-rank row kernels gather W columns: ordered claiming keeps them L2-resident
+      if (hw && (mode == kModeBuild || mode == kModeVifGrad) && rows > 0) {
+        a.next = claim_counter(ctx);
+        if (mode != kModeBuild) {
+          s->row_part.ensure(static_cast<size_t>(rows) * 8);
+          STGP_CUDA(cudaMemsetAsync(s->row_part.get(), 0, sizeof(double) * rows * 8, ctx->stream));
+          a.row_part = s->row_part.get();
+        }
+      }
       const int ks = s->m_v <= 8 ? 8 : (s->m_v <= 16 ? 16 : (s->m_v <= 24 ? 24 : 31));
-#define STGP_ROWS(M, HW, KS) vecchia_rows_kernel<M, HW, KS><<<blocks, kRowWarps * 32, 0, ctx->stream>>>(a)
+#define STGP_ROWS(M, HW, KS) blocks = launch_row_kernel(ctx, vecchia_rows_kernel<M, HW, KS>, blocks, a)
 #define STGP_ROWS_KS(M, HW)              \
   switch (ks) {                          \
     case 8: STGP_ROWS(M, HW, 8); break;   \
@@ -359,10 +409,10 @@ std::vector<double> run_rows_args(stgp_structure* s, int mode, RowArgs& a) {
   }
       if (mode == kModeVifGrad && a.Lfac_in) {
         switch (ks) {
-          case 8: vif_grad_stored_kernel<8><<<blocks, kRowWarps * 32, 0, ctx->stream>>>(a); break;
-          case 16: vif_grad_stored_kernel<16><<<blocks, kRowWarps * 32, 0, ctx->stream>>>(a); break;
-          case 24: vif_grad_stored_kernel<24><<<blocks, kRowWarps * 32, 0, ctx->stream>>>(a); break;
-          default: vif_grad_stored_kernel<31><<<blocks, kRowWarps * 32, 0, ctx->stream>>>(a); break;
+          case 8: blocks = launch_row_kernel(ctx, vif_grad_stored_kernel<8>, blocks, a); break;
+          case 16: blocks = launch_row_kernel(ctx, vif_grad_stored_kernel<16>, blocks, a); break;
+          case 24: blocks = launch_row_kernel(ctx, vif_grad_stored_kernel<24>, blocks, a); break;
+          default: blocks = launch_row_kernel(ctx, vif_grad_stored_kernel<31>, blocks, a); break;
         }
       } else if (mode == kModeBuild) { if (hw) { STGP_ROWS_KS(kModeBuild, true) } else { STGP_ROWS_KS(kModeBuild, false) } }
       else if (mode == kModeNll) { if (hw) { STGP_ROWS_KS(kModeNll, true) } else { STGP_ROWS_KS(kModeNll, false) } }
@@ -389,6 +439,14 @@ std::vector<double> run_rows_args(stgp_structure* s, int mode, RowArgs& a) {
   }
   ++ctx->launches;
   STGP_LAUNCH_CHECK();
+  if (a.row_part) {  // fixed-order reduction of the per-row contributions
+    const int rb2 = std::max(1, std::min(ceil_div(rows, 1024), 1024));
+    const int chunk = ceil_div(rows, rb2);
+    row_part_reduce_kernel<<<rb2, 256, 0, ctx->stream>>>(a.row_part, rows, chunk, s->red.part.get());
+    ++ctx->launches;
+    STGP_LAUNCH_CHECK();
+    blocks = rb2;
+  }
   std::vector<double> tot = s->red.finish(ctx, blocks, 8);
   prof_collect(ctx);
   int fail = 0;
@@ -517,6 +575,41 @@ int stgp_ctx_profile_reset(stgp_ctx* ctx) {
   return guarded([&] {
     prof_collect(ctx);
     ctx->prof_acc.clear();
+  });
+}
+
+int stgp_ctx_profile_names(stgp_ctx* ctx, char* buf, int cap) {
+  return guarded([&] {
+    if (!ctx || !buf || cap < 1) config_error("stgp_ctx_profile_names: bad argument");
+    prof_collect(ctx);
+    std::string all;
+    for (const auto& kv : ctx->prof_acc) all += kv.first + "\n";
+    const size_t n = std::min(all.size(), static_cast<size_t>(cap - 1));
+    std::memcpy(buf, all.data(), n);
+    buf[n] = 0;
+  });
+}
+
+int stgp_debug_dmma_peak(stgp_ctx* ctx, double* tflops) {
+  return guarded([&] {
+    const int blocks = ctx->num_sms * 4, threads = 256, iters = 2048;
+    DevBuf<double> out(static_cast<size_t>(blocks) * threads);
+    cudaEvent_t e0, e1;
+    STGP_CUDA(cudaEventCreate(&e0));
+    STGP_CUDA(cudaEventCreate(&e1));
+    dmma_peak_kernel<<<blocks, threads, 0, ctx->stream>>>(iters, out.get());  // warm-up
+    STGP_CUDA(cudaEventRecord(e0, ctx->stream));
+    for (int r = 0; r < 5; ++r) dmma_peak_kernel<<<blocks, threads, 0, ctx->stream>>>(iters, out.get());
+    STGP_CUDA(cudaEventRecord(e1, ctx->stream));
+    ctx->launches += 6;
+    STGP_LAUNCH_CHECK();
+    STGP_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    STGP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flops = 5.0 * blocks * (threads / 32) * static_cast<double>(iters) * 8 * 512;
+    *tflops = flops / (ms * 1e-3) / 1e12;
   });
 }
 

@@ -12,8 +12,12 @@
 // Sigma_m-pair weights and one TRSM for omega -- the canonical 3.5 n M^2 of
 // SURVEY.md §8(d).  All sparse B / B^T products are deterministic gathers (a
 // CSC of B's pattern is built once per structure).
+#include <algorithm>
 #include <climits>
+#include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <numeric>
 #include <set>
 
@@ -88,24 +92,36 @@ __global__ void cross_cov_kernel(ZPts z, int M, int ldm, const double* x, const 
 }
 
 // V'(:, r) = (W B^T)(:, r) = W(:, r) - sum_a A(r, a) W(:, N_a)   (approximations.cpp:298-305)
-__global__ void vprime_kernel(const double* W, int ldm, const int32_t* nbr, int m_v, const double* A, int r0, int r1,
-                              double* Vp) {
+// The neighbour count is fixed before the j loop so the m_v column loads are batched (unrolled)
+// rather than serialised behind a data-dependent exit.
+__global__ void __launch_bounds__(128) vprime_kernel(const double* W, int ldm, const int32_t* nbr, int m_v,
+                                                     const double* A, int r0, int r1, const int32_t* order,
+                                                     unsigned long long* next, double* Vp) {
   __shared__ int sN[kMaxGatherM];
   __shared__ double sA[kMaxGatherM];
-  for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
+  __shared__ int sk, s_kr;
+  for (;;) {  // rows claimed in order (claim_next): the in-flight rows stay a contiguous window
     __syncthreads();
-    for (int a = threadIdx.x; a < m_v; a += blockDim.x) {
-      sN[a] = nbr[static_cast<size_t>(r) * m_v + a];
-      sA[a] = A[static_cast<size_t>(r) * m_v + a];
+    if (threadIdx.x == 0) {
+      s_kr = static_cast<int>(atomicAdd(next, 1ull));
+      sk = m_v;
     }
     __syncthreads();
+    const int kr = s_kr;
+    if (kr >= r1 - r0) break;
+    const int r = order ? order[kr] : r0 + kr;
+    for (int a = threadIdx.x; a < m_v; a += blockDim.x) {
+      const int c = nbr[static_cast<size_t>(r) * m_v + a];
+      sN[a] = c;
+      sA[a] = A[static_cast<size_t>(r) * m_v + a];
+      if (c < 0 && (a == 0 || nbr[static_cast<size_t>(r) * m_v + a - 1] >= 0)) sk = a;  // packed: first -1
+    }
+    __syncthreads();
+    const int k = sk;
     for (int j = threadIdx.x; j < ldm; j += blockDim.x) {
       double acc = 0.0;
-      for (int a = 0; a < m_v; ++a) {
-        const int c = sN[a];
-        if (c < 0) break;
-        acc += -sA[a] * W[static_cast<size_t>(c) * ldm + j];
-      }
+#pragma unroll 8
+      for (int a = 0; a < k; ++a) acc += -sA[a] * __ldg(&W[static_cast<size_t>(sN[a]) * ldm + j]);
       acc += W[static_cast<size_t>(r) * ldm + j];
       Vp[static_cast<size_t>(r) * ldm + j] = acc;
     }
@@ -229,26 +245,37 @@ __global__ void bt_apply_kernel(int c0, int c1, int m_v, const int32_t* ptr, con
 // E_r = X_r / D_r - 2 c0_r V'_r + Zr_r - yhat (Bz)_r / D_r and F_r = c0_r V'_r - Zr_r with
 // Zr_r = sum_a Rv_r[a] W_{N_a} (E overwrites X in place: column r of X is read only here).
 // The yhat term folds yM (ur - Q t)^T of the reference row by row: ur - Q t = Q z = B^T D^{-1} B z.
-__global__ void ef_kernel(int r0, int r1, int ldm, int m_v, const int32_t* nbr, const double* Rv, const double* c0,
-                          const double* D, const double* W, const double* Vp, const double* yhat, const double* Bz,
-                          double* X_E, double* F) {
+__global__ void __launch_bounds__(128) ef_kernel(int r0, int r1, int ldm, int m_v, const int32_t* nbr,
+                                                 const double* Rv, const double* c0, const double* D, const double* W,
+                                                 const double* Vp, const double* yhat, const double* Bz,
+                                                 const int32_t* order, unsigned long long* next, double* X_E,
+                                                 double* F) {
   __shared__ int sN[kMaxGatherM];
   __shared__ double sR[kMaxGatherM];
-  for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
+  __shared__ int sk, s_kr;
+  for (;;) {
     __syncthreads();
-    for (int a = threadIdx.x; a < m_v; a += blockDim.x) {
-      sN[a] = nbr[static_cast<size_t>(r) * m_v + a];
-      sR[a] = Rv[static_cast<size_t>(r) * m_v + a];
+    if (threadIdx.x == 0) {
+      s_kr = static_cast<int>(atomicAdd(next, 1ull));
+      sk = m_v;
     }
     __syncthreads();
+    const int kr = s_kr;
+    if (kr >= r1 - r0) break;
+    const int r = order ? order[kr] : r0 + kr;
+    for (int a = threadIdx.x; a < m_v; a += blockDim.x) {
+      const int c = nbr[static_cast<size_t>(r) * m_v + a];
+      sN[a] = c;
+      sR[a] = Rv[static_cast<size_t>(r) * m_v + a];
+      if (c < 0 && (a == 0 || nbr[static_cast<size_t>(r) * m_v + a - 1] >= 0)) sk = a;
+    }
+    __syncthreads();
+    const int k = sk;
     const double cr = c0[r], inv = 1.0 / D[r], qr = Bz[r] * inv;
     for (int j = threadIdx.x; j < ldm; j += blockDim.x) {
       double zr = 0.0;
-      for (int a = 0; a < m_v; ++a) {
-        const int c = sN[a];
-        if (c < 0) break;
-        zr = fma(sR[a], W[static_cast<size_t>(c) * ldm + j], zr);
-      }
+#pragma unroll 8
+      for (int a = 0; a < k; ++a) zr = fma(sR[a], __ldg(&W[static_cast<size_t>(sN[a]) * ldm + j]), zr);
       const size_t o = static_cast<size_t>(r) * ldm + j;
       const double v = Vp[o];
       X_E[o] = X_E[o] * inv - 2.0 * cr * v + zr - yhat[j] * qr;
@@ -259,29 +286,51 @@ __global__ void ef_kernel(int r0, int r1, int ldm, int m_v, const int32_t* nbr, 
 
 // omega'(:, b) = sum_{(r, a) in col b, r0 <= r < r1} ( B(r, b) E_r + Rv_r[a] V'_r ): the
 // contribution of this shard's rows (the gradient is linear in omega, so shard partials add).
-__global__ void omega_prime_kernel(int c0, int c1, int r0, int r1, int ldm, int m_v, const int32_t* ptr,
-                                   const int32_t* erow, const int16_t* eslot, const double* A, const double* Rv,
-                                   const double* E, const double* Vp, double* Om) {
+// Work items are (M-chunk, column) pairs, chunk-major: one pass over all columns touches only
+// kOmChunk rows of E and V', so the ~m_v-fold reuse of each gathered column is served from L2
+// (a full-height pass has a working set of ~2 time blocks of E and V', beyond L2).
+template <int NJ>  // M-chunk = 128 * NJ rows, NJ per thread
+__global__ void __launch_bounds__(128) omega_prime_kernel(int c0, int c1, int r0, int r1, int ldm, int m_v,
+                                                          const int32_t* ptr, const int32_t* erow,
+                                                          const int16_t* eslot, const double* A, const double* Rv,
+                                                          const double* E, const double* Vp, const int32_t* corder,
+                                                          unsigned long long* next, double* Om) {
+  constexpr int kChunk = 128 * NJ;
   __shared__ int sr[64];
   __shared__ double sb[64], sv[64];
-  for (int b = c0 + blockIdx.x; b < c1; b += gridDim.x) {
+  __shared__ long long s_item;
+  const long long ncols = c1 - c0;
+  const int nch = (ldm + kChunk - 1) / kChunk;
+  // Items are claimed from a global counter: column entry counts vary widely, and a static
+  // grid-stride split lets blocks drift apart until the in-flight columns span most of the array
+  // (no L2 reuse of the gathered E/V' segments).  Dynamic claiming keeps them a contiguous window.
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_item = static_cast<long long>(atomicAdd(next, 1ull));
+    __syncthreads();
+    const long long e = s_item;
+    if (e >= ncols * nch) break;
+    const int q = static_cast<int>(e / ncols);
+    const int kc = static_cast<int>(e - static_cast<long long>(q) * ncols);
+    const int b = corder ? corder[kc] : c0 + kc;
+    const int jb = q * kChunk + threadIdx.x;
     const int p0 = ptr[b], p1 = ptr[b + 1];
-    double* out = Om + static_cast<size_t>(b) * ldm;
-    for (int j = threadIdx.x; j < ldm; j += blockDim.x) out[j] = 0.0;
+    double acc[NJ];
+#pragma unroll
+    for (int u = 0; u < NJ; ++u) acc[u] = 0.0;
     for (int pb = p0; pb < p1; pb += 64) {
       __syncthreads();
-      if (threadIdx.x < 64) {
+      if (threadIdx.x < 64) {  // entries of other shards' rows get weight 0 (fixed summation order)
         const int p = pb + threadIdx.x;
-        int r = -1;
+        int r = r0;
         double bb = 0.0, vv = 0.0;
         if (p < p1) {
-          r = erow[p];
-          const int sl = eslot[p];
-          if (r >= r0 && r < r1) {
-            bb = sl < 0 ? 1.0 : -A[static_cast<size_t>(r) * m_v + sl];
-            vv = sl < 0 ? 0.0 : Rv[static_cast<size_t>(r) * m_v + sl];
-          } else {
-            r = -1;
+          const int rr = erow[p];
+          if (rr >= r0 && rr < r1) {
+            const int sl = eslot[p];
+            r = rr;
+            bb = sl < 0 ? 1.0 : -A[static_cast<size_t>(rr) * m_v + sl];
+            vv = sl < 0 ? 0.0 : Rv[static_cast<size_t>(rr) * m_v + sl];
           }
         }
         sr[threadIdx.x] = r;
@@ -290,18 +339,46 @@ __global__ void omega_prime_kernel(int c0, int c1, int r0, int r1, int ldm, int 
       }
       __syncthreads();
       const int cnt = min(64, p1 - pb);
-      for (int j = threadIdx.x; j < ldm; j += blockDim.x) {
-        double acc = out[j];
-        for (int e = 0; e < cnt; ++e) {
-          if (sr[e] < 0) continue;
-          const size_t o = static_cast<size_t>(sr[e]) * ldm + j;
-          acc = fma(sb[e], E[o], acc);
-          acc = fma(sv[e], Vp[o], acc);
+#pragma unroll 2
+      for (int t = 0; t < cnt; ++t) {
+        const size_t o = static_cast<size_t>(sr[t]) * ldm;
+        const double cb = sb[t], cv = sv[t];
+#pragma unroll
+        for (int u = 0; u < NJ; ++u) {
+          const int j = jb + 128 * u;
+          if (j < ldm) acc[u] = fma(cv, __ldg(&Vp[o + j]), fma(cb, __ldg(&E[o + j]), acc[u]));
         }
-        out[j] = acc;
       }
     }
+    double* out = Om + static_cast<size_t>(b) * ldm;
+#pragma unroll
+    for (int u = 0; u < NJ; ++u)
+      if (jb + 128 * u < ldm) out[jb + 128 * u] = acc[u];
   }
+}
+
+static void launch_omega_prime(stgp_ctx* ctx, int c0, int c1, int r0, int r1, int ldm, int m_v, const int32_t* ptr,
+                               const int32_t* erow, const int16_t* eslot, const double* A, const double* Rv,
+                               const double* E, const double* Vp, const int32_t* corder, double* Om) {
+  static const int nj_env = [] {
+    const char* e = std::getenv("STGP_OM_NJ");  // tuning switch: 1, 2, 4 or 8 (rows per thread)
+    return e ? std::atoi(e) : 2;
+  }();
+  const int nj = nj_env == 1 || nj_env == 2 || nj_env == 4 || nj_env == 8 ? nj_env : 2;
+  const long long items = static_cast<long long>(c1 - c0) * ((ldm + 128 * nj - 1) / (128 * nj));
+  const int grid = static_cast<int>(std::min<long long>(items, ctx->num_sms * 16));
+  unsigned long long* next = claim_counter(ctx);
+#define STGP_OM(NJ)                                                                                            \
+  omega_prime_kernel<NJ><<<grid, 128, 0, ctx->stream>>>(c0, c1, r0, r1, ldm, m_v, ptr, erow, eslot, A, Rv, E, Vp, \
+                                                        corder, next, Om)
+  switch (nj) {
+    case 1: STGP_OM(1); break;
+    case 4: STGP_OM(4); break;
+    case 8: STGP_OM(8); break;
+    default: STGP_OM(2);
+  }
+#undef STGP_OM
+  launched(ctx);
 }
 
 // min over rows [r0, r1) of the first (smallest) neighbour index, and r0 itself
@@ -450,6 +527,57 @@ double dev_dot(stgp_ctx* ctx, const double* a, const double* b, long long n, Red
   return red.finish(ctx, blocks, 1)[0];
 }
 
+// L2 schedule for the W-gathering kernels (rows kernels, V', E/F, omega'): row i reads the
+// ~m_v columns W(:, N_i) of 7 KB each, and the rows sharing a column are its space-time
+// neighbours.  Index order interleaves stations randomly within a time block, so those rows run
+// thousands of rows apart and every column is re-fetched from HBM ~m_v times.  Processing rows
+// by (time bucket of >= kBucketRows rows, Morton code of (x, y)) keeps the in-flight rows'
+// neighbour columns (current and previous bucket, same spatial patch) L2-resident.  Only the
+// processing order changes: per-row outputs are identical, block partial sums are regrouped.
+std::vector<int32_t> locality_order(const stgp_dataset* ds, int lo, int hi) {
+  constexpr int kBucketRows = 4096;
+  std::vector<int32_t> out;
+  if (hi <= lo) return out;
+  const size_t nT = ds->Tdata.size();
+  std::vector<int> cnt(nT, 0), bucket(nT, 0);
+  for (int32_t t : ds->htid) ++cnt[static_cast<size_t>(t)];
+  int b = 0, acc = 0;
+  for (size_t t = 0; t < nT; ++t) {
+    bucket[t] = b;
+    acc += cnt[t];
+    if (acc >= kBucketRows) {
+      ++b;
+      acc = 0;
+    }
+  }
+  double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
+  for (int i = 0; i < ds->n; ++i) {
+    x0 = std::min(x0, ds->hx[i]);
+    x1 = std::max(x1, ds->hx[i]);
+    y0 = std::min(y0, ds->hy[i]);
+    y1 = std::max(y1, ds->hy[i]);
+  }
+  const double sx = x1 > x0 ? 65535.0 / (x1 - x0) : 0.0, sy = y1 > y0 ? 65535.0 / (y1 - y0) : 0.0;
+  auto spread = [](uint64_t v) {  // 16 bits -> even bit positions
+    v &= 0xffff;
+    v = (v | (v << 8)) & 0x00ff00ff;
+    v = (v | (v << 4)) & 0x0f0f0f0f;
+    v = (v | (v << 2)) & 0x33333333;
+    v = (v | (v << 1)) & 0x55555555;
+    return v;
+  };
+  std::vector<std::pair<uint64_t, int32_t>> key(static_cast<size_t>(hi - lo));
+  for (int i = lo; i < hi; ++i) {
+    const uint64_t qx = static_cast<uint64_t>((ds->hx[i] - x0) * sx), qy = static_cast<uint64_t>((ds->hy[i] - y0) * sy);
+    const uint64_t bk = static_cast<uint64_t>(bucket[static_cast<size_t>(ds->htid[static_cast<size_t>(i)])]);
+    key[static_cast<size_t>(i - lo)] = {(bk << 32) | spread(qx) | (spread(qy) << 1), i};
+  }
+  std::sort(key.begin(), key.end());
+  out.resize(key.size());
+  for (size_t k = 0; k < key.size(); ++k) out[k] = key[k].second;
+  return out;
+}
+
 ZPts zpts(const stgp_structure* s) { return ZPts{s->lr.zx.get(), s->lr.zy.get(), s->lr.ztid.get()}; }
 
 void lowrank_setup(stgp_structure* s, const stgp_inducing* ind) {
@@ -479,6 +607,16 @@ void lowrank_setup(stgp_structure* s, const stgp_inducing* ind) {
   s->ti_dirty = true;
   compute_halo(s);
   cudaStream_t st = s->ds->ctx->stream;
+  const char* om = std::getenv("STGP_ORDER");  // tuning switch: none | rows | all (default none)
+  const std::string omode = om ? om : "none";
+  s->order_rows = omode == "rows" || omode == "all";
+  s->order_gather = omode == "all";
+  if (s->kind == STGP_VIF && (s->order_rows || s->order_gather)) {
+    const std::vector<int32_t> ro = locality_order(s->ds, s->row_begin, s->row_end);
+    const std::vector<int32_t> co = locality_order(s->ds, s->col_begin, s->row_end);
+    if (!ro.empty()) s->rorder.upload(ro.data(), ro.size(), st);
+    if (!co.empty()) s->corder.upload(co.data(), co.size(), st);
+  }
   L.zx.upload(zx.data(), L.M, st);
   L.zy.upload(zy.data(), L.M, st);
   L.zt.upload(zt.data(), L.M, st);
@@ -514,10 +652,14 @@ void build_cross(stgp_structure* s, int c0, int c1, bool /*keep_U*/) {
   const size_t total = static_cast<size_t>(L.ldm) * s->n;
   L.U.ensure(total);
   L.W.ensure(total);
-  cross_cov_kernel<<<std::max(1, std::min(c1 - c0, ctx->num_sms * 16)), 128, 0, ctx->stream>>>(
-      zpts(s), L.M, L.ldm, s->ds->x.get(), s->ds->y.get(), s->ds->tid.get(), c0, c1, dev_kernel(s->th),
-      lag_view(s->lt), L.U.get());
-  launched(ctx);
+  {
+    ProfRegion pr(ctx, "U_cross_cov");
+    cross_cov_kernel<<<std::max(1, std::min(c1 - c0, ctx->num_sms * 16)), 128, 0, ctx->stream>>>(
+        zpts(s), L.M, L.ldm, s->ds->x.get(), s->ds->y.get(), s->ds->tid.get(), c0, c1, dev_kernel(s->th),
+        lag_view(s->lt), L.U.get());
+    launched(ctx);
+  }
+  ProfRegion pr(ctx, "W_trmm");
   dev_trmm_left(ctx, L.Lminv.get(), L.ldm, L.ldm, L.U.get() + static_cast<size_t>(c0) * L.ldm, L.ldm, c1 - c0, false,
                 L.W.get() + static_cast<size_t>(c0) * L.ldm, L.ldm);
 }
@@ -665,7 +807,10 @@ void vif_build(stgp_structure* s) {
     return;
   }
   const int rb = s->row_begin, re = s->row_end, hb = s->col_begin, ldm = L.ldm;
-  build_basis(s);
+  {
+    ProfRegion pr(ctx, "basis");
+    build_basis(s);
+  }
   build_cross(s, hb, re, false);  // W for this shard's rows and their halo
   {
     RowArgs ra = row_args(s, L.W.get(), ldm, nug);
@@ -679,10 +824,12 @@ void vif_build(stgp_structure* s) {
   const size_t total = static_cast<size_t>(ldm) * s->n;
   L.Vp.ensure(total);
   if (re > rb) {
+    ProfRegion pr(ctx, "vprime");
     vprime_kernel<<<std::min(re - rb, ctx->num_sms * 16), 128, 0, ctx->stream>>>(L.W.get(), ldm, s->nbr.get(), s->m_v,
-                                                                                s->A.get(), rb, re, L.Vp.get());
+                                                                                s->A.get(), rb, re, s->order_gather ? s->rorder.get() : nullptr, claim_counter(ctx), L.Vp.get());
     launched(ctx);
   }
+  ProfRegion prk(ctx, "K_gemm_chol");
   L.work1.ensure(total);
   const size_t off = static_cast<size_t>(rb) * ldm;
   scale_cols(ctx, L.Vp.get() + off, ldm, re - rb, s->D.get() + rb, true, L.work1.get() + off);
@@ -767,12 +914,14 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
   const size_t own = static_cast<size_t>(rb) * ldm, halo = static_cast<size_t>(hb) * ldm;
   cudaStream_t st = ctx->stream;
   // u = B r, NLL rows part
+  std::unique_ptr<ProfRegion> ph(new ProfRegion(ctx, "g_nll"));
   const int nb = std::max(1, std::min(ceil_div(n, 256), ctx->num_sms * 4));
   s->red.ensure(nb, 1);
   s->u.ensure(n);
   launch_nll_stored(s, nb, s->u.get());
   const double rows_sum = s->red.finish(ctx, nb, 1)[0];
   const double nll_val = vif_nll_given_u(s, rows_sum);  // leaves W ur (all shards) in L.vecM
+  ph.reset(new ProfRegion(ctx, "g_t_z"));
   if (nll_out) *nll_out = nll_val;
   double *t = L.tmp("t", n), *z = L.tmp("z", n), *Bz = L.tmp("Bz", n), *c0 = L.tmp("c0", n),
          *Rv = L.tmp("Rv", static_cast<size_t>(n) * s->m_v), *yhat = L.tmp("yhat", ldm), *S = L.tmp("S", mm),
@@ -787,6 +936,7 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
   b_apply_kernel<<<grid_for(re - rb), kT, 0, st>>>(rb, re, s->m_v, s->nbr.get(), s->A.get(), z, Bz);
   launched(ctx);
   // K^{-1} (explicit, M x M) and X = K^{-1} V' (own columns) as one GEMM
+  ph.reset(new ProfRegion(ctx, "g_X_gemm"));
   L.Kinv.ensure(mm);
   set_identity_kernel<<<grid_for(static_cast<long long>(mm)), kT, 0, st>>>(L.Kinv.get(), ldm, ldm);
   launched(ctx);
@@ -797,6 +947,7 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
     dev_gemm(ctx, false, false, ldm, re - rb, ldm, 1.0, L.Kinv.get(), ldm, L.Vp.get() + own, ldm, 0.0,
              L.work1.get() + own, ldm);
   // per-row Phi_i: direct pass + c0, Rv (own rows)
+  ph.reset();
   RowArgs a = row_args(s, L.W.get(), ldm, s->th.sigma2);
   a.X = L.work1.get();
   a.Vp = L.Vp.get();
@@ -813,35 +964,40 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
   }
   std::vector<double> rows = run_rows_args(s, kModeVifGrad, a);
   // E (in place of X) and F (own rows)
+  ph.reset(new ProfRegion(ctx, "g_ef"));
   L.work2.ensure(total);
   if (re > rb) {
     ef_kernel<<<std::min(re - rb, ctx->num_sms * 16), 128, 0, st>>>(rb, re, ldm, s->m_v, s->nbr.get(), Rv, c0,
                                                                     s->D.get(), L.W.get(), L.Vp.get(), yhat, Bz,
-                                                                    L.work1.get(), L.work2.get());
+                                                                    s->order_gather ? s->rorder.get() : nullptr, claim_counter(ctx), L.work1.get(), L.work2.get());
     launched(ctx);
   }
+  ph.reset(new ProfRegion(ctx, "g_S_gemm"));
   // W Phi W^T = sym(V' F^T) summed over shards -> wsig' = 0.5 yhat yhat^T + sym(V'F^T) + 0.5 (K^{-1} - I)
   if (re > rb)
     dev_gemm(ctx, false, true, ldm, ldm, re - rb, 1.0, L.Vp.get() + own, ldm, L.work2.get() + own, ldm, 0.0, S, ldm);
   else
     STGP_CUDA(cudaMemsetAsync(S, 0, sizeof(double) * mm, st));
   allreduce_sum(ctx, S, mm);
+  ph.reset(new ProfRegion(ctx, "g_wsig"));
   wsig_assemble_kernel<<<grid_for(static_cast<long long>(mm)), kT, 0, st>>>(L.M, ldm, yhat, S, L.Kinv.get(), Ws);
   launched(ctx);
   transform_wsig(ctx, L.Lm.get(), ldm, Ws);
   // omega' over the columns this shard's rows touch, omega = L_m^{-T} omega'
+  ph.reset(new ProfRegion(ctx, "g_omega"));
   ensure_csc(s);
   if (re > hb) {
-    omega_prime_kernel<<<std::min(re - hb, ctx->num_sms * 16), 128, 0, st>>>(
-        hb, re, rb, re, ldm, s->m_v, s->csc_ptr.get(), s->csc_row.get(), s->csc_slot.get(), s->A.get(), Rv,
-        L.work1.get(), L.Vp.get(), L.work2.get());
-    launched(ctx);
+    launch_omega_prime(ctx, hb, re, rb, re, ldm, s->m_v, s->csc_ptr.get(), s->csc_row.get(), s->csc_slot.get(),
+                       s->A.get(), Rv, L.work1.get(), L.Vp.get(), s->order_gather ? s->corder.get() : nullptr,
+                       L.work2.get());
+    ph.reset(new ProfRegion(ctx, "g_omega_trmm"));
     L.work3.ensure(total);
     dev_trmm_left(ctx, L.Lminv.get(), ldm, ldm, L.work2.get() + halo, ldm, re - hb, true, L.work3.get() + halo, ldm);
   }
   // U-pair (this shard's omega) and Sigma_m-pair (rank 0) kernel gradients, then one all-reduce
   std::vector<double> g(7, 0.0);
   for (int qd = 0; qd < 7; ++qd) g[qd] = rows[1 + qd];
+  ph.reset(new ProfRegion(ctx, "g_upair_sigma"));
   if (re > hb) {
     std::vector<double> gu = upair_grad(s, L.work3.get(), hb, re);
     for (int qd = 0; qd < 6; ++qd) g[1 + qd] += gu[qd];
@@ -850,6 +1006,7 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
     std::vector<double> gs = sigma_pair_grad(s, Ws);
     for (int qd = 0; qd < 6; ++qd) g[1 + qd] += gs[qd];
   }
+  ph.reset();
   allreduce_host(ctx, g);
   for (int qd = 0; qd < 7; ++qd) grad[qd] = g[qd];
 }

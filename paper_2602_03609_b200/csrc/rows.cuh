@@ -54,6 +54,9 @@ struct LagTable {
 struct RowArgs {
   int n, m_v;
   int row_begin, row_end;  // rows processed [row_begin, row_end)
+  const int32_t* order;    // optional locality schedule: the k-th row processed is order[k]
+  unsigned long long* next;  // optional: rows claimed in order from this (zeroed) counter
+  double* row_part;          // optional: per-row contributions [(i - row_begin) * 8 + q] instead of tot
   const int32_t* nbr;      // n * m_v, ascending, -1 padded
   const double *x, *y;
   const int32_t* tid;
@@ -96,9 +99,28 @@ constexpr int lfac_stride() {
 enum RowMode { kModeBuild = 0, kModeNll = 1, kModeGrad = 2, kModeVifGrad = 3 };
 
 __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
+}
+
+// Next row (schedule index) for this warp: a grid-stride step, or -- with a.next -- the next
+// unclaimed row, so the rows in flight stay a contiguous window of the schedule whatever the
+// per-row cost variations (L2 reuse of the gathered W columns).
+__device__ __forceinline__ int next_row(const RowArgs& a, int static_next, int lane) {
+  if (!a.next) return static_next;
+  int c = 0;
+  if (lane == 0) c = static_cast<int>(atomicAdd(a.next, 1ull));
+  return __shfl_sync(0xffffffffu, c, 0);
+}
+
+// Per-row reduction contribution (lane 0): into the per-row slot when a.row_part is set
+// (deterministic under dynamic claiming), else into the warp's running total.
+__device__ __forceinline__ void row_acc(const RowArgs& a, double* tot, int i, int q, double x) {
+  if (a.row_part)
+    a.row_part[static_cast<size_t>(i - a.row_begin) * 8 + q] = x;
+  else
+    tot[q] += x;
 }
 
 // Closure Gram G = W_cl^T W_cl over 32 slots (lower 8x8 tiles, mirrored) with
@@ -121,12 +143,20 @@ __device__ __forceinline__ void closure_gram_dmma(const double* __restrict__ W, 
     const int c = scol[8 * I + grp];
     colp[I] = c >= 0 ? W + static_cast<size_t>(c) * ldw + tig : nullptr;
   }
-  for (int kb = 0; kb < ldw; kb += 4) {
-    double f[4];
+  // software pipelined: the next k-step's fragments are in flight while this step's DMMAs issue
+  // (the loop is L2-latency bound otherwise).  ldw is a multiple of 8.
+  double f[4], bx = 0.0;
 #pragma unroll
-    for (int I = 0; I < 4; ++I) f[I] = colp[I] ? __ldg(colp[I] + kb) : 0.0;
+  for (int I = 0; I < 4; ++I) f[I] = colp[I] ? __ldg(colp[I]) : 0.0;
+  if (WITH_X) bx = grp == 0 ? __ldg(xcol + tig) : 0.0;
+#pragma unroll 2
+  for (int kb = 0; kb < ldw; kb += 4) {
+    const int kn = kb + 4 < ldw ? kb + 4 : kb;
+    double fn[4], bxn = 0.0;
+#pragma unroll
+    for (int I = 0; I < 4; ++I) fn[I] = colp[I] ? __ldg(colp[I] + kn) : 0.0;
     if (WITH_X) {
-      const double bx = grp == 0 ? __ldg(xcol + kb + tig) : 0.0;
+      bxn = grp == 0 ? __ldg(xcol + kn + tig) : 0.0;
 #pragma unroll
       for (int I = 0; I < 4; ++I) dmma_f64(accx[I][0], accx[I][1], f[I], bx);
     }
@@ -138,6 +168,9 @@ __device__ __forceinline__ void closure_gram_dmma(const double* __restrict__ W, 
         dmma_f64(acc[t][0], acc[t][1], f[I], f[J]);
         ++t;
       }
+#pragma unroll
+    for (int I = 0; I < 4; ++I) f[I] = fn[I];
+    bx = bxn;
   }
   int t = 0;
 #pragma unroll
@@ -184,7 +217,9 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
   for (int q = 0; q < 8; ++q) tot[q] = 0.0;
 
   const int gw = blockIdx.x * kRowWarps + w, nw = gridDim.x * kRowWarps;
-  for (int i = a.row_begin + gw; i < a.row_end; i += nw) {
+  const int nrows = a.row_end - a.row_begin;
+  for (int kr = next_row(a, gw, lane); kr < nrows; kr = next_row(a, kr + nw, lane)) {
+    const int i = a.order ? __ldg(&a.order[kr]) : a.row_begin + kr;
     // ---- closure slots ----
     int nb = -1;
     if (lane < a.m_v) nb = __ldg(&a.nbr[static_cast<size_t>(i) * a.m_v + lane]);
@@ -351,7 +386,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
     const double ri = __shfl_sync(kFull, rp, KS);
     const double u = ri - ar;
     if (a.u_out && lane == 0) a.u_out[i] = u;
-    if (lane == 0) tot[0] += log(D) + u * u / D;
+    if (lane == 0) row_acc(a, tot, i, 0, log(D) + u * u / D);
     if (!TWO) continue;
     // ---- phase D: gradient over closure pairs ----
     sAw[w][0][lane] = lane < k ? -Aval : (lane == KS ? 1.0 : 0.0);  // a~
@@ -389,9 +424,9 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
     const double s1n = 1.0 + aa, s2n = -aw;
     const double wd = cd * s1n - cu * s2n;
     if (lane == 0) {
-      tot[1] += wd;
+      row_acc(a, tot, i, 1, wd);
 #pragma unroll
-      for (int q = 0; q < 6; ++q) tot[2 + q] += g[q] + wd * a.g00[q];
+      for (int q = 0; q < 6; ++q) row_acc(a, tot, i, 2 + q, g[q] + wd * a.g00[q]);
     }
     __syncwarp();
   }
@@ -420,13 +455,31 @@ __device__ __forceinline__ void closure_x_dmma(const double* __restrict__ W, int
     const int c = scol[8 * I + grp];
     colp[I] = c >= 0 ? W + static_cast<size_t>(c) * ldw + tig : nullptr;
   }
+  // two k-steps of fragments in flight (L2-latency bound otherwise); ldw is a multiple of 8
+  double f[4], f1[4], bx, bx1;
+#pragma unroll
+  for (int I = 0; I < 4; ++I) {
+    f[I] = colp[I] ? __ldg(colp[I]) : 0.0;
+    f1[I] = colp[I] ? __ldg(colp[I] + 4) : 0.0;
+  }
+  bx = grp == 0 ? __ldg(xcol + tig) : 0.0;
+  bx1 = grp == 0 ? __ldg(xcol + 4 + tig) : 0.0;
+#pragma unroll 2
   for (int kb = 0; kb < ldw; kb += 4) {
-    const double bx = grp == 0 ? __ldg(xcol + kb + tig) : 0.0;
+    const int kn = kb + 8 < ldw ? kb + 8 : kb;
+    double fn[4];
+#pragma unroll
+    for (int I = 0; I < 4; ++I) fn[I] = colp[I] ? __ldg(colp[I] + kn) : 0.0;
+    const double bxn = grp == 0 ? __ldg(xcol + kn + tig) : 0.0;
+#pragma unroll
+    for (int I = 0; I < 4; ++I) dmma_f64(accx[I][0], accx[I][1], f[I], bx);
 #pragma unroll
     for (int I = 0; I < 4; ++I) {
-      const double f = colp[I] ? __ldg(colp[I] + kb) : 0.0;
-      dmma_f64(accx[I][0], accx[I][1], f, bx);
+      f[I] = f1[I];
+      f1[I] = fn[I];
     }
+    bx = bx1;
+    bx1 = bxn;
   }
   if (tig == 0)
 #pragma unroll
@@ -459,7 +512,9 @@ __global__ void __launch_bounds__(kRowWarps * 32) vif_grad_stored_kernel(RowArgs
 #pragma unroll
   for (int q = 0; q < 8; ++q) tot[q] = 0.0;
   const int gw = blockIdx.x * kRowWarps + w, nw = gridDim.x * kRowWarps;
-  for (int i = a.row_begin + gw; i < a.row_end; i += nw) {
+  const int nrows = a.row_end - a.row_begin;
+  for (int kr = next_row(a, gw, lane); kr < nrows; kr = next_row(a, kr + nw, lane)) {
+    const int i = a.order ? __ldg(&a.order[kr]) : a.row_begin + kr;
     int nb = -1;
     if (lane < a.m_v) nb = __ldg(&a.nbr[static_cast<size_t>(i) * a.m_v + lane]);
     const int k = __popc(__ballot_sync(kFull, nb >= 0));
@@ -540,9 +595,9 @@ __global__ void __launch_bounds__(kRowWarps * 32) vif_grad_stored_kernel(RowArgs
       for (int o = 16; o > 0; o >>= 1) g[q] += __shfl_xor_sync(kFull, g[q], o);
     const double wd = cd * (1.0 + aa) - (-aw);
     if (lane == 0) {
-      tot[1] += wd;
+      row_acc(a, tot, i, 1, wd);
 #pragma unroll
-      for (int q = 0; q < 6; ++q) tot[2 + q] += g[q] + wd * a.g00[q];
+      for (int q = 0; q < 6; ++q) row_acc(a, tot, i, 2 + q, g[q] + wd * a.g00[q]);
     }
     __syncwarp();
   }
@@ -555,6 +610,27 @@ __global__ void __launch_bounds__(kRowWarps * 32) vif_grad_stored_kernel(RowArgs
     for (int ww = 0; ww < kRowWarps; ++ww) s2 += sred[ww][threadIdx.x];
     a.part[static_cast<size_t>(blockIdx.x) * 8 + threadIdx.x] = s2;
   }
+}
+
+// Fixed-order reduction of per-row contributions: block b sums rows [b*chunk, (b+1)*chunk).
+static __global__ void __launch_bounds__(256) row_part_reduce_kernel(const double* rp, int nrows, int chunk,
+                                                                     double* part) {
+  __shared__ double red[8][256];
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int r0 = blockIdx.x * chunk, r1 = min(nrows, r0 + chunk);
+  for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s[q] += rp[static_cast<size_t>(r) * 8 + q];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) red[q][threadIdx.x] = s[q];
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x < 8) part[static_cast<size_t>(blockIdx.x) * 8 + threadIdx.x] = red[threadIdx.x][0];
 }
 
 // Sum per-block partials in a fixed order: out[q] = sum_b part[b][q] (compensated).

@@ -60,13 +60,16 @@ struct stgp_structure {
   stgp::DevLagTable lt;
   stgp::Reducer red;
   stgp::DevBuf<int> fail;
-  stgp::DevBuf<double> r, ywork, Xwork, betaw, u, scratch;
+  stgp::DevBuf<double> r, ywork, Xwork, betaw, u, scratch, row_part;
   stgp::LowRank lr;
   bool built = false;
   // CSC of B's pattern for deterministic B^T products
   bool csc_built = false;
   stgp::DevBuf<int32_t> csc_ptr, csc_row;
   stgp::DevBuf<int16_t> csc_slot;
+  // locality schedule (lowrank.cu: locality_order): rows [row_begin, row_end), columns [col_begin, row_end)
+  stgp::DevBuf<int32_t> rorder, corder;
+  bool order_rows = false, order_gather = false;
 };
 
 namespace stgp {
@@ -82,7 +85,8 @@ void prepare_tables(stgp_structure* s);
 double nll_const(int n);
 void launch_nll_stored(stgp_structure* s, int blocks, double* u_out);
 int row_blocks(stgp_ctx* ctx, int rows);
-int lfac_stride_for(int m_v);  // per-row stored closure factor size (doubles)
+int lfac_stride_for(int m_v);
+unsigned long long* claim_counter(stgp_ctx* ctx);  // zeroed in-order work counter  // per-row stored closure factor size (doubles)
 void upload_lag_table(DevLagTable& d, const TimeIndex& ti, const Params& p, const LagPolicy& pol,
                       cudaStream_t s, bool index_changed);
 LagTable lag_view(const DevLagTable& d);

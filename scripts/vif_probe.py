@@ -28,3 +28,8 @@ reps = int(sys.argv[6]) if len(sys.argv) > 6 else 3
 for rep in range(reps):
     t4 = time.perf_counter(); v, g = S.evaluate(s, theta); t5 = time.perf_counter()
     print(f"eval {rep}: {t5-t4:.3f}s nll={v:.6f} rows={ctx.profile_get('rows')} vifgrad={ctx.profile_get('rows_vifgrad')}", flush=True)
+    if rep == 0:
+        ctx.profile_reset()  # first evaluation allocates the work pool
+prof = ctx.profile_all()
+for k, (ms, cnt) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
+    print(f"  {k:16s} {ms / max(cnt, 1):9.2f} ms/call x{cnt}")

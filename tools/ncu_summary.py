@@ -21,8 +21,14 @@ def main(rep, nrows=None):
     h = next(r)
     mi, vi, ui = h.index('Metric Name'), h.index('Metric Value'), h.index('Metric Unit')
     ki = h.index('Kernel Name')
+    idi = h.index('ID')
     kern = None
+    first_id = None
     for row in r:
+        if first_id is None:
+            first_id = row[idi]
+        if row[idi] != first_id:
+            continue  # first captured launch only
         kern = row[ki]
         if row[mi] in KEEP:
             out.append(f"{row[mi]}: {row[vi]} {row[ui]}")
@@ -42,7 +48,9 @@ def main(rep, nrows=None):
     agg = collections.defaultdict(lambda: [0, 0])
     tot = [0, 0]
     for row in sass[2:]:
-        if len(row) <= ii:
+        if row and row[0] == 'Kernel Name':
+            break  # first captured launch only
+        if len(row) <= ii or not row[ii].isdigit():
             continue
         op = row[si].strip().split()
         if not op:
