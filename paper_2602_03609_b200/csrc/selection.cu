@@ -11,6 +11,8 @@
 //   * w_i.w_j: register-tiled Gram whose K loop runs sequentially per element.
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 
@@ -243,11 +245,13 @@ __global__ void tile_stats_kernel(const double* resid, const int32_t* degen, con
 
 constexpr int kQT = 64;   // queries per CTA
 constexpr int kCT = 64;   // candidates per tile
-constexpr int kKC = 16;   // K chunk
+constexpr int kKC = 16;   // K chunk staged per pipeline stage
+constexpr int kKS = kKC + 4;  // smem row stride (doubles): conflict-free DMMA fragment loads
+constexpr int kStages = 3;
 constexpr int kDrThreads = 256;
 
 struct DrArgs {
-  int n, m_v, M, ldm;
+  int n, m_v, M, ldm;  // ldm: multiple of kKC, rows [M, ldm) of W are zero
   const double *x, *y, *W, *resid;
   const int32_t *tid, *degen;
   DevKernel k;
@@ -258,25 +262,46 @@ struct DrArgs {
   const int *tmin, *tmax, *hasdeg;
   const double *wmax, *rmin;
   double s1;
+  unsigned long long* stats;  // optional: [0] candidate tiles evaluated, [1] tiles pruned
 };
 
-// Tiled exact d_r top-m over predecessors.  CTA = 64 consecutive queries; each
-// 64-candidate tile's Gram W_Q^T W_C is computed with a sequential fma chain per
-// element (4 x 4 register tile per thread), the epilogue forms d_r and the warps
-// merge the tile into per-query top-m lists kept in shared memory.
-constexpr size_t kDrSmem = sizeof(double) * (kQT * (kCT + 1) + kQT * 32) + sizeof(int) * kQT * 32;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+// Tiled exact d_r top-m over predecessors.  CTA = 64 consecutive queries; for each 64-candidate
+// tile the Gram W_Q^T W_C is formed on the FP64 tensor pipe: mma.m8n8k4.f64 evaluates each
+// element as the sequential fma chain over k (verified bit-identical on sm_100a,
+// scripts/exp/dmma_order.cu), so G equals the oracle's chain exactly.  W chunks of kKC rows are
+// staged by cp.async in a kStages ring; warp w owns the 16 x 32 sub-tile (rows 16 (w/2), cols
+// 32 (w%2)).  The epilogue forms d_r, the warps merge the tile into per-query top-m lists.
+constexpr size_t kDrStageDoubles = 2 * kQT * kKS;
+constexpr size_t kDrSmem =
+    sizeof(double) * (kStages * kDrStageDoubles + kQT * 32) + sizeof(int) * kQT * 32;
+static_assert(kStages * kDrStageDoubles >= kQT * (kCT + 1), "distance tile aliases the stages");
 
 __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
   extern __shared__ double sm[];
-  // the Gram staging tiles and the distance tile are never live together
-  double (*sWq)[kQT + 1] = reinterpret_cast<double (*)[kQT + 1]>(sm);
-  double (*sWc)[kCT + 1] = reinterpret_cast<double (*)[kCT + 1]>(sm + kKC * (kQT + 1));
+  // the staging ring and the distance tile are never live together
+  double* ring = sm;
   double (*sd)[kCT + 1] = reinterpret_cast<double (*)[kCT + 1]>(sm);
-  double (*topd)[32] = reinterpret_cast<double (*)[32]>(sm + kQT * (kCT + 1));
-  int (*topj)[32] = reinterpret_cast<int (*)[32]>(sm + kQT * (kCT + 1) + kQT * 32);
+  double (*topd)[32] = reinterpret_cast<double (*)[32]>(sm + kStages * kDrStageDoubles);
+  int (*topj)[32] = reinterpret_cast<int (*)[32]>(sm + kStages * kDrStageDoubles + kQT * 32);
   const int q0 = blockIdx.x * kQT;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int tq = (tid / 16) * 4, tc = (tid % 16) * 4;  // thread tile origin
+  const int grp = lane >> 2, tig = lane & 3;
+  const int wr = wid >> 1, wc = wid & 1;  // warp sub-tile: rows 16 wr.., cols 32 wc..
   for (int e = tid; e < kQT * 32; e += kDrThreads) {
     topd[e / 32][e % 32] = __longlong_as_double(0x7ff0000000000000LL);
     topj[e / 32][e % 32] = INT_MAX;
@@ -285,6 +310,10 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
   __shared__ double s_dmax[kDrThreads / 32];
   __shared__ int s_prune;
   const int qtile = q0 / kQT;
+  const int nch = a.ldm / kKC;
+  // staging: thread copies 16 B pieces; a tile column chunk is kKC doubles = kKC/2 pieces
+  constexpr int kPieces = 2 * kQT * (kKC / 2);  // Q and C
+  static_assert(kPieces % kDrThreads == 0, "staging split");
   // candidate tiles nearest-first: tight thresholds early, then exact pruning of far tiles
   for (int c0 = ((qmax - 2) / kCT) * kCT; c0 >= 0; c0 -= kCT) {
     {
@@ -316,64 +345,87 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
           if (cmax < 1.0 && (1.0 - cmax) - 1e-12 > d * d) prune = 1;
         }
         s_prune = prune;
+        if (a.stats) atomicAdd(&a.stats[prune], 1ull);
       }
       __syncthreads();
       if (s_prune) continue;
     }
-    double g[4][4];
+    double acc[2][4][2];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < 2; ++u)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) g[u][v] = 0.0;
-    for (int k0 = 0; k0 < a.M; k0 += kKC) {
-      __syncthreads();
-      for (int e = tid; e < kKC * kQT; e += kDrThreads) {
-        const int kk = e % kKC, qq = e / kKC;
-        const int i = min(q0 + qq, a.n - 1), j = min(c0 + qq, a.n - 1);
-        const bool in = k0 + kk < a.M;
-        sWq[kk][qq] = in ? a.W[static_cast<size_t>(i) * a.ldm + k0 + kk] : 0.0;
-        sWc[kk][qq] = in ? a.W[static_cast<size_t>(j) * a.ldm + k0 + kk] : 0.0;
+      for (int v = 0; v < 4; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
+    if (a.M > 0) {
+      auto stage = [&](int ch) {
+        double* sQ = ring + static_cast<size_t>(ch % kStages) * kDrStageDoubles;
+        double* sC = sQ + kQT * kKS;
+#pragma unroll
+        for (int it = 0; it < kPieces / kDrThreads; ++it) {
+          const int pc = tid + it * kDrThreads;
+          const int which = pc / (kQT * (kKC / 2));  // 0: Q, 1: C
+          const int rem = pc % (kQT * (kKC / 2));
+          const int col = rem / (kKC / 2), piece = rem % (kKC / 2);
+          const int g = min((which ? c0 : q0) + col, a.n - 1);
+          cp_async16((which ? sC : sQ) + col * kKS + 2 * piece,
+                     a.W + static_cast<size_t>(g) * a.ldm + static_cast<size_t>(ch) * kKC + 2 * piece);
+        }
+      };
+#pragma unroll
+      for (int ch = 0; ch < kStages - 1; ++ch) {
+        if (ch < nch) stage(ch);
+        cp_async_commit();
       }
-      __syncthreads();
-      const int kn = min(kKC, a.M - k0);
-      for (int kk = 0; kk < kn; ++kk) {
-        double wq[4], wc[4];
+      for (int ch = 0; ch < nch; ++ch) {
+        cp_async_wait<kStages - 2>();
+        __syncthreads();  // chunk ch visible; the stage about to be refilled is no longer read
+        if (ch + kStages - 1 < nch) stage(ch + kStages - 1);
+        cp_async_commit();
+        const double* sQ = ring + static_cast<size_t>(ch % kStages) * kDrStageDoubles;
+        const double* sC = sQ + kQT * kKS;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) wq[u] = sWq[kk][tq + u];
+        for (int kb = 0; kb < kKC; kb += 4) {
+          double fa[2], fb[4];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) wc[v] = sWc[kk][tc + v];
+          for (int u = 0; u < 2; ++u) fa[u] = sQ[(16 * wr + 8 * u + grp) * kKS + kb + tig];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+          for (int v = 0; v < 4; ++v) fb[v] = sC[(32 * wc + 8 * v + grp) * kKS + kb + tig];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) g[u][v] = __fma_rn(wq[u], wc[v], g[u][v]);
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) dmma_f64(acc[u][v][0], acc[u][v][1], fa[u], fb[v]);
+        }
       }
+      cp_async_wait<0>();
     }
-    // epilogue: d_r for the thread's 4 x 4 pairs (sd aliases the staging tiles)
+    // epilogue: d_r for the thread's 16 pairs (sd aliases the staging ring)
     __syncthreads();
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < 2; ++u)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int i = q0 + tq + u, j = c0 + tc + v;
-        double d = __longlong_as_double(0x7ff0000000000000LL);
-        if (i < a.n && j < i) {
-          if (a.degen[i] || a.degen[j]) {
-            d = 1.0;
-          } else {
-            double pe, pb;
-            a.lt.get2(a.tid[i], a.tid[j], pe, pb);
-            TF f;
-            f.pow_mE = pe;
-            f.pow_mbh = pb;
-            double rho = gneiting_eval(a.k, spatial_dist(a.x[i], a.y[i], a.x[j], a.y[j]), f);
-            if (a.M > 0) rho = __dsub_rn(rho, g[u][v]);
-            const double rad =
-                __dsub_rn(1.0, __ddiv_rn(fabs(rho), __dsqrt_rn(__dmul_rn(a.resid[i], a.resid[j]))));
-            d = __dsqrt_rn(rad < 0.0 ? 0.0 : rad);
+      for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int qq = 16 * wr + 8 * u + grp, cc = 32 * wc + 8 * v + 2 * tig + h;
+          const int i = q0 + qq, j = c0 + cc;
+          double d = __longlong_as_double(0x7ff0000000000000LL);
+          if (i < a.n && j < i) {
+            if (a.degen[i] || a.degen[j]) {
+              d = 1.0;
+            } else {
+              double pe, pb;
+              a.lt.get2(a.tid[i], a.tid[j], pe, pb);
+              TF f;
+              f.pow_mE = pe;
+              f.pow_mbh = pb;
+              double rho = gneiting_eval(a.k, spatial_dist(a.x[i], a.y[i], a.x[j], a.y[j]), f);
+              if (a.M > 0) rho = __dsub_rn(rho, acc[u][v][h]);
+              const double rad =
+                  __dsub_rn(1.0, __ddiv_rn(fabs(rho), __dsqrt_rn(__dmul_rn(a.resid[i], a.resid[j]))));
+              d = __dsqrt_rn(rad < 0.0 ? 0.0 : rad);
+            }
           }
+          sd[qq][cc] = d;
         }
-        sd[tq + u][tc + v] = d;
-      }
     __syncthreads();
     // merge: warp wid handles queries wid, wid + 8, ...
     for (int qq = wid; qq < kQT; qq += kDrThreads / 32) {
@@ -469,8 +521,9 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
     dzx.upload(zx.data(), M, st);
     dzy.upload(zy.data(), M, st);
     dzt.upload(ztid.data(), M, st);
-    const int ldm = std::max(1, M);
+    const int ldm = std::max(kKC, (M + kKC - 1) / kKC * kKC);  // zero rows [M, ldm): exact extra fma(0, 0, g)
     DevBuf<double> W(static_cast<size_t>(ldm) * n), resid(n);
+    STGP_CUDA(cudaMemsetAsync(W.get(), 0, sizeof(double) * ldm * n, st));
     DevBuf<int32_t> degen(n);
     {
       ProfRegion pr(ctx, "dr_whiten");
@@ -545,11 +598,23 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
       a.s1 = p.sigma1_2;
       // pruning needs time-sorted rows (tile time ranges); otherwise plain brute force
       if (!ds->time_sorted) a.tmin = nullptr;
+      DevBuf<unsigned long long> stats;
+      if (std::getenv("STGP_DR_STATS")) {  // diagnostics: tile pairs evaluated / pruned
+        stats.alloc(2);
+        STGP_CUDA(cudaMemsetAsync(stats.get(), 0, 16, st));
+        a.stats = stats.get();
+      }
       ProfRegion pr(ctx, "knn_dr");
       STGP_CUDA(cudaFuncSetAttribute(knn_dr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kDrSmem)));
       knn_dr_kernel<<<ceil_div(n, kQT), kDrThreads, kDrSmem, st>>>(a);
       launched(ctx);
+      if (a.stats) {
+        unsigned long long h[2];
+        STGP_CUDA(cudaMemcpyAsync(h, a.stats, 16, cudaMemcpyDeviceToHost, st));
+        STGP_CUDA(cudaStreamSynchronize(st));
+        std::fprintf(stderr, "[stgp] d_r tiles: evaluated %llu pruned %llu\n", h[0], h[1]);
+      }
     }
     STGP_CUDA(cudaStreamSynchronize(st));
     prof_collect(ctx);
