@@ -197,19 +197,37 @@ __global__ void resid_kernel(const double* W, int M, int ldm, int n, double s1, 
   }
 }
 
-// Per 64-row tile: time-id range, max |w| and min r over non-degenerate rows, degenerate flag.
-__global__ void tile_stats_kernel(const double* resid, const int32_t* degen, const int32_t* tid, int n, double s1,
-                                  int* tmin, int* tmax, double* wmax, double* rmin, int* hasdeg) {
+// Spatial tiles of the d_r search: tile t holds rows sp[tile_off[t] .. tile_off[t+1]) (<= 64, one
+// time bucket, Morton order).  Per tile: time-id range, bounding box, max |w| and min r over
+// non-degenerate rows, degenerate flag, row-index range.
+struct DrTiles {
+  const int32_t *sp, *off, *bucket, *b_tile0, *b_tmax;
+  const uint32_t* key;  // Morton key of the tile's first row (nondecreasing within a bucket)
+  int *tmin, *tmax, *hasdeg, *imin, *imax;
+  double *bx0, *bx1, *by0, *by1, *wmax, *rmin;
+  // block-norm bound of the low-rank term: inducing points are split into G groups (inducing time x
+  // spatial cell); A[t * G + g] = max over the tile's non-degenerate rows of |w_i[g]| / sqrt(r_i),
+  // so |w_i . w_j| / sqrt(r_i r_j) <= sum_g A_Q[g] A_C[g].  Apre / rpre: prefix (buckets <= b) max / min.
+  int G;
+  double *A, *Apre, *rpre;
+};
+
+__global__ void tile_stats_kernel(DrTiles T, const double* x, const double* y, const double* resid,
+                                  const int32_t* degen, const int32_t* tid, double s1) {
   const int tile = blockIdx.x;
-  const int i0 = tile * 64, i1 = min(n, i0 + 64);
-  __shared__ double sw[64], sr[64];
-  __shared__ int smn[64], smx[64], sdg[64];
+  const int p0 = T.off[tile], p1 = T.off[tile + 1];
+  __shared__ double sw[64], sr[64], sx0[64], sx1[64], sy0[64], sy1[64];
+  __shared__ int smn[64], smx[64], sdg[64], sim[64], six[64];
   const int t = threadIdx.x;
-  const int i = i0 + t;
-  double w = 0.0, r = __longlong_as_double(0x7ff0000000000000LL);
-  int mn = INT_MAX, mx = -1, dg = 0;
-  if (i < i1) {
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  double w = 0.0, r = inf, x0 = inf, x1 = -inf, y0 = inf, y1 = -inf;
+  int mn = INT_MAX, mx = -1, dg = 0, im = INT_MAX, ix = -1;
+  if (p0 + t < p1) {
+    const int i = T.sp[p0 + t];
     mn = mx = tid[i];
+    im = ix = i;
+    x0 = x1 = x[i];
+    y0 = y1 = y[i];
     if (degen[i]) {
       dg = 1;
     } else {
@@ -217,29 +235,72 @@ __global__ void tile_stats_kernel(const double* resid, const int32_t* degen, con
       w = s1 - resid[i];
     }
   }
-  sw[t] = w;
-  sr[t] = r;
-  smn[t] = mn;
-  smx[t] = mx;
-  sdg[t] = dg;
+  sw[t] = w; sr[t] = r; sx0[t] = x0; sx1[t] = x1; sy0[t] = y0; sy1[t] = y1;
+  smn[t] = mn; smx[t] = mx; sdg[t] = dg; sim[t] = im; six[t] = ix;
   __syncthreads();
   for (int o = 32; o > 0; o >>= 1) {
     if (t < o) {
       sw[t] = fmax(sw[t], sw[t + o]);
       sr[t] = fmin(sr[t], sr[t + o]);
+      sx0[t] = fmin(sx0[t], sx0[t + o]);
+      sx1[t] = fmax(sx1[t], sx1[t + o]);
+      sy0[t] = fmin(sy0[t], sy0[t + o]);
+      sy1[t] = fmax(sy1[t], sy1[t + o]);
       smn[t] = min(smn[t], smn[t + o]);
       smx[t] = max(smx[t], smx[t + o]);
       sdg[t] = sdg[t] | sdg[t + o];
+      sim[t] = min(sim[t], sim[t + o]);
+      six[t] = max(six[t], six[t + o]);
     }
     __syncthreads();
   }
   if (t == 0) {
     // |w|^2 = s1 - r up to one rounding of s1 (bounded by the 1e-11 factor of the prune test)
-    wmax[tile] = sqrt(fmax(sw[0], 0.0) + 1e-15 * s1);
-    rmin[tile] = sr[0];
-    tmin[tile] = smn[0];
-    tmax[tile] = smx[0];
-    hasdeg[tile] = sdg[0];
+    T.wmax[tile] = sqrt(fmax(sw[0], 0.0) + 1e-15 * s1);
+    T.rmin[tile] = sr[0];
+    T.tmin[tile] = smn[0];
+    T.tmax[tile] = smx[0];
+    T.hasdeg[tile] = sdg[0];
+    T.bx0[tile] = sx0[0];
+    T.bx1[tile] = sx1[0];
+    T.by0[tile] = sy0[0];
+    T.by1[tile] = sy1[0];
+    T.imin[tile] = sim[0];
+    T.imax[tile] = six[0];
+  }
+}
+
+constexpr int kMaxGroups = 48;
+
+// A[tile][g] (see DrTiles): warp per row, lanes over k, group sums of squares in shared memory.
+__global__ void __launch_bounds__(256) tile_groups_kernel(DrTiles T, const double* W, int ldm, int M,
+                                                          const int32_t* kgroup, const double* resid,
+                                                          const int32_t* degen) {
+  __shared__ double sN[8][kMaxGroups], sA[8][kMaxGroups];
+  const int tile = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p0 = T.off[tile], p1 = T.off[tile + 1], G = T.G;
+  for (int g = lane; g < G; g += 32) sA[w][g] = 0.0;
+  for (int q = p0 + w; q < p1; q += 8) {
+    const int i = T.sp[q];
+    for (int g = lane; g < G; g += 32) sN[w][g] = 0.0;
+    __syncwarp();
+    const double* col = W + static_cast<size_t>(i) * ldm;
+    for (int k = lane; k < M; k += 32) {
+      const double v = col[k];
+      atomicAdd(&sN[w][kgroup[k]], v * v);
+    }
+    __syncwarp();
+    if (!degen[i]) {
+      const double inv = 1.0 / sqrt(resid[i]);
+      for (int g = lane; g < G; g += 32) sA[w][g] = fmax(sA[w][g], sqrt(sN[w][g]) * inv * (1.0 + 1e-12));
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    double m = 0.0;
+    for (int w2 = 0; w2 < 8; ++w2) m = fmax(m, sA[w2][g]);
+    T.A[static_cast<size_t>(tile) * G + g] = m;
   }
 }
 
@@ -258,9 +319,8 @@ struct DrArgs {
   LagTable lt;
   int32_t* out;
   double* dist;
-  // exact tile pruning
-  const int *tmin, *tmax, *hasdeg;
-  const double *wmax, *rmin;
+  DrTiles T;
+  int prune;                  // exact tile pruning (time-sorted rows)
   double s1;
   unsigned long long* stats;  // optional: [0] candidate tiles evaluated, [1] tiles pruned
 };
@@ -280,12 +340,54 @@ __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, doubl
       : "d"(a), "d"(b));
 }
 
-// Tiled exact d_r top-m over predecessors.  CTA = 64 consecutive queries; for each 64-candidate
-// tile the Gram W_Q^T W_C is formed on the FP64 tensor pipe: mma.m8n8k4.f64 evaluates each
-// element as the sequential fma chain over k (verified bit-identical on sm_100a,
-// scripts/exp/dmma_order.cu), so G equals the oracle's chain exactly.  W chunks of kKC rows are
-// staged by cp.async in a kStages ring; warp w owns the 16 x 32 sub-tile (rows 16 (w/2), cols
-// 32 (w%2)).  The epilogue forms d_r, the warps merge the tile into per-query top-m lists.
+// Upper bound of |rho_r| over the pairs of query tile Q and candidate tile C:
+//   |k - w_i.w_j| / sqrt(r_i r_j) <= s1 T(u_min)^-E Matern(c h_min T(u_max)^-beta/2) / sqrt(rmin_Q rmin_C)
+//                                    + sum_g A_Q[g] A_C[g]
+// (T(u) and Matern are decreasing; h_min = box-to-box distance; degenerate rows excluded: they sit
+// at d = 1).
+__device__ __forceinline__ double tile_cmax(const DrArgs& a, int tminQ, int tmaxQ, double qx0, double qx1,
+                                            double qy0, double qy1, const double* AQ, double rQ, int ct) {
+  const DrTiles& T = a.T;
+  // lags: C's times precede or equal Q's (time-sorted rows, j < i)
+  const int tc0 = T.tmin[ct], tc1 = T.tmax[ct];
+  double pe_min, pb_dummy, pe_dummy, pb_max;
+  if (tc1 >= tminQ) {  // time ranges touch: u_min = 0
+    pe_min = 1.0;
+  } else {
+    a.lt.get2(tminQ, tc1, pe_min, pb_dummy);
+  }
+  a.lt.get2(tmaxQ, tc0, pe_dummy, pb_max);
+  double mat = 1.0;
+  if (a.k.nu_code >= 0) {
+    const double dx = fmax(0.0, fmax(T.bx0[ct] - qx1, qx0 - T.bx1[ct]));
+    const double dy = fmax(0.0, fmax(T.by0[ct] - qy1, qy0 - T.by1[ct]));
+    const double hmin = sqrt(dx * dx + dy * dy) * (1.0 - 1e-12);
+    const double xm = a.k.c * hmin * pb_max * (1.0 - 1e-12);
+    mat = matern_from_exp(xm, exp(-xm), a.k.nu_code);
+  }
+  double wt = 0.0;
+  const double* AC = T.A + static_cast<size_t>(ct) * T.G;
+  for (int g = 0; g < T.G; ++g) wt += AQ[g] * AC[g];
+  return (a.s1 * pe_min * mat / sqrt(rQ * T.rmin[ct]) + wt) * (1.0 + 1e-11);
+}
+
+// the worst current list entry over the tile's (non-degenerate) queries; inf while any list is short
+__device__ __forceinline__ double tile_threshold(const double (*topd)[32], const int* qm) {
+  double d = 0.0;
+  for (int qq = 0; qq < kQT; ++qq)
+    if (qm[qq] > 0) d = fmax(d, topd[qq][qm[qq] - 1]);
+  return d;
+}
+
+// Exact d_r top-m over predecessors on spatial tiles.  CTA = one query tile (<= 64 rows of one time
+// bucket, Morton order).  Candidate tiles are visited bucket by bucket backwards in time, each
+// bucket outward from the tile nearest to the query tile; warp 0 tests 32 candidates at a time
+// against the current thresholds (a bound that cannot beat the worst current list entry prunes the
+// tile exactly), and the whole scan stops at the first bucket whose time lag alone prunes it.
+// Survivors get the Gram W_Q^T W_C on the FP64 tensor pipe: mma.m8n8k4.f64 evaluates each element
+// as the sequential fma chain over k (verified bit-identical on sm_100a, scripts/exp/dmma_order.cu),
+// so G equals the oracle's chain exactly.  W chunks of kKC rows are staged by cp.async in a
+// kStages ring; warp w owns the 16 x 32 sub-tile (rows 16 (w/2), cols 32 (w%2)).
 constexpr size_t kDrStageDoubles = 2 * kQT * kKS;
 constexpr size_t kDrSmem =
     sizeof(double) * (kStages * kDrStageDoubles + kQT * 32) + sizeof(int) * kQT * 32;
@@ -298,7 +400,13 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
   double (*sd)[kCT + 1] = reinterpret_cast<double (*)[kCT + 1]>(sm);
   double (*topd)[32] = reinterpret_cast<double (*)[32]>(sm + kStages * kDrStageDoubles);
   int (*topj)[32] = reinterpret_cast<int (*)[32]>(sm + kStages * kDrStageDoubles + kQT * 32);
-  const int q0 = blockIdx.x * kQT;
+  __shared__ int qidx[kQT], cidx[kCT], qm[kQT], qemit[kQT];
+  __shared__ double s_dmax[kDrThreads / 32];
+  __shared__ int s_surv[32], s_nsurv, s_skip;
+  __shared__ double s_d;
+  __shared__ double sAQ[kMaxGroups];
+  const DrTiles& T = a.T;
+  const int qt = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int grp = lane >> 2, tig = lane & 3;
   const int wr = wid >> 1, wc = wid & 1;  // warp sub-tile: rows 16 wr.., cols 32 wc..
@@ -306,155 +414,257 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
     topd[e / 32][e % 32] = __longlong_as_double(0x7ff0000000000000LL);
     topj[e / 32][e % 32] = INT_MAX;
   }
-  const int qmax = min(q0 + kQT, a.n);
-  __shared__ double s_dmax[kDrThreads / 32];
-  __shared__ int s_prune;
-  const int qtile = q0 / kQT;
+  const int qp0 = T.off[qt], qn = T.off[qt + 1] - qp0;
+  if (tid < kQT) {
+    const int i = tid < qn ? T.sp[qp0 + tid] : -1;
+    qidx[tid] = i;
+    qemit[tid] = i >= 0 ? min(a.m_v, i) : 0;
+    // a degenerate query has d = 1 to every predecessor: its list is the m smallest indices
+    qm[tid] = (i >= 0 && !a.degen[i]) ? min(a.m_v, i) : 0;
+  }
+  for (int g = tid; g < T.G; g += kDrThreads) sAQ[g] = T.A[static_cast<size_t>(qt) * T.G + g];
+  __syncthreads();
+  for (int e = tid; e < kQT * 32; e += kDrThreads) {
+    const int qq = e / 32, l = e % 32, i = qidx[qq];
+    if (i >= 0 && a.degen[i] && l < qemit[qq]) {
+      topd[qq][l] = 1.0;
+      topj[qq][l] = l;
+    }
+  }
+  const int qb = T.bucket[qt];
+  const int tminQ = T.tmin[qt], tmaxQ = T.tmax[qt], imaxQ = T.imax[qt];
+  const double qx0 = T.bx0[qt], qx1 = T.bx1[qt], qy0 = T.by0[qt], qy1 = T.by1[qt];
+  const double rQ = T.rmin[qt];
+  const bool can_prune = a.prune != 0;
+  const uint32_t qkey = T.key[qt];
   const int nch = a.ldm / kKC;
-  // staging: thread copies 16 B pieces; a tile column chunk is kKC doubles = kKC/2 pieces
-  constexpr int kPieces = 2 * kQT * (kKC / 2);  // Q and C
+  constexpr int kPieces = 2 * kQT * (kKC / 2);  // Q and C, 16 B each
   static_assert(kPieces % kDrThreads == 0, "staging split");
-  // candidate tiles nearest-first: tight thresholds early, then exact pruning of far tiles
-  for (int c0 = ((qmax - 2) / kCT) * kCT; c0 >= 0; c0 -= kCT) {
-    {
+  __syncthreads();
+
+  // phase 0 seeds the lists with the 2 kSeed + 1 nearest tiles of this and the previous bucket
+  // (queries early in their bucket have few same-bucket predecessors, so thresholds would stay
+  // infinite through the whole same-bucket scan); phase 1 is the pruned traversal, skipping seeds.
+  constexpr int kSeed = 1;
+  for (int phase = 0; phase < 2; ++phase)
+  for (int b = qb; b >= 0; --b) {
+    if (phase == 0 && b < qb - 1) break;
+    const int t0 = T.b_tile0[b], t1 = T.b_tile0[b + 1];
+    int p = qt;
+    if (b != qb) {  // nearest tile by Morton key
+      int lo = t0, hi = t1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (T.key[mid] < qkey) lo = mid + 1; else hi = mid;
+      }
+      p = min(lo, t1 - 1);
+    }
+    const int R = max(p - t0, t1 - 1 - p);
+    const bool seeded = b >= qb - 1;
+    const int s_first = (phase == 1 && seeded) ? 2 * kSeed + 1 : 0;
+    const int s_last = phase == 0 ? min(2 * kSeed, 2 * R) : 2 * R;
+    bool stop = false;
+    for (int s0 = s_first; s0 <= s_last && !stop; s0 += 32) {
       // current worst threshold over the tile's queries (inf while any list is short)
-      double dm = 0.0;
-      for (int qq = tid; qq < kQT; qq += kDrThreads) {
-        const int i = q0 + qq;
-        if (i >= a.n) continue;
-        const int m = min(a.m_v, i);
-        if (m > 0) dm = fmax(dm, topd[qq][m - 1]);
-      }
+      {
+        double dm = 0.0;
+        for (int qq = tid; qq < kQT; qq += kDrThreads)
+          if (qm[qq] > 0) dm = fmax(dm, topd[qq][qm[qq] - 1]);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(kFull, dm, o));
-      if (lane == 0) s_dmax[wid] = dm;
-      __syncthreads();
-      if (tid == 0) {
-        double d = 0.0;
-        for (int w2 = 0; w2 < kDrThreads / 32; ++w2) d = fmax(d, s_dmax[w2]);
-        const int ct = c0 / kCT;
-        int prune = 0;
-        if (a.tmin && d < 1.0 && ct != qtile && !a.hasdeg[qtile]) {
-          // rows are time sorted and C precedes Q, so the smallest lag is T(tmin_Q) - T(tmax_C).
-          // |rho_r| <= |k| + |w_i||w_j| <= s1 T(u_min)^{-(delta+beta)} + wmax_Q wmax_C (non-degenerate
-          // candidates; degenerate ones sit at d = 1 > d).  rmin_C = inf when all are degenerate.
+        for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(kFull, dm, o));
+        if (lane == 0) s_dmax[wid] = dm;
+        __syncthreads();
+        if (tid == 0) {
+          double d = 0.0;
+          for (int w2 = 0; w2 < kDrThreads / 32; ++w2) d = fmax(d, s_dmax[w2]);
+          s_d = d;
+        }
+        __syncthreads();
+      }
+      const double d = s_d;
+      if (wid == 0) {
+        // bucket-level stop: the time lag alone prunes this and every earlier bucket
+        bool stop_b = false;
+        if (phase == 1 && can_prune && b != qb && s0 == s_first && d < 1.0) {
           double pe, pb;
-          a.lt.get2(a.tmin[qtile], a.tmax[ct], pe, pb);
-          const double cmax =
-              (a.s1 * pe + a.wmax[qtile] * a.wmax[ct]) * (1.0 + 1e-11) / sqrt(a.rmin[qtile] * a.rmin[ct]);
-          if (cmax < 1.0 && (1.0 - cmax) - 1e-12 > d * d) prune = 1;
+          a.lt.get2(tminQ, T.b_tmax[b], pe, pb);
+          double wt = 0.0;
+          const double* Ab = T.Apre + static_cast<size_t>(b) * T.G;
+          for (int g = 0; g < T.G; ++g) wt += sAQ[g] * Ab[g];
+          const double cb = (a.s1 * pe / sqrt(rQ * T.rpre[b]) + wt) * (1.0 + 1e-11);
+          stop_b = cb < 1.0 && (1.0 - cb) - 1e-12 > d * d;
         }
-        s_prune = prune;
-        if (a.stats) atomicAdd(&a.stats[prune], 1ull);
+        const int s = s0 + lane;
+        const int off = (s & 1) ? -((s + 1) >> 1) : (s >> 1);
+        const int ct = p + off;
+        bool take = !stop_b && s <= s_last && ct >= t0 && ct < t1 && T.imin[ct] < imaxQ;
+        int pruned = 0;
+        if (take && phase == 1 && can_prune && d < 1.0) {
+          const double cmax = tile_cmax(a, tminQ, tmaxQ, qx0, qx1, qy0, qy1, sAQ, rQ, ct);
+          if (cmax < 1.0 && (1.0 - cmax) - 1e-12 > d * d) {
+            take = false;
+            pruned = 1;
+          }
+        }
+        const unsigned mk = __ballot_sync(kFull, take);
+        if (take) s_surv[__popc(mk & ((1u << lane) - 1))] = ct;
+        if (lane == 0) {
+          s_nsurv = stop_b ? -1 : __popc(mk);
+          if (a.stats) {
+            atomicAdd(&a.stats[0], static_cast<unsigned long long>(__popc(mk)));
+            const int lg = min(qb - b, 15);
+            atomicAdd(&a.stats[2 + lg], static_cast<unsigned long long>(__popc(mk)));
+            if (stop_b) atomicAdd(&a.stats[34 + lg], 1ull);
+          }
+        }
+        if (a.stats) {
+          const unsigned pk = __ballot_sync(kFull, pruned);
+          if (lane == 0 && pk) {
+            atomicAdd(&a.stats[1], static_cast<unsigned long long>(__popc(pk)));
+            atomicAdd(&a.stats[18 + min(qb - b, 15)], static_cast<unsigned long long>(__popc(pk)));
+          }
+        }
       }
       __syncthreads();
-      if (s_prune) continue;
-    }
-    double acc[2][4][2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
-    if (a.M > 0) {
-      auto stage = [&](int ch) {
-        double* sQ = ring + static_cast<size_t>(ch % kStages) * kDrStageDoubles;
-        double* sC = sQ + kQT * kKS;
-#pragma unroll
-        for (int it = 0; it < kPieces / kDrThreads; ++it) {
-          const int pc = tid + it * kDrThreads;
-          const int which = pc / (kQT * (kKC / 2));  // 0: Q, 1: C
-          const int rem = pc % (kQT * (kKC / 2));
-          const int col = rem / (kKC / 2), piece = rem % (kKC / 2);
-          const int g = min((which ? c0 : q0) + col, a.n - 1);
-          cp_async16((which ? sC : sQ) + col * kKS + 2 * piece,
-                     a.W + static_cast<size_t>(g) * a.ldm + static_cast<size_t>(ch) * kKC + 2 * piece);
-        }
-      };
-#pragma unroll
-      for (int ch = 0; ch < kStages - 1; ++ch) {
-        if (ch < nch) stage(ch);
-        cp_async_commit();
+      const int nsurv = s_nsurv;
+      if (nsurv < 0) {
+        stop = true;
+        break;
       }
-      for (int ch = 0; ch < nch; ++ch) {
-        cp_async_wait<kStages - 2>();
-        __syncthreads();  // chunk ch visible; the stage about to be refilled is no longer read
-        if (ch + kStages - 1 < nch) stage(ch + kStages - 1);
-        cp_async_commit();
-        const double* sQ = ring + static_cast<size_t>(ch % kStages) * kDrStageDoubles;
-        const double* sC = sQ + kQT * kKS;
-#pragma unroll
-        for (int kb = 0; kb < kKC; kb += 4) {
-          double fa[2], fb[4];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) fa[u] = sQ[(16 * wr + 8 * u + grp) * kKS + kb + tig];
-#pragma unroll
-          for (int v = 0; v < 4; ++v) fb[v] = sC[(32 * wc + 8 * v + grp) * kKS + kb + tig];
-#pragma unroll
-          for (int u = 0; u < 2; ++u)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) dmma_f64(acc[u][v][0], acc[u][v][1], fa[u], fb[v]);
-        }
-      }
-      cp_async_wait<0>();
-    }
-    // epilogue: d_r for the thread's 16 pairs (sd aliases the staging ring)
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-      for (int v = 0; v < 4; ++v)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int qq = 16 * wr + 8 * u + grp, cc = 32 * wc + 8 * v + 2 * tig + h;
-          const int i = q0 + qq, j = c0 + cc;
-          double d = __longlong_as_double(0x7ff0000000000000LL);
-          if (i < a.n && j < i) {
-            if (a.degen[i] || a.degen[j]) {
-              d = 1.0;
-            } else {
-              double pe, pb;
-              a.lt.get2(a.tid[i], a.tid[j], pe, pb);
-              TF f;
-              f.pow_mE = pe;
-              f.pow_mbh = pb;
-              double rho = gneiting_eval(a.k, spatial_dist(a.x[i], a.y[i], a.x[j], a.y[j]), f);
-              if (a.M > 0) rho = __dsub_rn(rho, acc[u][v][h]);
-              const double rad =
-                  __dsub_rn(1.0, __ddiv_rn(fabs(rho), __dsqrt_rn(__dmul_rn(a.resid[i], a.resid[j]))));
-              d = __dsqrt_rn(rad < 0.0 ? 0.0 : rad);
+      for (int sv = 0; sv < nsurv; ++sv) {
+        const int ct = s_surv[sv];
+        if (sv > 0 && phase == 1 && can_prune) {  // re-test against the thresholds tightened by the previous survivors
+          if (tid == 0) {
+            const double dn = tile_threshold(topd, qm);
+            int skip = 0;
+            if (dn < 1.0) {
+              const double cmax = tile_cmax(a, tminQ, tmaxQ, qx0, qx1, qy0, qy1, sAQ, rQ, ct);
+              skip = cmax < 1.0 && (1.0 - cmax) - 1e-12 > dn * dn;
+            }
+            s_skip = skip;
+            if (a.stats && skip) {
+              atomicAdd(&a.stats[0], ~0ull);  // -1: moved from evaluated to pruned
+              atomicAdd(&a.stats[1], 1ull);
+              atomicAdd(&a.stats[2 + min(qb - b, 15)], ~0ull);
+              atomicAdd(&a.stats[18 + min(qb - b, 15)], 1ull);
             }
           }
-          sd[qq][cc] = d;
+          __syncthreads();
+          if (s_skip) continue;
         }
-    __syncthreads();
-    // merge: warp wid handles queries wid, wid + 8, ...
-    for (int qq = wid; qq < kQT; qq += kDrThreads / 32) {
-      const int i = q0 + qq;
-      if (i >= a.n) break;
-      const int m = min(a.m_v, i);
-      if (m <= 0) continue;
-      TopM e{topd[qq][lane], topj[qq][lane]};
+        const int cp0 = T.off[ct], cn = T.off[ct + 1] - cp0;
+        if (tid < kCT) cidx[tid] = tid < cn ? T.sp[cp0 + tid] : -1;
+        __syncthreads();
+        double acc[2][4][2];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int cc = lane + 32 * h;
-        const int j = c0 + cc;
-        const double d = sd[qq][cc];
-        const double wd = __shfl_sync(kFull, e.d, m - 1);
-        const int wj = __shfl_sync(kFull, e.j, m - 1);
-        const unsigned acc = __ballot_sync(kFull, j < i && lex_less(d, j, wd, wj));
-        if (acc) topm_insert(e, m, acc, d, j, lane);
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
+        if (a.M > 0) {
+          auto stage = [&](int ch) {
+            double* sQ = ring + static_cast<size_t>(ch % kStages) * kDrStageDoubles;
+            double* sC = sQ + kQT * kKS;
+#pragma unroll
+            for (int it = 0; it < kPieces / kDrThreads; ++it) {
+              const int pc = tid + it * kDrThreads;
+              const int which = pc / (kQT * (kKC / 2));  // 0: Q, 1: C
+              const int rem = pc % (kQT * (kKC / 2));
+              const int col = rem / (kKC / 2), piece = rem % (kKC / 2);
+              const int g0 = which ? cidx[col] : qidx[col];
+              const int g = g0 >= 0 ? g0 : 0;  // padding columns: any row, never read back
+              cp_async16((which ? sC : sQ) + col * kKS + 2 * piece,
+                         a.W + static_cast<size_t>(g) * a.ldm + static_cast<size_t>(ch) * kKC + 2 * piece);
+            }
+          };
+#pragma unroll
+          for (int ch = 0; ch < kStages - 1; ++ch) {
+            if (ch < nch) stage(ch);
+            cp_async_commit();
+          }
+          for (int ch = 0; ch < nch; ++ch) {
+            cp_async_wait<kStages - 2>();
+            __syncthreads();  // chunk ch visible; the stage about to be refilled is no longer read
+            if (ch + kStages - 1 < nch) stage(ch + kStages - 1);
+            cp_async_commit();
+            const double* sQ = ring + static_cast<size_t>(ch % kStages) * kDrStageDoubles;
+            const double* sC = sQ + kQT * kKS;
+#pragma unroll
+            for (int kb = 0; kb < kKC; kb += 4) {
+              double fa[2], fb[4];
+#pragma unroll
+              for (int u = 0; u < 2; ++u) fa[u] = sQ[(16 * wr + 8 * u + grp) * kKS + kb + tig];
+#pragma unroll
+              for (int v = 0; v < 4; ++v) fb[v] = sC[(32 * wc + 8 * v + grp) * kKS + kb + tig];
+#pragma unroll
+              for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) dmma_f64(acc[u][v][0], acc[u][v][1], fa[u], fb[v]);
+            }
+          }
+          cp_async_wait<0>();
+        }
+        // epilogue: d_r for the thread's 16 pairs (sd aliases the staging ring)
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int qq = 16 * wr + 8 * u + grp, cc = 32 * wc + 8 * v + 2 * tig + h;
+              const int i = qidx[qq], j = cidx[cc];
+              double dd = __longlong_as_double(0x7ff0000000000000LL);
+              if (i >= 0 && j >= 0 && j < i) {
+                if (a.degen[i] || a.degen[j]) {
+                  dd = 1.0;
+                } else {
+                  double pe, pb;
+                  a.lt.get2(a.tid[i], a.tid[j], pe, pb);
+                  TF f;
+                  f.pow_mE = pe;
+                  f.pow_mbh = pb;
+                  double rho = gneiting_eval(a.k, spatial_dist(a.x[i], a.y[i], a.x[j], a.y[j]), f);
+                  if (a.M > 0) rho = __dsub_rn(rho, acc[u][v][h]);
+                  const double rad =
+                      __dsub_rn(1.0, __ddiv_rn(fabs(rho), __dsqrt_rn(__dmul_rn(a.resid[i], a.resid[j]))));
+                  dd = __dsqrt_rn(rad < 0.0 ? 0.0 : rad);
+                }
+              }
+              sd[qq][cc] = dd;
+            }
+        __syncthreads();
+        // merge: warp wid handles queries wid, wid + 8, ...
+        for (int qq = wid; qq < kQT; qq += kDrThreads / 32) {
+          const int i = qidx[qq];
+          const int m = qm[qq];
+          if (m <= 0) continue;
+          TopM e{topd[qq][lane], topj[qq][lane]};
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int cc = lane + 32 * h;
+            const int j = cidx[cc];
+            const double dd = sd[qq][cc];
+            const double wd = __shfl_sync(kFull, e.d, m - 1);
+            const int wj = __shfl_sync(kFull, e.j, m - 1);
+            const unsigned acc2 = __ballot_sync(kFull, j >= 0 && j < i && lex_less(dd, j, wd, wj));
+            if (acc2) topm_insert(e, m, acc2, dd, j, lane);
+          }
+          topd[qq][lane] = e.d;
+          topj[qq][lane] = e.j;
+        }
+        __syncthreads();
       }
-      topd[qq][lane] = e.d;
-      topj[qq][lane] = e.j;
     }
+    if (stop) break;
   }
   __syncthreads();
   for (int qq = wid; qq < kQT; qq += kDrThreads / 32) {
-    const int i = q0 + qq;
-    if (i >= a.n) break;
-    const int m = min(a.m_v, i);
+    const int i = qidx[qq];
+    if (i < 0) continue;
+    const int m = qemit[qq];
     TopM e{topd[qq][lane], topj[qq][lane]};
-    topm_emit(e, a.m_v, m, lane, a.out + static_cast<size_t>(i) * a.m_v, a.dist ? a.dist + static_cast<size_t>(i) * a.m_v : nullptr);
+    topm_emit(e, a.m_v, m, lane, a.out + static_cast<size_t>(i) * a.m_v,
+              a.dist ? a.dist + static_cast<size_t>(i) * a.m_v : nullptr);
   }
 }
 
@@ -533,6 +743,7 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
         DevBuf<int> fail(1);
         const double jitter = 1e-8 * p.sigma1_2;
         bool ok = false;
+        ProfRegion prc(ctx, "dr_sigma_chol");
         for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
           sel_sigma_kernel<<<grid_for(static_cast<long long>(M) * M), 256, 0, st>>>(
               dzx.get(), dzy.get(), dzt.get(), M, k, lt, jitter, attempt == 0 ? 0.0 : 9.0 * jitter, A.get());
@@ -546,6 +757,7 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
           ok = f == 0;
         }
         if (!ok) numeric_error("InducingBasis: inducing covariance is not positive definite");
+        ProfRegion prw(ctx, "dr_whiten_seq");
         STGP_CUDA(cudaFuncSetAttribute(whiten_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(kWsmem)));
         whiten_seq_kernel<<<ceil_div(n, kWB), kWthreads, kWsmem, st>>>(dzx.get(), dzy.get(), dzt.get(), M, ldm,
@@ -584,36 +796,182 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
       a.lt = lt;
       a.out = nb->idx.get();
       a.dist = nb->dist.get();
-      const int ntile = ceil_div(n, 64);
-      DevBuf<int> tmn(ntile), tmx(ntile), hdg(ntile);
-      DevBuf<double> wmx(ntile), rmn(ntile);
-      tile_stats_kernel<<<ntile, 64, 0, st>>>(resid.get(), degen.get(), ds->tid.get(), n, p.sigma1_2, tmn.get(),
-                                              tmx.get(), wmx.get(), rmn.get(), hdg.get());
+      // spatial tiles: time buckets (consecutive equal-time blocks merged to >= 64 rows) sorted by
+      // the Morton code of (x, y), cut into tiles of <= 64 rows; one index-order bucket when the rows
+      // are not time sorted (no pruning: plain exact brute force over predecessors).
+      const bool ts = ds->time_sorted;
+      std::vector<int> bstart{0};
+      if (ts) {
+        int cnt = 0;
+        for (int i = 0; i < n; ++i) {
+          if (i > 0 && ds->htid[static_cast<size_t>(i)] != ds->htid[static_cast<size_t>(i - 1)] && cnt >= kQT) {
+            bstart.push_back(i);
+            cnt = 0;
+          }
+          ++cnt;
+        }
+      }
+      bstart.push_back(n);
+      const int nbucket = static_cast<int>(bstart.size()) - 1;
+      double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
+      for (int i = 0; i < n; ++i) {
+        x0 = std::min(x0, ds->hx[i]);
+        x1 = std::max(x1, ds->hx[i]);
+        y0 = std::min(y0, ds->hy[i]);
+        y1 = std::max(y1, ds->hy[i]);
+      }
+      const double sx = x1 > x0 ? 65535.0 / (x1 - x0) : 0.0, sy = y1 > y0 ? 65535.0 / (y1 - y0) : 0.0;
+      auto spread = [](uint32_t v) {
+        v &= 0xffff;
+        v = (v | (v << 8)) & 0x00ff00ffu;
+        v = (v | (v << 4)) & 0x0f0f0f0fu;
+        v = (v | (v << 2)) & 0x33333333u;
+        v = (v | (v << 1)) & 0x55555555u;
+        return v;
+      };
+      std::vector<uint32_t> key(static_cast<size_t>(n), 0u);
+      std::vector<int32_t> sp(static_cast<size_t>(n));
+      for (int i = 0; i < n; ++i) {
+        sp[static_cast<size_t>(i)] = i;
+        if (ts)
+          key[static_cast<size_t>(i)] = spread(static_cast<uint32_t>((ds->hx[i] - x0) * sx)) |
+                                        (spread(static_cast<uint32_t>((ds->hy[i] - y0) * sy)) << 1);
+      }
+      std::vector<int32_t> toff, tbucket, btile0;
+      std::vector<uint32_t> tkey;
+      for (int bb = 0; bb < nbucket; ++bb) {
+        const int b0 = bstart[static_cast<size_t>(bb)], b1 = bstart[static_cast<size_t>(bb) + 1];
+        if (ts)
+          std::sort(sp.begin() + b0, sp.begin() + b1, [&](int32_t u, int32_t v) {
+            const uint32_t ku = key[static_cast<size_t>(u)], kv = key[static_cast<size_t>(v)];
+            return ku != kv ? ku < kv : u < v;
+          });
+        btile0.push_back(static_cast<int32_t>(toff.size()));
+        for (int q = b0; q < b1; q += kQT) {
+          toff.push_back(q);
+          tbucket.push_back(bb);
+          tkey.push_back(key[static_cast<size_t>(sp[static_cast<size_t>(q)])]);
+        }
+      }
+      const int ntile = static_cast<int>(toff.size());
+      toff.push_back(n);
+      btile0.push_back(ntile);
+      DevBuf<int32_t> d_sp, d_off, d_bucket, d_bt0, d_btmax;
+      DevBuf<uint32_t> d_key;
+      d_sp.upload(sp.data(), sp.size(), st);
+      d_off.upload(toff.data(), toff.size(), st);
+      d_bucket.upload(tbucket.data(), tbucket.size(), st);
+      d_bt0.upload(btile0.data(), btile0.size(), st);
+      d_key.upload(tkey.data(), tkey.size(), st);
+      DevBuf<int> tmn(ntile), tmx(ntile), hdg(ntile), imn(ntile), imx(ntile);
+      DevBuf<double> wmx(ntile), rmn(ntile), bx0(ntile), bx1(ntile), by0(ntile), by1(ntile);
+      DrTiles T{};
+      T.sp = d_sp.get();
+      T.off = d_off.get();
+      T.bucket = d_bucket.get();
+      T.b_tile0 = d_bt0.get();
+      T.key = d_key.get();
+      T.tmin = tmn.get();
+      T.tmax = tmx.get();
+      T.hasdeg = hdg.get();
+      T.imin = imn.get();
+      T.imax = imx.get();
+      T.bx0 = bx0.get();
+      T.bx1 = bx1.get();
+      T.by0 = by0.get();
+      T.by1 = by1.get();
+      T.wmax = wmx.get();
+      T.rmin = rmn.get();
+      tile_stats_kernel<<<ntile, 64, 0, st>>>(T, ds->x.get(), ds->y.get(), resid.get(), degen.get(), ds->tid.get(),
+                                              p.sigma1_2);
       launched(ctx);
-      a.tmin = tmn.get();
-      a.tmax = tmx.get();
-      a.wmax = wmx.get();
-      a.rmin = rmn.get();
-      a.hasdeg = hdg.get();
+      // inducing-point groups for the block-norm bound: inducing time (<= 4 bins) x spatial cell
+      // (<= 12 cells of the inducing bounding box)
+      int G = 0;
+      std::vector<int32_t> kgroup(static_cast<size_t>(std::max(M, 1)), 0);
+      if (M > 0) {
+        const int gt = std::min<int>(4, static_cast<int>(Ti.size()));
+        double zx0 = INFINITY, zx1 = -INFINITY, zy0 = INFINITY, zy1 = -INFINITY;
+        for (int j = 0; j < M; ++j) {
+          zx0 = std::min(zx0, zx[j]);
+          zx1 = std::max(zx1, zx[j]);
+          zy0 = std::min(zy0, zy[j]);
+          zy1 = std::max(zy1, zy[j]);
+        }
+        const double ex = std::max(zx1 - zx0, 1e-300), ey = std::max(zy1 - zy0, 1e-300);
+        int gx = std::max(1, std::min(12, static_cast<int>(std::lround(std::sqrt(12.0 * ex / ey)))));
+        int gy = std::max(1, 12 / gx);
+        G = gt * gx * gy;
+        for (int j = 0; j < M; ++j) {
+          const int ti_ = static_cast<int>(std::lower_bound(Ti.begin(), Ti.end(), zt[j]) - Ti.begin());
+          const int tg = static_cast<int>(static_cast<long long>(ti_) * gt / static_cast<long long>(Ti.size()));
+          const int cx = std::min(gx - 1, static_cast<int>((zx[j] - zx0) / ex * gx));
+          const int cy = std::min(gy - 1, static_cast<int>((zy[j] - zy0) / ey * gy));
+          kgroup[static_cast<size_t>(j)] = (tg * gy + cy) * gx + cx;
+        }
+      }
+      DevBuf<int32_t> d_kgroup;
+      d_kgroup.upload(kgroup.data(), kgroup.size(), st);
+      DevBuf<double> dA(static_cast<size_t>(std::max(1, ntile * G)));
+      T.G = G;
+      T.A = dA.get();
+      if (G > 0) {
+        tile_groups_kernel<<<ntile, 256, 0, st>>>(T, W.get(), ldm, M, d_kgroup.get(), resid.get(), degen.get());
+        launched(ctx);
+      }
+      // per-bucket prefix bounds (buckets <= b) for the exact early stop (host, small)
+      std::vector<double> hA(static_cast<size_t>(ntile) * G), hr(static_cast<size_t>(ntile));
+      std::vector<int> htmax(static_cast<size_t>(ntile));
+      if (G > 0) dA.download(hA.data(), hA.size(), st);
+      rmn.download(hr.data(), hr.size(), st);
+      tmx.download(htmax.data(), htmax.size(), st);
+      STGP_CUDA(cudaStreamSynchronize(st));
+      std::vector<double> Apre(std::max<size_t>(static_cast<size_t>(nbucket) * G, 1), 0.0), rpre(static_cast<size_t>(nbucket), INFINITY);
+      std::vector<int32_t> btmax(static_cast<size_t>(nbucket), -1);
+      for (int t2 = 0; t2 < ntile; ++t2) {
+        const size_t bb = static_cast<size_t>(tbucket[static_cast<size_t>(t2)]);
+        btmax[bb] = std::max(btmax[bb], htmax[static_cast<size_t>(t2)]);
+        rpre[bb] = std::min(rpre[bb], hr[static_cast<size_t>(t2)]);
+        for (int g = 0; g < G; ++g)
+          Apre[bb * G + g] = std::max(Apre[bb * G + g], hA[static_cast<size_t>(t2) * G + g]);
+      }
+      for (int bb = 1; bb < nbucket; ++bb) {
+        rpre[static_cast<size_t>(bb)] = std::min(rpre[static_cast<size_t>(bb)], rpre[static_cast<size_t>(bb) - 1]);
+        for (int g = 0; g < G; ++g)
+          Apre[static_cast<size_t>(bb) * G + g] =
+              std::max(Apre[static_cast<size_t>(bb) * G + g], Apre[static_cast<size_t>(bb - 1) * G + g]);
+      }
+      DevBuf<double> dApre, drpre;
+      dApre.upload(Apre.data(), Apre.size(), st);
+      drpre.upload(rpre.data(), rpre.size(), st);
+      d_btmax.upload(btmax.data(), btmax.size(), st);
+      T.b_tmax = d_btmax.get();
+      T.Apre = dApre.get();
+      T.rpre = drpre.get();
+      a.T = T;
       a.s1 = p.sigma1_2;
       // pruning needs time-sorted rows (tile time ranges); otherwise plain brute force
-      if (!ds->time_sorted) a.tmin = nullptr;
+      a.prune = ts ? 1 : 0;
       DevBuf<unsigned long long> stats;
       if (std::getenv("STGP_DR_STATS")) {  // diagnostics: tile pairs evaluated / pruned
-        stats.alloc(2);
-        STGP_CUDA(cudaMemsetAsync(stats.get(), 0, 16, st));
+        stats.alloc(50);
+        STGP_CUDA(cudaMemsetAsync(stats.get(), 0, 50 * 8, st));
         a.stats = stats.get();
       }
       ProfRegion pr(ctx, "knn_dr");
       STGP_CUDA(cudaFuncSetAttribute(knn_dr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kDrSmem)));
-      knn_dr_kernel<<<ceil_div(n, kQT), kDrThreads, kDrSmem, st>>>(a);
+      knn_dr_kernel<<<ntile, kDrThreads, kDrSmem, st>>>(a);
       launched(ctx);
       if (a.stats) {
-        unsigned long long h[2];
-        STGP_CUDA(cudaMemcpyAsync(h, a.stats, 16, cudaMemcpyDeviceToHost, st));
+        unsigned long long h[50];
+        STGP_CUDA(cudaMemcpyAsync(h, a.stats, 50 * 8, cudaMemcpyDeviceToHost, st));
         STGP_CUDA(cudaStreamSynchronize(st));
-        std::fprintf(stderr, "[stgp] d_r tiles: evaluated %llu pruned %llu\n", h[0], h[1]);
+        std::fprintf(stderr, "[stgp] d_r tiles (%d query tiles, %d groups): evaluated %llu pruned %llu\n", ntile, G,
+                     h[0], h[1]);
+        for (int lg = 0; lg < 16; ++lg)
+          std::fprintf(stderr, "[stgp]   lag %2d: evaluated %llu pruned %llu stops %llu\n", lg, h[2 + lg], h[18 + lg],
+                       h[34 + lg]);
       }
     }
     STGP_CUDA(cudaStreamSynchronize(st));

@@ -111,3 +111,23 @@ def test_dr_empty_inducing_equals_dc(S):
     a = S.correlation_neighbors(ds, SEC4, 8).indices()
     b = S.residual_neighbors(ds, SEC4, S.InducingSet.from_points(np.zeros((0, 3))), 8).indices()
     assert (a == b).all()
+
+
+def test_dr_spatial_pruning_geometry(S):
+    # cfg4 geometry (Table 3 theta, 4600 x 2900 km box): spatial tiles, box-distance and
+    # block-norm pruning and the early time stop are all active; exactness against the oracle
+    x, y, t, _ = S.synth.station_day(2000, 8, box=(4.6e6, 2.9e6), theta=S.synth.THETA_T3, seed=21)
+    perm = O.order_observations(t, 21)
+    x, y, t = x[perm], y[perm], t[perm]
+    Z, _, _ = O.sts_kmeanspp(x, y, t, 200, 21)
+    _check_dr(S, x, y, t, S.synth.THETA_T3, Z, 30)
+
+
+def test_dr_unsorted_rows_brute_force(S):
+    # rows not time sorted: one index-order bucket, no pruning
+    x, y, t, _ = S.synth.station_day(60, 8, seed=5)
+    rng = np.random.default_rng(3)
+    perm = rng.permutation(len(x))
+    x, y, t = x[perm], y[perm], t[perm]
+    Z, _, _ = O.sts_kmeanspp(x, y, t, 40, 2)
+    _check_dr(S, x, y, t, SEC4, Z, 12)
