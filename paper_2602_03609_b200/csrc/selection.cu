@@ -10,11 +10,16 @@
 //     its terms in increasing column order, the same sequence as the oracle);
 //   * w_i.w_j: register-tiled Gram whose K loop runs sequentially per element.
 #include <algorithm>
+#include <chrono>
+#include <cmath>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <set>
+
+#include <cub/device/device_radix_sort.cuh>
 
 #include "comm.hpp"
 #include "lowrank_common.cuh"
@@ -48,17 +53,36 @@ __global__ void sel_sigma_kernel(const double* zx, const double* zy, const int32
   }
 }
 
-// Left-looking Cholesky in the oracle's order (chol_seq); A row-major in, L row-major out.
+// Left-looking Cholesky in the oracle's order (chol_seq); A row-major in, L row-major out.  Row j
+// of L is staged in shared memory; each row's chain streams its own row with loads batched ahead of
+// the (sequential) fma chain.
+__device__ __forceinline__ double chol_chain(const double* Lr, const double* Lj, int j, double s) {
+  int k = 0;
+  for (; k + 8 <= j; k += 8) {
+    double a[8], b[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      a[u] = Lr[k + u];
+      b[u] = Lj[k + u];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = __fma_rn(-a[u], b[u], s);
+  }
+  for (; k < j; ++k) s = __fma_rn(-Lr[k], Lj[k], s);
+  return s;
+}
+
 __global__ void __launch_bounds__(1024) chol_seq_kernel(const double* A, int M, double* L, int* fail) {
   __shared__ double diag;
   __shared__ int bad;
+  extern __shared__ double sLj[];  // row j of L (M doubles)
   if (threadIdx.x == 0) bad = 0;
   for (int j = 0; j < M; ++j) {
     __syncthreads();
+    for (int k = threadIdx.x; k < j; k += blockDim.x) sLj[k] = L[static_cast<size_t>(j) * M + k];
+    __syncthreads();
     if (threadIdx.x == 0) {
-      const double* Lj = L + static_cast<size_t>(j) * M;
-      double acc = A[static_cast<size_t>(j) * M + j];
-      for (int k = 0; k < j; ++k) acc = __fma_rn(-Lj[k], Lj[k], acc);
+      const double acc = chol_chain(sLj, sLj, j, A[static_cast<size_t>(j) * M + j]);
       if (acc <= 0.0) bad = 1;
       diag = __dsqrt_rn(acc);
       L[static_cast<size_t>(j) * M + j] = diag;
@@ -66,12 +90,9 @@ __global__ void __launch_bounds__(1024) chol_seq_kernel(const double* A, int M, 
     __syncthreads();
     if (bad) break;
     const double d = diag;
-    const double* Lj = L + static_cast<size_t>(j) * M;
     for (int r = j + 1 + threadIdx.x; r < M; r += blockDim.x) {
-      const double* Lr = L + static_cast<size_t>(r) * M;
-      double s = A[static_cast<size_t>(r) * M + j];
-      for (int k = 0; k < j; ++k) s = __fma_rn(-Lr[k], Lj[k], s);
-      L[static_cast<size_t>(r) * M + j] = __ddiv_rn(s, d);
+      const double sr = chol_chain(L + static_cast<size_t>(r) * M, sLj, j, A[static_cast<size_t>(r) * M + j]);
+      L[static_cast<size_t>(r) * M + j] = __ddiv_rn(sr, d);
     }
   }
   if (threadIdx.x == 0 && bad) *fail = 1;
@@ -79,107 +100,178 @@ __global__ void __launch_bounds__(1024) chol_seq_kernel(const double* A, int M, 
 
 constexpr int kWB = 64;      // rows per block and columns per CTA
 constexpr int kWKC = 16;     // K chunk of the off-diagonal update
+constexpr int kWKS = 20;     // smem row stride (doubles): conflict-free DMMA fragment loads
+constexpr int kWStages = 3;
 constexpr int kWthreads = 256;
-constexpr size_t kWsmem = sizeof(double) * (64 * 17 + 16 * 65 + 64 * 65 + 2 * 64 + 2 * 64) + sizeof(int) * 64;
+constexpr size_t kWStageDoubles = 2 * kWB * kWKS;
+constexpr size_t kWsmem = sizeof(double) * (kWStages * kWStageDoubles + 64 * 65 + 2 * 64 + 2 * 64) + sizeof(int) * 64;
+static_assert(kWStages * kWStageDoubles >= 64 * 65, "output tile aliases the staging ring");
 
-// W(:, i) = L^{-1} k_m(p_i) for 64 columns per CTA.  Row blocks of 64: the
-// off-diagonal part is a register-tiled update whose K loop runs in increasing
-// c, the diagonal block is a column wavefront, so every accumulator receives
-// -L[r][c] w_c for c = 0, 1, ... in order -- the oracle's fwd_seq sequence.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+// Zero-padded copy of L with a 16-double row stride (cp.async alignment).
+__global__ void pad_rows_kernel(const double* L, int M, int ldL, double* Lp) {
+  const long long total = static_cast<long long>(M) * ldL;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e / ldL), c = static_cast<int>(e % ldL);
+    Lp[e] = c < M ? L[static_cast<size_t>(r) * M + c] : 0.0;
+  }
+}
+
+// W(:, i) = L^{-1} k_m(p_i) for 64 columns per CTA, row blocks of 64.  Every accumulator starts at
+// k(z_r, p_i) and receives -L[r][c] w_c for c = 0, 1, ... in order -- the oracle's fwd_seq chain:
+// the off-diagonal part c < r0 runs on the FP64 tensor pipe (mma.m8n8k4.f64 = the sequential fma
+// chain over its k, scripts/exp/dmma_order.cu) over cp.async-staged 16-wide chunks in increasing c;
+// the diagonal block is a column wavefront.  Warp w owns rows 16 (w/2).., columns 32 (w%2)...
 __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx, const double* zy, const int32_t* ztid,
                                                               int M, int ldm, const double* x, const double* y,
                                                               const int32_t* tid, int n, DevKernel k, LagTable lt,
-                                                              const double* L, double* W) {
+                                                              const double* Lp, int ldL, double* W) {
   extern __shared__ double sm[];
-  double* sL = sm;               // [64][17]
-  double* sWt = sL + 64 * 17;    // [16][65]
-  double* sD = sWt + 16 * 65;    // [64][65]
-  double* wrow = sD + 64 * 65;   // [2][64]
-  double* sx = wrow + 2 * 64;    // [64]
-  double* sy = sx + 64;          // [64]
+  double* ring = sm;                                  // kWStages x [L 64 x kWKS | W 64 x kWKS]
+  double* sOut = sm;                                  // [64 cols][65] (aliases the ring)
+  double* sD = sm + kWStages * kWStageDoubles;        // [64][65]
+  double* wrow = sD + 64 * 65;                        // [2][64]
+  double* sx = wrow + 2 * 64;                         // [64]
+  double* sy = sx + 64;                               // [64]
   int* st = reinterpret_cast<int*>(sy + 64);
   const int i0 = blockIdx.x * kWB;
   const int nc = min(kWB, n - i0);
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int grp = lane >> 2, tig = lane & 3, wr = wid >> 1, wc = wid & 1;
   if (t < kWB) {
     const int i = i0 + (t < nc ? t : 0);
     sx[t] = x[i];
     sy[t] = y[i];
     st[t] = tid[i];
   }
-  const int tr = (t / 16) * 4, tc = (t % 16) * 4;
   __syncthreads();
+  constexpr int kPieces = 2 * kWB * (kWKC / 2);
+  static_assert(kPieces % kWthreads == 0, "staging split");
   for (int r0 = 0; r0 < M; r0 += kWB) {
     const int rb = min(kWB, M - r0);
-    double acc[4][4];
+    double acc[2][4][2];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < 2; ++u)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int r = r0 + tr + u, c = tc + v;
-        double val = 0.0;
-        if (r < M && c < nc) {
-          double pe, pb;
-          lt.get2(ztid[r], st[c], pe, pb);
-          TF f;
-          f.pow_mE = pe;
-          f.pow_mbh = pb;
-          val = gneiting_eval(k, spatial_dist(zx[r], zy[r], sx[c], sy[c]), f);  // k(z_r, p_i)
+      for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + 16 * wr + 8 * u + grp, c = 32 * wc + 8 * v + 2 * tig + h;
+          double val = 0.0;
+          if (r < M && c < nc) {
+            double pe, pb;
+            lt.get2(ztid[r], st[c], pe, pb);
+            TF f;
+            f.pow_mE = pe;
+            f.pow_mbh = pb;
+            val = gneiting_eval(k, spatial_dist(zx[r], zy[r], sx[c], sy[c]), f);  // k(z_r, p_i)
+          }
+          acc[u][v][h] = val;
         }
-        acc[u][v] = val;
+    const int nch = r0 / kWKC;
+    if (nch > 0) {
+      auto stage = [&](int ch) {
+        double* sL = ring + static_cast<size_t>(ch % kWStages) * kWStageDoubles;
+        double* sW = sL + kWB * kWKS;
+#pragma unroll
+        for (int it = 0; it < kPieces / kWthreads; ++it) {
+          const int pc = t + it * kWthreads;
+          const int which = pc / (kWB * (kWKC / 2));  // 0: L rows, 1: W columns
+          const int rem = pc % (kWB * (kWKC / 2));
+          const int rr = rem / (kWKC / 2), piece = rem % (kWKC / 2);
+          if (which == 0) {
+            const int r = min(r0 + rr, M - 1);
+            cp_async16(sL + rr * kWKS + 2 * piece, Lp + static_cast<size_t>(r) * ldL + ch * kWKC + 2 * piece);
+          } else {
+            const int i = i0 + (rr < nc ? rr : 0);
+            cp_async16(sW + rr * kWKS + 2 * piece, W + static_cast<size_t>(i) * ldm + ch * kWKC + 2 * piece);
+          }
+        }
+      };
+#pragma unroll
+      for (int ch = 0; ch < kWStages - 1; ++ch) {
+        if (ch < nch) stage(ch);
+        cp_async_commit();
       }
-    for (int c0 = 0; c0 < r0; c0 += kWKC) {
-      __syncthreads();
-      for (int e = t; e < 64 * kWKC; e += kWthreads) {
-        const int rr = e / kWKC, kk = e % kWKC;
-        sL[rr * 17 + kk] = r0 + rr < M ? L[static_cast<size_t>(r0 + rr) * M + c0 + kk] : 0.0;
-        const int cc = e / kWKC;
-        sWt[kk * 65 + cc] = cc < nc ? W[static_cast<size_t>(i0 + cc) * ldm + c0 + kk] : 0.0;
+      for (int ch = 0; ch < nch; ++ch) {
+        cp_async_wait<kWStages - 2>();
+        __syncthreads();
+        if (ch + kWStages - 1 < nch) stage(ch + kWStages - 1);
+        cp_async_commit();
+        const double* sL = ring + static_cast<size_t>(ch % kWStages) * kWStageDoubles;
+        const double* sW = sL + kWB * kWKS;
+#pragma unroll
+        for (int kb = 0; kb < kWKC; kb += 4) {
+          double fa[2], fb[4];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) fa[u] = -sL[(16 * wr + 8 * u + grp) * kWKS + kb + tig];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) fb[v] = sW[(32 * wc + 8 * v + grp) * kWKS + kb + tig];
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) dmma_f64(acc[u][v][0], acc[u][v][1], fa[u], fb[v]);
+        }
       }
-      __syncthreads();
-#pragma unroll
-      for (int kk = 0; kk < kWKC; ++kk) {
-        double lr[4], wv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) lr[u] = -sL[(tr + u) * 17 + kk];
-#pragma unroll
-        for (int v = 0; v < 4; ++v) wv[v] = sWt[kk * 65 + tc + v];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int v = 0; v < 4; ++v) acc[u][v] = __fma_rn(lr[u], wv[v], acc[u][v]);
-      }
+      cp_async_wait<0>();
     }
     __syncthreads();
     for (int e = t; e < 64 * 64; e += kWthreads) {
       const int rr = e / 64, cc = e % 64;
-      sD[rr * 65 + cc] = (rr < rb && cc <= rr) ? L[static_cast<size_t>(r0 + rr) * M + r0 + cc] : 0.0;
+      sD[rr * 65 + cc] = (rr < rb && cc <= rr) ? Lp[static_cast<size_t>(r0 + rr) * ldL + r0 + cc] : 0.0;
     }
     __syncthreads();
+    // diagonal block: column wavefront; outputs collected column-major in sOut
     for (int cl = 0; cl < rb; ++cl) {
       double* buf = wrow + (cl & 1) * 64;
-      if (cl >= tr && cl < tr + 4) {
+      if (wr == (cl >> 4) && grp == (cl & 7)) {
         const double d = sD[cl * 65 + cl];
+        const int uo = (cl >> 3) & 1;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (u == cl - tr)
+        for (int u = 0; u < 2; ++u)
+          if (u == uo)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const double wv = __ddiv_rn(acc[u][v], d);
-              buf[tc + v] = wv;
-              if (tc + v < nc) W[static_cast<size_t>(i0 + tc + v) * ldm + r0 + cl] = wv;
-            }
+            for (int v = 0; v < 4; ++v)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int c = 32 * wc + 8 * v + 2 * tig + h;
+                const double wv = __ddiv_rn(acc[u][v][h], d);
+                buf[c] = wv;
+                sOut[c * 65 + cl] = wv;
+              }
       }
       __syncthreads();
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int rr = tr + u;
+      for (int u = 0; u < 2; ++u) {
+        const int rr = 16 * wr + 8 * u + grp;
         if (rr > cl && rr < rb) {
           const double l = -sD[rr * 65 + cl];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) acc[u][v] = __fma_rn(l, buf[tc + v], acc[u][v]);
+          for (int v = 0; v < 4; ++v)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) acc[u][v][h] = __fma_rn(l, buf[32 * wc + 8 * v + 2 * tig + h], acc[u][v][h]);
         }
       }
+    }
+    __syncthreads();
+    for (int e = t; e < 64 * 64; e += kWthreads) {  // coalesced column segments
+      const int c = e / 64, rr = e % 64;
+      if (c < nc && rr < rb) W[static_cast<size_t>(i0 + c) * ldm + r0 + rr] = sOut[c * 65 + rr];
     }
     __syncthreads();
   }
@@ -324,21 +416,6 @@ struct DrArgs {
   double s1;
   unsigned long long* stats;  // optional: [0] candidate tiles evaluated, [1] tiles pruned
 };
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-      : "+d"(d0), "+d"(d1)
-      : "d"(a), "d"(b));
-}
 
 // Upper bound of |rho_r| over the pairs of query tile Q and candidate tile C:
 //   |k - w_i.w_j| / sqrt(r_i r_j) <= s1 T(u_min)^-E Matern(c h_min T(u_max)^-beta/2) / sqrt(rmin_Q rmin_C)
@@ -705,6 +782,17 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
     cudaStream_t st = ctx->stream;
     const int n = ds->n, M = ind->M();
     const DevKernel k = dev_kernel(p);
+    // diagnostics (STGP_DR_STATS): host-side phase times
+    const bool dbg = std::getenv("STGP_DR_STATS") != nullptr;
+    auto clk0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+      if (!dbg) return;
+      STGP_CUDA(cudaStreamSynchronize(st));
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[stgp] d_r phase %-12s %8.2f ms\n", what,
+                   std::chrono::duration<double, std::milli>(now - clk0).count());
+      clk0 = now;
+    };
     // time index over data + inducing times, live factors (no lag table in the selection kernel)
     std::vector<double> zx(M), zy(M), zt(M);
     for (int j = 0; j < M; ++j) {
@@ -736,6 +824,7 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
     STGP_CUDA(cudaMemsetAsync(W.get(), 0, sizeof(double) * ldm * n, st));
     DevBuf<int32_t> degen(n);
     {
+      lap("setup+alloc");
       ProfRegion pr(ctx, "dr_whiten");
       if (M > 0) {
         // InducingBasis(set, selection kernel): jittered Sigma_m, one retry at 10x (inducing.cpp:250-261)
@@ -743,31 +832,39 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
         DevBuf<int> fail(1);
         const double jitter = 1e-8 * p.sigma1_2;
         bool ok = false;
-        ProfRegion prc(ctx, "dr_sigma_chol");
+        STGP_CUDA(cudaFuncSetAttribute(chol_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sizeof(double) * M)));
         for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+          std::unique_ptr<ProfRegion> prc(new ProfRegion(ctx, "dr_sigma_chol"));
           sel_sigma_kernel<<<grid_for(static_cast<long long>(M) * M), 256, 0, st>>>(
               dzx.get(), dzy.get(), dzt.get(), M, k, lt, jitter, attempt == 0 ? 0.0 : 9.0 * jitter, A.get());
           launched(ctx);
           fail.zero(st);
-          chol_seq_kernel<<<1, 1024, 0, st>>>(A.get(), M, L.get(), fail.get());
+          chol_seq_kernel<<<1, 1024, sizeof(double) * M, st>>>(A.get(), M, L.get(), fail.get());
           launched(ctx);
+          prc.reset();
           int f = 0;
           fail.download(&f, 1, st);
           STGP_CUDA(cudaStreamSynchronize(st));
           ok = f == 0;
         }
         if (!ok) numeric_error("InducingBasis: inducing covariance is not positive definite");
-        ProfRegion prw(ctx, "dr_whiten_seq");
         STGP_CUDA(cudaFuncSetAttribute(whiten_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(kWsmem)));
+        const int ldL = (M + kWKC - 1) / kWKC * kWKC;
+        DevBuf<double> Lp(static_cast<size_t>(M) * ldL);
+        ProfRegion prw(ctx, "dr_whiten_seq");
+        pad_rows_kernel<<<grid_for(static_cast<long long>(M) * ldL), 256, 0, st>>>(L.get(), M, ldL, Lp.get());
+        launched(ctx);
         whiten_seq_kernel<<<ceil_div(n, kWB), kWthreads, kWsmem, st>>>(dzx.get(), dzy.get(), dzt.get(), M, ldm,
                                                                       ds->x.get(), ds->y.get(), ds->tid.get(), n, k, lt,
-                                                                      L.get(), W.get());
+                                                                      Lp.get(), ldL, W.get());
         launched(ctx);
       }
       resid_kernel<<<grid_for(n), 256, 0, st>>>(W.get(), M, ldm, n, p.sigma1_2, resid.get(), degen.get());
       launched(ctx);
     }
+    lap("whiten");
     auto nb = std::make_unique<stgp_neighbors>();
     nb->ctx = ctx;
     nb->n = n;
@@ -829,36 +926,61 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
         v = (v | (v << 1)) & 0x55555555u;
         return v;
       };
-      std::vector<uint32_t> key(static_cast<size_t>(n), 0u);
-      std::vector<int32_t> sp(static_cast<size_t>(n));
-      for (int i = 0; i < n; ++i) {
-        sp[static_cast<size_t>(i)] = i;
-        if (ts)
-          key[static_cast<size_t>(i)] = spread(static_cast<uint32_t>((ds->hx[i] - x0) * sx)) |
-                                        (spread(static_cast<uint32_t>((ds->hy[i] - y0) * sy)) << 1);
+      // rows sorted by (bucket, Morton key) on the device: a stable radix sort keeps index order
+      // within equal keys
+      std::vector<uint64_t> key64(static_cast<size_t>(n));
+      {
+        int bb = 0;
+        for (int i = 0; i < n; ++i) {
+          while (i >= bstart[static_cast<size_t>(bb) + 1]) ++bb;
+          const uint32_t mk = ts ? (spread(static_cast<uint32_t>((ds->hx[i] - x0) * sx)) |
+                                    (spread(static_cast<uint32_t>((ds->hy[i] - y0) * sy)) << 1))
+                                 : 0u;
+          key64[static_cast<size_t>(i)] = (static_cast<uint64_t>(bb) << 32) | mk;
+        }
+      }
+      lap("tiles:keys");
+      DevBuf<int32_t> d_sp;
+      DevBuf<uint64_t> d_keys_sorted;
+      {
+        DevBuf<uint64_t> d_keys;
+        DevBuf<int32_t> d_iota;
+        d_keys.upload(key64.data(), key64.size(), st);
+        std::vector<int32_t> iota(static_cast<size_t>(n));
+        for (int i = 0; i < n; ++i) iota[static_cast<size_t>(i)] = i;
+        d_iota.upload(iota.data(), iota.size(), st);
+        lap("tiles:upload");
+        d_sp.alloc(static_cast<size_t>(n));
+        d_keys_sorted.alloc(static_cast<size_t>(n));
+        const int endbit = 32 + std::max(1, static_cast<int>(std::ceil(std::log2(static_cast<double>(nbucket) + 1.0))));
+        size_t tmpb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmpb, d_keys.get(), d_keys_sorted.get(), d_iota.get(), d_sp.get(), n,
+                                        0, std::min(64, endbit), st);
+        DevBuf<unsigned char> tmp(tmpb);
+        lap("tiles:sortq");
+        cub::DeviceRadixSort::SortPairs(tmp.get(), tmpb, d_keys.get(), d_keys_sorted.get(), d_iota.get(), d_sp.get(),
+                                        n, 0, std::min(64, endbit), st);
+        launched(ctx);
+        lap("tiles:sort");
+        d_keys_sorted.download(key64.data(), key64.size(), st);  // sorted keys: tile anchors
+        STGP_CUDA(cudaStreamSynchronize(st));
       }
       std::vector<int32_t> toff, tbucket, btile0;
       std::vector<uint32_t> tkey;
       for (int bb = 0; bb < nbucket; ++bb) {
         const int b0 = bstart[static_cast<size_t>(bb)], b1 = bstart[static_cast<size_t>(bb) + 1];
-        if (ts)
-          std::sort(sp.begin() + b0, sp.begin() + b1, [&](int32_t u, int32_t v) {
-            const uint32_t ku = key[static_cast<size_t>(u)], kv = key[static_cast<size_t>(v)];
-            return ku != kv ? ku < kv : u < v;
-          });
         btile0.push_back(static_cast<int32_t>(toff.size()));
         for (int q = b0; q < b1; q += kQT) {
           toff.push_back(q);
           tbucket.push_back(bb);
-          tkey.push_back(key[static_cast<size_t>(sp[static_cast<size_t>(q)])]);
+          tkey.push_back(static_cast<uint32_t>(key64[static_cast<size_t>(q)] & 0xffffffffu));
         }
       }
       const int ntile = static_cast<int>(toff.size());
       toff.push_back(n);
       btile0.push_back(ntile);
-      DevBuf<int32_t> d_sp, d_off, d_bucket, d_bt0, d_btmax;
+      DevBuf<int32_t> d_off, d_bucket, d_bt0, d_btmax;
       DevBuf<uint32_t> d_key;
-      d_sp.upload(sp.data(), sp.size(), st);
       d_off.upload(toff.data(), toff.size(), st);
       d_bucket.upload(tbucket.data(), tbucket.size(), st);
       d_bt0.upload(btile0.data(), btile0.size(), st);
@@ -885,6 +1007,7 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
       tile_stats_kernel<<<ntile, 64, 0, st>>>(T, ds->x.get(), ds->y.get(), resid.get(), degen.get(), ds->tid.get(),
                                               p.sigma1_2);
       launched(ctx);
+      lap("tiles");
       // inducing-point groups for the block-norm bound: inducing time (<= 4 bins) x spatial cell
       // (<= 12 cells of the inducing bounding box)
       int G = 0;
@@ -952,6 +1075,7 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
       a.s1 = p.sigma1_2;
       // pruning needs time-sorted rows (tile time ranges); otherwise plain brute force
       a.prune = ts ? 1 : 0;
+      lap("groups");
       DevBuf<unsigned long long> stats;
       if (std::getenv("STGP_DR_STATS")) {  // diagnostics: tile pairs evaluated / pruned
         stats.alloc(50);
@@ -963,6 +1087,7 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
                                      static_cast<int>(kDrSmem)));
       knn_dr_kernel<<<ntile, kDrThreads, kDrSmem, st>>>(a);
       launched(ctx);
+      lap("knn");
       if (a.stats) {
         unsigned long long h[50];
         STGP_CUDA(cudaMemcpyAsync(h, a.stats, 50 * 8, cudaMemcpyDeviceToHost, st));
@@ -977,7 +1102,9 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
     STGP_CUDA(cudaStreamSynchronize(st));
     prof_collect(ctx);
     *out = nb.release();
+    lap("finish");
   });
+  // (W, tiles and stats are released here, after the lap above)
 }
 
 }  // extern "C"
