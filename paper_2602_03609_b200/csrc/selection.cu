@@ -820,7 +820,9 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
     dzy.upload(zy.data(), M, st);
     dzt.upload(ztid.data(), M, st);
     const int ldm = std::max(kKC, (M + kKC - 1) / kKC * kKC);  // zero rows [M, ldm): exact extra fma(0, 0, g)
+    lap("setup");
     DevBuf<double> W(static_cast<size_t>(ldm) * n), resid(n);
+    lap("alloc W");
     STGP_CUDA(cudaMemsetAsync(W.get(), 0, sizeof(double) * ldm * n, st));
     DevBuf<int32_t> degen(n);
     {
@@ -849,6 +851,7 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
           ok = f == 0;
         }
         if (!ok) numeric_error("InducingBasis: inducing covariance is not positive definite");
+        lap("w:sigma+chol");
         STGP_CUDA(cudaFuncSetAttribute(whiten_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(kWsmem)));
         const int ldL = (M + kWKC - 1) / kWKC * kWKC;
@@ -860,6 +863,7 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
                                                                       ds->x.get(), ds->y.get(), ds->tid.get(), n, k, lt,
                                                                       Lp.get(), ldL, W.get());
         launched(ctx);
+        lap("w:whiten_seq");
       }
       resid_kernel<<<grid_for(n), 256, 0, st>>>(W.get(), M, ldm, n, p.sigma1_2, resid.get(), degen.get());
       launched(ctx);
