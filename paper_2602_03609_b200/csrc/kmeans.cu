@@ -50,51 +50,111 @@ __global__ void d2_update_kernel(KArgs a, int j, bool init, double* d2) {
   }
 }
 
-// One weighted pick (inducing.cpp:32-42): total in Eigen's order, then the
-// sequential running sum.  Single thread on purpose: both reductions are
-// order-defined sequences.  Writes the pick and copies the point into C[j].
-__global__ void pick_kernel(KArgs a, const double* d2, double canon, int j, long* pick_out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// One weighted pick (inducing.cpp:32-42): total in Eigen's order, then the sequential running sum.
+// Both are order-defined chains, so one thread runs them -- over shared-memory chunks that the
+// whole block stages from global memory (loads batched ahead of the dependent adds).  Writes the
+// pick and copies the point into C[j].
+constexpr int kPickChunk = 12288;  // doubles (96 KB), a multiple of 8
+constexpr int kPickThreads = 1024;
+__global__ void __launch_bounds__(kPickThreads) pick_kernel(KArgs a, const double* d2, double canon, int j,
+                                                            long* pick_out) {
+  extern __shared__ double sd[];
+  __shared__ double s_u;
+  __shared__ int s_done;
   const long n = a.n;
-  double total;
-  const long aligned = (n / 2) * 2;
-  if (aligned == 0) {
-    total = d2[0];
-    for (long i = 1; i < n; ++i) total = __dadd_rn(total, d2[i]);
-  } else {
-    const long aligned2 = (n / 4) * 4;
-    double p0a = d2[0], p0b = d2[1];
+  const int t = threadIdx.x;
+  const long aligned = (n / 2) * 2, aligned2 = (n / 4) * 4;
+  // ---- pass 1: Eigen's SSE2 two-packet sum ----
+  double p0a = 0.0, p0b = 0.0, p1a = 0.0, p1b = 0.0;
+  if (t == 0 && aligned > 0) {
+    p0a = d2[0];
+    p0b = d2[1];
     if (aligned > 2) {
-      double p1a = d2[2], p1b = d2[3];
-      for (long i = 4; i < aligned2; i += 4) {
-        p0a = __dadd_rn(p0a, d2[i]);
-        p0b = __dadd_rn(p0b, d2[i + 1]);
-        p1a = __dadd_rn(p1a, d2[i + 2]);
-        p1b = __dadd_rn(p1b, d2[i + 3]);
-      }
-      p0a = __dadd_rn(p0a, p1a);
-      p0b = __dadd_rn(p0b, p1b);
-      if (aligned > aligned2) {
-        p0a = __dadd_rn(p0a, d2[aligned2]);
-        p0b = __dadd_rn(p0b, d2[aligned2 + 1]);
+      p1a = d2[2];
+      p1b = d2[3];
+    }
+  }
+  if (aligned > 2) {
+    for (long c0 = 4; c0 < aligned2; c0 += kPickChunk) {  // groups of 4 never straddle a chunk
+      const long c1 = min(aligned2, c0 + kPickChunk);
+      __syncthreads();
+      for (long i = c0 + t; i < c1; i += blockDim.x) sd[i - c0] = d2[i];
+      __syncthreads();
+      if (t == 0) {
+        const int len = static_cast<int>(c1 - c0);
+        for (int i = 0; i < len; i += 4) {
+          p0a = __dadd_rn(p0a, sd[i]);
+          p0b = __dadd_rn(p0b, sd[i + 1]);
+          p1a = __dadd_rn(p1a, sd[i + 2]);
+          p1b = __dadd_rn(p1b, sd[i + 3]);
+        }
       }
     }
-    total = __dadd_rn(p0a, p0b);
-    for (long i = aligned; i < n; ++i) total = __dadd_rn(total, d2[i]);
   }
-  // uniform_real_distribution<double>(0, total): canon * (total - 0) + 0
-  const double u = __dadd_rn(__dmul_rn(canon, __dsub_rn(total, 0.0)), 0.0);
-  long pick = n - 1;
+  if (t == 0) {
+    double total;
+    if (aligned == 0) {
+      total = d2[0];
+      for (long i = 1; i < n; ++i) total = __dadd_rn(total, d2[i]);
+    } else {
+      if (aligned > 2) {
+        p0a = __dadd_rn(p0a, p1a);
+        p0b = __dadd_rn(p0b, p1b);
+        if (aligned > aligned2) {
+          p0a = __dadd_rn(p0a, d2[aligned2]);
+          p0b = __dadd_rn(p0b, d2[aligned2 + 1]);
+        }
+      }
+      total = __dadd_rn(p0a, p0b);
+      for (long i = aligned; i < n; ++i) total = __dadd_rn(total, d2[i]);
+    }
+    // uniform_real_distribution<double>(0, total): canon * (total - 0) + 0
+    s_u = __dadd_rn(__dmul_rn(canon, __dsub_rn(total, 0.0)), 0.0);
+    s_done = 0;
+  }
+  // ---- pass 2: sequential running sum, first i with u <= acc ----
   double acc = 0.0;
-  for (long i = 0; i < n; ++i) {
-    acc = __dadd_rn(acc, d2[i]);
-    if (u <= acc) {
-      pick = i;
-      break;
+  long pick = n - 1;
+  for (long c0 = 0; c0 < n; c0 += kPickChunk) {
+    const long c1 = min(n, c0 + kPickChunk);
+    __syncthreads();
+    if (s_done) break;
+    for (long i = c0 + t; i < c1; i += blockDim.x) sd[i - c0] = d2[i];
+    __syncthreads();
+    if (t == 0) {
+      const double u = s_u;
+      const int len = static_cast<int>(c1 - c0);
+      int i = 0;
+      bool hit = false;
+      for (; i + 8 <= len && !hit; i += 8) {
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = sd[i + q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (!hit) {
+            acc = __dadd_rn(acc, v[q]);
+            if (u <= acc) {
+              pick = c0 + i + q;
+              hit = true;
+            }
+          }
+        }
+      }
+      for (; i < len && !hit; ++i) {
+        acc = __dadd_rn(acc, sd[i]);
+        if (u <= acc) {
+          pick = c0 + i;
+          hit = true;
+        }
+      }
+      if (hit) s_done = 1;
     }
   }
-  *pick_out = pick;
-  for (int c = 0; c < a.d; ++c) a.C[j + static_cast<size_t>(c) * a.k] = a.P[pick + c * n];
+  if (t == 0) {
+    *pick_out = pick;
+    for (int c = 0; c < a.d; ++c) a.C[j + static_cast<size_t>(c) * a.k] = a.P[pick + c * n];
+  }
 }
 
 // Lloyd assignment: best center with strict < (first minimum)
@@ -233,8 +293,11 @@ void kmeanspp_device(stgp_ctx* ctx, const double* P_host, long n, int d, int k, 
   const int gb = grid_for(n, 256, ctx->num_sms * 8);
   d2_update_kernel<<<gb, 256, 0, st>>>(a, 0, true, d2.get());
   launched(ctx);
+  STGP_CUDA(cudaFuncSetAttribute(pick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sizeof(double) * kPickChunk)));
   for (int j = 1; j < k; ++j) {
-    pick_kernel<<<1, 32, 0, st>>>(a, d2.get(), canon[static_cast<size_t>(j)], j, pick.get());
+    pick_kernel<<<1, kPickThreads, sizeof(double) * kPickChunk, st>>>(a, d2.get(), canon[static_cast<size_t>(j)], j,
+                                                                       pick.get());
     launched(ctx);
     d2_update_kernel<<<gb, 256, 0, st>>>(a, j, false, d2.get());
     launched(ctx);
