@@ -172,6 +172,22 @@ void dev_gemm(stgp_ctx* ctx, bool ta, bool tb, int m, int n, long long k, double
                "gemm");
 }
 
+// C = alpha A A^T (n x n, both triangles) as GEMMs on the lower blocks of an nb x nb partition:
+// (nb + 1) / (2 nb) of the full product's flops at GEMM efficiency (cuBLAS SYRK tiles this
+// small-output / long-K shape poorly).  Block edges are multiples of 16.
+void dev_syrk_blocked(stgp_ctx* ctx, int n, long long k, double alpha, const double* A, int lda, double* C, int ldc,
+                      int nb) {
+  nb = std::max(1, std::min(nb, (n + 15) / 16));
+  const int bs = ((n + nb - 1) / nb + 15) / 16 * 16;
+  for (int i0 = 0; i0 < n; i0 += bs)
+    for (int j0 = 0; j0 <= i0; j0 += bs) {
+      const int mi = std::min(bs, n - i0), mj = std::min(bs, n - j0);
+      dev_gemm(ctx, false, true, mi, mj, k, alpha, A + i0, lda, A + j0, lda, 0.0, C + static_cast<size_t>(j0) * ldc + i0,
+               ldc);
+    }
+  dev_symmetrize_lower(ctx, C, ldc, n);
+}
+
 void dev_gemv(stgp_ctx* ctx, bool ta, int m, long long n, double alpha, const double* A, int lda, const double* x,
               double beta, double* y) {
   cublas_check(cublasDgemv(ctx->cublas, ta ? CUBLAS_OP_T : CUBLAS_OP_N, m, static_cast<int>(n), &alpha, A, lda, x, 1,

@@ -128,238 +128,6 @@ __global__ void __launch_bounds__(128) vprime_kernel(const double* W, int ldm, c
   }
 }
 
-// ---------------------------------------------------------------------------
-// Row-group gathers.  Rows are processed in groups of kGR consecutive rows of the spatial order
-// (time bucket, Morton): spatially adjacent rows share most neighbour columns (at cfg4 the union of
-// 8 rows' closures is ~102 columns instead of 248), so a CTA stages the union's W (or E, V')
-// columns once per k-chunk through shared memory instead of every row re-reading its 31 columns
-// from L2.  The gathers are L2-bandwidth bound, so this divides their traffic by the overlap.
-// ---------------------------------------------------------------------------
-constexpr int kGR = 8;                  // rows per group
-constexpr int kGKC = 16;                // k chunk (doubles)
-constexpr int kGKS = kGKC + 2;          // smem stride: 16 B aligned rows for cp.async
-constexpr int kGU = kGR * 32;           // union capacity: kGR closures of <= 31 + 1 columns
-constexpr int kGThreads = kGR * kGKC;   // one output element per thread per chunk
-constexpr size_t kGSmem = 96 * 1024;    // staging ring; stages sized by each group's union
-constexpr int kGMaxStages = 8;
-
-// Group metadata, built once per structure (it depends only on the neighbour sets and the
-// schedule): rows, the sorted column union, and for each (row, slot) its union position
-// (slot 31 = the row itself).  ~1.5 KB per group.
-struct GroupMeta {
-  int32_t* rows;   // ngroups x kGR (-1 padded)
-  int32_t* u;      // ngroups x kGU
-  int32_t* nu;     // ngroups
-  int16_t* pos;    // ngroups x kGR x 32 (-1: empty slot)
-  int32_t* kcnt;   // ngroups x kGR
-};
-
-__global__ void __launch_bounds__(256) group_build_kernel(int ngroups, int nrows_total, const int32_t* order, int r0,
-                                                          const int32_t* nbr, int m_v, GroupMeta gm) {
-  __shared__ int keys[kGU];
-  __shared__ int su[kGU];
-  __shared__ int rows[kGR];
-  __shared__ int snu;
-  const int t = threadIdx.x;
-  for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
-    const int g0 = g * kGR, ng = min(kGR, nrows_total - g0);
-    __syncthreads();
-    if (t < kGR) {
-      rows[t] = t < ng ? (order ? order[g0 + t] : r0 + g0 + t) : -1;
-      gm.rows[static_cast<size_t>(g) * kGR + t] = rows[t];
-    }
-    __syncthreads();
-    for (int e = t; e < kGU; e += blockDim.x) {
-      const int q = e / 32, a = e % 32, row = rows[q];
-      int key = INT_MAX;
-      if (row >= 0) {
-        if (a == 31) {
-          key = row;
-        } else if (a < m_v) {
-          const int c = nbr[static_cast<size_t>(row) * m_v + a];
-          key = c >= 0 ? c : INT_MAX;
-        }
-      }
-      keys[e] = key;
-    }
-    __syncthreads();
-    for (int size = 2; size <= kGU; size <<= 1)  // bitonic sort, ascending
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        for (int e = t; e < kGU; e += blockDim.x) {
-          const int p = e ^ stride;
-          if (p > e) {
-            const bool up = (e & size) == 0;
-            const int x = keys[e], y = keys[p];
-            if ((x > y) == up) {
-              keys[e] = y;
-              keys[p] = x;
-            }
-          }
-        }
-        __syncthreads();
-      }
-    if (t < 32) {
-      int base = 0;
-      for (int c0 = 0; c0 < kGU; c0 += 32) {
-        const int e = c0 + t, key = keys[e];
-        const bool f = key != INT_MAX && (e == 0 || keys[e - 1] != key);
-        const unsigned m = __ballot_sync(0xffffffffu, f);
-        if (f) su[base + __popc(m & ((1u << t) - 1))] = key;
-        base += __popc(m);
-      }
-      if (t == 0) snu = base;
-    }
-    __syncthreads();
-    const int nu = snu;
-    for (int e = t; e < kGU; e += blockDim.x) gm.u[static_cast<size_t>(g) * kGU + e] = e < nu ? su[e] : 0;
-    if (t == 0) gm.nu[g] = nu;
-    for (int e = t; e < kGU; e += blockDim.x) {
-      const int q = e / 32, a = e % 32, row = rows[q];
-      int key = -1;
-      if (row >= 0) key = a == 31 ? row : (a < m_v ? nbr[static_cast<size_t>(row) * m_v + a] : -1);
-      int16_t ps = -1;
-      if (key >= 0) {
-        int lo = 0, hi = nu;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (su[mid] < key) lo = mid + 1; else hi = mid;
-        }
-        ps = static_cast<int16_t>(lo);
-      }
-      gm.pos[static_cast<size_t>(g) * kGU + e] = ps;
-    }
-    if (t < kGR) {
-      int k = 0;
-      const int row = rows[t];
-      if (row >= 0)
-        while (k < m_v && nbr[static_cast<size_t>(row) * m_v + k] >= 0) ++k;
-      gm.kcnt[static_cast<size_t>(g) * kGR + t] = k;
-    }
-  }
-}
-
-__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-// wait until at most `pending` groups are outstanding (runtime count, 0..kGMaxStages-1)
-__device__ __forceinline__ void cp_wait_rt(int pending) {
-  switch (pending) {
-    case 0: cp_wait<0>(); break;
-    case 1: cp_wait<1>(); break;
-    case 2: cp_wait<2>(); break;
-    case 3: cp_wait<3>(); break;
-    case 4: cp_wait<4>(); break;
-    case 5: cp_wait<5>(); break;
-    default: cp_wait<6>(); break;
-  }
-}
-
-// Shared-memory view of one claimed group.
-struct GroupSmem {
-  int rows[kGR];
-  int u[kGU];
-  int16_t pos[kGR][32];
-  int kcnt[kGR];
-  int nu, stages, g;
-};
-
-// Claim the next group in schedule order and load its metadata; false when done.
-__device__ bool load_group(GroupSmem& G, unsigned long long* next, int ngroups, const GroupMeta& gm) {
-  const int t = threadIdx.x;
-  __syncthreads();
-  if (t == 0) G.g = static_cast<int>(atomicAdd(next, 1ull));
-  __syncthreads();
-  const int g = G.g;
-  if (g >= ngroups) return false;
-  for (int e = t; e < kGU; e += blockDim.x) {
-    G.u[e] = gm.u[static_cast<size_t>(g) * kGU + e];
-    (&G.pos[0][0])[e] = gm.pos[static_cast<size_t>(g) * kGU + e];
-  }
-  if (t < kGR) {
-    G.rows[t] = gm.rows[static_cast<size_t>(g) * kGR + t];
-    G.kcnt[t] = gm.kcnt[static_cast<size_t>(g) * kGR + t];
-  }
-  if (t == 0) {
-    const int nu = gm.nu[g];
-    G.nu = nu;
-    const int per = max(1, nu) * kGKS * static_cast<int>(sizeof(double));
-    G.stages = max(2, min(kGMaxStages, static_cast<int>(kGSmem / per)));
-  }
-  __syncthreads();
-  return true;
-}
-
-// stage rows [kc, kc + kGKC) of the union's columns of X (ldm x n) into buf[u][kk]
-__device__ __forceinline__ void stage_union(const GroupSmem& G, const double* X, int ldm, int kc, double* buf) {
-  const int pieces = G.nu * (kGKC / 2);
-  for (int e = threadIdx.x; e < pieces; e += blockDim.x) {
-    const int u = e / (kGKC / 2), pc = e % (kGKC / 2);
-    cp16(buf + u * kGKS + 2 * pc, X + static_cast<size_t>(G.u[u]) * ldm + kc + 2 * pc);
-  }
-}
-
-// Ring of G.stages chunk buffers over the union's columns; body(ch, buf) consumes chunk ch.
-template <typename Body>
-__device__ __forceinline__ void union_pipeline(const GroupSmem& G, const double* X, int ldm, double* ring, Body body) {
-  const int nch = ldm / kGKC, S = G.stages;
-  const size_t stride = static_cast<size_t>(max(1, G.nu)) * kGKS;
-  for (int c = 0; c < S - 1; ++c) {
-    if (c < nch) stage_union(G, X, ldm, c * kGKC, ring + (c % S) * stride);
-    cp_commit();
-  }
-  for (int ch = 0; ch < nch; ++ch) {
-    cp_wait_rt(S - 2);
-    __syncthreads();  // chunk ch staged; the buffer refilled next was consumed in iteration ch - 1
-    if (ch + S - 1 < nch) stage_union(G, X, ldm, (ch + S - 1) * kGKC, ring + ((ch + S - 1) % S) * stride);
-    cp_commit();
-    body(ch, ring + (ch % S) * stride);
-  }
-  cp_wait<0>();
-}
-
-// V' for a group: V'_i = W_i - sum_a A_ia W_{N_a} (same algebra as vprime_kernel)
-__global__ void __launch_bounds__(kGThreads) vprime_group_kernel(const double* W, int ldm, int m_v, const double* A,
-                                                                 int ngroups, GroupMeta gm, unsigned long long* next,
-                                                                 double* Vp) {
-  extern __shared__ double gbuf[];
-  __shared__ GroupSmem G;
-  __shared__ double sA[kGR][32];
-  const int t = threadIdx.x, q = t / kGKC, kk = t % kGKC;
-  while (load_group(G, next, ngroups, gm)) {
-    for (int e = t; e < kGR * 32; e += blockDim.x) {
-      const int qq = e / 32, a = e % 32, row = G.rows[qq];
-      sA[qq][a] = (row >= 0 && a < m_v) ? A[static_cast<size_t>(row) * m_v + a] : 0.0;
-    }
-    __syncthreads();
-    const int row = G.rows[q], kq = G.kcnt[q];
-    // the row's slot offsets and coefficients in registers: the 31 loads of a chunk are independent
-    const int self = row >= 0 ? G.pos[q][31] * kGKS + kk : kk;
-    int off[31];
-    double ca[31];
-#pragma unroll
-    for (int a = 0; a < 31; ++a) {
-      const int ps = G.pos[q][a];
-      off[a] = (a < kq && ps >= 0) ? ps * kGKS + kk : self;
-      ca[a] = a < kq ? -sA[q][a] : 0.0;
-    }
-    union_pipeline(G, W, ldm, gbuf, [&](int ch, const double* buf) {
-      if (row >= 0) {
-        double acc = 0.0;
-#pragma unroll
-        for (int a = 0; a < 31; ++a) acc = fma(ca[a], buf[off[a]], acc);
-        acc += buf[self];
-        Vp[static_cast<size_t>(row) * ldm + ch * kGKC + kk] = acc;
-      }
-    });
-  }
-}
-
 // out(:, i) = in(:, i) * s_i
 __global__ void scale_cols_kernel(const double* in, int ldm, long long ncols, const double* s, bool rsqrt_of,
                                   double* out) {
@@ -810,41 +578,6 @@ std::vector<int32_t> locality_order(const stgp_dataset* ds, int lo, int hi) {
   return out;
 }
 
-// row-group gathers need the spatial schedule, m_v <= 31 and ldm a multiple of the chunk
-static bool use_groups(const stgp_structure* s) {
-  // opt-in (STGP_GROUPS=1): at cfg4 the per-thread gather is faster (it stays under the L2 roofline and
-  // the staged version is bound by its index arithmetic at 12.5% occupancy, profiles/r01)
-  return s->rorder.get() != nullptr && s->m_v <= 31 && s->lr.ldm % kGKC == 0 && std::getenv("STGP_GROUPS");
-}
-static GroupMeta group_meta(stgp_structure* s) {
-  return GroupMeta{s->g_rows.get(), s->g_u.get(), s->g_nu.get(), s->g_pos.get(), s->g_kcnt.get()};
-}
-// group metadata of this shard's rows, once per structure (neighbour sets and schedule are fixed)
-static void ensure_groups(stgp_structure* s) {
-  if (s->groups_built) return;
-  stgp_ctx* ctx = s->ds->ctx;
-  const int nrows = s->row_end - s->row_begin;
-  s->ngroups = (nrows + kGR - 1) / kGR;
-  const size_t ng = static_cast<size_t>(std::max(1, s->ngroups));
-  s->g_rows.ensure(ng * kGR);
-  s->g_u.ensure(ng * kGU);
-  s->g_nu.ensure(ng);
-  s->g_pos.ensure(ng * kGU);
-  s->g_kcnt.ensure(ng * kGR);
-  if (s->ngroups > 0) {
-    group_build_kernel<<<std::min(s->ngroups, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
-        s->ngroups, nrows, s->rorder.get(), s->row_begin, s->nbr.get(), s->m_v, group_meta(s));
-    launched(ctx);
-  }
-  s->groups_built = true;
-}
-template <typename K>
-static int group_grid(stgp_ctx* ctx, K kern) {
-  int per_sm = 0;
-  STGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGThreads, kGSmem));
-  return std::max(1, per_sm) * ctx->num_sms;
-}
-
 ZPts zpts(const stgp_structure* s) { return ZPts{s->lr.zx.get(), s->lr.zy.get(), s->lr.ztid.get()}; }
 
 void lowrank_setup(stgp_structure* s, const stgp_inducing* ind) {
@@ -852,7 +585,7 @@ void lowrank_setup(stgp_structure* s, const stgp_inducing* ind) {
   LowRank& L = s->lr;
   L.M = ind->M();
   L.zxyt = ind->xyt;
-  L.ldm = std::max(16, (L.M + 15) / 16 * 16);  // multiple of the row-group chunk
+  L.ldm = std::max(16, (L.M + 15) / 16 * 16);
   std::vector<double> zx(L.M), zy(L.M), zt(L.M);
   for (int j = 0; j < L.M; ++j) {
     zx[j] = ind->xyt[3 * j];
@@ -878,7 +611,7 @@ void lowrank_setup(stgp_structure* s, const stgp_inducing* ind) {
   const std::string omode = om ? om : "none";
   s->order_rows = omode == "rows" || omode == "all";
   s->order_gather = omode == "all";
-  if (s->kind == STGP_VIF) {  // spatial schedule: row-group gathers, and the opt-in orders above
+  if (s->kind == STGP_VIF && (s->order_rows || s->order_gather)) {
     const std::vector<int32_t> ro = locality_order(s->ds, s->row_begin, s->row_end);
     const std::vector<int32_t> co = locality_order(s->ds, s->col_begin, s->row_end);
     if (!ro.empty()) s->rorder.upload(ro.data(), ro.size(), st);
@@ -1092,17 +825,9 @@ void vif_build(stgp_structure* s) {
   L.Vp.ensure(total);
   if (re > rb) {
     ProfRegion pr(ctx, "vprime");
-    if (use_groups(s)) {
-      ensure_groups(s);
-      STGP_CUDA(cudaFuncSetAttribute(vprime_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kGSmem)));
-      vprime_group_kernel<<<group_grid(ctx, vprime_group_kernel), kGThreads, kGSmem, ctx->stream>>>(
-          L.W.get(), ldm, s->m_v, s->A.get(), s->ngroups, group_meta(s), claim_counter(ctx), L.Vp.get());
-    } else {
-      vprime_kernel<<<std::min(re - rb, ctx->num_sms * 16), 128, 0, ctx->stream>>>(
-          L.W.get(), ldm, s->nbr.get(), s->m_v, s->A.get(), rb, re, s->order_gather ? s->rorder.get() : nullptr,
-          claim_counter(ctx), L.Vp.get());
-    }
+    vprime_kernel<<<std::min(re - rb, ctx->num_sms * 16), 128, 0, ctx->stream>>>(
+        L.W.get(), ldm, s->nbr.get(), s->m_v, s->A.get(), rb, re, s->order_gather ? s->rorder.get() : nullptr,
+        claim_counter(ctx), L.Vp.get());
     launched(ctx);
   }
   ProfRegion prk(ctx, "K_gemm_chol");
@@ -1111,10 +836,14 @@ void vif_build(stgp_structure* s) {
   scale_cols(ctx, L.Vp.get() + off, ldm, re - rb, s->D.get() + rb, true, L.work1.get() + off);
   L.Mc.ensure(static_cast<size_t>(ldm) * ldm);
   STGP_CUDA(cudaMemsetAsync(L.Mc.get(), 0, sizeof(double) * ldm * ldm, ctx->stream));
-  // full S S^T by GEMM: cuBLAS SYRK tiles this small-output / long-K shape poorly
-  if (re > rb)
-    dev_gemm(ctx, false, true, ldm, ldm, re - rb, 1.0, L.work1.get() + off, ldm, L.work1.get() + off, ldm, 0.0,
-             L.Mc.get(), ldm);
+  // S S^T as GEMMs over the lower blocks of a partition (dense.cu dev_syrk_blocked)
+  if (re > rb) {
+    static const int kblocks = [] {
+      const char* e = std::getenv("STGP_KBLOCKS");
+      return e ? std::max(1, std::atoi(e)) : 4;  // 5/8 of the GEMM flops; measured best at M = 906
+    }();
+    dev_syrk_blocked(ctx, ldm, re - rb, 1.0, L.work1.get() + off, ldm, L.Mc.get(), ldm, kblocks);
+  }
   allreduce_sum(ctx, L.Mc.get(), static_cast<size_t>(ldm) * ldm);
   add_identity(ctx, L.Mc.get(), ldm);
   L.Kfull.ensure(static_cast<size_t>(ldm) * ldm);

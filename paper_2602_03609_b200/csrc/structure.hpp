@@ -70,11 +70,6 @@ struct stgp_structure {
   // locality schedule (lowrank.cu: locality_order): rows [row_begin, row_end), columns [col_begin, row_end)
   stgp::DevBuf<int32_t> rorder, corder;
   bool order_rows = false, order_gather = false;
-  // row groups of the spatial schedule (lowrank.cu: group_build_kernel), built once
-  bool groups_built = false;
-  int ngroups = 0;
-  stgp::DevBuf<int32_t> g_rows, g_u, g_nu, g_kcnt;
-  stgp::DevBuf<int16_t> g_pos;
 };
 
 namespace stgp {
