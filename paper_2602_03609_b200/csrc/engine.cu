@@ -335,6 +335,14 @@ RowArgs row_args(stgp_structure* s, const double* W, int ldw, double nugget) {
   a.nugget = nugget;
   a.W = W;
   a.ldw = ldw;
+  if (W) {
+    if (s->zcol_n < ldw) {
+      s->zcol.alloc(static_cast<size_t>(ldw));
+      s->zcol.zero(s->ds->ctx->stream);
+      s->zcol_n = ldw;
+    }
+    a.zcol = s->zcol.get();
+  }
   a.r = s->r.get();
   a.A_out = s->A.get();
   a.D_out = s->D.get();

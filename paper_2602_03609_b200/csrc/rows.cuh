@@ -67,6 +67,7 @@ struct RowArgs {
   // VIF: whitened cross covariance, column-major ldw x n (rows >= M are 0)
   const double* W;
   int ldw;
+  const double* zcol;  // ldw zeros: the fragment source of empty closure slots (no load predicates)
   const double* r;  // residual y - X beta (NLL / gradient modes)
   double* A_out;    // n * m_v (optional)
   double* D_out;    // n (optional)
@@ -129,7 +130,7 @@ __device__ __forceinline__ void row_acc(const RowArgs& a, double* tot, int i, in
 template <int LD, bool WITH_X>
 __device__ __forceinline__ void closure_gram_dmma(const double* __restrict__ W, int ldw, const int* scol,
                                                   double* sG, int lane, const double* __restrict__ xcol,
-                                                  double* sGa) {
+                                                  double* sGa, const double* __restrict__ zcol) {
   const int grp = lane >> 2, tig = lane & 3;
   double acc[10][2];
   double accx[4][2];
@@ -141,37 +142,43 @@ __device__ __forceinline__ void closure_gram_dmma(const double* __restrict__ W, 
 #pragma unroll
   for (int I = 0; I < 4; ++I) {
     const int c = scol[8 * I + grp];
-    colp[I] = c >= 0 ? W + static_cast<size_t>(c) * ldw + tig : nullptr;
+    colp[I] = (c >= 0 ? W + static_cast<size_t>(c) * ldw : zcol) + tig;
   }
+  const double* px = WITH_X ? xcol + tig : zcol + tig;
   // software pipelined: the next k-step's fragments are in flight while this step's DMMAs issue
-  // (the loop is L2-latency bound otherwise).  ldw is a multiple of 8.
+  // (L2-latency bound otherwise); empty slots read the zero column, so the loads carry no
+  // predicates.  ldw is a multiple of 8.
   double f[4], bx = 0.0;
 #pragma unroll
-  for (int I = 0; I < 4; ++I) f[I] = colp[I] ? __ldg(colp[I]) : 0.0;
-  if (WITH_X) bx = grp == 0 ? __ldg(xcol + tig) : 0.0;
-#pragma unroll 2
-  for (int kb = 0; kb < ldw; kb += 4) {
-    const int kn = kb + 4 < ldw ? kb + 4 : kb;
-    double fn[4], bxn = 0.0;
-#pragma unroll
-    for (int I = 0; I < 4; ++I) fn[I] = colp[I] ? __ldg(colp[I] + kn) : 0.0;
+  for (int I = 0; I < 4; ++I) f[I] = __ldg(colp[I]);
+  if (WITH_X) bx = __ldg(px);
+  auto step = [&](const double* fa, double xb) {
     if (WITH_X) {
-      bxn = grp == 0 ? __ldg(xcol + kn + tig) : 0.0;
+      const double b = grp == 0 ? xb : 0.0;
 #pragma unroll
-      for (int I = 0; I < 4; ++I) dmma_f64(accx[I][0], accx[I][1], f[I], bx);
+      for (int I = 0; I < 4; ++I) dmma_f64(accx[I][0], accx[I][1], fa[I], b);
     }
     int t = 0;
 #pragma unroll
     for (int I = 0; I < 4; ++I)
 #pragma unroll
       for (int J = 0; J <= I; ++J) {
-        dmma_f64(acc[t][0], acc[t][1], f[I], f[J]);
+        dmma_f64(acc[t][0], acc[t][1], fa[I], fa[J]);
         ++t;
       }
+  };
+#pragma unroll 4
+  for (int kb = 4; kb < ldw; kb += 4) {
+    double fn[4], bxn = 0.0;
+#pragma unroll
+    for (int I = 0; I < 4; ++I) fn[I] = __ldg(colp[I] + kb);
+    if (WITH_X) bxn = __ldg(px + kb);
+    step(f, bx);
 #pragma unroll
     for (int I = 0; I < 4; ++I) f[I] = fn[I];
     bx = bxn;
   }
+  step(f, bx);
   int t = 0;
 #pragma unroll
   for (int I = 0; I < 4; ++I)
@@ -239,7 +246,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
     if (HAS_W)
       closure_gram_dmma<LD, MODE == kModeVifGrad>(a.W, a.ldw, scol[w], C, lane,
                                                  MODE == kModeVifGrad ? a.X + static_cast<size_t>(i) * a.ldw : nullptr,
-                                                 sAw[w][0]);  // Gram staged in C
+                                                 sAw[w][0], a.zcol);  // Gram staged in C
     __syncwarp();
     double Ga = 0.0, aGa = 0.0;
     if (MODE == kModeVifGrad) {
@@ -444,7 +451,8 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
 
 // Ga[s] = W_{cl_s} . x for the 32 closure slots (4 DMMA blocks per k-step).
 __device__ __forceinline__ void closure_x_dmma(const double* __restrict__ W, int ldw, const int* scol,
-                                               const double* __restrict__ xcol, double* sGa, int lane) {
+                                               const double* __restrict__ xcol, double* sGa, int lane,
+                                               const double* __restrict__ zcol) {
   const int grp = lane >> 2, tig = lane & 3;
   double accx[4][2];
 #pragma unroll
@@ -453,34 +461,41 @@ __device__ __forceinline__ void closure_x_dmma(const double* __restrict__ W, int
 #pragma unroll
   for (int I = 0; I < 4; ++I) {
     const int c = scol[8 * I + grp];
-    colp[I] = c >= 0 ? W + static_cast<size_t>(c) * ldw + tig : nullptr;
+    colp[I] = (c >= 0 ? W + static_cast<size_t>(c) * ldw : zcol) + tig;
   }
-  // two k-steps of fragments in flight (L2-latency bound otherwise); ldw is a multiple of 8
-  double f[4], f1[4], bx, bx1;
+  const double* px = xcol + tig;
+  // two k-steps of fragments in flight (L2-latency bound otherwise); no load predicates (empty
+  // slots read the zero column); ldw is a multiple of 8
+  double f0[4], f1[4], x0, x1;
 #pragma unroll
   for (int I = 0; I < 4; ++I) {
-    f[I] = colp[I] ? __ldg(colp[I]) : 0.0;
-    f1[I] = colp[I] ? __ldg(colp[I] + 4) : 0.0;
+    f0[I] = __ldg(colp[I]);
+    f1[I] = __ldg(colp[I] + 4);
   }
-  bx = grp == 0 ? __ldg(xcol + tig) : 0.0;
-  bx1 = grp == 0 ? __ldg(xcol + 4 + tig) : 0.0;
-#pragma unroll 2
-  for (int kb = 0; kb < ldw; kb += 4) {
-    const int kn = kb + 8 < ldw ? kb + 8 : kb;
+  x0 = __ldg(px);
+  x1 = __ldg(px + 4);
+  auto step = [&](const double* fa, double xb) {
+    const double b = grp == 0 ? xb : 0.0;
+#pragma unroll
+    for (int I = 0; I < 4; ++I) dmma_f64(accx[I][0], accx[I][1], fa[I], b);
+  };
+#pragma unroll 4
+  for (int kb = 8; kb < ldw; kb += 4) {
     double fn[4];
 #pragma unroll
-    for (int I = 0; I < 4; ++I) fn[I] = colp[I] ? __ldg(colp[I] + kn) : 0.0;
-    const double bxn = grp == 0 ? __ldg(xcol + kn + tig) : 0.0;
-#pragma unroll
-    for (int I = 0; I < 4; ++I) dmma_f64(accx[I][0], accx[I][1], f[I], bx);
+    for (int I = 0; I < 4; ++I) fn[I] = __ldg(colp[I] + kb);
+    const double xn = __ldg(px + kb);
+    step(f0, x0);
 #pragma unroll
     for (int I = 0; I < 4; ++I) {
-      f[I] = f1[I];
+      f0[I] = f1[I];
       f1[I] = fn[I];
     }
-    bx = bx1;
-    bx1 = bxn;
+    x0 = x1;
+    x1 = xn;
   }
+  step(f0, x0);
+  step(f1, x1);
   if (tig == 0)
 #pragma unroll
     for (int I = 0; I < 4; ++I) sGa[8 * I + grp] = accx[I][0];
@@ -499,6 +514,12 @@ __global__ void __launch_bounds__(kRowWarps * 32) vif_grad_stored_kernel(RowArgs
   __shared__ double sx[kRowWarps][32], sy[kRowWarps][32], sAw[kRowWarps][2][32], sGa[kRowWarps][32];
   __shared__ int st[kRowWarps][32], scol[kRowWarps][32];
   __shared__ double sred[kRowWarps][8];
+  // per-row cache of the temporal factors of the closure's time classes (a row's closure spans a
+  // few distinct times: the KG loop then reads TF from shared memory instead of two dependent
+  // global lookups per pair)
+  constexpr int kMaxCls = 4;
+  __shared__ TF stf[kRowWarps][kMaxCls * kMaxCls];
+  __shared__ int scls[kRowWarps][32], sctid[kRowWarps][kMaxCls];
   for (int p = threadIdx.x; p < NP; p += blockDim.x) {
     int aa = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * static_cast<float>(p))) * 0.5f);
     while (aa * (aa - 1) / 2 > p) --aa;
@@ -529,7 +550,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) vif_grad_stored_kernel(RowArgs
     scol[w][lane] = pt;
     __syncwarp();
     const double* xi = a.X + static_cast<size_t>(i) * a.ldw;
-    closure_x_dmma(a.W, a.ldw, scol[w], xi, sGa[w], lane);
+    closure_x_dmma(a.W, a.ldw, scol[w], xi, sGa[w], lane, a.zcol);
     double aGa = 0.0;
     const double* vi = a.Vp + static_cast<size_t>(i) * a.ldw;
     for (int j = lane; j < a.ldw; j += 32) aGa = fma(__ldg(&vi[j]), __ldg(&xi[j]), aGa);
@@ -574,6 +595,19 @@ __global__ void __launch_bounds__(kRowWarps * 32) vif_grad_stored_kernel(RowArgs
     if (lane < a.m_v) a.Rv_out[static_cast<size_t>(i) * a.m_v + lane] = Rv;
     sAw[w][0][lane] = lane < k ? -Aval : (lane == KS ? 1.0 : 0.0);
     sAw[w][1][lane] = Rv;
+    // time classes of the closure slots
+    const int myt = pt >= 0 ? st[w][lane] : -1;
+    const unsigned same = __match_any_sync(kFull, myt);
+    const int leader = __ffs(same) - 1;
+    const unsigned leaders = __ballot_sync(kFull, lane == leader && pt >= 0);
+    const int nc = __popc(leaders);
+    const bool cached = nc <= kMaxCls;
+    if (cached) {
+      scls[w][lane] = __popc(leaders & ((1u << leader) - 1));
+      if (lane == leader && pt >= 0) sctid[w][__popc(leaders & ((1u << lane) - 1))] = myt;
+      __syncwarp();
+      if (lane < nc * nc) stf[w][lane] = a.lt.get(sctid[w][lane / nc], sctid[w][lane % nc]);
+    }
     __syncwarp();
     const int P = (k + 1) * k / 2;
     double g[6] = {0, 0, 0, 0, 0, 0};
@@ -581,7 +615,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) vif_grad_stored_kernel(RowArgs
       const int pr = sPair[p];
       const int ca = pr & 0xff, sb = pr >> 8;
       const int sa = ca == k ? KS : ca;
-      const TF f = a.lt.get(st[w][sa], st[w][sb]);
+      const TF f = cached ? stf[w][scls[w][sa] * nc + scls[w][sb]] : a.lt.get(st[w][sa], st[w][sb]);
       double kg[6];
       gneiting_grad_fast(a.k, a.inv_c, spatial_dist(sx[w][sa], sy[w][sa], sx[w][sb], sy[w][sb]), f, kg);
       const double ta = sAw[w][0][sa], tb = sAw[w][0][sb], wa = sAw[w][1][sa], wb = sAw[w][1][sb];

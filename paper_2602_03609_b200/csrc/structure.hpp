@@ -61,6 +61,8 @@ struct stgp_structure {
   stgp::Reducer red;
   stgp::DevBuf<int> fail;
   stgp::DevBuf<double> r, ywork, Xwork, betaw, u, scratch, row_part;
+  stgp::DevBuf<double> zcol;  // ldw zeros (fragment source of empty closure slots)
+  int zcol_n = 0;
   stgp::LowRank lr;
   bool built = false;
   // CSC of B's pattern for deterministic B^T products
