@@ -65,6 +65,7 @@ struct stgp_ctx {
   void* host_allreduce_user = nullptr;
   stgp::DevBuf<int> iscr;     // small persistent scratch (flags, scalars)
   stgp::DevBuf<double> dscr;
+  stgp::DevBuf<double> sel_W;  // d_r search: whitened cross covariance, kept across searches (8 GB at cfg4)
   // live per-region kernel timing (stgp_ctx_profile)
   bool prof = false;
   std::map<std::string, std::pair<double, int64_t>> prof_acc;

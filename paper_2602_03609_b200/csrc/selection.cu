@@ -277,15 +277,36 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
   }
 }
 
-// r_i = sigma1_2 - |w_i|^2 (sequential fma from 0); degenerate flag
-__global__ void resid_kernel(const double* W, int M, int ldm, int n, double s1, double* resid, int* degen) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const double* w = W + static_cast<size_t>(i) * ldm;
+// r_i = sigma1_2 - |w_i|^2 (sequential fma from 0); degenerate flag.  One thread per row keeps
+// the chain; the warp stages its 32 rows' k-chunks through shared memory with coalesced loads
+// (a thread streaming its own 7 KB column alone touches 32 lines per warp load).
+constexpr int kResRows = 128;
+__global__ void __launch_bounds__(kResRows) resid_kernel(const double* W, int M, int ldm, int n, double s1,
+                                                         double* resid, int* degen) {
+  __shared__ double sw[kResRows / 32][32][33];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  for (int base = blockIdx.x * kResRows; base < n; base += gridDim.x * kResRows) {
+    const int i = base + threadIdx.x;
+    const int r0 = base + wq * 32;
     double acc = 0.0;
-    for (int k2 = 0; k2 < M; ++k2) acc = __fma_rn(w[k2], w[k2], acc);
-    const double r = M > 0 ? __dsub_rn(s1, acc) : s1;
-    resid[i] = r;
-    degen[i] = r <= 1e-7 * s1 ? 1 : 0;
+    for (int k0 = 0; k0 < M; k0 += 32) {
+      __syncwarp();
+      for (int rr = 0; rr < 32; ++rr) {
+        const int row = r0 + rr;
+        sw[wq][rr][lane] = (row < n && k0 + lane < M) ? W[static_cast<size_t>(row) * ldm + k0 + lane] : 0.0;
+      }
+      __syncwarp();
+      const int kn = min(32, M - k0);
+      for (int kk = 0; kk < kn; ++kk) {
+        const double v = sw[wq][lane][kk];
+        acc = __fma_rn(v, v, acc);
+      }
+    }
+    if (i < n) {
+      const double r = M > 0 ? __dsub_rn(s1, acc) : s1;
+      resid[i] = r;
+      degen[i] = r <= 1e-7 * s1 ? 1 : 0;
+    }
   }
 }
 
@@ -399,7 +420,7 @@ __global__ void __launch_bounds__(256) tile_groups_kernel(DrTiles T, const doubl
 constexpr int kQT = 64;   // queries per CTA
 constexpr int kCT = 64;   // candidates per tile
 constexpr int kKC = 16;   // K chunk staged per pipeline stage
-constexpr int kKS = kKC + 4;  // smem row stride (doubles): conflict-free DMMA fragment loads
+constexpr int kKS = kKC + 4;  // smem row stride (doubles, = 4 mod 16): conflict-free DMMA fragment loads
 constexpr int kStages = 3;
 constexpr int kDrThreads = 256;
 
@@ -821,7 +842,10 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
     dzt.upload(ztid.data(), M, st);
     const int ldm = std::max(kKC, (M + kKC - 1) / kKC * kKC);  // zero rows [M, ldm): exact extra fma(0, 0, g)
     lap("setup");
-    DevBuf<double> W(static_cast<size_t>(ldm) * n), resid(n);
+    // W lives in the context between searches: an 8 GB cudaMalloc / cudaFree per call costs 0.1-1 s
+    DevBuf<double>& W = ctx->sel_W;
+    W.ensure(static_cast<size_t>(ldm) * n);
+    DevBuf<double> resid(n);
     lap("alloc W");
     STGP_CUDA(cudaMemsetAsync(W.get(), 0, sizeof(double) * ldm * n, st));
     DevBuf<int32_t> degen(n);
@@ -865,7 +889,9 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
         launched(ctx);
         lap("w:whiten_seq");
       }
-      resid_kernel<<<grid_for(n), 256, 0, st>>>(W.get(), M, ldm, n, p.sigma1_2, resid.get(), degen.get());
+      ProfRegion prr(ctx, "dr_resid");
+      resid_kernel<<<std::max(1, std::min(ceil_div(n, kResRows), ctx->num_sms * 16)), kResRows, 0, st>>>(
+          W.get(), M, ldm, n, p.sigma1_2, resid.get(), degen.get());
       launched(ctx);
     }
     lap("whiten");
