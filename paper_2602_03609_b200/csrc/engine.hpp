@@ -66,6 +66,7 @@ struct stgp_ctx {
   stgp::DevBuf<int> iscr;     // small persistent scratch (flags, scalars)
   stgp::DevBuf<double> dscr;
   stgp::DevBuf<double> sel_W;  // d_r search: whitened cross covariance, kept across searches (8 GB at cfg4)
+  stgp::DevBuf<uint16_t> sel_W16;  // d_r search: its fp16 copy for the certified filter
   // live per-region kernel timing (stgp_ctx_profile)
   bool prof = false;
   std::map<std::string, std::pair<double, int64_t>> prof_acc;

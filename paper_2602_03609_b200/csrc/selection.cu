@@ -20,6 +20,7 @@
 #include <set>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cuda_fp16.h>
 
 #include "comm.hpp"
 #include "lowrank_common.cuh"
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
 // (a thread streaming its own 7 KB column alone touches 32 lines per warp load).
 constexpr int kResRows = 128;
 __global__ void __launch_bounds__(kResRows) resid_kernel(const double* W, int M, int ldm, int n, double s1,
-                                                         double* resid, int* degen) {
+                                                         double* resid, int* degen, double* wnorm) {
   __shared__ double sw[kResRows / 32][32][33];
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
   for (int base = blockIdx.x * kResRows; base < n; base += gridDim.x * kResRows) {
@@ -306,7 +307,21 @@ __global__ void __launch_bounds__(kResRows) resid_kernel(const double* W, int M,
       const double r = M > 0 ? __dsub_rn(s1, acc) : s1;
       resid[i] = r;
       degen[i] = r <= 1e-7 * s1 ? 1 : 0;
+      wnorm[i] = sqrt(acc) * (1.0 + 1e-12);  // >= |w_i| (the chain's rounding is ~M ulp)
     }
+  }
+}
+
+// Half-precision copy of W for the d_r filter Gram: W16[i][k] = fp16(2^8 W[k][i]) (column i
+// contiguous, ld16 a multiple of 64, zero padded).  The 2^8 scale keeps |w| >= 2^-22 normal.
+constexpr double kW16Scale = 256.0;
+__global__ void w16_kernel(const double* W, int M, int ldm, int n, int ld16, __half* W16) {
+  const long long total = static_cast<long long>(n) * ld16;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = e / ld16;
+    const int k = static_cast<int>(e - i * ld16);
+    W16[e] = __double2half(k < M ? W[i * ldm + k] * kW16Scale : 0.0);
   }
 }
 
@@ -433,6 +448,10 @@ struct DrArgs {
   int32_t* out;
   double* dist;
   DrTiles T;
+  // certified half-precision filter (0 = off): W16 (ld16 halves per column), |w_i| bounds
+  const __half* W16;
+  int ld16;
+  const double* wnorm;
   int prune;                  // exact tile pruning (time-sorted rows)
   double s1;
   unsigned long long* stats;  // optional: [0] candidate tiles evaluated, [1] tiles pruned
@@ -490,6 +509,141 @@ constexpr size_t kDrStageDoubles = 2 * kQT * kKS;
 constexpr size_t kDrSmem =
     sizeof(double) * (kStages * kDrStageDoubles + kQT * 32) + sizeof(int) * kQT * 32;
 static_assert(kStages * kDrStageDoubles >= kQT * (kCT + 1), "distance tile aliases the stages");
+
+// Certified half-precision filter for one (query tile, candidate tile) pair.  G~ = W16_Q^T W16_C on
+// the FP16 tensor pipe (mma.m16n8k16, f32 accumulate) bounds the exact chain G within
+//   |G~ - G| <= 3e-3 |w_i||w_j| + 1e-5 (|w_i| + |w_j|)
+// (inputs rounded to fp16: 2 * 2^-11 relative; f32 accumulation of <= 1024 products: 1024 * 2^-24 with
+// a 16x margin for the tensor core's summation; the 2^8 prescale keeps values >= 2^-22 normal, and
+// flushed ones contribute < 2^-22 each).  A pair can enter i's list only if the resulting lower bound
+// of d_r does not exceed i's current worst entry; the tile is skipped when no pair can.  Block-wide
+// (all threads), returns the same value in every thread.
+constexpr int kHK = 64;        // halves per staged chunk
+constexpr int kHS = kHK + 8;   // smem row stride (halves): conflict-free 32-bit fragment loads
+static_assert(2 * kQT * kHS * 2 <= static_cast<int>(sizeof(double) * 2 * kQT * kKS), "half stage fits a ring slot");
+
+__device__ __forceinline__ void hmma_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                           uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* qidx, const int* cidx, const int* qm,
+                                     const double (*topd)[32], const int (*topj)[32]) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int grp = lane >> 2, tig = lane & 3, wr = wid >> 1, wc = wid & 1;
+  float hc[4][4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) hc[v][e] = 0.f;
+  const int nhc = a.ld16 / kHK;
+  constexpr int kHPieces = 2 * kQT * (kHK / 8);  // 16-byte pieces per stage
+  static_assert(kHPieces % kDrThreads == 0, "half staging split");
+  auto stage = [&](int ch) {
+    __half* hQ = reinterpret_cast<__half*>(ring + static_cast<size_t>(ch % kStages) * kDrStageDoubles);
+    __half* hC = hQ + kQT * kHS;
+#pragma unroll
+    for (int it = 0; it < kHPieces / kDrThreads; ++it) {
+      const int pc = tid + it * kDrThreads;
+      const int which = pc / (kQT * (kHK / 8));
+      const int rem = pc % (kQT * (kHK / 8));
+      const int col = rem / (kHK / 8), piece = rem % (kHK / 8);
+      const int g0 = which ? cidx[col] : qidx[col];
+      const int g = g0 >= 0 ? g0 : 0;
+      cp_async16((which ? hC : hQ) + col * kHS + 8 * piece,
+                 a.W16 + static_cast<size_t>(g) * a.ld16 + static_cast<size_t>(ch) * kHK + 8 * piece);
+    }
+  };
+#pragma unroll
+  for (int ch = 0; ch < kStages - 1; ++ch) {
+    if (ch < nhc) stage(ch);
+    cp_async_commit();
+  }
+  for (int ch = 0; ch < nhc; ++ch) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    if (ch + kStages - 1 < nhc) stage(ch + kStages - 1);
+    cp_async_commit();
+    const __half* hQ = reinterpret_cast<const __half*>(ring + static_cast<size_t>(ch % kStages) * kDrStageDoubles);
+    const __half* hC = hQ + kQT * kHS;
+#pragma unroll
+    for (int ks = 0; ks < kHK; ks += 16) {
+      const int r0 = 16 * wr + grp;
+      const uint32_t a0 = *reinterpret_cast<const uint32_t*>(hQ + r0 * kHS + ks + 2 * tig);
+      const uint32_t a1 = *reinterpret_cast<const uint32_t*>(hQ + (r0 + 8) * kHS + ks + 2 * tig);
+      const uint32_t a2 = *reinterpret_cast<const uint32_t*>(hQ + r0 * kHS + ks + 8 + 2 * tig);
+      const uint32_t a3 = *reinterpret_cast<const uint32_t*>(hQ + (r0 + 8) * kHS + ks + 8 + 2 * tig);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int cc = 32 * wc + 8 * v + grp;
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(hC + cc * kHS + ks + 2 * tig);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(hC + cc * kHS + ks + 8 + 2 * tig);
+        hmma_16816(hc[v], a0, a1, a2, a3, b0, b1);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  // pair test: can (i, j) still enter i's list?  k(i, j) in single precision with the fast exp:
+  // |k_f - k| <= 1e-5 |k_f| + 1e-30 covers its ~10 roundings and the 2-ulp __expf (rel. ~1.3e-6).
+  int surv = 0;
+  constexpr double kUnscale = 1.0 / (kW16Scale * kW16Scale);
+  const float cf = static_cast<float>(a.k.c), s1f = static_cast<float>(a.k.s1);
+  int iq[2];
+  float xq[2], yq[2];
+  double rq[2], wq[2], dwq[2];
+  int tq[2], mq[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int qq = 16 * wr + grp + 8 * h;
+    const int i = qidx[qq], m = qm[qq];
+    iq[h] = i;
+    mq[h] = m;
+    if (i >= 0) {
+      xq[h] = static_cast<float>(a.x[i]);
+      yq[h] = static_cast<float>(a.y[i]);
+      tq[h] = a.tid[i];
+      rq[h] = a.resid[i];
+      wq[h] = a.wnorm[i];
+      dwq[h] = m > 0 ? topd[qq][m - 1] : 0.0;
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < 4; ++v)
+#pragma unroll
+    for (int e2 = 0; e2 < 2; ++e2) {
+      const int cc = 32 * wc + 8 * v + 2 * tig + e2;
+      const int j = cidx[cc];
+      if (j < 0 || surv) continue;
+      const bool dj = a.degen[j] != 0;
+      const float xj = static_cast<float>(a.x[j]), yj = static_cast<float>(a.y[j]);
+      const int tj = a.tid[j];
+      const double rj = a.resid[j], wj = a.wnorm[j];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = iq[h], m = mq[h];
+        if (i < 0 || j >= i || m <= 0) continue;
+        const double dw = dwq[h];
+        if (dj) {  // d = 1 exactly
+          if (lex_less(1.0, j, dw, topj[16 * wr + grp + 8 * h][m - 1])) surv = 1;
+          continue;
+        }
+        double pe, pb;
+        a.lt.get2(tq[h], tj, pe, pb);
+        const float dx = xq[h] - xj, dy = yq[h] - yj;
+        const float xm = cf * sqrtf(dx * dx + dy * dy) * static_cast<float>(pb);
+        const float ex = __expf(-xm);
+        const float mat = a.k.nu_code == 0 ? ex : (a.k.nu_code == 1 ? (1.f + xm) * ex : (1.f + xm + xm * xm * (1.f / 3.f)) * ex);
+        const double kf = static_cast<double>(s1f * static_cast<float>(pe) * mat);
+        const double err = 3e-3 * wq[h] * wj + 1e-5 * (wq[h] + wj) + 1e-5 * fabs(kf) + 1e-30;
+        const double ub =
+            (fabs(kf - static_cast<double>(hc[v][2 * h + e2]) * kUnscale) + err) / sqrt(rq[h] * rj) * (1.0 + 1e-12);
+        if (!((1.0 - ub) - 1e-12 > dw * dw)) surv = 1;
+      }
+    }
+  return __syncthreads_or(surv) != 0;
+}
 
 __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
   extern __shared__ double sm[];
@@ -653,6 +807,12 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
         const int cp0 = T.off[ct], cn = T.off[ct + 1] - cp0;
         if (tid < kCT) cidx[tid] = tid < cn ? T.sp[cp0 + tid] : -1;
         __syncthreads();
+        if (a.W16 && phase == 1 && a.M > 0) {  // certified half-precision filter (seeds run exactly)
+          if (!half_filter_survives(a, ring, qidx, cidx, qm, topd, topj)) {
+            if (a.stats && tid == 0) atomicAdd(&a.stats[47], 1ull);
+            continue;
+          }
+        }
         double acc[2][4][2];
 #pragma unroll
         for (int u = 0; u < 2; ++u)
@@ -732,6 +892,7 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
             }
         __syncthreads();
         // merge: warp wid handles queries wid, wid + 8, ...
+        bool inserted = false;
         for (int qq = wid; qq < kQT; qq += kDrThreads / 32) {
           const int i = qidx[qq];
           const int m = qm[qq];
@@ -745,10 +906,17 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
             const double wd = __shfl_sync(kFull, e.d, m - 1);
             const int wj = __shfl_sync(kFull, e.j, m - 1);
             const unsigned acc2 = __ballot_sync(kFull, j >= 0 && j < i && lex_less(dd, j, wd, wj));
-            if (acc2) topm_insert(e, m, acc2, dd, j, lane);
+            if (acc2) {
+              topm_insert(e, m, acc2, dd, j, lane);
+              inserted = true;
+            }
           }
           topd[qq][lane] = e.d;
           topj[qq][lane] = e.j;
+        }
+        if (a.stats) {  // diagnostics: evaluated tiles that changed some list
+          const int any = __syncthreads_or(inserted ? 1 : 0);
+          if (tid == 0 && any) atomicAdd(&a.stats[48 + phase], 1ull);
         }
         __syncthreads();
       }
@@ -845,7 +1013,7 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
     // W lives in the context between searches: an 8 GB cudaMalloc / cudaFree per call costs 0.1-1 s
     DevBuf<double>& W = ctx->sel_W;
     W.ensure(static_cast<size_t>(ldm) * n);
-    DevBuf<double> resid(n);
+    DevBuf<double> resid(n), wnorm(n);
     lap("alloc W");
     STGP_CUDA(cudaMemsetAsync(W.get(), 0, sizeof(double) * ldm * n, st));
     DevBuf<int32_t> degen(n);
@@ -891,7 +1059,7 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
       }
       ProfRegion prr(ctx, "dr_resid");
       resid_kernel<<<std::max(1, std::min(ceil_div(n, kResRows), ctx->num_sms * 16)), kResRows, 0, st>>>(
-          W.get(), M, ldm, n, p.sigma1_2, resid.get(), degen.get());
+          W.get(), M, ldm, n, p.sigma1_2, resid.get(), degen.get(), wnorm.get());
       launched(ctx);
     }
     lap("whiten");
@@ -917,6 +1085,18 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
       a.y = ds->y.get();
       a.W = W.get();
       a.resid = resid.get();
+      // certified half-precision filter (STGP_DR_FILTER=0 disables): fp16 copy of W, |w| bounds
+      if (M > 0 && !(std::getenv("STGP_DR_FILTER") && std::getenv("STGP_DR_FILTER")[0] == '0')) {
+        const int ld16 = (M + kHK - 1) / kHK * kHK;
+        ctx->sel_W16.ensure(static_cast<size_t>(ld16) * n);
+        __half* w16 = reinterpret_cast<__half*>(ctx->sel_W16.get());
+        w16_kernel<<<grid_for(static_cast<long long>(ld16) * n, 256, ctx->num_sms * 32), 256, 0, st>>>(W.get(), M, ldm, n,
+                                                                                                      ld16, w16);
+        launched(ctx);
+        a.W16 = w16;
+        a.ld16 = ld16;
+        a.wnorm = wnorm.get();
+      }
       a.tid = ds->tid.get();
       a.degen = degen.get();
       a.k = k;
@@ -1122,8 +1302,10 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
         unsigned long long h[50];
         STGP_CUDA(cudaMemcpyAsync(h, a.stats, 50 * 8, cudaMemcpyDeviceToHost, st));
         STGP_CUDA(cudaStreamSynchronize(st));
-        std::fprintf(stderr, "[stgp] d_r tiles (%d query tiles, %d groups): evaluated %llu pruned %llu\n", ntile, G,
-                     h[0], h[1]);
+        std::fprintf(stderr,
+                     "[stgp] d_r tiles (%d query tiles, %d groups): evaluated %llu pruned %llu; half filter skipped "
+                     "%llu; with insertions: seed %llu, traversal %llu\n",
+                     ntile, G, h[0], h[1], h[47], h[48], h[49]);
         for (int lg = 0; lg < 16; ++lg)
           std::fprintf(stderr, "[stgp]   lag %2d: evaluated %llu pruned %llu stops %llu\n", lg, h[2 + lg], h[18 + lg],
                        h[34 + lg]);
