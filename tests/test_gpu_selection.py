@@ -131,3 +131,26 @@ def test_dr_unsorted_rows_brute_force(S):
     x, y, t = x[perm], y[perm], t[perm]
     Z, _, _ = O.sts_kmeanspp(x, y, t, 40, 2)
     _check_dr(S, x, y, t, SEC4, Z, 12)
+
+
+def test_dr_low_rank_dominant(S):
+    # many inducing points per datum: |w|^2 / r is large, the half-precision filter's bound is at
+    # its loosest; the sets must still equal the oracle's
+    x, y, t, _ = S.synth.station_day(120, 6, seed=8)
+    perm = O.order_observations(t, 8)
+    x, y, t = x[perm], y[perm], t[perm]
+    Z, _, _ = O.sts_kmeanspp(x, y, t, 300, 3)
+    _check_dr(S, x, y, t, SEC4, Z, 16)
+
+
+def test_dr_filter_on_off_identical(S, monkeypatch):
+    x, y, t, _ = S.synth.station_day(1500, 6, box=(4.6e6, 2.9e6), theta=S.synth.THETA_T3, seed=31)
+    perm = O.order_observations(t, 31)
+    x, y, t = x[perm], y[perm], t[perm]
+    ds = S.SpaceTimeDataset(x, y, t)
+    ind = S.sts_kmeanspp(ds, 300, 31)
+    a = S.residual_neighbors(ds, S.synth.THETA_T3, ind, 30)
+    monkeypatch.setenv("STGP_DR_FILTER", "0")
+    b = S.residual_neighbors(ds, S.synth.THETA_T3, ind, 30)
+    assert (a.indices() == b.indices()).all()
+    assert _bits(a.distances(), b.distances())
