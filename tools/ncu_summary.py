@@ -38,10 +38,17 @@ def main(rep, nrows=None):
         hh, vals = rr[0], rr[2]
         for name in ("dram__bytes_read.sum", "dram__bytes_write.sum", "sm__inst_executed_pipe_fp64.sum",
                      "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
-                     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+                     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
                      "smsp__inst_executed_op_dfma.sum"):
             if name in hh:
                 out.append(f"{name}: {vals[hh.index(name)]} {rr[1][hh.index(name)]}")
+        st = [(hh[i], vals[i]) for i in range(len(hh))
+              if "pcsamp_warps_issue_stalled" in hh[i] and not hh[i].endswith("_not_issued")]
+        st = [(a, float(b)) for a, b in st if b.replace(".", "").isdigit()]
+        tot = sum(b for _, b in st) or 1.0
+        out.append("stall reasons (pc sampling):")
+        for a, b in sorted(st, key=lambda x: -x[1])[:6]:
+            out.append(f"  {b / tot * 100:5.1f}% {a.split('stalled_')[-1]}")
     sass = list(csv.reader(io.StringIO(run(["-i", rep, "--page", "source", "--csv", "--print-source", "sass"]))))
     h = sass[1]
     si, ii, ws = h.index('Source'), h.index('Instructions Executed'), h.index('Warp Stall Sampling (All Samples)')
