@@ -121,7 +121,7 @@ double dev_logdet_chol(stgp_ctx* ctx, const double* L, int ld, int n) {
 
 void dev_trsm_left(stgp_ctx* ctx, const double* L, int ldl, int n, double* B, int ldb, long long ncols, bool transpose) {
   const double one = 1.0;
-  const long long chunk = INT_MAX / 2;
+  const long long chunk = std::max<long long>(1, ((1LL << 31) - 1) / ldb);  // < 2^31 elements per call
   for (long long c0 = 0; c0 < ncols; c0 += chunk) {
     const int nc = static_cast<int>(std::min(chunk, ncols - c0));
     cublas_check(cublasDtrsm(ctx->cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, transpose ? CUBLAS_OP_T : CUBLAS_OP_N,
@@ -148,7 +148,7 @@ void dev_tri_inverse(stgp_ctx* ctx, const double* L, int ld, int n, double* Linv
 void dev_trmm_left(stgp_ctx* ctx, const double* T, int ldt, int n, const double* B, int ldb, long long ncols,
                    bool transpose, double* C, int ldc) {
   const double one = 1.0;
-  const long long chunk = INT_MAX / 2;
+  const long long chunk = std::max<long long>(1, ((1LL << 31) - 1) / std::max(ldb, ldc));  // < 2^31 elements per call
   for (long long c0 = 0; c0 < ncols; c0 += chunk) {
     const int nc = static_cast<int>(std::min(chunk, ncols - c0));
     cublas_check(cublasDtrmm(ctx->cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, transpose ? CUBLAS_OP_T : CUBLAS_OP_N,
@@ -183,6 +183,21 @@ void dev_syrk_blocked(stgp_ctx* ctx, int n, long long k, double alpha, const dou
     for (int j0 = 0; j0 <= i0; j0 += bs) {
       const int mi = std::min(bs, n - i0), mj = std::min(bs, n - j0);
       dev_gemm(ctx, false, true, mi, mj, k, alpha, A + i0, lda, A + j0, lda, 0.0, C + static_cast<size_t>(j0) * ldc + i0,
+               ldc);
+    }
+  dev_symmetrize_lower(ctx, C, ldc, n);
+}
+
+// C = alpha A B^T for a product known to be symmetric (e.g. W diag(phi) W^T with B = W diag(phi)):
+// GEMMs on the lower blocks of an nb x nb partition, mirrored.
+void dev_gemm_sym_blocked(stgp_ctx* ctx, int n, long long k, double alpha, const double* A, int lda, const double* B,
+                          int ldb, double* C, int ldc, int nb) {
+  nb = std::max(1, std::min(nb, (n + 15) / 16));
+  const int bs = ((n + nb - 1) / nb + 15) / 16 * 16;
+  for (int i0 = 0; i0 < n; i0 += bs)
+    for (int j0 = 0; j0 <= i0; j0 += bs) {
+      const int mi = std::min(bs, n - i0), mj = std::min(bs, n - j0);
+      dev_gemm(ctx, false, true, mi, mj, k, alpha, A + i0, lda, B + j0, ldb, 0.0, C + static_cast<size_t>(j0) * ldc + i0,
                ldc);
     }
   dev_symmetrize_lower(ctx, C, ldc, n);

@@ -41,5 +41,7 @@ void dev_gemv(stgp_ctx* ctx, bool ta, int m, long long n, double alpha, const do
 void dev_symmetrize_lower(stgp_ctx* ctx, double* A, int ld, int n);
 void dev_syrk_blocked(stgp_ctx* ctx, int n, long long k, double alpha, const double* A, int lda, double* C, int ldc,
                       int nb);
+void dev_gemm_sym_blocked(stgp_ctx* ctx, int n, long long k, double alpha, const double* A, int lda, const double* B,
+                          int ldb, double* C, int ldc, int nb);
 
 }  // namespace stgp

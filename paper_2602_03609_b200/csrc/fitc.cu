@@ -43,16 +43,14 @@ __global__ void fitc_diag_kernel(int n, int M, int ldm, const double* W, double 
   }
 }
 
-// per-column: out_i = |Hw_i|^2
-__global__ void col_sqnorm_kernel(int n, int ldm, const double* A, double* out) {
+// per-column: out_i = A_i . B_i  (|L_K^{-1} W_i|^2 = W_i . (K^{-1} W)_i)
+__global__ void col_dot_kernel(int n, int ldm, const double* A, const double* B, double* out) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (int i = gw; i < n; i += nw) {
     double acc = 0.0;
-    for (int j = lane; j < ldm; j += 32) {
-      const double v = A[static_cast<size_t>(i) * ldm + j];
-      acc = fma(v, v, acc);
-    }
+    for (int j = lane; j < ldm; j += 32)
+      acc = fma(A[static_cast<size_t>(i) * ldm + j], B[static_cast<size_t>(i) * ldm + j], acc);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) out[i] = acc;
@@ -101,7 +99,10 @@ void fitc_build(stgp_structure* s) {
   stgp_ctx* ctx = s->ds->ctx;
   LowRank& L = s->lr;
   prepare_tables(s);
-  build_basis(s);
+  {
+    ProfRegion pr(ctx, "basis");
+    build_basis(s);
+  }
   const int rb = s->row_begin, re = s->row_end, ldm = L.ldm, n = s->n;
   build_cross(s, rb, re, false);
   L.fitc_diag.ensure(n);
@@ -131,11 +132,11 @@ void fitc_build(stgp_structure* s) {
   L.work1.ensure(total);
   L.Mc.ensure(static_cast<size_t>(ldm) * ldm);
   STGP_CUDA(cudaMemsetAsync(L.Mc.get(), 0, sizeof(double) * ldm * ldm, ctx->stream));
+  ProfRegion prk(ctx, "K_gemm_chol");
   if (re > rb) {
     scale_cols(ctx, L.W.get() + own, ldm, re - rb, L.lambda.get() + rb, true, L.work1.get() + own);
-    dev_syrk(ctx, ldm, re - rb, 1.0, L.work1.get() + own, ldm, 0.0, L.Mc.get(), ldm);
+    dev_syrk_blocked(ctx, ldm, re - rb, 1.0, L.work1.get() + own, ldm, L.Mc.get(), ldm, 4);
   }
-  dev_symmetrize_lower(ctx, L.Mc.get(), ldm, ldm);
   allreduce_sum(ctx, L.Mc.get(), static_cast<size_t>(ldm) * ldm);
   add_identity(ctx, L.Mc.get(), ldm);
   L.Kfull.ensure(static_cast<size_t>(ldm) * ldm);
@@ -197,32 +198,32 @@ void fitc_nll_grad(stgp_structure* s, double* nll, double* grad) {
   STGP_CUDA(cudaMemsetAsync(wa, 0, sizeof(double) * ldm, st));
   STGP_CUDA(cudaMemsetAsync(S, 0, sizeof(double) * mm, st));
   std::vector<double> phisum(1, 0.0);
+  // explicit K^{-1} (M^3): KW = K^{-1} W is one GEMM, and |L_K^{-1} W_i|^2 = W_i . KW_i
+  L.Kinv.ensure(mm);
+  set_identity(ctx, L.Kinv.get(), ldm);
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, false);
+  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, true);
   if (nown > 0) {
-    // Hw = L_K^{-1} W (|Hw_i|^2 -> diag of Sigma~^{-1}), then KW = K^{-1} W in place
-    STGP_CUDA(cudaMemcpyAsync(L.work1.get() + own, L.W.get() + own, sizeof(double) * ldm * nown,
-                              cudaMemcpyDeviceToDevice, st));
-    dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.work1.get() + own, ldm, nown, false);
-    col_sqnorm_kernel<<<grid_for(static_cast<long long>(nown) * 32), 256, 0, st>>>(nown, ldm, L.work1.get() + own,
-                                                                                  hsq + rb);
+    ProfRegion pr(ctx, "f_KW_gemm");
+    dev_gemm(ctx, false, false, ldm, nown, ldm, 1.0, L.Kinv.get(), ldm, L.W.get() + own, ldm, 0.0, L.work1.get() + own,
+             ldm);
+    col_dot_kernel<<<grid_for(static_cast<long long>(nown) * 32), 256, 0, st>>>(nown, ldm, L.W.get() + own,
+                                                                               L.work1.get() + own, hsq + rb);
     launched(ctx);
-    dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.work1.get() + own, ldm, nown, true);
     fitc_alpha_phi_kernel<<<grid_for(nown), 256, 0, st>>>(nown, s->r.get() + rb, L.lambda.get() + rb, t + rb, hsq + rb,
                                                           alpha + rb, phi + rb);
     launched(ctx);
     dev_gemv(ctx, false, ldm, nown, 1.0, L.W.get() + own, ldm, alpha + rb, 0.0, wa);
-    // S = W diag(phi) W^T
+    // S = W diag(phi) W^T (symmetric: lower blocks only)
+    ProfRegion prs(ctx, "f_S_gemm");
     scale_cols(ctx, L.W.get() + own, ldm, nown, phi + rb, false, L.work2.get() + own);
-    dev_gemm(ctx, false, true, ldm, ldm, nown, 1.0, L.W.get() + own, ldm, L.work2.get() + own, ldm, 0.0, S, ldm);
+    dev_gemm_sym_blocked(ctx, ldm, nown, 1.0, L.W.get() + own, ldm, L.work2.get() + own, ldm, S, ldm, 4);
     Reducer rr;
     phisum[0] = dev_sum(ctx, phi + rb, nown, rr);
   }
   allreduce_sum(ctx, wa, ldm);
   allreduce_sum(ctx, S, mm);
   allreduce_host(ctx, phisum);
-  L.Kinv.ensure(mm);
-  set_identity(ctx, L.Kinv.get(), ldm);
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, false);
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, true);
   fitc_wsig_kernel<<<grid_for(static_cast<long long>(mm)), 256, 0, st>>>(M, ldm, L.Kinv.get(), wa, S, Ws);
   launched(ctx);
   transform_wsig(ctx, L.Lm.get(), ldm, Ws);
@@ -233,6 +234,7 @@ void fitc_nll_grad(stgp_structure* s, double* nll, double* grad) {
         static_cast<long long>(ldm) * nown, ldm, L.lambda.get() + rb, alpha + rb, phi + rb, wa, L.W.get() + own,
         L.work1.get() + own);
     launched(ctx);
+    ProfRegion pr(ctx, "f_omega_trmm_upair");
     dev_trmm_left(ctx, L.Lminv.get(), ldm, ldm, L.work1.get() + own, ldm, nown, true, L.work2.get() + own, ldm);
     std::vector<double> gu = upair_grad(s, L.work2.get(), rb, re);
     for (int q = 0; q < 6; ++q) g[1 + q] += gu[q];
