@@ -36,13 +36,18 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="vif", choices=["vecchia", "vif"])
-    ap.add_argument("--m", type=int, default=1000, help="sts kMeans++ inducing request (VIF)")
+    ap.add_argument("--workload", default="vif", choices=["vecchia", "vif", "fitc"],
+                    help="vif: cfg4 (headline); vecchia: cfg4 data, d_c neighbours; fitc: cfg5 (FITC, 2000 "
+                         "inducing points, plus 1-day-ahead prediction at every station)")
+    ap.add_argument("--m", type=int, default=None, help="sts kMeans++ inducing request (VIF 1000, FITC 2000)")
     ap.add_argument("--stations", type=int, default=10000)
     ap.add_argument("--days", type=int, default=110)
     ap.add_argument("--m_v", type=int, default=30)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.m is None:
+        args.m = 2000 if args.workload == "fitc" else 1000
+    return args
 
 
 def peaks():
@@ -160,7 +165,13 @@ def vif_rows_flops(nbr_counts, M):
     return float(np.sum(2 * ((ck + k + 2) * M + k ** 3 / 6 + 2 * k ** 2) + ck * (KE_FLOP + KG_FLOP)))
 
 
-def cpu_sample_vif(x, y, t, resp, theta, nbr, Z, target_s=10.0):
+def fitc_flops(n, M):
+    """canonical FP64 work of one FITC NLL+grad: W = L_m^{-1} U, K = I + W Lambda^{-1} W^T (symmetric),
+    K^{-1} W, W diag(phi) W^T (symmetric), omega = L_m^{-T} omega' -> 3 n M^2 FMA, plus n M KE and KG."""
+    return float(2 * 3.0 * n * M * M + n * M * (KE_FLOP + KG_FLOP))
+
+
+def cpu_sample_vif(x, y, t, resp, theta, nbr, Z, target_s=10.0, kind="vif"):
     """Oracle VIF build + nll + build + nll_grad on a prefix of the ordered rows with the full
     inducing set; the n M^2 and per-row terms are linear in n, so scale linearly."""
     from oracle import oracle as O
@@ -168,7 +179,7 @@ def cpu_sample_vif(x, y, t, resp, theta, nbr, Z, target_s=10.0):
     n = len(x)
     ns = min(n, 1500)
     while True:
-        om = O.OracleModel("vif", x[:ns], y[:ns], t[:ns], theta, nbr=nbr[:ns], Z=Z)
+        om = O.OracleModel(kind, x[:ns], y[:ns], t[:ns], theta, nbr=None if nbr is None else nbr[:ns], Z=Z)
         t0 = time.perf_counter()
         om.nll(resp[:ns])
         om.nll_grad(resp[:ns])
@@ -178,7 +189,7 @@ def cpu_sample_vif(x, y, t, resp, theta, nbr, Z, target_s=10.0):
         ns = min(n, 40000, int(ns * max(2.0, min(target_s / max(dt, 1e-3), 8.0))))
     per_eval_full = dt * n / ns
     return {"value": 1.0 / per_eval_full, "unit": "evals/s", "cores": cores, "kind": "port",
-            "sample": f"oracle VIF build+nll+build+nll_grad on the first {ns} of {n} ordered rows with all "
+            "sample": f"oracle {kind.upper()} build+nll+build+nll_grad on the first {ns} of {n} ordered rows with all "
                       f"{len(Z)} inducing points ({dt:.2f} s), scaled linearly to n"}
 
 
@@ -199,6 +210,12 @@ def run_reference(args):
         nbr = O.dr_neighbors(x[:ns], y[:ns], t[:ns], theta, Z, args.m_v)
         kind, extra = "vif", {"Z": Z}
         desc = f"oracle VIF build+nll+build+nll_grad on the first {ns} of {n} ordered rows ({len(Z)} inducing points)"
+    elif args.workload == "fitc":
+        Z, _, _ = O.sts_kmeanspp(x, y, t, args.m, 20260203)
+        ns = min(n, 2000)
+        nbr = None
+        kind, extra = "fitc", {"Z": Z}
+        desc = f"oracle FITC build+nll+build+nll_grad on the first {ns} of {n} ordered rows ({len(Z)} inducing points)"
     else:
         ns = min(n, 30000)
         nbr = O.dc_neighbors(x[:ns], y[:ns], t[:ns], theta, args.m_v)
@@ -228,7 +245,7 @@ def run_reference(args):
 
 
 def workload_name(args):
-    return "cfg4-vif-dr-sts" if args.workload == "vif" else "cfg4-vecchia-dc"
+    return {"vif": "cfg4-vif-dr-sts", "vecchia": "cfg4-vecchia-dc", "fitc": "cfg5-fitc-sts-predict"}[args.workload]
 
 
 def main():
@@ -272,6 +289,14 @@ def main():
         s = S.build_vif(ds, theta, ind, nb, S.OBSERVATION)
         M = ind.M
         extra["inducing"] = {"m": args.m, "M": M, "m_s": ind.m_s, "m_t": ind.m_t}
+    elif args.workload == "fitc":
+        t0 = time.perf_counter()
+        ind = S.sts_kmeanspp(ds, args.m, 20260203)
+        extra["seeding_s"] = time.perf_counter() - t0
+        nb, nn_s, knn_ms = None, None, None
+        s = S.build_fitc(ds, theta, ind)
+        M = ind.M
+        extra["inducing"] = {"m": args.m, "M": M, "m_s": ind.m_s, "m_t": ind.m_t}
     else:
         t0 = time.perf_counter()
         nb = S.correlation_neighbors(ds, theta, args.m_v)
@@ -282,8 +307,8 @@ def main():
         extra["nn_search_warm_s"] = time.perf_counter() - t0
         s = S.build_vecchia(ds, theta, nb, S.OBSERVATION)
         M = 0
-    nbr = nb.indices()
-    counts = (nbr >= 0).sum(axis=1)
+    nbr = nb.indices() if nb is not None else None
+    counts = (nbr >= 0).sum(axis=1) if nbr is not None else np.zeros(n, dtype=np.int64)
 
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
     thetas = [tuple(v * (1.0 + 0.01 * ((i % 5) - 2)) if j in (1, 2, 3) else v for j, v in enumerate(theta))
@@ -336,6 +361,12 @@ def main():
         k_avg = region_avg("rows") + region_avg("rows_vifgrad")
         flops_launch = vif_rows_flops(counts[lo:hi], M)
         step_flops = vif_flops(counts, M)
+    elif args.workload == "fitc":
+        # FITC is dense low-rank algebra: the roofline object covers the whole evaluation
+        kname = "FITC evaluation (DMMA GEMM/TRMM over n x M, cross covariance, kernel-gradient pairs)"
+        k_avg = ms_step
+        flops_launch = fitc_flops(hi - lo, M)
+        step_flops = fitc_flops(n, M)
     else:
         kname = "vecchia_rows_kernel<grad>"
         k_avg = region_avg("rows")
@@ -358,19 +389,34 @@ def main():
             "config": {"workload": workload_name(args), "n": n, "m_v": args.m_v, "stations": args.stations,
                        "days": args.days, "theta": "PAPER.md Table 3 (NOAA temperature)" if args.stations >= 2000
                        else "PAPER.md section 4",
-                       "neighbors": "d_r exact kNN (residual_neighbors)" if args.workload == "vif"
-                       else "d_c exact kNN (correlation_neighbors)",
+                       "neighbors": {"vif": "d_r exact kNN (residual_neighbors)", "fitc": "none (FITC)",
+                                     "vecchia": "d_c exact kNN (correlation_neighbors)"}[args.workload],
                        "parallelism": f"index-shard x{world}",
-                       "l2": "inputs larger than L2 (W, V' 8 GB each)" if args.workload == "vif"
-                       else "inputs larger than L2 (nbr 132 MB + A 264 MB)"},
+                       "l2": "inputs larger than L2 (nbr 132 MB + A 264 MB)" if args.workload == "vecchia"
+                       else "inputs larger than L2 (n x M f64 work arrays, 8-19 GB each)"},
             "nn_search_s": nn_s, "nn_search_kernel_ms": knn_ms, "nll": v, "grad": list(g),
             "e2e": {"value": 1.0 / e2e_s, "unit": "evals/s", "h2d_bytes_per_step": n * 8 + 64,
                     "d2h_bytes_per_step": 64},
             "gpu_launches": launches, "roofline": roof, "clocks": clk.summary()}
     line.update(extra)
+    if args.workload == "fitc" and world == 1:
+        # cfg5's second half: 1-day-ahead predictive mean / variance at every station
+        last = t == t.max()
+        targets = np.column_stack([x[last], y[last], np.full(int(last.sum()), t.max() + 1.0)])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        S.predict(s, resp, None, None, targets)
+        line["predict_first_s"] = time.perf_counter() - t0  # includes first-use module loads / pools
+        t0 = time.perf_counter()
+        pr = S.predict(s, resp, None, None, targets)
+        line["predict_s"] = time.perf_counter() - t0
+        line["predict_targets"] = int(len(targets))
+        line["predict_var_range"] = [float(pr.var.min()), float(pr.var.max())]
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         if args.workload == "vif":
             line["cpu_baseline"] = cpu_sample_vif(x, y, t, resp, theta, nbr, ind.points)
+        elif args.workload == "fitc":
+            line["cpu_baseline"] = cpu_sample_vif(x, y, t, resp, theta, None, ind.points, kind="fitc")
         else:
             line["cpu_baseline"] = cpu_sample_vecchia(x, y, t, resp, theta, nbr)
     if rank == 0:

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstring>
+#include <memory>
 #include <set>
 
 #include "comm.hpp"
@@ -489,6 +490,7 @@ static void fitc_predict(stgp_structure* s, TargetSet& T, int np, double* mu, do
   const int n = s->n, ldm = L.ldm;
   cudaStream_t st = ctx->stream;
   // alpha = rl - Lambda^{-1} W^T K^{-1} W rl;  Walpha = W alpha
+  std::unique_ptr<ProfRegion> pr(new ProfRegion(ctx, "p_alpha"));
   double* rl = L.tmp("p_rl", n);
   double* kv = L.tmp("p_kv", ldm);
   double* t = L.tmp("p_t", n);
@@ -503,6 +505,7 @@ static void fitc_predict(stgp_structure* s, TargetSet& T, int np, double* mu, do
   double* walpha = L.tmp("p_walpha", ldm);
   dev_gemv(ctx, false, ldm, n, 1.0, L.W.get(), ldm, alpha, 0.0, walpha);
   // targets: Up, What = L_m^{-1} Up, Y = L_K^{-1} What
+  pr.reset(new ProfRegion(ctx, "p_targets"));
   DevBuf<double> Up(static_cast<size_t>(ldm) * np), Wh(static_cast<size_t>(ldm) * np), Y(static_cast<size_t>(ldm) * np);
   target_cross_kernel<<<std::max(1, std::min(np, ctx->num_sms * 8)), 128, 0, st>>>(
       L.zx.get(), L.zy.get(), L.ztid.get(), L.M, ldm, T.qx.get(), T.qy.get(), T.qtid.get(), np, dev_kernel(s->th),
@@ -517,6 +520,7 @@ static void fitc_predict(stgp_structure* s, TargetSet& T, int np, double* mu, do
   launched(ctx);
   coldot_kernel<<<grid_for(static_cast<long long>(np) * 32), 256, 0, st>>>(np, ldm, Y.get(), Y.get(), y2.get());
   launched(ctx);
+  pr.reset();
   std::vector<double> hw(np), hy(np);
   mu_d.download(mu, np, st);
   w2.download(hw.data(), np, st);
