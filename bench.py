@@ -245,7 +245,12 @@ def run_reference(args):
 
 
 def workload_name(args):
-    return {"vif": "cfg4-vif-dr-sts", "vecchia": "cfg4-vecchia-dc", "fitc": "cfg5-fitc-sts-predict"}[args.workload]
+    shape = (args.stations, args.days)
+    if shape == (10000, 110):
+        return {"vif": "cfg4-vif-dr-sts", "vecchia": "cfg4-vecchia-dc", "fitc": "cfg5-fitc-sts-predict"}[args.workload]
+    if shape == (1000, 100) and args.m_v == 20:
+        return {"vif": "cfg3-vif-dr-sts", "vecchia": "cfg2-vecchia-dc", "fitc": "fitc-1000x100"}[args.workload]
+    return f"{args.workload}-{args.stations}x{args.days}-m{args.m}-mv{args.m_v}"
 
 
 def main():

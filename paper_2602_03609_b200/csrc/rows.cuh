@@ -196,6 +196,26 @@ __device__ __forceinline__ void closure_gram_dmma(const double* __restrict__ W, 
     for (int I = 0; I < 4; ++I) sGa[8 * I + grp] = accx[I][0];
 }
 
+// Time classes of a row's closure (its slots span few distinct times: same and previous time
+// blocks).  Fills cls[lane] (class of slot `lane`) and the per-class-pair temporal factors of the
+// lag table into tf[nc * nc]; returns nc, or 0 when more than kMaxCls classes (use the table).
+constexpr int kMaxCls = 4;
+__device__ __forceinline__ int closure_time_classes(const LagTable& lt, int pt, int myt, int lane, int* cls,
+                                                    int* ctid, TF* tf) {
+  const int key = pt >= 0 ? myt : -1;
+  const unsigned same = __match_any_sync(kFull, key);
+  const int leader = __ffs(same) - 1;
+  const unsigned leaders = __ballot_sync(kFull, lane == leader && pt >= 0);
+  const int nc = __popc(leaders);
+  if (nc > kMaxCls) return 0;
+  cls[lane] = __popc(leaders & ((1u << leader) - 1));
+  if (lane == leader && pt >= 0) ctid[__popc(leaders & ((1u << lane) - 1))] = myt;
+  __syncwarp();
+  if (lane < nc * nc) tf[lane] = lt.get(ctid[lane / nc], ctid[lane % nc]);
+  __syncwarp();
+  return nc;
+}
+
 template <int MODE, bool HAS_W, int KS>
 __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs a) {
   static_assert(KS >= 1 && KS <= 31, "closure must fit a warp");
@@ -208,6 +228,8 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
   __shared__ double sCol[kRowWarps][2][32];
   __shared__ int st[kRowWarps][32], scol[kRowWarps][32];
   __shared__ double sred[kRowWarps][8];
+  __shared__ TF stf[kRowWarps][kMaxCls * kMaxCls];
+  __shared__ int scls[kRowWarps][32], sctid[kRowWarps][kMaxCls];
 
   for (int p = threadIdx.x; p < NP; p += blockDim.x) {
     int aa = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * static_cast<float>(p))) * 0.5f);
@@ -242,6 +264,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
     }
     scol[w][lane] = pt;
     __syncwarp();
+    const int nc = closure_time_classes(a.lt, pt, pt >= 0 ? st[w][lane] : -1, lane, scls[w], sctid[w], stf[w]);
     // VIF gradient: Ga[s] = W_{cl_s} . X_i (= U_{cl_s} . Hhat_i) from the same DMMA pass
     if (HAS_W)
       closure_gram_dmma<LD, MODE == kModeVifGrad>(a.W, a.ldw, scol[w], C, lane,
@@ -264,7 +287,13 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
       const int ca = pr & 0xff, sb = pr >> 8;
       const int sa = ca == k ? KS : ca;
       double pe, pb;
-      a.lt.get2(st[w][sa], st[w][sb], pe, pb);
+      if (nc) {
+        const TF& fc = stf[w][scls[w][sa] * nc + scls[w][sb]];
+        pe = fc.pow_mE;
+        pb = fc.pow_mbh;
+      } else {
+        a.lt.get2(st[w][sa], st[w][sb], pe, pb);
+      }
       TF f;
       f.pow_mE = pe;
       f.pow_mbh = pb;
@@ -415,7 +444,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
       const int pr = sPair[p];
       const int ca = pr & 0xff, sb = pr >> 8;
       const int sa = ca == k ? KS : ca;
-      const TF f = a.lt.get(st[w][sa], st[w][sb]);
+      const TF f = nc ? stf[w][scls[w][sa] * nc + scls[w][sb]] : a.lt.get(st[w][sa], st[w][sb]);
       double kg[6];
       gneiting_grad_fast(a.k, a.inv_c, spatial_dist(sx[w][sa], sy[w][sa], sx[w][sb], sy[w][sb]), f, kg);
       const double ta = sAw[w][0][sa], tb = sAw[w][0][sb], wa = sAw[w][1][sa], wb = sAw[w][1][sb];
@@ -517,7 +546,6 @@ __global__ void __launch_bounds__(kRowWarps * 32) vif_grad_stored_kernel(RowArgs
   // per-row cache of the temporal factors of the closure's time classes (a row's closure spans a
   // few distinct times: the KG loop then reads TF from shared memory instead of two dependent
   // global lookups per pair)
-  constexpr int kMaxCls = 4;
   __shared__ TF stf[kRowWarps][kMaxCls * kMaxCls];
   __shared__ int scls[kRowWarps][32], sctid[kRowWarps][kMaxCls];
   for (int p = threadIdx.x; p < NP; p += blockDim.x) {
@@ -595,20 +623,8 @@ __global__ void __launch_bounds__(kRowWarps * 32) vif_grad_stored_kernel(RowArgs
     if (lane < a.m_v) a.Rv_out[static_cast<size_t>(i) * a.m_v + lane] = Rv;
     sAw[w][0][lane] = lane < k ? -Aval : (lane == KS ? 1.0 : 0.0);
     sAw[w][1][lane] = Rv;
-    // time classes of the closure slots
-    const int myt = pt >= 0 ? st[w][lane] : -1;
-    const unsigned same = __match_any_sync(kFull, myt);
-    const int leader = __ffs(same) - 1;
-    const unsigned leaders = __ballot_sync(kFull, lane == leader && pt >= 0);
-    const int nc = __popc(leaders);
-    const bool cached = nc <= kMaxCls;
-    if (cached) {
-      scls[w][lane] = __popc(leaders & ((1u << leader) - 1));
-      if (lane == leader && pt >= 0) sctid[w][__popc(leaders & ((1u << lane) - 1))] = myt;
-      __syncwarp();
-      if (lane < nc * nc) stf[w][lane] = a.lt.get(sctid[w][lane / nc], sctid[w][lane % nc]);
-    }
-    __syncwarp();
+    const int nc = closure_time_classes(a.lt, pt, pt >= 0 ? st[w][lane] : -1, lane, scls[w], sctid[w], stf[w]);
+    const bool cached = nc > 0;
     const int P = (k + 1) * k / 2;
     double g[6] = {0, 0, 0, 0, 0, 0};
     for (int p = lane; p < P; p += 32) {
