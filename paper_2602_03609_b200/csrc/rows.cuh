@@ -579,11 +579,6 @@ __global__ void __launch_bounds__(kRowWarps * 32) vif_grad_stored_kernel(RowArgs
     __syncwarp();
     const double* xi = a.X + static_cast<size_t>(i) * a.ldw;
     closure_x_dmma(a.W, a.ldw, scol[w], xi, sGa[w], lane, a.zcol);
-    double aGa = 0.0;
-    const double* vi = a.Vp + static_cast<size_t>(i) * a.ldw;
-    for (int j = lane; j < a.ldw; j += 32) aGa = fma(__ldg(&vi[j]), __ldg(&xi[j]), aGa);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) aGa += __shfl_xor_sync(kFull, aGa, o);
     // stored factor: row `lane` of L into registers and shared memory
     const double* src = a.Lfac_in + static_cast<size_t>(i) * lfac_stride<KS>();
     double R[KS];
@@ -612,12 +607,15 @@ __global__ void __launch_bounds__(kRowWarps * 32) vif_grad_stored_kernel(RowArgs
     }
     const double Rv = lane < k ? b2 : 0.0;
     const double Aval = lane < k ? __ldg(&a.A_in[static_cast<size_t>(i) * a.m_v + lane]) : 0.0;
-    double aa = Aval * Aval, aw = Aval * Rv;
+    // aGa = V'_i . X_i = (W_i - sum_a A_ia W_{N_a}) . X_i = Ga[self] - sum_a A_ia Ga[a]: no pass over V'_i
+    double aa = Aval * Aval, aw = Aval * Rv, ag = Aval * Ga;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       aa += __shfl_xor_sync(kFull, aa, o);
       aw += __shfl_xor_sync(kFull, aw, o);
+      ag += __shfl_xor_sync(kFull, ag, o);
     }
+    const double aGa = __shfl_sync(kFull, Ga, KS) - ag;
     const double cd = 0.5 * (1.0 / Dst - (aGa + uz * uz) / (Dst * Dst));  // c0
     if (lane == 0) a.c0_out[i] = cd;
     if (lane < a.m_v) a.Rv_out[static_cast<size_t>(i) * a.m_v + lane] = Rv;
