@@ -785,24 +785,49 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
       }
       for (int sv = 0; sv < nsurv; ++sv) {
         const int ct = s_surv[sv];
-        if (sv > 0 && phase == 1 && can_prune) {  // re-test against the thresholds tightened by the previous survivors
-          if (tid == 0) {
-            const double dn = tile_threshold(topd, qm);
-            int skip = 0;
-            if (dn < 1.0) {
-              const double cmax = tile_cmax(a, tminQ, tmaxQ, qx0, qx1, qy0, qy1, sAQ, rQ, ct);
-              skip = cmax < 1.0 && (1.0 - cmax) - 1e-12 > dn * dn;
+        if (phase == 1 && can_prune) {
+          // per-query re-test with each row's own threshold, time, point-to-box distance and r
+          // (the tile-level test above used the worst of 64 of each): a valid bound per pair, the
+          // tile is skipped when no query row can take any of its candidates
+          int live = 0;
+          if (tid < kQT) {
+            const int qq = tid, m = qm[qq];
+            if (m > 0) {
+              const double dq = topd[qq][m - 1];
+              if (!(dq < 1.0)) {
+                live = 1;
+              } else {
+                const int i = qidx[qq];
+                const int ti = a.tid[i], tc0 = T.tmin[ct], tc1 = T.tmax[ct];
+                double pe_min, pb0, pe0, pb_max;
+                if (tc1 >= ti) pe_min = 1.0; else a.lt.get2(ti, tc1, pe_min, pb0);
+                a.lt.get2(ti, tc0, pe0, pb_max);
+                double mat = 1.0;
+                if (a.k.nu_code >= 0) {
+                  const double xi = a.x[i], yi = a.y[i];
+                  const double dx = fmax(0.0, fmax(T.bx0[ct] - xi, xi - T.bx1[ct]));
+                  const double dy = fmax(0.0, fmax(T.by0[ct] - yi, yi - T.by1[ct]));
+                  const double xm = a.k.c * sqrt(dx * dx + dy * dy) * (1.0 - 1e-12) * pb_max * (1.0 - 1e-12);
+                  mat = matern_from_exp(xm, exp(-xm), a.k.nu_code);
+                }
+                double wt = 0.0;
+                const double* AC = T.A + static_cast<size_t>(ct) * T.G;
+                for (int g = 0; g < T.G; ++g) wt += sAQ[g] * AC[g];
+                const double ci = (a.s1 * pe_min * mat / sqrt(a.resid[i] * T.rmin[ct]) + wt) * (1.0 + 1e-11);
+                live = !(ci < 1.0 && (1.0 - ci) - 1e-12 > dq * dq);
+              }
             }
-            s_skip = skip;
-            if (a.stats && skip) {
+          }
+          const int any = __syncthreads_or(live);
+          if (!any) {
+            if (a.stats && tid == 0) {
               atomicAdd(&a.stats[0], ~0ull);  // -1: moved from evaluated to pruned
               atomicAdd(&a.stats[1], 1ull);
               atomicAdd(&a.stats[2 + min(qb - b, 15)], ~0ull);
               atomicAdd(&a.stats[18 + min(qb - b, 15)], 1ull);
             }
+            continue;
           }
-          __syncthreads();
-          if (s_skip) continue;
         }
         const int cp0 = T.off[ct], cn = T.off[ct + 1] - cp0;
         if (tid < kCT) cidx[tid] = tid < cn ? T.sp[cp0 + tid] : -1;
