@@ -54,50 +54,6 @@ __global__ void sel_sigma_kernel(const double* zx, const double* zy, const int32
   }
 }
 
-// Left-looking Cholesky in the oracle's order (chol_seq); A row-major in, L row-major out.  Row j
-// of L is staged in shared memory; each row's chain streams its own row with loads batched ahead of
-// the (sequential) fma chain.
-__device__ __forceinline__ double chol_chain(const double* Lr, const double* Lj, int j, double s) {
-  int k = 0;
-  for (; k + 8 <= j; k += 8) {
-    double a[8], b[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      a[u] = Lr[k + u];
-      b[u] = Lj[k + u];
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s = __fma_rn(-a[u], b[u], s);
-  }
-  for (; k < j; ++k) s = __fma_rn(-Lr[k], Lj[k], s);
-  return s;
-}
-
-__global__ void __launch_bounds__(1024) chol_seq_kernel(const double* A, int M, double* L, int* fail) {
-  __shared__ double diag;
-  __shared__ int bad;
-  extern __shared__ double sLj[];  // row j of L (M doubles)
-  if (threadIdx.x == 0) bad = 0;
-  for (int j = 0; j < M; ++j) {
-    __syncthreads();
-    for (int k = threadIdx.x; k < j; k += blockDim.x) sLj[k] = L[static_cast<size_t>(j) * M + k];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const double acc = chol_chain(sLj, sLj, j, A[static_cast<size_t>(j) * M + j]);
-      if (acc <= 0.0) bad = 1;
-      diag = __dsqrt_rn(acc);
-      L[static_cast<size_t>(j) * M + j] = diag;
-    }
-    __syncthreads();
-    if (bad) break;
-    const double d = diag;
-    for (int r = j + 1 + threadIdx.x; r < M; r += blockDim.x) {
-      const double sr = chol_chain(L + static_cast<size_t>(r) * M, sLj, j, A[static_cast<size_t>(r) * M + j]);
-      L[static_cast<size_t>(r) * M + j] = __ddiv_rn(sr, d);
-    }
-  }
-  if (threadIdx.x == 0 && bad) *fail = 1;
-}
 
 constexpr int kWB = 64;      // rows per block and columns per CTA
 constexpr int kWKC = 16;     // K chunk of the off-diagonal update
@@ -121,6 +77,96 @@ __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, doubl
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(d0), "+d"(d1)
       : "d"(a), "d"(b));
+}
+
+// Blocked left-looking Cholesky in the oracle's order (chol_seq): every entry's chain
+//   s = A[r][j]; for k < j: s = fma(-L[r][k], L[j][k], s)   (diagonal: r = j, then sqrt)
+// is split at the panel start j0: the prefix k < j0 runs on the FP64 tensor pipe (DMMA = the
+// sequential fma chain, scripts/exp/dmma_order.cu) for all rows below the panel in parallel, the
+// rest k in [j0, j) inside the panel (<= 31 steps).  Row-major A, L (M x M).
+constexpr int kCP = 32;  // panel width
+
+// rows [j0, M) x panel columns [j0, j0 + pw): running values A[r][j] - sum_{k<j0} L[r][k] L[j][k]
+__global__ void __launch_bounds__(128) chol_panel_update_kernel(const double* A, int M, int j0, int pw, double* L) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, grp = lane >> 2, tig = lane & 3;
+  const int R0 = j0 + blockIdx.x * 64 + 16 * w;
+  double acc[2][4][2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = R0 + 8 * u + grp, j = j0 + 8 * v + 2 * tig + h;
+        acc[u][v][h] = (r < M && j < j0 + pw) ? A[static_cast<size_t>(r) * M + j] : 0.0;
+      }
+  const double* ra[2];
+  const double* rb[4];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int r = R0 + 8 * u + grp;
+    ra[u] = r < M ? L + static_cast<size_t>(r) * M + tig : nullptr;
+  }
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const int j = j0 + 8 * v + grp;
+    rb[v] = j < j0 + pw ? L + static_cast<size_t>(j) * M + tig : nullptr;
+  }
+  for (int kb = 0; kb < j0; kb += 4) {
+    double fa[2], fb[4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) fa[u] = ra[u] ? -ra[u][kb] : 0.0;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) fb[v] = rb[v] ? rb[v][kb] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) dmma_f64(acc[u][v][0], acc[u][v][1], fa[u], fb[v]);
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = R0 + 8 * u + grp, j = j0 + 8 * v + 2 * tig + h;
+        if (r < M && j < j0 + pw) L[static_cast<size_t>(r) * M + j] = acc[u][v][h];
+      }
+}
+
+// the panel's in-panel chain: column by column, the diagonal (thread of row j), then every row
+// below; one CTA, rows strided over the threads
+__global__ void __launch_bounds__(1024) chol_panel_factor_kernel(int M, int j0, int pw, double* L, int* fail) {
+  __shared__ double sP[kCP][kCP + 1];  // the panel's diagonal block (rows j0.., cols j0..)
+  __shared__ double s_d;
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  for (int jj = 0; jj < pw; ++jj) {
+    const int j = j0 + jj;
+    if (threadIdx.x == 0) {
+      double acc = L[static_cast<size_t>(j) * M + j];
+      for (int k = 0; k < jj; ++k) acc = __fma_rn(-sP[jj][k], sP[jj][k], acc);
+      if (acc <= 0.0) s_bad = 1;
+      const double d = __dsqrt_rn(acc);
+      s_d = d;
+      sP[jj][jj] = d;
+      L[static_cast<size_t>(j) * M + j] = d;
+    }
+    __syncthreads();
+    if (s_bad) break;
+    const double d = s_d;
+    for (int r = j + 1 + threadIdx.x; r < M; r += blockDim.x) {
+      const double* Lr = L + static_cast<size_t>(r) * M + j0;
+      double sv = Lr[jj];
+      for (int k = 0; k < jj; ++k) sv = __fma_rn(-Lr[k], sP[jj][k], sv);
+      const double v = __ddiv_rn(sv, d);
+      L[static_cast<size_t>(r) * M + j] = v;
+      if (r - j0 < kCP) sP[r - j0][jj] = v;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && s_bad) *fail = 1;
 }
 
 // Zero-padded copy of L with a 16-double row stride (cp.async alignment).
@@ -1051,15 +1097,19 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
         DevBuf<int> fail(1);
         const double jitter = 1e-8 * p.sigma1_2;
         bool ok = false;
-        STGP_CUDA(cudaFuncSetAttribute(chol_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(sizeof(double) * M)));
+
         for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
           std::unique_ptr<ProfRegion> prc(new ProfRegion(ctx, "dr_sigma_chol"));
           sel_sigma_kernel<<<grid_for(static_cast<long long>(M) * M), 256, 0, st>>>(
               dzx.get(), dzy.get(), dzt.get(), M, k, lt, jitter, attempt == 0 ? 0.0 : 9.0 * jitter, A.get());
           launched(ctx);
           fail.zero(st);
-          chol_seq_kernel<<<1, 1024, sizeof(double) * M, st>>>(A.get(), M, L.get(), fail.get());
+          for (int j0 = 0; j0 < M; j0 += kCP) {
+            const int pw = std::min(kCP, M - j0);
+            chol_panel_update_kernel<<<ceil_div(M - j0, 64), 128, 0, st>>>(A.get(), M, j0, pw, L.get());
+            chol_panel_factor_kernel<<<1, 1024, 0, st>>>(M, j0, pw, L.get(), fail.get());
+            ctx->launches += 1;
+          }
           launched(ctx);
           prc.reset();
           int f = 0;
