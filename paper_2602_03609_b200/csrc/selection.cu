@@ -278,41 +278,56 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
       cp_async_wait<0>();
     }
     __syncthreads();
+    // accumulators -> sOut (column-major: sOut[c][r]) and the diagonal block of L -> sD
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          sOut[(32 * wc + 8 * v + 2 * tig + h) * 65 + 16 * wr + 8 * u + grp] = acc[u][v][h];
     for (int e = t; e < 64 * 64; e += kWthreads) {
       const int rr = e / 64, cc = e % 64;
       sD[rr * 65 + cc] = (rr < rb && cc <= rr) ? Lp[static_cast<size_t>(r0 + rr) * ldL + r0 + cc] : 0.0;
     }
     __syncthreads();
-    // diagonal block: column wavefront; outputs collected column-major in sOut
-    for (int cl = 0; cl < rb; ++cl) {
-      double* buf = wrow + (cl & 1) * 64;
-      if (wr == (cl >> 4) && grp == (cl & 7)) {
-        const double d = sD[cl * 65 + cl];
-        const int uo = (cl >> 3) & 1;
+    // diagonal block: the columns are independent forward substitutions, so warp w solves columns
+    // 8w..8w+7 alone (lanes hold rows lane, lane + 32; lanes 0..7 divide, one column each): no
+    // block-wide barrier per step.  Row r still receives -L[r][c] w_c for c = r0.. in order.
+    {
+      const int cb = 8 * wid;
+      double a0[8], a1[8];
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
-          if (u == uo)
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int c = 32 * wc + 8 * v + 2 * tig + h;
-                const double wv = __ddiv_rn(acc[u][v][h], d);
-                buf[c] = wv;
-                sOut[c * 65 + cl] = wv;
-              }
+      for (int q = 0; q < 8; ++q) {
+        a0[q] = sOut[(cb + q) * 65 + lane];
+        a1[q] = sOut[(cb + q) * 65 + lane + 32];
       }
-      __syncthreads();
+      for (int cl = 0; cl < rb; ++cl) {
+        const int own = cl & 31;
+        const bool hi = cl >= 32;
+        double mine = 0.0;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int rr = 16 * wr + 8 * u + grp;
-        if (rr > cl && rr < rb) {
-          const double l = -sD[rr * 65 + cl];
-#pragma unroll
-          for (int v = 0; v < 4; ++v)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) acc[u][v][h] = __fma_rn(l, buf[32 * wc + 8 * v + 2 * tig + h], acc[u][v][h]);
+        for (int q = 0; q < 8; ++q) {
+          const double tq = __shfl_sync(kFull, hi ? a1[q] : a0[q], own);
+          if (lane == q) mine = tq;
         }
+        const double wq = lane < 8 ? __ddiv_rn(mine, sD[cl * 65 + cl]) : 0.0;
+        const double l0 = lane > cl ? -sD[lane * 65 + cl] : 0.0;
+        const double l1 = lane + 32 > cl && lane + 32 < rb ? -sD[(lane + 32) * 65 + cl] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double wv = __shfl_sync(kFull, wq, q);
+          if (lane > cl) a0[q] = __fma_rn(l0, wv, a0[q]);
+          if (lane + 32 > cl) a1[q] = __fma_rn(l1, wv, a1[q]);
+          if (lane == own) {
+            if (hi) a1[q] = wv; else a0[q] = wv;
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        sOut[(cb + q) * 65 + lane] = a0[q];
+        sOut[(cb + q) * 65 + lane + 32] = a1[q];
       }
     }
     __syncthreads();
