@@ -306,7 +306,7 @@ def main():
         t0 = time.perf_counter()
         nb = S.correlation_neighbors(ds, theta, args.m_v)
         nn_s = time.perf_counter() - t0
-        knn_ms = ctx.profile_get("knn_dc")[0]
+        knn_ms = ctx.profile_get("knn_dc")[0] + ctx.profile_get("knn_dr")[0] + ctx.profile_get("dr_whiten")[0]
         t0 = time.perf_counter()
         nb = S.correlation_neighbors(ds, theta, args.m_v)  # warm repeat (identical sets)
         extra["nn_search_warm_s"] = time.perf_counter() - t0

@@ -856,7 +856,15 @@ int stgp_correlation_neighbors(stgp_dataset* ds, const stgp_params* theta, int m
     Params p;
     std::memcpy(&p, theta, sizeof(p));
     validate_params(p);
-    *out = run_search(ds, STGP_METRIC_DC, &p, m_v, 1.0, 1.0);
+    // The spatial-tile search with an empty inducing set is also the exact d_c search (selection.cu,
+    // STGP_DC_SPATIAL=1; identical sets).  Without a Gram per tile its 64 x 64 evaluation is less
+    // selective than the per-query time-block pruning of knn_kernel<0>: 61 vs 70 ms on the device at
+    // cfg4, slower end to end with the tile set-up, so knn_kernel<0> stays the default.
+    const char* sp = std::getenv("STGP_DC_SPATIAL");
+    if (sp && sp[0] == '1')
+      *out = spatial_search(ds, p, std::vector<double>(), m_v, STGP_METRIC_DC);
+    else
+      *out = run_search(ds, STGP_METRIC_DC, &p, m_v, 1.0, 1.0);
   });
 }
 

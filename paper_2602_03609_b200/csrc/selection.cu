@@ -1044,18 +1044,23 @@ int guarded(F&& f) {
 
 extern "C" {
 
-int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const stgp_inducing* ind, int m_v,
-                            stgp_neighbors** out) {
-  return guarded([&] {
-    if (!ds || !theta || !ind || !out) config_error("stgp_residual_neighbors: null argument");
+}  // extern "C"
+
+namespace stgp {
+
+// The exact spatial-tile search over predecessors (header comments of knn_dr_kernel).  With
+// inducing points it is the d_r search (neighbors.cpp:51-83, 324-329); with none, r_i = s1 and
+// w = 0, so d = sqrt(1 - |k| / sqrt(s1 s1)) = sqrt(1 - |k / s1|) (sqrt(fl(s1 s1)) = s1 in round to
+// nearest): the d_c search (neighbors.cpp:37-43, 318-322), pruned spatially instead of by time only.
+stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vector<double>& zxyt, int m_v,
+                               int kind) {
+  stgp_neighbors* result = nullptr;
+  {
     if (m_v < 0) config_error("m_v must be >= 0");
     if (m_v > 32) config_error("neighbour search supports m_v <= 32 on the device");
-    Params p;
-    std::memcpy(&p, theta, sizeof(p));
-    validate_params(p);
     stgp_ctx* ctx = ds->ctx;
     cudaStream_t st = ctx->stream;
-    const int n = ds->n, M = ind->M();
+    const int n = ds->n, M = static_cast<int>(zxyt.size() / 3);
     const DevKernel k = dev_kernel(p);
     // diagnostics (STGP_DR_STATS): host-side phase times
     const bool dbg = std::getenv("STGP_DR_STATS") != nullptr;
@@ -1071,9 +1076,9 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
     // time index over data + inducing times, live factors (no lag table in the selection kernel)
     std::vector<double> zx(M), zy(M), zt(M);
     for (int j = 0; j < M; ++j) {
-      zx[j] = ind->xyt[3 * j];
-      zy[j] = ind->xyt[3 * j + 1];
-      zt[j] = ind->xyt[3 * j + 2];
+      zx[j] = zxyt[3 * j];
+      zy[j] = zxyt[3 * j + 1];
+      zt[j] = zxyt[3 * j + 2];
     }
     std::set<double> it(zt.begin(), zt.end());
     std::vector<double> Ti(it.begin(), it.end());
@@ -1157,7 +1162,7 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
     nb->ctx = ctx;
     nb->n = n;
     nb->m_v = std::max(m_v, 1);
-    nb->kind = STGP_METRIC_DR;
+    nb->kind = kind;
     const size_t total = static_cast<size_t>(n) * nb->m_v;
     nb->idx.alloc(total);
     nb->dist.alloc(total);
@@ -1403,10 +1408,26 @@ int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const st
     }
     STGP_CUDA(cudaStreamSynchronize(st));
     prof_collect(ctx);
-    *out = nb.release();
+    result = nb.release();
     lap("finish");
-  });
+  }
   // (W, tiles and stats are released here, after the lap above)
+  return result;
+}
+
+}  // namespace stgp
+
+extern "C" {
+
+int stgp_residual_neighbors(stgp_dataset* ds, const stgp_params* theta, const stgp_inducing* ind, int m_v,
+                            stgp_neighbors** out) {
+  return guarded([&] {
+    if (!ds || !theta || !ind || !out) config_error("stgp_residual_neighbors: null argument");
+    Params p;
+    std::memcpy(&p, theta, sizeof(p));
+    validate_params(p);
+    *out = spatial_search(ds, p, ind->xyt, m_v, STGP_METRIC_DR);
+  });
 }
 
 }  // extern "C"

@@ -88,7 +88,9 @@ double nll_const(int n);
 void launch_nll_stored(stgp_structure* s, int blocks, double* u_out);
 int row_blocks(stgp_ctx* ctx, int rows);
 int lfac_stride_for(int m_v);
-unsigned long long* claim_counter(stgp_ctx* ctx);  // zeroed in-order work counter  // per-row stored closure factor size (doubles)
+unsigned long long* claim_counter(stgp_ctx* ctx);  // zeroed in-order work counter
+// exact spatial-tile neighbour search (selection.cu): d_r with inducing points, d_c without
+stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vector<double>& zxyt, int m_v, int kind);  // per-row stored closure factor size (doubles)
 void upload_lag_table(DevLagTable& d, const TimeIndex& ti, const Params& p, const LagPolicy& pol,
                       cudaStream_t s, bool index_changed);
 LagTable lag_view(const DevLagTable& d);

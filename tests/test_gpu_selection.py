@@ -154,3 +154,16 @@ def test_dr_filter_on_off_identical(S, monkeypatch):
     b = S.residual_neighbors(ds, S.synth.THETA_T3, ind, 30)
     assert (a.indices() == b.indices()).all()
     assert _bits(a.distances(), b.distances())
+
+
+def test_dc_spatial_path_identical(S, monkeypatch):
+    # the spatial-tile search with no inducing points is the exact d_c search
+    x, y, t, _ = S.synth.station_day(1200, 5, box=(4.6e6, 2.9e6), theta=S.synth.THETA_T3, seed=12)
+    perm = O.order_observations(t, 12)
+    x, y, t = x[perm], y[perm], t[perm]
+    ds = S.SpaceTimeDataset(x, y, t)
+    a = S.correlation_neighbors(ds, S.synth.THETA_T3, 30)
+    monkeypatch.setenv("STGP_DC_SPATIAL", "1")
+    b = S.correlation_neighbors(ds, S.synth.THETA_T3, 30)
+    assert (a.indices() == b.indices()).all()
+    assert _bits(a.distances(), b.distances())
