@@ -4,6 +4,7 @@
 // partials (used by the single-GPU shard emulation tests).
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 
 #include "comm.hpp"
@@ -42,6 +43,43 @@ void allreduce_host(stgp_ctx* ctx, std::vector<double>& v) {
   d.upload(v.data(), v.size(), ctx->stream);
   allreduce_sum(ctx, d.get(), v.size());
   d.download(v.data(), v.size(), ctx->stream);
+  STGP_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+namespace {
+__global__ void gather_pack_kernel(long long total, int m_v, int r0, int r1, const int32_t* idx, const double* dist,
+                                   double* bi, double* bd) {
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long row = e / m_v;
+    const bool own = row >= r0 && row < r1;
+    bi[e] = own ? static_cast<double>(idx[e]) + 1.0 : 0.0;
+    bd[e] = own && dist ? dist[e] : 0.0;
+  }
+}
+__global__ void gather_unpack_kernel(long long total, const double* bi, const double* bd, int32_t* idx, double* dist) {
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    idx[e] = static_cast<int32_t>(bi[e]) - 1;
+    if (dist) dist[e] = bd[e];
+  }
+}
+}  // namespace
+
+// Every rank computed neighbour rows [r0, r1) of its shard; afterwards all ranks hold all rows.  A sum
+// all-reduce of zero-filled buffers (indices stored as idx + 1, exact in f64): x + 0 = x bit for bit,
+// and the same collective serves NCCL and the host hook.
+void gather_rows(stgp_ctx* ctx, int32_t* idx, double* dist, long long n, int m_v, int r0, int r1) {
+  if (ctx->world == 1 || n == 0) return;
+  const long long total = n * m_v;
+  DevBuf<double> bi(static_cast<size_t>(total)), bd(static_cast<size_t>(total));
+  const int grid = static_cast<int>(std::min<long long>((total + 255) / 256, ctx->num_sms * 32LL));
+  gather_pack_kernel<<<grid, 256, 0, ctx->stream>>>(total, m_v, r0, r1, idx, dist, bi.get(), bd.get());
+  ++ctx->launches;
+  allreduce_sum(ctx, bi.get(), static_cast<size_t>(total));
+  allreduce_sum(ctx, bd.get(), static_cast<size_t>(total));
+  gather_unpack_kernel<<<grid, 256, 0, ctx->stream>>>(total, bi.get(), bd.get(), idx, dist);
+  ++ctx->launches;
   STGP_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 

@@ -10,6 +10,7 @@
 #include <random>
 #include <set>
 
+#include "comm.hpp"
 #include "engine.hpp"
 #include "rows.cuh"
 #include "rows_serial.cuh"
@@ -789,16 +790,19 @@ static stgp_neighbors* run_search(stgp_dataset* ds, int metric, const Params* th
   SearchArgs a{};
   a.n = ds->n;
   a.m_v = m_v == 0 ? 1 : m_v;
-  a.q_begin = 0;
-  a.q_end = ds->n;
+  // queries shard by contiguous rows across ranks; candidates are replicated (gather_rows after)
+  int q0 = 0, q1 = ds->n;
+  shard_rows(ctx, ds->n, q0, q1);
+  a.q_begin = q0;
+  a.q_end = q1;
   a.x = ds->x.get();
   a.y = ds->y.get();
   a.t = ds->t.get();
   a.tid = ds->tid.get();
   a.ss = ss;
   a.ts = ts;
-  a.out = nb->idx.get();
-  a.dist = nb->dist.get();
+  a.out = nb->idx.get() + static_cast<size_t>(q0) * a.m_v;
+  a.dist = nb->dist.get() + static_cast<size_t>(q0) * a.m_v;
   DevLagTable dl;
   TimeIndex ti;
   if (ds->time_sorted) {
@@ -822,7 +826,7 @@ static stgp_neighbors* run_search(stgp_dataset* ds, int metric, const Params* th
     upload_lag_table(dl, ti, *th, live, ctx->stream, true);
     a.lt = lag_view(dl);
   }
-  const int blocks = std::max(1, std::min(ceil_div(ds->n, 8), ctx->num_sms * 8));
+  const int blocks = std::max(1, std::min(ceil_div(std::max(q1 - q0, 1), 8), ctx->num_sms * 8));
   if (m_v == 0) {
     std::vector<int32_t> neg(total, -1);
     nb->idx.upload(neg.data(), total, ctx->stream);
@@ -836,6 +840,7 @@ static stgp_neighbors* run_search(stgp_dataset* ds, int metric, const Params* th
     ++ctx->launches;
   }
   STGP_LAUNCH_CHECK();
+  if (m_v > 0) gather_rows(ctx, nb->idx.get(), nb->dist.get(), ds->n, a.m_v, q0, q1);
   STGP_CUDA(cudaStreamSynchronize(ctx->stream));
   prof_collect(ctx);
   return nb.release();

@@ -514,6 +514,7 @@ struct DrArgs {
   int ld16;
   const double* wnorm;
   int prune;                  // exact tile pruning (time-sorted rows)
+  int tile0;                  // first query tile of this launch (rank shard)
   double s1;
   unsigned long long* stats;  // optional: [0] candidate tiles evaluated, [1] tiles pruned
 };
@@ -719,7 +720,7 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
   __shared__ double s_d;
   __shared__ double sAQ[kMaxGroups];
   const DrTiles& T = a.T;
-  const int qt = blockIdx.x;
+  const int qt = a.tile0 + blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int grp = lane >> 2, tig = lane & 3;
   const int wr = wid >> 1, wc = wid & 1;  // warp sub-tile: rows 16 wr.., cols 32 wc..
@@ -1390,8 +1391,26 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
       ProfRegion pr(ctx, "knn_dr");
       STGP_CUDA(cudaFuncSetAttribute(knn_dr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kDrSmem)));
-      knn_dr_kernel<<<ntile, kDrThreads, kDrSmem, st>>>(a);
-      launched(ctx);
+      // ranks shard the queries by whole time buckets (contiguous rows), balanced by row count;
+      // candidates (W, tiles) are replicated and the rows gathered afterwards
+      int b0 = 0, b1 = nbucket;
+      if (ctx->world > 1) {
+        int r0 = 0, r1 = n;
+        shard_rows(ctx, n, r0, r1);
+        auto first_at = [&](int row) {
+          return static_cast<int>(std::lower_bound(bstart.begin(), bstart.end() - 1, row) - bstart.begin());
+        };
+        b0 = ctx->rank == 0 ? 0 : first_at(r0);
+        b1 = ctx->rank == ctx->world - 1 ? nbucket : first_at(r1);
+      }
+      a.tile0 = btile0[static_cast<size_t>(b0)];
+      const int nt = btile0[static_cast<size_t>(b1)] - a.tile0;
+      if (nt > 0) {
+        knn_dr_kernel<<<nt, kDrThreads, kDrSmem, st>>>(a);
+        launched(ctx);
+      }
+      gather_rows(ctx, nb->idx.get(), nb->dist.get(), n, m_v, bstart[static_cast<size_t>(b0)],
+                  bstart[static_cast<size_t>(b1)]);
       lap("knn");
       if (a.stats) {
         unsigned long long h[50];

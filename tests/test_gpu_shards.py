@@ -76,3 +76,55 @@ def test_sharded_equals_single(S, kind, world):
         assert np.allclose(g, g1, rtol=1e-10, atol=1e-10 * np.abs(g1).max())
     # every rank holds identical bits
     assert all(r[0] == res[0][0] and (r[1] == res[0][1]).all() for r in res)
+
+
+@pytest.mark.parametrize("metric", ["dr", "dc", "euclid"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_search_equals_single(S, metric, world):
+    # queries shard by rows / time buckets, rows are gathered: every rank holds the full sets, bit-equal
+    x, y, t, _ = S.synth.station_day(150, 8, seed=6)
+    perm = O.order_observations(t, 6)
+    x, y, t = x[perm], y[perm], t[perm]
+    Z, _, _ = O.sts_kmeanspp(x, y, t, 60, 6)
+
+    def search(S, ctx):
+        ds = S.SpaceTimeDataset(x, y, t, ctx=ctx)
+        if metric == "dr":
+            nb = S.residual_neighbors(ds, SEC4, S.InducingSet.from_points(Z, ctx=ctx), 10)
+        elif metric == "dc":
+            nb = S.correlation_neighbors(ds, SEC4, 10)
+        else:
+            nb = S.euclidean_neighbors(ds, 10, 0.5, 2.0)
+        return nb.indices(), nb.distances()
+
+    def run(world):
+        out, err = [None] * world, [None] * world
+        hub = S.api.HostAllreduce(world) if world > 1 else None
+
+        def work(rank):
+            try:
+                ctx = S.Context(0)
+                if world > 1:
+                    ctx.set_shard(rank, world)
+                    ctx.set_host_allreduce(hub.for_rank(rank))
+                out[rank] = search(S, ctx)
+            except Exception as e:  # noqa: BLE001
+                err[rank] = e
+                if hub:
+                    hub.barrier.abort()
+
+        th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+        for h in th:
+            h.start()
+        for h in th:
+            h.join()
+        for e in err:
+            if e is not None:
+                raise e
+        return out
+
+    (i1, d1), = run(1)
+    for ir, dr in run(world):
+        assert (ir == i1).all()
+        ok = ~np.isnan(d1)
+        assert (np.isnan(dr) == ~ok).all() and (dr[ok].view(np.int64) == d1[ok].view(np.int64)).all()
