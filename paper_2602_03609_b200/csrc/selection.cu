@@ -550,13 +550,6 @@ __device__ __forceinline__ double tile_cmax(const DrArgs& a, int tminQ, int tmax
   return (a.s1 * pe_min * mat / sqrt(rQ * T.rmin[ct]) + wt) * (1.0 + 1e-11);
 }
 
-// the worst current list entry over the tile's (non-degenerate) queries; inf while any list is short
-__device__ __forceinline__ double tile_threshold(const double (*topd)[32], const int* qm) {
-  double d = 0.0;
-  for (int qq = 0; qq < kQT; ++qq)
-    if (qm[qq] > 0) d = fmax(d, topd[qq][qm[qq] - 1]);
-  return d;
-}
 
 // Exact d_r top-m over predecessors on spatial tiles.  CTA = one query tile (<= 64 rows of one time
 // bucket, Morton order).  Candidate tiles are visited bucket by bucket backwards in time, each
@@ -716,7 +709,7 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
   int (*topj)[32] = reinterpret_cast<int (*)[32]>(sm + kStages * kDrStageDoubles + kQT * 32);
   __shared__ int qidx[kQT], cidx[kCT], qm[kQT], qemit[kQT];
   __shared__ double s_dmax[kDrThreads / 32];
-  __shared__ int s_surv[32], s_nsurv, s_skip;
+  __shared__ int s_surv[32], s_nsurv;
   __shared__ double s_d;
   __shared__ double sAQ[kMaxGroups];
   const DrTiles& T = a.T;
