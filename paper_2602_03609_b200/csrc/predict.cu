@@ -51,11 +51,16 @@ struct PredArgs {
   const double* resid;
   const double* Wq;     // ldm x np
   const double* rq;     // np
+  // d_r pruning: |w_j|^2 (n), |w_q|^2 (np); per time block min r and max |w| / sqrt(r) over its
+  // non-degenerate rows
+  const double *wsq, *wqsq, *blk_rmin, *blk_amax;
   int32_t* nbr_out;     // np x m (ascending)
   double* scratch_d;    // np x n (generic path)
 };
 
-__device__ __forceinline__ double target_dist(const PredArgs& a, int p, int j) {
+// wd: the target's current worst list entry (inf while short).  d_r returns +inf for a candidate
+// that provably cannot beat it: |k - w_q.w_j| <= |k| + |w_q||w_j| (skips the M-long dot product).
+__device__ __forceinline__ double target_dist(const PredArgs& a, int p, int j, double wd) {
   if (a.metric == 0) {
     const double dx = __ddiv_rn(__dsub_rn(a.qx[p], a.x[j]), a.ss);
     const double dy = __ddiv_rn(__dsub_rn(a.qy[p], a.y[j]), a.ss);
@@ -73,6 +78,10 @@ __device__ __forceinline__ double target_dist(const PredArgs& a, int p, int j) {
   const double dj = a.resid[j], rq = a.rq[p];
   if (dj <= tol || rq <= tol) return 1.0;
   double rho = cov;
+  if (a.M > 0 && a.wsq && wd < 1.0) {
+    const double ub = (fabs(cov) + sqrt(a.wqsq[p] * a.wsq[j]) * (1.0 + 1e-12)) / sqrt(dj * rq) * (1.0 + 1e-11);
+    if ((1.0 - ub) - 1e-12 > wd) return __longlong_as_double(0x7ff0000000000000LL);
+  }
   if (a.M > 0) {
     const double* wq = a.Wq + static_cast<size_t>(p) * a.ldm;
     const double* wj = a.W + static_cast<size_t>(j) * a.ldm;
@@ -81,6 +90,37 @@ __device__ __forceinline__ double target_dist(const PredArgs& a, int p, int j) {
     rho = __dsub_rn(rho, s);
   }
   return __dsub_rn(1.0, __ddiv_rn(fabs(rho), __dsqrt_rn(__dmul_rn(dj, rq))));
+}
+
+// per time block: min r and max |w| / sqrt(r) over its non-degenerate rows (inf / 0 when none)
+__global__ void __launch_bounds__(256) block_bound_kernel(int nblk, const int32_t* blk_start, const double* resid,
+                                                          const double* wsq, double s1, double* rmin, double* amax) {
+  __shared__ double sr[256], sa[256];
+  for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+    double r0 = __longlong_as_double(0x7ff0000000000000LL), a0 = 0.0;
+    for (int j = blk_start[b] + threadIdx.x; j < blk_start[b + 1]; j += blockDim.x) {
+      const double r = resid[j];
+      if (r > 1e-7 * s1) {
+        r0 = fmin(r0, r);
+        a0 = fmax(a0, sqrt(wsq[j] / r) * (1.0 + 1e-12));
+      }
+    }
+    sr[threadIdx.x] = r0;
+    sa[threadIdx.x] = a0;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+      if (threadIdx.x < o) {
+        sr[threadIdx.x] = fmin(sr[threadIdx.x], sr[threadIdx.x + o]);
+        sa[threadIdx.x] = fmax(sa[threadIdx.x], sa[threadIdx.x + o]);
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      rmin[b] = sr[0];
+      amax[b] = sa[0];
+    }
+    __syncthreads();
+  }
 }
 
 // warp per target, m <= 32: exact top-m over all rows, nearest time blocks first
@@ -121,6 +161,14 @@ __global__ void __launch_bounds__(256) target_knn_kernel(PredArgs a) {
             double pe, pb;
             a.lt.get2(a.qtid[p], a.tid[s0], pe, pb);
             if ((1.0 - pe) - 1e-12 > wd) continue;
+          } else if (a.M > 0 && a.blk_amax && wd < 1.0 && a.rq[p] > 1e-7 * a.s1) {
+            // d_r block bound: s1 T(u)^-E / sqrt(r_q rmin_b) + a_q amax_b (degenerate rows sit at d = 1)
+            double pe, pb;
+            a.lt.get2(a.qtid[p], a.tid[s0], pe, pb);
+            const double rq = a.rq[p];
+            const double cb = (a.s1 * pe / sqrt(rq * a.blk_rmin[b]) + sqrt(a.wqsq[p] / rq) * a.blk_amax[b]) *
+                              (1.0 + 1e-11);
+            if (cb < 1.0 && (1.0 - cb) - 1e-12 > wd) continue;
           }
         }
       } else {
@@ -130,8 +178,8 @@ __global__ void __launch_bounds__(256) target_knn_kernel(PredArgs a) {
       for (int j0 = s0; j0 < s1e; j0 += 32) {
         const int j = j0 + lane;
         double d = __longlong_as_double(0x7ff0000000000000LL);
-        if (j < s1e) d = target_dist(a, p, j);
         const double wd = __shfl_sync(kFull, e.d, m - 1);
+        if (j < s1e) d = target_dist(a, p, j, wd);
         const int wj = __shfl_sync(kFull, e.j, m - 1);
         const unsigned acc = __ballot_sync(kFull, j < s1e && lex_less(d, j, wd, wj));
         if (acc) topm_insert(e, m, acc, d, j, lane);
@@ -145,7 +193,7 @@ __global__ void __launch_bounds__(256) target_knn_kernel(PredArgs a) {
 __global__ void target_knn_generic_kernel(PredArgs a) {
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < a.np; p += gridDim.x * blockDim.x) {
     double* d = a.scratch_d + static_cast<size_t>(p) * a.n;
-    for (int j = 0; j < a.n; ++j) d[j] = target_dist(a, p, j);
+    for (int j = 0; j < a.n; ++j) d[j] = target_dist(a, p, j, __longlong_as_double(0x7ff0000000000000LL));
     const int m = min(a.m, a.n);
     int32_t* out = a.nbr_out + static_cast<size_t>(p) * a.m;
     // m rounds of arg-min over the remaining rows (ties to the smaller index)
@@ -377,7 +425,8 @@ static void setup_targets(stgp_structure* s, int np, const double* txyt, TargetS
 }
 
 static void target_neighbors(stgp_structure* s, TargetSet& T, int np, int pred_m_v, int metric, const double* Wq,
-                             const double* rq, const double* resid, DevBuf<int32_t>& nbr) {
+                             const double* rq, const double* resid, DevBuf<int32_t>& nbr, const double* wsq = nullptr,
+                             const double* wqsq = nullptr) {
   stgp_ctx* ctx = s->ds->ctx;
   PredArgs a{};
   a.n = s->n;
@@ -398,7 +447,7 @@ static void target_neighbors(stgp_structure* s, TargetSet& T, int np, int pred_m
   a.lt = lag_view(s->lt);
   a.s1 = s->th.sigma1_2;
   DevBuf<double> Td;
-  if (s->ds->time_sorted && metric != 2) {
+  if (s->ds->time_sorted) {
     Td.upload(s->ds->Tdata.data(), s->ds->Tdata.size(), ctx->stream);
     a.blk_start = s->ds->blk_start.get();
     a.Tdata = Td.get();
@@ -410,6 +459,20 @@ static void target_neighbors(stgp_structure* s, TargetSet& T, int np, int pred_m
   a.resid = resid;
   a.Wq = Wq;
   a.rq = rq;
+  DevBuf<double> brmin, bamax;
+  if (metric == 2 && s->lr.M > 0 && wsq && wqsq) {
+    a.wsq = wsq;
+    a.wqsq = wqsq;
+    if (a.blk_start) {
+      brmin.alloc(static_cast<size_t>(a.nblk));
+      bamax.alloc(static_cast<size_t>(a.nblk));
+      block_bound_kernel<<<std::max(1, std::min(a.nblk, ctx->num_sms * 4)), 256, 0, ctx->stream>>>(
+          a.nblk, a.blk_start, resid, wsq, s->th.sigma1_2, brmin.get(), bamax.get());
+      launched(ctx);
+      a.blk_rmin = brmin.get();
+      a.blk_amax = bamax.get();
+    }
+  }
   nbr.ensure(static_cast<size_t>(np) * pred_m_v);
   a.nbr_out = nbr.get();
   DevBuf<double> scratch;
@@ -588,7 +651,8 @@ static void vif_predict(stgp_structure* s, TargetSet& T, int np, int pred_m_v, d
   }
   const int m = std::max(1, std::min(pred_m_v, n));
   DevBuf<int32_t> nbr;
-  target_neighbors(s, T, np, m, 2, Wq.get(), rq.get(), resid, nbr);
+  target_neighbors(s, T, np, m, 2, Wq.get(), rq.get(), resid, nbr, M > 0 ? L.tmp("p_sq", n) : nullptr,
+                   M > 0 ? wq2.get() : nullptr);
   DevBuf<double> mp(np), Dp(np), A(static_cast<size_t>(np) * m);
   cond_solve(s, T, np, m, nbr, z, true, Wq.get(), rq.get(), mp.get(), Dp.get(), A.get());
   std::vector<double> hmu(np), hD(np), hwq2(np), hwa(np, 0.0), hcross(np, 0.0), hq(np, 0.0), hh(np, 0.0);

@@ -141,3 +141,23 @@ def test_gls_parity(S, kind):
         om = O.OracleModel("vif", x, y, t, th, nbr=nbr, Z=Z)
     b = S.gls_beta(s, yv, X)
     assert np.allclose(b, om.gls_beta(yv, X), rtol=1e-9, atol=1e-12)
+
+
+def test_vif_predict_station_day_pruned_search(S):
+    # time-sorted station x day data: the d_r target search visits time blocks nearest first and
+    # prunes blocks and pairs with the |w| bounds; results must equal the oracle's exhaustive search
+    x, y, t, yv = S.synth.station_day(150, 6, seed=17)
+    perm = O.order_observations(t, 17)
+    x, y, t, yv = x[perm], y[perm], t[perm], yv[perm]
+    th = S.synth.THETA_SEC4
+    Z, _, _ = O.sts_kmeanspp(x, y, t, 60, 17)
+    nbr = O.dr_neighbors(x, y, t, th, Z, 10)
+    ds = S.SpaceTimeDataset(x, y, t)
+    s = S.build_vif(ds, th, S.InducingSet.from_points(Z), S.NeighborSets.from_sets(ds, nbr, S.api.METRIC_DR),
+                    S.OBSERVATION)
+    last = t == t.max()
+    T = np.vstack([np.column_stack([x[last], y[last], np.full(int(last.sum()), t.max() + 1.0)]),
+                   np.column_stack([x[:20] + 0.01, y[:20], t[:20] + 0.5])])
+    pr = S.predict(s, yv, None, None, T, pred_m_v=10)
+    mu, var = O.OracleModel("vif", x, y, t, th, nbr=nbr, Z=Z).predict(yv, T, 10)
+    assert np.allclose(pr.mu, mu, rtol=1e-8, atol=1e-10) and np.allclose(pr.var, var, rtol=1e-8, atol=1e-10)
