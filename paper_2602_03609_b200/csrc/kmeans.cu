@@ -14,6 +14,7 @@
 #include <numeric>
 #include <random>
 #include <set>
+#include <unordered_map>
 
 #include "comm.hpp"
 #include "lowrank_common.cuh"
@@ -176,30 +177,62 @@ __global__ void assign_kernel(KArgs a, int* assign, double* best) {
 }
 
 // inertia = sequential sum of best distances
-__global__ void inertia_kernel(const double* best, long n, double* out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// Sequential sum of best[] (order-defined): the block stages chunks in shared memory, thread 0
+// runs the chain with loads batched ahead.
+constexpr int kLloydChunk = 4096;
+__global__ void __launch_bounds__(1024) inertia_kernel(const double* best, long n, double* out) {
+  __shared__ double sb[kLloydChunk];
   double s = 0.0;
-  for (long i = 0; i < n; ++i) s = __dadd_rn(s, best[i]);
-  *out = s;
+  for (long c0 = 0; c0 < n; c0 += kLloydChunk) {
+    const int len = static_cast<int>(min(static_cast<long>(kLloydChunk), n - c0));
+    __syncthreads();
+    for (int i = threadIdx.x; i < len; i += blockDim.x) sb[i] = best[c0 + i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int i = 0;
+      for (; i + 8 <= len; i += 8) {
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = sb[i + q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s = __dadd_rn(s, v[q]);
+      }
+      for (; i < len; ++i) s = __dadd_rn(s, sb[i]);
+    }
+  }
+  if (threadIdx.x == 0) *out = s;
 }
-
-// per-cluster sequential sums in point order (one thread per cluster)
-__global__ void cluster_sum_kernel(KArgs a, const int* assign, double* sums, int* counts) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < a.k; j += gridDim.x * blockDim.x) {
+// Per-cluster sums in point order (the reference's sequential accumulation): one thread per
+// cluster over block-staged chunks of assign[] and the points (d <= 3).
+__global__ void __launch_bounds__(1024) cluster_sum_kernel(KArgs a, const int* assign, double* sums, int* counts) {
+  constexpr int kCh = 1536;  // 42 KB of static shared memory
+  __shared__ int sa[kCh];
+  __shared__ double sp[3][kCh];
+  for (int j0 = 0; j0 < a.k; j0 += blockDim.x) {
+    const int j = j0 + threadIdx.x;
     double s[3] = {0.0, 0.0, 0.0};
     int cnt = 0;
-    for (long i = 0; i < a.n; ++i) {
-      if (assign[i] != j) continue;
-      for (int c = 0; c < a.d; ++c) s[c] = __dadd_rn(s[c], a.P[i + c * a.n]);
-      ++cnt;
+    for (long c0 = 0; c0 < a.n; c0 += kCh) {
+      const int len = static_cast<int>(min(static_cast<long>(kCh), a.n - c0));
+      __syncthreads();
+      for (int i = threadIdx.x; i < len; i += blockDim.x) {
+        sa[i] = assign[c0 + i];
+        for (int c = 0; c < a.d; ++c) sp[c][i] = a.P[c0 + i + static_cast<long>(c) * a.n];
+      }
+      __syncthreads();
+      if (j < a.k)
+        for (int i = 0; i < len; ++i) {
+          if (sa[i] != j) continue;
+          for (int c = 0; c < a.d; ++c) s[c] = __dadd_rn(s[c], sp[c][i]);
+          ++cnt;
+        }
     }
-    for (int c = 0; c < a.d; ++c) sums[j + static_cast<size_t>(c) * a.k] = s[c];
-    counts[j] = cnt;
+    if (j < a.k) {
+      for (int c = 0; c < a.d; ++c) sums[j + static_cast<size_t>(c) * a.k] = s[c];
+      counts[j] = cnt;
+    }
   }
 }
-
-// center update in cluster order; an empty cluster takes the point farthest
-// from its (current) center, first index on ties (inducing.cpp:89-107)
 __global__ void center_update_kernel(KArgs a, const int* assign, const double* sums, const int* counts) {
   __shared__ double bd[1024];
   __shared__ long bi[1024];
@@ -306,9 +339,10 @@ void kmeanspp_device(stgp_ctx* ctx, const double* P_host, long n, int d, int k, 
   for (int sweep = 0; sweep < 50; ++sweep) {
     assign_kernel<<<gb, 256, 0, st>>>(a, assign.get(), best.get());
     launched(ctx);
-    inertia_kernel<<<1, 32, 0, st>>>(best.get(), n, inertia.get());
+    inertia_kernel<<<1, 1024, 0, st>>>(best.get(), n, inertia.get());
     launched(ctx);
-    cluster_sum_kernel<<<grid_for(k, 64), 64, 0, st>>>(a, assign.get(), sums.get(), counts.get());
+    cluster_sum_kernel<<<1, std::min(1024, std::max(32, (k + 31) / 32 * 32)), 0, st>>>(a, assign.get(), sums.get(),
+                                                                                       counts.get());
     launched(ctx);
     center_update_kernel<<<1, 1024, 0, st>>>(a, assign.get(), sums.get(), counts.get());
     launched(ctx);
@@ -352,23 +386,54 @@ int stgp_kmeanspp(stgp_ctx* ctx, const double* P, int n, int d, int k, uint64_t 
 }
 
 // sts_kmeanspp (inducing.cpp:144-193): unique times / locations via ordered sets
+namespace {
+// bit key with -0.0 folded onto +0.0 (std::set's operator< treats them as equal)
+inline uint64_t dkey(double v) {
+  uint64_t b;
+  std::memcpy(&b, &v, sizeof(b));
+  return v == 0.0 ? 0 : b;
+}
+struct PairKeyHash {
+  size_t operator()(const std::pair<uint64_t, uint64_t>& k) const {
+    return std::hash<uint64_t>()(k.first * 0x9E3779B97F4A7C15ULL ^ (k.second + 0x632BE59BD9B4E019ULL));
+  }
+};
+std::vector<double> distinct_sorted_times(const std::vector<double>& t) {
+  std::unordered_map<uint64_t, double> first;
+  first.reserve(1024);
+  for (double v : t) first.emplace(dkey(v), v);
+  std::vector<double> out;
+  out.reserve(first.size());
+  for (const auto& kv : first) out.push_back(kv.second);
+  std::sort(out.begin(), out.end());
+  return out;
+}
+std::vector<std::pair<double, double>> distinct_sorted_locations(const std::vector<double>& x,
+                                                                 const std::vector<double>& y) {
+  std::unordered_map<std::pair<uint64_t, uint64_t>, std::pair<double, double>, PairKeyHash> first;
+  first.reserve(1 << 14);
+  for (size_t i = 0; i < x.size(); ++i) first.emplace(std::make_pair(dkey(x[i]), dkey(y[i])), std::make_pair(x[i], y[i]));
+  std::vector<std::pair<double, double>> out;
+  out.reserve(first.size());
+  for (const auto& kv : first) out.push_back(kv.second);
+  std::sort(out.begin(), out.end());
+  return out;
+}
+}  // namespace
+
 int stgp_sts_kmeanspp(stgp_dataset* ds, int m, uint64_t seed, stgp_inducing** out) {
   return guarded([&] {
     if (!ds || !out) config_error("stgp_sts_kmeanspp: null argument");
     if (m < 1) config_error("sts_kmeanspp: m must be >= 1");
     const int n = ds->n;
-    std::set<double> ts(ds->ht.begin(), ds->ht.end());
-    std::set<std::pair<double, double>> ss;
-    for (int i = 0; i < n; ++i) ss.insert({ds->hx[static_cast<size_t>(i)], ds->hy[static_cast<size_t>(i)]});
-    std::vector<double> times(ts.begin(), ts.end());
+    // the reference's std::set<double> / std::set<pair> (inducing.cpp:150-156): distinct values in
+    // ascending order, the first occurrence kept; hashed here (the sets cost ~0.3 s at n = 1.1M)
+    const std::vector<double> times = distinct_sorted_times(ds->ht);
+    const std::vector<std::pair<double, double>> ss = distinct_sorted_locations(ds->hx, ds->hy);
     std::vector<double> locs(2 * ss.size());
-    {
-      size_t i = 0;
-      for (const auto& p : ss) {
-        locs[i] = p.first;
-        locs[i + ss.size()] = p.second;
-        ++i;
-      }
+    for (size_t i = 0; i < ss.size(); ++i) {
+      locs[i] = ss[i].first;
+      locs[i + ss.size()] = ss[i].second;
     }
     const double nt = static_cast<double>(times.size());
     int m_s = static_cast<int>(std::lround(std::sqrt(static_cast<double>(m) * n / (nt * nt))));
