@@ -167,3 +167,20 @@ def test_dc_spatial_path_identical(S, monkeypatch):
     b = S.correlation_neighbors(ds, S.synth.THETA_T3, 30)
     assert (a.indices() == b.indices()).all()
     assert _bits(a.distances(), b.distances())
+
+
+def test_sts_signed_zero_and_duplicates(S):
+    # distinct locations / times follow std::set: -0.0 == +0.0 (first occurrence kept), duplicates merged
+    rng = np.random.default_rng(4)
+    x = rng.random(400)
+    y = rng.random(400)
+    x[::7] = 0.0
+    x[3::7] = -0.0
+    y[5::11] = -0.0
+    t = np.repeat(np.arange(1.0, 9.0), 50)
+    t[::13] = -0.0 + 0.0
+    ds = S.SpaceTimeDataset(x, y, t)
+    ind = S.sts_kmeanspp(ds, 40, 9)
+    Z, ms, mt = O.sts_kmeanspp(x, y, t, 40, 9)
+    assert (ind.m_s, ind.m_t) == (ms, mt)
+    assert _bits(ind.points, Z)
