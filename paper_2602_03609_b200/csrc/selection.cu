@@ -1058,10 +1058,11 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
     const DevKernel k = dev_kernel(p);
     // diagnostics (STGP_DR_STATS): host-side phase times
     const bool dbg = std::getenv("STGP_DR_STATS") != nullptr;
+    const bool host_laps = std::getenv("STGP_DR_HOSTLAPS") != nullptr;  // host-side time per phase, no sync
     auto clk0 = std::chrono::steady_clock::now();
     auto lap = [&](const char* what) {
-      if (!dbg) return;
-      STGP_CUDA(cudaStreamSynchronize(st));
+      if (!dbg && !host_laps) return;
+      if (dbg) STGP_CUDA(cudaStreamSynchronize(st));
       const auto now = std::chrono::steady_clock::now();
       std::fprintf(stderr, "[stgp] d_r phase %-12s %8.2f ms\n", what,
                    std::chrono::duration<double, std::milli>(now - clk0).count());
@@ -1102,13 +1103,18 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
     lap("alloc W");
     STGP_CUDA(cudaMemsetAsync(W.get(), 0, sizeof(double) * ldm * n, st));
     DevBuf<int32_t> degen(n);
+    // basis buffers live to the end of the search: freeing them here (cudaFree synchronizes the device)
+    // would hold the host until the whitening finishes instead of overlapping the tile set-up with it
+    DevBuf<double> A, L, Lp;
+    DevBuf<int> fail;
     {
       lap("setup+alloc");
       ProfRegion pr(ctx, "dr_whiten");
       if (M > 0) {
         // InducingBasis(set, selection kernel): jittered Sigma_m, one retry at 10x (inducing.cpp:250-261)
-        DevBuf<double> A(static_cast<size_t>(M) * M), L(static_cast<size_t>(M) * M);
-        DevBuf<int> fail(1);
+        A.alloc(static_cast<size_t>(M) * M);
+        L.alloc(static_cast<size_t>(M) * M);
+        fail.alloc(1);
         const double jitter = 1e-8 * p.sigma1_2;
         bool ok = false;
 
@@ -1136,7 +1142,7 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
         STGP_CUDA(cudaFuncSetAttribute(whiten_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(kWsmem)));
         const int ldL = (M + kWKC - 1) / kWKC * kWKC;
-        DevBuf<double> Lp(static_cast<size_t>(M) * ldL);
+        Lp.alloc(static_cast<size_t>(M) * ldL);
         ProfRegion prw(ctx, "dr_whiten_seq");
         pad_rows_kernel<<<grid_for(static_cast<long long>(M) * ldL), 256, 0, st>>>(L.get(), M, ldL, Lp.get());
         launched(ctx);
