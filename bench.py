@@ -411,6 +411,26 @@ def main():
                     "d2h_bytes_per_step": 64},
             "gpu_launches": launches, "roofline": roof, "clocks": clk.summary()}
     line.update(extra)
+    if args.workload == "vif":
+        # the metric's Vecchia half on the same data: d_c neighbours (m_v), NLL+grad evaluations
+        t0 = time.perf_counter()
+        nbc = S.correlation_neighbors(ds, theta, args.m_v)
+        vc_nn = time.perf_counter() - t0
+        sv = S.build_vecchia(ds, theta, nbc, S.OBSERVATION)
+        for i in range(args.warmup):
+            S.evaluate(sv, thetas[i])
+        D.barrier() if dist else None
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for i in range(args.steps):
+            vv, _ = S.evaluate(sv, thetas[args.warmup + i])
+        f1.record(stream)
+        torch.cuda.synchronize()
+        vms = D.max_over_ranks(f0.elapsed_time(f1) / args.steps)
+        line["vecchia"] = {"workload": "cfg4-vecchia-dc (same data)", "evals_per_s": 1e3 / vms, "ms_per_step": vms,
+                           "nn_search_s": vc_nn, "nll": vv}
+        del sv, nbc
     if args.workload == "fitc" and world == 1:
         # cfg5's second half: 1-day-ahead predictive mean / variance at every station
         last = t == t.max()

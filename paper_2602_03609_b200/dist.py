@@ -50,6 +50,12 @@ def sum_over_ranks(value: float) -> float:
     return float(t[0])
 
 
+def barrier():
+    import torch.distributed as tdist
+    if tdist.is_available() and tdist.is_initialized():
+        tdist.barrier()
+
+
 def setup_engine_comm(ctx, rank: int, world: int):
     """Rank 0 creates the NCCL unique id, every rank joins the communicator and takes its shard."""
     from .api import Context
