@@ -362,8 +362,8 @@ def main():
 
     if args.workload == "vif":
         kname = ("VIF row pass: vecchia_rows_kernel<build> (closure Gram by DMMA, Cholesky) + "
-                 "vif_grad_stored_kernel (Ga by DMMA, Phi_i, KG)")
-        k_avg = region_avg("rows") + region_avg("rows_vifgrad")
+                 "tile_ga_kernel (Ga over tile-staged closure columns) + vif_grad_stored_kernel (Phi_i, KG)")
+        k_avg = region_avg("rows") + region_avg("g_ga") + region_avg("rows_vifgrad")
         flops_launch = vif_rows_flops(counts[lo:hi], M)
         step_flops = vif_flops(counts, M)
     elif args.workload == "fitc":

@@ -352,6 +352,7 @@ RowArgs row_args(stgp_structure* s, const double* W, int ldw, double nugget) {
   a.Lfac_out = nullptr;
   a.Lfac_in = nullptr;
   a.A_in = nullptr;
+  a.Ga_in = nullptr;
   a.inv_c = 1.0 / s->th.c;
   host_grad00(s->th, a.g00);
   return a;

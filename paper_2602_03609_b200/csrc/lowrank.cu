@@ -825,10 +825,12 @@ void vif_build(stgp_structure* s) {
   L.Vp.ensure(total);
   if (re > rb) {
     ProfRegion pr(ctx, "vprime");
+    if (!tile_vprime(s, L.W.get(), s->A.get(), L.Vp.get())) {
     vprime_kernel<<<std::min(re - rb, ctx->num_sms * 16), 128, 0, ctx->stream>>>(
         L.W.get(), ldm, s->nbr.get(), s->m_v, s->A.get(), rb, re, s->order_gather ? s->rorder.get() : nullptr,
         claim_counter(ctx), L.Vp.get());
     launched(ctx);
+    }
   }
   ProfRegion prk(ctx, "K_gemm_chol");
   L.work1.ensure(total);
@@ -967,11 +969,16 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
     a.Lfac_in = L.Lfac.get();
     a.A_in = s->A.get();
   }
+  if (a.Lfac_in && re > rb) {  // Ga by the tiled SDDMM (falls back to the rows kernel's DMMA pass)
+    ProfRegion pg(ctx, "g_ga");
+    double* Ga = L.tmp("Ga", static_cast<size_t>(n) * 32);
+    if (tile_ga(s, L.W.get(), L.work1.get(), Ga)) a.Ga_in = Ga;
+  }
   std::vector<double> rows = run_rows_args(s, kModeVifGrad, a);
   // E (in place of X) and F (own rows)
   ph.reset(new ProfRegion(ctx, "g_ef"));
   L.work2.ensure(total);
-  if (re > rb) {
+  if (re > rb && !tile_ef(s, L.W.get(), Rv, c0, s->D.get(), L.Vp.get(), yhat, Bz, L.work1.get(), L.work2.get())) {
     ef_kernel<<<std::min(re - rb, ctx->num_sms * 16), 128, 0, st>>>(rb, re, ldm, s->m_v, s->nbr.get(), Rv, c0,
                                                                     s->D.get(), L.W.get(), L.Vp.get(), yhat, Bz,
                                                                     s->order_gather ? s->rorder.get() : nullptr, claim_counter(ctx), L.work1.get(), L.work2.get());

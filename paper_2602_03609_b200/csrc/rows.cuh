@@ -90,6 +90,7 @@ struct RowArgs {
   double* Lfac_out;
   const double* Lfac_in;
   const double* A_in;
+  const double* Ga_in;  // optional: Ga from the tiled SDDMM (tiles.cu tile_ga), n x 32, self at 31
 };
 
 template <int KS>
@@ -577,8 +578,12 @@ __global__ void __launch_bounds__(kRowWarps * 32) vif_grad_stored_kernel(RowArgs
     }
     scol[w][lane] = pt;
     __syncwarp();
-    const double* xi = a.X + static_cast<size_t>(i) * a.ldw;
-    closure_x_dmma(a.W, a.ldw, scol[w], xi, sGa[w], lane, a.zcol);
+    if (a.Ga_in) {
+      const double* gi = a.Ga_in + static_cast<size_t>(i) * 32;
+      sGa[w][lane] = lane < k ? __ldg(&gi[lane]) : (lane == KS ? __ldg(&gi[31]) : 0.0);
+    } else {
+      closure_x_dmma(a.W, a.ldw, scol[w], a.X + static_cast<size_t>(i) * a.ldw, sGa[w], lane, a.zcol);
+    }
     // stored factor: row `lane` of L into registers and shared memory
     const double* src = a.Lfac_in + static_cast<size_t>(i) * lfac_stride<KS>();
     double R[KS];

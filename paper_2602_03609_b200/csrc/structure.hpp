@@ -8,6 +8,7 @@
 
 #include "engine.hpp"
 #include "rows.cuh"
+#include "tiles.cuh"
 
 namespace stgp {
 
@@ -72,6 +73,9 @@ struct stgp_structure {
   // locality schedule (lowrank.cu: locality_order): rows [row_begin, row_end), columns [col_begin, row_end)
   stgp::DevBuf<int32_t> rorder, corder;
   bool order_rows = false, order_gather = false;
+  // tile-staged gathers (tiles.cu), built once per structure
+  bool tiles_built = false;
+  stgp::TileSets tiles;
 };
 
 namespace stgp {
