@@ -173,6 +173,15 @@ int stgp_debug_fp64_peak(stgp_ctx* ctx, double* tflops);
 int stgp_debug_dmma_peak(stgp_ctx* ctx, double* tflops);
 /* Names of the profiled regions recorded so far, newline separated (truncated to cap-1 bytes). */
 int stgp_ctx_profile_names(stgp_ctx* ctx, char* buf, int cap);
+/* FP64 product C[r][j] = sum_c A[r][c] B[j][c] (row-major host arrays, n x k, m x k -> n x m)
+ * through the int8 Ozaki path (emulated = 1) or cuBLAS DGEMM (emulated = 0); *ms = device time
+ * of the product (inputs resident). */
+int stgp_debug_gemm_rows(stgp_ctx* ctx, int emulated, long long n, int m, int k, const double* A_host,
+                         const double* B_host, double* C_host, double* ms);
+/* FP64 product C[j][i] = sum_r A[j + r m] B[i + r m] (column-major m x n host arrays -> m x m,
+ * row-major C) through the int8 Ozaki path (emulated = 1) or cuBLAS DGEMM (emulated = 0). */
+int stgp_debug_gemm_cols(stgp_ctx* ctx, int emulated, int m, long long n, const double* A_host,
+                         const double* B_host, double* C_host, double* ms);
 /* device Gneiting covariance / kernel gradient of (h, u) pairs with live factors */
 int stgp_debug_kernel(stgp_ctx* ctx, const stgp_params* theta, int n, const double* h_host,
                       const double* u_host, double* cov_out, double* grad6_out);

@@ -111,6 +111,28 @@ class Context:
         N.call("stgp_debug_dmma_peak", self.h, C.byref(out))
         return out.value
 
+    def gemm_rows(self, A, B, emulated: bool = True):
+        """C = A B^T (FP64) through the int8 Ozaki path or cuBLAS DGEMM; returns (C, device ms)."""
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        B = np.ascontiguousarray(B, dtype=np.float64)
+        n, k = A.shape
+        m = B.shape[0]
+        C_ = np.zeros((n, m))
+        ms = C.c_double(0.0)
+        N.call("stgp_debug_gemm_rows", self.h, int(emulated), n, m, k, _ptr(A), _ptr(B), _ptr(C_), C.byref(ms))
+        return C_, ms.value
+
+    def gemm_cols(self, A, B=None, emulated: bool = True):
+        """C = A^T B (A, B: n x m, i.e. m x n column-major), C[j][i] = sum_r A[r, j] B[r, i]; the
+        int8 Ozaki path for the long reduction or cuBLAS DGEMM.  B None: A^T A."""
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        n, m = A.shape
+        Bc = A if B is None else np.ascontiguousarray(B, dtype=np.float64)
+        C_ = np.zeros((m, m))
+        ms = C.c_double(0.0)
+        N.call("stgp_debug_gemm_cols", self.h, int(emulated), m, n, _ptr(A), _ptr(Bc), _ptr(C_), C.byref(ms))
+        return C_, ms.value
+
     def profile(self, enable: bool = True):
         N.call("stgp_ctx_profile", self.h, int(enable))
 

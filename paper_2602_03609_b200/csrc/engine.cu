@@ -11,7 +11,9 @@
 #include <set>
 
 #include "comm.hpp"
+#include "dense.cuh"
 #include "engine.hpp"
+#include "ozaki.cuh"
 #include "rows.cuh"
 #include "rows_serial.cuh"
 #include "search.cuh"
@@ -546,6 +548,7 @@ void stgp_ctx_destroy(stgp_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   stgp_ctx_release_comm(ctx);
+  stgp::ozaki_release(ctx);
   if (ctx->cublas) cublasDestroy(ctx->cublas);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -597,6 +600,71 @@ int stgp_ctx_profile_names(stgp_ctx* ctx, char* buf, int cap) {
     const size_t n = std::min(all.size(), static_cast<size_t>(cap - 1));
     std::memcpy(buf, all.data(), n);
     buf[n] = 0;
+  });
+}
+
+int stgp_debug_gemm_rows(stgp_ctx* ctx, int emulated, long long n, int m, int k, const double* A_host,
+                         const double* B_host, double* C_host, double* ms) {
+  return guarded([&] {
+    if (!ctx || n < 0 || m <= 0 || k <= 0 || !A_host || !B_host || !C_host) config_error("stgp_debug_gemm_rows: bad argument");
+    DevBuf<double> A, B, C(static_cast<size_t>(n) * m);
+    A.upload(A_host, static_cast<size_t>(n) * k, ctx->stream);
+    B.upload(B_host, static_cast<size_t>(m) * k, ctx->stream);
+    auto run = [&] {
+      if (emulated) {
+        ozaki_gemm_rows(ctx, n, m, k, A.get(), k, B.get(), k, C.get(), m);
+      } else {
+        dev_gemm(ctx, true, false, m, static_cast<int>(n), k, 1.0, B.get(), k, A.get(), k, 0.0, C.get(), m);
+      }
+    };
+    run();  // warm-up (plans, workspace)
+    cudaEvent_t e0, e1;
+    STGP_CUDA(cudaEventCreate(&e0));
+    STGP_CUDA(cudaEventCreate(&e1));
+    STGP_CUDA(cudaEventRecord(e0, ctx->stream));
+    run();
+    STGP_CUDA(cudaEventRecord(e1, ctx->stream));
+    STGP_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    STGP_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (ms) *ms = t;
+    C.download(C_host, static_cast<size_t>(n) * m, ctx->stream);
+    STGP_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int stgp_debug_gemm_cols(stgp_ctx* ctx, int emulated, int m, long long n, const double* A_host,
+                         const double* B_host, double* C_host, double* ms) {
+  return guarded([&] {
+    if (!ctx || m <= 0 || n <= 0 || !A_host || !B_host || !C_host) config_error("stgp_debug_gemm_cols: bad argument");
+    DevBuf<double> A, B, C(static_cast<size_t>(m) * m);
+    A.upload(A_host, static_cast<size_t>(m) * n, ctx->stream);
+    const bool same = A_host == B_host;
+    if (!same) B.upload(B_host, static_cast<size_t>(m) * n, ctx->stream);
+    const double* Bp = same ? A.get() : B.get();
+    auto run = [&] {
+      if (emulated)
+        ozaki_gemm_cols(ctx, m, n, A.get(), m, Bp, m, C.get(), m);
+      else  // C (column-major view: C(i, j) at j m + i) = B A^T
+        dev_gemm(ctx, false, true, m, m, n, 1.0, Bp, m, A.get(), m, 0.0, C.get(), m);
+    };
+    run();
+    cudaEvent_t e0, e1;
+    STGP_CUDA(cudaEventCreate(&e0));
+    STGP_CUDA(cudaEventCreate(&e1));
+    STGP_CUDA(cudaEventRecord(e0, ctx->stream));
+    run();
+    STGP_CUDA(cudaEventRecord(e1, ctx->stream));
+    STGP_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    STGP_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (ms) *ms = t;
+    C.download(C_host, static_cast<size_t>(m) * m, ctx->stream);
+    STGP_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

@@ -51,6 +51,7 @@ struct DevLagTable {
   std::vector<TF> host_tf;
 };
 
+struct OzakiState;  // ozaki.cu: int8 slice buffers and cuBLASLt plans
 }  // namespace stgp
 
 struct stgp_ctx {
@@ -67,6 +68,7 @@ struct stgp_ctx {
   stgp::DevBuf<double> dscr;
   stgp::DevBuf<double> sel_W;  // d_r search: whitened cross covariance, kept across searches (8 GB at cfg4)
   stgp::DevBuf<uint16_t> sel_W16;  // d_r search: its fp16 copy for the certified filter
+  stgp::OzakiState* ozaki = nullptr;  // FP64-on-int8 GEMM workspace (lazy)
   // live per-region kernel timing (stgp_ctx_profile)
   bool prof = false;
   std::map<std::string, std::pair<double, int64_t>> prof_acc;

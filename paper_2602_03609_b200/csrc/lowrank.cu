@@ -26,6 +26,7 @@
 #include "comm.hpp"
 #include "dense.cuh"
 #include "lowrank_common.cuh"
+#include "ozaki.cuh"
 #include "rows.cuh"
 #include "structure.hpp"
 #include "../../include/stgp_b200.h"
@@ -844,7 +845,10 @@ void vif_build(stgp_structure* s) {
       const char* e = std::getenv("STGP_KBLOCKS");
       return e ? std::max(1, std::atoi(e)) : 4;  // 5/8 of the GEMM flops; measured best at M = 906
     }();
-    dev_syrk_blocked(ctx, ldm, re - rb, 1.0, L.work1.get() + off, ldm, L.Mc.get(), ldm, kblocks);
+    if (ozaki_enabled())  // S S^T on the int8 tensor cores (exactly symmetric result)
+      ozaki_gemm_cols(ctx, ldm, re - rb, L.work1.get() + off, ldm, L.work1.get() + off, ldm, L.Mc.get(), ldm);
+    else
+      dev_syrk_blocked(ctx, ldm, re - rb, 1.0, L.work1.get() + off, ldm, L.Mc.get(), ldm, kblocks);
   }
   allreduce_sum(ctx, L.Mc.get(), static_cast<size_t>(ldm) * ldm);
   add_identity(ctx, L.Mc.get(), ldm);
@@ -950,9 +954,13 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
   dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, false);
   dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, true);
   L.work1.ensure(total);
-  if (re > rb)
-    dev_gemm(ctx, false, false, ldm, re - rb, ldm, 1.0, L.Kinv.get(), ldm, L.Vp.get() + own, ldm, 0.0,
-             L.work1.get() + own, ldm);
+  if (re > rb) {
+    if (ozaki_enabled())  // K^{-1} is symmetric: X_r = K^{-1} V'_r row by row on the int8 tensor cores
+      ozaki_gemm_rows(ctx, re - rb, ldm, ldm, L.Vp.get() + own, ldm, L.Kinv.get(), ldm, L.work1.get() + own, ldm);
+    else
+      dev_gemm(ctx, false, false, ldm, re - rb, ldm, 1.0, L.Kinv.get(), ldm, L.Vp.get() + own, ldm, 0.0,
+               L.work1.get() + own, ldm);
+  }
   // per-row Phi_i: direct pass + c0, Rv (own rows)
   ph.reset();
   RowArgs a = row_args(s, L.W.get(), ldm, s->th.sigma2);
@@ -986,7 +994,9 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
   }
   ph.reset(new ProfRegion(ctx, "g_S_gemm"));
   // W Phi W^T = sym(V' F^T) summed over shards -> wsig' = 0.5 yhat yhat^T + sym(V'F^T) + 0.5 (K^{-1} - I)
-  if (re > rb)
+  if (re > rb && ozaki_enabled())  // S(i, j) = sum_r V'(i, r) F(j, r)
+    ozaki_gemm_cols(ctx, ldm, re - rb, L.work2.get() + own, ldm, L.Vp.get() + own, ldm, S, ldm);
+  else if (re > rb)
     dev_gemm(ctx, false, true, ldm, ldm, re - rb, 1.0, L.Vp.get() + own, ldm, L.work2.get() + own, ldm, 0.0, S, ldm);
   else
     STGP_CUDA(cudaMemsetAsync(S, 0, sizeof(double) * mm, st));

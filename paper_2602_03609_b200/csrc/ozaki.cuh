@@ -1,0 +1,22 @@
+// FP64 GEMM emulated on the int8 tensor cores (ozaki.cu).
+#pragma once
+
+#include "common.cuh"
+
+struct stgp_ctx;
+
+namespace stgp {
+
+struct OzakiState;
+bool ozaki_enabled();
+int ozaki_slices();
+// C[r * ldc + j] = sum_{c < k} A[r * lda + c] * B[j * ldb + c]  for r < n, j < m (FP64 in and out)
+void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, int lda, const double* B, int ldb,
+                     double* C, int ldc);
+// C[j * ldc + i] = sum_{r < n} A[j + r * lda] * B[i + r * ldb]  for i, j < m: A B^T of two m x n
+// column-major matrices (the long reduction over n runs in exact int32 chunks)
+void ozaki_gemm_cols(stgp_ctx* ctx, int m, long long n, const double* A, int lda, const double* B, int ldb, double* C,
+                     int ldc);
+void ozaki_release(stgp_ctx* ctx);
+
+}  // namespace stgp

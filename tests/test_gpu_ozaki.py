@@ -1,0 +1,85 @@
+"""FP64 products on the int8 tensor cores (csrc/ozaki.cu) against exact references.
+
+The Ozaki slicing is error-free apart from the dropped low-order diagonals, so the error of each
+entry is bounded by ~2^-(7 S) * k * max|A_r| * max|B_j| (S = 7 slices by default).  The
+reference is math.fsum over the rounded products (error k 2^-53 max|a| max|b|, far inside the bound).
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2602_03609_b200 as S
+    return S.Context(0)
+
+
+def _exact(A, B):
+    out = np.empty((A.shape[0], B.shape[0]))
+    for r in range(A.shape[0]):
+        for j in range(B.shape[0]):
+            out[r, j] = math.fsum(A[r] * B[j])  # rounded products: error <= k 2^-53 max|a||b|, far inside the bound
+    return out
+
+
+@pytest.mark.parametrize("n,m,k", [(37, 24, 40), (300, 48, 912)])
+def test_ozaki_matches_exact_dot(ctx, n, m, k):
+    rng = np.random.default_rng(n + k)
+    # rows spanning many binades and signs, some zero rows
+    A = rng.standard_normal((n, k)) * np.exp2(rng.integers(-30, 30, size=(n, 1)))
+    B = rng.standard_normal((m, k)) * np.exp2(rng.integers(-20, 20, size=(m, 1)))
+    A[3] = 0.0
+    B[1, ::2] = 0.0
+    C, _ = ctx.gemm_rows(A, B, emulated=True)
+    ref = _exact(A[:40], B)
+    scale = np.abs(A[:40]).max(axis=1)[:, None] * np.abs(B).max(axis=1)[None, :] * k
+    err = np.abs(C[:40] - ref)
+    assert (err <= 2.0 ** -46 * scale).all(), (err / np.maximum(scale, 1e-300)).max()
+    assert (C[3] == 0.0).all()
+    D, _ = ctx.gemm_rows(A, B, emulated=False)
+    assert np.allclose(C, D, rtol=0, atol=2.0 ** -44 * np.abs(A).max(axis=1)[:, None] * np.abs(B).max(axis=1)[None, :] * k)
+
+
+def test_ozaki_cfg4_shape_timing(ctx):
+    # the X = K^{-1} V' shape of the VIF gradient (n x 912 rows against a 912 x 912 symmetric matrix)
+    rng = np.random.default_rng(1)
+    n, M = 200000, 912
+    A = rng.standard_normal((n, M))
+    B = rng.standard_normal((M, M))
+    B = B + B.T
+    C, ms_e = ctx.gemm_rows(A, B, emulated=True)
+    D, ms_d = ctx.gemm_rows(A, B, emulated=False)
+    scale = np.abs(A).max(axis=1)[:, None] * np.abs(B).max(axis=1)[None, :] * M
+    assert (np.abs(C - D) <= 2.0 ** -44 * scale).all()
+    print(f"ozaki {ms_e:.2f} ms vs DGEMM {ms_d:.2f} ms at n={n}")
+
+
+@pytest.mark.parametrize("n,m", [(1000, 40), (300001, 96)])
+def test_ozaki_long_reduction(ctx, n, m):
+    # C = A^T B over n rows in exact int32 chunks (the K = S S^T and V' F^T shapes), per-chunk scales
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((n, m)) * np.exp2(rng.integers(-8, 8, size=(n, 1)))
+    B = rng.standard_normal((n, m))
+    C, _ = ctx.gemm_cols(A, B)
+    ref = A.T @ B
+    # slicing error is relative to the per-chunk row maxima: <= ~2^-46 n max|A[:, j]| max|B[:, i]|
+    bound = 2.0 ** -44 * n * np.abs(A).max(axis=0)[:, None] * np.abs(B).max(axis=0)[None, :]
+    assert (np.abs(C - ref) <= bound).all(), (np.abs(C - ref) / bound).max()
+    G, _ = ctx.gemm_cols(A)  # A^T A: exactly symmetric
+    assert (G == G.T).all()
+    assert np.allclose(G, A.T @ A, rtol=0, atol=2.0 ** -44 * n * np.abs(A).max() ** 2)
+
+
+def test_ozaki_long_reduction_timing(ctx):
+    rng = np.random.default_rng(2)
+    n, m = 400000, 912
+    A = rng.standard_normal((n, m))
+    B = rng.standard_normal((n, m))
+    C, ms_e = ctx.gemm_cols(A, B)
+    D, ms_d = ctx.gemm_cols(A, B, emulated=False)
+    assert np.allclose(C, D, rtol=0, atol=2.0 ** -40 * n)
+    print(f"ozaki cols {ms_e:.2f} ms vs DGEMM {ms_d:.2f} ms at n={n}")
