@@ -9,6 +9,7 @@
 #include "comm.hpp"
 #include "dense.cuh"
 #include "lowrank_common.cuh"
+#include "ozaki.cuh"
 #include "structure.hpp"
 #include "../../include/stgp_b200.h"
 
@@ -134,8 +135,13 @@ void fitc_build(stgp_structure* s) {
   STGP_CUDA(cudaMemsetAsync(L.Mc.get(), 0, sizeof(double) * ldm * ldm, ctx->stream));
   ProfRegion prk(ctx, "K_gemm_chol");
   if (re > rb) {
-    scale_cols(ctx, L.W.get() + own, ldm, re - rb, L.lambda.get() + rb, true, L.work1.get() + own);
-    dev_syrk_blocked(ctx, ldm, re - rb, 1.0, L.work1.get() + own, ldm, L.Mc.get(), ldm, 4);
+    if (ozaki_enabled()) {  // W Lambda^{-1} W^T on the int8 tensor cores
+      ozaki_gemm_cols(ctx, ldm, re - rb, L.W.get() + own, ldm, L.W.get() + own, ldm, L.Mc.get(), ldm,
+                      L.lambda.get() + rb);
+    } else {
+      scale_cols(ctx, L.W.get() + own, ldm, re - rb, L.lambda.get() + rb, true, L.work1.get() + own);
+      dev_syrk_blocked(ctx, ldm, re - rb, 1.0, L.work1.get() + own, ldm, L.Mc.get(), ldm, 4);
+    }
   }
   allreduce_sum(ctx, L.Mc.get(), static_cast<size_t>(ldm) * ldm);
   add_identity(ctx, L.Mc.get(), ldm);
@@ -205,8 +211,11 @@ void fitc_nll_grad(stgp_structure* s, double* nll, double* grad) {
   dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, true);
   if (nown > 0) {
     ProfRegion pr(ctx, "f_KW_gemm");
-    dev_gemm(ctx, false, false, ldm, nown, ldm, 1.0, L.Kinv.get(), ldm, L.W.get() + own, ldm, 0.0, L.work1.get() + own,
-             ldm);
+    if (ozaki_enabled())  // K^{-1} symmetric: KW_i = K^{-1} W_i row by row
+      ozaki_gemm_rows(ctx, nown, ldm, ldm, L.W.get() + own, ldm, L.Kinv.get(), ldm, L.work1.get() + own, ldm);
+    else
+      dev_gemm(ctx, false, false, ldm, nown, ldm, 1.0, L.Kinv.get(), ldm, L.W.get() + own, ldm, 0.0,
+               L.work1.get() + own, ldm);
     col_dot_kernel<<<grid_for(static_cast<long long>(nown) * 32), 256, 0, st>>>(nown, ldm, L.W.get() + own,
                                                                                L.work1.get() + own, hsq + rb);
     launched(ctx);
@@ -217,7 +226,11 @@ void fitc_nll_grad(stgp_structure* s, double* nll, double* grad) {
     // S = W diag(phi) W^T (symmetric: lower blocks only)
     ProfRegion prs(ctx, "f_S_gemm");
     scale_cols(ctx, L.W.get() + own, ldm, nown, phi + rb, false, L.work2.get() + own);
-    dev_gemm_sym_blocked(ctx, ldm, nown, 1.0, L.W.get() + own, ldm, L.work2.get() + own, ldm, S, ldm, 4);
+    if (ozaki_enabled()) {  // S(i, j) = sum_r W(i, r) phi_r W(j, r); mirrored lower triangle
+      ozaki_gemm_cols(ctx, ldm, nown, L.work2.get() + own, ldm, L.W.get() + own, ldm, S, ldm);
+      dev_symmetrize_lower(ctx, S, ldm, ldm);
+    } else
+      dev_gemm_sym_blocked(ctx, ldm, nown, 1.0, L.W.get() + own, ldm, L.work2.get() + own, ldm, S, ldm, 4);
     Reducer rr;
     phisum[0] = dev_sum(ctx, phi + rb, nown, rr);
   }

@@ -836,7 +836,7 @@ void vif_build(stgp_structure* s) {
   ProfRegion prk(ctx, "K_gemm_chol");
   L.work1.ensure(total);
   const size_t off = static_cast<size_t>(rb) * ldm;
-  scale_cols(ctx, L.Vp.get() + off, ldm, re - rb, s->D.get() + rb, true, L.work1.get() + off);
+  if (!ozaki_enabled()) scale_cols(ctx, L.Vp.get() + off, ldm, re - rb, s->D.get() + rb, true, L.work1.get() + off);
   L.Mc.ensure(static_cast<size_t>(ldm) * ldm);
   STGP_CUDA(cudaMemsetAsync(L.Mc.get(), 0, sizeof(double) * ldm * ldm, ctx->stream));
   // S S^T as GEMMs over the lower blocks of a partition (dense.cu dev_syrk_blocked)
@@ -846,7 +846,7 @@ void vif_build(stgp_structure* s) {
       return e ? std::max(1, std::atoi(e)) : 4;  // 5/8 of the GEMM flops; measured best at M = 906
     }();
     if (ozaki_enabled())  // S S^T on the int8 tensor cores (exactly symmetric result)
-      ozaki_gemm_cols(ctx, ldm, re - rb, L.work1.get() + off, ldm, L.work1.get() + off, ldm, L.Mc.get(), ldm);
+      ozaki_gemm_cols(ctx, ldm, re - rb, L.Vp.get() + off, ldm, L.Vp.get() + off, ldm, L.Mc.get(), ldm, s->D.get() + rb);
     else
       dev_syrk_blocked(ctx, ldm, re - rb, 1.0, L.work1.get() + off, ldm, L.Mc.get(), ldm, kblocks);
   }

@@ -77,15 +77,17 @@ __global__ void __launch_bounds__(256) slice_rows_kernel(long long nrows, int k,
   }
 }
 
-// Column form: A is m x n column-major (lda); the product runs over n in chunks of L.  Row j of
+// Column form: A is m x n column-major (lda), optionally with column r divided by sqrt(colD[r]);
+// the product runs over n in chunks of L.  Row j of
 // chunk c is scaled by scale[c * m + j] = 2^e (> max over the chunk) and sliced into
 // out[((c * m + j) * S + s - 1) * L + rl] and/or out_rev[((c * m + j) * S + S - s) * L + rl],
 // through a shared-memory transpose of 32 rows x 128 columns so that both the loads and the int8
 // stores are coalesced.
 constexpr int kSlTileR = 128;
 __global__ void __launch_bounds__(256) slice_cols_kernel(int m, long long n, int L, const double* __restrict__ A,
-                                                         int lda, int S, int8_t* __restrict__ out,
-                                                         int8_t* __restrict__ out_rev, double* __restrict__ scale) {
+                                                         int lda, const double* __restrict__ colD, int S,
+                                                         int8_t* __restrict__ out, int8_t* __restrict__ out_rev,
+                                                         double* __restrict__ scale) {
   __shared__ double T[32][kSlTileR + 1];
   __shared__ double red[8][32];
   __shared__ double sinv[32];
@@ -93,9 +95,16 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(int m, long long n, int
   const long long r0 = static_cast<long long>(c) * L, r1 = min(n, r0 + L);
   const int jj = threadIdx.x & 31, rr = threadIdx.x >> 5;
   const int j = j0 + jj;
+  // column r of A enters as A(:, r) / sqrt(colD[r]) when colD is given (V' D^{-1/2} of the K product)
+  auto val = [&](long long r) {
+    const double a = A[r * lda + j];
+    return colD ? a * __ldg(&colD[r]) : a;  // colD holds the factors 1 / sqrt(D_r) (rsqrt_vec_kernel)
+  };
   double mx = 0.0;
-  if (j < m)
-    for (long long r = r0 + rr; r < r1; r += 8) mx = fmax(mx, fabs(A[r * lda + j]));
+  if (j < m) {
+#pragma unroll 4
+    for (long long r = r0 + rr; r < r1; r += 8) mx = fmax(mx, fabs(val(r)));
+  }
   red[rr][jj] = mx;
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -111,7 +120,7 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(int m, long long n, int
   for (long long t0 = r0; t0 < r0 + L; t0 += kSlTileR) {
     for (int q = rr; q < kSlTileR; q += 8) {
       const long long r = t0 + q;
-      T[jj][q] = (j < m && r < r1) ? A[r * lda + j] * sinv[jj] : 0.0;
+      T[jj][q] = (j < m && r < r1) ? val(r) * sinv[jj] : 0.0;
     }
     __syncthreads();
     if (j0 + wj < m) {
@@ -137,7 +146,8 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(int m, long long n, int
   }
 }
 
-// C[r * ldc + j] = sA[r] sB[j] sum_{d = S+1 .. 2} 2^-7d Cd[d][r * mp + j]   (one row per iteration)
+// C[r * ldc + j] = sA[r] sB[j] sum_{d = S+1 .. 2} 2^-7d Cd[d][r * mp + j]   (one row per iteration,
+// 4 consecutive j per thread: m, mp and ldc are multiples of 4, rows 16-byte aligned)
 __global__ void __launch_bounds__(256) combine_rows_kernel(long long nrows, int m, int mp, const int32_t* __restrict__ Cd,
                                                            long long dstride, int S, const double* __restrict__ sA,
                                                            const double* __restrict__ sB, double* __restrict__ C,
@@ -145,21 +155,33 @@ __global__ void __launch_bounds__(256) combine_rows_kernel(long long nrows, int 
   for (long long r = blockIdx.x; r < nrows; r += gridDim.x) {
     const double fa = sA[r];
     const int32_t* src = Cd + r * mp;
-    for (int j = threadIdx.x; j < m; j += blockDim.x) {
-      int32_t v[12];
+    for (int j = threadIdx.x * 4; j < m; j += blockDim.x * 4) {
+      int4 v[12];
 #pragma unroll
       for (int d = 0; d < 12; ++d)
-        if (d < S) v[d] = __ldg(&src[d * dstride + j]);
-      double acc = 0.0, w = ldexp(1.0, -7 * (S + 1));  // weight of the smallest diagonal
+        if (d < S) v[d] = __ldg(reinterpret_cast<const int4*>(src + d * dstride + j));
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, w = ldexp(1.0, -7 * (S + 1));  // smallest diagonal first
 #pragma unroll
       for (int d = 11; d >= 0; --d)
-        if (d < S) {
-          acc = fma(static_cast<double>(v[d]), w, acc);  // exact product (power of two), one rounding per add
+        if (d < S) {  // exact products (power-of-two weights), one rounding per add
+          a0 = fma(static_cast<double>(v[d].x), w, a0);
+          a1 = fma(static_cast<double>(v[d].y), w, a1);
+          a2 = fma(static_cast<double>(v[d].z), w, a2);
+          a3 = fma(static_cast<double>(v[d].w), w, a3);
           w *= 128.0;
         }
-      C[r * ldc + j] = acc * fa * sB[j];
+      double* o = C + r * ldc + j;
+      const double4 fb = *reinterpret_cast<const double4*>(sB + j);
+      *reinterpret_cast<double2*>(o) = make_double2(a0 * fa * fb.x, a1 * fa * fb.y);
+      *reinterpret_cast<double2*>(o + 2) = make_double2(a2 * fa * fb.z, a3 * fa * fb.w);
     }
   }
+}
+
+__global__ void rsqrt_vec_kernel(long long n, const double* __restrict__ d, double* __restrict__ f) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    f[i] = 1.0 / sqrt(d[i]);  // the factor of lowrank.cu scale_cols_kernel
 }
 
 // C[j * ldc + i] = sum_c sA[c m + j] sB[c m + i] sum_d 2^-7d Cd[d][c][j * mp + i]   (chunks in order)
@@ -205,7 +227,7 @@ struct OzakiState {
   DevBuf<unsigned char> ws;
   DevBuf<int8_t> As, Bs;
   DevBuf<int32_t> Cd;
-  DevBuf<double> sA, sB;
+  DevBuf<double> sA, sB, colf;
   std::map<std::tuple<int, int, long long, int, int, int>, std::unique_ptr<LtPlan>> plans;
   ~OzakiState() {
     plans.clear();
@@ -297,6 +319,7 @@ static void lt_matmul(stgp_ctx* ctx, OzakiState* oz, LtPlan* p, const int8_t* a,
 void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, int lda, const double* B, int ldb,
                      double* C, int ldc) {
   if (n <= 0 || m <= 0) return;
+  if (m % 4 || ldc % 4) config_error("ozaki_gemm_rows: m and ldc must be multiples of 4");
   const int S = ozaki_slices();
   const int kp = (k + 15) / 16 * 16;  // slice stride: every diagonal segment 16-byte aligned
   if (static_cast<long long>(S) * kp * 127 * 127 >= (1LL << 31)) config_error("ozaki: k too large for exact int32");
@@ -310,7 +333,7 @@ void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, 
   slice_rows_kernel<<<grid_for(static_cast<long long>(m) * 32, 256), 256, 0, st>>>(m, k, kp, B, ldb, S, true,
                                                                                  oz->Bs.get(), ldk, oz->sB.get());
   launched(ctx);
-  const long long chunk = std::min<long long>(n, 262144);
+  const long long chunk = std::min<long long>(n, std::max<long long>(16384, (1LL << 28) / mp));  // Cd ~ S GB
   oz->As.ensure(static_cast<size_t>(chunk) * ldk);
   oz->sA.ensure(static_cast<size_t>(chunk));
   const long long dstride = chunk * mp;
@@ -332,7 +355,7 @@ void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, 
 }
 
 void ozaki_gemm_cols(stgp_ctx* ctx, int m, long long n, const double* A, int lda, const double* B, int ldb, double* C,
-                     int ldc) {
+                     int ldc, const double* colD) {
   if (m <= 0) return;
   const int S = ozaki_slices();
   OzakiState* oz = state(ctx);
@@ -348,14 +371,20 @@ void ozaki_gemm_cols(stgp_ctx* ctx, int m, long long n, const double* A, int lda
   oz->As.ensure(sl);
   oz->sA.ensure(static_cast<size_t>(nch) * m);
   const bool same = A == B && lda == ldb;  // A A^T: one pass writes both slice orders
+  if (colD) {
+    oz->colf.ensure(static_cast<size_t>(n));
+    rsqrt_vec_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, colD, oz->colf.get());
+    launched(ctx);
+    colD = oz->colf.get();
+  }
   oz->Bs.ensure(sl);
   oz->sB.ensure(static_cast<size_t>(nch) * m);
   const dim3 grid(nch, (m + 31) / 32);
-  slice_cols_kernel<<<grid, 256, 0, st>>>(m, n, L, A, lda, S, oz->As.get(), same ? oz->Bs.get() : nullptr,
+  slice_cols_kernel<<<grid, 256, 0, st>>>(m, n, L, A, lda, colD, S, oz->As.get(), same ? oz->Bs.get() : nullptr,
                                           oz->sA.get());
   launched(ctx);
   if (!same) {
-    slice_cols_kernel<<<grid, 256, 0, st>>>(m, n, L, B, ldb, S, nullptr, oz->Bs.get(), oz->sB.get());
+    slice_cols_kernel<<<grid, 256, 0, st>>>(m, n, L, B, ldb, colD, S, nullptr, oz->Bs.get(), oz->sB.get());
     launched(ctx);
   }
   const double* sB = same ? oz->sA.get() : oz->sB.get();

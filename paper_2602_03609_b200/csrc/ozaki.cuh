@@ -10,13 +10,15 @@ namespace stgp {
 struct OzakiState;
 bool ozaki_enabled();
 int ozaki_slices();
-// C[r * ldc + j] = sum_{c < k} A[r * lda + c] * B[j * ldb + c]  for r < n, j < m (FP64 in and out)
+// C[r * ldc + j] = sum_{c < k} A[r * lda + c] * B[j * ldb + c]  for r < n, j < m (FP64 in and out;
+// m and ldc multiples of 4)
 void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, int lda, const double* B, int ldb,
                      double* C, int ldc);
-// C[j * ldc + i] = sum_{r < n} A[j + r * lda] * B[i + r * ldb]  for i, j < m: A B^T of two m x n
-// column-major matrices (the long reduction over n runs in exact int32 chunks)
+// C[j * ldc + i] = sum_{r < n} A[j + r * lda] * B[i + r * ldb] / colD[r]  for i, j < m: A B^T of two
+// m x n column-major matrices, each column scaled by colD[r]^{-1/2} when colD is given (the long
+// reduction over n runs in exact int32 chunks)
 void ozaki_gemm_cols(stgp_ctx* ctx, int m, long long n, const double* A, int lda, const double* B, int ldb, double* C,
-                     int ldc);
+                     int ldc, const double* colD = nullptr);
 void ozaki_release(stgp_ctx* ctx);
 
 }  // namespace stgp
