@@ -34,10 +34,35 @@ void lt_check(cublasStatus_t s, const char* what) {
     throw Error(kInternal, std::string("cuBLASLt error in ") + what + ": " + std::to_string(static_cast<int>(s)));
 }
 
+// The S base-128 digits of trunc(v 2^(7 S)) for |v| < 1 (v already scaled, exact): all digits carry
+// the sign of v and lie in [-127, 127]; digit 1 is the most significant.  Same digits as the FP64
+// recurrence w = 128 v, t = trunc(w), v = w - t, at one FP64 multiply, one conversion and 32-bit
+// funnel shifts (S is a compile-time constant).
+struct Fixed {
+  unsigned lo, hi;
+  int sg;  // 0 or -1
+};
+template <int S>
+__device__ __forceinline__ Fixed fixed_point(double v) {
+  const long long q = __double2ll_rz(v * static_cast<double>(1LL << (7 * S)));  // exact scaling, truncation
+  const unsigned long long a = q < 0 ? static_cast<unsigned long long>(-q) : static_cast<unsigned long long>(q);
+  return Fixed{static_cast<unsigned>(a), static_cast<unsigned>(a >> 32), q < 0 ? -1 : 0};
+}
+template <int S>
+__device__ __forceinline__ int digit(const Fixed& f, int s) {
+  const int sh = 7 * (S - s);
+  const unsigned d = (sh >= 32 ? (f.hi >> (sh - 32)) : __funnelshift_r(f.lo, f.hi, sh)) & 127u;
+  return (static_cast<int>(d) ^ f.sg) - f.sg;
+}
+__device__ __forceinline__ unsigned pack4(int a, int b, int c, int d) {
+  return (a & 0xff) | ((b & 0xff) << 8) | ((c & 0xff) << 16) | (static_cast<unsigned>(d & 0xff) << 24);
+}
+
 // One warp per row: exponent of the row maximum (scale[r] = 2^e > max |row|), then the S slices
 // (char4 stores).  reverse: slice t stored at (S - t) kp (B operand), else at (t - 1) kp.
+template <int S>
 __global__ void __launch_bounds__(256) slice_rows_kernel(long long nrows, int k, int kp, const double* __restrict__ A,
-                                                         int lda, int S, bool reverse, int8_t* __restrict__ out,
+                                                         int lda, bool reverse, int8_t* __restrict__ out,
                                                          long long ldo, double* __restrict__ scale) {
   const int lane = threadIdx.x & 31;
   const long long warp = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
@@ -54,97 +79,117 @@ __global__ void __launch_bounds__(256) slice_rows_kernel(long long nrows, int k,
     const double inv = ldexp(1.0, -e);
     int8_t* o = out + r * ldo;
     for (int c4 = lane * 4; c4 < kp; c4 += 128) {  // kp: k padded to 16 (zero slices)
-      double v[4];
+      Fixed q[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = c4 + u < k ? a[c4 + u] * inv : 0.0;  // exact: power-of-two scale
-      for (int s = 1; s <= S; ++s) {
-        char4 q;
-        signed char qq[4];
+      for (int u = 0; u < 4; ++u) q[u] = fixed_point<S>(c4 + u < k ? a[c4 + u] * inv : 0.0);  // exact scale
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double w = v[u] * 128.0;  // exact
-          const double t = trunc(w);      // |t| <= 127
-          v[u] = w - t;                   // exact remainder in (-1, 1)
-          qq[u] = static_cast<signed char>(t);
-        }
-        q.x = qq[0];
-        q.y = qq[1];
-        q.z = qq[2];
-        q.w = qq[3];
-        *reinterpret_cast<char4*>(o + (reverse ? (S - s) : (s - 1)) * kp + c4) = q;
-      }
+      for (int s = 1; s <= S; ++s)
+        *reinterpret_cast<unsigned*>(o + (reverse ? (S - s) : (s - 1)) * kp + c4) =
+            pack4(digit<S>(q[0], s), digit<S>(q[1], s), digit<S>(q[2], s), digit<S>(q[3], s));
     }
   }
 }
 
-// Column form: A is m x n column-major (lda), optionally with column r divided by sqrt(colD[r]);
-// the product runs over n in chunks of L.  Row j of
-// chunk c is scaled by scale[c * m + j] = 2^e (> max over the chunk) and sliced into
-// out[((c * m + j) * S + s - 1) * L + rl] and/or out_rev[((c * m + j) * S + S - s) * L + rl],
-// through a shared-memory transpose of 32 rows x 128 columns so that both the loads and the int8
-// stores are coalesced.
-constexpr int kSlTileR = 128;
-__global__ void __launch_bounds__(256) slice_cols_kernel(int m, long long n, int L, const double* __restrict__ A,
-                                                         int lda, const double* __restrict__ colD, int S,
-                                                         int8_t* __restrict__ out, int8_t* __restrict__ out_rev,
-                                                         double* __restrict__ scale) {
-  __shared__ double T[32][kSlTileR + 1];
-  __shared__ double red[8][32];
-  __shared__ double sinv[32];
-  const int c = blockIdx.x, j0 = blockIdx.y * 32;
-  const long long r0 = static_cast<long long>(c) * L, r1 = min(n, r0 + L);
-  const int jj = threadIdx.x & 31, rr = threadIdx.x >> 5;
-  const int j = j0 + jj;
-  // column r of A enters as A(:, r) / sqrt(colD[r]) when colD is given (V' D^{-1/2} of the K product)
-  auto val = [&](long long r) {
-    const double a = A[r * lda + j];
-    return colD ? a * __ldg(&colD[r]) : a;  // colD holds the factors 1 / sqrt(D_r) (rsqrt_vec_kernel)
-  };
+// Column form (A m x n column-major, lda; column r optionally multiplied by colD[r]); the product
+// runs over n in chunks of L.  A block covers 32 rows j (lanes: every load is a 256-byte row
+// segment) and 8 x 32 columns r (warps); each thread keeps its 32 values of one row in registers.
+constexpr int kSlCols = 256;  // columns r per block; L is a multiple
+
+// per-(chunk, row) maxima: atomicMax on the bit patterns of non-negative doubles (order-preserving)
+__global__ void __launch_bounds__(256) colmax_kernel(int m, long long n, int L, const double* __restrict__ A, int lda,
+                                                     const double* __restrict__ colD,
+                                                     unsigned long long* __restrict__ maxbits) {
+  const long long rb = static_cast<long long>(blockIdx.x) * kSlCols + (threadIdx.x >> 5) * 32;
+  const int j = blockIdx.y * 32 + (threadIdx.x & 31);
+  const int c = static_cast<int>((static_cast<long long>(blockIdx.x) * kSlCols) / L);
   double mx = 0.0;
   if (j < m) {
-#pragma unroll 4
-    for (long long r = r0 + rr; r < r1; r += 8) mx = fmax(mx, fabs(val(r)));
-  }
-  red[rr][jj] = mx;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double v = 0.0;
-    for (int q = 0; q < 8; ++q) v = fmax(v, red[q][threadIdx.x]);
-    int e = 0;
-    if (v > 0.0) frexp(v, &e);
-    sinv[threadIdx.x] = ldexp(1.0, -e);
-    if (j0 + threadIdx.x < m) scale[static_cast<size_t>(c) * m + j0 + threadIdx.x] = ldexp(1.0, e);
-  }
-  __syncthreads();
-  const int wj = threadIdx.x >> 3, wr = (threadIdx.x & 7) * 16;  // slicing: row wj, 16 columns
-  for (long long t0 = r0; t0 < r0 + L; t0 += kSlTileR) {
-    for (int q = rr; q < kSlTileR; q += 8) {
-      const long long r = t0 + q;
-      T[jj][q] = (j < m && r < r1) ? val(r) * sinv[jj] : 0.0;
-    }
-    __syncthreads();
-    if (j0 + wj < m) {
-      double v[16];
-#pragma unroll
-      for (int u = 0; u < 16; ++u) v[u] = T[wj][wr + u];
-      const size_t base = (static_cast<size_t>(c) * m + j0 + wj) * S * static_cast<size_t>(L) + (t0 - r0) + wr;
-      for (int s = 1; s <= S; ++s) {
-        alignas(16) signed char qq[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const double w = v[u] * 128.0;
-          const double tq = trunc(w);
-          v[u] = w - tq;
-          qq[u] = static_cast<signed char>(tq);
-        }
-        const int4 q = *reinterpret_cast<const int4*>(qq);
-        if (out) *reinterpret_cast<int4*>(out + base + static_cast<size_t>(s - 1) * L) = q;
-        if (out_rev) *reinterpret_cast<int4*>(out_rev + base + static_cast<size_t>(S - s) * L) = q;
+#pragma unroll 8
+    for (int u = 0; u < 32; ++u) {
+      const long long r = rb + u;
+      if (r < n) {
+        const double a = A[r * lda + j];
+        mx = fmax(mx, fabs(colD ? a * __ldg(&colD[r]) : a));
       }
     }
-    __syncthreads();
+  }
+  if (j < m && mx > 0.0) atomicMax(&maxbits[static_cast<size_t>(c) * m + j], __double_as_longlong(mx));
+}
+
+// Row j of chunk c is scaled by scale[c * m + j] = 2^e (> the chunk maximum) and sliced into
+// out[((c * m + j) * S + s - 1) * L + rl] and/or out_rev[((c * m + j) * S + S - s) * L + rl].  The
+// digits of the block's 32 rows x 256 columns are staged in shared memory and leave as 256-byte
+// row runs (full sectors, no partial-sector write-backs).
+constexpr int kSlRow = kSlCols + 16;  // staged row pitch (bytes): spreads the 16-byte stores over banks
+template <int S>
+__global__ void __launch_bounds__(256) slice_cols_kernel(int m, long long n, int L, const double* __restrict__ A,
+                                                         int lda, const double* __restrict__ colD,
+                                                         const unsigned long long* __restrict__ maxbits,
+                                                         int8_t* __restrict__ out, int8_t* __restrict__ out_rev,
+                                                         double* __restrict__ scale) {
+  extern __shared__ __align__(16) unsigned char sd[];  // S * 32 * kSlRow bytes
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long rc0 = static_cast<long long>(blockIdx.x) * kSlCols;
+  const long long rb = rc0 + w * 32;
+  const int j0 = blockIdx.y * 32, j = j0 + lane;
+  const int c = static_cast<int>(rc0 / L);
+  double inv = 0.0;
+  if (j < m) {
+    const double mx = __longlong_as_double(static_cast<long long>(maxbits[static_cast<size_t>(c) * m + j]));
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
+    if (rc0 % L == 0 && w == 0) scale[static_cast<size_t>(c) * m + j] = ldexp(1.0, e);
+    inv = ldexp(1.0, -e);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    Fixed q[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const long long r = rb + 16 * h + u;
+      double v = 0.0;
+      if (j < m && r < n) {
+        const double a = A[r * lda + j];
+        v = (colD ? a * __ldg(&colD[r]) : a) * inv;  // exact power-of-two scale
+      }
+      q[u] = fixed_point<S>(v);
+    }
+#pragma unroll
+    for (int s = 1; s <= S; ++s) {
+      uint4 v4;
+      v4.x = pack4(digit<S>(q[0], s), digit<S>(q[1], s), digit<S>(q[2], s), digit<S>(q[3], s));
+      v4.y = pack4(digit<S>(q[4], s), digit<S>(q[5], s), digit<S>(q[6], s), digit<S>(q[7], s));
+      v4.z = pack4(digit<S>(q[8], s), digit<S>(q[9], s), digit<S>(q[10], s), digit<S>(q[11], s));
+      v4.w = pack4(digit<S>(q[12], s), digit<S>(q[13], s), digit<S>(q[14], s), digit<S>(q[15], s));
+      *reinterpret_cast<uint4*>(sd + ((s - 1) * 32 + lane) * kSlRow + w * 32 + 16 * h) = v4;
+    }
+  }
+  __syncthreads();
+  // copy-out: 16 threads per (slice, row) run of 256 bytes
+  const size_t off = static_cast<size_t>(rc0 - static_cast<long long>(c) * L);
+  for (int e = threadIdx.x; e < S * 32 * 16; e += blockDim.x) {
+    const int row = e >> 4, piece = e & 15;
+    const int s = row / 32 + 1, jj = row - (s - 1) * 32;
+    if (j0 + jj >= m) continue;
+    const uint4 v4 = *reinterpret_cast<const uint4*>(sd + row * kSlRow + piece * 16);
+    const size_t base = (static_cast<size_t>(c) * m + j0 + jj) * S * static_cast<size_t>(L) + off + piece * 16;
+    if (out) *reinterpret_cast<uint4*>(out + base + static_cast<size_t>(s - 1) * L) = v4;
+    if (out_rev) *reinterpret_cast<uint4*>(out_rev + base + static_cast<size_t>(S - s) * L) = v4;
   }
 }
+
+// dispatch on the slice count (compile-time shifts)
+#define STGP_OZ_SWITCH(S_, CALL)                                                  \
+  switch (S_) {                                                                   \
+    case 2: { constexpr int kS = 2; CALL; } break;                                \
+    case 3: { constexpr int kS = 3; CALL; } break;                                \
+    case 4: { constexpr int kS = 4; CALL; } break;                                \
+    case 5: { constexpr int kS = 5; CALL; } break;                                \
+    case 6: { constexpr int kS = 6; CALL; } break;                                \
+    case 7: { constexpr int kS = 7; CALL; } break;                                \
+    case 8: { constexpr int kS = 8; CALL; } break;                                \
+    default: throw Error(kConfig, "ozaki: STGP_OZAKI_S must lie in [2, 8]");   \
+  }
 
 // C[r * ldc + j] = sA[r] sB[j] sum_{d = S+1 .. 2} 2^-7d Cd[d][r * mp + j]   (one row per iteration,
 // 4 consecutive j per thread: m, mp and ldc are multiples of 4, rows 16-byte aligned)
@@ -208,10 +253,14 @@ __global__ void __launch_bounds__(256) combine_cols_kernel(int m, int mp, int nc
   }
 }
 
+constexpr int kAlgoCands = 4;
 struct LtPlan {
   cublasLtMatmulDesc_t op = nullptr;
   cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
   cublasLtMatmulAlgo_t algo{};
+  cublasLtMatmulAlgo_t cand[kAlgoCands];
+  int ncand = 0;
+  bool tuned = false;  // heuristic candidates timed once on the first call (results are identical: exact int32)
   ~LtPlan() {
     if (la) cublasLtMatrixLayoutDestroy(la);
     if (lb) cublasLtMatrixLayoutDestroy(lb);
@@ -228,6 +277,7 @@ struct OzakiState {
   DevBuf<int8_t> As, Bs;
   DevBuf<int32_t> Cd;
   DevBuf<double> sA, sB, colf;
+  DevBuf<unsigned long long> maxbits;
   std::map<std::tuple<int, int, long long, int, int, int>, std::unique_ptr<LtPlan>> plans;
   ~OzakiState() {
     plans.clear();
@@ -243,7 +293,7 @@ void ozaki_release(stgp_ctx* ctx) {
 int ozaki_slices() {
   static const int s = [] {
     const char* e = std::getenv("STGP_OZAKI_S");
-    return std::max(2, std::min(12, e ? std::atoi(e) : 7));
+    return std::max(2, std::min(8, e ? std::atoi(e) : 7));
   }();
   return s;
 }
@@ -296,13 +346,15 @@ static LtPlan* plan_for(OzakiState* oz, int m, int mp, int K, long long ncols, i
   const size_t wsz = oz->ws.n;
   lt_check(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsz, sizeof(wsz)),
            "pref ws");
-  cublasLtMatmulHeuristicResult_t res{};
+  cublasLtMatmulHeuristicResult_t res[kAlgoCands];
   int found = 0;
-  lt_check(cublasLtMatmulAlgoGetHeuristic(oz->lt, p->op, p->la, p->lb, p->lc, p->lc, pref, 1, &res, &found),
+  lt_check(cublasLtMatmulAlgoGetHeuristic(oz->lt, p->op, p->la, p->lb, p->lc, p->lc, pref, kAlgoCands, res, &found),
            "heuristic");
   cublasLtMatmulPreferenceDestroy(pref);
   if (found < 1) throw Error(kInternal, "cuBLASLt: no int8 IMMA algorithm for the Ozaki slices");
-  p->algo = res.algo;
+  p->ncand = found;
+  for (int i = 0; i < found; ++i) p->cand[i] = res[i].algo;
+  p->algo = res[0].algo;
   LtPlan* raw = p.get();
   oz->plans[key] = std::move(p);
   return raw;
@@ -310,6 +362,34 @@ static LtPlan* plan_for(OzakiState* oz, int m, int mp, int K, long long ncols, i
 
 static void lt_matmul(stgp_ctx* ctx, OzakiState* oz, LtPlan* p, const int8_t* a, const int8_t* b, int32_t* c) {
   const int32_t one = 1, zero = 0;
+  if (!p->tuned) {
+    p->tuned = true;
+    if (p->ncand > 1) {
+      cudaEvent_t e0, e1;
+      STGP_CUDA(cudaEventCreate(&e0));
+      STGP_CUDA(cudaEventCreate(&e1));
+      float best = 1e30f;
+      for (int i = 0; i < p->ncand; ++i) {
+        if (cublasLtMatmul(oz->lt, p->op, &one, a, p->la, b, p->lb, &zero, c, p->lc, c, p->lc, &p->cand[i], oz->ws.get(),
+                           oz->ws.n, ctx->stream) != CUBLAS_STATUS_SUCCESS)
+          continue;  // untimed first run of each candidate
+        STGP_CUDA(cudaEventRecord(e0, ctx->stream));
+        if (cublasLtMatmul(oz->lt, p->op, &one, a, p->la, b, p->lb, &zero, c, p->lc, c, p->lc, &p->cand[i], oz->ws.get(),
+                           oz->ws.n, ctx->stream) != CUBLAS_STATUS_SUCCESS)
+          continue;
+        STGP_CUDA(cudaEventRecord(e1, ctx->stream));
+        STGP_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        STGP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        if (ms < best) {
+          best = ms;
+          p->algo = p->cand[i];
+        }
+      }
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+  }
   lt_check(cublasLtMatmul(oz->lt, p->op, &one, a, p->la, b, p->lb, &zero, c, p->lc, c, p->lc, &p->algo, oz->ws.get(),
                           oz->ws.n, ctx->stream),
            "matmul");
@@ -330,8 +410,8 @@ void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, 
   // B slices (m rows, reversed slice order) and scales
   oz->Bs.ensure(static_cast<size_t>(m) * ldk);
   oz->sB.ensure(m);
-  slice_rows_kernel<<<grid_for(static_cast<long long>(m) * 32, 256), 256, 0, st>>>(m, k, kp, B, ldb, S, true,
-                                                                                 oz->Bs.get(), ldk, oz->sB.get());
+  STGP_OZ_SWITCH(S, (slice_rows_kernel<kS><<<grid_for(static_cast<long long>(m) * 32, 256), 256, 0, st>>>(
+                         m, k, kp, B, ldb, true, oz->Bs.get(), ldk, oz->sB.get())));
   launched(ctx);
   const long long chunk = std::min<long long>(n, std::max<long long>(16384, (1LL << 28) / mp));  // Cd ~ S GB
   oz->As.ensure(static_cast<size_t>(chunk) * ldk);
@@ -340,8 +420,8 @@ void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, 
   oz->Cd.ensure(static_cast<size_t>(S) * dstride);
   for (long long r0 = 0; r0 < n; r0 += chunk) {
     const long long nr = std::min(chunk, n - r0);
-    slice_rows_kernel<<<grid_for(nr * 32, 256), 256, 0, st>>>(nr, k, kp, A + r0 * lda, lda, S, false, oz->As.get(),
-                                                              ldk, oz->sA.get());
+    STGP_OZ_SWITCH(S, (slice_rows_kernel<kS><<<grid_for(nr * 32, 256), 256, 0, st>>>(
+                           nr, k, kp, A + r0 * lda, lda, false, oz->As.get(), ldk, oz->sA.get())));
     launched(ctx);
     for (int d = 2; d <= S + 1; ++d) {
       LtPlan* p = plan_for(oz, m, mp, (d - 1) * kp, nr, ldk);
@@ -362,7 +442,7 @@ void ozaki_gemm_cols(stgp_ctx* ctx, int m, long long n, const double* A, int lda
   cudaStream_t st = ctx->stream;
   // chunk of the reduction: exact int32 for the longest diagonal, (S) L 127^2 < 2^31
   const long long lmax = ((1LL << 31) - 1) / (static_cast<long long>(S) * 127 * 127);
-  const int L = static_cast<int>(std::min<long long>(lmax / kSlTileR * kSlTileR, (n + kSlTileR - 1) / kSlTileR * kSlTileR));
+  const int L = static_cast<int>(std::min<long long>(lmax / kSlCols * kSlCols, (n + kSlCols - 1) / kSlCols * kSlCols));
   const int nch = static_cast<int>((n + L - 1) / L);
   const int mp = (m + 3) / 4 * 4;
   const long long ldk = static_cast<long long>(S) * L;
@@ -379,14 +459,23 @@ void ozaki_gemm_cols(stgp_ctx* ctx, int m, long long n, const double* A, int lda
   }
   oz->Bs.ensure(sl);
   oz->sB.ensure(static_cast<size_t>(nch) * m);
-  const dim3 grid(nch, (m + 31) / 32);
-  slice_cols_kernel<<<grid, 256, 0, st>>>(m, n, L, A, lda, colD, S, oz->As.get(), same ? oz->Bs.get() : nullptr,
-                                          oz->sA.get());
-  launched(ctx);
-  if (!same) {
-    slice_cols_kernel<<<grid, 256, 0, st>>>(m, n, L, B, ldb, colD, S, nullptr, oz->Bs.get(), oz->sB.get());
+  const dim3 grid(static_cast<unsigned>((n + kSlCols - 1) / kSlCols), (m + 31) / 32);
+  oz->maxbits.ensure(static_cast<size_t>(nch) * m);
+  auto slice = [&](const double* X, int ldx, int8_t* fwd, int8_t* rev, double* sc) {
+    STGP_CUDA(cudaMemsetAsync(oz->maxbits.get(), 0, sizeof(unsigned long long) * nch * m, st));
+    colmax_kernel<<<grid, 256, 0, st>>>(m, n, L, X, ldx, colD, oz->maxbits.get());
     launched(ctx);
-  }
+    STGP_OZ_SWITCH(S, ({
+                     const int smem = kS * 32 * kSlRow;
+                     STGP_CUDA(cudaFuncSetAttribute(slice_cols_kernel<kS>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                     slice_cols_kernel<kS><<<grid, 256, smem, st>>>(m, n, L, X, ldx, colD, oz->maxbits.get(), fwd,
+                                                                     rev, sc);
+                   }));
+    launched(ctx);
+  };
+  slice(A, lda, oz->As.get(), same ? oz->Bs.get() : nullptr, oz->sA.get());
+  if (!same) slice(B, ldb, nullptr, oz->Bs.get(), oz->sB.get());
   const double* sB = same ? oz->sA.get() : oz->sB.get();
   const long long cstride = static_cast<long long>(m) * mp;
   const long long dstride = nch * cstride;
