@@ -394,6 +394,20 @@ def main():
             "step_canonical_flop": step_flops, "step_tflops": step_flops / (ms_step * 1e-3) / 1e12,
             "step_frac": step_flops / (ms_step * 1e-3) / 1e12 / fp64_peak,
             "phase_ms": breakdown}
+    # the FP64 products that run on the int8 tensor cores (Ozaki slicing, csrc/ozaki.cu): X = K^-1 V'
+    # (FITC: K^-1 W), K = S S^T and V'F^T (FITC: W diag(phi) W^T), each S(S+1)/2 int8 MACs per FP64 FMA
+    # per evaluation: the region total over the evaluations profiled (timed steps and e2e steps alike)
+    oz_ms = prof.get("oz_imma", (0.0, 0))[0] / max(prof.get("K_gemm_chol", (0.0, 1))[1], 1)
+    if args.workload in ("vif", "fitc") and oz_ms > 0:
+        sl = int(os.environ.get("STGP_OZAKI_S", "7"))
+        ldm = (M + 15) // 16 * 16
+        int8_ops = 3 * 2.0 * sl * (sl + 1) / 2 * ldm * ldm * (hi - lo)
+        int8_peak = 2.0 * peaks().get("bf16_tflops", 1669.7)
+        roof["int8_tensor"] = {
+            "bound": "tensor", "achieved": int8_ops / (oz_ms * 1e-3) / 1e12, "peak": int8_peak, "unit": "TOPS",
+            "frac": int8_ops / (oz_ms * 1e-3) / 1e12 / int8_peak, "kernel_ms": oz_ms, "ops_per_step": int8_ops,
+            "kernel": "cuBLASLt IMMA (tcgen05 kind::i8, cutlass3x_sm100 i256x256) over the Ozaki slices",
+            "peak_source": "2 x measured dense bf16 (MEASURED_PEAKS.json burst; B200 int8:bf16 dense = 2:1)"}
     line = {"metric": METRIC, "value": 1e3 / ms_step, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",

@@ -362,6 +362,7 @@ static LtPlan* plan_for(OzakiState* oz, int m, int mp, int K, long long ncols, i
 
 static void lt_matmul(stgp_ctx* ctx, OzakiState* oz, LtPlan* p, const int8_t* a, const int8_t* b, int32_t* c) {
   const int32_t one = 1, zero = 0;
+  ProfRegion pr(ctx, "oz_imma");  // int8 tensor-core time (bench.py roofline_int8)
   if (!p->tuned) {
     p->tuned = true;
     if (p->ncand > 1) {
