@@ -54,8 +54,8 @@ __device__ __forceinline__ int digit(const Fixed& f, int s) {
   const unsigned d = (sh >= 32 ? (f.hi >> (sh - 32)) : __funnelshift_r(f.lo, f.hi, sh)) & 127u;
   return (static_cast<int>(d) ^ f.sg) - f.sg;
 }
-__device__ __forceinline__ unsigned pack4(int a, int b, int c, int d) {
-  return (a & 0xff) | ((b & 0xff) << 8) | ((c & 0xff) << 16) | (static_cast<unsigned>(d & 0xff) << 24);
+__device__ __forceinline__ unsigned pack4(int a, int b, int c, int d) {  // low bytes of a, b, c, d
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
 
 // One warp per row: exponent of the row maximum (scale[r] = 2^e > max |row|), then the S slices
