@@ -164,6 +164,37 @@ int stgp_eval(stgp_structure* s, const stgp_params* theta, const double* y_host,
               const double* X_host, int p, const double* beta, double* nll_out,
               double* grad_out);
 
+/* ---- fit driver (estimation.hpp:23-56, estimation.cpp:423-619; Gaussian likelihood) ---- */
+/* FitConfig::Method */
+#define STGP_FIT_VECCHIA_EUCLID 0
+#define STGP_FIT_VECCHIA_CORR 1
+#define STGP_FIT_FITC_KMEANSPP 2
+#define STGP_FIT_FITC_STS 3
+#define STGP_FIT_VIF 4
+typedef struct {
+  int method, m_v, m, max_iterations;
+  double tol_objective, tol_gradient, nu;
+  uint64_t seed;
+} stgp_fit_config;
+/* TraceRow (estimation.hpp:61-66) */
+typedef struct {
+  int iteration;
+  double nll, grad_norm;
+  int refresh;
+} stgp_trace_row;
+/* default_init (estimation.cpp:68-114) on an ordered dataset with host response y (n) and
+ * covariates X (n x p column-major). */
+int stgp_default_init(const stgp_dataset* ds, const double* y_host, const double* X_host, int p,
+                      const stgp_fit_config* config, stgp_params* out);
+/* fit (estimation.cpp:423-619), Gaussian path: L-BFGS in the transformed coordinates with selection
+ * refresh at power-of-two iterations, NumericError step halving and GLS beta profiling (p > 0).
+ * ds is the ordered dataset (FittedModel.data: order it with stgp_order_observations(config.seed)).
+ * init may be NULL (default_init).  Up to trace_cap rows of the trace are copied; *n_trace gets
+ * the full count. */
+int stgp_fit(stgp_dataset* ds, const double* y_host, const double* X_host, int p, const stgp_fit_config* config,
+             const stgp_params* init, stgp_params* theta_out, double* beta_out, double* final_nll,
+             int* converged, stgp_trace_row* trace_out, int trace_cap, int* n_trace);
+
 /* ---- diagnostics ---- */
 /* device exp port on n inputs (KAT against the host libm) */
 int stgp_debug_exp(stgp_ctx* ctx, int n, const double* x_host, double* out);

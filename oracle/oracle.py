@@ -7,6 +7,7 @@ timed CPU baseline -- never the product path.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 
@@ -316,3 +317,171 @@ def full_conditioning(n: int) -> np.ndarray:
     for i in range(1, n):
         nb[i, :i] = np.arange(i)
     return nb
+
+
+# ---------------------------------------------------------------------------
+# fit (estimation.cpp:121-263, 423-619), Gaussian likelihood: the checker of the device fit driver.
+# Data are the ordered arrays (FittedModel.data).  Objective values and gradients come from the
+# oracle structures above; the selection is rebuilt with the oracle searches.
+# ---------------------------------------------------------------------------
+_BOUNDARY_EPS = 1e-6
+
+
+def _sigmoid(z):
+    if z >= 0.0:
+        return 1.0 / (1.0 + math.exp(-z))
+    e = math.exp(z)
+    return e / (1.0 + e)
+
+
+def _to_z(th):  # estimation.cpp:126-147
+    s2, s1, a, c, al, nu, be, de = th
+    lg = lambda p: math.log(p / (1.0 - p))  # noqa: E731
+    return np.array([math.log(max(s2, 1e-12)), math.log(s1), math.log(a), math.log(c),
+                     lg(min(max(al, _BOUNDARY_EPS), 1 - _BOUNDARY_EPS)), lg(min(max(be, _BOUNDARY_EPS), 1 - _BOUNDARY_EPS)),
+                     math.log(max(de, 1e-8))])
+
+
+def _theta_of(z, nu):  # estimation.cpp:149-159
+    return (math.exp(z[0]), math.exp(z[1]), math.exp(z[2]), math.exp(z[3]),
+            min(max(_sigmoid(z[4]), _BOUNDARY_EPS), 1.0), nu, min(max(_sigmoid(z[5]), 0.0), 1.0), math.exp(z[6]))
+
+
+def _dtheta_dz(z):  # estimation.cpp:167-188
+    sa, sb = _sigmoid(z[4]), _sigmoid(z[5])
+    return np.array([math.exp(z[0]), math.exp(z[1]), math.exp(z[2]), math.exp(z[3]), sa * (1 - sa), sb * (1 - sb),
+                     math.exp(z[6])])
+
+
+class _Lbfgs:  # estimation.cpp:234-263
+    def __init__(self):
+        self.pairs = []
+
+    def reset(self):
+        self.pairs = []
+
+    def push(self, s, y):
+        if s.dot(y) > 1e-12 * np.linalg.norm(s) * np.linalg.norm(y):
+            self.pairs.append((s, y))
+            if len(self.pairs) > 10:
+                self.pairs.pop(0)
+
+    def direction(self, g):
+        q = -g.copy()
+        if not self.pairs:
+            return q
+        al = [0.0] * len(self.pairs)
+        for i in range(len(self.pairs) - 1, -1, -1):
+            s, y = self.pairs[i]
+            al[i] = (1.0 / s.dot(y)) * s.dot(q)
+            q = q - al[i] * y
+        s, y = self.pairs[-1]
+        q = q * (s.dot(y) / y.dot(y))
+        for i, (s, y) in enumerate(self.pairs):
+            bc = (1.0 / s.dot(y)) * y.dot(q)
+            q = q + (al[i] - bc) * s
+        return q
+
+
+def _selection(x, y, t, method, m_v, m, seed, th):  # estimation.cpp:197-231
+    tr, sr = effective_ranges(th)
+    ss = sr if math.isfinite(sr) and sr > 0 else 1.0
+    ts = tr if math.isfinite(tr) and tr > 0 else 1e6
+    if method == "vecchia-euclid":
+        return "vecchia", euclid_neighbors(x, y, t, m_v, ss, ts), None
+    if method == "vecchia-corr":
+        return "vecchia", dc_neighbors(x, y, t, th, m_v), None
+    if method == "fitc-kmeanspp":
+        return "fitc", None, joint_kmeanspp(x, y, t, m, ss, ts, seed)
+    if method == "fitc-sts":
+        return "fitc", None, sts_kmeanspp(x, y, t, m, seed)[0]
+    Z = sts_kmeanspp(x, y, t, m, seed)[0]
+    return "vif", dr_neighbors(x, y, t, th, Z, m_v), Z
+
+
+def fit_gaussian(x, y, t, yv, X, method, m_v, m, seed, nu, init, max_iterations=200, tol_objective=1e-8,
+                 tol_gradient=1e-5):
+    """estimation.cpp:423-619 (Gaussian path) on ordered data; returns (theta, beta, f, converged, trace)."""
+    n = len(x)
+    p = 0 if X is None else np.asarray(X).reshape(n, -1).shape[1]
+    X = None if p == 0 else np.asarray(X, dtype=np.float64).reshape(n, p)
+    th0 = tuple(init)
+    th0 = th0[:5] + (nu,) + th0[6:]
+    z = _to_z(th0)
+    beta = np.linalg.solve(X.T @ X, X.T @ yv) if p else None
+    sel = None
+
+    def model(zz):
+        kind, nbr, Z = sel
+        return OracleModel(kind, x, y, t, _theta_of(zz, nu), nbr=nbr, Z=Z)
+
+    def value(zz):
+        return model(zz).nll(yv, X, beta)
+
+    def grad(zz):
+        return model(zz).nll_grad(yv, X, beta) * _dtheta_dz(zz)
+
+    lb = _Lbfgs()
+    f, g = float("nan"), None
+    have, done, conv, term = False, False, False, 0
+    trace = []
+    for it in range(1, max_iterations + 1):
+        if done:
+            break
+        refreshed = False
+        sched = (it & (it - 1)) == 0
+        if sched or not have:
+            sel = _selection(x, y, t, method, m_v, m, seed, _theta_of(z, nu))
+            refreshed = sched
+            fn = value(z)
+            if have and abs(fn - f) > tol_objective * max(1.0, abs(f)):
+                lb.reset()
+            f = fn
+            g = grad(z)
+            have = True
+        if p:
+            beta = model(z).gls_beta(yv, X)
+            f = value(z)
+            g = grad(z)
+        gn = float(np.abs(g).max())
+        trace.append((it, f, gn, refreshed))
+        if gn < tol_gradient and len(trace) >= 2 and abs(trace[-2][1] - f) < tol_objective * max(1.0, abs(f)):
+            rs = _selection(x, y, t, method, m_v, m, seed, _theta_of(z, nu))
+            old, sel = sel, rs
+            fr = value(z)
+            if abs(fr - f) <= tol_objective * max(1.0, abs(f)) or term >= 3:
+                f = fr
+                trace.append((it, f, gn, True))
+                conv, done = True, True
+                break
+            f = fr
+            g = grad(z)
+            lb.reset()
+            term += 1
+            trace.append((it, f, gn, True))
+            continue
+        d = lb.direction(g)
+        if d.dot(g) >= 0.0:
+            d = -g
+        step, slope, acc = 1.0, g.dot(d), False
+        for _ in range(40):
+            zn = z + step * d
+            try:
+                ft = value(zn)
+            except OracleError as e:
+                if e.code != 4:
+                    raise
+                step *= 0.5
+                continue
+            if math.isfinite(ft) and ft <= f + 1e-4 * step * slope:
+                fnew, acc = ft, True
+                break
+            step *= 0.5
+        if not acc:
+            if gn < tol_gradient * 10.0:
+                conv = True
+            break
+        gnew = grad(zn)
+        lb.push(zn - z, gnew - g)
+        z, f, g = zn, fnew, gnew
+    return _theta_of(z, nu), beta, f, conv, trace

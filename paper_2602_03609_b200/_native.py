@@ -79,6 +79,9 @@ _SIGS = {
     "stgp_debug_exp": [_P, C.c_int, _P, _P],
     "stgp_debug_fp64_peak": [_P, _D],
     "stgp_debug_dmma_peak": [_P, _D],
+    "stgp_default_init": [_P, _P, _P, C.c_int, _P, C.POINTER(Params)],
+    "stgp_fit": [_P, _P, _P, C.c_int, _P, _P, C.POINTER(Params), _P, _D, C.POINTER(C.c_int), _P, C.c_int,
+                 C.POINTER(C.c_int)],
     "stgp_debug_gemm_rows": [_P, C.c_int, C.c_longlong, C.c_int, C.c_int, _P, _P, _P, _D],
     "stgp_debug_gemm_cols": [_P, C.c_int, C.c_int, C.c_longlong, _P, _P, _P, _D],
     "stgp_ctx_profile_names": [_P, C.c_char_p, C.c_int],

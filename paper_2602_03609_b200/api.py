@@ -484,3 +484,69 @@ def debug_kernel(theta, h, u, ctx: Context | None = None):
     p = as_params(theta).c_struct()
     N.call("stgp_debug_kernel", ctx.h, C.byref(p), len(h), _ptr(h), _ptr(u), _ptr(cov), _ptr(g))
     return cov, g
+
+
+# ---------------------------------------------------------------------------
+# fit driver (estimation.hpp:23-110, estimation.cpp:423-619; Gaussian likelihood)
+# ---------------------------------------------------------------------------
+FIT_METHODS = {"vecchia-euclid": 0, "vecchia-corr": 1, "fitc-kmeanspp": 2, "fitc-sts": 3, "vif": 4}
+
+
+class FitConfig(C.Structure):
+    """FitConfig (estimation.hpp:23-56): method, m_v, m, max_iterations, tolerances, nu, seed."""
+    _fields_ = [("method", C.c_int), ("m_v", C.c_int), ("m", C.c_int), ("max_iterations", C.c_int),
+                ("tol_objective", C.c_double), ("tol_gradient", C.c_double), ("nu", C.c_double),
+                ("seed", C.c_uint64)]
+
+    def __init__(self, method="vecchia-corr", m_v=30, m=500, max_iterations=200, tol_objective=1e-8,
+                 tol_gradient=1e-5, nu=1.5, seed=0):
+        super().__init__(FIT_METHODS[method] if isinstance(method, str) else int(method), m_v, m, max_iterations,
+                         tol_objective, tol_gradient, nu, seed)
+
+
+class TraceRow(C.Structure):
+    _fields_ = [("iteration", C.c_int), ("nll", C.c_double), ("grad_norm", C.c_double), ("refresh", C.c_int)]
+
+
+@dataclass
+class FittedModel:
+    """FittedModel (estimation.hpp:68-83): parameters, coefficients, the ordered data and the trace."""
+    theta: CovarianceParams
+    beta: np.ndarray
+    final_nll: float
+    converged: bool
+    trace: list
+    data: "SpaceTimeDataset"
+
+
+def default_init(ds: "SpaceTimeDataset", config: FitConfig, y=None, X=None) -> CovarianceParams:
+    """default_init (estimation.cpp:68-114) on an ordered dataset."""
+    yv = _f64(ds.resp if y is None else y)
+    Xv = ds.X if X is None else np.asfortranarray(np.asarray(X, dtype=np.float64).reshape(ds.n, -1))
+    p = 0 if Xv is None else Xv.shape[1]
+    out = N.Params()
+    N.call("stgp_default_init", ds.h, _ptr(yv), _ptr(Xv) if p else None, p, C.byref(config), C.byref(out))
+    return CovarianceParams(*[getattr(out, f) for f, _ in N.Params._fields_])
+
+
+def fit(x, y, t, resp, X=None, config: FitConfig | None = None, init=None, ctx: Context | None = None,
+        trace_cap: int = 4096) -> FittedModel:
+    """fit (estimation.cpp:423-619): orders the observations with config.seed (FittedModel.data),
+    then maximises the Gaussian likelihood on the device."""
+    config = config or FitConfig()
+    ds = order_observations(x, y, t, resp, X, seed=config.seed, ctx=ctx)
+    yv = ds.resp
+    p = ds.p
+    theta = N.Params()
+    beta = np.zeros(max(p, 1))
+    fnll = C.c_double(0.0)
+    conv = C.c_int(0)
+    ntr = C.c_int(0)
+    rows = (TraceRow * trace_cap)()
+    init_p = as_params(init).c_struct() if init is not None else None
+    N.call("stgp_fit", ds.h, _ptr(yv), _ptr(ds.X) if p else None, p, C.byref(config),
+           C.byref(init_p) if init_p is not None else None, C.byref(theta), _ptr(beta), C.byref(fnll), C.byref(conv),
+           C.cast(rows, C.c_void_p), trace_cap, C.byref(ntr))
+    trace = [(r.iteration, r.nll, r.grad_norm, bool(r.refresh)) for r in rows[:min(ntr.value, trace_cap)]]
+    th = CovarianceParams(*[getattr(theta, f) for f, _ in N.Params._fields_])
+    return FittedModel(th, beta[:p].copy(), fnll.value, bool(conv.value), trace, ds)

@@ -122,6 +122,35 @@ void vecchia_predict(stgp_structure* s, int n_p, const double* txyt, int pred_m_
 void gls_beta_device(stgp_structure* s, const double* y_host, const double* X_host, int p, double* beta_out);
 }  // namespace stgp
 
+namespace stgp {
+double lowrank_nll(stgp_structure* s);
+// Objective value at theta: rebuild + NLL (the fit driver's line search, estimation.cpp:358-379)
+double eval_value(stgp_structure* s, const Params& th, const double* y, const double* X, int p, const double* beta) {
+  s->th = th;
+  compute_residual(s, y, X, p, beta);
+  if (s->kind == STGP_VECCHIA) {
+    vecchia_build(s);
+    return vecchia_nll(s);
+  }
+  if (s->kind == STGP_FITC) fitc_build(s);
+  else vif_build(s);
+  return lowrank_nll(s);
+}
+// Value and gradient at theta: one rebuild + the fused NLL and gradient
+void eval_both(stgp_structure* s, const Params& th, const double* y, const double* X, int p, const double* beta,
+               double* nll, double* grad) {
+  s->th = th;
+  compute_residual(s, y, X, p, beta);
+  if (s->kind == STGP_VECCHIA) {
+    vecchia_nll_grad(s, nll, grad);
+  } else {
+    if (s->kind == STGP_FITC) fitc_build(s);
+    else vif_build(s);
+    lowrank_nll_grad(s, nll, grad);
+  }
+}
+}  // namespace stgp
+
 extern "C" {
 
 int stgp_build_vecchia(stgp_dataset* ds, const stgp_params* theta, const stgp_neighbors* nb, int policy,
