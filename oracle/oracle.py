@@ -342,9 +342,19 @@ def _to_z(th):  # estimation.cpp:126-147
                      math.log(max(de, 1e-8))])
 
 
-def _theta_of(z, nu):  # estimation.cpp:149-159
-    return (math.exp(z[0]), math.exp(z[1]), math.exp(z[2]), math.exp(z[3]),
-            min(max(_sigmoid(z[4]), _BOUNDARY_EPS), 1.0), nu, min(max(_sigmoid(z[5]), 0.0), 1.0), math.exp(z[6]))
+def _exp(v):
+    return math.exp(v) if v < 709.78 else math.inf
+
+
+def _theta_of(z, nu):  # estimation.cpp:149-159; CovarianceParams::validate (covariance.cpp:34-46)
+    th = (_exp(z[0]), _exp(z[1]), _exp(z[2]), _exp(z[3]),
+          min(max(_sigmoid(z[4]), _BOUNDARY_EPS), 1.0), nu, min(max(_sigmoid(z[5]), 0.0), 1.0), _exp(z[6]))
+    s2, s1, a, c, al, _, be, de = th
+    ok = (0 <= s2 < math.inf and 0 < s1 < math.inf and 0 < a < math.inf and 0 < c < math.inf and 0 < al <= 1
+          and 0 <= be <= 1 and 0 <= de < math.inf)
+    if not ok:
+        raise OracleError(2, "CovarianceParams: parameter out of range")
+    return th
 
 
 def _dtheta_dz(z):  # estimation.cpp:167-188

@@ -11,7 +11,10 @@
 // iterations; a selection refresh replaces them.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <deque>
 #include <limits>
 #include <memory>
@@ -60,6 +63,19 @@ vec to_z(const Params& t) {
           logit(std::clamp(t.beta, kBoundaryEps, 1.0 - kBoundaryEps)),
           std::log(std::max(t.delta, 1e-8))};
 }
+// CovarianceParams::validate (covariance.cpp:34-46): the reference's theta_of constructs a
+// CovarianceParams, so a non-finite step raises ConfigError (not caught by the line search).
+void validate_theta(const Params& t) {
+  auto fail = [](const char* what) { config_error(std::string("CovarianceParams: ") + what); };
+  if (!(t.sigma2 >= 0.0) || !std::isfinite(t.sigma2)) fail("sigma2 must be >= 0");
+  if (!(t.sigma1_2 > 0.0) || !std::isfinite(t.sigma1_2)) fail("sigma1_2 must be > 0");
+  if (!(t.a > 0.0) || !std::isfinite(t.a)) fail("a must be > 0");
+  if (!(t.c > 0.0) || !std::isfinite(t.c)) fail("c must be > 0");
+  if (!(t.alpha > 0.0 && t.alpha <= 1.0)) fail("alpha must be in (0, 1]");
+  if (!(t.nu > 0.0) || !std::isfinite(t.nu)) fail("nu must be > 0");
+  if (!(t.beta >= 0.0 && t.beta <= 1.0)) fail("beta must be in [0, 1]");
+  if (!(t.delta >= 0.0) || !std::isfinite(t.delta)) fail("delta must be >= 0");
+}
 Params theta_of(const vec& z, double nu) {  // estimation.cpp:149-159
   Params t;
   t.sigma2 = std::exp(z[0]);
@@ -70,6 +86,7 @@ Params theta_of(const vec& z, double nu) {  // estimation.cpp:149-159
   t.nu = nu;
   t.beta = std::clamp(sigmoid(z[5]), 0.0, 1.0);
   t.delta = std::exp(z[6]);
+  validate_theta(t);
   return t;
 }
 vec dtheta_dz(const vec& z) {  // estimation.cpp:167-188
@@ -329,13 +346,25 @@ int stgp_fit(stgp_dataset* ds, const double* y, const double* X, int p, const st
     theta0.nu = cfg.nu;  // nu is fixed per fit
     vec z = to_z(theta0);
     vec beta = p > 0 ? ols(X, y, ds->n, p) : vec();
+    static const bool verbose = std::getenv("STGP_FIT_VERBOSE") != nullptr;  // per-evaluation log (stderr)
+    auto log_eval = [&](const char* what, const vec& zz, double f) {
+      if (!verbose) return;
+      const Params t = theta_of(zz, cfg.nu);
+      std::fprintf(stderr, "[fit] %s f=%.12g theta=(%g %g %g %g %g %g %g)\n", what, f, t.sigma2, t.sigma1_2, t.a, t.c,
+                   t.alpha, t.beta, t.delta);
+    };
     auto value = [&](stgp_structure* s, const vec& zz) {
-      return eval_value(s, theta_of(zz, cfg.nu), y, X, p, p > 0 ? beta.data() : nullptr);
+      log_eval("value?", zz, std::nan(""));
+      const double f = eval_value(s, theta_of(zz, cfg.nu), y, X, p, p > 0 ? beta.data() : nullptr);
+      log_eval("value", zz, f);
+      return f;
     };
     auto value_grad = [&](stgp_structure* s, const vec& zz, vec& g) {
       double f = 0.0;
       vec gt(7);
+      log_eval("grad?", zz, std::nan(""));
       eval_both(s, theta_of(zz, cfg.nu), y, X, p, p > 0 ? beta.data() : nullptr, &f, gt.data());
+      log_eval("grad", zz, f);
       const vec d = dtheta_dz(zz);
       g.assign(7, 0.0);
       for (int k = 0; k < 7; ++k) g[k] = gt[k] * d[k];
@@ -352,6 +381,7 @@ int stgp_fit(stgp_dataset* ds, const double* y, const double* X, int p, const st
     for (int iter = 1; iter <= cfg.max_iterations && !done; ++iter) {
       bool refreshed = false;
       if (refresh(iter) || !have_eval) {
+        if (verbose) std::fprintf(stderr, "[fit] iteration %d: selection refresh\n", iter);
         sel = build_selection(ds, cfg, theta_of(z, cfg.nu));
         refreshed = refresh(iter);
         vec gn;

@@ -126,6 +126,7 @@ namespace stgp {
 double lowrank_nll(stgp_structure* s);
 // Objective value at theta: rebuild + NLL (the fit driver's line search, estimation.cpp:358-379)
 double eval_value(stgp_structure* s, const Params& th, const double* y, const double* X, int p, const double* beta) {
+  validate_params(th);
   s->th = th;
   compute_residual(s, y, X, p, beta);
   if (s->kind == STGP_VECCHIA) {
@@ -139,6 +140,7 @@ double eval_value(stgp_structure* s, const Params& th, const double* y, const do
 // Value and gradient at theta: one rebuild + the fused NLL and gradient
 void eval_both(stgp_structure* s, const Params& th, const double* y, const double* X, int p, const double* beta,
                double* nll, double* grad) {
+  validate_params(th);
   s->th = th;
   compute_residual(s, y, X, p, beta);
   if (s->kind == STGP_VECCHIA) {
