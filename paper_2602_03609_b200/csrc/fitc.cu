@@ -135,7 +135,7 @@ void fitc_build(stgp_structure* s) {
   STGP_CUDA(cudaMemsetAsync(L.Mc.get(), 0, sizeof(double) * ldm * ldm, ctx->stream));
   ProfRegion prk(ctx, "K_gemm_chol");
   if (re > rb) {
-    if (ozaki_enabled()) {  // W Lambda^{-1} W^T on the int8 tensor cores
+    if (ozaki_for(ldm)) {  // W Lambda^{-1} W^T on the int8 tensor cores
       ozaki_gemm_cols(ctx, ldm, re - rb, L.W.get() + own, ldm, L.W.get() + own, ldm, L.Mc.get(), ldm,
                       L.lambda.get() + rb);
     } else {
@@ -211,7 +211,7 @@ void fitc_nll_grad(stgp_structure* s, double* nll, double* grad) {
   dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, true);
   if (nown > 0) {
     ProfRegion pr(ctx, "f_KW_gemm");
-    if (ozaki_enabled())  // K^{-1} symmetric: KW_i = K^{-1} W_i row by row
+    if (ozaki_for(ldm))  // K^{-1} symmetric: KW_i = K^{-1} W_i row by row
       ozaki_gemm_rows(ctx, nown, ldm, ldm, L.W.get() + own, ldm, L.Kinv.get(), ldm, L.work1.get() + own, ldm);
     else
       dev_gemm(ctx, false, false, ldm, nown, ldm, 1.0, L.Kinv.get(), ldm, L.W.get() + own, ldm, 0.0,
@@ -226,7 +226,7 @@ void fitc_nll_grad(stgp_structure* s, double* nll, double* grad) {
     // S = W diag(phi) W^T (symmetric: lower blocks only)
     ProfRegion prs(ctx, "f_S_gemm");
     scale_cols(ctx, L.W.get() + own, ldm, nown, phi + rb, false, L.work2.get() + own);
-    if (ozaki_enabled()) {  // S(i, j) = sum_r W(i, r) phi_r W(j, r); mirrored lower triangle
+    if (ozaki_for(ldm)) {  // S(i, j) = sum_r W(i, r) phi_r W(j, r); mirrored lower triangle
       ozaki_gemm_cols(ctx, ldm, nown, L.work2.get() + own, ldm, L.W.get() + own, ldm, S, ldm);
       dev_symmetrize_lower(ctx, S, ldm, ldm);
     } else

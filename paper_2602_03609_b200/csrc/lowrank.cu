@@ -836,7 +836,7 @@ void vif_build(stgp_structure* s) {
   ProfRegion prk(ctx, "K_gemm_chol");
   L.work1.ensure(total);
   const size_t off = static_cast<size_t>(rb) * ldm;
-  if (!ozaki_enabled()) scale_cols(ctx, L.Vp.get() + off, ldm, re - rb, s->D.get() + rb, true, L.work1.get() + off);
+  if (!ozaki_for(ldm)) scale_cols(ctx, L.Vp.get() + off, ldm, re - rb, s->D.get() + rb, true, L.work1.get() + off);
   L.Mc.ensure(static_cast<size_t>(ldm) * ldm);
   STGP_CUDA(cudaMemsetAsync(L.Mc.get(), 0, sizeof(double) * ldm * ldm, ctx->stream));
   // S S^T as GEMMs over the lower blocks of a partition (dense.cu dev_syrk_blocked)
@@ -845,7 +845,7 @@ void vif_build(stgp_structure* s) {
       const char* e = std::getenv("STGP_KBLOCKS");
       return e ? std::max(1, std::atoi(e)) : 4;  // 5/8 of the GEMM flops; measured best at M = 906
     }();
-    if (ozaki_enabled())  // S S^T on the int8 tensor cores (exactly symmetric result)
+    if (ozaki_for(ldm))  // S S^T on the int8 tensor cores (exactly symmetric result)
       ozaki_gemm_cols(ctx, ldm, re - rb, L.Vp.get() + off, ldm, L.Vp.get() + off, ldm, L.Mc.get(), ldm, s->D.get() + rb);
     else
       dev_syrk_blocked(ctx, ldm, re - rb, 1.0, L.work1.get() + off, ldm, L.Mc.get(), ldm, kblocks);
@@ -955,7 +955,7 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
   dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, true);
   L.work1.ensure(total);
   if (re > rb) {
-    if (ozaki_enabled())  // K^{-1} is symmetric: X_r = K^{-1} V'_r row by row on the int8 tensor cores
+    if (ozaki_for(ldm))  // K^{-1} is symmetric: X_r = K^{-1} V'_r row by row on the int8 tensor cores
       ozaki_gemm_rows(ctx, re - rb, ldm, ldm, L.Vp.get() + own, ldm, L.Kinv.get(), ldm, L.work1.get() + own, ldm);
     else
       dev_gemm(ctx, false, false, ldm, re - rb, ldm, 1.0, L.Kinv.get(), ldm, L.Vp.get() + own, ldm, 0.0,
@@ -994,7 +994,7 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
   }
   ph.reset(new ProfRegion(ctx, "g_S_gemm"));
   // W Phi W^T = sym(V' F^T) summed over shards -> wsig' = 0.5 yhat yhat^T + sym(V'F^T) + 0.5 (K^{-1} - I)
-  if (re > rb && ozaki_enabled())  // S(i, j) = sum_r V'(i, r) F(j, r)
+  if (re > rb && ozaki_for(ldm))  // S(i, j) = sum_r V'(i, r) F(j, r)
     ozaki_gemm_cols(ctx, ldm, re - rb, L.work2.get() + own, ldm, L.Vp.get() + own, ldm, S, ldm);
   else if (re > rb)
     dev_gemm(ctx, false, true, ldm, ldm, re - rb, 1.0, L.Vp.get() + own, ldm, L.work2.get() + own, ldm, 0.0, S, ldm);

@@ -9,6 +9,7 @@ namespace stgp {
 
 struct OzakiState;
 bool ozaki_enabled();
+bool ozaki_for(int m);  // enabled and worth it at this inner size
 int ozaki_slices();
 // C[r * ldc + j] = sum_{c < k} A[r * lda + c] * B[j * ldb + c]  for r < n, j < m (FP64 in and out;
 // m and ldc multiples of 4)

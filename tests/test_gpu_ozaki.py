@@ -83,3 +83,44 @@ def test_ozaki_long_reduction_timing(ctx):
     D, ms_d = ctx.gemm_cols(A, B, emulated=False)
     assert np.allclose(C, D, rtol=0, atol=2.0 ** -40 * n)
     print(f"ozaki cols {ms_e:.2f} ms vs DGEMM {ms_d:.2f} ms at n={n}")
+
+
+_FITC_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, %(root)r)
+import paper_2602_03609_b200 as S
+from oracle import oracle as O
+x, y, t, yv, X = O.test_dataset(1, 1500, 47, n_times=8, p=1)
+rng = np.random.default_rng(9)
+Z = np.column_stack([rng.random(40), rng.random(40), 1 + 7 * rng.random(40)])
+th = (0.2, 1.1, 0.8, 12.0, 0.6, 1.5, 0.3, 0.5)
+s = S.build_fitc(S.SpaceTimeDataset(x, y, t), th, S.InducingSet.from_points(Z))
+v, g = S.nll_and_grad(s, yv, X, np.array([-0.2]))
+print(json.dumps({"nll": v, "grad": list(map(float, g))}))
+"""
+
+
+def test_ozaki_products_inside_fitc_match_oracle():
+    # FITC's K, K^-1 W and W diag(phi) W^T forced onto the int8 path at test size
+    import json
+    import os
+    import subprocess
+    import sys
+    from oracle import oracle as O
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, STGP_OZAKI_MIN_M="0")
+    r = subprocess.run([sys.executable, "-c", _FITC_SCRIPT % dict(root=root)], env=env, capture_output=True, text=True,
+                       timeout=300, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    a = json.loads(r.stdout.strip().splitlines()[-1])
+    x, y, t, yv, X = O.test_dataset(1, 1500, 47, n_times=8, p=1)
+    rng = np.random.default_rng(9)
+    Z = np.column_stack([rng.random(40), rng.random(40), 1 + 7 * rng.random(40)])
+    th = (0.2, 1.1, 0.8, 12.0, 0.6, 1.5, 0.3, 0.5)
+    om = O.OracleModel("fitc", x, y, t, th, Z=Z)
+    beta = np.array([-0.2])
+    gr = om.nll_grad(yv, X, beta)
+    assert a["nll"] == pytest.approx(om.nll(yv, X, beta), rel=1e-8)
+    g = np.array(a["grad"])
+    assert np.allclose(g, gr, rtol=1e-8, atol=1e-8 * np.abs(gr).max()), (g, gr)

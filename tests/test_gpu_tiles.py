@@ -39,9 +39,9 @@ print(json.dumps({"nll": v, "grad": list(map(float, g))}))
 """
 
 
-def _run(tmp_path, tiles, st, days, m, mv):
-    out = str(tmp_path / f"case_{tiles}.npz")
-    env = dict(os.environ, STGP_TILES=str(tiles))
+def _run(tmp_path, tiles, st, days, m, mv, **extra_env):
+    out = str(tmp_path / f"case_{tiles}_{len(extra_env)}.npz")
+    env = dict(os.environ, STGP_TILES=str(tiles), **extra_env)
     code = _SCRIPT % dict(root=ROOT, st=st, days=days, m=m, mv=mv, out=out)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
@@ -55,6 +55,20 @@ def test_tiles_match_row_gathers_and_oracle(tmp_path, st, days, m, mv):
     ga, gb = np.array(a["grad"]), np.array(b["grad"])
     assert a["nll"] == pytest.approx(b["nll"], rel=1e-12)
     assert np.allclose(ga, gb, rtol=1e-10, atol=1e-10 * np.abs(gb).max())
+    th = (0.01, 1.0, 0.5, 20.0, 0.4, 1.5, 0.4, 0.2)
+    om = O.OracleModel("vif", case["x"], case["y"], case["t"], th, nbr=case["nbr"], Z=case["Z"])
+    vr, gr = om.nll(case["resp"]), om.nll_grad(case["resp"])
+    assert a["nll"] == pytest.approx(vr, rel=1e-8)
+    assert np.allclose(ga, gr, rtol=1e-8, atol=1e-8 * np.abs(gr).max()), (ga, gr)
+
+
+def test_ozaki_products_inside_vif_match_oracle(tmp_path):
+    # the int8 Ozaki products run only from M >= 512 by default; force them at test size
+    a, case = _run(tmp_path, 1, 300, 9, 40, 17, STGP_OZAKI_MIN_M="0")
+    b, _ = _run(tmp_path, 1, 300, 9, 40, 17, STGP_OZAKI="0")
+    ga, gb = np.array(a["grad"]), np.array(b["grad"])
+    assert a["nll"] == pytest.approx(b["nll"], rel=1e-11)
+    assert np.allclose(ga, gb, rtol=1e-9, atol=1e-9 * np.abs(gb).max())
     th = (0.01, 1.0, 0.5, 20.0, 0.4, 1.5, 0.4, 0.2)
     om = O.OracleModel("vif", case["x"], case["y"], case["t"], th, nbr=case["nbr"], Z=case["Z"])
     vr, gr = om.nll(case["resp"]), om.nll_grad(case["resp"])
