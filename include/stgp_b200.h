@@ -195,6 +195,28 @@ int stgp_fit(stgp_dataset* ds, const double* y_host, const double* X_host, int p
              const stgp_params* init, stgp_params* theta_out, double* beta_out, double* final_nll,
              int* converged, stgp_trace_row* trace_out, int trace_cap, int* n_trace);
 
+/* ---- dataset CSV and neighbour audit formats (dataset.cpp:191-316, neighbors.cpp:336-355) ---- */
+typedef struct stgp_table stgp_table; /* a parsed dataset CSV (host memory) */
+/* read_dataset_csv: '#' lines skipped, header names x, y, t, value (required), station_id
+ * (optional), every other column a covariate; DataError on malformed input. */
+int stgp_read_dataset_csv(const char* path, stgp_table** out);
+int stgp_table_shape(const stgp_table* tab, int* n, int* p, int* has_stations);
+/* columns in file order; X is n x p column-major (any pointer may be NULL) */
+int stgp_table_columns(const stgp_table* tab, double* x, double* y, double* t, double* value, double* X);
+/* copy station i / covariate name j into buf (NUL-terminated, truncated to cap); returns the full
+ * length, -1 when out of range */
+int stgp_table_station(const stgp_table* tab, int i, char* buf, int cap);
+int stgp_table_covariate_name(const stgp_table* tab, int j, char* buf, int cap);
+void stgp_table_destroy(stgp_table* tab);
+/* write_dataset_csv (precision 17, "# comment" line when given, covariates named x0..x{p-1}) */
+int stgp_write_dataset_csv(const char* path, int n, const double* x, const double* y, const double* t,
+                           const double* value, int p, const double* X, const char* const* stations,
+                           const char* header_comment);
+/* write_neighbor_debug_csv: "i,rank,neighbor_index,distance" rows, each set sorted by
+ * (distance, index), with the metric of the search (cli.cpp:516-572) */
+int stgp_write_neighbor_debug_csv(const char* path, const stgp_neighbors* nb, const stgp_dataset* ds,
+                                  const char* header_comment);
+
 /* ---- diagnostics ---- */
 /* device exp port on n inputs (KAT against the host libm) */
 int stgp_debug_exp(stgp_ctx* ctx, int n, const double* x_host, double* out);

@@ -79,6 +79,11 @@ _SIGS = {
     "stgp_debug_exp": [_P, C.c_int, _P, _P],
     "stgp_debug_fp64_peak": [_P, _D],
     "stgp_debug_dmma_peak": [_P, _D],
+    "stgp_read_dataset_csv": [C.c_char_p, C.POINTER(_P)],
+    "stgp_table_shape": [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)],
+    "stgp_table_columns": [_P, _P, _P, _P, _P, _P],
+    "stgp_write_dataset_csv": [C.c_char_p, C.c_int, _P, _P, _P, _P, C.c_int, _P, _P, C.c_char_p],
+    "stgp_write_neighbor_debug_csv": [C.c_char_p, _P, _P, C.c_char_p],
     "stgp_default_init": [_P, _P, _P, C.c_int, _P, C.POINTER(Params)],
     "stgp_fit": [_P, _P, _P, C.c_int, _P, _P, C.POINTER(Params), _P, _D, C.POINTER(C.c_int), _P, C.c_int,
                  C.POINTER(C.c_int)],
@@ -91,7 +96,7 @@ _SIGS = {
     "stgp_ctx_profile_reset": [_P],
     "stgp_debug_kernel": [_P, C.POINTER(Params), C.c_int, _P, _P, _P, _P],
 }
-_VOID = ["stgp_ctx_destroy", "stgp_dataset_destroy", "stgp_neighbors_destroy", "stgp_inducing_destroy",
+_VOID = ["stgp_table_destroy", "stgp_ctx_destroy", "stgp_dataset_destroy", "stgp_neighbors_destroy", "stgp_inducing_destroy",
          "stgp_structure_destroy"]
 
 _lib = None
@@ -118,6 +123,9 @@ def lib():
         L.stgp_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
         L.stgp_ctx_kernel_launches.restype = C.c_int64
         L.stgp_ctx_kernel_launches.argtypes = [_P]
+        for name in ("stgp_table_station", "stgp_table_covariate_name"):  # return a length, not a code
+            getattr(L, name).restype = C.c_int
+            getattr(L, name).argtypes = [_P, C.c_int, C.c_char_p, C.c_int]
         L.stgp_ctx_stream.restype = C.c_void_p
         L.stgp_ctx_stream.argtypes = [_P]
         _lib = L
@@ -135,4 +143,5 @@ def call(name: str, *args) -> None:
 
 
 def exported_symbols() -> list[str]:
-    return sorted(list(_SIGS) + _VOID + ["stgp_last_error", "stgp_mix_seed", "stgp_ctx_kernel_launches", "stgp_ctx_stream"])
+    return sorted(list(_SIGS) + _VOID + ["stgp_last_error", "stgp_mix_seed", "stgp_ctx_kernel_launches", "stgp_ctx_stream",
+                                         "stgp_table_station", "stgp_table_covariate_name"])

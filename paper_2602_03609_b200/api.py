@@ -550,3 +550,58 @@ def fit(x, y, t, resp, X=None, config: FitConfig | None = None, init=None, ctx: 
     trace = [(r.iteration, r.nll, r.grad_norm, bool(r.refresh)) for r in rows[:min(ntr.value, trace_cap)]]
     th = CovarianceParams(*[getattr(theta, f) for f, _ in N.Params._fields_])
     return FittedModel(th, beta[:p].copy(), fnll.value, bool(conv.value), trace, ds)
+
+
+# ---------------------------------------------------------------------------
+# dataset CSV and neighbour audit (dataset.cpp:191-316, neighbors.cpp:336-355)
+# ---------------------------------------------------------------------------
+@dataclass
+class DatasetTable:
+    """read_dataset_csv's SpaceTimeDataset fields (host): points, value, X (n x p), stations."""
+    x: np.ndarray
+    y: np.ndarray
+    t: np.ndarray
+    value: np.ndarray
+    X: np.ndarray
+    stations: list
+    covariate_names: list
+
+
+def read_dataset_csv(path: str) -> DatasetTable:
+    h = C.c_void_p()
+    N.call("stgp_read_dataset_csv", str(path).encode(), C.byref(h))
+    try:
+        n, p, hs = C.c_int(), C.c_int(), C.c_int()
+        N.call("stgp_table_shape", h, C.byref(n), C.byref(p), C.byref(hs))
+        n, p = n.value, p.value
+        x, y, t, v = (np.zeros(n) for _ in range(4))
+        X = np.zeros((n, p), order="F")
+        N.call("stgp_table_columns", h, _ptr(x), _ptr(y), _ptr(t), _ptr(v), _ptr(X) if p else None)
+        L = N.lib()
+
+        def text(fn, i):
+            k = fn(h, i, None, 0)
+            buf = C.create_string_buffer(k + 1)
+            fn(h, i, buf, k + 1)
+            return buf.value.decode()
+        stations = [text(L.stgp_table_station, i) for i in range(n)] if hs.value else []
+        names = [text(L.stgp_table_covariate_name, j) for j in range(p)]
+        return DatasetTable(x, y, t, v, X, stations, names)
+    finally:
+        N.lib().stgp_table_destroy(h)
+
+
+def write_dataset_csv(path: str, x, y, t, value, X=None, stations=None, header_comment: str = ""):
+    x, y, t, value = _f64(x), _f64(y), _f64(t), _f64(value)
+    n = len(x)
+    Xf = None if X is None else np.asfortranarray(np.asarray(X, dtype=np.float64).reshape(n, -1))
+    p = 0 if Xf is None else Xf.shape[1]
+    st = None
+    if stations is not None:
+        st = (C.c_char_p * n)(*[str(s).encode() for s in stations])
+    N.call("stgp_write_dataset_csv", str(path).encode(), n, _ptr(x), _ptr(y), _ptr(t), _ptr(value), p,
+           _ptr(Xf) if p else None, C.cast(st, C.c_void_p) if st is not None else None, header_comment.encode())
+
+
+def write_neighbor_debug_csv(path: str, neighbors: "NeighborSets", ds: "SpaceTimeDataset", header_comment: str = ""):
+    N.call("stgp_write_neighbor_debug_csv", str(path).encode(), neighbors.h, ds.h, header_comment.encode())
