@@ -16,6 +16,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <algorithm>
 #include <vector>
 
 #include "stgp_b200.h"
@@ -269,6 +270,41 @@ inline PredictiveDistribution predict(Structure& s, const std::vector<double>& y
   check(stgp_predict(s.get(), y.data(), p ? X.data() : nullptr, p, p ? beta.data() : nullptr, np, targets_xyt.data(),
                      p ? X_p.data() : nullptr, pred_m_v, out.mu.data(), out.var.data()));
   return out;
+}
+
+// FitConfig / TraceRow / FittedModel (estimation.hpp:23-83), Gaussian likelihood
+using FitConfig = stgp_fit_config;
+using TraceRow = stgp_trace_row;
+struct FittedModel {
+  CovarianceParams theta{};
+  std::vector<double> beta;
+  double final_nll = 0.0;
+  bool converged = false;
+  std::vector<TraceRow> trace;
+};
+inline FitConfig default_fit_config() {
+  return FitConfig{STGP_FIT_VECCHIA_CORR, 30, 500, 200, 1e-8, 1e-5, 1.5, 0};
+}
+// default_init (estimation.cpp:68-114) on an ordered dataset
+inline CovarianceParams default_init(const SpaceTimeDataset& ds, const std::vector<double>& y, const FitConfig& config,
+                                     const std::vector<double>& X = {}, int p = 0) {
+  CovarianceParams out{};
+  check(stgp_default_init(ds.get(), y.data(), p ? X.data() : nullptr, p, &config, &out));
+  return out;
+}
+// fit (estimation.cpp:423-619) on the ordered dataset (FittedModel.data); init nullptr -> default_init
+inline FittedModel fit(SpaceTimeDataset& ds, const std::vector<double>& y, const FitConfig& config,
+                       const CovarianceParams* init = nullptr, const std::vector<double>& X = {}, int p = 0) {
+  FittedModel m;
+  m.beta.assign(static_cast<size_t>(p), 0.0);
+  std::vector<TraceRow> tr(4096);
+  int conv = 0, ntr = 0;
+  check(stgp_fit(ds.get(), y.data(), p ? X.data() : nullptr, p, &config, init, &m.theta, p ? m.beta.data() : nullptr,
+                 &m.final_nll, &conv, tr.data(), static_cast<int>(tr.size()), &ntr));
+  tr.resize(static_cast<size_t>(std::min(ntr, static_cast<int>(tr.size()))));
+  m.trace = std::move(tr);
+  m.converged = conv != 0;
+  return m;
 }
 
 }  // namespace stgp_b200
