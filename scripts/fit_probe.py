@@ -21,7 +21,6 @@ init = tuple(v * 1.5 if j in (0, 1, 2, 3, 7) else v for j, v in enumerate(theta)
 t0 = time.perf_counter()
 fm = S.fit(x, y, t, resp, config=cfg, ctx=ctx, init=init)
 dt = time.perf_counter() - t0
-evals = sum(c for k, (ms, c) in ctx.profile_all().items() if k in ("rows", "K_gemm_chol")) if False else None
 print(f"n={len(x)} {method} m_v={mv} m={m}: {dt:.2f} s, {len(fm.trace)} trace rows, converged={fm.converged}, "
       f"nll {fm.trace[0][1]:.6f} -> {fm.final_nll:.6f}")
 print("theta:", fm.theta)
