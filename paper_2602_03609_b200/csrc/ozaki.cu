@@ -16,6 +16,9 @@
 // evaluation, tests/test_gpu_ozaki.py measures it against cuBLAS DGEMM).
 #include <cublasLt.h>
 
+#include <fstream>
+#include <string>
+
 #include <algorithm>
 #include <cstdlib>
 #include <map>
@@ -261,6 +264,7 @@ struct LtPlan {
   cublasLtMatmulAlgo_t cand[kAlgoCands];
   int ncand = 0;
   bool tuned = false;  // heuristic candidates timed once on the first call (results are identical: exact int32)
+  std::string key;     // plan shape, for the tuning cache
   ~LtPlan() {
     if (la) cublasLtMatrixLayoutDestroy(la);
     if (lb) cublasLtMatrixLayoutDestroy(lb);
@@ -271,7 +275,32 @@ struct LtPlan {
 
 }  // namespace
 
+// Tuning cache (STGP_OZAKI_TUNE_SAVE / STGP_OZAKI_TUNE_LOAD = path): the candidate chosen per plan
+// shape by a normal run is replayed by a run under a profiler, whose event timings are not the
+// kernels' (ncu serialises and instruments every launch).
+struct TuneCache {
+  std::map<std::string, int> pick;
+  bool loaded = false;
+  void load() {
+    if (loaded) return;
+    loaded = true;
+    const char* path = std::getenv("STGP_OZAKI_TUNE_LOAD");
+    if (!path) return;
+    std::ifstream is(path);
+    std::string k;
+    int v;
+    while (is >> k >> v) pick[k] = v;
+  }
+  void save(const std::string& k, int v) {
+    const char* path = std::getenv("STGP_OZAKI_TUNE_SAVE");
+    if (!path) return;
+    std::ofstream os(path, std::ios::app);
+    os << k << " " << v << "\n";
+  }
+};
+
 struct OzakiState {
+  TuneCache tune;
   cublasLtHandle_t lt = nullptr;
   DevBuf<unsigned char> ws;
   DevBuf<int8_t> As, Bs;
@@ -334,6 +363,8 @@ static LtPlan* plan_for(OzakiState* oz, int m, int mp, int K, long long ncols, i
   auto it = oz->plans.find(key);
   if (it != oz->plans.end()) return it->second.get();
   auto p = std::make_unique<LtPlan>();
+  p->key = std::to_string(m) + "x" + std::to_string(K) + "x" + std::to_string(ncols) + "/" + std::to_string(ldk) + "/" +
+           std::to_string(mp) + "/" + std::to_string(batch);
   lt_check(cublasLtMatmulDescCreate(&p->op, CUBLAS_COMPUTE_32I, CUDA_R_32I), "desc");
   const cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
   lt_check(cublasLtMatmulDescSetAttribute(p->op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof(ta)), "transa");
@@ -375,7 +406,12 @@ static void lt_matmul(stgp_ctx* ctx, OzakiState* oz, LtPlan* p, const int8_t* a,
   ProfRegion pr(ctx, "oz_imma");  // int8 tensor-core time (bench.py roofline_int8)
   if (!p->tuned) {
     p->tuned = true;
-    if (p->ncand > 1) {
+    oz->tune.load();
+    const auto hit = oz->tune.pick.find(p->key);
+    if (hit != oz->tune.pick.end() && hit->second >= 0 && hit->second < p->ncand) {
+      p->algo = p->cand[hit->second];
+    } else if (p->ncand > 1) {
+      int best_i = 0;
       cudaEvent_t e0, e1;
       STGP_CUDA(cudaEventCreate(&e0));
       STGP_CUDA(cudaEventCreate(&e1));
@@ -394,11 +430,13 @@ static void lt_matmul(stgp_ctx* ctx, OzakiState* oz, LtPlan* p, const int8_t* a,
         STGP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
         if (ms < best) {
           best = ms;
+          best_i = i;
           p->algo = p->cand[i];
         }
       }
       cudaEventDestroy(e0);
       cudaEventDestroy(e1);
+      oz->tune.save(p->key, best_i);
     }
   }
   lt_check(cublasLtMatmul(oz->lt, p->op, &one, a, p->la, b, p->lb, &zero, c, p->lc, c, p->lc, &p->algo, oz->ws.get(),
