@@ -388,13 +388,14 @@ def main():
     achieved = flops_launch / (k_avg * 1e-3) / 1e12
     # DRAM bytes of the row pass from one ncu --set full capture per kernel (cfg4, N = 1):
     # dram__bytes_read.sum + dram__bytes_write.sum, profiles/r01/rows_{build,grad}_full_ncu.txt
-    traffic = (14.376859e9 + 5.982890e9 + 45.472518e9 + 0.351775e9) if (
+    traffic = (14.263361e9 + 5.968408e9 + 24.170873e9 + 0.283e9 + 5.41e9 + 0.34e9) if (
         args.workload == "vif" and (args.stations, args.days) == (10000, 110) and world == 1) else None
     breakdown = {k: round(ms_ / max(c_, 1), 3) for k, (ms_, c_) in sorted(prof.items(), key=lambda kv: -kv[1][0])}
     roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
             "frac": achieved / fp64_peak, "traffic": traffic,
-            "traffic_source": ("ncu --set full: vecchia_rows_kernel<build> 20.36 GB + vif_grad_stored_kernel 45.82 GB "
-                               "(profiles/r01/rows_*_full_ncu.txt)") if traffic else None,
+            "traffic_source": ("ncu dram__bytes_read+write: vecchia_rows_kernel<build> 20.23 GB + tile_ga_kernel 24.45 GB "
+                               "+ vif_grad_stored_kernel 5.75 GB (profiles/r01/v13_ncu_summary.txt, "
+                               "tiles_ncu_summary.txt)") if traffic else None,
             "kernel": kname, "kernel_ms": k_avg,
             "kernel_share": k_avg / ms_step, "flop_per_launch": flops_launch,
             "peak_source": (f"measured in-run: max of DMMA m8n8k4 ({dmma_peak:.1f}) and DFMA ({dfma_peak:.1f}) "
