@@ -405,12 +405,16 @@ def main():
             "phase_ms": breakdown}
     # the FP64 products that run on the int8 tensor cores (Ozaki slicing, csrc/ozaki.cu): X = K^-1 V'
     # (FITC: K^-1 W), K = S S^T and V'F^T (FITC: W diag(phi) W^T), each S(S+1)/2 int8 MACs per FP64 FMA
+    # (S = 6 slices for the row form, 7 for the long reductions)
     # per evaluation: the region total over the evaluations profiled (timed steps and e2e steps alike)
     oz_ms = prof.get("oz_imma", (0.0, 0))[0] / max(prof.get("K_gemm_chol", (0.0, 1))[1], 1)
     if args.workload in ("vif", "fitc") and oz_ms > 0:
-        sl = int(os.environ.get("STGP_OZAKI_S", "7"))
+        s_all = os.environ.get("STGP_OZAKI_S")
+        s_rows = int(os.environ.get("STGP_OZAKI_S_ROWS", s_all or 6))
+        s_cols = int(os.environ.get("STGP_OZAKI_S_COLS", s_all or 7))
         ldm = (M + 15) // 16 * 16
-        int8_ops = 3 * 2.0 * sl * (sl + 1) / 2 * ldm * ldm * (hi - lo)
+        pairs = s_rows * (s_rows + 1) / 2 + 2 * s_cols * (s_cols + 1) / 2  # X (rows form) + K and V'F^T
+        int8_ops = 2.0 * pairs * ldm * ldm * (hi - lo)
         int8_peak = 2.0 * peaks().get("bf16_tflops", 1669.7)
         roof["int8_tensor"] = {
             "bound": "tensor", "achieved": int8_ops / (oz_ms * 1e-3) / 1e12, "peak": int8_peak, "unit": "TOPS",

@@ -319,6 +319,16 @@ void ozaki_release(stgp_ctx* ctx) {
   ctx->ozaki = nullptr;
 }
 
+// Slices per form: the long reductions (K = S S^T, V'F^T; STGP_OZAKI_S_COLS, default S) carry the
+// error budget (cfg4, worst gradient component vs DMMA: 2.8e-11 at 7 slices, 3.1e-9 at 6); the row
+// form (X = K^-1 V', FITC K^-1 W; STGP_OZAKI_S_ROWS) costs nothing measurable at 6 (3.4e-11 with
+// the column products at 7; 1.6e-9 at 5), which saves a quarter of its int8 work.
+static int slices_for(const char* var, int dflt) {
+  const char* e = std::getenv(var);
+  if (e) return std::max(2, std::min(8, std::atoi(e)));
+  return std::getenv("STGP_OZAKI_S") ? ozaki_slices() : dflt;
+}
+
 int ozaki_slices() {
   static const int s = [] {
     const char* e = std::getenv("STGP_OZAKI_S");
@@ -449,7 +459,7 @@ void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, 
                      double* C, int ldc) {
   if (n <= 0 || m <= 0) return;
   if (m % 4 || ldc % 4) config_error("ozaki_gemm_rows: m and ldc must be multiples of 4");
-  const int S = ozaki_slices();
+  const int S = slices_for("STGP_OZAKI_S_ROWS", 6);
   const int kp = (k + 15) / 16 * 16;  // slice stride: every diagonal segment 16-byte aligned
   if (static_cast<long long>(S) * kp * 127 * 127 >= (1LL << 31)) config_error("ozaki: k too large for exact int32");
   OzakiState* oz = state(ctx);
@@ -486,7 +496,7 @@ void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, 
 void ozaki_gemm_cols(stgp_ctx* ctx, int m, long long n, const double* A, int lda, const double* B, int ldb, double* C,
                      int ldc, const double* colD) {
   if (m <= 0) return;
-  const int S = ozaki_slices();
+  const int S = slices_for("STGP_OZAKI_S_COLS", 7);
   OzakiState* oz = state(ctx);
   cudaStream_t st = ctx->stream;
   // chunk of the reduction: exact int32 for the longest diagonal, (S) L 127^2 < 2^31
