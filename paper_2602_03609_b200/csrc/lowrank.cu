@@ -846,7 +846,7 @@ void vif_build(stgp_structure* s) {
       return e ? std::max(1, std::atoi(e)) : 4;  // 5/8 of the GEMM flops; measured best at M = 906
     }();
     if (ozaki_for(ldm))  // S S^T on the int8 tensor cores (exactly symmetric result)
-      ozaki_gemm_cols(ctx, ldm, re - rb, L.Vp.get() + off, ldm, L.Vp.get() + off, ldm, L.Mc.get(), ldm, s->D.get() + rb);
+      ozaki_syrk_keep(ctx, ldm, re - rb, L.Vp.get() + off, ldm, s->D.get() + rb, L.Mc.get(), ldm, s->uid);
     else
       dev_syrk_blocked(ctx, ldm, re - rb, 1.0, L.work1.get() + off, ldm, L.Mc.get(), ldm, kblocks);
   }
@@ -994,8 +994,11 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
   }
   ph.reset(new ProfRegion(ctx, "g_S_gemm"));
   // W Phi W^T = sym(V' F^T) summed over shards -> wsig' = 0.5 yhat yhat^T + sym(V'F^T) + 0.5 (K^{-1} - I)
-  if (re > rb && ozaki_for(ldm))  // S(i, j) = sum_r V'(i, r) F(j, r)
-    ozaki_gemm_cols(ctx, ldm, re - rb, L.work2.get() + own, ldm, L.Vp.get() + own, ldm, S, ldm);
+  if (re > rb && ozaki_for(ldm)) {  // S(i, j) = sum_r V'(i, r) F(j, r), or its transpose (symmetrised below)
+    // V' D^{-1/2} was sliced for K in the build: reuse its digits, slice only F D^{1/2}
+    if (!ozaki_gemm_kept(ctx, ldm, re - rb, L.work2.get() + own, ldm, s->D.get() + rb, S, ldm, s->uid))
+      ozaki_gemm_cols(ctx, ldm, re - rb, L.work2.get() + own, ldm, L.Vp.get() + own, ldm, S, ldm);
+  }
   else if (re > rb)
     dev_gemm(ctx, false, true, ldm, ldm, re - rb, 1.0, L.Vp.get() + own, ldm, L.work2.get() + own, ldm, 0.0, S, ldm);
   else

@@ -226,6 +226,12 @@ __global__ void __launch_bounds__(256) combine_rows_kernel(long long nrows, int 
   }
 }
 
+__global__ void sqrt_vec_kernel(long long n, const double* __restrict__ d, double* __restrict__ f) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    f[i] = sqrt(d[i]);
+}
+
 __global__ void rsqrt_vec_kernel(long long n, const double* __restrict__ d, double* __restrict__ f) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
@@ -305,7 +311,12 @@ struct OzakiState {
   DevBuf<unsigned char> ws;
   DevBuf<int8_t> As, Bs;
   DevBuf<int32_t> Cd;
-  DevBuf<double> sA, sB, colf;
+  DevBuf<double> sA, sB, colf, colf2;
+  DevBuf<int8_t> keep;  // forward digits of the last ozaki_syrk_keep operand (V' D^{-1/2})
+  DevBuf<double> keep_s;
+  uint64_t keep_tag = 0;
+  int keep_m = 0;
+  long long keep_n = 0;
   DevBuf<unsigned long long> maxbits;
   std::map<std::tuple<int, int, long long, int, int, int>, std::unique_ptr<LtPlan>> plans;
   ~OzakiState() {
@@ -493,9 +504,12 @@ void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, 
   }
 }
 
-void ozaki_gemm_cols(stgp_ctx* ctx, int m, long long n, const double* A, int lda, const double* B, int ldb, double* C,
-                     int ldc, const double* colD) {
-  if (m <= 0) return;
+// Column-form product C[j ldc + i] = sum_r (fA_r A[j + r lda]) (fB_r B[i + r ldb]) with optional
+// per-column factors fA, fB (device vectors).  same: A == B with fA == fB (one slicing pass writes
+// both digit orders).  keep: the forward digits of A go to the context's kept buffer (tag);
+// kept: A's digits are taken from there instead of slicing A.
+static void cols_product(stgp_ctx* ctx, int m, long long n, const double* A, int lda, const double* fA, const double* B,
+                         int ldb, const double* fB, bool same, uint64_t keep_tag, bool use_kept, double* C, int ldc) {
   const int S = slices_for("STGP_OZAKI_S_COLS", 7);
   OzakiState* oz = state(ctx);
   cudaStream_t st = ctx->stream;
@@ -507,46 +521,86 @@ void ozaki_gemm_cols(stgp_ctx* ctx, int m, long long n, const double* A, int lda
   const long long ldk = static_cast<long long>(S) * L;
   const long long bstride = static_cast<long long>(m) * ldk;
   const size_t sl = static_cast<size_t>(nch) * bstride;
-  oz->As.ensure(sl);
-  oz->sA.ensure(static_cast<size_t>(nch) * m);
-  const bool same = A == B && lda == ldb;  // A A^T: one pass writes both slice orders
-  if (colD) {
-    oz->colf.ensure(static_cast<size_t>(n));
-    rsqrt_vec_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, colD, oz->colf.get());
-    launched(ctx);
-    colD = oz->colf.get();
+  int8_t* Aslices;
+  double* sA;
+  if (keep_tag != 0 || use_kept) {
+    oz->keep.ensure(sl);
+    oz->keep_s.ensure(static_cast<size_t>(nch) * m);
+    Aslices = oz->keep.get();
+    sA = oz->keep_s.get();
+  } else {
+    oz->As.ensure(sl);
+    oz->sA.ensure(static_cast<size_t>(nch) * m);
+    Aslices = oz->As.get();
+    sA = oz->sA.get();
   }
   oz->Bs.ensure(sl);
   oz->sB.ensure(static_cast<size_t>(nch) * m);
   const dim3 grid(static_cast<unsigned>((n + kSlCols - 1) / kSlCols), (m + 31) / 32);
   oz->maxbits.ensure(static_cast<size_t>(nch) * m);
-  auto slice = [&](const double* X, int ldx, int8_t* fwd, int8_t* rev, double* sc) {
+  auto slice = [&](const double* X, int ldx, const double* f, int8_t* fwd, int8_t* rev, double* sc) {
     STGP_CUDA(cudaMemsetAsync(oz->maxbits.get(), 0, sizeof(unsigned long long) * nch * m, st));
-    colmax_kernel<<<grid, 256, 0, st>>>(m, n, L, X, ldx, colD, oz->maxbits.get());
+    colmax_kernel<<<grid, 256, 0, st>>>(m, n, L, X, ldx, f, oz->maxbits.get());
     launched(ctx);
     STGP_OZ_SWITCH(S, ({
                      const int smem = kS * 32 * kSlRow;
                      STGP_CUDA(cudaFuncSetAttribute(slice_cols_kernel<kS>,
                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-                     slice_cols_kernel<kS><<<grid, 256, smem, st>>>(m, n, L, X, ldx, colD, oz->maxbits.get(), fwd,
-                                                                     rev, sc);
+                     slice_cols_kernel<kS><<<grid, 256, smem, st>>>(m, n, L, X, ldx, f, oz->maxbits.get(), fwd, rev,
+                                                                     sc);
                    }));
     launched(ctx);
   };
-  slice(A, lda, oz->As.get(), same ? oz->Bs.get() : nullptr, oz->sA.get());
-  if (!same) slice(B, ldb, nullptr, oz->Bs.get(), oz->sB.get());
-  const double* sB = same ? oz->sA.get() : oz->sB.get();
+  if (!use_kept) slice(A, lda, fA, Aslices, same ? oz->Bs.get() : nullptr, sA);
+  if (!same) slice(B, ldb, fB, nullptr, oz->Bs.get(), oz->sB.get());
+  if (keep_tag != 0) {
+    oz->keep_tag = keep_tag;
+    oz->keep_m = m;
+    oz->keep_n = n;
+  }
+  const double* sB = same ? sA : oz->sB.get();
   const long long cstride = static_cast<long long>(m) * mp;
   const long long dstride = nch * cstride;
   oz->Cd.ensure(static_cast<size_t>(S) * dstride);
   for (int d = 2; d <= S + 1; ++d) {
     LtPlan* p = plan_for(oz, m, mp, (d - 1) * L, m, static_cast<int>(ldk), nch, bstride, cstride);
-    lt_matmul(ctx, oz, p, oz->Bs.get() + static_cast<size_t>(S - d + 1) * L, oz->As.get(),
-              oz->Cd.get() + (d - 2) * dstride);
+    lt_matmul(ctx, oz, p, oz->Bs.get() + static_cast<size_t>(S - d + 1) * L, Aslices, oz->Cd.get() + (d - 2) * dstride);
   }
   combine_cols_kernel<<<grid_for(static_cast<long long>(m) * m, 256), 256, 0, st>>>(
-      m, mp, nch, oz->Cd.get(), dstride, cstride, S, oz->sA.get(), sB, C, ldc);
+      m, mp, nch, oz->Cd.get(), dstride, cstride, S, sA, sB, C, ldc);
   launched(ctx);
+}
+
+// per-column factor vector 1 / sqrt(D) (inverse) or sqrt(D)
+static const double* col_factors(stgp_ctx* ctx, DevBuf<double>& buf, const double* D, long long n, bool inverse) {
+  buf.ensure(static_cast<size_t>(n));
+  if (inverse) rsqrt_vec_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(n, D, buf.get());
+  else sqrt_vec_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(n, D, buf.get());
+  launched(ctx);
+  return buf.get();
+}
+
+void ozaki_gemm_cols(stgp_ctx* ctx, int m, long long n, const double* A, int lda, const double* B, int ldb, double* C,
+                     int ldc, const double* colD) {
+  if (m <= 0) return;
+  const double* f = colD ? col_factors(ctx, state(ctx)->colf, colD, n, true) : nullptr;
+  cols_product(ctx, m, n, A, lda, f, B, ldb, f, A == B && lda == ldb, 0, false, C, ldc);
+}
+
+void ozaki_syrk_keep(stgp_ctx* ctx, int m, long long n, const double* A, int lda, const double* D, double* C, int ldc,
+                     uint64_t tag) {
+  if (m <= 0) return;
+  const double* f = col_factors(ctx, state(ctx)->colf, D, n, true);
+  cols_product(ctx, m, n, A, lda, f, A, lda, f, true, tag, false, C, ldc);
+}
+
+bool ozaki_gemm_kept(stgp_ctx* ctx, int m, long long n, const double* B, int ldb, const double* D, double* C, int ldc,
+                     uint64_t tag) {
+  OzakiState* oz = state(ctx);
+  if (m <= 0 || tag == 0 || oz->keep_tag != tag || oz->keep_m != m || oz->keep_n != n) return false;
+  const double* f = col_factors(ctx, oz->colf2, D, n, false);
+  cols_product(ctx, m, n, nullptr, 0, nullptr, B, ldb, f, false, 0, true, C, ldc);
+  return true;
 }
 
 }  // namespace stgp

@@ -20,6 +20,14 @@ void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, 
 // reduction over n runs in exact int32 chunks)
 void ozaki_gemm_cols(stgp_ctx* ctx, int m, long long n, const double* A, int lda, const double* B, int ldb, double* C,
                      int ldc, const double* colD = nullptr);
+// K = (A D^{-1/2})(A D^{-1/2})^T keeping the digits of A D^{-1/2} in the context (tag: the owner's
+// process-unique id, stgp_structure::uid);
+// ozaki_gemm_kept then forms C[j ldc + i] = sum_r A[j, r] B[i, r] = (A D^{-1/2})(B D^{1/2})^T from
+// them, slicing only B (false when the kept digits belong to another tag or shape).
+void ozaki_syrk_keep(stgp_ctx* ctx, int m, long long n, const double* A, int lda, const double* D, double* C, int ldc,
+                     uint64_t tag);
+bool ozaki_gemm_kept(stgp_ctx* ctx, int m, long long n, const double* B, int ldb, const double* D, double* C, int ldc,
+                     uint64_t tag);
 void ozaki_release(stgp_ctx* ctx);
 
 }  // namespace stgp

@@ -46,6 +46,8 @@ struct LowRank {
 }  // namespace stgp
 
 struct stgp_structure {
+  stgp_structure();  // assigns uid
+  uint64_t uid = 0;  // process-unique, never reused (owner tag of kept Ozaki digits)
   stgp_dataset* ds = nullptr;
   int kind = 0, policy = 0;
   stgp::Params th{};

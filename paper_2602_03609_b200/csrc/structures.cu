@@ -1,5 +1,6 @@
 // Structure builders and likelihood entry points (approximations.cpp:198-744).
 // Vecchia lives here; the low-rank FITC/VIF algebra is in lowrank.cu.
+#include <atomic>
 #include <climits>
 #include <cstring>
 
@@ -93,6 +94,11 @@ void vecchia_nll_grad(stgp_structure* s, double* nll, double* grad) {
 }  // namespace stgp
 
 using namespace stgp;
+
+stgp_structure::stgp_structure() {
+  static std::atomic<uint64_t> next{1};
+  uid = next.fetch_add(1);
+}
 
 namespace {
 template <class F>
