@@ -136,8 +136,7 @@ void fitc_build(stgp_structure* s) {
   ProfRegion prk(ctx, "K_gemm_chol");
   if (re > rb) {
     if (ozaki_for(ldm)) {  // W Lambda^{-1} W^T on the int8 tensor cores
-      ozaki_gemm_cols(ctx, ldm, re - rb, L.W.get() + own, ldm, L.W.get() + own, ldm, L.Mc.get(), ldm,
-                      L.lambda.get() + rb);
+      ozaki_syrk_keep(ctx, ldm, re - rb, L.W.get() + own, ldm, L.lambda.get() + rb, L.Mc.get(), ldm, s->uid);
     } else {
       scale_cols(ctx, L.W.get() + own, ldm, re - rb, L.lambda.get() + rb, true, L.work1.get() + own);
       dev_syrk_blocked(ctx, ldm, re - rb, 1.0, L.work1.get() + own, ldm, L.Mc.get(), ldm, 4);
@@ -227,7 +226,9 @@ void fitc_nll_grad(stgp_structure* s, double* nll, double* grad) {
     ProfRegion prs(ctx, "f_S_gemm");
     scale_cols(ctx, L.W.get() + own, ldm, nown, phi + rb, false, L.work2.get() + own);
     if (ozaki_for(ldm)) {  // S(i, j) = sum_r W(i, r) phi_r W(j, r); mirrored lower triangle
-      ozaki_gemm_cols(ctx, ldm, nown, L.work2.get() + own, ldm, L.W.get() + own, ldm, S, ldm);
+      // (W Lambda^{-1/2}) digits kept from K: S = (W Lambda^{-1/2}) (W diag(phi) Lambda^{1/2})^T
+      if (!ozaki_gemm_kept(ctx, ldm, nown, L.work2.get() + own, ldm, L.lambda.get() + rb, S, ldm, s->uid))
+        ozaki_gemm_cols(ctx, ldm, nown, L.work2.get() + own, ldm, L.W.get() + own, ldm, S, ldm);
       dev_symmetrize_lower(ctx, S, ldm, ldm);
     } else
       dev_gemm_sym_blocked(ctx, ldm, nown, 1.0, L.W.get() + own, ldm, L.work2.get() + own, ldm, S, ldm, 4);
