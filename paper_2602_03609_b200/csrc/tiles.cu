@@ -337,7 +337,19 @@ int env_int(const char* name, int dflt) {
 
 template <typename K>
 int resident_grid(stgp_ctx* ctx, K kern, size_t smem, long long items, int threads) {
-  STGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  // the attribute is per function and process-wide: always the device maximum, so that concurrent
+  // contexts (in-process ranks) launching with different tile unions never race on it
+  static const int max_optin = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v > 0 ? v : 227 * 1024;
+  }();
+  cudaFuncAttributes fa{};
+  STGP_CUDA(cudaFuncGetAttributes(&fa, kern));
+  const int dyn_max = max_optin - static_cast<int>(fa.sharedSizeBytes);
+  if (static_cast<long long>(smem) > dyn_max) return 0;
+  STGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max));
   int per_sm = 0;
   STGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
   return static_cast<int>(std::max<long long>(1, std::min<long long>(items, std::max(1, per_sm) * ctx->num_sms)));

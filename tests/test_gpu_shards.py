@@ -46,9 +46,10 @@ def _run(S, world, build, x, y, t, yv, X=None, beta=None):
         h.start()
     for h in th:
         h.join()
-    for e in err:
-        if e is not None:
-            raise e
+    # the first rank's own failure, not the aborted all-reduce it caused on the other ranks
+    real = [e for e in err if e is not None and "all-reduce callback failed" not in str(e)]
+    for e in real + [e for e in err if e is not None]:
+        raise e
     return out
 
 
@@ -118,9 +119,9 @@ def test_sharded_search_equals_single(S, metric, world):
             h.start()
         for h in th:
             h.join()
-        for e in err:
-            if e is not None:
-                raise e
+        real = [e for e in err if e is not None and "all-reduce callback failed" not in str(e)]
+        for e in real + [e for e in err if e is not None]:
+            raise e
         return out
 
     (i1, d1), = run(1)
