@@ -33,6 +33,14 @@ struct Error : std::runtime_error {
 
 #define STGP_LAUNCH_CHECK() STGP_CUDA(cudaGetLastError())
 
+// Device memory for DevBuf (engine.cu): the device's memory pool with an unbounded release
+// threshold, so steady-state allocations and frees stay inside the process instead of going to
+// the driver (cudaMalloc / cudaFree calls blocked the host for up to 1.7 s at random on the B200
+// boxes).  dev_free keeps cudaFree's semantics: it waits for the device before the block can be
+// reused.  STGP_POOL=0 restores cudaMalloc / cudaFree.
+void* dev_alloc(size_t bytes);
+void dev_free(void* p);
+
 // Owning device buffer.
 template <class T>
 struct DevBuf {
@@ -60,13 +68,13 @@ struct DevBuf {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) STGP_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    if (count) p = static_cast<T*>(dev_alloc(count * sizeof(T)));
   }
   void ensure(size_t count) {
     if (count > n) alloc(count);
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) dev_free(p);
     p = nullptr;
     n = 0;
   }

@@ -5,6 +5,8 @@
 // results.  Every O(n) loop of the hot path runs in a CUDA kernel.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
+#include <mutex>
 #include <cstring>
 #include <numeric>
 #include <random>
@@ -21,6 +23,75 @@
 #include "../../include/stgp_b200.h"
 
 namespace stgp {
+
+namespace {
+struct PoolDev {
+  bool init = false;
+  bool on = false;
+  cudaMemPool_t pool = nullptr;
+  cudaStream_t stream = nullptr;  // private, idle between calls: allocations are ready on return
+};
+PoolDev g_pool[64];
+std::mutex g_pool_mu;
+
+PoolDev& pool_dev(int dev) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  PoolDev& d = g_pool[dev & 63];
+  if (!d.init) {
+    d.init = true;
+    const char* e = std::getenv("STGP_POOL");
+    d.on = !(e && e[0] == '0');
+    if (d.on) {
+      STGP_CUDA(cudaDeviceGetDefaultMemPool(&d.pool, dev));
+      uint64_t thr = UINT64_MAX;
+      STGP_CUDA(cudaMemPoolSetAttribute(d.pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      STGP_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+    }
+  }
+  return d;
+}
+}  // namespace
+
+void* dev_alloc(size_t bytes) {
+  int dev = 0;
+  STGP_CUDA(cudaGetDevice(&dev));
+  PoolDev& d = pool_dev(dev);
+  void* p = nullptr;
+  if (!d.on) {
+    STGP_CUDA(cudaMalloc(&p, bytes));
+    return p;
+  }
+  cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, d.pool, d.stream);
+  if (e == cudaErrorMemoryAllocation) {  // cached blocks of other sizes: hand them back and retry
+    (void)cudaGetLastError();
+    STGP_CUDA(cudaDeviceSynchronize());
+    STGP_CUDA(cudaMemPoolTrimTo(d.pool, 0));
+    e = cudaMallocFromPoolAsync(&p, bytes, d.pool, d.stream);
+  }
+  STGP_CUDA(e);
+  STGP_CUDA(cudaStreamSynchronize(d.stream));
+  return p;
+}
+
+void dev_free(void* p) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  PoolDev& d = pool_dev(dev);
+  if (!d.on) {
+    cudaFree(p);
+    return;
+  }
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) == cudaSuccess && a.device != dev) {
+    cudaSetDevice(a.device);
+    dev_free(p);
+    cudaSetDevice(dev);
+    return;
+  }
+  cudaDeviceSynchronize();  // cudaFree semantics: no stream may still be using the block
+  cudaFreeAsync(p, d.stream);
+}
+
 
 thread_local std::string g_last_error;
 

@@ -537,6 +537,9 @@ static void cols_product(stgp_ctx* ctx, int m, long long n, const double* A, int
   oz->Bs.ensure(sl);
   oz->sB.ensure(static_cast<size_t>(nch) * m);
   const dim3 grid(static_cast<unsigned>((n + kSlCols - 1) / kSlCols), (m + 31) / 32);
+  // the slicer covers every chunk to its full length L: the padding columns [n, nch L) of the
+  // last chunk enter the int8 products and must be zero digits (reused buffers hold old data)
+  const dim3 sgrid(static_cast<unsigned>(static_cast<long long>(nch) * L / kSlCols), (m + 31) / 32);
   oz->maxbits.ensure(static_cast<size_t>(nch) * m);
   auto slice = [&](const double* X, int ldx, const double* f, int8_t* fwd, int8_t* rev, double* sc) {
     STGP_CUDA(cudaMemsetAsync(oz->maxbits.get(), 0, sizeof(unsigned long long) * nch * m, st));
@@ -546,7 +549,7 @@ static void cols_product(stgp_ctx* ctx, int m, long long n, const double* A, int
                      const int smem = kS * 32 * kSlRow;
                      STGP_CUDA(cudaFuncSetAttribute(slice_cols_kernel<kS>,
                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-                     slice_cols_kernel<kS><<<grid, 256, smem, st>>>(m, n, L, X, ldx, f, oz->maxbits.get(), fwd, rev,
+                     slice_cols_kernel<kS><<<sgrid, 256, smem, st>>>(m, n, L, X, ldx, f, oz->maxbits.get(), fwd, rev,
                                                                      sc);
                    }));
     launched(ctx);

@@ -1049,6 +1049,7 @@ namespace stgp {
 stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vector<double>& zxyt, int m_v,
                                int kind) {
   stgp_neighbors* result = nullptr;
+  auto frees_clk = std::chrono::steady_clock::now();
   {
     if (m_v < 0) config_error("m_v must be >= 0");
     if (m_v > 32) config_error("neighbour search supports m_v <= 32 on the device");
@@ -1424,12 +1425,24 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
                        h[34 + lg]);
       }
     }
-    STGP_CUDA(cudaStreamSynchronize(st));
+    if (std::getenv("STGP_SPIN_SYNC")) {
+      cudaError_t e;
+      while ((e = cudaStreamQuery(st)) == cudaErrorNotReady) {
+      }
+      STGP_CUDA(e);
+    } else {
+      STGP_CUDA(cudaStreamSynchronize(st));
+    }
+    lap("sync");
     prof_collect(ctx);
     result = nb.release();
     lap("finish");
+    frees_clk = std::chrono::steady_clock::now();
   }
   // (W, tiles and stats are released here, after the lap above)
+  if (std::getenv("STGP_DR_HOSTLAPS"))
+    std::fprintf(stderr, "[stgp] d_r phase %-12s %8.2f ms\n", "frees",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - frees_clk).count());
   return result;
 }
 

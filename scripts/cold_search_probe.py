@@ -16,7 +16,7 @@ t0 = time.perf_counter(); ctx.dmma_peak_tflops(); print(f"dmma peak {time.perf_c
 ds = S.SpaceTimeDataset(x, y, t, resp, ctx=ctx)
 ctx.profile(True)
 ind = S.sts_kmeanspp(ds, 1000, 20260203)
-for rep in range(3):
+for rep in range(int(os.environ.get("REPS", "3"))):
     ctx.profile_reset()
     t0 = time.perf_counter(); nb = S.residual_neighbors(ds, theta, ind, 30); dt = time.perf_counter() - t0
     prof = {k: round(v[0], 1) for k, v in ctx.profile_all().items()}
