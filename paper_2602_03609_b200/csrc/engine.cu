@@ -217,8 +217,14 @@ LagTable lag_view(const DevLagTable& d) { return LagTable{d.lagid.get(), d.tf.ge
 
 ProfRegion::ProfRegion(stgp_ctx* c, const char* n) : ctx(c), name(n) {
   if (!ctx->prof) return;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
+  for (cudaEvent_t* e : {&e0, &e1}) {
+    if (!ctx->prof_events.empty()) {
+      *e = ctx->prof_events.back();
+      ctx->prof_events.pop_back();
+    } else {
+      cudaEventCreate(e);
+    }
+  }
   cudaEventRecord(e0, ctx->stream);
 }
 ProfRegion::~ProfRegion() {
@@ -234,8 +240,8 @@ void prof_collect(stgp_ctx* ctx) {
     auto& acc = ctx->prof_acc[p.first];
     acc.first += ms;
     acc.second += 1;
-    cudaEventDestroy(p.second.first);
-    cudaEventDestroy(p.second.second);
+    ctx->prof_events.push_back(p.second.first);
+    ctx->prof_events.push_back(p.second.second);
   }
   ctx->prof_pending.clear();
 }
@@ -620,6 +626,8 @@ void stgp_ctx_destroy(stgp_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   stgp_ctx_release_comm(ctx);
   stgp::ozaki_release(ctx);
+  stgp::prof_collect(ctx);
+  for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
   if (ctx->cublas) cublasDestroy(ctx->cublas);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;

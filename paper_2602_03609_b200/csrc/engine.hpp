@@ -73,6 +73,7 @@ struct stgp_ctx {
   bool prof = false;
   std::map<std::string, std::pair<double, int64_t>> prof_acc;
   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
+  std::vector<cudaEvent_t> prof_events;  // collected events, reused (no driver calls per region)
 };
 
 namespace stgp {
