@@ -289,7 +289,7 @@ def main():
         nn_s = time.perf_counter() - t0
         knn_ms = ctx.profile_get("knn_dr")[0] + ctx.profile_get("dr_whiten")[0]
         warm = []
-        for _ in range(3):  # warm repeats (identical sets); wall times vary with host-side allocation stalls
+        for _ in range(3):  # warm repeats (identical sets)
             t0 = time.perf_counter()
             nb = S.residual_neighbors(ds, theta, ind, args.m_v)
             warm.append(time.perf_counter() - t0)
