@@ -18,6 +18,7 @@
 #include <cstring>
 #include <memory>
 #include <set>
+#include <type_traits>
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_fp16.h>
@@ -302,9 +303,11 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
         a0[q] = sOut[(cb + q) * 65 + lane];
         a1[q] = sOut[(cb + q) * 65 + lane + 32];
       }
-      for (int cl = 0; cl < rb; ++cl) {
+      // rows cl < 32 live in a0 (lanes), rows 32.. in a1: two loops without per-step selects, and
+      // the second skips the a0 updates (all predicated off there)
+      auto step = [&](const int cl, auto hi_t) {
+        constexpr bool hi = decltype(hi_t)::value;
         const int own = cl & 31;
-        const bool hi = cl >= 32;
         double mine = 0.0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -317,13 +320,16 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const double wv = __shfl_sync(kFull, wq, q);
-          if (lane > cl) a0[q] = __fma_rn(l0, wv, a0[q]);
+          if (!hi && lane > cl) a0[q] = __fma_rn(l0, wv, a0[q]);
           if (lane + 32 > cl) a1[q] = __fma_rn(l1, wv, a1[q]);
           if (lane == own) {
             if (hi) a1[q] = wv; else a0[q] = wv;
           }
         }
-      }
+      };
+      const int rlo = min(rb, 32);
+      for (int cl = 0; cl < rlo; ++cl) step(cl, std::false_type{});
+      for (int cl = 32; cl < rb; ++cl) step(cl, std::true_type{});
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         sOut[(cb + q) * 65 + lane] = a0[q];
