@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
   double* ring = sm;                                  // kWStages x [L 64 x kWKS | W 64 x kWKS]
   double* sOut = sm;                                  // [64 cols][65] (aliases the ring)
   double* sD = sm + kWStages * kWStageDoubles;        // [64][65]
-  double* wrow = sD + 64 * 65;                        // [2][64]
+  double* wrow = sD + 64 * 65;                        // [2][64]; [8] per warp in the diagonal solve
   double* sx = wrow + 2 * 64;                         // [64]
   double* sy = sx + 64;                               // [64]
   int* st = reinterpret_cast<int*>(sy + 64);
@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
     // block-wide barrier per step.  Row r still receives -L[r][c] w_c for c = r0.. in order.
     {
       const int cb = 8 * wid;
+      double* xw = wrow + 8 * wid;  // [8] per warp
       double a0[8], a1[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -308,13 +309,16 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
       auto step = [&](const int cl, auto hi_t) {
         constexpr bool hi = decltype(hi_t)::value;
         const int own = cl & 31;
-        double mine = 0.0;
+        // row cl's 8 values reach lanes 0..7 through the warp's shared slot (4 vector stores and
+        // one load instead of 8 shuffles and 8 selects)
+        if (lane == own) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const double tq = __shfl_sync(kFull, hi ? a1[q] : a0[q], own);
-          if (lane == q) mine = tq;
+          for (int q = 0; q < 8; q += 2)
+            reinterpret_cast<double2*>(xw)[q / 2] = hi ? make_double2(a1[q], a1[q + 1]) : make_double2(a0[q], a0[q + 1]);
         }
-        const double wq = lane < 8 ? __ddiv_rn(mine, sD[cl * 65 + cl]) : 0.0;
+        __syncwarp();
+        const double wq = lane < 8 ? __ddiv_rn(xw[lane], sD[cl * 65 + cl]) : 0.0;
+        __syncwarp();
         const double l0 = lane > cl ? -sD[lane * 65 + cl] : 0.0;
         const double l1 = lane + 32 > cl && lane + 32 < rb ? -sD[(lane + 32) * 65 + cl] : 0.0;
 #pragma unroll
