@@ -297,7 +297,8 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
     // block-wide barrier per step.  Row r still receives -L[r][c] w_c for c = r0.. in order.
     {
       const int cb = 8 * wid;
-      double* xw = wrow + 8 * wid;  // [8] per warp
+      double* xw = wrow + 8 * wid;       // [8] per warp: row cl's values
+      double* xq = wrow + 64 + 8 * wid;  // [8] per warp: their quotients
       double a0[8], a1[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -317,13 +318,20 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
             reinterpret_cast<double2*>(xw)[q / 2] = hi ? make_double2(a1[q], a1[q + 1]) : make_double2(a0[q], a0[q + 1]);
         }
         __syncwarp();
-        const double wq = lane < 8 ? __ddiv_rn(xw[lane], sD[cl * 65 + cl]) : 0.0;
+        if (lane < 8) xq[lane] = __ddiv_rn(xw[lane], sD[cl * 65 + cl]);
         __syncwarp();
+        double wqv[8];
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+          const double2 v2 = reinterpret_cast<const double2*>(xq)[q / 2];
+          wqv[q] = v2.x;
+          wqv[q + 1] = v2.y;
+        }
         const double l0 = lane > cl ? -sD[lane * 65 + cl] : 0.0;
         const double l1 = lane + 32 > cl && lane + 32 < rb ? -sD[(lane + 32) * 65 + cl] : 0.0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const double wv = __shfl_sync(kFull, wq, q);
+          const double wv = wqv[q];
           if (!hi && lane > cl) a0[q] = __fma_rn(l0, wv, a0[q]);
           if (lane + 32 > cl) a1[q] = __fma_rn(l1, wv, a1[q]);
           if (lane == own) {
