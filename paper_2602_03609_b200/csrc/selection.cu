@@ -318,7 +318,11 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
             reinterpret_cast<double2*>(xw)[q / 2] = hi ? make_double2(a1[q], a1[q + 1]) : make_double2(a0[q], a0[q + 1]);
         }
         __syncwarp();
-        if (lane < 8) xq[lane] = __ddiv_rn(xw[lane], sD[cl * 65 + cl]);
+        if (lane < 8) {  // lane q divides column cb + q's row cl and writes the result in place
+          const double w = __ddiv_rn(xw[lane], sD[cl * 65 + cl]);
+          xq[lane] = w;
+          sOut[(cb + lane) * 65 + cl] = w;
+        }
         __syncwarp();
         double wqv[8];
 #pragma unroll
@@ -334,19 +338,11 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
           const double wv = wqv[q];
           if (!hi && lane > cl) a0[q] = __fma_rn(l0, wv, a0[q]);
           if (lane + 32 > cl) a1[q] = __fma_rn(l1, wv, a1[q]);
-          if (lane == own) {
-            if (hi) a1[q] = wv; else a0[q] = wv;
-          }
         }
       };
       const int rlo = min(rb, 32);
       for (int cl = 0; cl < rlo; ++cl) step(cl, std::false_type{});
       for (int cl = 32; cl < rb; ++cl) step(cl, std::true_type{});
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        sOut[(cb + q) * 65 + lane] = a0[q];
-        sOut[(cb + q) * 65 + lane + 32] = a1[q];
-      }
     }
     __syncthreads();
     for (int e = t; e < 64 * 64; e += kWthreads) {  // coalesced column segments
