@@ -233,23 +233,23 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
         }
     const int nch = r0 / kWKC;
     if (nch > 0) {
-      auto stage = [&](int ch) {
-        double* sL = ring + static_cast<size_t>(ch % kWStages) * kWStageDoubles;
-        double* sW = sL + kWB * kWKS;
+      // per-thread source rows and shared offsets, fixed over the chunks of this row block
+      const double* gsrc[kPieces / kWthreads];
+      int soff[kPieces / kWthreads];
 #pragma unroll
-        for (int it = 0; it < kPieces / kWthreads; ++it) {
-          const int pc = t + it * kWthreads;
-          const int which = pc / (kWB * (kWKC / 2));  // 0: L rows, 1: W columns
-          const int rem = pc % (kWB * (kWKC / 2));
-          const int rr = rem / (kWKC / 2), piece = rem % (kWKC / 2);
-          if (which == 0) {
-            const int r = min(r0 + rr, M - 1);
-            cp_async16(sL + rr * kWKS + 2 * piece, Lp + static_cast<size_t>(r) * ldL + ch * kWKC + 2 * piece);
-          } else {
-            const int i = i0 + (rr < nc ? rr : 0);
-            cp_async16(sW + rr * kWKS + 2 * piece, W + static_cast<size_t>(i) * ldm + ch * kWKC + 2 * piece);
-          }
-        }
+      for (int it = 0; it < kPieces / kWthreads; ++it) {
+        const int pc = t + it * kWthreads;
+        const int which = pc / (kWB * (kWKC / 2));  // 0: L rows, 1: W columns
+        const int rem = pc % (kWB * (kWKC / 2));
+        const int rr = rem / (kWKC / 2), piece = rem % (kWKC / 2);
+        soff[it] = (which ? kWB * kWKS : 0) + rr * kWKS + 2 * piece;
+        gsrc[it] = which == 0 ? Lp + static_cast<size_t>(min(r0 + rr, M - 1)) * ldL + 2 * piece
+                              : W + static_cast<size_t>(i0 + (rr < nc ? rr : 0)) * ldm + 2 * piece;
+      }
+      auto stage = [&](int ch) {
+        double* base = ring + static_cast<size_t>(ch % kWStages) * kWStageDoubles;
+#pragma unroll
+        for (int it = 0; it < kPieces / kWthreads; ++it) cp_async16(base + soff[it], gsrc[it] + ch * kWKC);
       };
 #pragma unroll
       for (int ch = 0; ch < kWStages - 1; ++ch) {
