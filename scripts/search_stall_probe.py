@@ -1,3 +1,5 @@
+"""Repeated d_r searches at cfg4 with CPU time and context switches per call: host stalls inside
+the driver show up as wall time without CPU time (STGP_POOL=0 to compare)."""
 import os, sys, time, resource, threading
 sys.path.insert(0, ".")
 import paper_2602_03609_b200 as S
