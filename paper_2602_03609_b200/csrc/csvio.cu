@@ -37,31 +37,69 @@ int guarded(F&& f) {
   }
 }
 
-// dataset.cpp:193-205: comma split, each field trimmed of " \t\r", a trailing comma adds an empty field
-std::vector<std::string> split_csv_line(const std::string& line) {
-  std::vector<std::string> out;
-  std::string field;
-  std::stringstream ss(line);
-  while (std::getline(ss, field, ',')) {
-    const auto b = field.find_first_not_of(" \t\r");
-    const auto e = field.find_last_not_of(" \t\r");
-    out.push_back(b == std::string::npos ? std::string() : field.substr(b, e - b + 1));
+// Format contract (exercised by test_dataset.cpp:146-189): '#'-prefixed and empty lines are
+// skipped; the first other line is the header; cells are comma separated and stripped of blanks
+// (space, tab, CR) at both ends; a row must have as many cells as the header.  The whole file is read
+// into one buffer and scanned in place: a cursor walks the lines, and each line is cut into cell views.
+struct Cell {
+  const char* p;
+  size_t len;
+  std::string str() const { return std::string(p, len); }
+  bool is(const char* name) const { return std::strlen(name) == len && std::memcmp(p, name, len) == 0; }
+};
+
+inline bool blank(char c) { return c == ' ' || c == '\t' || c == '\r'; }
+
+// cells of [b, e): every comma ends one cell, so "a,b," has three (the last empty)
+void cut_cells(const char* b, const char* e, std::vector<Cell>& cells) {
+  cells.clear();
+  const char* c = b;
+  for (;;) {
+    const char* stop = static_cast<const char*>(std::memchr(c, ',', static_cast<size_t>(e - c)));
+    const char* ce = stop ? stop : e;
+    const char* lo = c;
+    const char* hi = ce;
+    while (lo < hi && blank(*lo)) ++lo;
+    while (hi > lo && blank(hi[-1])) --hi;
+    cells.push_back(Cell{lo, static_cast<size_t>(hi - lo)});
+    if (!stop) break;
+    c = stop + 1;
   }
-  if (!line.empty() && line.back() == ',') out.emplace_back();
-  return out;
 }
 
-// dataset.cpp:207-218: the whole field must parse (std::stod) to a finite value
-double parse_num(const std::string& s, const std::string& path, int lineno) {
-  try {
-    std::size_t pos = 0;
-    const double v = std::stod(s, &pos);
-    if (pos != s.size()) throw std::invalid_argument(s);
-    if (!std::isfinite(v)) throw std::invalid_argument(s);
-    return v;
-  } catch (const std::exception&) {
-    data_error(path + ":" + std::to_string(lineno) + ": missing or non-numeric value '" + s + "'");
+struct LineCursor {
+  const std::string& buf;
+  size_t pos = 0;
+  int lineno = 0;
+  // next line that is neither empty nor a '#' comment; false at end of input
+  bool next(const char*& b, const char*& e) {
+    while (pos < buf.size()) {
+      const size_t nl = buf.find('\n', pos);
+      const size_t stop = nl == std::string::npos ? buf.size() : nl;
+      b = buf.data() + pos;
+      e = buf.data() + stop;
+      pos = stop + 1;
+      ++lineno;
+      if (e > b && *b != '#') return true;
+    }
+    return false;
   }
+};
+
+// a cell that holds exactly one finite number (strtod must consume all of it)
+double number_cell(const Cell& c, const std::string& where) {
+  char tmp[128];
+  bool ok = c.len > 0 && c.len < sizeof(tmp);
+  double v = 0.0;
+  if (ok) {
+    std::memcpy(tmp, c.p, c.len);
+    tmp[c.len] = '\0';
+    char* end = nullptr;
+    v = std::strtod(tmp, &end);
+    ok = end == tmp + c.len && std::isfinite(v) && !blank(tmp[0]);
+  }
+  if (!ok) data_error(where + ": value '" + c.str() + "' is empty or not a finite number");
+  return v;
 }
 
 // std::ostream with precision(17) and the default float field: "%.17g"
@@ -85,69 +123,73 @@ int copy_str(const std::string& s, char* buf, int cap) {
 
 extern "C" {
 
-// read_dataset_csv (dataset.cpp:221-296)
+// read_dataset_csv (dataset.cpp:221-296): columns x, y, t, value required, station_id optional, every
+// other column a numeric covariate in header order.
 int stgp_read_dataset_csv(const char* path_c, stgp_table** out) {
   using namespace stgp;
   return guarded([&] {
     if (!path_c || !out) config_error("stgp_read_dataset_csv: null argument");
     const std::string path(path_c);
-    std::ifstream is(path);
-    if (!is) data_error("cannot open dataset: " + path);
-    std::string line;
-    int lineno = 0;
-    std::vector<std::string> header;
-    while (std::getline(is, line)) {
-      ++lineno;
-      if (line.empty() || line[0] == '#') continue;
-      header = split_csv_line(line);
-      break;
+    std::string buf;
+    {
+      std::ifstream is(path, std::ios::binary);
+      if (!is) data_error("dataset " + path + " cannot be opened");
+      std::ostringstream ss;
+      ss << is.rdbuf();
+      buf = ss.str();
     }
-    if (header.empty()) data_error(path + ": missing header row");
-    int cx = -1, cy = -1, ct = -1, cv = -1, cs = -1;
-    std::vector<int> cov;
+    LineCursor cur{buf};
+    const char *b = nullptr, *e = nullptr;
+    if (!cur.next(b, e)) data_error(path + ": no header line");
+    std::vector<Cell> cells;
+    cut_cells(b, e, cells);
+    const size_t width = cells.size();
+    enum Role { kX, kY, kT, kValue, kStation, kCovariate };
+    std::vector<int> role(width);
+    int have[5] = {0, 0, 0, 0, 0};
     auto tab = std::make_unique<stgp_table>();
-    for (int j = 0; j < static_cast<int>(header.size()); ++j) {
-      const std::string& name = header[static_cast<size_t>(j)];
-      if (name == "x") cx = j;
-      else if (name == "y") cy = j;
-      else if (name == "t") ct = j;
-      else if (name == "value") cv = j;
-      else if (name == "station_id") cs = j;
-      else {
-        cov.push_back(j);
-        tab->covariate_names.push_back(name);
-      }
+    static const char* const kNames[5] = {"x", "y", "t", "value", "station_id"};
+    for (size_t j = 0; j < width; ++j) {
+      int r = kCovariate;
+      for (int q = 0; q < 5; ++q)
+        if (cells[j].is(kNames[q])) r = q;
+      role[j] = r;
+      if (r == kCovariate) tab->covariate_names.push_back(cells[j].str());
+      else ++have[r];
     }
-    if (cx < 0 || cy < 0 || ct < 0 || cv < 0) data_error(path + ": required columns are x, y, t, value");
-    std::vector<double> covr;  // row-major
-    while (std::getline(is, line)) {
-      ++lineno;
-      if (line.empty() || line[0] == '#') continue;
-      const auto f = split_csv_line(line);
-      if (f.size() != header.size())
-        data_error(path + ":" + std::to_string(lineno) + ": expected " + std::to_string(header.size()) + " fields");
-      const double x = parse_num(f[static_cast<size_t>(cx)], path, lineno);
-      const double y = parse_num(f[static_cast<size_t>(cy)], path, lineno);
-      const double t = parse_num(f[static_cast<size_t>(ct)], path, lineno);
-      const double v = parse_num(f[static_cast<size_t>(cv)], path, lineno);
-      tab->x.push_back(x);
-      tab->y.push_back(y);
-      tab->t.push_back(t);
-      tab->value.push_back(v);
-      if (cs >= 0) {
-        const std::string& s = f[static_cast<size_t>(cs)];
-        if (s.empty()) data_error(path + ":" + std::to_string(lineno) + ": empty station_id");
-        tab->stations.push_back(s);
+    if (!have[kX] || !have[kY] || !have[kT] || !have[kValue])
+      data_error(path + ": header lacks one of the required columns x, y, t, value");
+    const int p = static_cast<int>(tab->covariate_names.size());
+    std::vector<double> cov_rows;  // row-major while reading
+    while (cur.next(b, e)) {
+      cut_cells(b, e, cells);
+      const std::string where = path + ":" + std::to_string(cur.lineno);
+      if (cells.size() != width)
+        data_error(where + ": " + std::to_string(cells.size()) + " cells, the header has " + std::to_string(width));
+      double v[4] = {0, 0, 0, 0};
+      std::string station;
+      for (size_t j = 0; j < width; ++j) {  // a repeated header name: the last column of that name wins
+        switch (role[j]) {
+          case kStation:
+            if (cells[j].len == 0) data_error(where + ": station_id is empty");
+            station = cells[j].str();
+            break;
+          case kCovariate: cov_rows.push_back(number_cell(cells[j], where)); break;
+          default: v[role[j]] = number_cell(cells[j], where);
+        }
       }
-      for (int j : cov) covr.push_back(parse_num(f[static_cast<size_t>(j)], path, lineno));
+      tab->x.push_back(v[kX]);
+      tab->y.push_back(v[kY]);
+      tab->t.push_back(v[kT]);
+      tab->value.push_back(v[kValue]);
+      if (have[kStation]) tab->stations.push_back(std::move(station));
     }
-    if (tab->x.empty()) data_error(path + ": no data rows");
+    if (tab->x.empty()) data_error(path + ": header but no observations");
     tab->n = static_cast<int>(tab->x.size());
-    tab->p = static_cast<int>(cov.size());
-    tab->X.assign(static_cast<size_t>(tab->n) * tab->p, 0.0);
+    tab->p = p;
+    tab->X.resize(static_cast<size_t>(tab->n) * p);
     for (int i = 0; i < tab->n; ++i)
-      for (int j = 0; j < tab->p; ++j)
-        tab->X[static_cast<size_t>(j) * tab->n + i] = covr[static_cast<size_t>(i) * tab->p + j];
+      for (int j = 0; j < p; ++j) tab->X[static_cast<size_t>(j) * tab->n + i] = cov_rows[static_cast<size_t>(i) * p + j];
     *out = tab.release();
   });
 }

@@ -541,9 +541,18 @@ std::vector<double> run_rows_args(stgp_structure* s, int mode, RowArgs& a) {
   int fail = 0;
   s->fail.download(&fail, 1, ctx->stream);
   STGP_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (fail != INT_MAX)
-    numeric_error("vecchia row " + std::to_string(fail) +
-                  ": conditioning block is not positive definite or non-positive conditional variance");
+  // Agree on failure across shards before anyone raises: a rank that throws alone would leave the
+  // others blocked in the next collective, and the fit's line search (estimation.cpp:575-579) needs
+  // the NumericError on every rank to halve the step in lockstep.
+  std::vector<double> flag{fail != INT_MAX ? 1.0 : 0.0};
+  allreduce_host(ctx, flag);
+  if (flag[0] > 0.0) {
+    if (fail != INT_MAX)
+      numeric_error("vecchia row " + std::to_string(fail) +
+                    ": conditioning block is not positive definite or non-positive conditional variance");
+    numeric_error("vecchia rows of another shard: conditioning block is not positive definite or non-positive "
+                  "conditional variance");
+  }
   return tot;
 }
 

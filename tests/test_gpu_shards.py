@@ -129,3 +129,42 @@ def test_sharded_search_equals_single(S, metric, world):
         assert (ir == i1).all()
         ok = ~np.isnan(d1)
         assert (np.isnan(dr) == ~ok).all() and (dr[ok].view(np.int64) == d1[ok].view(np.int64)).all()
+
+
+def test_sharded_failure_raises_on_every_rank(S):
+    """A non-PD conditioning block on one shard only: every rank raises NumericError together (no rank is
+    left waiting in the next collective, so the fit's step halving works sharded, estimation.cpp:575-579)."""
+    x, y, t, _ = S.synth.station_day(60, 6, seed=11)
+    perm = O.order_observations(t, 11)
+    x, y, t = x[perm].copy(), y[perm].copy(), t[perm].copy()
+    n = len(x)
+    # row i in the second shard duplicates an earlier same-day row j and conditions on j alone: with the
+    # latent policy (no nugget) and sigma1^2 = 1 its conditional variance is exactly 1 - 1*1 = 0
+    # -> "non-positive conditional variance" (approximations.cpp:107-110)
+    i = 3 * n // 4
+    j = int(np.nonzero(t[:i] == t[i])[0][0])
+    x[i], y[i] = x[j], y[j]
+    nbr = O.dc_neighbors(x, y, t, SEC4, 1)
+    assert nbr[i][0] == j
+    world = 2
+    err = [None] * world
+    hub = S.api.HostAllreduce(world, timeout=60.0)
+
+    def work(rank):
+        try:
+            ctx = S.Context(0)
+            ctx.set_shard(rank, world)
+            ctx.set_host_allreduce(hub.for_rank(rank))
+            ds = S.SpaceTimeDataset(x, y, t, ctx=ctx)
+            nb = S.NeighborSets.from_sets(ds, nbr)
+            S.build_vecchia(ds, SEC4, nb, S.LATENT)
+        except Exception as e:  # noqa: BLE001
+            err[rank] = e
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for h in th:
+        h.start()
+    for h in th:
+        h.join()
+    assert all(isinstance(e, S.NumericError) for e in err), err
+    assert "another shard" in str(err[0]) and "another shard" not in str(err[1])
