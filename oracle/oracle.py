@@ -273,6 +273,15 @@ class OracleModel:
         _chk(lib().orc_nll_grad(C.byref(self.m), _p(yv), p, _p(Xf), _p(b), _p(g)))
         return g
 
+    def nll_grad_scale(self, yv, X=None, beta=None):
+        """(gradient, scale): scale[k] = sum over rows of |row contribution to component k| (the
+        conditioning of the gradient sum; parity tolerances are 1e-8 * scale)."""
+        p, Xf, b = self._xb(self.n, X, beta)
+        yv = _f64(yv)
+        g, sc = np.zeros(7), np.zeros(7)
+        _chk(lib().orc_nll_grad_scale(C.byref(self.m), _p(yv), p, _p(Xf), _p(b), _p(g), _p(sc)))
+        return g, sc
+
     def gls_beta(self, yv, X) -> np.ndarray:
         X = np.asfortranarray(np.asarray(X, dtype=np.float64).reshape(self.n, -1))
         yv = _f64(yv)
@@ -495,3 +504,19 @@ def fit_gaussian(x, y, t, yv, X, method, m_v, m, seed, nu, init, max_iterations=
         lb.push(zn - z, gnew - g)
         z, f, g = zn, fnew, gnew
     return _theta_of(z, nu), beta, f, conv, trace
+
+
+def dr_neighbors_rows(x, y, t, theta, Z, m_v: int, rows=None, with_dist: bool = False, by_dist: bool = False):
+    """residual_neighbors for the given query rows (time-ordered data) with certified exact pruning
+    (orc_dr_neighbors_rows); rows None = all rows.  Equal to dr_neighbors on those rows.  by_dist: each
+    row's indices in (distance, index) order instead of ascending."""
+    x, y, t = _f64(x), _f64(y), _f64(t)
+    Z = np.asarray(Z, dtype=np.float64).reshape(-1, 3)
+    zx, zy, zt = _f64(Z[:, 0]), _f64(Z[:, 1]), _f64(Z[:, 2])
+    r = None if rows is None else np.ascontiguousarray(rows, dtype=np.int32)
+    nq = len(x) if r is None else len(r)
+    out = np.zeros((nq, m_v), dtype=np.int32)
+    dist = np.zeros((nq, m_v)) if with_dist else None
+    _chk(lib().orc_dr_neighbors_rows(len(x), _p(x), _p(y), _p(t), C.byref(params(theta)), len(Z), _p(zx), _p(zy),
+                                     _p(zt), m_v, nq, _p(r), _p(out), _p(dist), int(by_dist)))
+    return (out, dist) if with_dist else out

@@ -928,7 +928,9 @@ inline void add_pair(const Kernel& k, const Pt& a, const Pt& b, double w, double
 }
 
 // nll_grad Vecchia (approximations.cpp:403-493)
-void grad_vecchia(const Model& s, const std::vector<double>& r, double* grad) {
+// scale (nullable): per component, the sum over rows of |row contribution| -- the conditioning of the
+// gradient sum, the yardstick of the parity tolerance
+void grad_vecchia(const Model& s, const std::vector<double>& r, double* grad, double* scale) {
   if (s.policy != 1) throw NumericError("nll_grad: analytic gradient is defined for the observation-policy structure driven by the optimizer");
   const int n = s.n;
   const orc_params& th = s.kernel.th;
@@ -1005,6 +1007,49 @@ void grad_vecchia(const Model& s, const std::vector<double>& r, double* grad) {
   for (int q = 0; q < 7; ++q) grad[q] = 0.0;
   for (int i = 0; i < n; ++i)
     for (int q = 0; q < 7; ++q) grad[q] += part[static_cast<size_t>(i) * 7 + q];
+  if (scale) {
+    for (int q = 0; q < 7; ++q) scale[q] = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int q = 0; q < 7; ++q) scale[q] += std::abs(part[static_cast<size_t>(i) * 7 + q]);
+  }
+}
+
+// U-pair and Sigma_m-pair kernel-gradient sums shared by FITC and VIF: sum_{j,i} om(j,i) dk(z_j, p_i) and
+// sum_{j1,j2} wsig(j1,j2) dk(z_j1, z_j2); each data column i and each inducing row j1 is one contribution
+// to the scale.
+template <class Om>
+void lowrank_pairs(const Model& s, int M, Om&& om, const Mat& wsig, double* grad, double* scale) {
+  const int n = s.n;
+  const int T = std::max(1, omp_get_max_threads());
+  std::vector<double> loc(static_cast<size_t>(T) * 14, 0.0);
+#pragma omp parallel
+  {
+    double* g = &loc[static_cast<size_t>(omp_get_thread_num()) * 14];
+#pragma omp for schedule(static)
+    for (int i = 0; i < n; ++i) {
+      double gi[7] = {0, 0, 0, 0, 0, 0, 0};
+      for (int j = 0; j < M; ++j) add_pair(s.kernel, s.basis.z[static_cast<size_t>(j)], s.pts[static_cast<size_t>(i)], om(j, i), gi);
+      for (int q = 0; q < 7; ++q) {
+        g[q] += gi[q];
+        g[7 + q] += std::abs(gi[q]);
+      }
+    }
+  }
+  for (int tt = 0; tt < T; ++tt)
+    for (int q = 0; q < 7; ++q) {
+      grad[q] += loc[static_cast<size_t>(tt) * 14 + q];
+      if (scale) scale[q] += loc[static_cast<size_t>(tt) * 14 + 7 + q];
+    }
+  for (int j1 = 0; j1 < M; ++j1) {
+    double gj[7] = {0, 0, 0, 0, 0, 0, 0};
+    add_pair(s.kernel, s.basis.z[static_cast<size_t>(j1)], s.basis.z[static_cast<size_t>(j1)], wsig(j1, j1), gj);
+    for (int j2 = 0; j2 < j1; ++j2)
+      add_pair(s.kernel, s.basis.z[static_cast<size_t>(j1)], s.basis.z[static_cast<size_t>(j2)], wsig(j1, j2) + wsig(j2, j1), gj);
+    for (int q = 0; q < 7; ++q) {
+      grad[q] += gj[q];
+      if (scale) scale[q] += std::abs(gj[q]);
+    }
+  }
 }
 
 // helper: Y = Cholesky-solve of each column (M x n)
@@ -1022,7 +1067,7 @@ Mat chol_lsolve_cols(const Chol& c, const Mat& B) {
 }
 
 // nll_grad FITC (approximations.cpp:495-571)
-void grad_fitc(const Model& s, const std::vector<double>& r, double* grad) {
+void grad_fitc(const Model& s, const std::vector<double>& r, double* grad, double* scale) {
   const int n = s.n, M = s.basis.m();
   const Mat& U = s.U;
   std::vector<double> lam_inv(static_cast<size_t>(n)), rl(static_cast<size_t>(n));
@@ -1095,36 +1140,30 @@ void grad_fitc(const Model& s, const std::vector<double>& r, double* grad) {
       wsig(a, b) = -0.5 * W2(a, b) + 0.5 * (Pa[static_cast<size_t>(a)] * Pa[static_cast<size_t>(b)]) + acc;
     }
   for (int q = 0; q < 7; ++q) grad[q] = 0.0;
-  double phisum = 0.0;
-  for (int i = 0; i < n; ++i) phisum += phi[static_cast<size_t>(i)];
+  if (scale)
+    for (int q = 0; q < 7; ++q) scale[q] = 0.0;
+  double phisum = 0.0, phiabs = 0.0;
+  for (int i = 0; i < n; ++i) {
+    phisum += phi[static_cast<size_t>(i)];
+    phiabs += std::abs(phi[static_cast<size_t>(i)]);
+  }
   grad[0] += phisum;
   grad[1] += phisum;
-  const int T = std::max(1, omp_get_max_threads());
-  std::vector<double> loc(static_cast<size_t>(T) * 7, 0.0);
-#pragma omp parallel
-  {
-    double* g = &loc[static_cast<size_t>(omp_get_thread_num()) * 7];
-#pragma omp for schedule(static)
-    for (int i = 0; i < n; ++i)
-      for (int j = 0; j < M; ++j) {
-        const double om = K2(j, i) - Pa[static_cast<size_t>(j)] * alpha[static_cast<size_t>(i)] - P(j, i) * (2.0 * phi[static_cast<size_t>(i)]);
-        add_pair(s.kernel, s.basis.z[static_cast<size_t>(j)], s.pts[static_cast<size_t>(i)], om, g);
-      }
+  if (scale) {
+    scale[0] += phiabs;
+    scale[1] += phiabs;
   }
-  for (int t = 0; t < T; ++t)
-    for (int q = 0; q < 7; ++q) grad[q] += loc[static_cast<size_t>(t) * 7 + q];
-  for (int j1 = 0; j1 < M; ++j1) {
-    add_pair(s.kernel, s.basis.z[static_cast<size_t>(j1)], s.basis.z[static_cast<size_t>(j1)], wsig(j1, j1), grad);
-    for (int j2 = 0; j2 < j1; ++j2)
-      add_pair(s.kernel, s.basis.z[static_cast<size_t>(j1)], s.basis.z[static_cast<size_t>(j2)], wsig(j1, j2) + wsig(j2, j1), grad);
-  }
+  auto om = [&](int j, int i) {
+    return K2(j, i) - Pa[static_cast<size_t>(j)] * alpha[static_cast<size_t>(i)] - P(j, i) * (2.0 * phi[static_cast<size_t>(i)]);
+  };
+  lowrank_pairs(s, M, om, wsig, grad, scale);
 }
 
 // nll_grad VIF (approximations.cpp:573-744).  Phi is kept as per-row dense
 // (k+1)^2 blocks instead of one sparse n x n matrix; the direct pass and P*Phi
 // then sum the same entries (the reference's lower-triangle + coeff(b,a) fold
 // equals the full symmetric sum because d k is symmetric).
-void grad_vif(const Model& s, const std::vector<double>& r, double* grad) {
+void grad_vif(const Model& s, const std::vector<double>& r, double* grad, double* scale) {
   require_obs(s, "nll_grad");
   const int n = s.n, M = s.basis.m();
   const orc_params& th = s.kernel.th;
@@ -1243,6 +1282,11 @@ void grad_vif(const Model& s, const std::vector<double>& r, double* grad) {
     }
     for (int i = 0; i < n; ++i)
       for (int q = 0; q < 7; ++q) grad[q] += part[static_cast<size_t>(i) * 7 + q];
+    if (scale) {
+      for (int q = 0; q < 7; ++q) scale[q] = 0.0;
+      for (int i = 0; i < n; ++i)
+        for (int q = 0; q < 7; ++q) scale[q] += std::abs(part[static_cast<size_t>(i) * 7 + q]);
+    }
   }
   if (M == 0) return;
   const Mat P = chol_solve_cols(s.basis.llt, U);
@@ -1292,22 +1336,7 @@ void grad_vif(const Model& s, const std::vector<double>& r, double* grad) {
     const Mat Sinv = chol_solve_cols(s.basis.llt, I);
     for (size_t e = 0; e < wsig.a.size(); ++e) wsig.a[e] += 0.5 * (Minv.a[e] - Sinv.a[e]);
   }
-  const int T = std::max(1, omp_get_max_threads());
-  std::vector<double> loc(static_cast<size_t>(T) * 7, 0.0);
-#pragma omp parallel
-  {
-    double* g = &loc[static_cast<size_t>(omp_get_thread_num()) * 7];
-#pragma omp for schedule(static)
-    for (int i = 0; i < n; ++i)
-      for (int j = 0; j < M; ++j) add_pair(s.kernel, s.basis.z[static_cast<size_t>(j)], s.pts[static_cast<size_t>(i)], omega(j, i), g);
-  }
-  for (int tt = 0; tt < T; ++tt)
-    for (int q = 0; q < 7; ++q) grad[q] += loc[static_cast<size_t>(tt) * 7 + q];
-  for (int j1 = 0; j1 < M; ++j1) {
-    add_pair(s.kernel, s.basis.z[static_cast<size_t>(j1)], s.basis.z[static_cast<size_t>(j1)], wsig(j1, j1), grad);
-    for (int j2 = 0; j2 < j1; ++j2)
-      add_pair(s.kernel, s.basis.z[static_cast<size_t>(j1)], s.basis.z[static_cast<size_t>(j2)], wsig(j1, j2) + wsig(j2, j1), grad);
-  }
+  lowrank_pairs(s, M, [&](int j, int i) { return omega(j, i); }, wsig, grad, scale);
 }
 
 // gls_beta (approximations.cpp:752-798)
@@ -1562,6 +1591,172 @@ int orc_dr_neighbors(int n, const double* x, const double* y, const double* t,
   });
 }
 
+// residual_neighbors restricted to chosen query rows, with exact pruning so the large configurations
+// (cfg3: 1e5 rows, cfg4: 1.1e6) are checkable.  The answer is the brute force's (orc_dr_neighbors); a
+// candidate j is skipped only when a certified lower bound on its distance exceeds the query's current
+// m-th distance by a margin, so (d, j) ties cannot be lost:
+//   |rho_r(i,j)| = |k(i,j) - w_i.w_j| <= |k(i,j)| + sum_g |w_i[g]| |w_j[g]|       (Cauchy-Schwarz per group)
+//   |k(i,j)|     <= s1 T(u)^{-(delta+beta)}                                         (Matern <= 1)
+// The groups split the inducing points by time (and spatial cell): a query far from an inducing day has
+// little weight in that day's group.  The computed dot differs from the exact one by at most
+// gamma_M sum_a |w_i[a] w_j[a]|, covered by the (1 + 1e-9) factor; lb^2 carries a 1e-12 margin.
+// Query lists are scanned backwards from i, time block by time block (blocks with a certified bound
+// above the threshold are skipped whole), and candidates that survive every bound are evaluated exactly
+// as in orc_dr_neighbors (kernel value minus the sequential-fma dot, sqrt(max(1 - |rho| / sqrt(r r), 0))).
+static void dr_search_rows(int n, const double* x, const double* y, const double* t, const orc_params* p, int M,
+                           const double* zx, const double* zy, const double* zt, int m_v, int nq, const int32_t* rows,
+                           int32_t* out, double* dist, bool by_dist) {
+  Kernel k(*p);
+  const std::vector<Pt> pts = make_pts(n, x, y, t);
+  if (!time_sorted(pts)) throw ConfigError("dr_search_rows: rows must be time ordered");
+  bool integral = true;  // integer lags: the table equals the live factors bit for bit (covariance.cpp:115-123)
+  double tmin = pts[0].t, tmax = pts[0].t;
+  for (const Pt& q : pts) {
+    integral = integral && q.t == std::nearbyint(q.t);
+    tmin = std::min(tmin, q.t);
+    tmax = std::max(tmax, q.t);
+  }
+  if (integral && tmax - tmin <= 200000.0) k.precompute(static_cast<int>(tmax - tmin) + 1);
+  std::vector<Pt> z;
+  for (int j = 0; j < M; ++j) z.push_back({zx[j], zy[j], zt[j]});
+  // the candidates reach up to the last query row only
+  int top = 0;
+  for (int q = 0; q < nq; ++q) top = std::max(top, rows ? rows[q] + 1 : n);
+  const std::vector<Pt> head(pts.begin(), pts.begin() + top);
+  Basis basis(z, Kernel(*p));  // selection kernel: no lag table (estimation.cpp:200)
+  Mat W(M, top);
+  if (M > 0) cross_and_whiten(basis, Kernel(*p), head, nullptr, W);
+  const double s1 = p->sigma1_2, tol = 1e-7 * s1;
+  // inducing groups: distinct time (<= 8 quantile bins) x 3 x 3 spatial cells
+  std::vector<int> grp(static_cast<size_t>(M), 0);
+  int G = 1;
+  if (M > 0) {
+    std::vector<double> ts;
+    for (const Pt& q : z) ts.push_back(q.t);
+    std::sort(ts.begin(), ts.end());
+    ts.erase(std::unique(ts.begin(), ts.end()), ts.end());
+    const int nt = std::min<int>(8, static_cast<int>(ts.size()));
+    double x0 = zx[0], x1 = zx[0], y0 = zy[0], y1 = zy[0];
+    for (int j = 0; j < M; ++j) {
+      x0 = std::min(x0, zx[j]); x1 = std::max(x1, zx[j]);
+      y0 = std::min(y0, zy[j]); y1 = std::max(y1, zy[j]);
+    }
+    for (int j = 0; j < M; ++j) {
+      const long ti = std::lower_bound(ts.begin(), ts.end(), zt[j]) - ts.begin();
+      const int tb = static_cast<int>(ti * nt / static_cast<long>(ts.size()));
+      const int cx = x1 > x0 ? std::min(2, static_cast<int>(3.0 * (zx[j] - x0) / (x1 - x0))) : 0;
+      const int cy = y1 > y0 ? std::min(2, static_cast<int>(3.0 * (zy[j] - y0) / (y1 - y0))) : 0;
+      grp[static_cast<size_t>(j)] = (tb * 3 + cx) * 3 + cy;
+    }
+    G = nt * 9;
+  }
+  std::vector<double> resid(static_cast<size_t>(top)), gn(static_cast<size_t>(top) * G, 0.0), nrm(static_cast<size_t>(top));
+  std::vector<char> degen(static_cast<size_t>(top));
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < top; ++i) {
+    const double* w = W.col(i);
+    resid[static_cast<size_t>(i)] = M > 0 ? s1 - dot_seq(w, w, M) : s1;
+    degen[static_cast<size_t>(i)] = resid[static_cast<size_t>(i)] <= tol;
+    double* g = &gn[static_cast<size_t>(i) * G];
+    double tot = 0.0;
+    for (int a = 0; a < M; ++a) g[grp[static_cast<size_t>(a)]] += w[a] * w[a];
+    for (int q = 0; q < G; ++q) {
+      tot += g[q];
+      g[q] = std::sqrt(g[q]);
+    }
+    nrm[static_cast<size_t>(i)] = std::sqrt(tot);
+  }
+  // per time block: max |w_j| / sqrt(r_j) and min r_j over its non-degenerate rows
+  const auto blocks = time_blocks(head);
+  const size_t nb = blocks.size();
+  std::vector<double> bA(nb, 0.0), bR(nb, std::numeric_limits<double>::infinity());
+  for (size_t b = 0; b < nb; ++b)
+    for (int j = blocks[b].first; j < blocks[b].second; ++j)
+      if (!degen[static_cast<size_t>(j)]) {
+        bA[b] = std::max(bA[b], nrm[static_cast<size_t>(j)] / std::sqrt(resid[static_cast<size_t>(j)]));
+        bR[b] = std::min(bR[b], resid[static_cast<size_t>(j)]);
+      }
+  const double slack = 1.0 + 1e-9, margin = 1e-12;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int q = 0; q < nq; ++q) {
+    const int i = rows ? rows[q] : q;
+    int32_t* o = out + static_cast<size_t>(q) * m_v;
+    double* od = dist ? dist + static_cast<size_t>(q) * m_v : nullptr;
+    const int want = std::min(m_v, i);
+    for (int a = 0; a < m_v; ++a) {
+      o[a] = -1;
+      if (od) od[a] = std::numeric_limits<double>::quiet_NaN();
+    }
+    if (want <= 0) continue;
+    std::vector<std::pair<double, int>> heap;
+    auto consider = [&](double d, int j) {
+      const std::pair<double, int> c{d, j};
+      if (static_cast<int>(heap.size()) < want) {
+        heap.push_back(c);
+        std::push_heap(heap.begin(), heap.end());
+      } else if (c < heap.front()) {
+        std::pop_heap(heap.begin(), heap.end());
+        heap.back() = c;
+        std::push_heap(heap.begin(), heap.end());
+      }
+    };
+    const Pt& pi = pts[static_cast<size_t>(i)];
+    const bool dq = degen[static_cast<size_t>(i)];
+    const double ri = resid[static_cast<size_t>(i)], sri = std::sqrt(ri), ni = nrm[static_cast<size_t>(i)];
+    const double* gi = &gn[static_cast<size_t>(i) * G];
+    const double* wi = W.col(i);
+    for (long b = static_cast<long>(nb) - 1; b >= 0; --b) {
+      const int s = blocks[static_cast<size_t>(b)].first, e = std::min(blocks[static_cast<size_t>(b)].second, i);
+      if (s >= e) continue;
+      const double kb = s1 * k.factors(std::abs(pi.t - pts[static_cast<size_t>(s)].t)).pow_mE;
+      const bool full = static_cast<int>(heap.size()) == want;
+      if (full && !dq && bR[static_cast<size_t>(b)] < std::numeric_limits<double>::infinity()) {
+        const double dm = heap.front().first;
+        const double ub = (kb / (sri * std::sqrt(bR[static_cast<size_t>(b)])) + ni / sri * bA[static_cast<size_t>(b)]) * slack;
+        // degenerate candidates sit at d = 1 and could only enter at dm == 1, where nothing is pruned
+        if (1.0 - ub - margin > dm * dm) continue;
+      }
+      for (int j = e - 1; j >= s; --j) {
+        if (dq || degen[static_cast<size_t>(j)]) {
+          consider(1.0, j);
+          continue;
+        }
+        const double rj = resid[static_cast<size_t>(j)], den = sri * std::sqrt(rj);
+        if (static_cast<int>(heap.size()) == want) {
+          const double dm2 = heap.front().first * heap.front().first;
+          const double nj = nrm[static_cast<size_t>(j)];
+          if (1.0 - (kb + ni * nj * slack) / den - margin > dm2) continue;
+          const double kij = k(pi, pts[static_cast<size_t>(j)]);
+          if (1.0 - (std::abs(kij) + ni * nj * slack) / den - margin > dm2) continue;
+          const double* gj = &gn[static_cast<size_t>(j) * G];
+          double gb = 0.0;
+          for (int g = 0; g < G; ++g) gb += gi[g] * gj[g];
+          if (1.0 - (std::abs(kij) + gb * slack) / den - margin > dm2) continue;
+          const double rho = kij - (M > 0 ? dot_seq(wi, W.col(j), M) : 0.0);
+          consider(std::sqrt(std::max(1.0 - std::abs(rho) / std::sqrt(ri * rj), 0.0)), j);
+        } else {
+          double rho = k(pi, pts[static_cast<size_t>(j)]);
+          if (M > 0) rho -= dot_seq(wi, W.col(j), M);
+          consider(std::sqrt(std::max(1.0 - std::abs(rho) / std::sqrt(ri * rj), 0.0)), j);
+        }
+      }
+    }
+    std::sort(heap.begin(), heap.end());
+    if (od)
+      for (size_t a = 0; a < heap.size(); ++a) od[a] = heap[a].first;
+    std::vector<int> idx;
+    for (const auto& h : heap) idx.push_back(h.second);
+    if (!by_dist) std::sort(idx.begin(), idx.end());
+    for (size_t a = 0; a < idx.size(); ++a) o[a] = idx[a];
+  }
+}
+
+int orc_dr_neighbors_rows(int n, const double* x, const double* y, const double* t, const orc_params* p, int M,
+                          const double* zx, const double* zy, const double* zt, int m_v, int nq, const int32_t* rows,
+                          int32_t* out, double* dist, int by_dist) {
+  return guarded([&] { dr_search_rows(n, x, y, t, p, M, zx, zy, zt, m_v, nq, rows, out, dist, by_dist != 0); });
+}
+
 // euclidean_neighbors (neighbors.cpp:257-316)
 int orc_euclid_neighbors(int n, const double* x, const double* y, const double* t, int m_v,
                          double ss, double ts, int32_t* out) {
@@ -1728,9 +1923,21 @@ int orc_nll_grad(const orc_model* m, const double* yv, int p, const double* X,
     Model s(m);
     build_model(s, m);
     const std::vector<double> r = residual(m->n, yv, p, X, beta);
-    if (m->kind == 0) grad_vecchia(s, r, grad7);
-    else if (m->kind == 1) grad_fitc(s, r, grad7);
-    else grad_vif(s, r, grad7);
+    if (m->kind == 0) grad_vecchia(s, r, grad7, nullptr);
+    else if (m->kind == 1) grad_fitc(s, r, grad7, nullptr);
+    else grad_vif(s, r, grad7, nullptr);
+  });
+}
+
+int orc_nll_grad_scale(const orc_model* m, const double* yv, int p, const double* X, const double* beta,
+                       double* grad7, double* scale7) {
+  return guarded([&] {
+    Model s(m);
+    build_model(s, m);
+    const std::vector<double> r = residual(m->n, yv, p, X, beta);
+    if (m->kind == 0) grad_vecchia(s, r, grad7, scale7);
+    else if (m->kind == 1) grad_fitc(s, r, grad7, scale7);
+    else grad_vif(s, r, grad7, scale7);
   });
 }
 

@@ -65,6 +65,12 @@ int orc_dr_neighbors(int n, const double* x, const double* y, const double* t,
                      const orc_params* p, int M, const double* zx, const double* zy,
                      const double* zt, int m_v, int32_t* out, double* dist,
                      double* W_out, double* resid_out);
+/* residual_neighbors for chosen query rows (rows == NULL: 0..nq-1) with certified exact pruning; rows must
+ * be time ordered; out / dist are nq x m_v; by_dist != 0 lists each row's indices in (distance, index)
+ * order instead of ascending */
+int orc_dr_neighbors_rows(int n, const double* x, const double* y, const double* t, const orc_params* p, int M,
+                          const double* zx, const double* zy, const double* zt, int m_v, int nq,
+                          const int32_t* rows, int32_t* out, double* dist, int by_dist);
 int orc_euclid_neighbors(int n, const double* x, const double* y, const double* t,
                          int m_v, double space_scale, double time_scale, int32_t* out);
 /* brute-force cover-tree emulation over query subset [q0,q1) only (CPU baseline) */
@@ -88,6 +94,9 @@ int orc_nll(const orc_model* m, const double* yv, int p, const double* X,
             const double* beta, double* out);
 int orc_nll_grad(const orc_model* m, const double* yv, int p, const double* X,
                  const double* beta, double* grad7);
+/* nll_grad plus, per component, the sum over rows of |row contribution| (the tolerance yardstick) */
+int orc_nll_grad_scale(const orc_model* m, const double* yv, int p, const double* X, const double* beta,
+                       double* grad7, double* scale7);
 int orc_gls_beta(const orc_model* m, const double* yv, int p, const double* X,
                  double* beta_out);
 int orc_predict(const orc_model* m, const double* yv, int p, const double* X,
