@@ -103,13 +103,43 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def make_data(stations, days, seed=20260203):
-    import paper_2602_03609_b200 as S
-    theta = S.synth.THETA_T3 if stations >= 2000 else S.synth.THETA_SEC4
+def _synth():
+    """synth.py loaded by path: the reference arm must not import the engine package (no libstgp_b200)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_stgp_synth", os.path.join(ROOT, "paper_2602_03609_b200", "synth.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def make_data(stations, days, seed=20260203, reference=False):
+    """Synthetic station x day data in order_observations order (dataset.cpp:81-114): the engine's
+    ordering on the GPU arm, the oracle's (identical permutation, tests/test_ordering.py) on the
+    reference arm."""
+    synth = _synth()
+    theta = synth.THETA_T3 if stations >= 2000 else synth.THETA_SEC4
     box = (4.6e6, 2.9e6) if stations >= 2000 else (1.0, 1.0)
-    x, y, t, resp = S.synth.station_day(stations, days, box=box, theta=theta, seed=seed)
-    perm = S.order_observations_perm(t, seed)
+    x, y, t, resp = synth.station_day(stations, days, box=box, theta=theta, seed=seed)
+    if reference:
+        from oracle import oracle as O
+        perm = O.order_observations(t, seed)
+    else:
+        import paper_2602_03609_b200 as S
+        perm = S.order_observations_perm(t, seed)
     return x[perm], y[perm], t[perm], resp[perm], theta
+
+
+def bench_config(args, n, world):
+    """The `config` object both arms print (same keys and values: the driver compares them)."""
+    return {"workload": workload_name(args), "n": n, "m_v": args.m_v, "stations": args.stations,
+            "days": args.days, "theta": "PAPER.md Table 3 (NOAA temperature)" if args.stations >= 2000
+            else "PAPER.md section 4",
+            "neighbors": {"vif": "d_r exact kNN (residual_neighbors)", "fitc": "none (FITC)",
+                          "vecchia": "d_c exact kNN (correlation_neighbors)"}[args.workload],
+            "inducing_request": args.m if args.workload in ("vif", "fitc") else None,
+            "parallelism": f"index-shard x{world}",
+            "l2": "inputs larger than L2 (nbr 132 MB + A 264 MB)" if args.workload == "vecchia"
+            else "inputs larger than L2 (n x M f64 work arrays, 8-19 GB each)"}
 
 
 # canonical algorithmic FP64 work per row (DESIGN.md §4): FMA = k^3/6 + 3 k^2 (Cholesky,
@@ -123,29 +153,6 @@ def vecchia_flops(nbr_counts):
     k = nbr_counts.astype(np.float64)
     ck = (k + 1) * (k + 2) / 2
     return float(np.sum(2 * (k ** 3 / 6 + 3 * k ** 2) + ck * (KE_FLOP + KG_FLOP)))
-
-
-def cpu_sample_vecchia(x, y, t, resp, theta, nbr, target_s=10.0):
-    """Time the oracle (reference algorithm restated: build + nll + build + nll_grad,
-    i.e. Objective::value + Objective::gradient) on a prefix of the ordered rows; a
-    prefix with its own neighbour rows is a self-contained Vecchia model."""
-    from oracle import oracle as O
-    cores = O.set_threads(os.cpu_count() or 1)
-    n = len(x)
-    ns = min(n, 20000)
-    while True:
-        om = O.OracleModel("vecchia", x[:ns], y[:ns], t[:ns], theta, nbr=nbr[:ns])
-        t0 = time.perf_counter()
-        om.nll(resp[:ns])
-        om.nll_grad(resp[:ns])
-        dt = time.perf_counter() - t0
-        if dt >= 2.0 or ns >= n:
-            break
-        ns = min(n, int(ns * max(2.0, min(target_s / max(dt, 1e-3), 20.0))))
-    per_eval_full = dt * n / ns
-    return {"value": 1.0 / per_eval_full, "unit": "evals/s", "cores": cores, "kind": "port",
-            "sample": f"oracle build+nll+build+nll_grad on the first {ns} of {n} ordered rows "
-                      f"({dt:.2f} s), scaled linearly to n"}
 
 
 def vif_flops(nbr_counts, M):
@@ -171,75 +178,89 @@ def fitc_flops(n, M):
     return float(2 * 3.0 * n * M * M + n * M * (KE_FLOP + KG_FLOP))
 
 
-def cpu_sample_vif(x, y, t, resp, theta, nbr, Z, target_s=10.0, kind="vif"):
-    """Oracle VIF build + nll + build + nll_grad on a prefix of the ordered rows with the full
-    inducing set; the n M^2 and per-row terms are linear in n, so scale linearly."""
+def _oracle_sample(kind, x, y, t, theta, m_v, ns, Z=None):
+    """Oracle model on the first ns ordered rows (a prefix with its predecessor neighbour sets is a
+    self-contained model); the neighbour search is setup, not timed."""
+    from oracle import oracle as O
+    nbr = None
+    if kind == "vif":
+        nbr = O.dr_neighbors_rows(x[:ns], y[:ns], t[:ns], theta, Z, m_v)
+    elif kind == "vecchia":
+        nbr = O.dc_neighbors(x[:ns], y[:ns], t[:ns], theta, m_v)
+    return O.OracleModel(kind, x[:ns], y[:ns], t[:ns], theta, nbr=nbr, Z=Z)
+
+
+def _time_eval(om, resp, ns):
+    """Objective::value + Objective::gradient as the reference runs them: build + nll, build + nll_grad
+    (estimation.cpp:277-325; the oracle rebuilds the structure inside each call)."""
+    t0 = time.perf_counter()
+    om.nll(resp[:ns])
+    om.nll_grad(resp[:ns])
+    return time.perf_counter() - t0
+
+
+SAMPLE_ROWS = {"vif": 30000, "fitc": 20000, "vecchia": 200000}
+
+
+def cpu_sample(kind, x, y, t, resp, theta, m_v, Z=None):
+    """cpu_baseline: the reference algorithm (oracle restatement, dense n x M^2 parts on OpenBLAS with
+    all host threads, per-row work on OpenMP) on a prefix of >= 2 days of the ordered rows, scaled
+    linearly to n (every term of one evaluation is linear in n at fixed M and m_v)."""
     from oracle import oracle as O
     cores = O.set_threads(os.cpu_count() or 1)
+    blas = O.set_blas(True, cores)
     n = len(x)
-    ns = min(n, 1500)
-    while True:
-        om = O.OracleModel(kind, x[:ns], y[:ns], t[:ns], theta, nbr=None if nbr is None else nbr[:ns], Z=Z)
-        t0 = time.perf_counter()
-        om.nll(resp[:ns])
-        om.nll_grad(resp[:ns])
-        dt = time.perf_counter() - t0
-        if dt >= 3.0 or ns >= n or ns >= 40000:
-            break
-        ns = min(n, 40000, int(ns * max(2.0, min(target_s / max(dt, 1e-3), 8.0))))
+    ns = min(n, SAMPLE_ROWS[kind])
+    om = _oracle_sample(kind, x, y, t, theta, m_v, ns, Z)
+    dt = _time_eval(om, resp, ns)
+    O.set_blas(False)
     per_eval_full = dt * n / ns
+    days = len(np.unique(t[:ns]))
     return {"value": 1.0 / per_eval_full, "unit": "evals/s", "cores": cores, "kind": "port",
-            "sample": f"oracle {kind.upper()} build+nll+build+nll_grad on the first {ns} of {n} ordered rows with all "
-                      f"{len(Z)} inducing points ({dt:.2f} s), scaled linearly to n"}
+            "sample": f"oracle {kind.upper()} build+nll+build+nll_grad on the first {ns} of {n} ordered rows "
+                      f"({days} days{'' if Z is None else f', all {len(Z)} inducing points'}; {dt:.2f} s; dense "
+                      f"parts on {'OpenBLAS' if blas else 'sequential loops'}), scaled linearly to n"}
 
 
 def run_reference(args):
-    """--impl reference: the reference algorithm's CPU path (oracle port; the reference
-    itself cannot be built here) on all host cores, one bounded prefix
-    sample of the workload per step, scaled to n."""
+    """--impl reference: the reference algorithm's CPU path (the oracle restatement -- the reference itself
+    cannot be built here, DESIGN.md §2 -- with its dense n x M^2 contractions on OpenBLAS) on all host
+    cores, one bounded prefix sample of the workload per step, scaled to n.  Neither the engine package
+    nor libstgp_b200.so is loaded on this arm."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     from oracle import oracle as O
-    x, y, t, resp, theta = make_data(args.stations, args.days)
+    x, y, t, resp, theta = make_data(args.stations, args.days, reference=True)
     n = len(x)
     cores = O.set_threads(os.cpu_count() or 1)
-    if args.workload == "vif":
+    kind = args.workload
+    Z = None
+    if kind in ("vif", "fitc"):
         Z, _, _ = O.sts_kmeanspp(x, y, t, args.m, 20260203)
-        ns = min(n, 3000)
-        nbr = O.dr_neighbors(x[:ns], y[:ns], t[:ns], theta, Z, args.m_v)
-        kind, extra = "vif", {"Z": Z}
-        desc = f"oracle VIF build+nll+build+nll_grad on the first {ns} of {n} ordered rows ({len(Z)} inducing points)"
-    elif args.workload == "fitc":
-        Z, _, _ = O.sts_kmeanspp(x, y, t, args.m, 20260203)
-        ns = min(n, 2000)
-        nbr = None
-        kind, extra = "fitc", {"Z": Z}
-        desc = f"oracle FITC build+nll+build+nll_grad on the first {ns} of {n} ordered rows ({len(Z)} inducing points)"
-    else:
-        ns = min(n, 30000)
-        nbr = O.dc_neighbors(x[:ns], y[:ns], t[:ns], theta, args.m_v)
-        kind, extra = "vecchia", {}
-        desc = f"oracle build+nll+build+nll_grad on the first {ns} of {n} ordered rows"
+    ns = min(n, SAMPLE_ROWS[kind])
+    om = _oracle_sample(kind, x, y, t, theta, args.m_v, ns, Z)
+    blas = O.set_blas(True, cores)
     times = []
     for step in range(args.warmup + args.steps):
-        om = O.OracleModel(kind, x[:ns], y[:ns], t[:ns], theta, nbr=nbr, **extra)
-        t0 = time.perf_counter()
-        om.nll(resp[:ns])
-        om.nll_grad(resp[:ns])
-        dt = time.perf_counter() - t0
+        dt = _time_eval(om, resp, ns)
         if step >= args.warmup:
             times.append(dt * n / ns)
+    O.set_blas(False)
     per = statistics.median(times)
     val = 1.0 / per
+    days = len(np.unique(t[:ns]))
+    desc = (f"oracle {kind.upper()} build+nll+build+nll_grad on the first {ns} of {n} ordered rows ({days} days"
+            f"{'' if Z is None else f', all {len(Z)} inducing points'}; dense parts on "
+            f"{'OpenBLAS' if blas else 'sequential loops'}) per step, scaled linearly to n")
     line = {"metric": METRIC, "value": val, "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(args), "n": n, "m_v": args.m_v, "stations": args.stations,
-                       "days": args.days},
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (station x day layout of simulate.cpp, random-feature field + nugget)",
+            "config": bench_config(args, n, world),
             "impl": "reference",
-            "cpu_baseline": {"value": val, "unit": "evals/s", "cores": cores, "kind": "port",
-                             "sample": desc + " per step, scaled linearly to n"},
+            "cpu_baseline": {"value": val, "unit": "evals/s", "cores": cores, "kind": "port", "sample": desc},
             "e2e": {"value": val, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -425,14 +446,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (station x day layout of simulate.cpp, random-feature field + nugget)",
-            "config": {"workload": workload_name(args), "n": n, "m_v": args.m_v, "stations": args.stations,
-                       "days": args.days, "theta": "PAPER.md Table 3 (NOAA temperature)" if args.stations >= 2000
-                       else "PAPER.md section 4",
-                       "neighbors": {"vif": "d_r exact kNN (residual_neighbors)", "fitc": "none (FITC)",
-                                     "vecchia": "d_c exact kNN (correlation_neighbors)"}[args.workload],
-                       "parallelism": f"index-shard x{world}",
-                       "l2": "inputs larger than L2 (nbr 132 MB + A 264 MB)" if args.workload == "vecchia"
-                       else "inputs larger than L2 (n x M f64 work arrays, 8-19 GB each)"},
+            "config": bench_config(args, n, world),
             "nn_search_s": nn_s, "nn_search_kernel_ms": knn_ms, "nll": v, "grad": list(g),
             "e2e": {"value": 1.0 / e2e_s, "unit": "evals/s", "h2d_bytes_per_step": n * 8 + 64,
                     "d2h_bytes_per_step": 64},
@@ -472,12 +486,8 @@ def main():
         line["predict_targets"] = int(len(targets))
         line["predict_var_range"] = [float(pr.var.min()), float(pr.var.max())]
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        if args.workload == "vif":
-            line["cpu_baseline"] = cpu_sample_vif(x, y, t, resp, theta, nbr, ind.points)
-        elif args.workload == "fitc":
-            line["cpu_baseline"] = cpu_sample_vif(x, y, t, resp, theta, None, ind.points, kind="fitc")
-        else:
-            line["cpu_baseline"] = cpu_sample_vecchia(x, y, t, resp, theta, nbr)
+        line["cpu_baseline"] = cpu_sample(args.workload, x, y, t, resp, theta, args.m_v,
+                                          None if args.workload == "vecchia" else ind.points)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

@@ -520,3 +520,22 @@ def dr_neighbors_rows(x, y, t, theta, Z, m_v: int, rows=None, with_dist: bool = 
     _chk(lib().orc_dr_neighbors_rows(len(x), _p(x), _p(y), _p(t), C.byref(params(theta)), len(Z), _p(zx), _p(zy),
                                      _p(zt), m_v, nq, _p(r), _p(out), _p(dist), int(by_dist)))
     return (out, dist) if with_dist else out
+
+
+def openblas_path():
+    """the scipy-bundled OpenBLAS (LP64, scipy_* symbols) of this image, or None"""
+    import glob
+    import scipy
+    libs = glob.glob(os.path.join(os.path.dirname(os.path.dirname(scipy.__file__)), "scipy.libs",
+                                  "libscipy_openblas-*.so"))
+    return libs[0] if libs else None
+
+
+def set_blas(on: bool = True, threads: int = 0) -> bool:
+    """BLAS timing mode (orc_set_blas): the dense n x M^2 contractions go to OpenBLAS; off restores the
+    sequential-order restatement the parity tests use.  Returns whether BLAS is active."""
+    path = openblas_path() if on else None
+    if on and path is None:
+        return False
+    _chk(lib().orc_set_blas(path.encode() if path else None, int(threads)))
+    return on

@@ -18,6 +18,8 @@
 #include <utility>
 #include <vector>
 
+#include <dlfcn.h>
+
 #ifdef _OPENMP
 #include <omp.h>
 #endif
@@ -221,6 +223,44 @@ inline double dot_seq(const double* a, const double* b, int n) {
   return acc;
 }
 
+// ---------------------------------------------------------------------------
+// Optional BLAS timing mode (orc_set_blas): the dense n x M^2 contractions -- W = L^{-1} U, the Woodbury
+// cores, the gradient's triangular solves and Gram products -- go to an OpenBLAS (the scipy-bundled one,
+// LP64 Fortran symbols) the way the reference hands them to Eigen's blocked GEMM/TRSM
+// (approximations.cpp:269-306, 513-536, 595-601, 711).  Results then differ from the sequential-order
+// restatement by rounding only (~1e-13 relative); parity checks keep the default sequential order, the
+// CPU baseline of bench.py uses this mode.
+// ---------------------------------------------------------------------------
+using dgemm_fn = void (*)(const char*, const char*, const int*, const int*, const int*, const double*, const double*,
+                          const int*, const double*, const int*, const double*, double*, const int*);
+using dsyrk_fn = void (*)(const char*, const char*, const int*, const int*, const double*, const double*, const int*,
+                          const double*, double*, const int*);
+using dtrsm_fn = void (*)(const char*, const char*, const char*, const char*, const int*, const int*, const double*,
+                          const double*, const int*, double*, const int*);
+struct Blas {
+  dgemm_fn gemm = nullptr;
+  dsyrk_fn syrk = nullptr;
+  dtrsm_fn trsm = nullptr;
+  void (*set_threads)(int) = nullptr;
+};
+Blas g_blas_fns;
+bool g_blas = false;
+
+// C (r x c) = alpha op(A) op(B) + beta C, all column-major Mats
+void blas_gemm(bool ta, bool tb, double alpha, const Mat& A, const Mat& B, double beta, Mat& C) {
+  const int m = C.r, n = C.c, k = ta ? A.r : A.c;
+  const int lda = std::max(1, A.r), ldb = std::max(1, B.r), ldc = std::max(1, C.r);
+  if (m == 0 || n == 0) return;
+  g_blas_fns.gemm(ta ? "T" : "N", tb ? "T" : "N", &m, &n, &k, &alpha, A.a.data(), &lda, B.a.data(), &ldb, &beta,
+                  C.a.data(), &ldc);
+}
+// C (lower) = alpha A A^T + beta C, A n x k
+void blas_syrk(double alpha, const Mat& A, double beta, Mat& C) {
+  const int n = A.r, k = A.c, lda = std::max(1, A.r), ldc = std::max(1, C.r);
+  if (n == 0) return;
+  g_blas_fns.syrk("L", "N", &n, &k, &alpha, A.a.data(), &lda, &beta, C.a.data(), &ldc);
+}
+
 // Cholesky A = L L^T, lower triangle, row-major scratch Lr (n*n) for speed.
 // Fails when a pivot is <= 0 (Eigen's LLT info() != Success criterion).
 // Element (r,c) accumulates A(r,c) - sum_{k<c} L(r,k) L(c,k) in increasing k.
@@ -298,7 +338,33 @@ struct Chol {
     return 2.0 * s;
   }
   double diag(int i) const { return Lr[static_cast<size_t>(i) * n + i]; }
+  // B <- L^{-1} B (trans: L^{-T} B) through BLAS, B n x ncols column-major
+  void trsm(Mat& B, bool trans) const {
+    if (Lc.empty()) {
+      auto& self = const_cast<Chol&>(*this);
+      self.Lc.assign(static_cast<size_t>(n) * n, 0.0);
+      for (int r = 0; r < n; ++r)
+        for (int c = 0; c <= r; ++c) self.Lc[static_cast<size_t>(c) * n + r] = Lr[static_cast<size_t>(r) * n + c];
+    }
+    const int m = B.r, nc = B.c, ld = std::max(1, n), ldb = std::max(1, B.r);
+    const double one = 1.0;
+    if (m == 0 || nc == 0) return;
+    g_blas_fns.trsm("L", "L", trans ? "T" : "N", "N", &m, &nc, &one, Lc.data(), &ld, B.a.data(), &ldb);
+  }
+  std::vector<double> Lc;  // column-major copy of L for BLAS (lazily formed)
 };
+
+// Mc (lower, symmetrized) += sum_i A(:,i) A(:,i)^T / d_i through BLAS (scaled copy + SYRK)
+void blas_core(const Mat& A, const std::vector<double>& d, Mat& Mc) {
+  Mat As = A;
+  for (int i = 0; i < A.c; ++i) {
+    const double sc = 1.0 / std::sqrt(d[static_cast<size_t>(i)]);
+    for (int j = 0; j < A.r; ++j) As(j, i) *= sc;
+  }
+  blas_syrk(1.0, As, 1.0, Mc);
+  for (int a = 0; a < Mc.r; ++a)
+    for (int b = 0; b < a; ++b) Mc(b, a) = Mc(a, b);
+}
 
 // ---------------------------------------------------------------------------
 // InducingBasis (inducing.cpp:237-284)
@@ -337,10 +403,21 @@ struct Basis {
 };
 
 // U (M x n) and W = L^{-1} U (M x n)
-void cross_and_whiten(const Basis& b, const Kernel& k, const std::vector<Pt>& pts, Mat* U, Mat& W) {
+// exact = true keeps the sequential fma chain even in BLAS mode: the searches' d_r distances are defined
+// by it bit for bit
+void cross_and_whiten(const Basis& b, const Kernel& k, const std::vector<Pt>& pts, Mat* U, Mat& W,
+                      bool exact = false) {
   const int M = b.m(), n = static_cast<int>(pts.size());
   W = Mat(M, n);
   if (U) *U = Mat(M, n);
+  if (g_blas && !exact) {  // U by kernel evaluations, then one TRSM
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < M; ++j) W(j, i) = k(b.z[static_cast<size_t>(j)], pts[static_cast<size_t>(i)]);
+    if (U) *U = W;
+    b.llt.trsm(W, false);
+    return;
+  }
 #pragma omp parallel
   {
     std::vector<double> kv(static_cast<size_t>(M));
@@ -808,14 +885,18 @@ void build_model(Model& s, const orc_model* m) {
         throw NumericError("build_fitc: zero observation diagonal; a positive nugget is required");
     }
     Mat Mc = s.basis.sigma;
+    if (g_blas) {
+      blas_core(s.U, s.lambda, Mc);
+    } else {
 #pragma omp parallel for schedule(dynamic)
-    for (int a = 0; a < M; ++a)
-      for (int b = 0; b <= a; ++b) {
-        double acc = 0.0;
-        for (int i = 0; i < n; ++i) acc += s.U(a, i) * s.U(b, i) / s.lambda[static_cast<size_t>(i)];
-        Mc(a, b) += acc;
-        if (a != b) Mc(b, a) = Mc(a, b);
-      }
+      for (int a = 0; a < M; ++a)
+        for (int b = 0; b <= a; ++b) {
+          double acc = 0.0;
+          for (int i = 0; i < n; ++i) acc += s.U(a, i) * s.U(b, i) / s.lambda[static_cast<size_t>(i)];
+          Mc(a, b) += acc;
+          if (a != b) Mc(b, a) = Mc(a, b);
+        }
+    }
     if (!s.Mllt.compute(Mc)) throw NumericError("build_fitc: Woodbury core factorization failed");
     return;
   }
@@ -846,14 +927,18 @@ void build_model(Model& s, const orc_model* m) {
       }
     }
     Mat Mc = s.basis.sigma;
+    if (g_blas) {
+      blas_core(VB, s.rows.D, Mc);
+    } else {
 #pragma omp parallel for schedule(dynamic)
-    for (int a = 0; a < M; ++a)
-      for (int b = 0; b <= a; ++b) {
-        double acc = 0.0;
-        for (int i = 0; i < n; ++i) acc += VB(a, i) * VB(b, i) / s.rows.D[static_cast<size_t>(i)];
-        Mc(a, b) += acc;
-        if (a != b) Mc(b, a) = Mc(a, b);
-      }
+      for (int a = 0; a < M; ++a)
+        for (int b = 0; b <= a; ++b) {
+          double acc = 0.0;
+          for (int i = 0; i < n; ++i) acc += VB(a, i) * VB(b, i) / s.rows.D[static_cast<size_t>(i)];
+          Mc(a, b) += acc;
+          if (a != b) Mc(b, a) = Mc(a, b);
+        }
+    }
     if (!s.Mllt.compute(Mc)) throw NumericError("build_vif: Woodbury core factorization failed");
   }
 }
@@ -1054,12 +1139,23 @@ void lowrank_pairs(const Model& s, int M, Om&& om, const Mat& wsig, double* grad
 
 // helper: Y = Cholesky-solve of each column (M x n)
 Mat chol_solve_cols(const Chol& c, const Mat& B) {
+  if (g_blas) {
+    Mat X = B;
+    c.trsm(X, false);
+    c.trsm(X, true);
+    return X;
+  }
   Mat X(B.r, B.c);
 #pragma omp parallel for schedule(static)
   for (int i = 0; i < B.c; ++i) c.solve(B.col(i), X.col(i));
   return X;
 }
 Mat chol_lsolve_cols(const Chol& c, const Mat& B) {
+  if (g_blas) {
+    Mat X = B;
+    c.trsm(X, false);
+    return X;
+  }
   Mat X(B.r, B.c);
 #pragma omp parallel for schedule(static)
   for (int i = 0; i < B.c; ++i) c.lsolve(B.col(i), X.col(i));
@@ -1100,29 +1196,37 @@ void grad_fitc(const Model& s, const std::vector<double>& r, double* grad, doubl
   }
   const Mat NL = chol_solve_cols(s.Mllt, UL);
   Mat G1(M, M);  // P * UL^T
-#pragma omp parallel for schedule(static)
-  for (int a = 0; a < M; ++a)
-    for (int b = 0; b < M; ++b) {
-      double acc = 0.0;
-      for (int i = 0; i < n; ++i) acc += P(a, i) * UL(b, i);
-      G1(a, b) = acc;
-    }
   Mat K2(M, n);
-#pragma omp parallel for schedule(static)
-  for (int i = 0; i < n; ++i)
-    for (int a = 0; a < M; ++a) {
-      double acc = 0.0;
-      for (int b = 0; b < M; ++b) acc += G1(a, b) * NL(b, i);
-      K2(a, i) = P(a, i) * lam_inv[static_cast<size_t>(i)] - acc;
-    }
   Mat W2(M, M);  // K2 P^T
+  if (g_blas) {
+    blas_gemm(false, true, 1.0, P, UL, 0.0, G1);
+    for (int i = 0; i < n; ++i)
+      for (int a = 0; a < M; ++a) K2(a, i) = P(a, i) * lam_inv[static_cast<size_t>(i)];
+    blas_gemm(false, false, -1.0, G1, NL, 1.0, K2);
+    blas_gemm(false, true, 1.0, K2, P, 0.0, W2);
+  } else {
 #pragma omp parallel for schedule(static)
-  for (int a = 0; a < M; ++a)
-    for (int b = 0; b < M; ++b) {
-      double acc = 0.0;
-      for (int i = 0; i < n; ++i) acc += K2(a, i) * P(b, i);
-      W2(a, b) = acc;
-    }
+    for (int a = 0; a < M; ++a)
+      for (int b = 0; b < M; ++b) {
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) acc += P(a, i) * UL(b, i);
+        G1(a, b) = acc;
+      }
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < n; ++i)
+      for (int a = 0; a < M; ++a) {
+        double acc = 0.0;
+        for (int b = 0; b < M; ++b) acc += G1(a, b) * NL(b, i);
+        K2(a, i) = P(a, i) * lam_inv[static_cast<size_t>(i)] - acc;
+      }
+#pragma omp parallel for schedule(static)
+    for (int a = 0; a < M; ++a)
+      for (int b = 0; b < M; ++b) {
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) acc += K2(a, i) * P(b, i);
+        W2(a, b) = acc;
+      }
+  }
   std::vector<double> Pa(static_cast<size_t>(M)), phi(static_cast<size_t>(n));
   for (int a = 0; a < M; ++a) {
     double acc = 0.0;
@@ -1132,13 +1236,23 @@ void grad_fitc(const Model& s, const std::vector<double>& r, double* grad, doubl
   for (int i = 0; i < n; ++i)
     phi[static_cast<size_t>(i)] = 0.5 * (dsinv[static_cast<size_t>(i)] - alpha[static_cast<size_t>(i)] * alpha[static_cast<size_t>(i)]);
   Mat wsig(M, M);
+  if (g_blas) {
+    Mat Pphi = P;
+    for (int i = 0; i < n; ++i)
+      for (int a = 0; a < M; ++a) Pphi(a, i) *= phi[static_cast<size_t>(i)];
+    blas_gemm(false, true, 1.0, Pphi, P, 0.0, wsig);
+    for (int a = 0; a < M; ++a)
+      for (int b = 0; b < M; ++b)
+        wsig(a, b) += -0.5 * W2(a, b) + 0.5 * (Pa[static_cast<size_t>(a)] * Pa[static_cast<size_t>(b)]);
+  } else {
 #pragma omp parallel for schedule(static)
-  for (int a = 0; a < M; ++a)
-    for (int b = 0; b < M; ++b) {
-      double acc = 0.0;
-      for (int i = 0; i < n; ++i) acc += P(a, i) * phi[static_cast<size_t>(i)] * P(b, i);
-      wsig(a, b) = -0.5 * W2(a, b) + 0.5 * (Pa[static_cast<size_t>(a)] * Pa[static_cast<size_t>(b)]) + acc;
-    }
+    for (int a = 0; a < M; ++a)
+      for (int b = 0; b < M; ++b) {
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) acc += P(a, i) * phi[static_cast<size_t>(i)] * P(b, i);
+        wsig(a, b) = -0.5 * W2(a, b) + 0.5 * (Pa[static_cast<size_t>(a)] * Pa[static_cast<size_t>(b)]) + acc;
+      }
+  }
   for (int q = 0; q < 7; ++q) grad[q] = 0.0;
   if (scale)
     for (int q = 0; q < 7; ++q) scale[q] = 0.0;
@@ -1199,8 +1313,13 @@ void grad_vif(const Model& s, const std::vector<double>& r, double* grad, double
     }
     LVB = chol_lsolve_cols(s.Mllt, VB);
     Hhat = Mat(M, n);
+    if (g_blas) {
+      Hhat = LVB;
+      s.Mllt.trsm(Hhat, true);
+    } else {
 #pragma omp parallel for schedule(static)
-    for (int i = 0; i < n; ++i) bwd_seq(s.Mllt.Lr, M, LVB.col(i), Hhat.col(i));
+      for (int i = 0; i < n; ++i) bwd_seq(s.Mllt.Lr, M, LVB.col(i), Hhat.col(i));
+    }
     N1 = chol_solve_cols(s.Mllt, U);
   }
   std::vector<double> z(static_cast<size_t>(n)), Bz(static_cast<size_t>(n));
@@ -1305,30 +1424,45 @@ void grad_vif(const Model& s, const std::vector<double>& r, double* grad, double
   const std::vector<double> qt = q_apply(s.nb, s.rows, t.data());
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < M; ++j) omega(j, i) -= yM[static_cast<size_t>(j)] * (ur[static_cast<size_t>(i)] - qt[static_cast<size_t>(i)]);
+  // PPhi(j, pb) += sum_a P(j, pa) Phi_i(a, b), rows i in order, a in order; each thread owns a slice of
+  // j so the column accesses stay contiguous (same per-element order as a j-outer loop)
   Mat PPhi(M, n);
-#pragma omp parallel for schedule(static)
-  for (int j = 0; j < M; ++j) {
-    for (int i = 0; i < n; ++i) {
+#pragma omp parallel
+  {
+    const int T = omp_get_num_threads(), tid = omp_get_thread_num();
+    const int j0 = static_cast<int>(static_cast<long>(M) * tid / T), j1 = static_cast<int>(static_cast<long>(M) * (tid + 1) / T);
+    std::vector<double> acc(static_cast<size_t>(std::max(j1 - j0, 0)));
+    for (int i = 0; i < n && j1 > j0; ++i) {
       const int k = s.nb.count(i);
       const double* ph = &phi[static_cast<size_t>(i) * K1 * K1];
       for (int b = 0; b <= k; ++b) {
-        const int pb = clidx(i, b);
-        double acc = 0.0;
-        for (int a = 0; a <= k; ++a) acc += P(j, clidx(i, a)) * ph[a * K1 + b];
-        PPhi(j, pb) += acc;
+        std::fill(acc.begin(), acc.end(), 0.0);
+        for (int a = 0; a <= k; ++a) {
+          const double w = ph[a * K1 + b];
+          const double* Pa = P.col(clidx(i, a));
+          for (int j = j0; j < j1; ++j) acc[static_cast<size_t>(j - j0)] += Pa[j] * w;
+        }
+        double* dst = PPhi.col(clidx(i, b));
+        for (int j = j0; j < j1; ++j) dst[j] += acc[static_cast<size_t>(j - j0)];
       }
     }
   }
   for (size_t e = 0; e < omega.a.size(); ++e) omega.a[e] -= 2.0 * PPhi.a[e];
   // wsig = 0.5 yM yM^T + PPhi P^T + 0.5 (M^{-1} - Sigma_m^{-1})
   Mat wsig(M, M);
+  if (g_blas) {
+    blas_gemm(false, true, 1.0, PPhi, P, 0.0, wsig);
+    for (int a = 0; a < M; ++a)
+      for (int b = 0; b < M; ++b) wsig(a, b) += 0.5 * (yM[static_cast<size_t>(a)] * yM[static_cast<size_t>(b)]);
+  } else {
 #pragma omp parallel for schedule(static)
-  for (int a = 0; a < M; ++a)
-    for (int b = 0; b < M; ++b) {
-      double acc = 0.0;
-      for (int i = 0; i < n; ++i) acc += PPhi(a, i) * P(b, i);
-      wsig(a, b) = 0.5 * (yM[static_cast<size_t>(a)] * yM[static_cast<size_t>(b)]) + acc;
-    }
+    for (int a = 0; a < M; ++a)
+      for (int b = 0; b < M; ++b) {
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) acc += PPhi(a, i) * P(b, i);
+        wsig(a, b) = 0.5 * (yM[static_cast<size_t>(a)] * yM[static_cast<size_t>(b)]) + acc;
+      }
+  }
   {
     Mat I(M, M);
     for (int j = 0; j < M; ++j) I(j, j) = 1.0;
@@ -1448,6 +1582,29 @@ int orc_set_threads(int n) {
   return 1;
 #endif
 }
+int orc_set_blas(const char* path, int threads) {
+  return guarded([&] {
+    if (!path || !*path) {
+      g_blas = false;
+      return;
+    }
+    void* h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+    if (!h) throw ConfigError(std::string("orc_set_blas: ") + dlerror());
+    auto sym = [&](const char* a, const char* b) {
+      void* f = dlsym(h, a);
+      if (!f) f = dlsym(h, b);
+      if (!f) throw ConfigError(std::string("orc_set_blas: missing ") + a);
+      return f;
+    };
+    g_blas_fns.gemm = reinterpret_cast<dgemm_fn>(sym("scipy_dgemm_", "dgemm_"));
+    g_blas_fns.syrk = reinterpret_cast<dsyrk_fn>(sym("scipy_dsyrk_", "dsyrk_"));
+    g_blas_fns.trsm = reinterpret_cast<dtrsm_fn>(sym("scipy_dtrsm_", "dtrsm_"));
+    g_blas_fns.set_threads = reinterpret_cast<void (*)(int)>(sym("scipy_openblas_set_num_threads", "openblas_set_num_threads"));
+    if (threads > 0) g_blas_fns.set_threads(threads);
+    g_blas = true;
+  });
+}
+
 int orc_set_prune(int on) {
   g_prune = on != 0;
   return 0;
@@ -1565,7 +1722,7 @@ int orc_dr_neighbors(int n, const double* x, const double* y, const double* t,
     for (int j = 0; j < M; ++j) z.push_back({zx[j], zy[j], zt[j]});
     Basis basis(z, k);
     Mat W(M, n);
-    if (M > 0) cross_and_whiten(basis, k, pts, nullptr, W);
+    if (M > 0) cross_and_whiten(basis, k, pts, nullptr, W, true);
     const double s1 = p->sigma1_2;
     const double tol = 1e-7 * s1;
     std::vector<double> resid(static_cast<size_t>(n));
@@ -1625,7 +1782,7 @@ static void dr_search_rows(int n, const double* x, const double* y, const double
   const std::vector<Pt> head(pts.begin(), pts.begin() + top);
   Basis basis(z, Kernel(*p));  // selection kernel: no lag table (estimation.cpp:200)
   Mat W(M, top);
-  if (M > 0) cross_and_whiten(basis, Kernel(*p), head, nullptr, W);
+  if (M > 0) cross_and_whiten(basis, Kernel(*p), head, nullptr, W, true);
   const double s1 = p->sigma1_2, tol = 1e-7 * s1;
   // inducing groups: distinct time (<= 8 quantile bins) x 3 x 3 spatial cells
   std::vector<int> grp(static_cast<size_t>(M), 0);
@@ -2061,22 +2218,31 @@ int orc_predict(const orc_model* m, const double* yv, int p, const double* X, co
       }
       s.basis.llt.solve(Ua.data(), v2.data());
       Mat A1(M, M);
+      if (g_blas) {
+        blas_core(U, s.lambda, A1);
+      } else {
 #pragma omp parallel for schedule(static)
-      for (int a = 0; a < M; ++a)
-        for (int b = 0; b < M; ++b) {
-          double acc = 0.0;
-          for (int i = 0; i < n; ++i) acc += U(a, i) * (1.0 / s.lambda[static_cast<size_t>(i)]) * U(b, i);
-          A1(a, b) = acc;
-        }
+        for (int a = 0; a < M; ++a)
+          for (int b = 0; b < M; ++b) {
+            double acc = 0.0;
+            for (int i = 0; i < n; ++i) acc += U(a, i) * (1.0 / s.lambda[static_cast<size_t>(i)]) * U(b, i);
+            A1(a, b) = acc;
+          }
+      }
       const Mat MA1 = chol_solve_cols(s.Mllt, A1);
       Mat D12(M, M);
+      if (g_blas) {
+        D12 = A1;
+        blas_gemm(false, false, -1.0, A1, MA1, 1.0, D12);
+      } else {
 #pragma omp parallel for schedule(static)
-      for (int a = 0; a < M; ++a)
-        for (int b = 0; b < M; ++b) {
-          double acc = 0.0;
-          for (int c = 0; c < M; ++c) acc += A1(a, c) * MA1(c, b);
-          D12(a, b) = A1(a, b) - acc;
-        }
+        for (int a = 0; a < M; ++a)
+          for (int b = 0; b < M; ++b) {
+            double acc = 0.0;
+            for (int c = 0; c < M; ++c) acc += A1(a, c) * MA1(c, b);
+            D12(a, b) = A1(a, b) - acc;
+          }
+      }
 #pragma omp parallel for schedule(static)
       for (int pp = 0; pp < n_p; ++pp) {
         const Pt& q = tg[static_cast<size_t>(pp)];

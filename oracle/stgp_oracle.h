@@ -118,6 +118,9 @@ int orc_test_dataset(int kind, int n, uint64_t seed, int n_times, int p, double*
 int orc_set_threads(int n);
 /* 1 (default): exact lag-bound block pruning in the d_c scan; 0: plain brute force */
 int orc_set_prune(int on);
+/* BLAS timing mode: dense n x M^2 contractions through the OpenBLAS at path (scipy-bundled LP64, symbols
+ * scipy_dgemm_ etc.) with the given thread count; path NULL or "" restores the sequential restatement */
+int orc_set_blas(const char* path, int threads);
 
 #ifdef __cplusplus
 }

@@ -306,6 +306,7 @@ struct TuneCache {
 };
 
 struct OzakiState {
+  OzakiTcState* tc = nullptr;  // the hand-written tcgen05 kernel's work lists
   TuneCache tune;
   cublasLtHandle_t lt = nullptr;
   DevBuf<unsigned char> ws;
@@ -320,6 +321,7 @@ struct OzakiState {
   DevBuf<unsigned long long> maxbits;
   std::map<std::tuple<int, int, long long, int, int, int>, std::unique_ptr<LtPlan>> plans;
   ~OzakiState() {
+    ozaki_tc_release(tc);
     plans.clear();
     if (lt) cublasLtDestroy(lt);
   }
@@ -348,6 +350,16 @@ int ozaki_slices() {
   return s;
 }
 
+// The int8 products run on the hand-written tcgen05 kernel (ozaki_tc.cu); STGP_OZAKI_TC=0 switches
+// back to cuBLASLt IMMA per diagonal plus the combine kernels (A/B comparison only).
+bool ozaki_tc_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("STGP_OZAKI_TC");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 bool ozaki_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("STGP_OZAKI");  // A/B switch: 0 = cuBLAS DGEMM
@@ -369,8 +381,10 @@ bool ozaki_for(int m) {
 static OzakiState* state(stgp_ctx* ctx) {
   if (!ctx->ozaki) {
     ctx->ozaki = new OzakiState();
-    lt_check(cublasLtCreate(&ctx->ozaki->lt), "create");
-    ctx->ozaki->ws.alloc(64ull << 20);
+    if (!ozaki_tc_enabled()) {
+      lt_check(cublasLtCreate(&ctx->ozaki->lt), "create");
+      ctx->ozaki->ws.alloc(64ull << 20);
+    }
   }
   return ctx->ozaki;
 }
@@ -471,7 +485,9 @@ void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, 
   if (n <= 0 || m <= 0) return;
   if (m % 4 || ldc % 4) config_error("ozaki_gemm_rows: m and ldc must be multiples of 4");
   const int S = slices_for("STGP_OZAKI_S_ROWS", 6);
-  const int kp = (k + 15) / 16 * 16;  // slice stride: every diagonal segment 16-byte aligned
+  const bool tc = ozaki_tc_enabled();
+  // slice stride: every diagonal segment 16-byte aligned (cuBLASLt), whole 32-byte K steps (tcgen05)
+  const int kp = tc ? (k + 31) / 32 * 32 : (k + 15) / 16 * 16;
   if (static_cast<long long>(S) * kp * 127 * 127 >= (1LL << 31)) config_error("ozaki: k too large for exact int32");
   OzakiState* oz = state(ctx);
   cudaStream_t st = ctx->stream;
@@ -483,16 +499,24 @@ void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, 
   STGP_OZ_SWITCH(S, (slice_rows_kernel<kS><<<grid_for(static_cast<long long>(m) * 32, 256), 256, 0, st>>>(
                          m, k, kp, B, ldb, true, oz->Bs.get(), ldk, oz->sB.get())));
   launched(ctx);
-  const long long chunk = std::min<long long>(n, std::max<long long>(16384, (1LL << 28) / mp));  // Cd ~ S GB
+  // tcgen05: no int32 partials, so chunks only bound the digit buffer (~1.5 GB)
+  const long long chunk = tc ? std::min<long long>(n, std::max<long long>(16384, (3LL << 29) / ldk))
+                             : std::min<long long>(n, std::max<long long>(16384, (1LL << 28) / mp));  // Cd ~ S GB
   oz->As.ensure(static_cast<size_t>(chunk) * ldk);
   oz->sA.ensure(static_cast<size_t>(chunk));
   const long long dstride = chunk * mp;
-  oz->Cd.ensure(static_cast<size_t>(S) * dstride);
+  if (!tc) oz->Cd.ensure(static_cast<size_t>(S) * dstride);
   for (long long r0 = 0; r0 < n; r0 += chunk) {
     const long long nr = std::min(chunk, n - r0);
     STGP_OZ_SWITCH(S, (slice_rows_kernel<kS><<<grid_for(nr * 32, 256), 256, 0, st>>>(
                            nr, k, kp, A + r0 * lda, lda, false, oz->As.get(), ldk, oz->sA.get())));
     launched(ctx);
+    if (tc) {
+      ProfRegion pr(ctx, "oz_imma");
+      ozaki_tc_rows(ctx, oz->tc, S, kp, nr, m, oz->As.get(), false, oz->sA.get(), oz->Bs.get(), true, oz->sB.get(),
+                    C + r0 * ldc, ldc);
+      continue;
+    }
     for (int d = 2; d <= S + 1; ++d) {
       LtPlan* p = plan_for(oz, m, mp, (d - 1) * kp, nr, ldk);
       lt_matmul(ctx, oz, p, oz->Bs.get() + static_cast<size_t>(S - d + 1) * kp, oz->As.get(),
@@ -562,6 +586,11 @@ static void cols_product(stgp_ctx* ctx, int m, long long n, const double* A, int
     oz->keep_n = n;
   }
   const double* sB = same ? sA : oz->sB.get();
+  if (ozaki_tc_enabled()) {
+    ProfRegion pr(ctx, "oz_imma");
+    ozaki_tc_cols(ctx, oz->tc, S, L, nch, m, Aslices, false, sA, oz->Bs.get(), true, sB, same, C, ldc);
+    return;
+  }
   const long long cstride = static_cast<long long>(m) * mp;
   const long long dstride = nch * cstride;
   oz->Cd.ensure(static_cast<size_t>(S) * dstride);

@@ -30,4 +30,14 @@ bool ozaki_gemm_kept(stgp_ctx* ctx, int m, long long n, const double* B, int ldb
                      uint64_t tag);
 void ozaki_release(stgp_ctx* ctx);
 
+// the hand-written tcgen05 kernel behind the products (ozaki_tc.cu)
+struct OzakiTcState;
+void ozaki_tc_release(OzakiTcState* s);
+void ozaki_tc_rows(stgp_ctx* ctx, OzakiTcState*& st, int S, int kp, long long nx, int ny, const int8_t* xd, bool x_rev,
+                   const double* sx, const int8_t* yd, bool y_rev, const double* sy, double* out, long long ldo);
+void ozaki_tc_cols(stgp_ctx* ctx, OzakiTcState*& st, int S, int L, int nch, int m, const int8_t* xd, bool x_rev,
+                   const double* sx, const int8_t* yd, bool y_rev, const double* sy, bool symmetric, double* C,
+                   long long ldc);
+bool ozaki_tc_enabled();
+
 }  // namespace stgp

@@ -1,0 +1,491 @@
+// Hand-written sm_100a int8 tensor-core kernel for the Ozaki products (ozaki.cu): TMA-fed tcgen05.mma
+// kind::i8 with every digit diagonal accumulated in its own TMEM block and the FP64 recombination in the
+// epilogue, so the exact int32 partial products never leave the SM.
+//
+// Operands are the int8 digit slices the slicers of ozaki.cu write (7-bit digits, per-row power-of-two
+// scales).  For an output tile of 128 X rows x 64 Y rows the kernel keeps S accumulators
+//     C_d[x][y] = sum_{s + t = d} sum_k X_s[x][k] Y_t[y][k],     d = 2 .. S + 1,
+// in TMEM columns (d - 2) * 64 .. (d - 2) * 64 + 63 (S <= 8: at most 512 columns), fed one 32-byte K step
+// at a time: each pipeline stage holds the S slices of both operands for that K step (TMA, 32-byte
+// swizzle), and the single MMA thread issues the S (S + 1) / 2 pair products of the stage.  The epilogue
+// warps read the S accumulators back (tcgen05.ld), sum them from the smallest diagonal up in FP64
+// (exact power-of-two weights, one rounding per add, the order of the former combine kernels) and scale
+// by the row / column scales:
+//   rows form  out[x ldo + y]  = (sum_d 2^-7d C_d) sx[x] sy[y]                        (one chunk)
+//   cols form  out[x ldo + y] += (sum_d 2^-7d C_d) (sx[c nx + x] sy[c ny + y])  over reduction chunks c
+// (a chunk keeps every diagonal exact in int32).  The cols form splits its chunks over `groups` CTAs per
+// tile; group partials are summed in group order by ozaki_tc_reduce (deterministic).
+//
+// Warp roles (192 threads, one CTA per SM, persistent over the work items):
+//   warp 0: TMA producer; warp 1: TMEM owner and MMA issuer; warps 2-5: epilogue (TMEM lane quarter
+//   warp % 4).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "lowrank_common.cuh"
+#include "ozaki.cuh"
+
+namespace stgp {
+namespace {
+
+constexpr int kBM = 128;     // X rows per tile = TMEM lanes = MMA M
+constexpr int kBN = 64;      // Y rows per tile = MMA N = TMEM columns per diagonal
+constexpr int kBK = 32;      // int8 K per stage (one MMA K step, one 32-byte swizzle row)
+constexpr int kStages = 4;
+constexpr int kThreads = 192;
+constexpr int kTileX = kBM * kBK;  // bytes of one X slice tile
+constexpr int kTileY = kBN * kBK;
+
+struct TcArgs {
+  int S;
+  int kblocks;            // K steps per chunk
+  int nx, ny;             // valid X / Y rows
+  int nchunks, groups;    // reduction chunks and the split of a tile's chunks over CTAs
+  int x_rev, y_rev;       // slice s (1-based) sits at slice coordinate rev ? S - s : s - 1
+  int cols;               // 0: rows form (one chunk, write), 1: cols form (accumulate over chunks)
+  int nitems;
+  const int4* items;      // (tile x, tile y, group, -)
+  const double* sx;       // scales: rows form sx[x]; cols form sx[c nx + x]
+  const double* sy;
+  double* out;            // out[x ldo + y] (+ group * part_stride in the cols form with groups > 1)
+  long long ldo, part_stride;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load4(const CUtensorMap* map, void* dst, uint64_t* bar, int c0, int c1, int c2,
+                                          int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+// K-major operand tile of rows x 32 bytes written by TMA with 32-byte swizzling: core matrices of 8 rows
+// x 16 bytes, 8-row groups 256 bytes apart (SBO), layout type SWIZZLE_32B, descriptor version 1
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(256 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(6) << 61);
+}
+// instruction descriptor: kind::i8, signed int8 A and B, int32 D, both K-major, M = 128, N = 64
+constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kBN >> 3) << 17) |
+                            (static_cast<uint32_t>(kBM >> 4) << 24);
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %5, %5, %5}, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate), "r"(0u));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void chunk_range(const TcArgs& a, int g, int& c0, int& c1) {
+  c0 = static_cast<int>(static_cast<long long>(a.nchunks) * g / a.groups);
+  c1 = static_cast<int>(static_cast<long long>(a.nchunks) * (g + 1) / a.groups);
+}
+
+template <int S>
+__global__ void __launch_bounds__(kThreads, 1)
+    ozaki_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy, TcArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte aligned stage buffers: [stage][X slices S x 4 KB | Y slices S x 2 KB]
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int kStageBytes = S * (kTileX + kTileY);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tmem_full = empty + kStages;
+  uint64_t* tmem_empty = tmem_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // TMEM: 512 columns (S diagonals x 64)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmx)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmy)) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---- TMA producer ----
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
+        const int4 job = a.items[it];
+        int c0, c1;
+        chunk_range(a, job.z, c0, c1);
+        for (int c = c0; c < c1; ++c)
+          for (int kb = 0; kb < a.kblocks; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            unsigned char* st = smem + stage * kStageBytes;
+            mbar_expect_tx(&full[stage], kStageBytes);
+#pragma unroll
+            for (int s = 1; s <= S; ++s)
+              tma_load4(&tmx, st + (s - 1) * kTileX, &full[stage], kb * kBK, a.x_rev ? S - s : s - 1, job.x * kBM, c);
+#pragma unroll
+            for (int t = 1; t <= S; ++t)
+              tma_load4(&tmy, st + S * kTileX + (t - 1) * kTileY, &full[stage], kb * kBK, a.y_rev ? S - t : t - 1,
+                        job.y * kBN, c);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer ----
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0, te_phase = 0;
+      for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
+        const int4 job = a.items[it];
+        int c0, c1;
+        chunk_range(a, job.z, c0, c1);
+        for (int c = c0; c < c1; ++c) {
+          mbar_wait(tmem_empty, te_phase ^ 1);  // the epilogue has read the previous accumulators
+          te_phase ^= 1;
+          tc_fence_after();
+          for (int kb = 0; kb < a.kblocks; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t sbase = smem_u32(smem + stage * kStageBytes);
+#pragma unroll
+            for (int s = 1; s <= S; ++s) {
+              const uint64_t da = smem_desc(sbase + (s - 1) * kTileX);
+#pragma unroll
+              for (int t = 1; t <= S + 1 - s; ++t) {
+                const uint64_t db = smem_desc(sbase + S * kTileX + (t - 1) * kTileY);
+                // diagonal s + t - 2; its first product (s = 1) of the chunk's first K step starts it
+                mma_i8(tmem + (s + t - 2) * kBN, da, db, (kb > 0 || s > 1) ? 1u : 0u);
+              }
+            }
+            mma_commit(&empty[stage]);  // frees the stage once these MMAs have read it
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          mma_commit(tmem_full);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---- epilogue: warps 2..5, TMEM lanes 32 (warp % 4) .. + 31 ----
+    const int quarter = warp & 3;
+    const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    uint32_t tf_phase = 0;
+    for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
+      const int4 job = a.items[it];
+      int c0, c1;
+      chunk_range(a, job.z, c0, c1);
+      const int x = job.x * kBM + quarter * 32 + lane;
+      const int y0 = job.y * kBN;
+      double acc[kBN];
+#pragma unroll
+      for (int e = 0; e < kBN; ++e) acc[e] = 0.0;
+      for (int c = c0; c < c1; ++c) {
+        mbar_wait(tmem_full, tf_phase);
+        tf_phase ^= 1;
+        tc_fence_after();
+        const double sxv = x < a.nx ? a.sx[static_cast<size_t>(a.cols ? c : 0) * a.nx + x] : 0.0;
+#pragma unroll
+        for (int q = 0; q < kBN / 16; ++q) {
+          // smallest diagonal first: exact products by powers of two, one rounding per add
+          double sq[16];
+          double w = 0x1p-14;
+#pragma unroll
+          for (int d = 0; d < S - 1; ++d) w *= 0x1p-7;  // 2^-7(S+1)
+#pragma unroll
+          for (int d = S - 1; d >= 0; --d) {
+            int v[16];
+            tmem_ld16(lane_addr + d * kBN + q * 16, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) sq[e] = d == S - 1 ? static_cast<double>(v[e]) * w : fma(static_cast<double>(v[e]), w, sq[e]);
+            w *= 128.0;
+          }
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int y = y0 + q * 16 + e;
+            const double syv = y < a.ny ? __ldg(&a.sy[static_cast<size_t>(a.cols ? c : 0) * a.ny + y]) : 0.0;
+            if (a.cols) acc[q * 16 + e] = fma(sq[e], sxv * syv, acc[q * 16 + e]);
+            else acc[q * 16 + e] = sq[e] * sxv * syv;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tmem_empty);
+      }
+      if (x < a.nx) {
+        double* o = a.out + (a.cols && a.groups > 1 ? job.z * a.part_stride : 0) + static_cast<long long>(x) * a.ldo + y0;
+        const int ny = min(kBN, a.ny - y0);
+        if (ny == kBN && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+#pragma unroll
+          for (int e = 0; e < kBN; e += 2) *reinterpret_cast<double2*>(o + e) = make_double2(acc[e], acc[e + 1]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < kBN; ++e)
+            if (e < ny) o[e] = acc[e];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// C (m x m, ldc) = sum_g P_g in group order; lower_only: then mirror the strictly upper triangle
+__global__ void reduce_groups_kernel(int nx, int ny, int groups, const double* __restrict__ P, long long ldp,
+                                     long long pstride, double* __restrict__ C, long long ldc) {
+  const long long total = static_cast<long long>(nx) * ny;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long x = e / ny, y = e - x * ny;
+    double s = P[x * ldp + y];
+    for (int g = 1; g < groups; ++g) s += P[g * pstride + x * ldp + y];
+    C[x * ldc + y] = s;
+  }
+}
+// symmetric products: rows x < y were not computed; C[x][y] = C[y][x] (bitwise: the products commute)
+__global__ void mirror_upper_kernel(int m, double* __restrict__ C, long long ldc) {
+  const long long total = static_cast<long long>(m) * m;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long x = e / m, y = e - x * m;
+    if (y > x) C[x * ldc + y] = C[y * ldc + x];
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      throw Error(kInternal, "ozaki_tc: cuTensorMapEncodeTiled is unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// 4-D map over int8 digits: (K bytes, slice, row, chunk) with byte strides (1, slice_stride, row_stride,
+// chunk_stride); box (32, 1, box_rows, 1), 32-byte swizzle, out-of-range rows read as zero digits
+CUtensorMap make_map(const int8_t* base, long long kext, int S, long long rows, int nch, long long slice_stride,
+                     long long row_stride, long long chunk_stride, int box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(kext), static_cast<cuuint64_t>(S), static_cast<cuuint64_t>(rows),
+                              static_cast<cuuint64_t>(nch)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(slice_stride), static_cast<cuuint64_t>(row_stride),
+                                 static_cast<cuuint64_t>(chunk_stride)};
+  const cuuint32_t box[4] = {static_cast<cuuint32_t>(kBK), 1u, static_cast<cuuint32_t>(box_rows), 1u};
+  const cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(base), dims, strides, box,
+                                 es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(kInternal, "ozaki_tc: cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return m;
+}
+
+template <int S>
+void launch_tc(stgp_ctx* ctx, const CUtensorMap& tx, const CUtensorMap& ty, const TcArgs& a) {
+  // at least 116 KB so that one CTA holds an SM: it owns all 512 TMEM columns
+  constexpr int smem = std::max(kStages * S * (kTileX + kTileY) + 1024 + 256, 116 * 1024);
+  static bool attr = false;
+  if (!attr) {
+    STGP_CUDA(cudaFuncSetAttribute(ozaki_tc_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  const int grid = std::min(a.nitems, ctx->num_sms);
+  ozaki_tc_kernel<S><<<grid, kThreads, smem, ctx->stream>>>(tx, ty, a);
+  launched(ctx);
+}
+
+void dispatch(stgp_ctx* ctx, int S, const CUtensorMap& tx, const CUtensorMap& ty, const TcArgs& a) {
+  switch (S) {
+    case 2: launch_tc<2>(ctx, tx, ty, a); break;
+    case 3: launch_tc<3>(ctx, tx, ty, a); break;
+    case 4: launch_tc<4>(ctx, tx, ty, a); break;
+    case 5: launch_tc<5>(ctx, tx, ty, a); break;
+    case 6: launch_tc<6>(ctx, tx, ty, a); break;
+    case 7: launch_tc<7>(ctx, tx, ty, a); break;
+    case 8: launch_tc<8>(ctx, tx, ty, a); break;
+    default: throw Error(kConfig, "ozaki_tc: slice count must lie in [2, 8]");
+  }
+}
+
+}  // namespace
+
+struct OzakiTcState {
+  DevBuf<int4> items;
+  DevBuf<double> part;
+};
+
+void ozaki_tc_release(OzakiTcState* s) { delete s; }
+
+static OzakiTcState* tc_state(OzakiTcState*& s) {
+  if (!s) s = new OzakiTcState();
+  return s;
+}
+
+// rows form: out[x ldo + y] = sx[x] sy[y] sum_d 2^-7d sum_{s+t=d} X_s[x] . Y_t[y]; X digits at
+// xd[x ldk + slot(s) kp + k], Y digits likewise (ldk = S kp, kp a multiple of 32)
+void ozaki_tc_rows(stgp_ctx* ctx, OzakiTcState*& st, int S, int kp, long long nx, int ny, const int8_t* xd, bool x_rev,
+                   const double* sx, const int8_t* yd, bool y_rev, const double* sy, double* out, long long ldo) {
+  if (kp % kBK) throw Error(kInternal, "ozaki_tc_rows: kp must be a multiple of 32");
+  OzakiTcState* s = tc_state(st);
+  const long long ldk = static_cast<long long>(S) * kp;
+  const CUtensorMap tx = make_map(xd, kp, S, nx, 1, kp, ldk, nx * ldk, kBM);
+  const CUtensorMap ty = make_map(yd, kp, S, ny, 1, kp, ldk, static_cast<long long>(ny) * ldk, kBN);
+  const int tiles_x = static_cast<int>((nx + kBM - 1) / kBM), tiles_y = (ny + kBN - 1) / kBN;
+  std::vector<int4> items;
+  items.reserve(static_cast<size_t>(tiles_x) * tiles_y);
+  for (int bx = 0; bx < tiles_x; ++bx)  // Y tiles fastest: the CTAs in flight share one X block in L2
+    for (int by = 0; by < tiles_y; ++by) items.push_back(make_int4(bx, by, 0, 0));
+  s->items.upload(items.data(), items.size(), ctx->stream);
+  TcArgs a{};
+  a.S = S;
+  a.kblocks = kp / kBK;
+  a.nx = static_cast<int>(nx);
+  a.ny = ny;
+  a.nchunks = 1;
+  a.groups = 1;
+  a.x_rev = x_rev;
+  a.y_rev = y_rev;
+  a.cols = 0;
+  a.nitems = static_cast<int>(items.size());
+  a.items = s->items.get();
+  a.sx = sx;
+  a.sy = sy;
+  a.out = out;
+  a.ldo = ldo;
+  dispatch(ctx, S, tx, ty, a);
+}
+
+// cols form: C[x ldc + y] = sum_c (sx[c m + x] sy[c m + y]) sum_d 2^-7d sum_{s+t=d} X_s,c[x] . Y_t,c[y];
+// digits at d[((c m + row) S + slot(s)) L + k]; symmetric: X and Y are one matrix, only tiles reaching
+// the lower triangle are computed and the upper triangle is mirrored
+void ozaki_tc_cols(stgp_ctx* ctx, OzakiTcState*& st, int S, int L, int nch, int m, const int8_t* xd, bool x_rev,
+                   const double* sx, const int8_t* yd, bool y_rev, const double* sy, bool symmetric, double* C,
+                   long long ldc) {
+  if (L % kBK) throw Error(kInternal, "ozaki_tc_cols: L must be a multiple of 32");
+  OzakiTcState* s = tc_state(st);
+  const long long rs = static_cast<long long>(S) * L;
+  const CUtensorMap tx = make_map(xd, L, S, m, nch, L, rs, static_cast<long long>(m) * rs, kBM);
+  const CUtensorMap ty = make_map(yd, L, S, m, nch, L, rs, static_cast<long long>(m) * rs, kBN);
+  const int tiles_x = (m + kBM - 1) / kBM, tiles_y = (m + kBN - 1) / kBN;
+  std::vector<int2> tiles;
+  for (int bx = 0; bx < tiles_x; ++bx)
+    for (int by = 0; by < tiles_y; ++by)
+      if (!symmetric || by * kBN < (bx + 1) * kBM) tiles.push_back(make_int2(bx, by));
+  // split the chunks of each tile over G CTAs so the work items fill whole waves of the SMs
+  const int nt = static_cast<int>(tiles.size());
+  int G = 1;
+  double best = 0.0;
+  for (int g = 1; g <= std::min(nch, 16); ++g) {
+    const long long it = static_cast<long long>(nt) * g;
+    const long long waves = (it + ctx->num_sms - 1) / ctx->num_sms;
+    const double eff = static_cast<double>(it) / (waves * ctx->num_sms) * (1.0 - 0.02 * (g - 1));
+    if (eff > best + 1e-9) {
+      best = eff;
+      G = g;
+    }
+  }
+  std::vector<int4> items;
+  for (int g = 0; g < G; ++g)
+    for (const int2& t : tiles) items.push_back(make_int4(t.x, t.y, g, 0));
+  s->items.upload(items.data(), items.size(), ctx->stream);
+  TcArgs a{};
+  a.S = S;
+  a.kblocks = L / kBK;
+  a.nx = m;
+  a.ny = m;
+  a.nchunks = nch;
+  a.groups = G;
+  a.x_rev = x_rev;
+  a.y_rev = y_rev;
+  a.cols = 1;
+  a.nitems = static_cast<int>(items.size());
+  a.items = s->items.get();
+  a.sx = sx;
+  a.sy = sy;
+  const long long ldp = (m + 1) / 2 * 2;
+  if (G > 1) {
+    a.part_stride = static_cast<long long>(m) * ldp;
+    s->part.ensure(static_cast<size_t>(G) * a.part_stride);
+    a.out = s->part.get();
+    a.ldo = ldp;
+  } else {
+    a.out = C;
+    a.ldo = ldc;
+  }
+  dispatch(ctx, S, tx, ty, a);
+  if (G > 1) {
+    reduce_groups_kernel<<<grid_for(static_cast<long long>(m) * m, 256), 256, 0, ctx->stream>>>(
+        m, m, G, s->part.get(), ldp, a.part_stride, C, ldc);
+    launched(ctx);
+  }
+  if (symmetric) {
+    mirror_upper_kernel<<<grid_for(static_cast<long long>(m) * m, 256), 256, 0, ctx->stream>>>(m, C, ldc);
+    launched(ctx);
+  }
+}
+
+}  // namespace stgp

@@ -7,6 +7,11 @@ arrays) and compare the CUDA path with these values.
 
     python tests/golden/make_golden.py [case ...]      (cases: cfg2 cfg3 cfg4g cfg4s cfg5s; default all)
 
+Searches and kMeans++ always run the sequential-order restatement (their outputs are defined bit for bit).
+At M ~ 900-1900 the NLL / gradient / prediction of cfg4g and cfg5s take the oracle's BLAS mode for the
+dense n x M^2 contractions (oracle.set_blas; it agrees with the sequential restatement to ~1e-14, see
+tests/test_oracle_pinning.py::test_blas_mode_matches_sequential), which the tolerances dwarf.
+
 Each case is one compressed .npz next to this script.  Full neighbour sets are stored as the SHA-256 of
 their n x m_v int32 array (ascending, -1 padded) plus 2000 sampled rows for diagnosis.
 """
@@ -41,13 +46,15 @@ CASES = {
     "cfg3": dict(stations=1000, days=100, box=(1.0, 1.0), theta=synth.THETA_SEC4, kind="vif", m_v=20, m=200),
     # cfg4 geometry at n = 2e4: 1000 stations x 20 days in the cfg4 box, theta T3, m = 1000 -> M = 224 x 4 = 896
     # (>= 512: the default int8 Ozaki products are what is compared)
-    "cfg4g": dict(stations=1000, days=20, box=BOX4, theta=synth.THETA_T3, kind="vif", m_v=30, m=1000),
+    "cfg4g": dict(stations=1000, days=20, box=BOX4, theta=synth.THETA_T3, kind="vif", m_v=30, m=1000,
+                  blas=True),
     # cfg4 itself: sts (M = 906) and the d_r sets of 2000 sampled query rows against all their predecessors
     "cfg4s": dict(stations=10000, days=110, box=BOX4, theta=synth.THETA_T3, kind="dr-sample", m_v=30, m=1000,
                   rows=2000),
     # cfg5 shape at reduced n: FITC with sts m = 2000 on 2000 stations x 10 days (M = 632 x 3 = 1896), NLL,
     # gradient and the 1-day-ahead predictive mean / variance at every station
-    "cfg5s": dict(stations=2000, days=10, box=BOX4, theta=synth.THETA_T3, kind="fitc", m=2000),
+    "cfg5s": dict(stations=2000, days=10, box=BOX4, theta=synth.THETA_T3, kind="fitc", m=2000,
+                  blas=True),
 }
 
 
@@ -81,6 +88,7 @@ def sampled_rows(n, k, seed=SEED):
 
 def make(name):
     c = CASES[name]
+    O.set_blas(False)
     th = c["theta"]
     x, y, t, r = inputs(c)
     out = {"input_sha": input_sha(x, y, t, r), "theta": np.array(th)}
@@ -93,6 +101,7 @@ def make(name):
     elif c["kind"] == "vif":
         Z, ms, mt = O.sts_kmeanspp(x, y, t, c["m"], SEED)
         nbr = O.dr_neighbors_rows(x, y, t, th, Z, c["m_v"])
+        O.set_blas(bool(c.get("blas")), os.cpu_count() or 1)
         om = O.OracleModel("vif", x, y, t, th, nbr=nbr, Z=Z)
         out.update(Z=Z, ms=ms, mt=mt, **pack_sets(nbr), nll=om.nll(r))
         out["grad"], out["scale"] = om.nll_grad_scale(r)
@@ -108,6 +117,7 @@ def make(name):
                    gap=dist[:, m] - dist[:, m - 1])
     elif c["kind"] == "fitc":
         Z, ms, mt = O.sts_kmeanspp(x, y, t, c["m"], SEED)
+        O.set_blas(bool(c.get("blas")), os.cpu_count() or 1)
         om = O.OracleModel("fitc", x, y, t, th, Z=Z)
         out.update(Z=Z, ms=ms, mt=mt, nll=om.nll(r))
         out["grad"], out["scale"] = om.nll_grad_scale(r)
@@ -116,6 +126,7 @@ def make(name):
         mu, var = om.predict(r, targets, 0)
         out.update(targets=targets, mu=mu, var=var)
     out["oracle_s"] = time.time() - t0
+    out["dense"] = "openblas" if c.get("blas") else "sequential"
     path = os.path.join(HERE, f"{name}.npz")
     np.savez_compressed(path, **out)
     print(f"{name}: {time.time() - t0:.1f} s -> {os.path.getsize(path) / 1e6:.2f} MB", flush=True)

@@ -441,3 +441,26 @@ def test_ordering_properties():
     assert (np.diff(t[perm]) >= 0).all()
     assert (O.order_observations(t, 42) == perm).all()
     assert not (O.order_observations(t, 43) == perm).all()
+
+
+@pytest.mark.parametrize("kind", ["fitc", "vif"])
+def test_blas_mode_matches_sequential(kind):
+    """The oracle's BLAS timing mode (dense n x M^2 contractions on OpenBLAS) equals the sequential
+    restatement up to rounding: NLL 1e-12 relative, gradient 1e-12 of the per-component scale."""
+    if O.openblas_path() is None:
+        pytest.skip("no scipy OpenBLAS in this image")
+    x, y, t, yv, _ = O.test_dataset(1, 1200, 5, n_times=6)
+    th = (0.05, 1.0, 0.5, 20.0, 0.4, 1.5, 0.4, 0.2)
+    nb = O.dc_neighbors(x, y, t, th, 12) if kind == "vif" else None
+    Z = np.column_stack([x, y, t])[::17]
+    res = []
+    try:
+        for mode in (False, True):
+            O.set_blas(mode, 4)
+            om = O.OracleModel(kind, x, y, t, th, nbr=nb, Z=Z)
+            res.append((om.nll(yv),) + om.nll_grad_scale(yv))
+    finally:
+        O.set_blas(False)
+    (v0, g0, sc), (v1, g1, _) = res
+    assert v1 == pytest.approx(v0, rel=1e-12)
+    assert (np.abs(g1 - g0) <= 1e-12 * sc).all()
