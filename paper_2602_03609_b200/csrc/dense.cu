@@ -6,51 +6,84 @@
 
 namespace stgp {
 
-void cublas_check(cublasStatus_t s, const char* what) {
-  if (s != CUBLAS_STATUS_SUCCESS) throw Error(kInternal, std::string("cuBLAS ") + what + " failed: " + std::to_string(s));
-}
-
 namespace {
 
 constexpr int kNB = 64;
 
-// Factor one diagonal block (nb <= 64) in place with one CTA; flags[0] = 1 on a
-// non-positive pivot.  Right-looking, column by column.
-__global__ void potrf_diag_kernel(double* A, int ld, int j0, int nb, int* flag) {
+// Factor one diagonal block (nb <= 64) in place; flag[0] = 1 on a non-positive pivot.  Left-looking,
+// thread r owns row r: column j is s[r][j] - sum_{k<j} s[r][k] s[j][k] (sequential in k), then the
+// pivot's square root and the division.
+__global__ void __launch_bounds__(kNB) potrf_diag_kernel(double* A, int ld, int j0, int nb, int* flag) {
   __shared__ double s[kNB][kNB + 1];
-  const int tid = threadIdx.x;
-  for (int e = tid; e < nb * nb; e += blockDim.x) {
-    const int r = e % nb, c = e / nb;
-    s[r][c] = A[static_cast<size_t>(j0 + c) * ld + j0 + r];
-  }
-  __syncthreads();
   __shared__ int bad;
-  if (tid == 0) bad = 0;
+  const int r = threadIdx.x;
+  for (int e = r; e < nb * nb; e += kNB) {
+    const int rr = e % nb, c = e / nb;
+    s[rr][c] = A[static_cast<size_t>(j0 + c) * ld + j0 + rr];
+  }
+  if (r == 0) bad = 0;
   __syncthreads();
   for (int j = 0; j < nb; ++j) {
-    if (tid == 0) {
-      const double p = s[j][j];
-      if (!(p > 0.0)) bad = 1;
-      s[j][j] = sqrt(p);
+    if (r >= j && r < nb) {
+      double v = s[r][j];
+      for (int k = 0; k < j; ++k) v = fma(-s[r][k], s[j][k], v);
+      s[r][j] = v;
     }
     __syncthreads();
-    if (bad) break;
-    const double d = s[j][j];
-    for (int r = j + 1 + tid; r < nb; r += blockDim.x) s[r][j] /= d;
-    __syncthreads();
-    for (int e = tid; e < (nb - j - 1) * (nb - j - 1); e += blockDim.x) {
-      const int r = j + 1 + e % (nb - j - 1), c = j + 1 + e / (nb - j - 1);
-      if (c <= r) s[r][c] = fma(-s[r][j], s[c][j], s[r][c]);
+    const double p = s[j][j];
+    if (!(p > 0.0)) {
+      if (r == 0) bad = 1;
+      break;
     }
+    const double d = sqrt(p);
+    if (r > j && r < nb) s[r][j] /= d;
     __syncthreads();
+    if (r == j) s[j][j] = d;
   }
+  __syncthreads();
   if (bad) {
-    if (tid == 0) *flag = 1;
+    if (r == 0) *flag = 1;
     return;
   }
-  for (int e = tid; e < nb * nb; e += blockDim.x) {
-    const int r = e % nb, c = e / nb;
-    if (c <= r) A[static_cast<size_t>(j0 + c) * ld + j0 + r] = s[r][c];
+  for (int e = r; e < nb * nb; e += kNB) {
+    const int rr = e % nb, c = e / nb;
+    if (c <= rr) A[static_cast<size_t>(j0 + c) * ld + j0 + rr] = s[rr][c];
+  }
+}
+
+// Inverse of the nb x nb lower-triangular block L[j0.., j0..] (nb <= 64) into Inv (ld 64, zero upper part):
+// thread c solves L x = e_c by forward substitution (column c of the inverse); transpose = 1 stores the
+// inverse transposed (Inv = L^{-T}).
+__global__ void __launch_bounds__(kNB) tri_inv64_kernel(const double* L, long long ld, int j0, int nb, double* Inv,
+                                                        int transpose, int n) {
+  if (n > 0) {  // batched: block blockIdx.x of an n x n factor, inverse at Inv + blockIdx.x 64^2
+    j0 = blockIdx.x * kNB;
+    nb = min(kNB, n - j0);
+    Inv += static_cast<size_t>(blockIdx.x) * kNB * kNB;
+  }
+  extern __shared__ double inv_sm[];  // s[kNB][kNB + 1] then x[kNB][kNB + 1] (x[r][c])
+  double (*s)[kNB + 1] = reinterpret_cast<double (*)[kNB + 1]>(inv_sm);
+  double (*x)[kNB + 1] = reinterpret_cast<double (*)[kNB + 1]>(inv_sm + kNB * (kNB + 1));
+  const int c = threadIdx.x;
+  for (int e = c; e < nb * nb; e += kNB) {
+    const int rr = e % nb, cc = e / nb;
+    s[rr][cc] = cc <= rr ? L[static_cast<size_t>(j0 + cc) * ld + j0 + rr] : 0.0;
+  }
+  __syncthreads();
+  if (c < nb) {
+    for (int r = 0; r < c; ++r) x[r][c] = 0.0;
+    for (int r = c; r < nb; ++r) {
+      double v = r == c ? 1.0 : 0.0;
+      for (int q = c; q < r; ++q) v = fma(-s[r][q], x[q][c], v);
+      x[r][c] = v / s[r][r];
+    }
+  }
+  __syncthreads();
+  for (int e = c; e < kNB * kNB; e += kNB) {
+    const int rr = e % kNB, cc = e / kNB;
+    const double v = rr < nb && cc < nb ? x[rr][cc] : 0.0;
+    if (transpose) Inv[rr * kNB + cc] = v;  // column-major, ld 64: Inv(cc, rr) = x[rr][cc]
+    else Inv[cc * kNB + rr] = v;
   }
 }
 
@@ -75,30 +108,174 @@ __global__ void symmetrize_kernel(double* A, int ld, int n) {
   }
 }
 
+
+// L x = b (or L^T x = b) for one right-hand side in one CTA: 32-row blocks, the diagonal block by one
+// warp, the update of the remaining rows by the whole CTA with coalesced column (forward) or row-dot
+// (backward) reads of L
+constexpr int kTv = 1024;
+__global__ void __launch_bounds__(kTv) trsv_kernel(const double* __restrict__ L, long long ld, int n, double* __restrict__ b,
+                                                  int transpose) {
+  __shared__ double xs[32];
+  __shared__ double dg[32][33];  // dg[c][r] = L[j0 + r][j0 + c]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (!transpose) {
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int nb = min(32, n - j0);
+      for (int e = tid; e < nb * 32; e += kTv) {  // the diagonal block, coalesced, into shared memory
+        const int r = e & 31, c = e >> 5;
+        if (r < nb) dg[c][r] = L[static_cast<size_t>(j0 + c) * ld + j0 + r];
+      }
+      __syncthreads();
+      if (warp == 0) {  // lane r owns row j0 + r of the block
+        double v = lane < nb ? b[j0 + lane] : 0.0;
+        for (int c = 0; c < nb; ++c) {
+          const double xc = __shfl_sync(0xffffffffu, v / dg[c][c], c);
+          if (lane == c) v = xc;
+          if (lane > c && lane < nb) v = fma(-dg[c][lane], xc, v);
+        }
+        if (lane < nb) {
+          b[j0 + lane] = v;
+          xs[lane] = v;
+        }
+      }
+      __syncthreads();
+      for (int r = j0 + nb + tid; r < n; r += kTv) {
+        double v = b[r];
+        for (int c = 0; c < nb; ++c) v = fma(-L[static_cast<size_t>(j0 + c) * ld + r], xs[c], v);
+        b[r] = v;
+      }
+      __syncthreads();
+    }
+  } else {
+    for (int j1 = n; j1 > 0; j1 -= 32) {
+      const int j0 = max(0, j1 - 32), nb = j1 - j0;
+      for (int e = tid; e < nb * 32; e += kTv) {
+        const int r = e & 31, c = e >> 5;
+        if (r < nb) dg[c][r] = L[static_cast<size_t>(j0 + c) * ld + j0 + r];
+      }
+      __syncthreads();
+      if (warp == 0) {  // backward within the block: lane r owns row j0 + r
+        double v = lane < nb ? b[j0 + lane] : 0.0;
+        for (int c = nb - 1; c >= 0; --c) {
+          const double xc = __shfl_sync(0xffffffffu, v / dg[c][c], c);
+          if (lane == c) v = xc;
+          if (lane < c) v = fma(-dg[lane][c], xc, v);
+        }
+        if (lane < nb) {
+          b[j0 + lane] = v;
+          xs[lane] = v;
+        }
+      }
+      __syncthreads();
+      // rows r < j0: b[r] -= sum_c L[j0 + c][r] x[c] -- a warp per row, lanes over c (contiguous)
+      for (int r = warp; r < j0; r += kTv / 32) {
+        double v = lane < nb ? L[static_cast<size_t>(r) * ld + j0 + lane] * xs[lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) b[r] -= v;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// y = alpha A x + beta y (A m x n col-major, n long): block b sums its column range into P[b][.]
+// (four interleaved partial sums per row keep four loads in flight)
+__global__ void gemv_n_part_kernel(int m, long long n, const double* __restrict__ A, long long lda,
+                                   const double* __restrict__ x, double* __restrict__ P) {
+  const long long c0 = n * blockIdx.x / gridDim.x, c1 = n * (blockIdx.x + 1) / gridDim.x;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    long long c = c0;
+    for (; c + 4 <= c1; c += 4) {
+      s0 = fma(A[r + c * lda], __ldg(&x[c]), s0);
+      s1 = fma(A[r + (c + 1) * lda], __ldg(&x[c + 1]), s1);
+      s2 = fma(A[r + (c + 2) * lda], __ldg(&x[c + 2]), s2);
+      s3 = fma(A[r + (c + 3) * lda], __ldg(&x[c + 3]), s3);
+    }
+    for (; c < c1; ++c) s0 = fma(A[r + c * lda], __ldg(&x[c]), s0);
+    P[static_cast<size_t>(blockIdx.x) * m + r] = (s0 + s1) + (s2 + s3);
+  }
+}
+__global__ void gemv_n_reduce_kernel(int m, int parts, const double* __restrict__ P, double alpha, double beta,
+                                     double* __restrict__ y) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < parts; ++b) s += P[static_cast<size_t>(b) * m + r];
+    y[r] = beta == 0.0 ? alpha * s : fma(alpha, s, beta * y[r]);
+  }
+}
+// y = alpha A^T x + beta y: one warp per column of A
+__global__ void gemv_t_kernel(int m, long long n, const double* __restrict__ A, long long lda,
+                              const double* __restrict__ x, double alpha, double beta, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  for (long long c = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; c < n;
+       c += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+    const double* a = A + c * lda;
+    double s = 0.0;
+    for (int r = lane; r < m; r += 32) s = fma(a[r], __ldg(&x[r]), s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) y[c] = beta == 0.0 ? alpha * s : fma(alpha, s, beta * y[c]);
+  }
+}
+__global__ void transpose_kernel(int rows, int cols, const double* __restrict__ A, long long lda, double* __restrict__ T,
+                                 long long ldt) {
+  __shared__ double tile[32][33];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + threadIdx.x, c = c0 + i;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = A[r + static_cast<long long>(c) * lda];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + threadIdx.x, r = r0 + i;
+    if (r < rows && c < cols) T[c + static_cast<long long>(r) * ldt] = tile[threadIdx.x][i];
+  }
+}
+
+constexpr int kInvSmem = 2 * kNB * (kNB + 1) * 8;
+void launch_tri_inv64(stgp_ctx* ctx, const double* L, long long ld, int j0, int nb, double* Inv, int transpose,
+                      int batched_n = 0) {
+  static bool attr = false;
+  if (!attr) {
+    STGP_CUDA(cudaFuncSetAttribute(tri_inv64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kInvSmem));
+    attr = true;
+  }
+  const int grid = batched_n > 0 ? (batched_n + kNB - 1) / kNB : 1;
+  tri_inv64_kernel<<<grid, kNB, kInvSmem, ctx->stream>>>(L, ld, j0, nb, Inv, transpose, batched_n);
+  ++ctx->launches;
+  STGP_LAUNCH_CHECK();
+}
+
 }  // namespace
 
+// Blocked right-looking Cholesky: diagonal block (potrf_diag_kernel), panel A21 L11^{-T} through the
+// block's explicit inverse (tri_inv64_kernel) on the DMMA GEMM, trailing update A22 -= A21 A21^T on the
+// DMMA GEMM.
 bool dev_cholesky(stgp_ctx* ctx, double* A, int ld, int n) {
   DevBuf<int>& flag = ctx->iscr;
   flag.ensure(1);
+  DevBuf<double>& inv = ctx->dense_inv;
+  inv.ensure(kNB * kNB);
+  DevBuf<double>& T = ctx->dense_tmp;
+  T.ensure(static_cast<size_t>(std::max(n, 1)) * kNB);
   STGP_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), ctx->stream));
-  const double one = 1.0, mone = -1.0;
   for (int j0 = 0; j0 < n; j0 += kNB) {
     const int nb = std::min(kNB, n - j0);
-    potrf_diag_kernel<<<1, 256, 0, ctx->stream>>>(A, ld, j0, nb, flag.get());
+    potrf_diag_kernel<<<1, kNB, 0, ctx->stream>>>(A, ld, j0, nb, flag.get());
     ++ctx->launches;
     STGP_LAUNCH_CHECK();
     const int rest = n - j0 - nb;
-    if (rest > 0) {
-      // A21 <- A21 L11^{-T}
-      cublas_check(cublasDtrsm(ctx->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
-                               CUBLAS_DIAG_NON_UNIT, rest, nb, &one, A + static_cast<size_t>(j0) * ld + j0, ld,
-                               A + static_cast<size_t>(j0) * ld + j0 + nb, ld),
-                   "trsm(potrf)");
-      // A22 <- A22 - A21 A21^T
-      cublas_check(cublasDsyrk(ctx->cublas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, rest, nb, &mone,
-                               A + static_cast<size_t>(j0) * ld + j0 + nb, ld, &one,
-                               A + static_cast<size_t>(j0 + nb) * ld + j0 + nb, ld),
-                   "syrk(potrf)");
+    if (rest > 0) {  // A21 <- A21 L11^{-T} = A21 (L11^{-1})^T on the DMMA GEMM (through a copy), then
+                     // A22 -= A21 A21^T
+      launch_tri_inv64(ctx, A, ld, j0, nb, inv.get(), 0);
+      double* A21 = A + static_cast<size_t>(j0) * ld + j0 + nb;
+      double* A22 = A + static_cast<size_t>(j0 + nb) * ld + j0 + nb;
+      dev_gemm_tri(ctx, false, true, rest, nb, nb, 1.0, A21, ld, inv.get(), kNB, 0.0, T.get(), rest, 0);
+      STGP_CUDA(cudaMemcpy2DAsync(A21, sizeof(double) * ld, T.get(), sizeof(double) * rest, sizeof(double) * rest, nb,
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+      dev_gemm_tri(ctx, false, true, rest, rest, nb, -1.0, A21, ld, A21, ld, 1.0, A22, ld, 0);
     }
   }
   int h = 0;
@@ -119,15 +296,69 @@ double dev_logdet_chol(stgp_ctx* ctx, const double* L, int ld, int n) {
   return h;
 }
 
+// B <- op(L)^{-1} B, L lower (only its lower triangle is read).  One right-hand side: trsv_kernel.
+// Several: left-looking 64-row blocks -- subtract the solved part with the DMMA GEMM, then apply the
+// diagonal block's explicit inverse with the DMMA GEMM.
 void dev_trsm_left(stgp_ctx* ctx, const double* L, int ldl, int n, double* B, int ldb, long long ncols, bool transpose) {
-  const double one = 1.0;
-  const long long chunk = std::max<long long>(1, ((1LL << 31) - 1) / ldb);  // < 2^31 elements per call
-  for (long long c0 = 0; c0 < ncols; c0 += chunk) {
-    const int nc = static_cast<int>(std::min(chunk, ncols - c0));
-    cublas_check(cublasDtrsm(ctx->cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, transpose ? CUBLAS_OP_T : CUBLAS_OP_N,
-                             CUBLAS_DIAG_NON_UNIT, n, nc, &one, L, ldl, B + static_cast<size_t>(c0) * ldb, ldb),
-                 "trsm");
+  if (n <= 0 || ncols <= 0) return;
+  if (ncols == 1) {
+    trsv_kernel<<<1, kTv, 0, ctx->stream>>>(L, ldl, n, B, transpose ? 1 : 0);
+    ++ctx->launches;
+    STGP_LAUNCH_CHECK();
+    return;
   }
+  const int nbk = (n + kNB - 1) / kNB;
+  DevBuf<double>& inv = ctx->dense_inv;  // every diagonal block's inverse, one launch
+  inv.ensure(static_cast<size_t>(nbk) * kNB * kNB);
+  launch_tri_inv64(ctx, L, ldl, 0, 0, inv.get(), transpose ? 1 : 0, n);
+  DevBuf<double>& T = ctx->dense_tmp2;
+  T.ensure(static_cast<size_t>(kNB) * ncols);
+  for (int q = 0; q < nbk; ++q) {
+    const int blk = transpose ? nbk - 1 - q : q;
+    const int j0 = blk * kNB, nb = std::min(kNB, n - j0);
+    if (!transpose && j0 > 0)  // B[j0:j0+nb] -= L[j0:j0+nb, 0:j0] X[0:j0]
+      dev_gemm_tri(ctx, false, false, nb, static_cast<int>(ncols), j0, -1.0, L + j0, ldl, B, ldb, 1.0, B + j0, ldb, 0);
+    if (transpose && j0 + nb < n)  // B[j0:j0+nb] -= L[j0+nb:n, j0:j0+nb]^T X[j0+nb:n]
+      dev_gemm_tri(ctx, true, false, nb, static_cast<int>(ncols), n - j0 - nb, -1.0,
+                   L + static_cast<size_t>(j0) * ldl + j0 + nb, ldl, B + j0 + nb, ldb, 1.0, B + j0, ldb, 0);
+    // X[j0:j0+nb] = L_jj^{-1} B[j0:j0+nb] (or L_jj^{-T}): the block's explicit inverse on the GEMM
+    dev_gemm_tri(ctx, false, false, nb, static_cast<int>(ncols), nb, 1.0, inv.get() + static_cast<size_t>(blk) * kNB * kNB,
+                 kNB, B + j0, ldb, 0.0, T.get(), nb, 0);
+    STGP_CUDA(cudaMemcpy2DAsync(B + j0, sizeof(double) * ldb, T.get(), sizeof(double) * nb, sizeof(double) * nb, ncols,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+}
+
+// out = (L L^T)^{-1} = L^{-T} L^{-1} from the Cholesky factor (LAPACK potri: triangular inverse, then the
+// product), exactly symmetric (each entry one DMMA chain over k, the same for (i, j) and (j, i))
+void dev_chol_inverse(stgp_ctx* ctx, const double* L, int ld, int n, double* out) {
+  DevBuf<double>& T = ctx->dense_tmp3;
+  T.ensure(static_cast<size_t>(ld) * n);
+  dev_tri_inverse(ctx, L, ld, n, T.get());
+  dev_gemm_tri(ctx, true, false, n, n, n, 1.0, T.get(), ld, T.get(), ld, 0.0, out, ld, 2);
+}
+
+// W <- Linv^T W Linv (n x n) with an explicit lower-triangular inverse factor (zero upper part)
+void dev_congruence_t(stgp_ctx* ctx, const double* Linv, int ld, int n, double* W) {
+  DevBuf<double>& T = ctx->dense_tmp3;
+  T.ensure(static_cast<size_t>(ld) * n);
+  dev_gemm_tri(ctx, false, false, n, n, n, 1.0, W, ld, Linv, ld, 0.0, T.get(), ld, 0);
+  dev_gemm_tri(ctx, true, false, n, n, n, 1.0, Linv, ld, T.get(), ld, 0.0, W, ld, 2);
+}
+
+// B (nrows x n) <- B L^{-1}: X L = B is L^T X^T = B^T, solved on the transposed copy
+void dev_trsm_right(stgp_ctx* ctx, const double* L, int ldl, int n, double* B, int ldb, int nrows) {
+  if (n <= 0 || nrows <= 0) return;
+  DevBuf<double>& T = ctx->dense_tmp;
+  const int ldt = (n + 1) / 2 * 2;
+  T.ensure(static_cast<size_t>(ldt) * nrows);
+  const dim3 blk(32, 8);
+  transpose_kernel<<<dim3((n + 31) / 32, (nrows + 31) / 32), blk, 0, ctx->stream>>>(nrows, n, B, ldb, T.get(), ldt);
+  ++ctx->launches;
+  dev_trsm_left(ctx, L, ldl, n, T.get(), ldt, nrows, true);
+  transpose_kernel<<<dim3((nrows + 31) / 32, (n + 31) / 32), blk, 0, ctx->stream>>>(n, nrows, T.get(), ldt, B, ldb);
+  ++ctx->launches;
+  STGP_LAUNCH_CHECK();
 }
 
 static __global__ void identity_kernel(double* A, int ld, int n) {
@@ -137,6 +368,7 @@ static __global__ void identity_kernel(double* A, int ld, int n) {
     A[e] = (e % ld == e / ld) ? 1.0 : 0.0;
 }
 
+// Linv = L^{-1}: lower triangular with an exactly zero upper part (the solve of L X = I gives 0 there)
 void dev_tri_inverse(stgp_ctx* ctx, const double* L, int ld, int n, double* Linv) {
   const long long total = static_cast<long long>(ld) * n;
   identity_kernel<<<static_cast<int>(std::min<long long>((total + 255) / 256, 4096)), 256, 0, ctx->stream>>>(Linv, ld, n);
@@ -145,36 +377,30 @@ void dev_tri_inverse(stgp_ctx* ctx, const double* L, int ld, int n, double* Linv
   dev_trsm_left(ctx, L, ld, n, Linv, ld, n, false);
 }
 
+// C = op(T) B for an explicit lower-triangular T whose upper part is zero (dev_tri_inverse): the DMMA
+// GEMM over each row block's support (k <= i, or k >= i for T^T)
 void dev_trmm_left(stgp_ctx* ctx, const double* T, int ldt, int n, const double* B, int ldb, long long ncols,
                    bool transpose, double* C, int ldc) {
-  const double one = 1.0;
-  const long long chunk = std::max<long long>(1, ((1LL << 31) - 1) / std::max(ldb, ldc));  // < 2^31 elements per call
+  const long long chunk = 65535LL * 128;  // grid.x limit of the GEMM is far above; keep launches < 2^31 elements
   for (long long c0 = 0; c0 < ncols; c0 += chunk) {
     const int nc = static_cast<int>(std::min(chunk, ncols - c0));
-    cublas_check(cublasDtrmm(ctx->cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, transpose ? CUBLAS_OP_T : CUBLAS_OP_N,
-                             CUBLAS_DIAG_NON_UNIT, n, nc, &one, T, ldt, B + static_cast<size_t>(c0) * ldb, ldb,
-                             C + static_cast<size_t>(c0) * ldc, ldc),
-                 "trmm");
+    dev_gemm_tri(ctx, transpose, false, n, nc, n, 1.0, T, ldt, B + static_cast<size_t>(c0) * ldb, ldb, 0.0,
+                 C + static_cast<size_t>(c0) * ldc, ldc, transpose ? 2 : 1);
   }
 }
 
 void dev_syrk(stgp_ctx* ctx, int n, long long k, double alpha, const double* A, int lda, double beta, double* C,
               int ldc) {
-  cublas_check(cublasDsyrk(ctx->cublas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, n, static_cast<int>(k), &alpha, A, lda,
-                           &beta, C, ldc),
-               "syrk");
+  dev_gemm_tri(ctx, false, true, n, n, k, alpha, A, lda, A, lda, beta, C, ldc, 0);
 }
 
 void dev_gemm(stgp_ctx* ctx, bool ta, bool tb, int m, int n, long long k, double alpha, const double* A, int lda,
               const double* B, int ldb, double beta, double* C, int ldc) {
-  cublas_check(cublasDgemm(ctx->cublas, ta ? CUBLAS_OP_T : CUBLAS_OP_N, tb ? CUBLAS_OP_T : CUBLAS_OP_N, m, n,
-                           static_cast<int>(k), &alpha, A, lda, B, ldb, &beta, C, ldc),
-               "gemm");
+  dev_gemm_tri(ctx, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, 0);
 }
 
-// C = alpha A A^T (n x n, both triangles) as GEMMs on the lower blocks of an nb x nb partition:
-// (nb + 1) / (2 nb) of the full product's flops at GEMM efficiency (cuBLAS SYRK tiles this
-// small-output / long-K shape poorly).  Block edges are multiples of 16.
+// C = alpha A A^T (n x n, both triangles) as GEMMs on the lower blocks of an nb x nb partition,
+// mirrored.  Block edges are multiples of 16.
 void dev_syrk_blocked(stgp_ctx* ctx, int n, long long k, double alpha, const double* A, int lda, double* C, int ldc,
                       int nb) {
   nb = std::max(1, std::min(nb, (n + 15) / 16));
@@ -205,9 +431,21 @@ void dev_gemm_sym_blocked(stgp_ctx* ctx, int n, long long k, double alpha, const
 
 void dev_gemv(stgp_ctx* ctx, bool ta, int m, long long n, double alpha, const double* A, int lda, const double* x,
               double beta, double* y) {
-  cublas_check(cublasDgemv(ctx->cublas, ta ? CUBLAS_OP_T : CUBLAS_OP_N, m, static_cast<int>(n), &alpha, A, lda, x, 1,
-                           &beta, y, 1),
-               "gemv");
+  if (m <= 0 || n <= 0) return;
+  if (ta) {
+    gemv_t_kernel<<<static_cast<int>(std::min<long long>((n * 32 + 255) / 256, ctx->num_sms * 64LL)), 256, 0,
+                    ctx->stream>>>(m, n, A, lda, x, alpha, beta, y);
+    ++ctx->launches;
+    STGP_LAUNCH_CHECK();
+    return;
+  }
+  const int parts = static_cast<int>(std::max<long long>(1, std::min<long long>(n / 256, ctx->num_sms * 4LL)));
+  DevBuf<double>& P = ctx->dense_tmp;
+  P.ensure(static_cast<size_t>(parts) * m);
+  gemv_n_part_kernel<<<parts, 256, 0, ctx->stream>>>(m, n, A, lda, x, P.get());
+  gemv_n_reduce_kernel<<<(m + 255) / 256, 256, 0, ctx->stream>>>(m, parts, P.get(), alpha, beta, y);
+  ctx->launches += 2;
+  STGP_LAUNCH_CHECK();
 }
 
 void dev_symmetrize_lower(stgp_ctx* ctx, double* A, int ld, int n) {

@@ -1,11 +1,8 @@
-// Dense FP64 linear algebra on the device for the M x M / M x n low-rank pieces.
-// Large contractions (TRSM, SYRK, GEMM over n columns) are plain library
-// products (cuBLAS, FP64 tensor cores); the blocked Cholesky drives them with a
-// hand-written diagonal-block factorization that reports failure instead of
-// producing NaNs (Eigen's LLT info() semantics, used by the jitter ladders).
+// Dense FP64 linear algebra on the device for the M x M / M x n low-rank pieces, all on the repo's own
+// kernels: the DMMA GEMM of dgemm.cu (TRMM with explicit triangular factors, SYRK as lower-block GEMMs,
+// split-K long reductions), blocked triangular solves and a blocked Cholesky that reports failure
+// instead of producing NaNs (Eigen's LLT info() semantics, used by the jitter ladders).
 #pragma once
-
-#include <cublas_v2.h>
 
 #include "common.cuh"
 
@@ -13,7 +10,16 @@ struct stgp_ctx;
 
 namespace stgp {
 
-void cublas_check(cublasStatus_t s, const char* what);
+// C = alpha op(A) op(B) + beta C (column-major, DMMA); tri: 0 general, 1 op(A) lower with a zero upper
+// part (row i sums k <= i), 2 op(A) upper with a zero lower part (k >= i)
+void dev_gemm_tri(stgp_ctx* ctx, bool ta, bool tb, int m, int n, long long k, double alpha, const double* A,
+                  long long lda, const double* B, long long ldb, double beta, double* C, long long ldc, int tri);
+// out = (L L^T)^{-1} from the Cholesky factor L (explicit, exactly symmetric)
+void dev_chol_inverse(stgp_ctx* ctx, const double* L, int ld, int n, double* out);
+// W <- Linv^T W Linv for an explicit lower-triangular Linv (zero upper part)
+void dev_congruence_t(stgp_ctx* ctx, const double* Linv, int ld, int n, double* W);
+// B (nrows x n, ldb) <- B L^{-1} for lower-triangular L
+void dev_trsm_right(stgp_ctx* ctx, const double* L, int ldl, int n, double* B, int ldb, int nrows);
 
 // In-place lower Cholesky of the leading n x n block of A (column-major, ld).
 // Returns false when a pivot is not positive (the factor is then unusable).

@@ -623,8 +623,6 @@ int stgp_ctx_create(int device, stgp_ctx** out) {
       config_error("stgp_b200 is built for sm_100a (B200); found compute capability " +
                    std::to_string(prop.major) + "." + std::to_string(prop.minor));
     ctx->num_sms = prop.multiProcessorCount;
-    if (cublasCreate(&ctx->cublas) != CUBLAS_STATUS_SUCCESS) throw Error(kInternal, "cublasCreate failed");
-    cublasSetStream(ctx->cublas, ctx->stream);
     *out = ctx.release();
   });
 }
@@ -637,7 +635,6 @@ void stgp_ctx_destroy(stgp_ctx* ctx) {
   stgp::ozaki_release(ctx);
   stgp::prof_collect(ctx);
   for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
-  if (ctx->cublas) cublasDestroy(ctx->cublas);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

@@ -1,7 +1,6 @@
 // Host-side engine objects behind the C ABI (include/stgp_b200.h).
 #pragma once
 
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -57,7 +56,6 @@ struct OzakiState;  // ozaki.cu: int8 slice buffers and cuBLASLt plans
 struct stgp_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cublasHandle_t cublas = nullptr;
   int rank = 0, world = 1;
   ncclComm* comm = nullptr;
   int64_t launches = 0;
@@ -66,6 +64,11 @@ struct stgp_ctx {
   void* host_allreduce_user = nullptr;
   stgp::DevBuf<int> iscr;     // small persistent scratch (flags, scalars)
   stgp::DevBuf<double> dscr;
+  stgp::DevBuf<double> gemm_part;  // split-K partial tiles of the DMMA GEMM
+  stgp::DevBuf<double> dense_tmp;  // GEMV partials, transposed TRSM operands, Cholesky panels
+  stgp::DevBuf<double> dense_tmp2;  // blocked TRSM: one row block of the solution
+  stgp::DevBuf<double> dense_inv;   // inverses of the 64 x 64 diagonal blocks of a factor
+  stgp::DevBuf<double> dense_tmp3;  // n x n: triangular inverse / congruence product
   stgp::DevBuf<double> sel_W;  // d_r search: whitened cross covariance, kept across searches (8 GB at cfg4)
   stgp::DevBuf<uint16_t> sel_W16;  // d_r search: its fp16 copy for the certified filter
   stgp::OzakiState* ozaki = nullptr;  // FP64-on-int8 GEMM workspace (lazy)

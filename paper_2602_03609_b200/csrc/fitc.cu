@@ -205,9 +205,7 @@ void fitc_nll_grad(stgp_structure* s, double* nll, double* grad) {
   std::vector<double> phisum(1, 0.0);
   // explicit K^{-1} (M^3): KW = K^{-1} W is one GEMM, and |L_K^{-1} W_i|^2 = W_i . KW_i
   L.Kinv.ensure(mm);
-  set_identity(ctx, L.Kinv.get(), ldm);
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, false);
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, true);
+  dev_chol_inverse(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get());
   if (nown > 0) {
     ProfRegion pr(ctx, "f_KW_gemm");
     if (ozaki_for(ldm))  // K^{-1} symmetric: KW_i = K^{-1} W_i row by row
@@ -240,7 +238,7 @@ void fitc_nll_grad(stgp_structure* s, double* nll, double* grad) {
   allreduce_host(ctx, phisum);
   fitc_wsig_kernel<<<grid_for(static_cast<long long>(mm)), 256, 0, st>>>(M, ldm, L.Kinv.get(), wa, S, Ws);
   launched(ctx);
-  transform_wsig(ctx, L.Lm.get(), ldm, Ws);
+  transform_wsig(ctx, L.Lminv.get(), ldm, Ws);
   std::vector<double> g(7, 0.0);
   if (nown > 0) {
     // omega' (in place of KW), omega = L_m^{-T} omega'

@@ -764,13 +764,8 @@ double dev_sum_log(stgp_ctx* ctx, const double* v, long long n, Reducer& red) {
   launched(ctx);
   return red.finish(ctx, blocks, 1)[0];
 }
-void transform_wsig(stgp_ctx* ctx, const double* Lm, int ldm, double* Ws) {
-  dev_trsm_left(ctx, Lm, ldm, ldm, Ws, ldm, ldm, true);
-  const double one = 1.0;
-  cublas_check(cublasDtrsm(ctx->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, ldm,
-                           ldm, &one, Lm, ldm, Ws, ldm),
-               "trsm(wsig)");
-}
+// Ws <- L_m^{-T} Ws L_m^{-1} with the basis' explicit inverse factor
+void transform_wsig(stgp_ctx* ctx, const double* Lminv, int ldm, double* Ws) { dev_congruence_t(ctx, Lminv, ldm, ldm, Ws); }
 std::vector<double> upair_grad(stgp_structure* s, const double* Om, int c0, int c1) {
   stgp_ctx* ctx = s->ds->ctx;
   const int ub = std::max(1, std::min(c1 - c0, ctx->num_sms * 8));
@@ -949,10 +944,7 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
   // K^{-1} (explicit, M x M) and X = K^{-1} V' (own columns) as one GEMM
   ph.reset(new ProfRegion(ctx, "g_X_gemm"));
   L.Kinv.ensure(mm);
-  set_identity_kernel<<<grid_for(static_cast<long long>(mm)), kT, 0, st>>>(L.Kinv.get(), ldm, ldm);
-  launched(ctx);
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, false);
-  dev_trsm_left(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get(), ldm, ldm, true);
+  dev_chol_inverse(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get());
   L.work1.ensure(total);
   if (re > rb) {
     if (ozaki_for(ldm))  // K^{-1} is symmetric: X_r = K^{-1} V'_r row by row on the int8 tensor cores
@@ -1007,7 +999,7 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
   ph.reset(new ProfRegion(ctx, "g_wsig"));
   wsig_assemble_kernel<<<grid_for(static_cast<long long>(mm)), kT, 0, st>>>(L.M, ldm, yhat, S, L.Kinv.get(), Ws);
   launched(ctx);
-  transform_wsig(ctx, L.Lm.get(), ldm, Ws);
+  transform_wsig(ctx, L.Lminv.get(), ldm, Ws);
   // omega' over the columns this shard's rows touch, omega = L_m^{-T} omega'
   ph.reset(new ProfRegion(ctx, "g_omega"));
   ensure_csc(s);

@@ -31,7 +31,7 @@ double dev_dot(stgp_ctx* ctx, const double* a, const double* b, long long n, Red
 double dev_sum(stgp_ctx* ctx, const double* v, long long n, Reducer& red);
 double dev_sum_log(stgp_ctx* ctx, const double* v, long long n, Reducer& red);
 // wsig = L_m^{-T} wsig' L_m^{-1} in place
-void transform_wsig(stgp_ctx* ctx, const double* Lm, int ldm, double* Ws);
+void transform_wsig(stgp_ctx* ctx, const double* Lminv, int ldm, double* Ws);
 // sum_{j,i} Om(j,i) dk(z_j, p_i) and the Sigma_m-pair sum (6 components each)
 std::vector<double> upair_grad(stgp_structure* s, const double* Om, int c0, int c1);
 void add_identity(stgp_ctx* ctx, double* A, int ld);
