@@ -164,6 +164,18 @@ int stgp_eval(stgp_structure* s, const stgp_params* theta, const double* y_host,
               const double* X_host, int p, const double* beta, double* nll_out,
               double* grad_out);
 
+/* ---- latent-policy likelihoods ----
+ * stgp_nll on a latent-policy Vecchia / VIF structure is the Gaussian latent-policy NLL through the
+ * Laplace algebra (approximations.cpp:320-334, 348-349, 369-371).  The Laplace algebra factors Q + W
+ * densely on the device ("desk scale", n <= 40000; FITC: any n).
+ * laplace_marginal (laplace.cpp:115-203, LaplaceAlgebra approximations.cpp:1083-1375) with the
+ * zero-censored power-transformed normal likelihood (LikelihoodParams sigma, lambda; y >= 0): the
+ * negative Laplace log-marginal, and the state at the mode (mode, grad_at_mode, w: n each, may be NULL).
+ * warm (n, may be NULL) is the Newton warm start. */
+int stgp_laplace_marginal(stgp_structure* s, const double* y_host, const double* X_host, int p, const double* beta,
+                          double lik_sigma, double lik_lambda, const double* warm_host, double* nll_out,
+                          double* mode_out, double* grad_at_mode_out, double* w_out, int* iterations_out);
+
 /* ---- fit driver (estimation.hpp:23-56, estimation.cpp:423-619; Gaussian likelihood) ---- */
 /* FitConfig::Method */
 #define STGP_FIT_VECCHIA_EUCLID 0

@@ -539,3 +539,52 @@ def set_blas(on: bool = True, threads: int = 0) -> bool:
         return False
     _chk(lib().orc_set_blas(path.encode() if path else None, int(threads)))
     return on
+
+
+def zcptn(y, mu, sigma, lam):
+    """(loglik, d1, d2) of the ZC-PTN observation model (laplace.cpp:56-91)."""
+    out = np.zeros(3)
+    _chk(lib().orc_zcptn(C.c_double(y), C.c_double(mu), C.c_double(sigma), C.c_double(lam), _p(out)))
+    return tuple(out)
+
+
+def normal_tail(z):
+    """(norm_cdf, log_norm_cdf, inverse_mills) (laplace.cpp:25-54)."""
+    out = np.zeros(3)
+    lib().orc_normal_tail(C.c_double(z), _p(out))
+    return tuple(out)
+
+
+def laplace_marginal(om: "OracleModel", yv, lik_sigma: float, lik_lambda: float, X=None, beta=None, warm=None):
+    """laplace_marginal (laplace.cpp:115-203), ZC-PTN likelihood: (negative log-marginal, state dict)."""
+    p, Xf, b = OracleModel._xb(om.n, X, beta)
+    yv = _f64(yv)
+    n = om.n
+    mode, ga, w = np.zeros(n), np.zeros(n), np.zeros(n)
+    out, it = C.c_double(), C.c_int()
+    wm = None if warm is None else _f64(warm)
+    _chk(lib().orc_laplace_marginal(C.byref(om.m), _p(yv), p, _p(Xf), _p(b), C.c_double(lik_sigma),
+                                    C.c_double(lik_lambda), _p(wm), C.byref(out), _p(mode), _p(ga), _p(w),
+                                    C.byref(it)))
+    return out.value, {"mode": mode, "grad_at_mode": ga, "w": w, "iterations": it.value}
+
+
+def zcptn_predict(om: "OracleModel", state, targets, lik_sigma: float, lik_lambda: float, pred_m_v: int,
+                  n_samples: int, seed: int, Xp=None, beta=None):
+    """zcptn_predict (laplace.cpp:205-259): latent moments, P(rain), Monte Carlo amounts and draws."""
+    T = np.asarray(targets, dtype=np.float64).reshape(-1, 3)
+    qx, qy, qt = _f64(T[:, 0]), _f64(T[:, 1]), _f64(T[:, 2])
+    npred = len(T)
+    p = 0 if Xp is None or beta is None else np.asarray(Xp).reshape(npred, -1).shape[1]
+    Xpf = None if p == 0 else np.asfortranarray(np.asarray(Xp, dtype=np.float64).reshape(npred, -1))
+    b = None if p == 0 else _f64(beta)
+    outs = [np.zeros(npred) for _ in range(5)]
+    samples = np.zeros((npred, n_samples), order="F")
+    _chk(lib().orc_zcptn_predict(C.byref(om.m), _p(_f64(state["grad_at_mode"])), _p(_f64(state["w"])), npred,
+                                 _p(qx), _p(qy), _p(qt), _p(Xpf), p, _p(b), C.c_double(lik_sigma),
+                                 C.c_double(lik_lambda), pred_m_v, n_samples, C.c_uint64(seed),
+                                 *[_p(o) for o in outs], _p(samples)))
+    keys = ["mu_latent", "var_latent", "p_rain", "amount_mean", "amount_median"]
+    d = dict(zip(keys, outs))
+    d["samples"] = np.ascontiguousarray(samples)
+    return d

@@ -1562,6 +1562,397 @@ std::vector<int> target_nbrs(const Pt& q, const Model& s, int kind_metric, doubl
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Laplace algebra (approximations.cpp:1083-1375) and the ZC-PTN likelihood / Newton mode finding /
+// prediction (laplace.cpp:25-259), dense at the oracle's sizes: the reference factors Q + W with a
+// sparse LDLT (SimplicialLDLT), whose determinant and solves equal the dense Cholesky's up to rounding.
+// ---------------------------------------------------------------------------
+// Q = B^T D^{-1} B (form_precision, approximations.cpp:181-190)
+Mat form_precision_dense(const Model& s) {
+  const int n = s.n;
+  Mat Q(n, n);
+  for (int r = 0; r < n; ++r) {
+    const int k = s.nb.count(r);
+    const int32_t* N = s.nb.row(r);
+    const double Dr = s.rows.D[static_cast<size_t>(r)];
+    std::vector<int> idx(static_cast<size_t>(k) + 1);
+    std::vector<double> val(static_cast<size_t>(k) + 1);
+    for (int a = 0; a < k; ++a) {
+      idx[static_cast<size_t>(a)] = N[a];
+      val[static_cast<size_t>(a)] = -s.rows.A[static_cast<size_t>(r) * s.nb.m_v + a];
+    }
+    idx[static_cast<size_t>(k)] = r;
+    val[static_cast<size_t>(k)] = 1.0;
+    for (int a = 0; a <= k; ++a)
+      for (int b = 0; b <= k; ++b)
+        Q(idx[static_cast<size_t>(a)], idx[static_cast<size_t>(b)]) +=
+            val[static_cast<size_t>(a)] * val[static_cast<size_t>(b)] / Dr;
+  }
+  return Q;
+}
+
+struct Laplace {
+  const Model* s;
+  int kind;
+  // Vecchia / VIF: Q, the factor of S = Q + W and log|Sigma_s| = sum log D
+  Mat Q;
+  Chol S;
+  double logdet_sigma = 0.0, logdet_S = 0.0;
+  // VIF: QUt = Q U^T (n x M), Z = S^{-1} QUt, the core M_w
+  Mat QUt, Z;
+  Chol Mw;
+  double logdet_Mw = 0.0;
+  // FITC (approximations.cpp:1168-1200)
+  std::vector<double> scale, e1;
+  double logdet_fitc = 0.0;
+
+  explicit Laplace(const Model& m) : s(&m), kind(m.kind) {
+    if (kind != 1) {  // VecchiaLaplace / VifLaplace (approximations.cpp:1090-1097, 1230-1237)
+      if (m.policy != 0) throw NumericError("LaplaceAlgebra: requires a latent-policy structure");
+      Q = form_precision_dense(m);
+      for (int i = 0; i < m.n; ++i) logdet_sigma += std::log(m.rows.D[static_cast<size_t>(i)]);
+      const int M = m.basis.m();
+      if (kind == 2 && M > 0) {  // QUt = sparse_q_apply(B, D, U^T) (approximations.cpp:303)
+        QUt = Mat(m.n, M);
+        std::vector<double> col(static_cast<size_t>(m.n));
+        for (int j = 0; j < M; ++j) {
+          for (int i = 0; i < m.n; ++i) col[static_cast<size_t>(i)] = m.U(j, i);
+          const std::vector<double> q = q_apply(m.nb, m.rows, col.data());
+          for (int i = 0; i < m.n; ++i) QUt(i, j) = q[static_cast<size_t>(i)];
+        }
+      }
+    }
+  }
+  int n() const { return s->n; }
+  // prepare(w) (approximations.cpp:1100-1108, 1168-1184, 1240-1259)
+  void prepare(const std::vector<double>& w) {
+    const int n_ = n(), M = s->basis.m();
+    if (kind == 1) {
+      const std::vector<double>& lam0 = s->fitc_diag;
+      scale.assign(static_cast<size_t>(n_), 0.0);
+      e1.assign(static_cast<size_t>(n_), 0.0);
+      std::vector<double> dw(static_cast<size_t>(n_));
+      for (int i = 0; i < n_; ++i) {
+        scale[static_cast<size_t>(i)] = 1.0 / (1.0 + w[static_cast<size_t>(i)] * lam0[static_cast<size_t>(i)]);
+        e1[static_cast<size_t>(i)] = lam0[static_cast<size_t>(i)] * scale[static_cast<size_t>(i)];
+        dw[static_cast<size_t>(i)] = w[static_cast<size_t>(i)] * scale[static_cast<size_t>(i)];
+      }
+      Mat Mc = s->basis.sigma;
+      for (int a = 0; a < M; ++a)
+        for (int b = 0; b < M; ++b) {
+          double acc = 0.0;
+          for (int i = 0; i < n_; ++i) acc += s->U(a, i) * dw[static_cast<size_t>(i)] * s->U(b, i);
+          Mc(a, b) += acc;
+        }
+      if (!Mw.compute(Mc)) throw NumericError("FitcLaplace: core factorization failed");
+      double l1 = 0.0;
+      for (int i = 0; i < n_; ++i) l1 += std::log(1.0 + w[static_cast<size_t>(i)] * lam0[static_cast<size_t>(i)]);
+      logdet_fitc = l1 + Mw.logdet() - s->basis.llt.logdet();
+      return;
+    }
+    Mat Sm = Q;
+    for (int i = 0; i < n_; ++i) Sm(i, i) += w[static_cast<size_t>(i)];
+    if (!S.compute(Sm)) throw NumericError(kind == 0 ? "VecchiaLaplace: factorization of Q + W failed"
+                                                     : "VifLaplace: factorization of Q + W failed");
+    logdet_S = S.logdet();
+    if (kind == 2 && M > 0) {
+      Z = chol_solve_cols(S, QUt);
+      Mat Mc = s->basis.sigma;
+      for (int a = 0; a < M; ++a)
+        for (int b = 0; b < M; ++b) {
+          double acc = 0.0, acc2 = 0.0;
+          for (int i = 0; i < n_; ++i) {
+            acc += s->U(a, i) * QUt(i, b);
+            acc2 += QUt(i, a) * Z(i, b);
+          }
+          Mc(a, b) += acc - acc2;
+        }
+      for (int a = 0; a < M; ++a)  // symmetric by construction up to rounding: use the lower triangle
+        for (int b = a + 1; b < M; ++b) Mc(a, b) = Mc(b, a);
+      if (!Mw.compute(Mc)) throw NumericError("VifLaplace: core factorization failed");
+      logdet_Mw = Mw.logdet();
+    }
+  }
+  // (Sigma^{-1} + W)^{-1} x
+  std::vector<double> solve(const std::vector<double>& x) const {
+    const int n_ = n(), M = s->basis.m();
+    std::vector<double> out(static_cast<size_t>(n_));
+    if (kind == 1) {
+      std::vector<double> tx(static_cast<size_t>(M)), mt(static_cast<size_t>(M));
+      for (int j = 0; j < M; ++j) {
+        double acc = 0.0;
+        for (int i = 0; i < n_; ++i) acc += s->U(j, i) * (x[static_cast<size_t>(i)] * scale[static_cast<size_t>(i)]);
+        tx[static_cast<size_t>(j)] = acc;
+      }
+      Mw.solve(tx.data(), mt.data());
+      for (int i = 0; i < n_; ++i) {
+        double acc = 0.0;
+        for (int j = 0; j < M; ++j) acc += s->U(j, i) * mt[static_cast<size_t>(j)];
+        out[static_cast<size_t>(i)] = e1[static_cast<size_t>(i)] * x[static_cast<size_t>(i)] + scale[static_cast<size_t>(i)] * acc;
+      }
+      return out;
+    }
+    S.solve(x.data(), out.data());
+    if (kind == 2 && M > 0) {
+      std::vector<double> q(static_cast<size_t>(M)), mq(static_cast<size_t>(M));
+      for (int j = 0; j < M; ++j) {
+        double acc = 0.0;
+        for (int i = 0; i < n_; ++i) acc += QUt(i, j) * out[static_cast<size_t>(i)];
+        q[static_cast<size_t>(j)] = acc;
+      }
+      Mw.solve(q.data(), mq.data());
+      for (int i = 0; i < n_; ++i) {
+        double acc = 0.0;
+        for (int j = 0; j < M; ++j) acc += Z(i, j) * mq[static_cast<size_t>(j)];
+        out[static_cast<size_t>(i)] += acc;
+      }
+    }
+    return out;
+  }
+  double logdet_I_plus_WS() const {
+    if (kind == 1) return logdet_fitc;
+    double v = logdet_S + logdet_sigma;
+    if (kind == 2 && s->basis.m() > 0) v += logdet_Mw - s->basis.llt.logdet();
+    return v;
+  }
+  // latent cross covariance to a target and its prior variance (approximations.cpp:1121-1160,
+  // 1202-1215, 1290-1355)
+  std::pair<std::vector<double>, double> target_row(const Pt& q, int pred_m_v) const {
+    const Model& m = *s;
+    const orc_params& th = m.kernel.th;
+    const int n_ = m.n, M = m.basis.m();
+    if (kind == 1) {
+      std::vector<double> up(static_cast<size_t>(M)), wp(static_cast<size_t>(M)), out(static_cast<size_t>(n_));
+      for (int j = 0; j < M; ++j) up[static_cast<size_t>(j)] = m.kernel(m.basis.z[static_cast<size_t>(j)], q);
+      m.basis.llt.solve(up.data(), wp.data());
+      for (int i = 0; i < n_; ++i) {
+        double acc = 0.0;
+        for (int j = 0; j < M; ++j) acc += m.U(j, i) * wp[static_cast<size_t>(j)];
+        out[static_cast<size_t>(i)] = acc;
+      }
+      return {out, th.sigma1_2};
+    }
+    std::vector<double> resid(static_cast<size_t>(n_));
+    std::vector<double> up(static_cast<size_t>(M)), wp(static_cast<size_t>(M)), wq(static_cast<size_t>(M));
+    double u_smu = 0.0, rq = th.sigma1_2;
+    if (kind == 2) {
+      for (int i = 0; i < n_; ++i)
+        resid[static_cast<size_t>(i)] = th.sigma1_2 - (M > 0 ? dot_seq(m.W.col(i), m.W.col(i), M) : 0.0);
+      if (M > 0) {
+        for (int j = 0; j < M; ++j) up[static_cast<size_t>(j)] = m.kernel(m.basis.z[static_cast<size_t>(j)], q);
+        m.basis.llt.solve(up.data(), wp.data());
+        m.basis.llt.lsolve(up.data(), wq.data());
+        for (int j = 0; j < M; ++j) u_smu += up[static_cast<size_t>(j)] * wp[static_cast<size_t>(j)];
+        rq -= dot_seq(wq.data(), wq.data(), M);
+      }
+    }
+    const std::vector<int> N = kind == 0 ? target_nbrs(q, m, 1, 1.0, 1.0, nullptr, nullptr, 0.0, pred_m_v)
+                                         : target_nbrs(q, m, 2, 1.0, 1.0, &resid, wq.data(), rq, pred_m_v);
+    const int k = static_cast<int>(N.size());
+    Mat C(k, k);
+    std::vector<double> c(static_cast<size_t>(k)), A(static_cast<size_t>(k));
+    for (int a = 0; a < k; ++a) {
+      const int ja = N[static_cast<size_t>(a)];
+      const Pt& pa = m.pts[static_cast<size_t>(ja)];
+      double va = m.kernel(q, pa);
+      if (kind == 2 && M > 0) va -= dot_seq(wq.data(), m.W.col(ja), M);
+      c[static_cast<size_t>(a)] = va;
+      for (int b = 0; b <= a; ++b) {
+        const int jb = N[static_cast<size_t>(b)];
+        double v = m.kernel(pa, m.pts[static_cast<size_t>(jb)]);
+        if (kind == 2 && M > 0) v -= dot_seq(m.W.col(ja), m.W.col(jb), M);
+        C(a, b) = v;
+        C(b, a) = v;
+      }
+    }
+    for (int a = 0; a < k; ++a) C(a, a) += 1e-10 * th.sigma1_2;
+    Chol llt;
+    if (!llt.compute(C))
+      throw NumericError(kind == 0 ? "VecchiaLaplace: target conditioning block failed"
+                                   : "VifLaplace: target conditioning block failed");
+    if (k > 0) llt.solve(c.data(), A.data());
+    double ac = 0.0;
+    for (int a = 0; a < k; ++a) ac += A[static_cast<size_t>(a)] * c[static_cast<size_t>(a)];
+    const double Dp = (kind == 0 ? th.sigma1_2 : rq) - ac;
+    std::vector<double> sN(static_cast<size_t>(n_), 0.0);
+    for (int a = 0; a < k; ++a) sN[static_cast<size_t>(N[static_cast<size_t>(a)])] = A[static_cast<size_t>(a)];
+    std::vector<double> kvec = sigma_s_apply(m.nb, m.rows, sN.data());
+    double var = (kind == 0 ? 0.0 : u_smu) + Dp;
+    for (int a = 0; a < k; ++a) var += A[static_cast<size_t>(a)] * kvec[static_cast<size_t>(N[static_cast<size_t>(a)])];
+    if (kind == 2 && M > 0)
+      for (int i = 0; i < n_; ++i) {
+        double acc = 0.0;
+        for (int j = 0; j < M; ++j) acc += m.U(j, i) * wp[static_cast<size_t>(j)];
+        kvec[static_cast<size_t>(i)] += acc;
+      }
+    return {kvec, var};
+  }
+};
+
+// latent_policy_nll (approximations.cpp:320-334)
+double latent_policy_nll(Laplace& alg, double sigma2, const std::vector<double>& r) {
+  if (!(sigma2 > 0.0)) throw NumericError("nll: the Gaussian path requires a positive nugget");
+  const int n = static_cast<int>(r.size());
+  const double w = 1.0 / sigma2;
+  alg.prepare(std::vector<double>(static_cast<size_t>(n), w));
+  const double logdet = n * std::log(sigma2) + alg.logdet_I_plus_WS();
+  const std::vector<double> z = alg.solve(r);
+  double rr = 0.0, rz = 0.0;
+  for (int i = 0; i < n; ++i) {
+    rr += r[static_cast<size_t>(i)] * r[static_cast<size_t>(i)];
+    rz += r[static_cast<size_t>(i)] * z[static_cast<size_t>(i)];
+  }
+  const double quad = w * (rr - w * rz);
+  return 0.5 * (logdet + quad + n * kLog2Pi);
+}
+
+// ZC-PTN observation model (laplace.cpp:25-91)
+constexpr double kSqrt2 = 1.4142135623730951;
+double norm_pdf(double z) { return std::exp(-0.5 * z * z - 0.5 * kLog2Pi); }
+double norm_cdf(double z) { return 0.5 * std::erfc(-z / kSqrt2); }
+double lower_tail_series(double z) {
+  const double z2 = z * z, z4 = z2 * z2;
+  return 1.0 - 1.0 / z2 + 3.0 / z4 - 15.0 / (z4 * z2) + 105.0 / (z4 * z4) - 945.0 / (z4 * z4 * z2);
+}
+double log_norm_cdf(double z) {
+  if (z > -8.0) return std::log(norm_cdf(z));
+  return -0.5 * z * z - 0.5 * kLog2Pi - std::log(-z) + std::log(lower_tail_series(z));
+}
+double inverse_mills(double z) {
+  if (z > -8.0) return norm_pdf(z) / norm_cdf(z);
+  return -z / lower_tail_series(z);
+}
+void validate_lik(double sigma, double lambda) {
+  if (!(sigma > 0.0) || !std::isfinite(sigma)) throw ConfigError("LikelihoodParams: sigma must be > 0");
+  if (!(lambda > 0.0) || !std::isfinite(lambda)) throw ConfigError("LikelihoodParams: lambda must be > 0");
+}
+double zcptn_loglik(double y, double mu, double sigma, double lambda) {
+  if (y < 0.0) throw DataError("zcptn_loglik: negative precipitation amount");
+  if (y == 0.0) return log_norm_cdf(-mu / sigma);
+  const double g = std::pow(y, 1.0 / lambda);
+  const double z = (g - mu) / sigma;
+  return -0.5 * z * z - 0.5 * kLog2Pi - std::log(sigma) - std::log(lambda) - (1.0 - 1.0 / lambda) * std::log(y);
+}
+std::pair<double, double> zcptn_derivs(double y, double mu, double sigma, double lambda) {
+  if (y < 0.0) throw DataError("zcptn_derivs: negative precipitation amount");
+  if (y == 0.0) {
+    const double z = -mu / sigma;
+    const double h = inverse_mills(z);
+    const double d1 = -h / sigma;
+    const double d2 = (-z * h - h * h) / (sigma * sigma);
+    return {d1, std::min(d2, 0.0)};
+  }
+  const double g = std::pow(y, 1.0 / lambda);
+  return {(g - mu) / (sigma * sigma), -1.0 / (sigma * sigma)};
+}
+
+struct LapState {
+  std::vector<double> mode, grad_at_mode, w;
+  double log_marginal = 0.0;
+  bool converged = false;
+  int iterations = 0;
+};
+
+// laplace_marginal (laplace.cpp:115-203): Newton in (b, a = Sigma^{-1} b) with step halving
+double laplace_marginal(Laplace& alg, const std::vector<double>& y, const std::vector<double>& offset, double sigma,
+                        double lambda, const double* warm, LapState& st) {
+  validate_lik(sigma, lambda);
+  const int n = alg.n();
+  auto value = [&](const std::vector<double>& b) {
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) acc += zcptn_loglik(y[static_cast<size_t>(i)], offset[static_cast<size_t>(i)] + b[static_cast<size_t>(i)], sigma, lambda);
+    return acc;
+  };
+  auto derivs = [&](const std::vector<double>& b, std::vector<double>& g, std::vector<double>& w) {
+    g.resize(static_cast<size_t>(n));
+    w.resize(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+      const auto d = zcptn_derivs(y[static_cast<size_t>(i)], offset[static_cast<size_t>(i)] + b[static_cast<size_t>(i)], sigma, lambda);
+      g[static_cast<size_t>(i)] = d.first;
+      w[static_cast<size_t>(i)] = std::max(-d.second, 0.0);
+    }
+  };
+  auto dot = [&](const std::vector<double>& u, const std::vector<double>& v) {
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) acc += u[static_cast<size_t>(i)] * v[static_cast<size_t>(i)];
+    return acc;
+  };
+  std::vector<double> b(static_cast<size_t>(n), 0.0), a(static_cast<size_t>(n), 0.0), g, w;
+  bool warm_nonzero = false;
+  if (warm) {
+    for (int i = 0; i < n; ++i) {
+      b[static_cast<size_t>(i)] = warm[i];
+      warm_nonzero = warm_nonzero || warm[i] != 0.0;
+    }
+  }
+  if (warm_nonzero) {
+    derivs(b, g, w);
+    alg.prepare(w);
+    std::vector<double> rhs(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) rhs[static_cast<size_t>(i)] = w[static_cast<size_t>(i)] * b[static_cast<size_t>(i)] + g[static_cast<size_t>(i)];
+    const std::vector<double> bn = alg.solve(rhs);
+    for (int i = 0; i < n; ++i) a[static_cast<size_t>(i)] = rhs[static_cast<size_t>(i)] - w[static_cast<size_t>(i)] * bn[static_cast<size_t>(i)];
+    b = bn;
+  }
+  double psi = value(b) - 0.5 * dot(a, b);
+  bool converged = false;
+  int iter = 0;
+  auto gap = [&]() {
+    double mg = 0.0, md = 0.0;
+    for (int i = 0; i < n; ++i) {
+      mg = std::max(mg, std::abs(g[static_cast<size_t>(i)]));
+      md = std::max(md, std::abs(g[static_cast<size_t>(i)] - a[static_cast<size_t>(i)]));
+    }
+    return md < 1e-6 * std::max(1.0, mg);
+  };
+  for (iter = 1; iter <= 100; ++iter) {
+    derivs(b, g, w);
+    if (gap()) {
+      converged = true;
+      break;
+    }
+    alg.prepare(w);
+    std::vector<double> rhs(static_cast<size_t>(n)), an(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) rhs[static_cast<size_t>(i)] = w[static_cast<size_t>(i)] * b[static_cast<size_t>(i)] + g[static_cast<size_t>(i)];
+    const std::vector<double> bn = alg.solve(rhs);
+    for (int i = 0; i < n; ++i) an[static_cast<size_t>(i)] = rhs[static_cast<size_t>(i)] - w[static_cast<size_t>(i)] * bn[static_cast<size_t>(i)];
+    double step = 1.0;
+    bool accepted = false;
+    for (int h = 0; h < 30; ++h) {
+      std::vector<double> bt(static_cast<size_t>(n)), at(static_cast<size_t>(n));
+      for (int i = 0; i < n; ++i) {
+        bt[static_cast<size_t>(i)] = b[static_cast<size_t>(i)] + step * (bn[static_cast<size_t>(i)] - b[static_cast<size_t>(i)]);
+        at[static_cast<size_t>(i)] = a[static_cast<size_t>(i)] + step * (an[static_cast<size_t>(i)] - a[static_cast<size_t>(i)]);
+      }
+      const double pt = value(bt) - 0.5 * dot(at, bt);
+      if (pt >= psi - 1e-12 * std::abs(psi)) {
+        b = bt;
+        a = at;
+        psi = pt;
+        accepted = true;
+        break;
+      }
+      step *= 0.5;
+    }
+    if (!accepted) break;
+  }
+  if (!converged) {
+    derivs(b, g, w);
+    converged = gap();
+    if (!converged) throw NumericError("laplace_marginal: Newton did not converge in 100 iterations");
+  }
+  derivs(b, g, w);
+  alg.prepare(w);
+  const double lm = value(b) - 0.5 * dot(a, b) - 0.5 * alg.logdet_I_plus_WS();
+  st.mode = b;
+  st.grad_at_mode = a;
+  st.w = w;
+  st.log_marginal = lm;
+  st.converged = converged;
+  st.iterations = iter;
+  return -lm;
+}
+
 // ===========================================================================
 // C ABI
 // ===========================================================================
@@ -2070,7 +2461,13 @@ int orc_nll(const orc_model* m, const double* yv, int p, const double* X, const 
   return guarded([&] {
     Model s(m);
     build_model(s, m);
-    *out = nll_model(s, residual(m->n, yv, p, X, beta));
+    const std::vector<double> r = residual(m->n, yv, p, X, beta);
+    if (m->kind != 1 && m->policy != 1) {  // latent policy: nll through the Laplace algebra (approximations.cpp:348-349, 369-370)
+      Laplace alg(s);
+      *out = latent_policy_nll(alg, m->theta.sigma2, r);
+      return;
+    }
+    *out = nll_model(s, r);
   });
 }
 
@@ -2083,6 +2480,103 @@ int orc_nll_grad(const orc_model* m, const double* yv, int p, const double* X,
     if (m->kind == 0) grad_vecchia(s, r, grad7, nullptr);
     else if (m->kind == 1) grad_fitc(s, r, grad7, nullptr);
     else grad_vif(s, r, grad7, nullptr);
+  });
+}
+
+// ZC-PTN helpers (laplace.cpp:25-91): out = {loglik, d1, d2}; tail = {norm_cdf, log_norm_cdf, inverse_mills}
+int orc_zcptn(double y, double mu, double sigma, double lambda, double* out3) {
+  return guarded([&] {
+    validate_lik(sigma, lambda);
+    out3[0] = zcptn_loglik(y, mu, sigma, lambda);
+    const auto d = zcptn_derivs(y, mu, sigma, lambda);
+    out3[1] = d.first;
+    out3[2] = d.second;
+  });
+}
+void orc_normal_tail(double z, double* out3) {
+  out3[0] = norm_cdf(z);
+  out3[1] = log_norm_cdf(z);
+  out3[2] = inverse_mills(z);
+}
+
+// Laplace / ZC-PTN (laplace.cpp:115-259): the negative Laplace log-marginal, its state, and the
+// latent predictive moments with the Monte Carlo draws on the observation scale
+int orc_laplace_marginal(const orc_model* m, const double* yv, int p, const double* X, const double* beta,
+                         double lik_sigma, double lik_lambda, const double* warm, double* nll_out, double* mode,
+                         double* grad_at_mode, double* w_out, int* iterations) {
+  return guarded([&] {
+    Model s(m);
+    build_model(s, m);
+    Laplace alg(s);
+    const int n = m->n;
+    std::vector<double> y(yv, yv + n), offset(static_cast<size_t>(n), 0.0);
+    if (p > 0 && X && beta)
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < p; ++j) offset[static_cast<size_t>(i)] += X[static_cast<size_t>(i) + static_cast<size_t>(j) * n] * beta[j];
+    LapState st;
+    *nll_out = laplace_marginal(alg, y, offset, lik_sigma, lik_lambda, warm, st);
+    for (int i = 0; i < n; ++i) {
+      if (mode) mode[i] = st.mode[static_cast<size_t>(i)];
+      if (grad_at_mode) grad_at_mode[i] = st.grad_at_mode[static_cast<size_t>(i)];
+      if (w_out) w_out[i] = st.w[static_cast<size_t>(i)];
+    }
+    if (iterations) *iterations = st.iterations;
+  });
+}
+
+int orc_zcptn_predict(const orc_model* m, const double* grad_at_mode, const double* w, int n_p, const double* qx,
+                      const double* qy, const double* qt, const double* Xp, int p, const double* beta,
+                      double lik_sigma, double lik_lambda, int pred_m_v, int n_samples, uint64_t seed,
+                      double* mu_latent, double* var_latent, double* p_rain, double* amount_mean,
+                      double* amount_median, double* samples) {
+  return guarded([&] {
+    if (n_samples < 2) throw ConfigError("zcptn_predict: need at least two samples for scoring");
+    Model s(m);
+    build_model(s, m);
+    Laplace alg(s);
+    const int n = m->n;
+    std::vector<double> wv(w, w + n), a(grad_at_mode, grad_at_mode + n);
+    alg.prepare(wv);
+    for (int pp = 0; pp < n_p; ++pp) {
+      double off = 0.0;
+      if (p > 0 && Xp && beta)
+        for (int j = 0; j < p; ++j) off += Xp[static_cast<size_t>(pp) + static_cast<size_t>(j) * n_p] * beta[j];
+      const Pt q{qx[pp], qy[pp], qt[pp]};
+      const auto kr = alg.target_row(q, pred_m_v);
+      const std::vector<double>& k = kr.first;
+      double ka = 0.0, kwk = 0.0;
+      std::vector<double> wk(static_cast<size_t>(n));
+      for (int i = 0; i < n; ++i) {
+        ka += k[static_cast<size_t>(i)] * a[static_cast<size_t>(i)];
+        wk[static_cast<size_t>(i)] = wv[static_cast<size_t>(i)] * k[static_cast<size_t>(i)];
+        kwk += k[static_cast<size_t>(i)] * wk[static_cast<size_t>(i)];
+      }
+      const std::vector<double> sw = alg.solve(wk);
+      double wsw = 0.0;
+      for (int i = 0; i < n; ++i) wsw += wk[static_cast<size_t>(i)] * sw[static_cast<size_t>(i)];
+      const double mu_lat = off + ka;
+      const double var_lat = std::max(kr.second - kwk + wsw, 0.0);
+      mu_latent[pp] = mu_lat;
+      var_latent[pp] = var_lat;
+      const double s_tot = std::sqrt(lik_sigma * lik_sigma + var_lat);
+      p_rain[pp] = 1.0 - norm_cdf(-mu_lat / s_tot);
+      std::mt19937_64 rng(mix_seed(seed, static_cast<uint64_t>(pp)));
+      std::normal_distribution<double> gauss(0.0, 1.0);
+      const double sd = std::sqrt(var_lat);
+      double acc = 0.0;
+      std::vector<double> draws(static_cast<size_t>(n_samples));
+      for (int t = 0; t < n_samples; ++t) {
+        const double latent = mu_lat + sd * gauss(rng);
+        const double zval = latent + lik_sigma * gauss(rng);
+        const double amount = zval <= 0.0 ? 0.0 : std::pow(zval, lik_lambda);
+        if (samples) samples[static_cast<size_t>(pp) + static_cast<size_t>(t) * n_p] = amount;
+        draws[static_cast<size_t>(t)] = amount;
+        acc += amount;
+      }
+      amount_mean[pp] = acc / n_samples;
+      std::nth_element(draws.begin(), draws.begin() + n_samples / 2, draws.end());
+      amount_median[pp] = draws[static_cast<size_t>(n_samples) / 2];
+    }
   });
 }
 

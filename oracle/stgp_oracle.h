@@ -97,6 +97,19 @@ int orc_nll_grad(const orc_model* m, const double* yv, int p, const double* X,
 /* nll_grad plus, per component, the sum over rows of |row contribution| (the tolerance yardstick) */
 int orc_nll_grad_scale(const orc_model* m, const double* yv, int p, const double* X, const double* beta,
                        double* grad7, double* scale7);
+int orc_zcptn(double y, double mu, double sigma, double lambda, double* out3);
+void orc_normal_tail(double z, double* out3);
+/* laplace_marginal (laplace.cpp:115-203) with the ZC-PTN likelihood: negative log-marginal and the state
+ * at the mode (mode, grad_at_mode, w: n each, may be NULL); warm may be NULL */
+int orc_laplace_marginal(const orc_model* m, const double* yv, int p, const double* X, const double* beta,
+                         double lik_sigma, double lik_lambda, const double* warm, double* nll_out, double* mode,
+                         double* grad_at_mode, double* w_out, int* iterations);
+/* zcptn_predict (laplace.cpp:205-259); samples n_p x n_samples column-major (may be NULL) */
+int orc_zcptn_predict(const orc_model* m, const double* grad_at_mode, const double* w, int n_p, const double* qx,
+                      const double* qy, const double* qt, const double* Xp, int p, const double* beta,
+                      double lik_sigma, double lik_lambda, int pred_m_v, int n_samples, uint64_t seed,
+                      double* mu_latent, double* var_latent, double* p_rain, double* amount_mean,
+                      double* amount_median, double* samples);
 int orc_gls_beta(const orc_model* m, const double* yv, int p, const double* X,
                  double* beta_out);
 int orc_predict(const orc_model* m, const double* yv, int p, const double* X,

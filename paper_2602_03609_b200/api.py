@@ -469,6 +469,38 @@ def predict(s: Structure, y, X, beta, targets, X_p=None, pred_m_v: int = 0) -> P
     return PredictiveDistribution(mu, var)
 
 
+@dataclass
+class LikelihoodParams:
+    """LikelihoodParams (covariance.hpp:41-48): ZC-PTN noise sd and power."""
+    sigma: float = 1.0
+    lambda_: float = 1.0
+
+
+@dataclass
+class LaplaceState:
+    """LaplaceState (laplace.hpp:37-44)."""
+    mode: np.ndarray
+    grad_at_mode: np.ndarray
+    w: np.ndarray
+    log_marginal: float
+    converged: bool
+    iterations: int
+
+
+def laplace_marginal(s: Structure, y, X=None, beta=None, lik: LikelihoodParams | None = None, warm_start=None):
+    """laplace_marginal (laplace.hpp:47-53): (negative Laplace log-marginal, LaplaceState) for the ZC-PTN
+    likelihood on a latent-policy Vecchia / VIF structure or a FITC structure."""
+    lik = lik or LikelihoodParams()
+    yv, Xf, p, b = _yxb(s, y, X, beta)
+    n = s.data.n
+    mode, ga, w = np.zeros(n), np.zeros(n), np.zeros(n)
+    out, it = C.c_double(), C.c_int()
+    warm = None if warm_start is None else _f64(warm_start)
+    N.call("stgp_laplace_marginal", s.h, _ptr(yv), _ptr(Xf), p, _ptr(b), float(lik.sigma), float(lik.lambda_),
+           _ptr(warm), C.byref(out), _ptr(mode), _ptr(ga), _ptr(w), C.byref(it))
+    return out.value, LaplaceState(mode, ga, w, -out.value, True, it.value)
+
+
 def debug_exp(x, ctx: Context | None = None) -> np.ndarray:
     ctx = ctx or default_context()
     x = _f64(x)

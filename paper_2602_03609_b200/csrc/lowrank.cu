@@ -889,8 +889,12 @@ static double vif_nll_given_u(stgp_structure* s, double rows_sum) {
 double lowrank_nll(stgp_structure* s) {
   stgp_ctx* ctx = s->ds->ctx;
   if (s->kind == STGP_FITC) return fitc_nll(s);
-  if (s->policy != STGP_OBSERVATION)
-    config_error("nll: latent-policy likelihood goes through the Laplace algebra (out of scope, SURVEY.md §8(f) f3)");
+  if (s->policy != STGP_OBSERVATION) {  // approximations.cpp:369-371: through the Laplace algebra
+    laplace_release(s);
+    const double v = latent_policy_nll_dev(s);
+    laplace_release(s);
+    return v;
+  }
   const int blocks = std::max(1, std::min(ceil_div(s->n, 256), ctx->num_sms * 4));
   s->red.ensure(blocks, 1);
   s->u.ensure(s->n);

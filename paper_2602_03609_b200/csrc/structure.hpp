@@ -45,8 +45,13 @@ struct LowRank {
 
 }  // namespace stgp
 
+namespace stgp {
+struct LaplaceDev;  // laplace.cu: latent-policy Laplace algebra state
+}
+
 struct stgp_structure {
   stgp_structure();  // assigns uid
+  ~stgp_structure();
   uint64_t uid = 0;  // process-unique, never reused (owner tag of kept Ozaki digits)
   stgp_dataset* ds = nullptr;
   int kind = 0, policy = 0;
@@ -78,6 +83,7 @@ struct stgp_structure {
   // tile-staged gathers (tiles.cu), built once per structure
   bool tiles_built = false;
   stgp::TileSets tiles;
+  stgp::LaplaceDev* lap = nullptr;  // dense Q + W factor etc. (laplace.cu), per call
 };
 
 namespace stgp {
@@ -100,6 +106,12 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
 void upload_lag_table(DevLagTable& d, const TimeIndex& ti, const Params& p, const LagPolicy& pol,
                       cudaStream_t s, bool index_changed);
 LagTable lag_view(const DevLagTable& d);
+// latent-policy likelihoods (laplace.cu)
+void laplace_release(stgp_structure* s);
+double latent_policy_nll_dev(stgp_structure* s);
+double laplace_marginal_dev(stgp_structure* s, const double* y_host, const double* off_dev, double sigma,
+                            double lambda, const double* warm_host, double* mode_out, double* a_out, double* w_out,
+                            int* iters_out);
 
 }  // namespace stgp
 

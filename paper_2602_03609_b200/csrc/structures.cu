@@ -6,6 +6,7 @@
 
 #include "comm.hpp"
 #include "structure.hpp"
+#include "lowrank_common.cuh"
 #include "../../include/stgp_b200.h"
 
 namespace stgp {
@@ -68,8 +69,12 @@ void vecchia_build(stgp_structure* s) {
 }
 
 double vecchia_nll(stgp_structure* s) {
-  if (s->policy != STGP_OBSERVATION)
-    config_error("nll: latent-policy likelihood goes through the Laplace algebra (out of scope, SURVEY.md §8(f) f3)");
+  if (s->policy != STGP_OBSERVATION) {  // approximations.cpp:348-349: through the Laplace algebra
+    laplace_release(s);
+    const double v = latent_policy_nll_dev(s);
+    laplace_release(s);
+    return v;
+  }
   stgp_ctx* ctx = s->ds->ctx;
   const int rows = s->row_end - s->row_begin;
   const int blocks = std::max(1, std::min(ceil_div(rows, 256), ctx->num_sms * 4));
@@ -94,6 +99,8 @@ void vecchia_nll_grad(stgp_structure* s, double* nll, double* grad) {
 }  // namespace stgp
 
 using namespace stgp;
+
+stgp_structure::~stgp_structure() { stgp::laplace_release(this); }
 
 stgp_structure::stgp_structure() {
   static std::atomic<uint64_t> next{1};
@@ -293,6 +300,21 @@ int stgp_predict(stgp_structure* s, const double* y, const double* X, int p, con
         for (int j = 0; j < p; ++j) fe += Xp[static_cast<size_t>(k) + static_cast<size_t>(j) * n_p] * beta[j];
         mu[k] += fe;
       }
+  });
+}
+
+// laplace_marginal (laplace.cpp:115-203) with the ZC-PTN likelihood on a latent-policy structure (FITC: any)
+int stgp_laplace_marginal(stgp_structure* s, const double* y, const double* X, int p, const double* beta,
+                          double lik_sigma, double lik_lambda, const double* warm, double* nll_out, double* mode,
+                          double* grad_at_mode, double* w, int* iterations) {
+  return guarded([&] {
+    if (!s || !y || !nll_out) config_error("stgp_laplace_marginal: null argument");
+    compute_residual(s, y, X, p, beta);  // ywork = y, r = y - X beta
+    DevBuf<double> off(static_cast<size_t>(s->n));
+    vsub(s->ds->ctx, s->n, s->ywork.get(), s->r.get(), off.get());  // X beta
+    laplace_release(s);
+    *nll_out = laplace_marginal_dev(s, y, off.get(), lik_sigma, lik_lambda, warm, mode, grad_at_mode, w, iterations);
+    laplace_release(s);
   });
 }
 

@@ -464,3 +464,82 @@ def test_blas_mode_matches_sequential(kind):
     (v0, g0, sc), (v1, g1, _) = res
     assert v1 == pytest.approx(v0, rel=1e-12)
     assert (np.abs(g1 - g0) <= 1e-12 * sc).all()
+
+
+# ---- latent policy / Laplace / ZC-PTN (restating test_laplace.cpp and the latent-policy limits) ----
+LATENT = (0.0, 1.0, 0.5, 20.0, 0.4, 1.5, 0.4, 0.2)  # test_laplace.cpp:14-16
+
+
+def _tiny(n, seed=404):
+    rng = np.random.default_rng(seed)
+    x, y = rng.random(n), rng.random(n)
+    t = 1.0 + np.arange(n) % 3
+    perm = O.order_observations(t, 1)
+    return x[perm], y[perm], t[perm]
+
+
+def test_normal_tail_helpers():  # test_laplace.cpp:44-53
+    assert O.normal_tail(0.0)[1] == pytest.approx(math.log(0.5), rel=1e-12)
+    assert O.normal_tail(1.96)[0] == pytest.approx(0.9750021, rel=1e-6)
+    assert O.normal_tail(-7.999999)[1] == pytest.approx(O.normal_tail(-8.000001)[1], rel=1e-6)
+    assert O.normal_tail(-7.999999)[2] == pytest.approx(O.normal_tail(-8.000001)[2], rel=1e-6)
+    assert math.isfinite(O.normal_tail(-40.0)[1])
+    assert O.normal_tail(-40.0)[2] == pytest.approx(40.0, rel=1e-2)
+
+
+def test_zcptn_branches_and_derivatives():  # test_laplace.cpp:55-142
+    assert O.zcptn(0.0, 0.0, 1.0, 1.0)[0] == pytest.approx(math.log(0.5), rel=1e-12)
+    assert O.zcptn(1.0, 1.0, 1.0, 1.0)[0] == pytest.approx(-0.5 * math.log(2 * math.pi), rel=1e-12)
+    with pytest.raises(O.OracleError):
+        O.zcptn(-0.5, 0.0, 1.0, 1.0)
+    d1 = O.zcptn(0.0, 0.0, 2.0, 1.0)[1]
+    assert d1 == pytest.approx(-2.0 * math.exp(-0.5 * math.log(2 * math.pi)) / 2.0, rel=1e-12)
+    assert O.zcptn(2.3, 0.4, 1.7, 1.0)[2] == pytest.approx(-1.0 / 1.7 ** 2, rel=1e-12)
+    rng = np.random.default_rng(31)
+    for _ in range(200):
+        sig, lam = 0.3 + 2.0 * rng.random(), 0.4 + 2.0 * rng.random()
+        yy = 0.0 if rng.random() < 0.3 else 3.0 * rng.random()
+        mu = -2.0 + 4.0 * rng.random()
+        _, d1, d2 = O.zcptn(yy, mu, sig, lam)
+        h1, h2 = 1e-6, 2e-4
+        fd1 = (O.zcptn(yy, mu + h1, sig, lam)[0] - O.zcptn(yy, mu - h1, sig, lam)[0]) / (2 * h1)
+        fd2 = (O.zcptn(yy, mu + h2, sig, lam)[0] - 2 * O.zcptn(yy, mu, sig, lam)[0]
+               + O.zcptn(yy, mu - h2, sig, lam)[0]) / h2 ** 2
+        assert d1 == pytest.approx(fd1, rel=1e-6, abs=1e-8)
+        assert d2 == pytest.approx(fd2, rel=1e-5, abs=1e-6)
+        assert d2 <= 0.0
+
+
+def test_latent_gaussian_nll_full_conditioning_is_exact():
+    """Latent-policy Vecchia at full conditioning through the Laplace algebra equals the dense GP
+    (approximations.cpp:320-334 with w = 1 / sigma^2)."""
+    x, y, t = _tiny(40)
+    yv = np.sin(7 * x) + y
+    th = (0.3,) + LATENT[1:]
+    om = O.OracleModel("vecchia", x, y, t, th, nbr=O.full_conditioning(len(x)), policy="latent")
+    assert om.nll(yv) == pytest.approx(O.dense_nll(x, y, t, th, yv), rel=1e-10)
+
+
+@pytest.mark.parametrize("kind", ["vecchia", "fitc", "vif"])
+def test_laplace_exact_in_gaussian_case(kind):
+    """test_laplace.cpp:144-192: lambda = 1 and strictly positive data make the ZC-PTN model Gaussian with
+    noise sigma^2, so the Laplace marginal equals the Gaussian marginal."""
+    x, y, t = _tiny(8)
+    yv = np.array([3.1, 2.4, 4.0, 2.9, 3.3, 2.2, 3.8, 2.6])
+    sig = 0.9
+    th_obs = (sig * sig,) + LATENT[1:]
+    full = O.full_conditioning(len(x))
+    P = np.column_stack([x, y, t])
+    if kind == "vecchia":
+        om = O.OracleModel("vecchia", x, y, t, LATENT, nbr=full, policy="latent")
+        ref = O.dense_nll(x, y, t, th_obs, yv)
+    elif kind == "fitc":
+        Z = P[[0, 3, 6]]
+        om = O.OracleModel("fitc", x, y, t, LATENT, Z=Z)
+        ref = O.OracleModel("fitc", x, y, t, th_obs, Z=Z).nll(yv)
+    else:
+        Z = P[[1, 4]]
+        om = O.OracleModel("vif", x, y, t, LATENT, nbr=full, Z=Z, policy="latent")
+        ref = O.dense_nll(x, y, t, th_obs, yv)
+    v, st = O.laplace_marginal(om, yv, sig, 1.0)
+    assert v == pytest.approx(ref, rel=1e-8)
