@@ -176,6 +176,16 @@ int stgp_laplace_marginal(stgp_structure* s, const double* y_host, const double*
                           double lik_sigma, double lik_lambda, const double* warm_host, double* nll_out,
                           double* mode_out, double* grad_at_mode_out, double* w_out, int* iterations_out);
 
+/* zcptn_predict (laplace.cpp:205-259): latent predictive mean / variance at the targets (n_p x 3 host
+ * x, y, t) through the LaplaceAlgebra target rows at the Laplace state (grad_at_mode, w from
+ * stgp_laplace_marginal), P(Y > 0), and n_samples Monte Carlo draws per target from
+ * mt19937_64(mix_seed(seed, p)); samples (may be NULL) is n_p x n_samples column-major. */
+int stgp_zcptn_predict(stgp_structure* s, const double* grad_at_mode_host, const double* w_host, int n_p,
+                       const double* targets_xyt_host, const double* Xp_host, int p, const double* beta,
+                       double lik_sigma, double lik_lambda, int pred_m_v, int n_samples, uint64_t seed,
+                       double* mu_latent_out, double* var_latent_out, double* p_rain_out, double* amount_mean_out,
+                       double* amount_median_out, double* samples_out);
+
 /* ---- fit driver (estimation.hpp:23-56, estimation.cpp:423-619; Gaussian likelihood) ---- */
 /* FitConfig::Method */
 #define STGP_FIT_VECCHIA_EUCLID 0

@@ -580,11 +580,13 @@ def zcptn_predict(om: "OracleModel", state, targets, lik_sigma: float, lik_lambd
     b = None if p == 0 else _f64(beta)
     outs = [np.zeros(npred) for _ in range(5)]
     samples = np.zeros((npred, n_samples), order="F")
+    vscale = np.zeros(npred)
     _chk(lib().orc_zcptn_predict(C.byref(om.m), _p(_f64(state["grad_at_mode"])), _p(_f64(state["w"])), npred,
                                  _p(qx), _p(qy), _p(qt), _p(Xpf), p, _p(b), C.c_double(lik_sigma),
                                  C.c_double(lik_lambda), pred_m_v, n_samples, C.c_uint64(seed),
-                                 *[_p(o) for o in outs], _p(samples)))
+                                 *[_p(o) for o in outs], _p(samples), _p(vscale)))
     keys = ["mu_latent", "var_latent", "p_rain", "amount_mean", "amount_median"]
     d = dict(zip(keys, outs))
+    d["var_scale"] = vscale
     d["samples"] = np.ascontiguousarray(samples)
     return d

@@ -2528,7 +2528,7 @@ int orc_zcptn_predict(const orc_model* m, const double* grad_at_mode, const doub
                       const double* qy, const double* qt, const double* Xp, int p, const double* beta,
                       double lik_sigma, double lik_lambda, int pred_m_v, int n_samples, uint64_t seed,
                       double* mu_latent, double* var_latent, double* p_rain, double* amount_mean,
-                      double* amount_median, double* samples) {
+                      double* amount_median, double* samples, double* var_scale) {
   return guarded([&] {
     if (n_samples < 2) throw ConfigError("zcptn_predict: need at least two samples for scoring");
     Model s(m);
@@ -2558,6 +2558,7 @@ int orc_zcptn_predict(const orc_model* m, const double* grad_at_mode, const doub
       const double var_lat = std::max(kr.second - kwk + wsw, 0.0);
       mu_latent[pp] = mu_lat;
       var_latent[pp] = var_lat;
+      if (var_scale) var_scale[pp] = std::abs(kr.second) + std::abs(kwk) + std::abs(wsw);
       const double s_tot = std::sqrt(lik_sigma * lik_sigma + var_lat);
       p_rain[pp] = 1.0 - norm_cdf(-mu_lat / s_tot);
       std::mt19937_64 rng(mix_seed(seed, static_cast<uint64_t>(pp)));

@@ -104,12 +104,13 @@ void orc_normal_tail(double z, double* out3);
 int orc_laplace_marginal(const orc_model* m, const double* yv, int p, const double* X, const double* beta,
                          double lik_sigma, double lik_lambda, const double* warm, double* nll_out, double* mode,
                          double* grad_at_mode, double* w_out, int* iterations);
-/* zcptn_predict (laplace.cpp:205-259); samples n_p x n_samples column-major (may be NULL) */
+/* zcptn_predict (laplace.cpp:205-259); samples n_p x n_samples column-major (may be NULL); var_scale (may
+ * be NULL): |k_pp| + |k'Wk| + |(Wk)'(Sigma^-1 + W)^-1 (Wk)|, the magnitude the variance cancels from */
 int orc_zcptn_predict(const orc_model* m, const double* grad_at_mode, const double* w, int n_p, const double* qx,
                       const double* qy, const double* qt, const double* Xp, int p, const double* beta,
                       double lik_sigma, double lik_lambda, int pred_m_v, int n_samples, uint64_t seed,
                       double* mu_latent, double* var_latent, double* p_rain, double* amount_mean,
-                      double* amount_median, double* samples);
+                      double* amount_median, double* samples, double* var_scale);
 int orc_gls_beta(const orc_model* m, const double* yv, int p, const double* X,
                  double* beta_out);
 int orc_predict(const orc_model* m, const double* yv, int p, const double* X,

@@ -10,7 +10,7 @@ from .api import (CovarianceParams, Context, SpaceTimeDataset, NeighborSets, Ind
                   build_vecchia, build_fitc, build_vif, nll, nll_grad, nll_and_grad, evaluate, gls_beta, predict,
                   euclidean_neighbors, correlation_neighbors, residual_neighbors, sts_kmeanspp,
                   joint_kmeanspp_inducing, kmeanspp, order_observations, order_observations_perm,
-                  effective_ranges, fit, default_init, read_dataset_csv, write_dataset_csv, write_neighbor_debug_csv, FitConfig, FittedModel, LikelihoodParams, LaplaceState, laplace_marginal, ConfigError, DataError, NumericError, StgpError, LATENT, OBSERVATION)
+                  effective_ranges, fit, default_init, read_dataset_csv, write_dataset_csv, write_neighbor_debug_csv, FitConfig, FittedModel, LikelihoodParams, LaplaceState, laplace_marginal, ZcptnPrediction, zcptn_predict, ConfigError, DataError, NumericError, StgpError, LATENT, OBSERVATION)
 from ._native import LIB_PATH, exported_symbols  # noqa: F401
 from . import synth  # noqa: F401
 

@@ -75,6 +75,8 @@ _SIGS = {
     "stgp_nll_and_grad": [_P, _P, _P, C.c_int, _P, _D, _P],
     "stgp_gls_beta": [_P, _P, _P, C.c_int, _P],
     "stgp_predict": [_P, _P, _P, C.c_int, _P, C.c_int, _P, _P, C.c_int, _P, _P],
+    "stgp_zcptn_predict": [_P, _P, _P, C.c_int, _P, _P, C.c_int, _P, C.c_double, C.c_double, C.c_int, C.c_int,
+                           C.c_uint64, _P, _P, _P, _P, _P, _P],
     "stgp_laplace_marginal": [_P, _P, _P, C.c_int, _P, C.c_double, C.c_double, _P, _D, _P, _P, _P,
                               C.POINTER(C.c_int)],
     "stgp_eval": [_P, C.POINTER(Params), _P, _P, C.c_int, _P, _D, _P],

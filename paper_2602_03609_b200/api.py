@@ -501,6 +501,35 @@ def laplace_marginal(s: Structure, y, X=None, beta=None, lik: LikelihoodParams |
     return out.value, LaplaceState(mode, ga, w, -out.value, True, it.value)
 
 
+@dataclass
+class ZcptnPrediction:
+    """ZcptnPrediction (laplace.hpp:55-62)."""
+    mu_latent: np.ndarray
+    var_latent: np.ndarray
+    p_rain: np.ndarray
+    amount_mean: np.ndarray
+    amount_median: np.ndarray
+    samples: np.ndarray
+
+
+def zcptn_predict(state: LaplaceState, s: Structure, targets, X_p=None, beta=None,
+                  lik: LikelihoodParams | None = None, pred_m_v: int = 0, n_samples: int = 200,
+                  seed: int = 0) -> ZcptnPrediction:
+    """zcptn_predict (laplace.hpp:67-72) from the Laplace state of laplace_marginal."""
+    lik = lik or LikelihoodParams()
+    T = np.ascontiguousarray(np.asarray(targets, dtype=np.float64).reshape(-1, 3))
+    npred = len(T)
+    p = 0 if X_p is None or beta is None or np.size(beta) == 0 else np.asarray(X_p).reshape(npred, -1).shape[1]
+    Xp = None if p == 0 else np.asfortranarray(np.asarray(X_p, dtype=np.float64).reshape(npred, -1))
+    b = None if p == 0 else _f64(beta)
+    outs = [np.zeros(npred) for _ in range(5)]
+    samples = np.zeros((npred, n_samples), order="F")
+    N.call("stgp_zcptn_predict", s.h, _ptr(_f64(state.grad_at_mode)), _ptr(_f64(state.w)), npred, _ptr(T), _ptr(Xp), p,
+           _ptr(b), float(lik.sigma), float(lik.lambda_), int(pred_m_v), int(n_samples), C.c_uint64(seed),
+           *[_ptr(o) for o in outs], _ptr(samples))
+    return ZcptnPrediction(*outs, np.ascontiguousarray(samples))
+
+
 def debug_exp(x, ctx: Context | None = None) -> np.ndarray:
     ctx = ctx or default_context()
     x = _f64(x)

@@ -307,6 +307,61 @@ static void lap_solve(stgp_structure* s, const double* x, double* out) {
   }
 }
 
+namespace {
+__global__ void scale_rows_kernel(int n, long long ncols, const double* d, const double* X, double* out) {
+  const long long total = static_cast<long long>(n) * ncols;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x)
+    out[e] = X[e] * d[e % n];
+}
+__global__ void fitc_combine_kernel(int n, long long ncols, const double* e1, const double* X, const double* scale,
+                                    const double* H, double* out) {
+  const long long total = static_cast<long long>(n) * ncols;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = e % n;
+    out[e] = e1[i] * X[e] + scale[i] * H[e];
+  }
+}
+}  // namespace
+
+void laplace_prepare_w(stgp_structure* s, const double* w_dev) {
+  laplace_release(s);
+  lap_prepare(s, w_dev, 0.0);
+}
+
+// out (n x ncols) = (Sigma^{-1} + W)^{-1} X after laplace_prepare_w
+void laplace_solve_cols(stgp_structure* s, const double* X, long long ncols, double* out) {
+  LaplaceDev* L = s->lap;
+  stgp_ctx* ctx = s->ds->ctx;
+  cudaStream_t st = ctx->stream;
+  const int n = L->n, ldm = L->ldm;
+  const int nc = static_cast<int>(ncols);
+  if (L->kind == STGP_FITC) {
+    DevBuf<double> T1(static_cast<size_t>(n) * nc), G(static_cast<size_t>(ldm) * nc), H(static_cast<size_t>(n) * nc);
+    scale_rows_kernel<<<grid_for(static_cast<long long>(n) * nc), kT, 0, st>>>(n, nc, L->scale.get(), X, T1.get());
+    launched(ctx);
+    dev_gemm(ctx, false, false, ldm, nc, n, 1.0, s->lr.W.get(), ldm, T1.get(), n, 0.0, G.get(), ldm);
+    dev_trsm_left(ctx, L->Kw.get(), ldm, ldm, G.get(), ldm, nc, false);
+    dev_trsm_left(ctx, L->Kw.get(), ldm, ldm, G.get(), ldm, nc, true);
+    dev_gemm(ctx, true, false, n, nc, ldm, 1.0, s->lr.W.get(), ldm, G.get(), ldm, 0.0, H.get(), n);
+    fitc_combine_kernel<<<grid_for(static_cast<long long>(n) * nc), kT, 0, st>>>(n, nc, L->e1.get(), X, L->scale.get(),
+                                                                                   H.get(), out);
+    launched(ctx);
+    return;
+  }
+  STGP_CUDA(cudaMemcpyAsync(out, X, sizeof(double) * n * nc, cudaMemcpyDeviceToDevice, st));
+  dev_trsm_left(ctx, L->S.get(), n, n, out, n, nc, false);
+  dev_trsm_left(ctx, L->S.get(), n, n, out, n, nc, true);
+  if (L->kind == STGP_VIF && L->M > 0) {
+    DevBuf<double> Q1(static_cast<size_t>(ldm) * nc);
+    dev_gemm(ctx, true, false, ldm, nc, n, 1.0, L->QWt.get(), n, out, n, 0.0, Q1.get(), ldm);
+    dev_trsm_left(ctx, L->Kw.get(), ldm, ldm, Q1.get(), ldm, nc, false);
+    dev_trsm_left(ctx, L->Kw.get(), ldm, ldm, Q1.get(), ldm, nc, true);
+    dev_gemm(ctx, false, false, n, nc, ldm, 1.0, L->Zw.get(), n, Q1.get(), ldm, 1.0, out, n);
+  }
+}
+
 // latent_policy_nll (approximations.cpp:320-334) on the structure's residual s->r
 double latent_policy_nll_dev(stgp_structure* s) {
   const double sigma2 = s->th.sigma2;

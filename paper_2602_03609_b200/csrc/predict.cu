@@ -237,6 +237,7 @@ struct CondArgs {
   double* A_out;    // np x m (VIF: for W sN)
   double* scratch;  // per-thread k x k + 2k
   int* fail;
+  int laplace;  // Laplace target rows (approximations.cpp:1135-1146, 1320-1331): no nugget, C + 1e-10 s1, no retry
 };
 
 // thread per target: conditional block over N with one jitter retry (approximations.cpp:889-913, 1016-1043)
@@ -278,10 +279,10 @@ __global__ void cond_solve_kernel(CondArgs a, bool vif) {
       }
     }
     bool ok = false;
-    for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+    for (int attempt = a.laplace ? 1 : 0; attempt < 2 && !ok; ++attempt) {
       // restore the lower triangle from the upper one (diagonal kept in A[] on the first pass)
       for (int i = 0; i < k; ++i) {
-        if (attempt == 0) A[i] = C[i * K + i];
+        if (attempt == 0 || a.laplace) A[i] = C[i * K + i];
         for (int b = 0; b < i; ++b) C[i * K + b] = C[b * K + i];
         C[i * K + i] = attempt == 0 ? A[i] : A[i] + 1e-10 * a.s1;
       }
@@ -319,11 +320,14 @@ __global__ void cond_solve_kernel(CondArgs a, bool vif) {
     }
     double ar = 0.0, ac = 0.0;
     for (int i = 0; i < k; ++i) {
-      ar += A[i] * a.r[N[i]];
+      if (a.r) ar += A[i] * a.r[N[i]];
       ac += A[i] * c[i];
     }
-    a.mu_part[p] = ar;
-    if (vif) {
+    if (a.mu_part) a.mu_part[p] = ar;
+    if (a.laplace) {  // D_p = (s1 or r_q) - A.c, and A
+      a.var_out[p] = (vif ? a.rq[p] : a.s1) - ac;
+      for (int i = 0; i < K; ++i) a.A_out[static_cast<size_t>(p) * K + i] = i < k ? A[i] : 0.0;
+    } else if (vif) {
       a.var_out[p] = a.rq[p] + a.sigma2 - ac;  // D_p
       for (int i = 0; i < K; ++i) a.A_out[static_cast<size_t>(p) * K + i] = i < k ? A[i] : 0.0;
     } else {
@@ -489,7 +493,7 @@ static void target_neighbors(stgp_structure* s, TargetSet& T, int np, int pred_m
 
 static void cond_solve(stgp_structure* s, TargetSet& T, int np, int pred_m_v, const DevBuf<int32_t>& nbr,
                        const double* rvec, bool vif, const double* Wq, const double* rq, double* mu_part, double* var,
-                       double* Aout) {
+                       double* Aout, bool laplace = false) {
   stgp_ctx* ctx = s->ds->ctx;
   CondArgs c{};
   c.np = np;
@@ -515,6 +519,8 @@ static void cond_solve(stgp_structure* s, TargetSet& T, int np, int pred_m_v, co
   c.mu_part = mu_part;
   c.var_out = var;
   c.A_out = Aout;
+  c.laplace = laplace ? 1 : 0;
+  if (laplace) c.sigma2 = 0.0;
   DevBuf<double> scratch(static_cast<size_t>(np) * (static_cast<size_t>(pred_m_v) * pred_m_v + 2 * pred_m_v));
   c.scratch = scratch.get();
   DevBuf<int> fail(1);
@@ -525,6 +531,8 @@ static void cond_solve(stgp_structure* s, TargetSet& T, int np, int pred_m_v, co
   int f = 0;
   fail.download(&f, 1, ctx->stream);
   STGP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (f && laplace)
+    numeric_error(vif ? "VifLaplace: target conditioning block failed" : "VecchiaLaplace: target conditioning block failed");
   if (f)
     numeric_error(vif ? "predict: residual conditioning block not positive definite"
                       : "predict: conditioning block not positive definite");
@@ -689,6 +697,153 @@ static void vif_predict(stgp_structure* s, TargetSet& T, int np, int pred_m_v, d
     const double v = hwq2[p] + hD[p] - 2.0 * hcross[p] - hq[p] + hh[p];
     var[p] = v > 0.0 ? v : 0.0;
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// ZC-PTN prediction (laplace.cpp:205-259) on the Laplace state at the mode: latent cross covariances
+// k_p (the LaplaceAlgebra target rows, approximations.cpp:1121-1160, 1202-1215, 1290-1355), then
+//   mu_p = x_p beta + k_p . a,   var_p = k_pp - k_p' W k_p + (W k_p)' (Sigma^{-1} + W)^{-1} (W k_p),
+// for all targets at once (n x n_p matrices).  For Vecchia / VIF, Sigma_s s_N = B^{-1} D B^{-T} s_N is
+// two triangular solves with the dense unit-lower B.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void dense_b_kernel(int n, int m_v, const int32_t* nbr, const double* A, double* B) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    B[static_cast<size_t>(i) * n + i] = 1.0;
+    for (int a = 0; a < m_v; ++a) {
+      const int j = nbr[static_cast<size_t>(i) * m_v + a];
+      if (j >= 0) B[static_cast<size_t>(j) * n + i] = -A[static_cast<size_t>(i) * m_v + a];
+    }
+  }
+}
+// SN(:, p) = A_p scattered at the target's neighbours
+__global__ void scatter_sn_kernel(int n, int np, int m, const int32_t* nbr, const double* A, double* SN) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x)
+    for (int a = 0; a < m; ++a) {
+      const int j = nbr[static_cast<size_t>(p) * m + a];
+      if (j >= 0) SN[static_cast<size_t>(p) * n + j] = A[static_cast<size_t>(p) * m + a];
+    }
+}
+__global__ void scale_rows_kernel(int n, long long ncols, const double* d, double* X) {
+  const long long total = static_cast<long long>(n) * ncols;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x)
+    X[e] *= d[e % n];
+}
+// var_prior(p) = base(p) + D_p + sum_a A_p[a] Kp(N_p[a], p)
+__global__ void prior_var_kernel(int n, int np, int m, const int32_t* nbr, const double* A, const double* Kp,
+                                 const double* Dp, const double* base, double* out) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x) {
+    double v = (base ? base[p] : 0.0) + Dp[p];
+    for (int a = 0; a < m; ++a) {
+      const int j = nbr[static_cast<size_t>(p) * m + a];
+      if (j >= 0) v += A[static_cast<size_t>(p) * m + a] * Kp[static_cast<size_t>(p) * n + j];
+    }
+    out[p] = v;
+  }
+}
+}  // namespace
+
+void zcptn_moments_dev(stgp_structure* s, const double* a_host, const double* w_host, int np, const double* txyt,
+                       int pred_m_v, double* mu_lat, double* var_lat) {
+  stgp_ctx* ctx = s->ds->ctx;
+  cudaStream_t st = ctx->stream;
+  const int n = s->n;
+  LowRank& L = s->lr;
+  const int ldm = L.ldm, M = s->kind == STGP_VECCHIA ? 0 : L.M;
+  if (pred_m_v < 0) config_error("predict: pred_m_v must be >= 0");
+  if (s->kind != STGP_FITC && n > 40000)
+    config_error("Laplace algebra: the dense factorization of Q + W supports n <= 40000 (desk scale, SPEC.md:9)");
+  DevBuf<double> wv(n), av(n);
+  wv.upload(w_host, n, st);
+  av.upload(a_host, n, st);
+  laplace_prepare_w(s, wv.get());
+  TargetSet T;
+  setup_targets(s, np, txyt, T);
+  DevBuf<double> Kp(static_cast<size_t>(n) * np), kpp(np);
+  DevBuf<double> Up, Wq;
+  if (M > 0) {
+    Up.alloc(static_cast<size_t>(ldm) * np);
+    Wq.alloc(static_cast<size_t>(ldm) * np);
+    target_cross_kernel<<<std::max(1, std::min(np, ctx->num_sms * 8)), 128, 0, st>>>(
+        L.zx.get(), L.zy.get(), L.ztid.get(), M, ldm, T.qx.get(), T.qy.get(), T.qtid.get(), np, dev_kernel(s->th),
+        lag_view(s->lt), Up.get());
+    launched(ctx);
+    dev_trmm_left(ctx, L.Lminv.get(), ldm, ldm, Up.get(), ldm, np, false, Wq.get(), ldm);  // w_q = L_m^{-1} u_p
+  }
+  if (s->kind == STGP_FITC) {  // k_p = U^T Sigma_m^{-1} u_p = W^T w_q, k_pp = s1
+    dev_gemm(ctx, true, false, n, np, ldm, 1.0, L.W.get(), ldm, Wq.get(), ldm, 0.0, Kp.get(), n);
+    std::vector<double> s1v(np, s->th.sigma1_2);
+    kpp.upload(s1v.data(), np, st);
+  } else {
+    const bool vif = s->kind == STGP_VIF;
+    DevBuf<double> rq(np), wq2(np);
+    double* resid = nullptr;
+    if (vif && M > 0) {
+      coldot_kernel<<<grid_for(static_cast<long long>(np) * 32), 256, 0, st>>>(np, ldm, Wq.get(), Wq.get(), wq2.get());
+      launched(ctx);
+      resid_from_sq_kernel<<<grid_for(np), 256, 0, st>>>(np, s->th.sigma1_2, wq2.get(), rq.get());
+      launched(ctx);
+      double* sq = L.tmp("p_sq", n);
+      coldot_kernel<<<grid_for(static_cast<long long>(n) * 32), 256, 0, st>>>(n, ldm, L.W.get(), L.W.get(), sq);
+      launched(ctx);
+      resid = L.tmp("p_resid", n);
+      resid_from_sq_kernel<<<grid_for(n), 256, 0, st>>>(n, s->th.sigma1_2, sq, resid);
+      launched(ctx);
+    } else if (vif) {
+      std::vector<double> s1v(std::max(n, np), s->th.sigma1_2);
+      resid = L.tmp("p_resid", n);
+      STGP_CUDA(cudaMemcpyAsync(rq.get(), s1v.data(), sizeof(double) * np, cudaMemcpyHostToDevice, st));
+      STGP_CUDA(cudaMemcpyAsync(resid, s1v.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      STGP_CUDA(cudaMemsetAsync(wq2.get(), 0, sizeof(double) * np, st));
+    }
+    const int m = std::max(1, std::min(pred_m_v, n));
+    DevBuf<int32_t> nbr;
+    if (vif)
+      target_neighbors(s, T, np, m, 2, M > 0 ? Wq.get() : nullptr, rq.get(), resid, nbr, M > 0 ? L.tmp("p_sq", n) : nullptr,
+                       M > 0 ? wq2.get() : nullptr);
+    else
+      target_neighbors(s, T, np, m, s->nbr_kind == STGP_METRIC_EUCLID ? 0 : 1, nullptr, nullptr, nullptr, nbr);
+    DevBuf<double> Dp(np), A(static_cast<size_t>(np) * m);
+    cond_solve(s, T, np, m, nbr, nullptr, vif, M > 0 ? Wq.get() : nullptr, vif ? rq.get() : nullptr, nullptr, Dp.get(),
+               A.get(), true);
+    // Kp = Sigma_s SN = B^{-1} D B^{-T} SN
+    DevBuf<double> Bd(static_cast<size_t>(n) * n);
+    Bd.zero(st);
+    dense_b_kernel<<<grid_for(n), 256, 0, st>>>(n, s->m_v, s->nbr.get(), s->A.get(), Bd.get());
+    launched(ctx);
+    Kp.zero(st);
+    scatter_sn_kernel<<<grid_for(np), 256, 0, st>>>(n, np, m, nbr.get(), A.get(), Kp.get());
+    launched(ctx);
+    dev_trsm_left(ctx, Bd.get(), n, n, Kp.get(), n, np, true);
+    scale_rows_kernel<<<grid_for(static_cast<long long>(n) * np), 256, 0, st>>>(n, np, s->D.get(), Kp.get());
+    launched(ctx);
+    dev_trsm_left(ctx, Bd.get(), n, n, Kp.get(), n, np, false);
+    prior_var_kernel<<<grid_for(np), 256, 0, st>>>(n, np, m, nbr.get(), A.get(), Kp.get(), Dp.get(),
+                                                   vif && M > 0 ? wq2.get() : nullptr, kpp.get());
+    launched(ctx);
+    if (vif && M > 0)  // + U^T Sigma_m^{-1} u_p = W^T w_q
+      dev_gemm(ctx, true, false, n, np, ldm, 1.0, L.W.get(), ldm, Wq.get(), ldm, 1.0, Kp.get(), n);
+  }
+  // mu = k . a ; var = k_pp - k' W k + (W k)' (Sigma^{-1} + W)^{-1} (W k)
+  DevBuf<double> muv(np), q1(np), q2(np), WK(static_cast<size_t>(n) * np), SW(static_cast<size_t>(n) * np);
+  dev_gemv(ctx, true, n, np, 1.0, Kp.get(), n, av.get(), 0.0, muv.get());
+  STGP_CUDA(cudaMemcpyAsync(WK.get(), Kp.get(), sizeof(double) * n * np, cudaMemcpyDeviceToDevice, st));
+  scale_rows_kernel<<<grid_for(static_cast<long long>(n) * np), 256, 0, st>>>(n, np, wv.get(), WK.get());
+  launched(ctx);
+  coldot_kernel<<<grid_for(static_cast<long long>(np) * 32), 256, 0, st>>>(np, n, Kp.get(), WK.get(), q1.get());
+  launched(ctx);
+  laplace_solve_cols(s, WK.get(), np, SW.get());
+  coldot_kernel<<<grid_for(static_cast<long long>(np) * 32), 256, 0, st>>>(np, n, WK.get(), SW.get(), q2.get());
+  launched(ctx);
+  std::vector<double> hk(np), h1(np), h2(np);
+  muv.download(mu_lat, np, st);
+  kpp.download(hk.data(), np, st);
+  q1.download(h1.data(), np, st);
+  q2.download(h2.data(), np, st);
+  STGP_CUDA(cudaStreamSynchronize(st));
+  for (int p = 0; p < np; ++p) var_lat[p] = std::max(hk[p] - h1[p] + h2[p], 0.0);
 }
 
 void lowrank_predict(stgp_structure* s, int np, const double* txyt, int pred_m_v, double* mu, double* var) {

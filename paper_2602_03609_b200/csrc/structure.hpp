@@ -109,6 +109,10 @@ LagTable lag_view(const DevLagTable& d);
 // latent-policy likelihoods (laplace.cu)
 void laplace_release(stgp_structure* s);
 double latent_policy_nll_dev(stgp_structure* s);
+void laplace_prepare_w(stgp_structure* s, const double* w_dev);
+void laplace_solve_cols(stgp_structure* s, const double* X, long long ncols, double* out);
+void zcptn_moments_dev(stgp_structure* s, const double* a_host, const double* w_host, int np, const double* txyt,
+                       int pred_m_v, double* mu_lat, double* var_lat);
 double laplace_marginal_dev(stgp_structure* s, const double* y_host, const double* off_dev, double sigma,
                             double lambda, const double* warm_host, double* mode_out, double* a_out, double* w_out,
                             int* iters_out);

@@ -1,3 +1,6 @@
+#include <cmath>
+#include <algorithm>
+#include <random>
 // Structure builders and likelihood entry points (approximations.cpp:198-744).
 // Vecchia lives here; the low-rank FITC/VIF algebra is in lowrank.cu.
 #include <atomic>
@@ -315,6 +318,55 @@ int stgp_laplace_marginal(stgp_structure* s, const double* y, const double* X, i
     laplace_release(s);
     *nll_out = laplace_marginal_dev(s, y, off.get(), lik_sigma, lik_lambda, warm, mode, grad_at_mode, w, iterations);
     laplace_release(s);
+  });
+}
+
+// zcptn_predict (laplace.cpp:205-259): latent moments on the device from the Laplace state, then the
+// occurrence probability and the Monte Carlo amounts with the reference's per-target RNG streams
+// (mt19937_64(mix_seed(seed, p)), std::normal_distribution) on the host
+int stgp_zcptn_predict(stgp_structure* s, const double* grad_at_mode, const double* w, int n_p, const double* txyt,
+                       const double* Xp, int p, const double* beta, double lik_sigma, double lik_lambda, int pred_m_v,
+                       int n_samples, uint64_t seed, double* mu_latent, double* var_latent, double* p_rain,
+                       double* amount_mean, double* amount_median, double* samples) {
+  return guarded([&] {
+    if (!s || !grad_at_mode || !w || (n_p > 0 && (!txyt || !mu_latent || !var_latent || !p_rain || !amount_mean ||
+                                                  !amount_median)))
+      config_error("stgp_zcptn_predict: null argument");
+    if (n_samples < 2) config_error("zcptn_predict: need at least two samples for scoring");
+    if (!(lik_sigma > 0.0) || !std::isfinite(lik_sigma)) config_error("LikelihoodParams: sigma must be > 0");
+    if (!(lik_lambda > 0.0) || !std::isfinite(lik_lambda)) config_error("LikelihoodParams: lambda must be > 0");
+    if (s->kind != STGP_FITC && s->policy != STGP_LATENT)
+      numeric_error("LaplaceAlgebra: requires a latent-policy structure");
+    if (n_p <= 0) return;
+    laplace_release(s);
+    zcptn_moments_dev(s, grad_at_mode, w, n_p, txyt, pred_m_v, mu_latent, var_latent);
+    laplace_release(s);
+    for (int q = 0; q < n_p; ++q) {
+      double off = 0.0;
+      if (p > 0 && Xp && beta)
+        for (int j = 0; j < p; ++j) off += Xp[static_cast<size_t>(q) + static_cast<size_t>(j) * n_p] * beta[j];
+      const double mu = off + mu_latent[q];
+      const double var = var_latent[q];
+      mu_latent[q] = mu;
+      const double s_tot = std::sqrt(lik_sigma * lik_sigma + var);
+      p_rain[q] = 1.0 - 0.5 * std::erfc((mu / s_tot) / 1.4142135623730951);
+      std::mt19937_64 rng(mix_seed(seed, static_cast<uint64_t>(q)));
+      std::normal_distribution<double> gauss(0.0, 1.0);
+      const double sd = std::sqrt(var);
+      double acc = 0.0;
+      std::vector<double> draws(static_cast<size_t>(n_samples));
+      for (int k = 0; k < n_samples; ++k) {
+        const double latent = mu + sd * gauss(rng);
+        const double zval = latent + lik_sigma * gauss(rng);
+        const double amount = zval <= 0.0 ? 0.0 : std::pow(zval, lik_lambda);
+        if (samples) samples[static_cast<size_t>(q) + static_cast<size_t>(k) * n_p] = amount;
+        draws[static_cast<size_t>(k)] = amount;
+        acc += amount;
+      }
+      amount_mean[q] = acc / n_samples;
+      std::nth_element(draws.begin(), draws.begin() + n_samples / 2, draws.end());
+      amount_median[q] = draws[static_cast<size_t>(n_samples) / 2];
+    }
   });
 }
 

@@ -117,3 +117,31 @@ def test_laplace_rejects_bad_inputs(S):
     so = S.build_vecchia(ds, TH, S.NeighborSets.from_sets(ds, O.dc_neighbors(x, y, t, TH, 5)), S.OBSERVATION)
     with pytest.raises(S.NumericError):  # LaplaceAlgebra: requires a latent-policy structure
         S.laplace_marginal(so, np.abs(resp), lik=S.LikelihoodParams(1.0, 1.0))
+
+
+@pytest.mark.parametrize("kind", ["vecchia", "fitc", "vif"])
+def test_zcptn_predict(S, kind):
+    """zcptn_predict (laplace.cpp:205-259): latent moments 1e-8, P(rain) and the Monte Carlo amounts from
+    the same RNG streams (draws differ from the oracle's only through the moments)."""
+    x, y, t, resp = _data(S)
+    rng = np.random.default_rng(13)
+    amounts = np.where(rng.random(len(x)) < 0.4, 0.0, rng.gamma(1.5, 1.0, len(x)))
+    s, om, keep = _structures(S, kind, x, y, t, LATENT)
+    lik = S.LikelihoodParams(0.7, 1.4)
+    last = t == t.max()
+    T = np.column_stack([x[last][:25], y[last][:25], np.full(min(25, int(last.sum())), t.max() + 1.0)])
+    # the same Laplace state on both sides (each Newton stops at its own 1e-6 gradient gap, which would
+    # otherwise enter mu = k . a at that level)
+    _, str_ = O.laplace_marginal(om, amounts, 0.7, 1.4)
+    st = S.LaplaceState(str_["mode"], str_["grad_at_mode"], str_["w"], 0.0, True, str_["iterations"])
+    pr = S.zcptn_predict(st, s, T, lik=lik, pred_m_v=8, n_samples=64, seed=9)
+    ref = O.zcptn_predict(om, str_, T, 0.7, 1.4, 8, 64, 9)
+    s1 = LATENT[1]
+    assert np.allclose(pr.mu_latent, ref["mu_latent"], rtol=1e-8, atol=1e-8 * np.sqrt(s1))
+    # the variance is k_pp - k'Wk + (Wk)'(Sigma^-1 + W)^-1 (Wk): 1e-8 of the magnitude it cancels from
+    verr = np.abs(pr.var_latent - ref["var_latent"])
+    assert (verr <= 1e-8 * ref["var_scale"]).all(), (verr / ref["var_scale"]).max()
+    tol = 1e-8 * np.maximum(ref["var_scale"], 1.0)  # P(rain), draws: through mu and var
+    assert (np.abs(pr.p_rain - ref["p_rain"]) <= tol).all()
+    assert (np.abs(pr.samples - ref["samples"]) <= 10 * tol[:, None] * (1 + np.abs(ref["samples"]))).all()
+    assert (np.abs(pr.amount_mean - ref["amount_mean"]) <= 10 * tol * (1 + np.abs(ref["amount_mean"]))).all()
