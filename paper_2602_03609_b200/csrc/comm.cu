@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "comm.hpp"
 #include "structure.hpp"
@@ -66,11 +67,48 @@ __global__ void gather_unpack_kernel(long long total, const double* bi, const do
 }
 }  // namespace
 
-// Every rank computed neighbour rows [r0, r1) of its shard; afterwards all ranks hold all rows.  A sum
-// all-reduce of zero-filled buffers (indices stored as idx + 1, exact in f64): x + 0 = x bit for bit,
-// and the same collective serves NCCL and the host hook.
+// Every rank computed neighbour rows [r0, r1) of its shard; afterwards all ranks hold all rows.
+// NCCL: the ranks' row ranges are exchanged once (a 2 x world host all-reduce), then the int32 indices
+// and f64 distances of the own rows go out in one ncclAllGather each, padded to the longest range, and
+// land at their ranges with device copies: 12 bytes per neighbour slot, stream ordered, no host sync.
+// Host hook (in-process test ranks): a sum all-reduce of zero-filled buffers, indices stored as idx + 1
+// (exact in f64; distances are >= +0, so x + 0 = x bit for bit).
 void gather_rows(stgp_ctx* ctx, int32_t* idx, double* dist, long long n, int m_v, int r0, int r1) {
   if (ctx->world == 1 || n == 0) return;
+  if (ctx->comm) {
+    std::vector<double> rng(static_cast<size_t>(2 * ctx->world), 0.0);
+    rng[static_cast<size_t>(2 * ctx->rank)] = r0;
+    rng[static_cast<size_t>(2 * ctx->rank + 1)] = r1;
+    allreduce_host(ctx, rng);
+    long long maxrows = 0;
+    for (int k = 0; k < ctx->world; ++k)
+      maxrows = std::max<long long>(maxrows, static_cast<long long>(rng[2 * k + 1] - rng[2 * k]));
+    const size_t slot = static_cast<size_t>(std::max<long long>(maxrows, 1)) * m_v;
+    DevBuf<int32_t> si(slot), ri(slot * ctx->world);
+    DevBuf<double> sd(slot), rd(slot * ctx->world);
+    const size_t own = static_cast<size_t>(r1 - r0) * m_v;
+    if (own) {
+      STGP_CUDA(cudaMemcpyAsync(si.get(), idx + static_cast<size_t>(r0) * m_v, own * 4, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+      if (dist)
+        STGP_CUDA(cudaMemcpyAsync(sd.get(), dist + static_cast<size_t>(r0) * m_v, own * 8, cudaMemcpyDeviceToDevice,
+                                  ctx->stream));
+    }
+    ncclComm_t c = reinterpret_cast<ncclComm_t>(ctx->comm);
+    ncclResult_t r = ncclAllGather(si.get(), ri.get(), slot, ncclInt32, c, ctx->stream);
+    if (r == ncclSuccess && dist) r = ncclAllGather(sd.get(), rd.get(), slot, ncclDouble, c, ctx->stream);
+    if (r != ncclSuccess) throw Error(kInternal, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    for (int k = 0; k < ctx->world; ++k) {
+      const long long k0 = static_cast<long long>(rng[2 * k]), k1 = static_cast<long long>(rng[2 * k + 1]);
+      if (k == ctx->rank || k1 <= k0) continue;
+      const size_t cnt = static_cast<size_t>(k1 - k0) * m_v;
+      STGP_CUDA(cudaMemcpyAsync(idx + k0 * m_v, ri.get() + k * slot, cnt * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+      if (dist)
+        STGP_CUDA(cudaMemcpyAsync(dist + k0 * m_v, rd.get() + k * slot, cnt * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    STGP_CUDA(cudaStreamSynchronize(ctx->stream));  // the staging buffers are freed at scope exit
+    return;
+  }
   const long long total = n * m_v;
   DevBuf<double> bi(static_cast<size_t>(total)), bd(static_cast<size_t>(total));
   const int grid = static_cast<int>(std::min<long long>((total + 255) / 256, ctx->num_sms * 32LL));

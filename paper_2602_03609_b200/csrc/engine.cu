@@ -41,8 +41,13 @@ PoolDev& pool_dev(int dev) {
     d.init = true;
     const char* e = std::getenv("STGP_POOL");
     d.on = !(e && e[0] == '0');
-    if (d.on) {
-      STGP_CUDA(cudaDeviceGetDefaultMemPool(&d.pool, dev));
+    if (d.on) {  // a private pool: the process's default pool (and other libraries using it) keep their settings
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.handleTypes = cudaMemHandleTypeNone;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      STGP_CUDA(cudaMemPoolCreate(&d.pool, &props));
       uint64_t thr = UINT64_MAX;
       STGP_CUDA(cudaMemPoolSetAttribute(d.pool, cudaMemPoolAttrReleaseThreshold, &thr));
       STGP_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
