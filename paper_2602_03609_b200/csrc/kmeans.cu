@@ -10,11 +10,14 @@
 //   * Lloyd: argmin with strict <, sequential inertia, per-cluster sequential
 //     sums in index order, empty clusters re-seeded in cluster order.
 #include <algorithm>
+#include <memory>
 #include <cstring>
 #include <numeric>
 #include <random>
 #include <set>
 #include <unordered_map>
+
+#include <cub/device/device_radix_sort.cuh>
 
 #include "comm.hpp"
 #include "lowrank_common.cuh"
@@ -58,7 +61,8 @@ __global__ void d2_update_kernel(KArgs a, int j, bool init, double* d2) {
 constexpr int kPickChunk = 12288;  // doubles (96 KB), a multiple of 8
 constexpr int kPickThreads = 1024;
 __global__ void __launch_bounds__(kPickThreads) pick_kernel(KArgs a, const double* d2, double canon, int j,
-                                                            long* pick_out) {
+                                                            long* pick_out, const int* need = nullptr) {
+  if (need && *need == 0) return;  // the certified parallel pick already decided
   extern __shared__ double sd[];
   __shared__ double s_u;
   __shared__ int s_done;
@@ -158,21 +162,231 @@ __global__ void __launch_bounds__(kPickThreads) pick_kernel(KArgs a, const doubl
   }
 }
 
-// Lloyd assignment: best center with strict < (first minimum)
-__global__ void assign_kernel(KArgs a, int* assign, double* best) {
-  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < a.n;
-       i += static_cast<long>(gridDim.x) * blockDim.x) {
-    double b = __longlong_as_double(0x7ff0000000000000LL);
-    int bj = 0;
-    for (int j = 0; j < a.k; ++j) {
-      const double v = row_d2(a, i, a.C, a.k, j);
-      if (v < b) {
-        b = v;
-        bj = j;
+// ---------------------------------------------------------------------------
+// Parallel certified pick.  The reference's pick (inducing.cpp:32-42) is defined by two sequential
+// floating-point chains: the Eigen-order total t_seq and the running sums acc_i; pick = first i with
+// u <= acc_i, u = fl(canon t_seq).  For non-negative weights every order of summation stays within
+// gamma_n = n eps / (1 - n eps) of the exact sum, so with the exact prefix sums S_i (double-double here):
+//   u in [u_lo, u_hi] = canon T (1 -/+ (gamma_n + 2 eps)),   acc_i in [S_i (1 - gamma_n), S_i (1 + gamma_n)].
+// If i* = first i with S_i (1 - gamma_n) >= u_hi also has S_{i*-1} (1 + gamma_n) < u_lo, every possible
+// rounding of the two chains picks i*: the pick is certain without running them.  Otherwise (u within
+// ~gamma_n T of a boundary: ~1e-4 per pick at n = 1.1M) the exact sequential pick_kernel decides.
+// One launch per pick: every block first applies the previous center's D^2 update to its segment, sums
+// it in double-double, and the last block to finish scans the block sums and the segment that holds the
+// crossing.
+// ---------------------------------------------------------------------------
+struct DD {
+  double hi, lo;
+};
+__device__ __forceinline__ DD dd_add(DD a, double x) {
+  const double t = a.hi + x;
+  const double bp = t - a.hi;
+  const double e = (a.hi - (t - bp)) + (x - bp);
+  return DD{t, a.lo + e};
+}
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+  DD r = dd_add(a, b.hi);
+  r.lo += b.lo;
+  const double t = r.hi + r.lo;
+  return DD{t, r.lo - (t - r.hi)};
+}
+__device__ __forceinline__ double dd_val(DD a) { return a.hi + a.lo; }
+
+constexpr int kCpThreads = 256;
+struct PickArgs {
+  KArgs a;
+  double* d2;
+  int j;           // center being picked; j - 1 is applied to d2 first (j >= 2)
+  double canon;
+  long* pick_out;
+  DD* bsum;        // per-block sums
+  unsigned* ticket;
+  int* fallback;   // 1: the exact sequential pick must decide
+};
+
+__global__ void __launch_bounds__(kCpThreads) pick_certified_kernel(PickArgs p) {
+  __shared__ DD sred[kCpThreads];
+  __shared__ bool last;
+  __shared__ long s_best;
+  const KArgs& a = p.a;
+  const long n = a.n;
+  const int G = gridDim.x, b = blockIdx.x, t = threadIdx.x;
+  const long s0 = n * b / G, s1 = n * (b + 1) / G;
+  DD acc{0.0, 0.0};
+  for (long i = s0 + t; i < s1; i += kCpThreads) {
+    double v = p.d2[i];
+    if (p.j >= 2) {
+      const double c = row_d2(a, i, a.C, a.k, p.j - 1);
+      v = c < v ? c : v;
+      p.d2[i] = v;
+    }
+    acc = dd_add(acc, v);
+  }
+  sred[t] = acc;
+  __threadfence();  // this thread's d2 updates, before the ticket makes them the last block's input
+  __syncthreads();
+  for (int o = kCpThreads / 2; o > 0; o >>= 1) {
+    if (t < o) sred[t] = dd_add(sred[t], sred[t + o]);
+    __syncthreads();
+  }
+  if (t == 0) {
+    p.bsum[b] = sred[0];
+    __threadfence();
+    last = atomicAdd(p.ticket, 1u) == static_cast<unsigned>(G - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // ---- last block: total, crossing block, certified index ----
+  const double eps = 1.1102230246251565e-16;
+  const double gam = static_cast<double>(n) * eps / (1.0 - static_cast<double>(n) * eps);
+  __shared__ double s_ulo, s_uhi;
+  __shared__ int s_blk;
+  __shared__ DD s_base;
+  if (t == 0) {
+    DD tot{0.0, 0.0};
+    for (int q = 0; q < G; ++q) tot = dd_add(tot, p.bsum[q]);
+    const double T = dd_val(tot);
+    s_ulo = p.canon * T * (1.0 - (gam + 2.0 * eps) - 1e-15);
+    s_uhi = p.canon * T * (1.0 + (gam + 2.0 * eps) + 1e-15);
+    // first block whose end prefix certainly reaches u_hi
+    DD run{0.0, 0.0};
+    int blk = -1;
+    DD base{0.0, 0.0};
+    for (int q = 0; q < G; ++q) {
+      const DD nx = dd_add(run, p.bsum[q]);
+      if (dd_val(nx) * (1.0 - gam) >= s_uhi) {
+        blk = q;
+        base = run;
+        break;
+      }
+      run = nx;
+    }
+    s_blk = blk;
+    s_base = base;
+    s_best = -1;
+    *p.ticket = 0;  // reset for the next launch
+  }
+  __syncthreads();
+  if (s_blk < 0) {
+    if (t == 0) *p.fallback = 1;
+    return;
+  }
+  // inclusive prefixes of the crossing block's segment: per-thread contiguous chunks, then a scan of the
+  // chunk totals (one thread, G <= kCpThreads chunks)
+  const long c0 = n * s_blk / G, c1 = n * (s_blk + 1) / G;
+  const long len = c1 - c0;
+  const long per = (len + kCpThreads - 1) / kCpThreads;
+  const long my0 = c0 + t * per, my1 = min(c1, my0 + per);
+  DD part{0.0, 0.0};
+  for (long i = my0; i < my1; ++i) part = dd_add(part, p.d2[i]);
+  sred[t] = part;
+  __syncthreads();
+  if (t == 0) {
+    DD run = s_base;
+    for (int q = 0; q < kCpThreads; ++q) {
+      const DD nx = dd_add(run, sred[q]);
+      sred[q] = run;  // exclusive prefix of chunk q
+      run = nx;
+    }
+  }
+  __syncthreads();
+  DD run = sred[t];
+  long found = -1;
+  double prev_hi = dd_val(run) * (1.0 + gam);
+  for (long i = my0; i < my1; ++i) {
+    run = dd_add(run, p.d2[i]);
+    const double S = dd_val(run);
+    if (S * (1.0 - gam) >= s_uhi) {
+      found = i;
+      break;
+    }
+    prev_hi = S * (1.0 + gam);
+  }
+  (void)prev_hi;
+  if (found >= 0) atomicMin(reinterpret_cast<unsigned long long*>(&s_best), static_cast<unsigned long long>(found));
+  __syncthreads();
+  if (t == 0) {
+    const long i = s_best;
+    bool ok = i >= 0;
+    if (ok) {
+      // the prefix before i must certainly stay below u_lo
+      DD pre = s_base;
+      for (long q = c0; q < i; ++q) pre = dd_add(pre, p.d2[q]);
+      ok = dd_val(pre) * (1.0 + gam) < s_ulo;
+    }
+    if (!ok) {
+      *p.fallback = 1;
+    } else {
+      *p.pick_out = i;
+      for (int c = 0; c < a.d; ++c) a.C[p.j + static_cast<size_t>(c) * a.k] = a.P[i + c * n];
+    }
+  }
+}
+
+// exact sequential pick when the certificate failed (pick_kernel semantics), else nothing
+__global__ void fallback_gate_kernel(const int* fallback, int* run) { *run = *fallback; }
+
+// Lloyd assignment: best center with strict < (first minimum).  Centers staged in shared memory in
+// tiles (broadcast reads), two points per thread; the same D^2 expression as row_d2 (no FMA).
+constexpr int kAsTile = 1024;
+__global__ void __launch_bounds__(256) assign_kernel(KArgs a, int* assign, double* best) {
+  __shared__ double sc[3][kAsTile];
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x * 2;
+  for (long i0 = (blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x) * 2; i0 - threadIdx.x * 2 < a.n;
+       i0 += stride) {
+    double p0[3] = {0, 0, 0}, p1[3] = {0, 0, 0};
+    const bool v0 = i0 < a.n, v1 = i0 + 1 < a.n;
+    for (int c = 0; c < a.d; ++c) {
+      if (v0) p0[c] = a.P[i0 + c * a.n];
+      if (v1) p1[c] = a.P[i0 + 1 + c * a.n];
+    }
+    double b0 = __longlong_as_double(0x7ff0000000000000LL), b1 = b0;
+    int j0 = 0, j1 = 0;
+    for (int t0 = 0; t0 < a.k; t0 += kAsTile) {
+      const int tl = min(kAsTile, a.k - t0);
+      __syncthreads();
+      for (int e = threadIdx.x; e < tl; e += blockDim.x)
+        for (int c = 0; c < a.d; ++c) sc[c][e] = a.C[t0 + e + static_cast<size_t>(c) * a.k];
+      __syncthreads();
+      for (int e = 0; e < tl; ++e) {
+        double r0 = 0.0, r1 = 0.0;
+        for (int c = 0; c < a.d; ++c) {
+          const double q0 = __dsub_rn(p0[c], sc[c][e]), q1 = __dsub_rn(p1[c], sc[c][e]);
+          r0 = c == 0 ? __dmul_rn(q0, q0) : __dadd_rn(r0, __dmul_rn(q0, q0));
+          r1 = c == 0 ? __dmul_rn(q1, q1) : __dadd_rn(r1, __dmul_rn(q1, q1));
+        }
+        if (r0 < b0) {
+          b0 = r0;
+          j0 = t0 + e;
+        }
+        if (r1 < b1) {
+          b1 = r1;
+          j1 = t0 + e;
+        }
       }
     }
-    assign[i] = bj;
-    best[i] = b;
+    if (v0) {
+      assign[i0] = j0;
+      best[i0] = b0;
+    }
+    if (v1) {
+      assign[i0 + 1] = j1;
+      best[i0 + 1] = b1;
+    }
+  }
+}
+
+// new centers of the non-empty clusters (sums / counts), written out of place; empties counted
+__global__ void center_means_kernel(KArgs a, const double* sums, const int* counts, double* Cn, int* n_empty) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < a.k; j += gridDim.x * blockDim.x) {
+    if (counts[j] > 0) {
+      for (int c = 0; c < a.d; ++c)
+        Cn[j + static_cast<size_t>(c) * a.k] =
+            __ddiv_rn(sums[j + static_cast<size_t>(c) * a.k], static_cast<double>(counts[j]));
+    } else {
+      atomicAdd(n_empty, 1);
+    }
   }
 }
 
@@ -233,6 +447,36 @@ __global__ void __launch_bounds__(1024) cluster_sum_kernel(KArgs a, const int* a
     }
   }
 }
+// Per-cluster sums over the points sorted by cluster (stable radix sort: each cluster's members stay in
+// point order), one thread per cluster: the reference's sequential per-cluster accumulation
+// (inducing.cpp:80-91) in parallel across clusters.
+__global__ void cluster_bounds_kernel(long n, int k, const int* key, int* start, int* count) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n; i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int c = key[i];
+    if (i == 0 || key[i - 1] != c) start[c] = static_cast<int>(i);
+    if (i == n - 1 || key[i + 1] != c) count[c] = static_cast<int>(i + 1);  // end, turned into a count below
+  }
+}
+__global__ void cluster_sorted_sum_kernel(KArgs a, const int* order, const int* start, int* counts, double* sums) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < a.k; j += gridDim.x * blockDim.x) {
+    const int s0 = start[j], e = counts[j];
+    double s[3] = {0.0, 0.0, 0.0};
+    int cnt = 0;
+    if (s0 >= 0)
+      for (int q = s0; q < e; ++q) {
+        const long i = order[q];
+        for (int c = 0; c < a.d; ++c) s[c] = __dadd_rn(s[c], a.P[i + static_cast<long>(c) * a.n]);
+        ++cnt;
+      }
+    for (int c = 0; c < a.d; ++c) sums[j + static_cast<size_t>(c) * a.k] = s[c];
+    counts[j] = cnt;
+  }
+}
+__global__ void iota_kernel(long n, int* v) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n; i += static_cast<long>(gridDim.x) * blockDim.x)
+    v[i] = static_cast<int>(i);
+}
+
 __global__ void center_update_kernel(KArgs a, const int* assign, const double* sums, const int* counts) {
   __shared__ double bd[1024];
   __shared__ long bi[1024];
@@ -275,6 +519,82 @@ __global__ void center_update_kernel(KArgs a, const int* assign, const double* s
 }
 
 }  // namespace
+
+namespace {
+// double-double partial sums of best[] per block (certified inertia)
+__global__ void __launch_bounds__(256) inertia_dd_kernel(const double* best, long n, DD* part) {
+  __shared__ DD sred[256];
+  DD acc{0.0, 0.0};
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n; i += static_cast<long>(gridDim.x) * blockDim.x)
+    acc = dd_add(acc, best[i]);
+  sred[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sred[threadIdx.x] = dd_add(sred[threadIdx.x], sred[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sred[0];
+}
+// order-preserving uint64 key of a double, -0.0 folded onto +0.0 (operator< treats them as equal)
+__global__ void dkey_kernel(long n, const double* v, unsigned long long* key) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n; i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const double x = v[i] == 0.0 ? 0.0 : v[i];
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+    key[i] = (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+  }
+}
+__global__ void gather_key_kernel(long n, const unsigned long long* key, const int* perm, unsigned long long* out) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n; i += static_cast<long>(gridDim.x) * blockDim.x)
+    out[i] = key[perm[i]];
+}
+// rows i of the sorted order that start a new distinct row
+__global__ void distinct_kernel(long n, int d, const unsigned long long* keys, const int* perm, unsigned long long* cnt) {
+  unsigned long long local = 0;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n; i += static_cast<long>(gridDim.x) * blockDim.x) {
+    bool fresh = i == 0;
+    for (int c = 0; c < d && !fresh; ++c)
+      fresh = keys[static_cast<size_t>(c) * n + perm[i]] != keys[static_cast<size_t>(c) * n + perm[i - 1]];
+    local += fresh ? 1 : 0;
+  }
+  atomicAdd(cnt, local);
+}
+}  // namespace
+
+// count_distinct_rows (inducing.cpp:22-30) on the device: stable LSD sorts by the order-preserving keys of
+// the columns (last column first) give the lexicographic row order; count the row changes
+static int count_distinct_rows_device(stgp_ctx* ctx, const double* P_host, long n, int d) {
+  cudaStream_t st = ctx->stream;
+  DevBuf<double> P(static_cast<size_t>(n) * d);
+  P.upload(P_host, static_cast<size_t>(n) * d, st);
+  DevBuf<unsigned long long> keys(static_cast<size_t>(n) * d), kin(static_cast<size_t>(n)), kout(static_cast<size_t>(n)),
+      cnt(1);
+  DevBuf<int> pa(static_cast<size_t>(n)), pb(static_cast<size_t>(n));
+  const int gb = grid_for(n, 256, ctx->num_sms * 8);
+  for (int c = 0; c < d; ++c) {
+    dkey_kernel<<<gb, 256, 0, st>>>(n, P.get() + static_cast<size_t>(c) * n, keys.get() + static_cast<size_t>(c) * n);
+    launched(ctx);
+  }
+  iota_kernel<<<gb, 256, 0, st>>>(n, pa.get());
+  launched(ctx);
+  size_t tb = 0;
+  STGP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin.get(), kout.get(), pa.get(), pb.get(), static_cast<int>(n), 0, 64, st));
+  DevBuf<unsigned char> tmp(std::max<size_t>(tb, 1));
+  for (int c = d - 1; c >= 0; --c) {  // least significant column first; stable
+    gather_key_kernel<<<gb, 256, 0, st>>>(n, keys.get() + static_cast<size_t>(c) * n, pa.get(), kin.get());
+    launched(ctx);
+    size_t t2 = tmp.n;
+    STGP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), t2, kin.get(), kout.get(), pa.get(), pb.get(), static_cast<int>(n), 0, 64, st));
+    launched(ctx);
+    std::swap(pa, pb);
+  }
+  cnt.zero(st);
+  distinct_kernel<<<gb, 256, 0, st>>>(n, d, keys.get(), pa.get(), cnt.get());
+  launched(ctx);
+  unsigned long long h = 0;
+  cnt.download(&h, 1, st);
+  STGP_CUDA(cudaStreamSynchronize(st));
+  return static_cast<int>(h);
+}
 
 static int count_distinct_rows(const double* P, long n, int d) {
   std::vector<long> idx(static_cast<size_t>(n));
@@ -328,27 +648,158 @@ void kmeanspp_device(stgp_ctx* ctx, const double* P_host, long n, int d, int k, 
   launched(ctx);
   STGP_CUDA(cudaFuncSetAttribute(pick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(sizeof(double) * kPickChunk)));
+  static const bool certified = [] {
+    const char* e = std::getenv("STGP_KMEANS_CERTIFIED");  // 0: the one-thread exact pick for every center
+    return !(e && e[0] == '0');
+  }();
+  const int G = std::max(1, std::min<int>(kCpThreads, static_cast<int>((n + 4095) / 4096)));
+  DevBuf<DD> bsum(static_cast<size_t>(G));
+  DevBuf<unsigned> ticket(1);
+  DevBuf<int> fb(1);
+  ticket.zero(st);
+  long fallbacks = 0;
+  std::unique_ptr<ProfRegion> prk(new ProfRegion(ctx, "km_picks"));
   for (int j = 1; j < k; ++j) {
-    pick_kernel<<<1, kPickThreads, sizeof(double) * kPickChunk, st>>>(a, d2.get(), canon[static_cast<size_t>(j)], j,
-                                                                       pick.get());
+    if (certified) {
+      fb.zero(st);
+      PickArgs pa{a, d2.get(), j, canon[static_cast<size_t>(j)], pick.get(), bsum.get(), ticket.get(), fb.get()};
+      pick_certified_kernel<<<G, kCpThreads, 0, st>>>(pa);
+      launched(ctx);
+      if (j >= 2) {  // the fallback needs d2 updated with center j - 1: the certified kernel did it
+      }
+      pick_kernel<<<1, kPickThreads, sizeof(double) * kPickChunk, st>>>(a, d2.get(), canon[static_cast<size_t>(j)], j,
+                                                                         pick.get(), fb.get());
+      launched(ctx);
+    } else {
+      if (j >= 2) {
+        d2_update_kernel<<<gb, 256, 0, st>>>(a, j - 1, false, d2.get());
+        launched(ctx);
+      }
+      pick_kernel<<<1, kPickThreads, sizeof(double) * kPickChunk, st>>>(a, d2.get(), canon[static_cast<size_t>(j)], j,
+                                                                         pick.get());
+      launched(ctx);
+    }
+  }
+  (void)fallbacks;
+  prk.reset();
+  DevBuf<double> Cn(static_cast<size_t>(k) * d);
+  DevBuf<int> nempty(1);
+  // certified inertia (large n): double-double partials; best[] double-buffered for the exact fallback
+  const bool cert_inertia = certified && n >= 65536;
+  constexpr int kInBlocks = 128;
+  DevBuf<DD> inpart(kInBlocks);
+  DevBuf<double> best_prev(cert_inertia ? static_cast<size_t>(n) : 1);
+  double prev_lo = 0.0, prev_hi = std::numeric_limits<double>::infinity();
+  // Lloyd cluster sums: sorted by cluster for large n (one thread per cluster), else the one-block kernel
+  const bool sorted_sums = n >= 65536;
+  DevBuf<int> iota, order, keys_s, cstart;
+  DevBuf<unsigned char> sort_tmp;
+  int key_bits = 1;
+  while ((1 << key_bits) < k) ++key_bits;
+  if (sorted_sums) {
+    iota.alloc(static_cast<size_t>(n));
+    order.alloc(static_cast<size_t>(n));
+    keys_s.alloc(static_cast<size_t>(n));
+    cstart.alloc(static_cast<size_t>(k));
+    iota_kernel<<<gb, 256, 0, st>>>(n, iota.get());
     launched(ctx);
-    d2_update_kernel<<<gb, 256, 0, st>>>(a, j, false, d2.get());
-    launched(ctx);
+    size_t tb = 0;
+    STGP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, assign.get(), keys_s.get(), iota.get(), order.get(),
+                                              static_cast<int>(n), 0, key_bits, st));
+    sort_tmp.alloc(std::max<size_t>(tb, 1));
   }
   double prev = std::numeric_limits<double>::infinity();
+  int sweeps = 0;
   for (int sweep = 0; sweep < 50; ++sweep) {
+    ++sweeps;
+    ProfRegion prl(ctx, "km_lloyd_sweep");
     assign_kernel<<<gb, 256, 0, st>>>(a, assign.get(), best.get());
     launched(ctx);
-    inertia_kernel<<<1, 1024, 0, st>>>(best.get(), n, inertia.get());
-    launched(ctx);
-    cluster_sum_kernel<<<1, std::min(1024, std::max(32, (k + 31) / 32 * 32)), 0, st>>>(a, assign.get(), sums.get(),
-                                                                                       counts.get());
-    launched(ctx);
-    center_update_kernel<<<1, 1024, 0, st>>>(a, assign.get(), sums.get(), counts.get());
+    if (cert_inertia) {
+      inertia_dd_kernel<<<kInBlocks, 256, 0, st>>>(best.get(), n, inpart.get());
+      launched(ctx);
+    } else {
+      inertia_kernel<<<1, 1024, 0, st>>>(best.get(), n, inertia.get());
+      launched(ctx);
+    }
+    if (sorted_sums) {
+      size_t tb = sort_tmp.n;
+      STGP_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp.get(), tb, assign.get(), keys_s.get(), iota.get(), order.get(),
+                                                static_cast<int>(n), 0, key_bits, st));
+      launched(ctx);
+      STGP_CUDA(cudaMemsetAsync(cstart.get(), 0xff, sizeof(int) * k, st));
+      STGP_CUDA(cudaMemsetAsync(counts.get(), 0, sizeof(int) * k, st));
+      cluster_bounds_kernel<<<gb, 256, 0, st>>>(n, k, keys_s.get(), cstart.get(), counts.get());
+      launched(ctx);
+      cluster_sorted_sum_kernel<<<grid_for(k, 128), 128, 0, st>>>(a, order.get(), cstart.get(), counts.get(), sums.get());
+      launched(ctx);
+    } else {
+      cluster_sum_kernel<<<1, std::min(1024, std::max(32, (k + 31) / 32 * 32)), 0, st>>>(a, assign.get(), sums.get(),
+                                                                                         counts.get());
+      launched(ctx);
+    }
+    // center update (inducing.cpp:93-111): all means in parallel; the re-seeding of empty clusters reads
+    // the partly updated centers in cluster order, so any empty cluster takes the sequential kernel
+    STGP_CUDA(cudaMemsetAsync(nempty.get(), 0, sizeof(int), st));
+    center_means_kernel<<<grid_for(k, 128), 128, 0, st>>>(a, sums.get(), counts.get(), Cn.get(), nempty.get());
     launched(ctx);
     double in = 0.0;
-    inertia.download(&in, 1, st);
+    int ne = 0;
+    DD hp[kInBlocks];
+    if (cert_inertia) inpart.download(hp, kInBlocks, st);
+    else inertia.download(&in, 1, st);
+    nempty.download(&ne, 1, st);
     STGP_CUDA(cudaStreamSynchronize(st));
+    if (ne == 0) {
+      STGP_CUDA(cudaMemcpyAsync(C.get(), Cn.get(), sizeof(double) * k * d, cudaMemcpyDeviceToDevice, st));
+    } else {
+      center_update_kernel<<<1, 1024, 0, st>>>(a, assign.get(), sums.get(), counts.get());
+      launched(ctx);
+    }
+    if (cert_inertia) {
+      // inducing.cpp:113: stop when in == 0 or |prev - in| < 1e-6 in, in = the sequential sum of best[].
+      // The exact value lies within gamma_n of the double-double sum; decide from the bounds, and run the
+      // sequential chains (this sweep's and, kept in the other buffer, the previous sweep's) only when
+      // the bounds straddle the threshold.
+      double hi = 0.0, lo = 0.0;
+      for (int q = 0; q < kInBlocks; ++q) {  // fixed block order
+        const double t2 = hi + hp[q].hi;
+        const double bp = t2 - hi;
+        lo += (hi - (t2 - bp)) + (hp[q].hi - bp) + hp[q].lo;
+        hi = t2;
+      }
+      const double T = hi + lo;
+      const double gam = static_cast<double>(n) * 1.1102230246251565e-16 / (1.0 - static_cast<double>(n) * 1.1102230246251565e-16) + 1e-15;
+      const double in_lo = T * (1.0 - gam), in_hi = T * (1.0 + gam);
+      bool stop, certain = true;
+      if (in_hi == 0.0) {
+        stop = true;
+      } else if (!std::isfinite(prev_hi)) {
+        stop = false;
+      } else {
+        const double dmax = std::max(std::abs(prev_hi - in_lo), std::abs(in_hi - prev_lo));
+        const double dmin = (prev_lo > in_hi) ? prev_lo - in_hi : (in_lo > prev_hi ? in_lo - prev_hi : 0.0);
+        if (dmax < 1e-6 * in_lo) stop = true;
+        else if (dmin >= 1e-6 * in_hi && in_lo > 0.0) stop = false;
+        else certain = false, stop = false;
+      }
+      if (!certain) {  // exact sequential sums of this and the previous sweep
+        double pe = 0.0;
+        inertia_kernel<<<1, 1024, 0, st>>>(best.get(), n, inertia.get());
+        launched(ctx);
+        inertia.download(&in, 1, st);
+        inertia_kernel<<<1, 1024, 0, st>>>(best_prev.get(), n, inertia.get());
+        launched(ctx);
+        inertia.download(&pe, 1, st);
+        STGP_CUDA(cudaStreamSynchronize(st));
+        stop = in == 0.0 || std::abs(pe - in) < 1e-6 * std::max(in, 1e-300);
+      }
+      if (stop) break;
+      prev_lo = in_lo;
+      prev_hi = in_hi;
+      std::swap(best, best_prev);
+      continue;
+    }
     if (in == 0.0 || std::abs(prev - in) < 1e-6 * std::max(in, 1e-300)) break;
     prev = in;
   }
@@ -470,7 +921,7 @@ int stgp_joint_kmeanspp_inducing(stgp_dataset* ds, int m, double ss, double ts, 
       S[static_cast<size_t>(i) + n] = ds->hy[static_cast<size_t>(i)] / ss;
       S[static_cast<size_t>(i) + 2 * static_cast<size_t>(n)] = ds->ht[static_cast<size_t>(i)] / ts;
     }
-    const int distinct = count_distinct_rows(S.data(), n, 3);
+    const int distinct = count_distinct_rows_device(ds->ctx, S.data(), n, 3);
     const int k = std::min(m, distinct);
     std::vector<double> C(static_cast<size_t>(k) * 3);
     kmeanspp_device(ds->ctx, S.data(), n, 3, k, seed, C.data(), distinct);

@@ -68,6 +68,17 @@ def test_joint_kmeanspp_bits(S):
         S.joint_kmeanspp_inducing(ds, 25, 0.0, 2.0, 5)
 
 
+def test_joint_kmeanspp_large_certified(S):
+    """Certified parallel picks and cluster-sorted Lloyd sums (csrc/kmeans.cu) at n = 2e5, k = 300: bit-equal
+    to the oracle's sequential kmeanspp (inducing.cpp:32-115)."""
+    rng = np.random.default_rng(3)
+    n = 200000
+    x, y, t = rng.random(n), rng.random(n), np.repeat(np.arange(100.0), n // 100)
+    ds = S.SpaceTimeDataset(x, y, t)
+    ind = S.joint_kmeanspp_inducing(ds, 300, 0.2, 5.0, 7)
+    assert _bits(ind.points, O.joint_kmeanspp(x, y, t, 300, 0.2, 5.0, 7))
+
+
 def _check_dr(S, x, y, t, th, Z, m):
     ds = S.SpaceTimeDataset(x, y, t)
     nb = S.residual_neighbors(ds, th, S.InducingSet.from_points(Z), m)
