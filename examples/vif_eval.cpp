@@ -44,6 +44,16 @@ int main(int argc, char** argv) {
     const double v = nll(s, oresp);
     const std::vector<double> gr = nll_grad(s, oresp);
     std::printf("n=%d M=%d nll=%.10f grad[0]=%.6e\n", ds.n(), ind.size(), v, gr[0]);
+    // the precipitation path: ZC-PTN amounts (censored at 0) through the Laplace algebra of a FITC structure
+    std::vector<double> amounts(oresp.size());
+    for (size_t i = 0; i < oresp.size(); ++i) amounts[i] = oresp[i] > 0.3 ? oresp[i] : 0.0;
+    const CovarianceParams latent{0.0, 1.0, 0.5, 20.0, 0.4, 1.5, 0.4, 0.2};
+    Structure f = build_fitc(ds, latent, ind);
+    const LikelihoodParams lik{0.8, 1.5};
+    auto lm = laplace_marginal(f, amounts, {}, 0, {}, lik);
+    const std::vector<double> target{ox[0], oy[0], ot.back() + 1.0};
+    const ZcptnPrediction zp = zcptn_predict(lm.second, f, target, {}, 0, {}, lik, 0, 16, 3);
+    std::printf("laplace nll=%.10f iterations=%d p_rain=%.6f\n", lm.first, lm.second.iterations, zp.p_rain[0]);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "error: %s\n", e.what());
     return 1;

@@ -7,8 +7,9 @@
 //    column-major std::vector<double> with explicit row/column counts;
 //  * structures are move-only handles to device-resident state; the fields the
 //    reference tests read (B, D, fitc_diag) are downloaded on demand;
-//  * the latent-policy likelihood (Laplace algebra) is out of scope and raises
-//    ConfigError, as documented in DESIGN.md.
+//  * the Laplace algebra (latent policy, ZC-PTN) factors Q + W densely on the device, so
+//    Vecchia / VIF latent-policy structures are limited to n <= 40000 (the reference's
+//    SimplicialLDLT is likewise a desk-scale method).
 #ifndef STGP_B200_HPP
 #define STGP_B200_HPP
 
@@ -269,6 +270,54 @@ inline PredictiveDistribution predict(Structure& s, const std::vector<double>& y
   PredictiveDistribution out{std::vector<double>(static_cast<size_t>(np)), std::vector<double>(static_cast<size_t>(np))};
   check(stgp_predict(s.get(), y.data(), p ? X.data() : nullptr, p, p ? beta.data() : nullptr, np, targets_xyt.data(),
                      p ? X_p.data() : nullptr, pred_m_v, out.mu.data(), out.var.data()));
+  return out;
+}
+
+// LikelihoodParams / LaplaceState / ZcptnPrediction (covariance.hpp:41-48, laplace.hpp:37-62)
+struct LikelihoodParams {
+  double sigma = 1.0, lambda = 1.0;
+};
+struct LaplaceState {
+  std::vector<double> mode, grad_at_mode, w;
+  double log_marginal = 0.0;
+  bool converged = false;
+  int iterations = 0;
+};
+// laplace_marginal (laplace.hpp:47-53): {-log marginal, state}; latent-policy Vecchia / VIF or FITC
+inline std::pair<double, LaplaceState> laplace_marginal(Structure& s, const std::vector<double>& y,
+                                                        const std::vector<double>& X, int p,
+                                                        const std::vector<double>& beta, const LikelihoodParams& lik,
+                                                        const std::vector<double>* warm_start = nullptr) {
+  const size_t n = y.size();
+  LaplaceState st;
+  st.mode.resize(n);
+  st.grad_at_mode.resize(n);
+  st.w.resize(n);
+  double v = 0.0;
+  check(stgp_laplace_marginal(s.get(), y.data(), p ? X.data() : nullptr, p, p ? beta.data() : nullptr, lik.sigma,
+                              lik.lambda, warm_start && warm_start->size() == n ? warm_start->data() : nullptr, &v,
+                              st.mode.data(), st.grad_at_mode.data(), st.w.data(), &st.iterations));
+  st.log_marginal = -v;
+  st.converged = true;  // a non-converged Newton raises NumericError (laplace.cpp:188-190)
+  return {v, std::move(st)};
+}
+struct ZcptnPrediction {
+  std::vector<double> mu_latent, var_latent, p_rain, amount_mean, amount_median;
+  std::vector<double> samples;  // n_p x n_samples, column-major
+};
+// zcptn_predict (laplace.hpp:67-72)
+inline ZcptnPrediction zcptn_predict(const LaplaceState& state, Structure& s, const std::vector<double>& targets_xyt,
+                                     const std::vector<double>& X_p, int p, const std::vector<double>& beta,
+                                     const LikelihoodParams& lik, int pred_m_v, int n_samples, std::uint64_t seed) {
+  const int np = static_cast<int>(targets_xyt.size() / 3);
+  ZcptnPrediction out;
+  for (auto* v : {&out.mu_latent, &out.var_latent, &out.p_rain, &out.amount_mean, &out.amount_median})
+    v->resize(static_cast<size_t>(np));
+  out.samples.resize(static_cast<size_t>(np) * std::max(n_samples, 0));
+  check(stgp_zcptn_predict(s.get(), state.grad_at_mode.data(), state.w.data(), np, targets_xyt.data(),
+                           p ? X_p.data() : nullptr, p, p ? beta.data() : nullptr, lik.sigma, lik.lambda, pred_m_v,
+                           n_samples, seed, out.mu_latent.data(), out.var_latent.data(), out.p_rain.data(),
+                           out.amount_mean.data(), out.amount_median.data(), out.samples.data()));
   return out;
 }
 

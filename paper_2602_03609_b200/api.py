@@ -112,7 +112,7 @@ class Context:
         return out.value
 
     def gemm_rows(self, A, B, emulated: bool = True):
-        """C = A B^T (FP64) through the int8 Ozaki path or cuBLAS DGEMM; returns (C, device ms)."""
+        """C = A B^T (FP64) through the int8 Ozaki path (tcgen05) or the DMMA GEMM; returns (C, device ms)."""
         A = np.ascontiguousarray(A, dtype=np.float64)
         B = np.ascontiguousarray(B, dtype=np.float64)
         n, k = A.shape
@@ -124,7 +124,7 @@ class Context:
 
     def gemm_cols(self, A, B=None, emulated: bool = True):
         """C = A^T B (A, B: n x m, i.e. m x n column-major), C[j][i] = sum_r A[r, j] B[r, i]; the
-        int8 Ozaki path for the long reduction or cuBLAS DGEMM.  B None: A^T A."""
+        int8 Ozaki path for the long reduction or the DMMA GEMM.  B None: A^T A."""
         A = np.ascontiguousarray(A, dtype=np.float64)
         n, m = A.shape
         Bc = A if B is None else np.ascontiguousarray(B, dtype=np.float64)

@@ -50,7 +50,7 @@ struct DevLagTable {
   std::vector<TF> host_tf;
 };
 
-struct OzakiState;  // ozaki.cu: int8 slice buffers and cuBLASLt plans
+struct OzakiState;  // ozaki.cu: int8 slice buffers and the tcgen05 kernel work lists
 }  // namespace stgp
 
 struct stgp_ctx {

@@ -1,20 +1,19 @@
 // FP64 GEMM on the INT8 tensor cores (Ozaki scheme I, error-free slicing).
 //
-// B200's FP64 pipes (DMMA and DFMA) peak at ~37 TFLOP/s, while its int8 tensor cores run
-// cuBLASLt IMMA at ~2.4 POPS (scripts/exp/imma_probe.py).  An FP64 product
+// B200's FP64 pipes (DMMA and DFMA) peak at ~37 TFLOP/s, while its int8 tensor cores (tcgen05.mma
+// kind::i8) run at several POPS.  An FP64 product
 //   C[r][j] = sum_c A[r][c] B[j][c]            (rows of A and B contiguous over c)
 // is computed exactly up to the slicing truncation:
 //   * row r of A is scaled by 2^-eA[r] into (-1, 1) and cut into S int8 slices of 7 bits each,
 //     a = sum_s A_s 2^-7s (every step exact in FP64); B likewise per row j;
-//   * the products A_s B_t with s + t = d share the scale 2^-7d and are one int8 GEMM over the
-//     concatenated K = (d - 1) k (A slices stored consecutively, B slices in reverse order, so
-//     each diagonal is a prefix of A's row times a suffix of B's row); its int32 result is exact
+//   * the products A_s B_t with s + t = d share the scale 2^-7d; the hand-written tcgen05 kernel
+//     (ozaki_tc.cu) accumulates every diagonal d in its own TMEM block, exactly in int32
 //     (|C_d| <= S k 127^2 < 2^31 for k < 2^31 / (S 127^2));
-//   * C = 2^(eA + eB) sum_{d = 2}^{S + 1} 2^-7d C_d, summed in FP64 from the smallest term.
+//   * C = 2^(eA + eB) sum_{d = 2}^{S + 1} 2^-7d C_d, summed in FP64 from the smallest term in the
+//     kernel's epilogue (the int32 partials never reach HBM).
 // Terms with s + t > S + 1 are dropped: the result carries ~7 S bits relative to
 // max_c |A[r][c]| max_c |B[j][c]| k (S = 7: 49 bits; far below the 1e-8 parity tolerance of the
-// evaluation, tests/test_gpu_ozaki.py measures it against cuBLAS DGEMM).
-#include <cublasLt.h>
+// evaluation, tests/test_gpu_ozaki.py measures it against exact dot products and the DMMA GEMM).
 
 #include <fstream>
 #include <string>
@@ -31,11 +30,6 @@
 namespace stgp {
 
 namespace {
-
-void lt_check(cublasStatus_t s, const char* what) {
-  if (s != CUBLAS_STATUS_SUCCESS)
-    throw Error(kInternal, std::string("cuBLASLt error in ") + what + ": " + std::to_string(static_cast<int>(s)));
-}
 
 // The S base-128 digits of trunc(v 2^(7 S)) for |v| < 1 (v already scaled, exact): all digits carry
 // the sign of v and lie in [-127, 127]; digit 1 is the most significant.  Same digits as the FP64
@@ -194,38 +188,6 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(int m, long long n, int
     default: throw Error(kConfig, "ozaki: STGP_OZAKI_S must lie in [2, 8]");   \
   }
 
-// C[r * ldc + j] = sA[r] sB[j] sum_{d = S+1 .. 2} 2^-7d Cd[d][r * mp + j]   (one row per iteration,
-// 4 consecutive j per thread: m, mp and ldc are multiples of 4, rows 16-byte aligned)
-__global__ void __launch_bounds__(256) combine_rows_kernel(long long nrows, int m, int mp, const int32_t* __restrict__ Cd,
-                                                           long long dstride, int S, const double* __restrict__ sA,
-                                                           const double* __restrict__ sB, double* __restrict__ C,
-                                                           int ldc) {
-  for (long long r = blockIdx.x; r < nrows; r += gridDim.x) {
-    const double fa = sA[r];
-    const int32_t* src = Cd + r * mp;
-    for (int j = threadIdx.x * 4; j < m; j += blockDim.x * 4) {
-      int4 v[12];
-#pragma unroll
-      for (int d = 0; d < 12; ++d)
-        if (d < S) v[d] = __ldg(reinterpret_cast<const int4*>(src + d * dstride + j));
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, w = ldexp(1.0, -7 * (S + 1));  // smallest diagonal first
-#pragma unroll
-      for (int d = 11; d >= 0; --d)
-        if (d < S) {  // exact products (power-of-two weights), one rounding per add
-          a0 = fma(static_cast<double>(v[d].x), w, a0);
-          a1 = fma(static_cast<double>(v[d].y), w, a1);
-          a2 = fma(static_cast<double>(v[d].z), w, a2);
-          a3 = fma(static_cast<double>(v[d].w), w, a3);
-          w *= 128.0;
-        }
-      double* o = C + r * ldc + j;
-      const double4 fb = *reinterpret_cast<const double4*>(sB + j);
-      *reinterpret_cast<double2*>(o) = make_double2(a0 * fa * fb.x, a1 * fa * fb.y);
-      *reinterpret_cast<double2*>(o + 2) = make_double2(a2 * fa * fb.z, a3 * fa * fb.w);
-    }
-  }
-}
-
 __global__ void sqrt_vec_kernel(long long n, const double* __restrict__ d, double* __restrict__ f) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
@@ -238,80 +200,11 @@ __global__ void rsqrt_vec_kernel(long long n, const double* __restrict__ d, doub
     f[i] = 1.0 / sqrt(d[i]);  // the factor of lowrank.cu scale_cols_kernel
 }
 
-// C[j * ldc + i] = sum_c sA[c m + j] sB[c m + i] sum_d 2^-7d Cd[d][c][j * mp + i]   (chunks in order)
-__global__ void __launch_bounds__(256) combine_cols_kernel(int m, int mp, int nch, const int32_t* __restrict__ Cd,
-                                                           long long dstride, long long cstride, int S,
-                                                           const double* __restrict__ sA,
-                                                           const double* __restrict__ sB, double* __restrict__ C,
-                                                           int ldc) {
-  const long long total = static_cast<long long>(m) * m;
-  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int j = static_cast<int>(e / m), i = static_cast<int>(e - static_cast<long long>(j) * m);
-    double out = 0.0;
-    for (int c = 0; c < nch; ++c) {
-      const int32_t* src = Cd + c * cstride + static_cast<long long>(j) * mp + i;
-      double acc = 0.0, w = ldexp(1.0, -7 * (S + 1));
-      for (int d = S - 1; d >= 0; --d) {
-        acc = fma(static_cast<double>(src[d * dstride]), w, acc);
-        w *= 128.0;
-      }
-      out = fma(acc, sA[static_cast<size_t>(c) * m + j] * sB[static_cast<size_t>(c) * m + i], out);
-    }
-    C[static_cast<long long>(j) * ldc + i] = out;
-  }
-}
-
-constexpr int kAlgoCands = 4;
-struct LtPlan {
-  cublasLtMatmulDesc_t op = nullptr;
-  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
-  cublasLtMatmulAlgo_t algo{};
-  cublasLtMatmulAlgo_t cand[kAlgoCands];
-  int ncand = 0;
-  bool tuned = false;  // heuristic candidates timed once on the first call (results are identical: exact int32)
-  std::string key;     // plan shape, for the tuning cache
-  ~LtPlan() {
-    if (la) cublasLtMatrixLayoutDestroy(la);
-    if (lb) cublasLtMatrixLayoutDestroy(lb);
-    if (lc) cublasLtMatrixLayoutDestroy(lc);
-    if (op) cublasLtMatmulDescDestroy(op);
-  }
-};
-
 }  // namespace
 
-// Tuning cache (STGP_OZAKI_TUNE_SAVE / STGP_OZAKI_TUNE_LOAD = path): the candidate chosen per plan
-// shape by a normal run is replayed by a run under a profiler, whose event timings are not the
-// kernels' (ncu serialises and instruments every launch).
-struct TuneCache {
-  std::map<std::string, int> pick;
-  bool loaded = false;
-  void load() {
-    if (loaded) return;
-    loaded = true;
-    const char* path = std::getenv("STGP_OZAKI_TUNE_LOAD");
-    if (!path) return;
-    std::ifstream is(path);
-    std::string k;
-    int v;
-    while (is >> k >> v) pick[k] = v;
-  }
-  void save(const std::string& k, int v) {
-    const char* path = std::getenv("STGP_OZAKI_TUNE_SAVE");
-    if (!path) return;
-    std::ofstream os(path, std::ios::app);
-    os << k << " " << v << "\n";
-  }
-};
-
 struct OzakiState {
-  OzakiTcState* tc = nullptr;  // the hand-written tcgen05 kernel's work lists
-  TuneCache tune;
-  cublasLtHandle_t lt = nullptr;
-  DevBuf<unsigned char> ws;
+  OzakiTcState* tc = nullptr;  // the tcgen05 kernel's work lists
   DevBuf<int8_t> As, Bs;
-  DevBuf<int32_t> Cd;
   DevBuf<double> sA, sB, colf, colf2;
   DevBuf<int8_t> keep;  // forward digits of the last ozaki_syrk_keep operand (V' D^{-1/2})
   DevBuf<double> keep_s;
@@ -319,12 +212,7 @@ struct OzakiState {
   int keep_m = 0;
   long long keep_n = 0;
   DevBuf<unsigned long long> maxbits;
-  std::map<std::tuple<int, int, long long, int, int, int>, std::unique_ptr<LtPlan>> plans;
-  ~OzakiState() {
-    ozaki_tc_release(tc);
-    plans.clear();
-    if (lt) cublasLtDestroy(lt);
-  }
+  ~OzakiState() { ozaki_tc_release(tc); }
 };
 
 void ozaki_release(stgp_ctx* ctx) {
@@ -350,19 +238,9 @@ int ozaki_slices() {
   return s;
 }
 
-// The int8 products run on the hand-written tcgen05 kernel (ozaki_tc.cu); STGP_OZAKI_TC=0 switches
-// back to cuBLASLt IMMA per diagonal plus the combine kernels (A/B comparison only).
-bool ozaki_tc_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("STGP_OZAKI_TC");
-    return !(e && std::atoi(e) == 0);
-  }();
-  return on;
-}
-
 bool ozaki_enabled() {
   static const bool on = [] {
-    const char* e = std::getenv("STGP_OZAKI");  // A/B switch: 0 = cuBLAS DGEMM
+    const char* e = std::getenv("STGP_OZAKI");  // A/B switch: 0 = the DMMA GEMM
     return !(e && std::atoi(e) == 0);
   }();
   return on;
@@ -379,105 +257,8 @@ bool ozaki_for(int m) {
 }
 
 static OzakiState* state(stgp_ctx* ctx) {
-  if (!ctx->ozaki) {
-    ctx->ozaki = new OzakiState();
-    if (!ozaki_tc_enabled()) {
-      lt_check(cublasLtCreate(&ctx->ozaki->lt), "create");
-      ctx->ozaki->ws.alloc(64ull << 20);
-    }
-  }
+  if (!ctx->ozaki) ctx->ozaki = new OzakiState();
   return ctx->ozaki;
-}
-
-// Plan for Cd (m x ncols, int32, ld mp) = op(Bseg)^T (m x K) * Aseg (K x ncols), both K-contiguous
-// with leading dimension ldk (TN int8 IMMA); `batch` products strided by bstride (operands) and
-// cstride (results).
-static LtPlan* plan_for(OzakiState* oz, int m, int mp, int K, long long ncols, int ldk, int batch = 1,
-                        long long bstride = 0, long long cstride = 0) {
-  auto key = std::make_tuple(m, K, ncols, ldk, mp, batch);
-  auto it = oz->plans.find(key);
-  if (it != oz->plans.end()) return it->second.get();
-  auto p = std::make_unique<LtPlan>();
-  p->key = std::to_string(m) + "x" + std::to_string(K) + "x" + std::to_string(ncols) + "/" + std::to_string(ldk) + "/" +
-           std::to_string(mp) + "/" + std::to_string(batch);
-  lt_check(cublasLtMatmulDescCreate(&p->op, CUBLAS_COMPUTE_32I, CUDA_R_32I), "desc");
-  const cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
-  lt_check(cublasLtMatmulDescSetAttribute(p->op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof(ta)), "transa");
-  lt_check(cublasLtMatmulDescSetAttribute(p->op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof(tb)), "transb");
-  lt_check(cublasLtMatrixLayoutCreate(&p->la, CUDA_R_8I, K, m, ldk), "layout a");
-  lt_check(cublasLtMatrixLayoutCreate(&p->lb, CUDA_R_8I, K, ncols, ldk), "layout b");
-  lt_check(cublasLtMatrixLayoutCreate(&p->lc, CUDA_R_32I, m, ncols, mp), "layout c");
-  if (batch > 1) {
-    for (auto* l : {p->la, p->lb}) {
-      lt_check(cublasLtMatrixLayoutSetAttribute(l, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &batch, sizeof(batch)), "batch");
-      lt_check(cublasLtMatrixLayoutSetAttribute(l, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &bstride,
-                                                sizeof(bstride)), "bstride");
-    }
-    lt_check(cublasLtMatrixLayoutSetAttribute(p->lc, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &batch, sizeof(batch)), "batch");
-    lt_check(cublasLtMatrixLayoutSetAttribute(p->lc, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &cstride,
-                                              sizeof(cstride)), "cstride");
-  }
-  cublasLtMatmulPreference_t pref;
-  lt_check(cublasLtMatmulPreferenceCreate(&pref), "pref");
-  const size_t wsz = oz->ws.n;
-  lt_check(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsz, sizeof(wsz)),
-           "pref ws");
-  cublasLtMatmulHeuristicResult_t res[kAlgoCands];
-  int found = 0;
-  lt_check(cublasLtMatmulAlgoGetHeuristic(oz->lt, p->op, p->la, p->lb, p->lc, p->lc, pref, kAlgoCands, res, &found),
-           "heuristic");
-  cublasLtMatmulPreferenceDestroy(pref);
-  if (found < 1) throw Error(kInternal, "cuBLASLt: no int8 IMMA algorithm for the Ozaki slices");
-  p->ncand = found;
-  for (int i = 0; i < found; ++i) p->cand[i] = res[i].algo;
-  p->algo = res[0].algo;
-  LtPlan* raw = p.get();
-  oz->plans[key] = std::move(p);
-  return raw;
-}
-
-static void lt_matmul(stgp_ctx* ctx, OzakiState* oz, LtPlan* p, const int8_t* a, const int8_t* b, int32_t* c) {
-  const int32_t one = 1, zero = 0;
-  ProfRegion pr(ctx, "oz_imma");  // int8 tensor-core time (bench.py roofline_int8)
-  if (!p->tuned) {
-    p->tuned = true;
-    oz->tune.load();
-    const auto hit = oz->tune.pick.find(p->key);
-    if (hit != oz->tune.pick.end() && hit->second >= 0 && hit->second < p->ncand) {
-      p->algo = p->cand[hit->second];
-    } else if (p->ncand > 1) {
-      int best_i = 0;
-      cudaEvent_t e0, e1;
-      STGP_CUDA(cudaEventCreate(&e0));
-      STGP_CUDA(cudaEventCreate(&e1));
-      float best = 1e30f;
-      for (int i = 0; i < p->ncand; ++i) {
-        if (cublasLtMatmul(oz->lt, p->op, &one, a, p->la, b, p->lb, &zero, c, p->lc, c, p->lc, &p->cand[i], oz->ws.get(),
-                           oz->ws.n, ctx->stream) != CUBLAS_STATUS_SUCCESS)
-          continue;  // untimed first run of each candidate
-        STGP_CUDA(cudaEventRecord(e0, ctx->stream));
-        if (cublasLtMatmul(oz->lt, p->op, &one, a, p->la, b, p->lb, &zero, c, p->lc, c, p->lc, &p->cand[i], oz->ws.get(),
-                           oz->ws.n, ctx->stream) != CUBLAS_STATUS_SUCCESS)
-          continue;
-        STGP_CUDA(cudaEventRecord(e1, ctx->stream));
-        STGP_CUDA(cudaEventSynchronize(e1));
-        float ms = 0.f;
-        STGP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-        if (ms < best) {
-          best = ms;
-          best_i = i;
-          p->algo = p->cand[i];
-        }
-      }
-      cudaEventDestroy(e0);
-      cudaEventDestroy(e1);
-      oz->tune.save(p->key, best_i);
-    }
-  }
-  lt_check(cublasLtMatmul(oz->lt, p->op, &one, a, p->la, b, p->lb, &zero, c, p->lc, c, p->lc, &p->algo, oz->ws.get(),
-                          oz->ws.n, ctx->stream),
-           "matmul");
-  launched(ctx);
 }
 
 void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, int lda, const double* B, int ldb,
@@ -485,46 +266,29 @@ void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, 
   if (n <= 0 || m <= 0) return;
   if (m % 4 || ldc % 4) config_error("ozaki_gemm_rows: m and ldc must be multiples of 4");
   const int S = slices_for("STGP_OZAKI_S_ROWS", 6);
-  const bool tc = ozaki_tc_enabled();
-  // slice stride: every diagonal segment 16-byte aligned (cuBLASLt), whole 32-byte K steps (tcgen05)
-  const int kp = tc ? (k + 31) / 32 * 32 : (k + 15) / 16 * 16;
+  const int kp = (k + 31) / 32 * 32;  // slice stride: whole 32-byte K steps of the tcgen05 kernel
   if (static_cast<long long>(S) * kp * 127 * 127 >= (1LL << 31)) config_error("ozaki: k too large for exact int32");
   OzakiState* oz = state(ctx);
   cudaStream_t st = ctx->stream;
   const int ldk = S * kp;
-  const int mp = (m + 3) / 4 * 4;  // int32 result rows (16-byte aligned columns)
   // B slices (m rows, reversed slice order) and scales
   oz->Bs.ensure(static_cast<size_t>(m) * ldk);
   oz->sB.ensure(m);
   STGP_OZ_SWITCH(S, (slice_rows_kernel<kS><<<grid_for(static_cast<long long>(m) * 32, 256), 256, 0, st>>>(
                          m, k, kp, B, ldb, true, oz->Bs.get(), ldk, oz->sB.get())));
   launched(ctx);
-  // tcgen05: no int32 partials, so chunks only bound the digit buffer (~1.5 GB)
-  const long long chunk = tc ? std::min<long long>(n, std::max<long long>(16384, (3LL << 29) / ldk))
-                             : std::min<long long>(n, std::max<long long>(16384, (1LL << 28) / mp));  // Cd ~ S GB
+  // no int32 partials leave the SM, so chunks only bound the digit buffer (~1.5 GB)
+  const long long chunk = std::min<long long>(n, std::max<long long>(16384, (3LL << 29) / ldk));
   oz->As.ensure(static_cast<size_t>(chunk) * ldk);
   oz->sA.ensure(static_cast<size_t>(chunk));
-  const long long dstride = chunk * mp;
-  if (!tc) oz->Cd.ensure(static_cast<size_t>(S) * dstride);
   for (long long r0 = 0; r0 < n; r0 += chunk) {
     const long long nr = std::min(chunk, n - r0);
     STGP_OZ_SWITCH(S, (slice_rows_kernel<kS><<<grid_for(nr * 32, 256), 256, 0, st>>>(
                            nr, k, kp, A + r0 * lda, lda, false, oz->As.get(), ldk, oz->sA.get())));
     launched(ctx);
-    if (tc) {
-      ProfRegion pr(ctx, "oz_imma");
-      ozaki_tc_rows(ctx, oz->tc, S, kp, nr, m, oz->As.get(), false, oz->sA.get(), oz->Bs.get(), true, oz->sB.get(),
-                    C + r0 * ldc, ldc);
-      continue;
-    }
-    for (int d = 2; d <= S + 1; ++d) {
-      LtPlan* p = plan_for(oz, m, mp, (d - 1) * kp, nr, ldk);
-      lt_matmul(ctx, oz, p, oz->Bs.get() + static_cast<size_t>(S - d + 1) * kp, oz->As.get(),
-                oz->Cd.get() + (d - 2) * dstride);
-    }
-    combine_rows_kernel<<<static_cast<int>(std::min<long long>(nr, ctx->num_sms * 16)), 256, 0, st>>>(
-        nr, m, mp, oz->Cd.get(), dstride, S, oz->sA.get(), oz->sB.get(), C + r0 * ldc, ldc);
-    launched(ctx);
+    ProfRegion pr(ctx, "oz_imma");
+    ozaki_tc_rows(ctx, oz->tc, S, kp, nr, m, oz->As.get(), false, oz->sA.get(), oz->Bs.get(), true, oz->sB.get(),
+                  C + r0 * ldc, ldc);
   }
 }
 
@@ -541,7 +305,6 @@ static void cols_product(stgp_ctx* ctx, int m, long long n, const double* A, int
   const long long lmax = ((1LL << 31) - 1) / (static_cast<long long>(S) * 127 * 127);
   const int L = static_cast<int>(std::min<long long>(lmax / kSlCols * kSlCols, (n + kSlCols - 1) / kSlCols * kSlCols));
   const int nch = static_cast<int>((n + L - 1) / L);
-  const int mp = (m + 3) / 4 * 4;
   const long long ldk = static_cast<long long>(S) * L;
   const long long bstride = static_cast<long long>(m) * ldk;
   const size_t sl = static_cast<size_t>(nch) * bstride;
@@ -586,21 +349,8 @@ static void cols_product(stgp_ctx* ctx, int m, long long n, const double* A, int
     oz->keep_n = n;
   }
   const double* sB = same ? sA : oz->sB.get();
-  if (ozaki_tc_enabled()) {
-    ProfRegion pr(ctx, "oz_imma");
-    ozaki_tc_cols(ctx, oz->tc, S, L, nch, m, Aslices, false, sA, oz->Bs.get(), true, sB, same, C, ldc);
-    return;
-  }
-  const long long cstride = static_cast<long long>(m) * mp;
-  const long long dstride = nch * cstride;
-  oz->Cd.ensure(static_cast<size_t>(S) * dstride);
-  for (int d = 2; d <= S + 1; ++d) {
-    LtPlan* p = plan_for(oz, m, mp, (d - 1) * L, m, static_cast<int>(ldk), nch, bstride, cstride);
-    lt_matmul(ctx, oz, p, oz->Bs.get() + static_cast<size_t>(S - d + 1) * L, Aslices, oz->Cd.get() + (d - 2) * dstride);
-  }
-  combine_cols_kernel<<<grid_for(static_cast<long long>(m) * m, 256), 256, 0, st>>>(
-      m, mp, nch, oz->Cd.get(), dstride, cstride, S, sA, sB, C, ldc);
-  launched(ctx);
+  ProfRegion pr(ctx, "oz_imma");
+  ozaki_tc_cols(ctx, oz->tc, S, L, nch, m, Aslices, false, sA, oz->Bs.get(), true, sB, same, C, ldc);
 }
 
 // per-column factor vector 1 / sqrt(D) (inverse) or sqrt(D)

@@ -38,6 +38,5 @@ void ozaki_tc_rows(stgp_ctx* ctx, OzakiTcState*& st, int S, int kp, long long nx
 void ozaki_tc_cols(stgp_ctx* ctx, OzakiTcState*& st, int S, int L, int nch, int m, const int8_t* xd, bool x_rev,
                    const double* sx, const int8_t* yd, bool y_rev, const double* sy, bool symmetric, double* C,
                    long long ldc);
-bool ozaki_tc_enabled();
 
 }  // namespace stgp
