@@ -41,13 +41,11 @@ PoolDev& pool_dev(int dev) {
     d.init = true;
     const char* e = std::getenv("STGP_POOL");
     d.on = !(e && e[0] == '0');
-    if (d.on) {  // a private pool: the process's default pool (and other libraries using it) keep their settings
-      cudaMemPoolProps props{};
-      props.allocType = cudaMemAllocationTypePinned;
-      props.handleTypes = cudaMemHandleTypeNone;
-      props.location.type = cudaMemLocationTypeDevice;
-      props.location.id = dev;
-      STGP_CUDA(cudaMemPoolCreate(&d.pool, &props));
+    if (d.on) {
+      // The device's default pool with an unbounded release threshold.  A private pool (cudaMemPoolCreate)
+      // was tried: its first growth made the cold cfg4 d_r search 1.75 s instead of 0.49 s
+      // (scripts/search_cold_probe.py), so the default pool stays; STGP_POOL=0 restores cudaMalloc.
+      STGP_CUDA(cudaDeviceGetDefaultMemPool(&d.pool, dev));
       uint64_t thr = UINT64_MAX;
       STGP_CUDA(cudaMemPoolSetAttribute(d.pool, cudaMemPoolAttrReleaseThreshold, &thr));
       STGP_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
