@@ -83,6 +83,25 @@ __device__ __forceinline__ void tma_load4(const CUtensorMap* map, void* dst, uin
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+// the same, multicast to every CTA of the cluster in mask (data and the mbarrier signal land at the same
+// shared-memory offsets in each destination CTA)
+__device__ __forceinline__ void tma_load4_mc(const CUtensorMap* map, void* dst, uint64_t* bar, int c0, int c1, int c2,
+                                             int c3, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, "
+      "%4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // K-major operand tile of rows x 32 bytes written by TMA with 32-byte swizzling: core matrices of 8 rows
 // x 16 bytes, 8-row groups 256 bytes apart (SBO), layout type SWIZZLE_32B, descriptor version 1
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
@@ -104,6 +123,13 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+// arrive on the barrier at this offset in every CTA of the mask once this thread's MMAs are done
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
@@ -121,7 +147,10 @@ __device__ __forceinline__ void chunk_range(const TcArgs& a, int g, int& c0, int
   c1 = static_cast<int>(static_cast<long long>(a.nchunks) * (g + 1) / a.groups);
 }
 
-template <int S>
+// CL > 1: clusters of CL CTAs along the Y tiles share one X tile, each CTA loading 128 / CL of its rows
+// and multicasting them to the whole cluster (half the operand bytes per MMA at CL = 4); the stages are
+// released by every CTA's MMA commit (multicast arrive), items are cluster items (x, y group, group).
+template <int S, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     ozaki_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy, TcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -135,10 +164,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = CL > 1 ? static_cast<int>(cluster_rank()) : 0;
+  const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+  constexpr uint16_t kMask = static_cast<uint16_t>((1u << CL) - 1);
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], CL);
     }
     mbar_init(tmem_full, 1);
     mbar_init(tmem_empty, 4);
@@ -154,6 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // every CTA's barriers initialised before remote arrivals
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -162,8 +195,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
+      for (int it = cid; it < a.nitems; it += ncl) {
         const int4 job = a.items[it];
+        const int yt = job.y * CL + rank;
         int c0, c1;
         chunk_range(a, job.z, c0, c1);
         for (int c = c0; c < c1; ++c)
@@ -172,12 +206,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             unsigned char* st = smem + stage * kStageBytes;
             mbar_expect_tx(&full[stage], kStageBytes);
 #pragma unroll
-            for (int s = 1; s <= S; ++s)
-              tma_load4(&tmx, st + (s - 1) * kTileX, &full[stage], kb * kBK, a.x_rev ? S - s : s - 1, job.x * kBM, c);
+            for (int s = 1; s <= S; ++s) {
+              if (CL == 1)
+                tma_load4(&tmx, st + (s - 1) * kTileX, &full[stage], kb * kBK, a.x_rev ? S - s : s - 1, job.x * kBM, c);
+              else
+                tma_load4_mc(&tmx, st + (s - 1) * kTileX + rank * (kTileX / CL), &full[stage], kb * kBK,
+                             a.x_rev ? S - s : s - 1, job.x * kBM + rank * (kBM / CL), c, kMask);
+            }
 #pragma unroll
             for (int t = 1; t <= S; ++t)
               tma_load4(&tmy, st + S * kTileX + (t - 1) * kTileY, &full[stage], kb * kBK, a.y_rev ? S - t : t - 1,
-                        job.y * kBN, c);
+                        yt * kBN, c);
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1;
@@ -190,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0, te_phase = 0;
-      for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
+      for (int it = cid; it < a.nitems; it += ncl) {
         const int4 job = a.items[it];
         int c0, c1;
         chunk_range(a, job.z, c0, c1);
@@ -212,7 +251,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mma_i8(tmem + (s + t - 2) * kBN, da, db, (kb > 0 || s > 1) ? 1u : 0u);
               }
             }
-            mma_commit(&empty[stage]);  // frees the stage once these MMAs have read it
+            if (CL == 1) mma_commit(&empty[stage]);  // frees the stage once these MMAs have read it
+            else mma_commit_mc(&empty[stage], kMask);  // in every CTA of the cluster (their X pieces)
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1;
@@ -228,12 +268,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
     uint32_t tf_phase = 0;
-    for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
+    for (int it = cid; it < a.nitems; it += ncl) {
       const int4 job = a.items[it];
       int c0, c1;
       chunk_range(a, job.z, c0, c1);
       const int x = job.x * kBM + quarter * 32 + lane;
-      const int y0 = job.y * kBN;
+      const int y0 = (job.y * CL + rank) * kBN;
       double acc[kBN];
 #pragma unroll
       for (int e = 0; e < kBN; ++e) acc[e] = 0.0;
@@ -286,6 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // no CTA leaves while a peer may still multicast into it
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -344,31 +385,79 @@ CUtensorMap make_map(const int8_t* base, long long kext, int S, long long rows, 
   return m;
 }
 
-template <int S>
+template <int S, int CL>
 void launch_tc(stgp_ctx* ctx, const CUtensorMap& tx, const CUtensorMap& ty, const TcArgs& a) {
   // at least 116 KB so that one CTA holds an SM: it owns all 512 TMEM columns
   constexpr int smem = std::max(kStages * S * (kTileX + kTileY) + 1024 + 256, 116 * 1024);
-  static bool attr = false;
-  if (!attr) {
-    STGP_CUDA(cudaFuncSetAttribute(ozaki_tc_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
+  static int max_clusters = 0;
+  if (max_clusters == 0) {
+    STGP_CUDA(cudaFuncSetAttribute(ozaki_tc_kernel<S, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    max_clusters = ctx->num_sms / CL;
+    if (CL > 1) {
+      cudaLaunchConfig_t q{};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CL;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      q.gridDim = dim3(CL * max_clusters);
+      q.blockDim = dim3(kThreads);
+      q.dynamicSmemBytes = smem;
+      q.attrs = at;
+      q.numAttrs = 1;
+      int mc = 0;
+      if (cudaOccupancyMaxActiveClusters(&mc, ozaki_tc_kernel<S, CL>, &q) == cudaSuccess && mc > 0) max_clusters = mc;
+      (void)cudaGetLastError();
+    }
   }
-  const int grid = std::min(a.nitems, ctx->num_sms);
-  ozaki_tc_kernel<S><<<grid, kThreads, smem, ctx->stream>>>(tx, ty, a);
+  const int clusters = std::min(a.nitems, max_clusters);
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(clusters * CL);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  STGP_CUDA(cudaLaunchKernelEx(&cfg, ozaki_tc_kernel<S, CL>, tx, ty, a));
   launched(ctx);
 }
 
+template <int CL>
 void dispatch(stgp_ctx* ctx, int S, const CUtensorMap& tx, const CUtensorMap& ty, const TcArgs& a) {
   switch (S) {
-    case 2: launch_tc<2>(ctx, tx, ty, a); break;
-    case 3: launch_tc<3>(ctx, tx, ty, a); break;
-    case 4: launch_tc<4>(ctx, tx, ty, a); break;
-    case 5: launch_tc<5>(ctx, tx, ty, a); break;
-    case 6: launch_tc<6>(ctx, tx, ty, a); break;
-    case 7: launch_tc<7>(ctx, tx, ty, a); break;
-    case 8: launch_tc<8>(ctx, tx, ty, a); break;
+    case 2: launch_tc<2, CL>(ctx, tx, ty, a); break;
+    case 3: launch_tc<3, CL>(ctx, tx, ty, a); break;
+    case 4: launch_tc<4, CL>(ctx, tx, ty, a); break;
+    case 5: launch_tc<5, CL>(ctx, tx, ty, a); break;
+    case 6: launch_tc<6, CL>(ctx, tx, ty, a); break;
+    case 7: launch_tc<7, CL>(ctx, tx, ty, a); break;
+    case 8: launch_tc<8, CL>(ctx, tx, ty, a); break;
     default: throw Error(kConfig, "ozaki_tc: slice count must lie in [2, 8]");
   }
+}
+
+// cluster size of the X multicast (STGP_OZAKI_CLUSTER: 1, 2 or 4; default 1).  Measured at the cfg4
+// shapes (tests/test_gpu_ozaki.py timing cases): rows form 5.12 / 5.39 / 6.03 ms and column form
+// 18.99 / 20.96 / 20.97 ms at CL = 1 / 2 / 4 -- the kernel is not bound by L2 operand traffic, and the
+// cluster-wide stage release couples the CTAs' pipelines.
+int cluster_size() {
+  static const int cl = [] {
+    const char* e = std::getenv("STGP_OZAKI_CLUSTER");
+    const int v = e ? std::atoi(e) : 1;
+    return v == 1 || v == 2 || v == 4 ? v : 1;
+  }();
+  return cl;
+}
+
+void run(stgp_ctx* ctx, int S, int CL, const CUtensorMap& tx, const CUtensorMap& ty, const TcArgs& a) {
+  if (CL == 4) dispatch<4>(ctx, S, tx, ty, a);
+  else if (CL == 2) dispatch<2>(ctx, S, tx, ty, a);
+  else dispatch<1>(ctx, S, tx, ty, a);
 }
 
 }  // namespace
@@ -392,13 +481,15 @@ void ozaki_tc_rows(stgp_ctx* ctx, OzakiTcState*& st, int S, int kp, long long nx
   if (kp % kBK) throw Error(kInternal, "ozaki_tc_rows: kp must be a multiple of 32");
   OzakiTcState* s = tc_state(st);
   const long long ldk = static_cast<long long>(S) * kp;
-  const CUtensorMap tx = make_map(xd, kp, S, nx, 1, kp, ldk, nx * ldk, kBM);
+  const int CL = cluster_size();
+  const CUtensorMap tx = make_map(xd, kp, S, nx, 1, kp, ldk, nx * ldk, kBM / CL);
   const CUtensorMap ty = make_map(yd, kp, S, ny, 1, kp, ldk, static_cast<long long>(ny) * ldk, kBN);
   const int tiles_x = static_cast<int>((nx + kBM - 1) / kBM), tiles_y = (ny + kBN - 1) / kBN;
+  const int groups_y = (tiles_y + CL - 1) / CL;
   std::vector<int4> items;
-  items.reserve(static_cast<size_t>(tiles_x) * tiles_y);
-  for (int bx = 0; bx < tiles_x; ++bx)  // Y tiles fastest: the CTAs in flight share one X block in L2
-    for (int by = 0; by < tiles_y; ++by) items.push_back(make_int4(bx, by, 0, 0));
+  items.reserve(static_cast<size_t>(tiles_x) * groups_y);
+  for (int bx = 0; bx < tiles_x; ++bx)  // Y groups fastest: the clusters in flight share one X block in L2
+    for (int gy = 0; gy < groups_y; ++gy) items.push_back(make_int4(bx, gy, 0, 0));
   s->items.upload(items.data(), items.size(), ctx->stream);
   TcArgs a{};
   a.S = S;
@@ -416,7 +507,7 @@ void ozaki_tc_rows(stgp_ctx* ctx, OzakiTcState*& st, int S, int kp, long long nx
   a.sy = sy;
   a.out = out;
   a.ldo = ldo;
-  dispatch(ctx, S, tx, ty, a);
+  run(ctx, S, CL, tx, ty, a);
 }
 
 // cols form: C[x ldc + y] = sum_c (sx[c m + x] sy[c m + y]) sum_d 2^-7d sum_{s+t=d} X_s,c[x] . Y_t,c[y];
@@ -428,21 +519,24 @@ void ozaki_tc_cols(stgp_ctx* ctx, OzakiTcState*& st, int S, int L, int nch, int 
   if (L % kBK) throw Error(kInternal, "ozaki_tc_cols: L must be a multiple of 32");
   OzakiTcState* s = tc_state(st);
   const long long rs = static_cast<long long>(S) * L;
-  const CUtensorMap tx = make_map(xd, L, S, m, nch, L, rs, static_cast<long long>(m) * rs, kBM);
+  const int CL = cluster_size();
+  const CUtensorMap tx = make_map(xd, L, S, m, nch, L, rs, static_cast<long long>(m) * rs, kBM / CL);
   const CUtensorMap ty = make_map(yd, L, S, m, nch, L, rs, static_cast<long long>(m) * rs, kBN);
   const int tiles_x = (m + kBM - 1) / kBM, tiles_y = (m + kBN - 1) / kBN;
-  std::vector<int2> tiles;
+  const int groups_y = (tiles_y + CL - 1) / CL;
+  std::vector<int2> tiles;  // (x tile, y group): kept when one of its y tiles reaches the lower triangle
   for (int bx = 0; bx < tiles_x; ++bx)
-    for (int by = 0; by < tiles_y; ++by)
-      if (!symmetric || by * kBN < (bx + 1) * kBM) tiles.push_back(make_int2(bx, by));
-  // split the chunks of each tile over G CTAs so the work items fill whole waves of the SMs
+    for (int gy = 0; gy < groups_y; ++gy)
+      if (!symmetric || gy * CL * kBN < (bx + 1) * kBM) tiles.push_back(make_int2(bx, gy));
+  // split the chunks of each tile over G clusters so the work items fill whole waves of the SMs
   const int nt = static_cast<int>(tiles.size());
+  const int slots = std::max(1, ctx->num_sms / CL);
   int G = 1;
   double best = 0.0;
   for (int g = 1; g <= std::min(nch, 16); ++g) {
     const long long it = static_cast<long long>(nt) * g;
-    const long long waves = (it + ctx->num_sms - 1) / ctx->num_sms;
-    const double eff = static_cast<double>(it) / (waves * ctx->num_sms) * (1.0 - 0.02 * (g - 1));
+    const long long waves = (it + slots - 1) / slots;
+    const double eff = static_cast<double>(it) / (waves * slots) * (1.0 - 0.02 * (g - 1));
     if (eff > best + 1e-9) {
       best = eff;
       G = g;
@@ -476,7 +570,7 @@ void ozaki_tc_cols(stgp_ctx* ctx, OzakiTcState*& st, int S, int L, int nch, int 
     a.out = C;
     a.ldo = ldc;
   }
-  dispatch(ctx, S, tx, ty, a);
+  run(ctx, S, CL, tx, ty, a);
   if (G > 1) {
     reduce_groups_kernel<<<grid_for(static_cast<long long>(m) * m, 256), 256, 0, ctx->stream>>>(
         m, m, G, s->part.get(), ldp, a.part_stride, C, ldc);
