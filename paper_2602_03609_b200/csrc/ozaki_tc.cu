@@ -39,6 +39,7 @@ constexpr int kThreads = 192;
 constexpr int kTileX = kBM * kBK;  // bytes of one X slice tile
 constexpr int kTileY = kBN * kBK;
 
+
 struct TcArgs {
   int S;
   int kblocks;            // K steps per chunk
@@ -109,15 +110,19 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
          (static_cast<uint64_t>(256 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
          (static_cast<uint64_t>(6) << 61);
 }
-// instruction descriptor: kind::i8, signed int8 A and B, int32 D, both K-major, M = 128, N = 64
-constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kBN >> 3) << 17) |
-                            (static_cast<uint32_t>(kBM >> 4) << 24);
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+// instruction descriptor: kind::i8, signed int8 A and B, int32 D, both K-major, M = 128, N = n
+__host__ __device__ constexpr uint32_t idesc_i8(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(kBM >> 4) << 24);
+}
+constexpr uint32_t kIdesc = idesc_i8(kBN);
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate,
+                                       uint32_t idesc = kIdesc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %5, %5, %5}, p;\n\t}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate), "r"(0u));
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate), "r"(0u));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -241,14 +246,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const uint32_t sbase = smem_u32(smem + stage * kStageBytes);
+            // For X slice s the pairs (s, t), t = 1 .. S + 1 - s, feed the consecutive diagonals s - 1 .. S - 1,
+            // and the Y slices t are consecutive 64-row tiles: one MMA with N = 64 (S + 1 - s) (<= 256 per
+            // instruction) covers them all -- S (S + 1) / 2 pair products in 2 S - S / 4 instructions.
 #pragma unroll
             for (int s = 1; s <= S; ++s) {
               const uint64_t da = smem_desc(sbase + (s - 1) * kTileX);
+              const int nt = S + 1 - s;
 #pragma unroll
-              for (int t = 1; t <= S + 1 - s; ++t) {
-                const uint64_t db = smem_desc(sbase + S * kTileX + (t - 1) * kTileY);
-                // diagonal s + t - 2; its first product (s = 1) of the chunk's first K step starts it
-                mma_i8(tmem + (s + t - 2) * kBN, da, db, (kb > 0 || s > 1) ? 1u : 0u);
+              for (int t0 = 1; t0 <= nt; t0 += 4) {
+                const int cnt = nt - t0 + 1 < 4 ? nt - t0 + 1 : 4;
+                const uint64_t db = smem_desc(sbase + S * kTileX + (t0 - 1) * kTileY);
+                // diagonals s + t0 - 2 ..; the first product (s = 1) of the chunk's first K step starts them
+                mma_i8(tmem + (s + t0 - 2) * kBN, da, db, (kb > 0 || s > 1) ? 1u : 0u, idesc_i8(kBN * cnt));
               }
             }
             if (CL == 1) mma_commit(&empty[stage]);  // frees the stage once these MMAs have read it
