@@ -171,8 +171,11 @@ uint64_t mix_seed(uint64_t seed, uint64_t stream) {
 
 void TimeIndex::build() {
   const int nt = nT();
-  if (nt > 4096)
-    config_error("more than 4096 distinct time values: the device lag tables need a discrete time axis");
+  if (nt > kMaxTableTimes) {  // live mode: the device evaluates each pair's lag (upload_lag_table)
+    lags.clear();
+    lagid.clear();
+    return;
+  }
   std::vector<double> all;
   all.reserve(static_cast<size_t>(nt) * (nt + 1) / 2);
   for (int a = 0; a < nt; ++a)
@@ -208,6 +211,28 @@ std::vector<TF> tabulate(const Params& p, const std::vector<double>& lags, const
 
 void upload_lag_table(DevLagTable& d, const TimeIndex& ti, const Params& p, const LagPolicy& pol,
                       cudaStream_t s, bool index_changed) {
+  if (ti.nT() > kMaxTableTimes) {
+    d.live = true;
+    if (index_changed || d.nT != ti.nT()) {
+      d.Tv.upload(ti.T.data(), ti.T.size(), s);
+      d.nT = ti.nT();
+    }
+    // the integer-lag table of the policy (host glibc), bit-identical to the table mode
+    d.itab_n = pol.table ? pol.size : 0;
+    if (d.itab_n > 0) {
+      std::vector<double> ul(static_cast<size_t>(d.itab_n));
+      for (int u = 0; u < d.itab_n; ++u) ul[static_cast<size_t>(u)] = u;
+      LagPolicy none;
+      d.host_tf = tabulate(p, ul, none);
+      d.itab.upload(d.host_tf.data(), d.host_tf.size(), s);
+    }
+    d.la = p.a;
+    d.two_alpha = 2.0 * p.alpha;
+    d.E = exponent_E(p);
+    d.half_beta = p.beta / 2.0;
+    return;
+  }
+  d.live = false;
   if (index_changed || d.nT != ti.nT()) {
     d.lagid.upload(ti.lagid.data(), ti.lagid.size(), s);
     d.nT = ti.nT();
@@ -216,7 +241,12 @@ void upload_lag_table(DevLagTable& d, const TimeIndex& ti, const Params& p, cons
   d.tf.upload(d.host_tf.data(), d.host_tf.size(), s);
 }
 
-LagTable lag_view(const DevLagTable& d) { return LagTable{d.lagid.get(), d.tf.get(), d.nT}; }
+LagTable lag_view(const DevLagTable& d) {
+  if (d.live)
+    return LagTable{nullptr, nullptr, d.nT, d.Tv.get(), d.itab_n > 0 ? d.itab.get() : nullptr, d.itab_n,
+                    d.la, d.two_alpha, d.E, d.half_beta};
+  return LagTable{d.lagid.get(), d.tf.get(), d.nT, nullptr, nullptr, 0, 0.0, 0.0, 0.0, 0.0};
+}
 
 ProfRegion::ProfRegion(stgp_ctx* c, const char* n) : ctx(c), name(n) {
   if (!ctx->prof) return;

@@ -48,7 +48,14 @@ struct DevLagTable {
   DevBuf<TF> tf;
   int nT = 0;
   std::vector<TF> host_tf;
+  // live mode (more than kMaxTableTimes distinct times): time values, integer-lag table, parameters
+  bool live = false;
+  DevBuf<double> Tv;
+  DevBuf<TF> itab;
+  int itab_n = 0;
+  double la = 0.0, two_alpha = 0.0, E = 0.0, half_beta = 0.0;
 };
+constexpr int kMaxTableTimes = 4096;  // nT x nT lag ids above this: live factors
 
 struct OzakiState;  // ozaki.cu: int8 slice buffers and the tcgen05 kernel work lists
 }  // namespace stgp

@@ -26,19 +26,68 @@ constexpr int kRowWarps = 4;
 constexpr int kKmax = 32;  // closure slots per warp (k <= 31 neighbours)
 constexpr unsigned kFull = 0xffffffffu;
 
+// Temporal factors of a time-id pair.  Table mode (nT <= 4096 distinct times): lagid[ta nT + tb] indexes
+// the host-tabulated factors of the distinct lags.  Live mode (more distinct times): u = |T[ta] - T[tb]|,
+// the structure's integer-lag table when it applies (covariance.cpp:127-146 snap rule, host glibc:
+// bit-identical to the table mode), otherwise the factors evaluated on the device (covariance.cpp:94-113
+// with CUDA's pow / log: within a few ulp of glibc).
 struct LagTable {
-  const int32_t* lagid;  // nT * nT -> index into tf
+  const int32_t* lagid;  // nT * nT -> index into tf (table mode), or null (live mode)
   const TF* tf;
   int nT;
+  const double* Tv;   // live mode: the time value of each id
+  const TF* itab;     // live mode: integer-lag table (null when the policy has none)
+  int itab_n;
+  double la, two_alpha, E, half_beta;  // live mode: a, 2 alpha, delta + beta, beta / 2
+  // out of line: the table-mode fast path of get / get2 stays small (register pressure of the hot kernels)
+  __device__ __noinline__ TF live(double u) const {
+    TF f;
+    if (u == 0.0) {
+      f.pow_mE = 1.0;
+      f.pow_mbh = 1.0;
+      f.inv_T = 1.0;
+      f.log_T = 0.0;
+      f.u2a = 0.0;
+      f.u2a_logu = 0.0;
+      return f;
+    }
+    const double r = nearbyint(u);
+    if (itab && fabs(u - r) < 1e-9 && r < static_cast<double>(itab_n)) {
+      const TF* p = itab + static_cast<int>(r);
+      f.pow_mE = __ldg(&p->pow_mE);
+      f.pow_mbh = __ldg(&p->pow_mbh);
+      f.inv_T = __ldg(&p->inv_T);
+      f.log_T = __ldg(&p->log_T);
+      f.u2a = __ldg(&p->u2a);
+      f.u2a_logu = __ldg(&p->u2a_logu);
+      return f;
+    }
+    f.u2a = pow(u, two_alpha);
+    f.u2a_logu = f.u2a * log(u);
+    const double T = la * f.u2a + 1.0;
+    f.inv_T = 1.0 / T;
+    f.log_T = log(T);
+    f.pow_mE = pow(T, -E);
+    f.pow_mbh = pow(T, -half_beta);
+    return f;
+  }
+  __device__ __forceinline__ double lag(int ta, int tb) const { return fabs(__ldg(&Tv[ta]) - __ldg(&Tv[tb])); }
   __device__ __forceinline__ const TF* at(int ta, int tb) const {
     return tf + __ldg(&lagid[static_cast<size_t>(ta) * nT + tb]);
   }
   __device__ __forceinline__ void get2(int ta, int tb, double& pow_mE, double& pow_mbh) const {
+    if (!lagid) {
+      const TF f = live(lag(ta, tb));
+      pow_mE = f.pow_mE;
+      pow_mbh = f.pow_mbh;
+      return;
+    }
     const TF* p = at(ta, tb);
     pow_mE = __ldg(&p->pow_mE);
     pow_mbh = __ldg(&p->pow_mbh);
   }
   __device__ __forceinline__ TF get(int ta, int tb) const {
+    if (!lagid) return live(lag(ta, tb));
     const TF* p = at(ta, tb);
     TF f;
     f.pow_mE = __ldg(&p->pow_mE);
