@@ -257,7 +257,9 @@ int stgp_debug_gemm_rows(stgp_ctx* ctx, int emulated, long long n, int m, int k,
  * row-major C) through the int8 Ozaki path (emulated = 1) or cuBLAS DGEMM (emulated = 0). */
 int stgp_debug_gemm_cols(stgp_ctx* ctx, int emulated, int m, long long n, const double* A_host,
                          const double* B_host, double* C_host, double* ms);
-/* device Gneiting covariance / kernel gradient of (h, u) pairs with live factors */
+/* device Gneiting covariance / kernel gradient of (h, u) pairs with live factors; grad6_out may be
+   NULL (covariances only).  A general nu (outside {0.5, 1.5, 2.5}) evaluates covariances through the
+   Bessel-K Matern and returns STGP_ERR_NUMERIC when a gradient is requested (covariance.cpp:79-87). */
 int stgp_debug_kernel(stgp_ctx* ctx, const stgp_params* theta, int n, const double* h_host,
                       const double* u_host, double* cov_out, double* grad6_out);
 

@@ -538,12 +538,13 @@ def debug_exp(x, ctx: Context | None = None) -> np.ndarray:
     return out
 
 
-def debug_kernel(theta, h, u, ctx: Context | None = None):
+def debug_kernel(theta, h, u, ctx: Context | None = None, grad: bool = True):
+    """Device GneitingKernel::eval (and ::grad unless grad=False; general nu raises NumericError there)."""
     ctx = ctx or default_context()
     h, u = _f64(h), _f64(u)
-    cov, g = np.zeros(len(h)), np.zeros((len(h), 6))
+    cov, g = np.zeros(len(h)), (np.zeros((len(h), 6)) if grad else None)
     p = as_params(theta).c_struct()
-    N.call("stgp_debug_kernel", ctx.h, C.byref(p), len(h), _ptr(h), _ptr(u), _ptr(cov), _ptr(g))
+    N.call("stgp_debug_kernel", ctx.h, C.byref(p), len(h), _ptr(h), _ptr(u), _ptr(cov), _ptr(g) if grad else None)
     return cov, g
 
 

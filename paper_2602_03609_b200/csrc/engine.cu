@@ -133,6 +133,14 @@ TF host_factors(const Params& p, double u) {
   return f;
 }
 
+// GneitingKernel::grad -> matern_corr_deriv (covariance.cpp:79-87): analytic only for the closed forms
+void require_analytic_grad(const Params& p) {
+  if (nu_code_of(p.nu) == kNuGeneral)
+    numeric_error(
+        "matern_corr_deriv: analytic derivative only for nu in {0.5, 1.5, 2.5}; use finite differences for "
+        "general nu");
+}
+
 void host_grad00(const Params& p, double g[6]) {
   // GneitingKernel::grad(0, 0): x = 0, M = 1, M' = matern_corr_deriv(0)
   const double x = 0.0;
@@ -157,8 +165,22 @@ DevKernel dev_kernel(const Params& p) {
   k.beta = p.beta;
   k.E = exponent_E(p);
   k.nu_code = nu_code_of(p.nu);
-  if (k.nu_code < 0)
-    config_error("device kernels support nu in {0.5, 1.5, 2.5} (Matern closed forms, covariance.cpp:66-71)");
+  k.g = MaternNu{};
+  if (k.nu_code == kNuGeneral) {
+    // constants of the general Matern (covariance.cpp:73-74) and Temme's Gamma combinations at mu
+    MaternNu& g = k.g;
+    g.nu = p.nu;
+    g.coef = std::pow(2.0, 1.0 - p.nu) / std::tgamma(p.nu);
+    g.nl = static_cast<int>(p.nu + 0.5);
+    g.mu = p.nu - g.nl;
+    constexpr double kEps = 2.220446049250313e-16;
+    g.gampl = 1.0 / std::tgamma(1.0 + g.mu);
+    g.gammi = 1.0 / std::tgamma(1.0 - g.mu);
+    g.gam1 = std::fabs(g.mu) < kEps ? -0.5772156649015328606 : (g.gammi - g.gampl) / (2.0 * g.mu);
+    g.gam2 = (g.gammi + g.gampl) / 2.0;
+    const double pimu = 3.141592653589793 * g.mu;
+    g.fact = std::fabs(pimu) < kEps ? 1.0 : pimu / std::sin(pimu);
+  }
   return k;
 }
 
@@ -358,7 +380,8 @@ __global__ void debug_kernel_kernel(int n, DevKernel k, const TF* tf, const doub
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double g[6];
     const TF f = tf[i];
-    cov[i] = gneiting_eval(k, h[i], f);
+    cov[i] = gneiting_eval<true>(k, h[i], f);
+    if (!g6) continue;
     gneiting_grad(k, h[i], f, g);
     for (int q = 0; q < 6; ++q) g6[static_cast<size_t>(i) * 6 + q] = g[q];
   }
@@ -521,7 +544,7 @@ std::vector<double> run_rows_args(stgp_structure* s, int mode, RowArgs& a) {
         }
       }
       const int ks = s->m_v <= 8 ? 8 : (s->m_v <= 16 ? 16 : (s->m_v <= 24 ? 24 : 31));
-#define STGP_ROWS(M, HW, KS) blocks = launch_row_kernel(ctx, vecchia_rows_kernel<M, HW, KS>, blocks, a)
+#define STGP_ROWS(M, HW, KS, ...) blocks = launch_row_kernel(ctx, vecchia_rows_kernel<M, HW, KS, ##__VA_ARGS__>, blocks, a)
 #define STGP_ROWS_KS(M, HW)              \
   switch (ks) {                          \
     case 8: STGP_ROWS(M, HW, 8); break;   \
@@ -529,7 +552,11 @@ std::vector<double> run_rows_args(stgp_structure* s, int mode, RowArgs& a) {
     case 24: STGP_ROWS(M, HW, 24); break; \
     default: STGP_ROWS(M, HW, 31); break; \
   }
-      if (mode == kModeVifGrad && a.Lfac_in) {
+      if (a.k.nu_code == kNuGeneral) {  // value modes only: the gradient needs a closed-form Matern
+        if (mode != kModeBuild && mode != kModeNll) require_analytic_grad(s->th);
+        if (mode == kModeBuild) { if (hw) STGP_ROWS(kModeBuild, true, 31, true); else STGP_ROWS(kModeBuild, false, 31, true); }
+        else { if (hw) STGP_ROWS(kModeNll, true, 31, true); else STGP_ROWS(kModeNll, false, 31, true); }
+      } else if (mode == kModeVifGrad && a.Lfac_in) {
         switch (ks) {
           case 8: blocks = launch_row_kernel(ctx, vif_grad_stored_kernel<8>, blocks, a); break;
           case 16: blocks = launch_row_kernel(ctx, vif_grad_stored_kernel<16>, blocks, a); break;
@@ -1019,7 +1046,8 @@ static stgp_neighbors* run_search(stgp_dataset* ds, int metric, const Params* th
     nb->idx.upload(neg.data(), total, ctx->stream);
   } else if (metric == STGP_METRIC_DC) {
     ProfRegion pr(ctx, "knn_dc");
-    knn_kernel<0><<<blocks, 256, 0, ctx->stream>>>(a);
+    if (a.k.nu_code == kNuGeneral) knn_kernel<0, true><<<blocks, 256, 0, ctx->stream>>>(a);
+    else knn_kernel<0><<<blocks, 256, 0, ctx->stream>>>(a);
     ++ctx->launches;
   } else {
     ProfRegion pr(ctx, "knn_euclid");
@@ -1135,8 +1163,9 @@ int stgp_debug_kernel(stgp_ctx* ctx, const stgp_params* theta, int n, const doub
     DevBuf<double> dh, dc(static_cast<size_t>(n)), dg(static_cast<size_t>(n) * 6);
     dtf.upload(tf.data(), n, ctx->stream);
     dh.upload(h, n, ctx->stream);
+    if (g6) require_analytic_grad(p);
     debug_kernel_kernel<<<std::max(1, ceil_div(n, 128)), 128, 0, ctx->stream>>>(n, dev_kernel(p), dtf.get(), dh.get(),
-                                                                               dc.get(), dg.get());
+                                                                               dc.get(), g6 ? dg.get() : nullptr);
     ++ctx->launches;
     STGP_LAUNCH_CHECK();
     dc.download(cov, n, ctx->stream);

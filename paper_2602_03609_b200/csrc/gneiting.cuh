@@ -90,21 +90,109 @@ __device__ __forceinline__ double matern_deriv_from_exp(double x, double e, int 
   return __dmul_rn(-__ddiv_rn(__dmul_rn(x, __dadd_rn(1.0, x)), 3.0), e);
 }
 
+constexpr int kNuGeneral = 3;  // nu outside {0.5, 1.5, 2.5}: Bessel-K form, value only
+
+// nu-only constants of the general Matern (host-computed with glibc, MaternNu::make in engine.cu):
+// K_nu is evaluated at mu = nu - nl (|mu| <= 1/2) and raised to nu by the upward recurrence.
+struct MaternNu {
+  double nu, mu, coef;           // coef = 2^(1-nu) / Gamma(nu)   (covariance.cpp:73-74)
+  double gam1, gam2, gampl, gammi, fact;  // Temme's Gamma combinations at mu; fact = pi mu / sin(pi mu)
+  int nl;
+};
+
 struct DevKernel {
   double s1, c, a, beta, E;  // sigma1_2, spatial decay, temporal scale, beta, delta+beta
-  int nu_code;               // 0: 0.5, 1: 1.5, 2: 2.5
+  int nu_code;               // 0: 0.5, 1: 1.5, 2: 2.5, kNuGeneral: other (eval only)
+  MaternNu g;                // used when nu_code == kNuGeneral
 };
 
 inline int nu_code_of(double nu) {
   if (nu == 0.5) return 0;
   if (nu == 1.5) return 1;
   if (nu == 2.5) return 2;
-  return -1;
+  return kNuGeneral;
 }
 
-// GneitingKernel::eval (covariance.cpp:138-149)
+// K_mu(x), K_{mu+1}(x) for |mu| <= 1/2, x > 0: Temme's series below x = 2, Steed's continued
+// fraction CF2 (Temme's normalisation) above -- the method of the libstdc++ std::cyl_bessel_k the
+// reference calls (covariance.cpp:74), evaluated here with CUDA's log/exp/sinh/cosh (a few ulp,
+// so general-nu covariances match the reference to ~1e-15 relative, not bit for bit).
+__device__ __forceinline__ double bessel_k_nu(const MaternNu& g, double x) {
+  constexpr double kEps = 2.220446049250313e-16;
+  constexpr int kMaxIter = 15000;
+  const double mu = g.mu, xi = 1.0 / x, xi2 = 2.0 * xi;
+  double kmu, kmu1;
+  if (x < 2.0) {
+    const double x2 = 0.5 * x;
+    double d = -log(x2);
+    double e = mu * d;
+    const double fact2 = fabs(e) < kEps ? 1.0 : sinh(e) / e;
+    double ff = g.fact * (g.gam1 * cosh(e) + g.gam2 * fact2 * d);
+    double sum = ff;
+    e = exp(e);
+    double p = 0.5 * e / g.gampl, q = 0.5 / (e * g.gammi), c = 1.0;
+    d = x2 * x2;
+    double sum1 = p;
+    for (int i = 1; i <= kMaxIter; ++i) {
+      const double di = static_cast<double>(i);
+      ff = (di * ff + p + q) / (di * di - mu * mu);
+      c *= d / di;
+      p /= di - mu;
+      q /= di + mu;
+      const double del = c * ff;
+      sum += del;
+      sum1 += c * (p - di * ff);
+      if (fabs(del) < kEps * fabs(sum)) break;
+    }
+    kmu = sum;
+    kmu1 = sum1 * xi2;
+  } else {
+    double b = 2.0 * (1.0 + x), d = 1.0 / b, h = d, delh = d, q1 = 0.0, q2 = 1.0;
+    const double a1 = 0.25 - mu * mu;
+    double q = a1, c = a1, a = -a1, s = 1.0 + q * delh;
+    for (int i = 2; i <= kMaxIter; ++i) {
+      a -= 2.0 * (i - 1);
+      c = -a * c / i;
+      const double qnew = (q1 - b * q2) / a;
+      q1 = q2;
+      q2 = qnew;
+      q += c * qnew;
+      b += 2.0;
+      d = 1.0 / (b + a * d);
+      delh = (b * d - 1.0) * delh;
+      h += delh;
+      const double dels = q * delh;
+      s += dels;
+      if (fabs(dels / s) < kEps) break;
+    }
+    h = a1 * h;
+    kmu = sqrt(3.141592653589793 / (2.0 * x)) * exp(-x) / s;
+    kmu1 = kmu * (mu + x + 0.5 - h) * xi;
+  }
+  for (int i = 1; i <= g.nl; ++i) {  // K_{mu+i+1} = 2 (mu+i)/x K_{mu+i} + K_{mu+i-1}
+    const double kn = (mu + i) * xi2 * kmu1 + kmu;
+    kmu = kmu1;
+    kmu1 = kn;
+  }
+  return kmu;
+}
+
+// matern_corr for general nu (covariance.cpp:72-76): 2^(1-nu)/Gamma(nu) x^nu K_nu(x), 0 where
+// K_nu underflows
+// (out of line: the closed-form kernels keep their registers; only this branch pays the call)
+static __device__ __noinline__ double matern_general(const MaternNu& g, double x) {
+  if (x == 0.0) return 1.0;
+  const double v = g.coef * pow(x, g.nu) * bessel_k_nu(g, x);
+  return isfinite(v) ? v : 0.0;
+}
+
+// GneitingKernel::eval (covariance.cpp:138-149).  GEN = false compiles the closed forms only (the
+// hot kernels' default: the out-of-line general branch costs them registers); kernels that can see a
+// general nu are instantiated with GEN = true by their launchers.
+template <bool GEN = false>
 __device__ __forceinline__ double gneiting_eval(const DevKernel& k, double h, const TF& f) {
   const double x = __dmul_rn(__dmul_rn(k.c, h), f.pow_mbh);
+  if (GEN && k.nu_code == kNuGeneral) return __dmul_rn(__dmul_rn(k.s1, f.pow_mE), matern_general(k.g, x));
   const double e = (x == 0.0) ? 1.0 : glibc_exp(-x);
   return __dmul_rn(__dmul_rn(k.s1, f.pow_mE), matern_from_exp(x, e, k.nu_code));
 }

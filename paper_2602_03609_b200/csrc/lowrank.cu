@@ -60,7 +60,7 @@ __global__ void sigma_m_kernel(ZPts z, int M, int ldm, DevKernel k, LagTable lt,
       TF f;
       f.pow_mE = pe;
       f.pow_mbh = pb;
-      v = gneiting_eval(k, spatial_dist(z.zx[a], z.zy[a], z.zx[b], z.zy[b]), f);
+      v = gneiting_eval<true>(k, spatial_dist(z.zx[a], z.zy[a], z.zx[b], z.zy[b]), f);
       if (r == c) {
         v = __dadd_rn(v, jit1);
         if (jit2 != 0.0) v = __dadd_rn(v, jit2);
@@ -71,6 +71,7 @@ __global__ void sigma_m_kernel(ZPts z, int M, int ldm, DevKernel k, LagTable lt,
 }
 
 // U(j, i) = k(z_j, p_i) (approximations.cpp:226-232), columns [c0, c1)
+template <bool GEN>
 __global__ void cross_cov_kernel(ZPts z, int M, int ldm, const double* x, const double* y, const int32_t* tid,
                                  int c0, int c1, DevKernel k, LagTable lt, double* U) {
   for (int i = c0 + blockIdx.x; i < c1; i += gridDim.x) {
@@ -85,7 +86,7 @@ __global__ void cross_cov_kernel(ZPts z, int M, int ldm, const double* x, const 
         TF f;
         f.pow_mE = pe;
         f.pow_mbh = pb;
-        v = gneiting_eval(k, spatial_dist(z.zx[j], z.zy[j], xi, yi), f);
+        v = gneiting_eval<GEN>(k, spatial_dist(z.zx[j], z.zy[j], xi, yi), f);
       }
       col[j] = v;
     }
@@ -655,9 +656,11 @@ void build_cross(stgp_structure* s, int c0, int c1, bool /*keep_U*/) {
   L.W.ensure(total);
   {
     ProfRegion pr(ctx, "U_cross_cov");
-    cross_cov_kernel<<<std::max(1, std::min(c1 - c0, ctx->num_sms * 16)), 128, 0, ctx->stream>>>(
-        zpts(s), L.M, L.ldm, s->ds->x.get(), s->ds->y.get(), s->ds->tid.get(), c0, c1, dev_kernel(s->th),
-        lag_view(s->lt), L.U.get());
+    const DevKernel k = dev_kernel(s->th);
+    auto kern = k.nu_code == kNuGeneral ? cross_cov_kernel<true> : cross_cov_kernel<false>;
+    kern<<<std::max(1, std::min(c1 - c0, ctx->num_sms * 16)), 128, 0, ctx->stream>>>(
+        zpts(s), L.M, L.ldm, s->ds->x.get(), s->ds->y.get(), s->ds->tid.get(), c0, c1, k, lag_view(s->lt),
+        L.U.get());
     launched(ctx);
   }
   ProfRegion pr(ctx, "W_trmm");
@@ -1033,6 +1036,7 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
 }
 
 void lowrank_nll_grad(stgp_structure* s, double* nll, double* grad) {
+  require_analytic_grad(s->th);
   if (s->kind == STGP_FITC) {
     fitc_nll_grad(s, nll, grad);
     return;

@@ -72,7 +72,7 @@ __device__ __forceinline__ double target_dist(const PredArgs& a, int p, int j, d
   TF f;
   f.pow_mE = pe;
   f.pow_mbh = pb;
-  const double cov = gneiting_eval(a.k, spatial_dist(a.qx[p], a.qy[p], a.x[j], a.y[j]), f);  // kernel(q, p_j)
+  const double cov = gneiting_eval<true>(a.k, spatial_dist(a.qx[p], a.qy[p], a.x[j], a.y[j]), f);  // kernel(q, p_j)
   if (a.metric == 1) return __dsub_rn(1.0, fabs(__ddiv_rn(cov, a.s1)));
   const double tol = 1e-7 * a.s1;
   const double dj = a.resid[j], rq = a.rq[p];
@@ -263,7 +263,7 @@ __global__ void cond_solve_kernel(CondArgs a, bool vif) {
       TF f;
       f.pow_mE = pe;
       f.pow_mbh = pb;
-      double va = gneiting_eval(a.k, spatial_dist(a.qx[p], a.qy[p], a.x[ja], a.y[ja]), f);
+      double va = gneiting_eval<true>(a.k, spatial_dist(a.qx[p], a.qy[p], a.x[ja], a.y[ja]), f);
       if (vif && a.M > 0) va -= wdot(wq, a.W + static_cast<size_t>(ja) * a.ldm);
       c[i] = va;
       for (int b = 0; b <= i; ++b) {
@@ -271,7 +271,7 @@ __global__ void cond_solve_kernel(CondArgs a, bool vif) {
         a.lt.get2(a.tid[ja], a.tid[jb], pe, pb);
         f.pow_mE = pe;
         f.pow_mbh = pb;
-        double v = gneiting_eval(a.k, spatial_dist(a.x[ja], a.y[ja], a.x[jb], a.y[jb]), f);
+        double v = gneiting_eval<true>(a.k, spatial_dist(a.x[ja], a.y[ja], a.x[jb], a.y[jb]), f);
         if (vif && a.M > 0) v -= wdot(a.W + static_cast<size_t>(ja) * a.ldm, a.W + static_cast<size_t>(jb) * a.ldm);
         if (i == b) v += a.sigma2;
         C[i * K + b] = v;
@@ -350,7 +350,7 @@ __global__ void target_cross_kernel(const double* zx, const double* zy, const in
         TF f;
         f.pow_mE = pe;
         f.pow_mbh = pb;
-        v = gneiting_eval(k, spatial_dist(zx[j], zy[j], qx[p], qy[p]), f);
+        v = gneiting_eval<true>(k, spatial_dist(zx[j], zy[j], qx[p], qy[p]), f);
       }
       Up[static_cast<size_t>(p) * ldm + j] = v;
     }

@@ -266,7 +266,7 @@ __device__ __forceinline__ int closure_time_classes(const LagTable& lt, int pt, 
   return nc;
 }
 
-template <int MODE, bool HAS_W, int KS>
+template <int MODE, bool HAS_W, int KS, bool GEN = false>  // GEN: general-nu covariances (value modes)
 __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs a) {
   static_assert(KS >= 1 && KS <= 31, "closure must fit a warp");
   constexpr int NS = KS + 1;           // closure slots
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
       TF f;
       f.pow_mE = pe;
       f.pow_mbh = pb;
-      double v = gneiting_eval(a.k, spatial_dist(sx[w][sa], sy[w][sa], sx[w][sb], sy[w][sb]), f);
+      double v = gneiting_eval<GEN>(a.k, spatial_dist(sx[w][sa], sy[w][sa], sx[w][sb], sy[w][sb]), f);
       if (HAS_W) v = __dsub_rn(v, C[sa * LD + sb]);  // each pair slot is owned by one lane
       C[sa * LD + sb] = v;
       C[sb * LD + sa] = v;

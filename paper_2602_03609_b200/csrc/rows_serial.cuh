@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(64) vecchia_rows_serial_kernel(RowArgs a, doub
     TF f;
     f.pow_mE = pe;
     f.pow_mbh = pb;
-    double v = gneiting_eval(a.k, spatial_dist(a.x[p], a.y[p], a.x[q], a.y[q]), f);
+    double v = gneiting_eval<true>(a.k, spatial_dist(a.x[p], a.y[p], a.x[q], a.y[q]), f);
     if (HAS_W) {
       double s = 0.0;
       for (int j = 0; j < a.ldw; ++j) s = fma(a.W[static_cast<size_t>(p) * a.ldw + j], a.W[static_cast<size_t>(q) * a.ldw + j], s);

@@ -96,18 +96,19 @@ __device__ __forceinline__ void topm_emit(const TopM& e, int m_v, int m, int lan
 }
 
 // d_c(i, j) = sqrt(max(1 - |k(p_i, p_j) / sigma1_2|, 0))   (neighbors.cpp:37-43)
+template <bool GEN>
 __device__ __forceinline__ double dc_value(const DevKernel& k, double xi, double yi, double xj, double yj,
                                            double pow_mE, double pow_mbh) {
   TF f;
   f.pow_mE = pow_mE;
   f.pow_mbh = pow_mbh;
-  const double cov = gneiting_eval(k, spatial_dist(xi, yi, xj, yj), f);
+  const double cov = gneiting_eval<GEN>(k, spatial_dist(xi, yi, xj, yj), f);
   const double rho = __ddiv_rn(cov, k.s1);
   const double rad = __dsub_rn(1.0, fabs(rho));
   return __dsqrt_rn(rad < 0.0 ? 0.0 : rad);
 }
 
-template <int METRIC>  // 0: d_c, 1: euclid (squared scaled distance)
+template <int METRIC, bool GEN = false>  // 0: d_c, 1: euclid (squared scaled distance); GEN: general nu
 __global__ void __launch_bounds__(256) knn_kernel(SearchArgs a) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(256) knn_kernel(SearchArgs a) {
           const double xj = __ldg(&a.x[j]), yj = __ldg(&a.y[j]);
           if (METRIC == 0) {
             if (!a.blk_of) a.lt.get2(ti, __ldg(&a.tid[j]), pe, pbh);
-            d = dc_value(a.k, xi, yi, xj, yj, pe, pbh);
+            d = dc_value<GEN>(a.k, xi, yi, xj, yj, pe, pbh);
           } else {
             const double dx = __dsub_rn(sxi, __ddiv_rn(xj, a.ss));
             const double dy = __dsub_rn(syi, __ddiv_rn(yj, a.ss));

@@ -46,7 +46,7 @@ __global__ void sel_sigma_kernel(const double* zx, const double* zy, const int32
     TF f;
     f.pow_mE = pe;
     f.pow_mbh = pb;
-    double v = gneiting_eval(k, spatial_dist(zx[a], zy[a], zx[b], zy[b]), f);
+    double v = gneiting_eval<true>(k, spatial_dist(zx[a], zy[a], zx[b], zy[b]), f);
     if (r == c) {
       v = __dadd_rn(v, jit1);
       if (jit2 != 0.0) v = __dadd_rn(v, jit2);
@@ -185,6 +185,7 @@ __global__ void pad_rows_kernel(const double* L, int M, int ldL, double* Lp) {
 // the off-diagonal part c < r0 runs on the FP64 tensor pipe (mma.m8n8k4.f64 = the sequential fma
 // chain over its k, scripts/exp/dmma_order.cu) over cp.async-staged 16-wide chunks in increasing c;
 // the diagonal block is a column wavefront.  Warp w owns rows 16 (w/2).., columns 32 (w%2)...
+template <bool GEN>
 __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx, const double* zy, const int32_t* ztid,
                                                               int M, int ldm, const double* x, const double* y,
                                                               const int32_t* tid, int n, DevKernel k, LagTable lt,
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
             TF f;
             f.pow_mE = pe;
             f.pow_mbh = pb;
-            val = gneiting_eval(k, spatial_dist(zx[r], zy[r], sx[c], sy[c]), f);  // k(z_r, p_i)
+            val = gneiting_eval<GEN>(k, spatial_dist(zx[r], zy[r], sx[c], sy[c]), f);  // k(z_r, p_i)
           }
           acc[u][v][h] = val;
         }
@@ -551,7 +552,7 @@ __device__ __forceinline__ double tile_cmax(const DrArgs& a, int tminQ, int tmax
   }
   a.lt.get2(tmaxQ, tc0, pe_dummy, pb_max);
   double mat = 1.0;
-  if (a.k.nu_code >= 0) {
+  if (a.k.nu_code != kNuGeneral) {  // general nu: the bound 1 (correlations are <= 1)
     const double dx = fmax(0.0, fmax(T.bx0[ct] - qx1, qx0 - T.bx1[ct]));
     const double dy = fmax(0.0, fmax(T.by0[ct] - qy1, qy0 - T.by1[ct]));
     const double hmin = sqrt(dx * dx + dy * dy) * (1.0 - 1e-12);
@@ -656,7 +657,7 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
   cp_async_wait<0>();
   // pair test: can (i, j) still enter i's list?  k(i, j) in single precision with the fast exp:
   // |k_f - k| <= 1e-5 |k_f| + 1e-30 covers its ~10 roundings and the 2-ulp __expf (rel. ~1.3e-6).
-  int surv = 0;
+  int surv = a.k.nu_code == kNuGeneral ? 1 : 0;  // no single-precision general Matern: all go exact
   constexpr double kUnscale = 1.0 / (kW16Scale * kW16Scale);
   const float cf = static_cast<float>(a.k.c), s1f = static_cast<float>(a.k.s1);
   int iq[2];
@@ -714,6 +715,7 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
   return __syncthreads_or(surv) != 0;
 }
 
+template <bool GEN>
 __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
   extern __shared__ double sm[];
   // the staging ring and the distance tile are never live together
@@ -872,7 +874,7 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
                 if (tc1 >= ti) pe_min = 1.0; else a.lt.get2(ti, tc1, pe_min, pb0);
                 a.lt.get2(ti, tc0, pe0, pb_max);
                 double mat = 1.0;
-                if (a.k.nu_code >= 0) {
+                if (a.k.nu_code != kNuGeneral) {
                   const double xi = a.x[i], yi = a.y[i];
                   const double dx = fmax(0.0, fmax(T.bx0[ct] - xi, xi - T.bx1[ct]));
                   const double dy = fmax(0.0, fmax(T.by0[ct] - yi, yi - T.by1[ct]));
@@ -975,7 +977,7 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
                   TF f;
                   f.pow_mE = pe;
                   f.pow_mbh = pb;
-                  double rho = gneiting_eval(a.k, spatial_dist(a.x[i], a.y[i], a.x[j], a.y[j]), f);
+                  double rho = gneiting_eval<GEN>(a.k, spatial_dist(a.x[i], a.y[i], a.x[j], a.y[j]), f);
                   if (a.M > 0) rho = __dsub_rn(rho, acc[u][v][h]);
                   const double rad =
                       __dsub_rn(1.0, __ddiv_rn(fabs(rho), __dsqrt_rn(__dmul_rn(a.resid[i], a.resid[j]))));
@@ -1154,14 +1156,14 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
         }
         if (!ok) numeric_error("InducingBasis: inducing covariance is not positive definite");
         lap("w:sigma+chol");
-        STGP_CUDA(cudaFuncSetAttribute(whiten_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kWsmem)));
+        auto wkern = k.nu_code == kNuGeneral ? whiten_seq_kernel<true> : whiten_seq_kernel<false>;
+        STGP_CUDA(cudaFuncSetAttribute(wkern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kWsmem)));
         const int ldL = (M + kWKC - 1) / kWKC * kWKC;
         Lp.alloc(static_cast<size_t>(M) * ldL);
         ProfRegion prw(ctx, "dr_whiten_seq");
         pad_rows_kernel<<<grid_for(static_cast<long long>(M) * ldL), 256, 0, st>>>(L.get(), M, ldL, Lp.get());
         launched(ctx);
-        whiten_seq_kernel<<<ceil_div(n, kWB), kWthreads, kWsmem, st>>>(dzx.get(), dzy.get(), dzt.get(), M, ldm,
+        wkern<<<ceil_div(n, kWB), kWthreads, kWsmem, st>>>(dzx.get(), dzy.get(), dzt.get(), M, ldm,
                                                                       ds->x.get(), ds->y.get(), ds->tid.get(), n, k, lt,
                                                                       Lp.get(), ldL, W.get());
         launched(ctx);
@@ -1403,8 +1405,8 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
         a.stats = stats.get();
       }
       ProfRegion pr(ctx, "knn_dr");
-      STGP_CUDA(cudaFuncSetAttribute(knn_dr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kDrSmem)));
+      auto dkern = a.k.nu_code == kNuGeneral ? knn_dr_kernel<true> : knn_dr_kernel<false>;
+      STGP_CUDA(cudaFuncSetAttribute(dkern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kDrSmem)));
       // ranks shard the queries by whole time buckets (contiguous rows), balanced by row count;
       // candidates (W, tiles) are replicated and the rows gathered afterwards
       int b0 = 0, b1 = nbucket;
@@ -1420,7 +1422,7 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
       a.tile0 = btile0[static_cast<size_t>(b0)];
       const int nt = btile0[static_cast<size_t>(b1)] - a.tile0;
       if (nt > 0) {
-        knn_dr_kernel<<<nt, kDrThreads, kDrSmem, st>>>(a);
+        dkern<<<nt, kDrThreads, kDrSmem, st>>>(a);
         launched(ctx);
       }
       gather_rows(ctx, nb->idx.get(), nb->dist.get(), n, m_v, bstart[static_cast<size_t>(b0)],

@@ -90,6 +90,7 @@ double vecchia_nll(stgp_structure* s) {
 
 void vecchia_nll_grad(stgp_structure* s, double* nll, double* grad) {
   require_obs(s, "nll_grad");
+  require_analytic_grad(s->th);
   prepare_tables(s);
   std::vector<double> tot = run_rows(s, kModeGrad, nullptr, 0, s->th.sigma2);
   allreduce_host(s->ds->ctx, tot);
