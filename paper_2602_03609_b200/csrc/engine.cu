@@ -570,8 +570,6 @@ std::vector<double> run_rows_args(stgp_structure* s, int mode, RowArgs& a) {
 #undef STGP_ROWS_KS
 #undef STGP_ROWS
     } else {
-      if (mode == kModeVifGrad)
-        config_error("VIF gradient supports neighbour sets of size <= 31 (warp-per-row kernel)");
       const int threads = 64;
       blocks = std::max(1, std::min(ceil_div(rows, threads), 64));
       const size_t K = static_cast<size_t>(s->m_v);
@@ -582,7 +580,8 @@ std::vector<double> run_rows_args(stgp_structure* s, int mode, RowArgs& a) {
 #define STGP_ROWS(M, HW) vecchia_rows_serial_kernel<M, HW><<<blocks, threads, 0, ctx->stream>>>(a, s->scratch.get())
       if (mode == kModeBuild) { if (hw) STGP_ROWS(kModeBuild, true); else STGP_ROWS(kModeBuild, false); }
       else if (mode == kModeNll) { if (hw) STGP_ROWS(kModeNll, true); else STGP_ROWS(kModeNll, false); }
-      else { if (hw) STGP_ROWS(kModeGrad, true); else STGP_ROWS(kModeGrad, false); }
+      else if (mode == kModeGrad) { if (hw) STGP_ROWS(kModeGrad, true); else STGP_ROWS(kModeGrad, false); }
+      else STGP_ROWS(kModeVifGrad, true);
 #undef STGP_ROWS
     }
   }
@@ -989,7 +988,7 @@ static stgp_neighbors* run_search(stgp_dataset* ds, int metric, const Params* th
                                   double ts) {
   stgp_ctx* ctx = ds->ctx;
   if (m_v < 0) config_error("m_v must be >= 0");
-  if (m_v > 32) config_error("neighbour search supports m_v <= 32 on the device");
+  if (m_v > kMaxSearchM) config_error("neighbour search supports m_v <= 128 on the device");
   auto nb = std::make_unique<stgp_neighbors>();
   nb->ctx = ctx;
   nb->n = ds->n;
@@ -1046,12 +1045,24 @@ static stgp_neighbors* run_search(stgp_dataset* ds, int metric, const Params* th
     nb->idx.upload(neg.data(), total, ctx->stream);
   } else if (metric == STGP_METRIC_DC) {
     ProfRegion pr(ctx, "knn_dc");
-    if (a.k.nu_code == kNuGeneral) knn_kernel<0, true><<<blocks, 256, 0, ctx->stream>>>(a);
-    else knn_kernel<0><<<blocks, 256, 0, ctx->stream>>>(a);
+    const bool gen = a.k.nu_code == kNuGeneral;
+    // list slots per lane: m_v <= 32 R
+    if (m_v <= 32) {
+      if (gen) knn_kernel<0, true><<<blocks, 256, 0, ctx->stream>>>(a);
+      else knn_kernel<0><<<blocks, 256, 0, ctx->stream>>>(a);
+    } else if (m_v <= 64) {
+      if (gen) knn_kernel<0, true, 2><<<blocks, 256, 0, ctx->stream>>>(a);
+      else knn_kernel<0, false, 2><<<blocks, 256, 0, ctx->stream>>>(a);
+    } else {
+      if (gen) knn_kernel<0, true, 4><<<blocks, 256, 0, ctx->stream>>>(a);
+      else knn_kernel<0, false, 4><<<blocks, 256, 0, ctx->stream>>>(a);
+    }
     ++ctx->launches;
   } else {
     ProfRegion pr(ctx, "knn_euclid");
-    knn_kernel<1><<<blocks, 256, 0, ctx->stream>>>(a);
+    if (m_v <= 32) knn_kernel<1><<<blocks, 256, 0, ctx->stream>>>(a);
+    else if (m_v <= 64) knn_kernel<1, false, 2><<<blocks, 256, 0, ctx->stream>>>(a);
+    else knn_kernel<1, false, 4><<<blocks, 256, 0, ctx->stream>>>(a);
     ++ctx->launches;
   }
   STGP_LAUNCH_CHECK();

@@ -23,6 +23,7 @@ TF host_factors(const Params& p, double u);          // covariance.cpp:94-113
 void host_grad00(const Params& p, double g[6]);      // GneitingKernel::grad(0, 0)
 void require_analytic_grad(const Params& p);        // NumericError for general nu (covariance.cpp:79-87)
 DevKernel dev_kernel(const Params& p);
+constexpr int kMaxSearchM = 128;  // neighbour lists of up to 4 slots per lane (search.cuh topl_*)
 uint64_t mix_seed(uint64_t seed, uint64_t stream);   // types.hpp:65-70
 
 // Distinct-time groups of one computation (data times, then inducing times,

@@ -1,5 +1,6 @@
 // Generic per-row path for conditioning sets larger than a warp (k > 31), e.g.
-// the full-conditioning exactness tests (test_approximations.cpp:78-142).
+// the full-conditioning exactness tests (test_approximations.cpp:78-142); all four modes, including
+// the VIF gradient's per-row pass.
 // One thread per row, the k x k block in a per-thread global scratch slab.
 // Same semantics as rows.cuh; throughput is irrelevant at these sizes.
 #pragma once
@@ -117,9 +118,33 @@ __global__ void __launch_bounds__(64) vecchia_rows_serial_kernel(RowArgs a, doub
     double u = a.r[i];
     for (int p = 0; p < k; ++p) u -= A[p] * a.r[N[p]];
     tot[0] += log(D) + u * u / D;
-    if (MODE != kModeGrad) continue;
-    for (int p = 0; p < k; ++p) rn[p] = a.r[N[p]];
-    solve(rn, wv);
+    if (MODE != kModeGrad && MODE != kModeVifGrad) continue;
+    double cd, cu;
+    if (MODE == kModeVifGrad) {
+      // Rv = C^{-1} vrow_N with vrow_p = (W_{N_p} . X_i + Bz_i z_{N_p}) / D_i, and
+      // Phi_i = c0 a~a~' - sym(a~ Rv')   (approximations.cpp:616-661; rows.cuh kModeVifGrad)
+      const double Dst = a.D_in[i], uz = a.Bz[i];
+      const double* xi = a.X + static_cast<size_t>(i) * a.ldw;
+      for (int p = 0; p < k; ++p) {
+        const double* wp = a.W + static_cast<size_t>(N[p]) * a.ldw;
+        double ga = 0.0;
+        for (int j = 0; j < a.ldw; ++j) ga = fma(wp[j], xi[j], ga);
+        rn[p] = (ga + uz * a.z[N[p]]) / Dst;
+      }
+      solve(rn, wv);
+      const double* vi = a.Vp + static_cast<size_t>(i) * a.ldw;
+      double aGa = 0.0;
+      for (int j = 0; j < a.ldw; ++j) aGa = fma(vi[j], xi[j], aGa);
+      cd = 0.5 * (1.0 / Dst - (aGa + uz * uz) / (Dst * Dst));
+      cu = 1.0;
+      a.c0_out[i] = cd;
+      for (int p = 0; p < K; ++p) a.Rv_out[static_cast<size_t>(i) * K + p] = p < k ? wv[p] : 0.0;
+    } else {
+      for (int p = 0; p < k; ++p) rn[p] = a.r[N[p]];
+      solve(rn, wv);
+      cd = 0.5 * (1.0 / D - u * u / (D * D));
+      cu = u / D;
+    }
     double aa = 0.0, aw = 0.0;
     for (int p = 0; p < k; ++p) {
       aa += A[p] * A[p];
@@ -129,7 +154,6 @@ __global__ void __launch_bounds__(64) vecchia_rows_serial_kernel(RowArgs a, doub
     }
     tcl[k] = 1.0;
     wcl[k] = 0.0;
-    const double cd = 0.5 * (1.0 / D - u * u / (D * D)), cu = u / D;
     double g[6] = {0, 0, 0, 0, 0, 0};
     for (int p = 1; p <= k; ++p) {
       const int pp = p < k ? N[p] : i;

@@ -95,6 +95,111 @@ __device__ __forceinline__ void topm_emit(const TopM& e, int m_v, int m, int lan
   }
 }
 
+// Lists longer than a warp (32 < m <= 32 R): slot s = 32 r + lane lives in e[r] of that lane, slots
+// ascending by (d, j).  For R = 1 these reduce to topm_insert / topm_emit above.
+template <int R>
+__device__ __forceinline__ void topl_init(TopM (&e)[R]) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) e[r] = TopM{__longlong_as_double(0x7ff0000000000000LL), INT_MAX};
+}
+
+template <int R>
+__device__ __forceinline__ void topl_worst(const TopM (&e)[R], int m, double& wd, int& wj) {
+  const int rw = (m - 1) >> 5;
+  double d = e[0].d;
+  int j = e[0].j;
+#pragma unroll
+  for (int r = 1; r < R; ++r)
+    if (r == rw) {
+      d = e[r].d;
+      j = e[r].j;
+    }
+  wd = __shfl_sync(kFull, d, (m - 1) & 31);
+  wj = __shfl_sync(kFull, j, (m - 1) & 31);
+}
+
+template <int R>
+__device__ __forceinline__ void topl_insert(TopM (&e)[R], int m, unsigned mask, double cd, int cj, int lane) {
+  while (mask) {
+    const int src = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const double d = __shfl_sync(kFull, cd, src);
+    const int j = __shfl_sync(kFull, cj, src);
+    double wd;
+    int wj;
+    topl_worst(e, m, wd, wj);
+    if (!lex_less(d, j, wd, wj)) continue;
+    int pos = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) pos += __popc(__ballot_sync(kFull, 32 * r + lane < m && lex_less(e[r].d, e[r].j, d, j)));
+    double ud[R];
+    int uj[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      ud[r] = __shfl_up_sync(kFull, e[r].d, 1);
+      uj[r] = __shfl_up_sync(kFull, e[r].j, 1);
+    }
+#pragma unroll
+    for (int r = 1; r < R; ++r) {  // slot 32 r takes slot 32 r - 1 (lane 31 of the row below)
+      const double ld = __shfl_sync(kFull, e[r - 1].d, 31);
+      const int lj = __shfl_sync(kFull, e[r - 1].j, 31);
+      if (lane == 0) {
+        ud[r] = ld;
+        uj[r] = lj;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int slot = 32 * r + lane;
+      if (slot < m) {
+        if (slot == pos) {
+          e[r].d = d;
+          e[r].j = j;
+        } else if (slot > pos) {
+          e[r].d = ud[r];
+          e[r].j = uj[r];
+        }
+      }
+    }
+  }
+}
+
+// Write the list ascending by index; distances (optional) ascending by (d, j).
+template <int R>
+__device__ __forceinline__ void topl_emit(const TopM (&e)[R], int m_v, int m, int lane, int32_t* orow, double* drow) {
+  bool valid[R];
+  int rank[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    valid[r] = 32 * r + lane < m && e[r].j != INT_MAX;
+    rank[r] = 0;
+  }
+#pragma unroll
+  for (int rr = 0; rr < R; ++rr)
+    for (int s = 0; s < 32; ++s) {
+      const int oj = __shfl_sync(kFull, e[rr].j, s);
+      const bool ov = __shfl_sync(kFull, valid[rr] ? 1 : 0, s) != 0;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (ov && oj < e[r].j) ++rank[r];
+    }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int slot = 32 * r + lane;
+    if (slot < m_v) {
+      orow[slot] = -1;
+      if (drow) drow[slot] = __longlong_as_double(0x7ff8000000000000LL);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (valid[r]) {
+      orow[rank[r]] = e[r].j;
+      if (drow) drow[32 * r + lane] = e[r].d;
+    }
+}
+
 // d_c(i, j) = sqrt(max(1 - |k(p_i, p_j) / sigma1_2|, 0))   (neighbors.cpp:37-43)
 template <bool GEN>
 __device__ __forceinline__ double dc_value(const DevKernel& k, double xi, double yi, double xj, double yj,
@@ -108,14 +213,16 @@ __device__ __forceinline__ double dc_value(const DevKernel& k, double xi, double
   return __dsqrt_rn(rad < 0.0 ? 0.0 : rad);
 }
 
-template <int METRIC, bool GEN = false>  // 0: d_c, 1: euclid (squared scaled distance); GEN: general nu
+// METRIC 0: d_c, 1: euclid (squared scaled distance); GEN: general nu; R: list slots per lane (m_v <= 32 R)
+template <int METRIC, bool GEN = false, int R = 1>
 __global__ void __launch_bounds__(256) knn_kernel(SearchArgs a) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int i = a.q_begin + gw; i < a.q_end; i += nw) {
     const int m = a.m_v < i ? a.m_v : i;
-    TopM e{__longlong_as_double(0x7ff0000000000000LL), INT_MAX};
+    TopM e[R];
+    topl_init(e);
     const double xi = a.x[i], yi = a.y[i];
     double sxi = 0, syi = 0, sti = 0;
     if (METRIC == 1) {
@@ -135,13 +242,17 @@ __global__ void __launch_bounds__(256) knn_kernel(SearchArgs a) {
         eend = min(a.blk_start[b + 1], i);
         if (METRIC == 0) {
           a.lt.get2(ti, a.blk_tid[b], pe, pbh);
-          const double wd = __shfl_sync(kFull, e.d, m - 1);
+          double wd;
+          int wj;
+          topl_worst(e, m, wd, wj);
           // exact prune: every d^2 in the block >= 1 - T^{-(delta+beta)} - O(eps)
           if (wd != __longlong_as_double(0x7ff0000000000000LL) && (1.0 - pe) - 1e-12 > wd * wd) continue;
         } else {
           const double dt = __dsub_rn(sti, __ddiv_rn(a.t[s], a.ts));
           dt2 = __dmul_rn(dt, dt);
-          const double wd = __shfl_sync(kFull, e.d, m - 1);
+          double wd;
+          int wj;
+          topl_worst(e, m, wd, wj);
           if (dt2 > wd) continue;
         }
       } else {
@@ -162,14 +273,15 @@ __global__ void __launch_bounds__(256) knn_kernel(SearchArgs a) {
             d = __dadd_rn(__dadd_rn(dt2, __dmul_rn(dx, dx)), __dmul_rn(dy, dy));
           }
         }
-        const double wd = __shfl_sync(kFull, e.d, m - 1);
-        const int wj = __shfl_sync(kFull, e.j, m - 1);
+        double wd;
+        int wj;
+        topl_worst(e, m, wd, wj);
         const unsigned acc = __ballot_sync(kFull, j < eend && lex_less(d, j, wd, wj));
-        if (acc) topm_insert(e, m, acc, d, j, lane);
+        if (acc) topl_insert(e, m, acc, d, j, lane);
       }
     }
     const size_t o = static_cast<size_t>(i - a.q_begin) * a.m_v;
-    topm_emit(e, a.m_v, m, lane, a.out + o, a.dist ? a.dist + o : nullptr);
+    topl_emit(e, a.m_v, m, lane, a.out + o, a.dist ? a.dist + o : nullptr);
   }
 }
 

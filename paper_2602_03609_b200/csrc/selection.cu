@@ -576,8 +576,10 @@ __device__ __forceinline__ double tile_cmax(const DrArgs& a, int tminQ, int tmax
 // so G equals the oracle's chain exactly.  W chunks of kKC rows are staged by cp.async in a
 // kStages ring; warp w owns the 16 x 32 sub-tile (rows 16 (w/2), cols 32 (w%2)).
 constexpr size_t kDrStageDoubles = 2 * kQT * kKS;
-constexpr size_t kDrSmem =
-    sizeof(double) * (kStages * kDrStageDoubles + kQT * 32) + sizeof(int) * kQT * 32;
+// per-query lists of 32 LR slots (m_v <= 32 LR) follow the ring
+constexpr size_t dr_smem(int LR) {
+  return sizeof(double) * (kStages * kDrStageDoubles + kQT * 32 * LR) + sizeof(int) * kQT * 32 * LR;
+}
 static_assert(kStages * kDrStageDoubles >= kQT * (kCT + 1), "distance tile aliases the stages");
 
 // Certified half-precision filter for one (query tile, candidate tile) pair.  G~ = W16_Q^T W16_C on
@@ -599,8 +601,9 @@ __device__ __forceinline__ void hmma_16816(float (&c)[4], uint32_t a0, uint32_t 
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+template <int kL>
 __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* qidx, const int* cidx, const int* qm,
-                                     const double (*topd)[32], const int (*topj)[32]) {
+                                     const double (*topd)[kL], const int (*topj)[kL]) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int grp = lane >> 2, tig = lane & 3, wr = wid >> 1, wc = wid & 1;
   float hc[4][4];
@@ -715,14 +718,15 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
   return __syncthreads_or(surv) != 0;
 }
 
-template <bool GEN>
+template <bool GEN, int LR>  // GEN: general nu; LR: list slots per lane (m_v <= 32 LR)
 __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
+  constexpr int kL = 32 * LR;
   extern __shared__ double sm[];
   // the staging ring and the distance tile are never live together
   double* ring = sm;
   double (*sd)[kCT + 1] = reinterpret_cast<double (*)[kCT + 1]>(sm);
-  double (*topd)[32] = reinterpret_cast<double (*)[32]>(sm + kStages * kDrStageDoubles);
-  int (*topj)[32] = reinterpret_cast<int (*)[32]>(sm + kStages * kDrStageDoubles + kQT * 32);
+  double (*topd)[kL] = reinterpret_cast<double (*)[kL]>(sm + kStages * kDrStageDoubles);
+  int (*topj)[kL] = reinterpret_cast<int (*)[kL]>(sm + kStages * kDrStageDoubles + kQT * kL);
   __shared__ int qidx[kQT], cidx[kCT], qm[kQT], qemit[kQT];
   __shared__ double s_dmax[kDrThreads / 32];
   __shared__ int s_surv[32], s_nsurv;
@@ -733,9 +737,9 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int grp = lane >> 2, tig = lane & 3;
   const int wr = wid >> 1, wc = wid & 1;  // warp sub-tile: rows 16 wr.., cols 32 wc..
-  for (int e = tid; e < kQT * 32; e += kDrThreads) {
-    topd[e / 32][e % 32] = __longlong_as_double(0x7ff0000000000000LL);
-    topj[e / 32][e % 32] = INT_MAX;
+  for (int e = tid; e < kQT * kL; e += kDrThreads) {
+    topd[e / kL][e % kL] = __longlong_as_double(0x7ff0000000000000LL);
+    topj[e / kL][e % kL] = INT_MAX;
   }
   const int qp0 = T.off[qt], qn = T.off[qt + 1] - qp0;
   if (tid < kQT) {
@@ -747,8 +751,8 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
   }
   for (int g = tid; g < T.G; g += kDrThreads) sAQ[g] = T.A[static_cast<size_t>(qt) * T.G + g];
   __syncthreads();
-  for (int e = tid; e < kQT * 32; e += kDrThreads) {
-    const int qq = e / 32, l = e % 32, i = qidx[qq];
+  for (int e = tid; e < kQT * kL; e += kDrThreads) {
+    const int qq = e / kL, l = e % kL, i = qidx[qq];
     if (i >= 0 && a.degen[i] && l < qemit[qq]) {
       topd[qq][l] = 1.0;
       topj[qq][l] = l;
@@ -993,22 +997,28 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
           const int i = qidx[qq];
           const int m = qm[qq];
           if (m <= 0) continue;
-          TopM e{topd[qq][lane], topj[qq][lane]};
+          TopM e[LR];
+#pragma unroll
+          for (int r = 0; r < LR; ++r) e[r] = TopM{topd[qq][32 * r + lane], topj[qq][32 * r + lane]};
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int cc = lane + 32 * h;
             const int j = cidx[cc];
             const double dd = sd[qq][cc];
-            const double wd = __shfl_sync(kFull, e.d, m - 1);
-            const int wj = __shfl_sync(kFull, e.j, m - 1);
+            double wd;
+            int wj;
+            topl_worst(e, m, wd, wj);
             const unsigned acc2 = __ballot_sync(kFull, j >= 0 && j < i && lex_less(dd, j, wd, wj));
             if (acc2) {
-              topm_insert(e, m, acc2, dd, j, lane);
+              topl_insert(e, m, acc2, dd, j, lane);
               inserted = true;
             }
           }
-          topd[qq][lane] = e.d;
-          topj[qq][lane] = e.j;
+#pragma unroll
+          for (int r = 0; r < LR; ++r) {
+            topd[qq][32 * r + lane] = e[r].d;
+            topj[qq][32 * r + lane] = e[r].j;
+          }
         }
         if (a.stats) {  // diagnostics: evaluated tiles that changed some list
           const int any = __syncthreads_or(inserted ? 1 : 0);
@@ -1024,8 +1034,10 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
     const int i = qidx[qq];
     if (i < 0) continue;
     const int m = qemit[qq];
-    TopM e{topd[qq][lane], topj[qq][lane]};
-    topm_emit(e, a.m_v, m, lane, a.out + static_cast<size_t>(i) * a.m_v,
+    TopM e[LR];
+#pragma unroll
+    for (int r = 0; r < LR; ++r) e[r] = TopM{topd[qq][32 * r + lane], topj[qq][32 * r + lane]};
+    topl_emit(e, a.m_v, m, lane, a.out + static_cast<size_t>(i) * a.m_v,
               a.dist ? a.dist + static_cast<size_t>(i) * a.m_v : nullptr);
   }
 }
@@ -1068,7 +1080,7 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
   auto frees_clk = std::chrono::steady_clock::now();
   {
     if (m_v < 0) config_error("m_v must be >= 0");
-    if (m_v > 32) config_error("neighbour search supports m_v <= 32 on the device");
+    if (m_v > kMaxSearchM) config_error("neighbour search supports m_v <= 128 on the device");
     stgp_ctx* ctx = ds->ctx;
     cudaStream_t st = ctx->stream;
     const int n = ds->n, M = static_cast<int>(zxyt.size() / 3);
@@ -1405,8 +1417,13 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
         a.stats = stats.get();
       }
       ProfRegion pr(ctx, "knn_dr");
-      auto dkern = a.k.nu_code == kNuGeneral ? knn_dr_kernel<true> : knn_dr_kernel<false>;
-      STGP_CUDA(cudaFuncSetAttribute(dkern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kDrSmem)));
+      const bool gen = a.k.nu_code == kNuGeneral;
+      const int lr = m_v <= 32 ? 1 : (m_v <= 64 ? 2 : 4);
+      auto dkern = lr == 1 ? (gen ? knn_dr_kernel<true, 1> : knn_dr_kernel<false, 1>)
+                           : lr == 2 ? (gen ? knn_dr_kernel<true, 2> : knn_dr_kernel<false, 2>)
+                                     : (gen ? knn_dr_kernel<true, 4> : knn_dr_kernel<false, 4>);
+      const size_t dsmem = dr_smem(lr);
+      STGP_CUDA(cudaFuncSetAttribute(dkern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsmem)));
       // ranks shard the queries by whole time buckets (contiguous rows), balanced by row count;
       // candidates (W, tiles) are replicated and the rows gathered afterwards
       int b0 = 0, b1 = nbucket;
@@ -1422,7 +1439,7 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
       a.tile0 = btile0[static_cast<size_t>(b0)];
       const int nt = btile0[static_cast<size_t>(b1)] - a.tile0;
       if (nt > 0) {
-        dkern<<<nt, kDrThreads, kDrSmem, st>>>(a);
+        dkern<<<nt, kDrThreads, dsmem, st>>>(a);
         launched(ctx);
       }
       gather_rows(ctx, nb->idx.get(), nb->dist.get(), n, m_v, bstart[static_cast<size_t>(b0)],
