@@ -244,6 +244,66 @@ __device__ __forceinline__ void gneiting_grad_fast(const DevKernel& k, double in
   g[5] = -f.log_T * base * M;
 }
 
+// ---- branch-free pieces for the likelihood-gradient pair loops (1e-8 tolerance) ----
+// No special-case paths, so the scheduler can interleave several pairs' dependency chains.
+
+// sqrt(s), s >= 0, within ~1 ulp: approximate rsqrt, two Newton steps, one residual correction;
+// s below DBL_MIN maps to 0 (a distance under 1e-154: the kernel is at its x = 0 value anyway).
+__device__ __forceinline__ double sqrt_nr(double s) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
+  const double hs = 0.5 * s;
+  y = y * fma(-hs, y * y, 1.5);
+  y = y * fma(-hs, y * y, 1.5);
+  double h = s * y;
+  h = fma(fma(-h, h, s), 0.5 * y, h);
+  return s >= 2.2250738585072014e-308 ? h : 0.0;
+}
+
+// exp(t) for t <= 0: glibc's table method without its special cases; t is clamped at -708 (results
+// below 3e-308 only ever scale gradient terms that are already negligible), within ~1 ulp otherwise.
+__device__ __forceinline__ double exp_nonpos(double t) {
+  t = fmax(t, -708.0);
+  double kd = fma(STGP_EXP_invln2N, t, STGP_EXP_shift);
+  const uint64_t ki = static_cast<uint64_t>(__double_as_longlong(kd));
+  kd -= STGP_EXP_shift;
+  const double r = fma(kd, STGP_EXP_negln2loN, fma(kd, STGP_EXP_negln2hiN, t));
+  const uint32_t idx = 2u * static_cast<uint32_t>(ki & 127u);
+  const double tail = __longlong_as_double(static_cast<long long>(__ldg(&kExpTab[idx])));
+  const uint64_t sbits = __ldg(&kExpTab[idx + 1]) + (ki << 45);
+  const double r2 = r * r;
+  const double tmp = fma(r2 * r2, fma(r, STGP_EXP_C5, STGP_EXP_C4), fma(r2, fma(r, STGP_EXP_C3, STGP_EXP_C2), tail + r));
+  const double scale = __longlong_as_double(static_cast<long long>(sbits));
+  return fma(scale, tmp, scale);
+}
+
+// Matern M = (1 + m1 x + m2 x^2) e and M' = -(p0 + p1 x + p2 x^2) e for the closed forms
+struct MaternPoly {
+  double m1, m2, p0, p1, p2;
+};
+__host__ __device__ inline MaternPoly matern_poly(int nu_code) {
+  if (nu_code == 0) return MaternPoly{0.0, 0.0, 1.0, 0.0, 0.0};
+  if (nu_code == 1) return MaternPoly{1.0, 0.0, 0.0, 1.0, 0.0};
+  return MaternPoly{1.0, 1.0 / 3.0, 0.0, 1.0 / 3.0, 1.0 / 3.0};
+}
+
+// gneiting_grad_fast from the squared distance, branch free (same formulas, ~ulp-level differences)
+__device__ __forceinline__ void gneiting_grad_bf(const DevKernel& k, const MaternPoly& mp, double inv_c, double s,
+                                                 const TF& f, double g[6]) {
+  const double x = k.c * sqrt_nr(s) * f.pow_mbh;
+  const double e = exp_nonpos(-x);
+  const double M = fma(fma(mp.m2, x, mp.m1), x, 1.0) * e;
+  const double Mp = -fma(fma(mp.p2, x, mp.p1), x, mp.p0) * e;
+  const double base = k.s1 * f.pow_mE;
+  g[0] = f.pow_mE * M;
+  const double dC_dT = base * f.inv_T * (-k.E * M - 0.5 * k.beta * x * Mp);
+  g[1] = dC_dT * f.u2a;
+  g[3] = dC_dT * 2.0 * k.a * f.u2a_logu;
+  g[2] = base * Mp * x * inv_c;
+  g[4] = -f.log_T * base * (M + 0.5 * x * Mp);
+  g[5] = -f.log_T * base * M;
+}
+
 // Temporal-factor table indexed by time-id pairs (host-computed with glibc).
 struct TFTable {
   const TF* tab;  // nT * nT

@@ -398,13 +398,15 @@ __global__ void __launch_bounds__(256) upair_grad_kernel(int c0, int c1, int M, 
                                                          const double* y, const int32_t* tid, DevKernel k, double inv_c,
                                                          LagTable lt, const double* Om, double* part) {
   double g[6] = {0, 0, 0, 0, 0, 0};
+  const MaternPoly mp = matern_poly(k.nu_code);
   for (int i = c0 + blockIdx.x; i < c1; i += gridDim.x) {
     const double xi = x[i], yi = y[i];
     const int ti = tid[i];
     for (int j = threadIdx.x; j < M; j += blockDim.x) {
       const TF f = lt.get(z.ztid[j], ti);
       double kg[6];
-      gneiting_grad_fast(k, inv_c, spatial_dist(z.zx[j], z.zy[j], xi, yi), f, kg);
+      const double dx = z.zx[j] - xi, dy = z.zy[j] - yi;
+      gneiting_grad_bf(k, mp, inv_c, fma(dx, dx, dy * dy), f, kg);
       const double wgt = Om[static_cast<size_t>(i) * ldm + j];
 #pragma unroll
       for (int q = 0; q < 6; ++q) g[q] = fma(wgt, kg[q], g[q]);
@@ -427,6 +429,7 @@ __global__ void __launch_bounds__(256) upair_grad_kernel(int c0, int c1, int M, 
 __global__ void __launch_bounds__(256) sigma_pair_grad_kernel(int M, int ldm, ZPts z, DevKernel k, double inv_c,
                                                               LagTable lt, const double* Ws, double* part) {
   double g[6] = {0, 0, 0, 0, 0, 0};
+  const MaternPoly mp = matern_poly(k.nu_code);
   const long long total = static_cast<long long>(M) * M;
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -436,7 +439,8 @@ __global__ void __launch_bounds__(256) sigma_pair_grad_kernel(int M, int ldm, ZP
                                 : Ws[static_cast<size_t>(j2) * ldm + j1] + Ws[static_cast<size_t>(j1) * ldm + j2];
     const TF f = lt.get(z.ztid[j1], z.ztid[j2]);
     double kg[6];
-    gneiting_grad_fast(k, inv_c, spatial_dist(z.zx[j1], z.zy[j1], z.zx[j2], z.zy[j2]), f, kg);
+    const double dx = z.zx[j1] - z.zx[j2], dy = z.zy[j1] - z.zy[j2];
+    gneiting_grad_bf(k, mp, inv_c, fma(dx, dx, dy * dy), f, kg);
 #pragma unroll
     for (int q = 0; q < 6; ++q) g[q] = fma(wgt, kg[q], g[q]);
   }
