@@ -92,7 +92,48 @@ __global__ void __launch_bounds__(256) slice_rows_kernel(long long nrows, int k,
 // segment) and 8 x 32 columns r (warps); each thread keeps its 32 values of one row in registers.
 constexpr int kSlCols = 256;  // columns r per block; L is a multiple
 
-// per-(chunk, row) maxima: atomicMax on the bit patterns of non-negative doubles (order-preserving)
+// per-(chunk, row) maxima: atomicMax on the bit patterns of non-negative doubles (order-preserving).
+// A block takes 256 consecutive reduction rows r (one chunk: L is a multiple of 256) and walks the m
+// product rows j in segments of 256: each warp reads its 32 rows r as 2 KB contiguous runs, so the
+// column-major source streams through DRAM in whole pages (the 256-byte column pieces of a j-tiled
+// walk ran at ~3.3 TB/s); warp partials meet in shared memory, one global atomic per (block, j).
+constexpr int kMaxRowsPerBlock = 256;
+__global__ void __launch_bounds__(256) colmax_rows_kernel(int m, long long n, int L, const double* __restrict__ A,
+                                                          int lda, const double* __restrict__ colD,
+                                                          unsigned long long* __restrict__ maxbits) {
+  __shared__ double part[8][256];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long r0 = static_cast<long long>(blockIdx.x) * kMaxRowsPerBlock;
+  const int c = static_cast<int>(r0 / L);
+  for (int j0 = 0; j0 < m; j0 += 256) {
+    double mx[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) mx[u] = 0.0;
+    for (int q = 0; q < 32; ++q) {
+      const long long r = r0 + w * 32 + q;
+      if (r >= n) break;
+      const double f = colD ? fabs(__ldg(&colD[r])) : 1.0;
+      const double* row = A + r * lda + j0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = 32 * u + lane;
+        if (j0 + j < m) mx[u] = fmax(mx[u], fabs(__ldg(&row[j])) * f);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) part[w][32 * u + lane] = mx[u];
+    __syncthreads();
+    {
+      const int j = threadIdx.x;
+      double v = part[0][j];
+#pragma unroll
+      for (int ww = 1; ww < 8; ++ww) v = fmax(v, part[ww][j]);
+      if (j0 + j < m && v > 0.0) atomicMax(&maxbits[static_cast<size_t>(c) * m + j0 + j], __double_as_longlong(v));
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(256) colmax_kernel(int m, long long n, int L, const double* __restrict__ A, int lda,
                                                      const double* __restrict__ colD,
                                                      unsigned long long* __restrict__ maxbits) {
@@ -117,17 +158,19 @@ __global__ void __launch_bounds__(256) colmax_kernel(int m, long long n, int L, 
 // out[((c * m + j) * S + s - 1) * L + rl] and/or out_rev[((c * m + j) * S + S - s) * L + rl].  The
 // digits of the block's 32 rows x 256 columns are staged in shared memory and leave as 256-byte
 // row runs (full sectors, no partial-sector write-backs).
-constexpr int kSlRow = kSlCols + 16;  // staged row pitch (bytes): spreads the 16-byte stores over banks
-template <int S>
+template <int H>  // rows r per block = 128 H
+constexpr int sl_row() { return 128 * H + 16; }  // staged row pitch (bytes): spreads the 16-byte stores over banks
+template <int S, int H>
 __global__ void __launch_bounds__(256) slice_cols_kernel(int m, long long n, int L, const double* __restrict__ A,
                                                          int lda, const double* __restrict__ colD,
                                                          const unsigned long long* __restrict__ maxbits,
                                                          int8_t* __restrict__ out, int8_t* __restrict__ out_rev,
                                                          double* __restrict__ scale) {
-  extern __shared__ __align__(16) unsigned char sd[];  // S * 32 * kSlRow bytes
+  constexpr int kRB = 128 * H, kRow = sl_row<H>();
+  extern __shared__ __align__(16) unsigned char sd[];  // S * 32 * kRow bytes
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const long long rc0 = static_cast<long long>(blockIdx.x) * kSlCols;
-  const long long rb = rc0 + w * 32;
+  const long long rc0 = static_cast<long long>(blockIdx.x) * kRB;
+  const long long rb = rc0 + w * 16 * H;
   const int j0 = blockIdx.y * 32, j = j0 + lane;
   const int c = static_cast<int>(rc0 / L);
   double inv = 0.0;
@@ -139,7 +182,7 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(int m, long long n, int
     inv = ldexp(1.0, -e);
   }
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < H; ++h) {
     Fixed q[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
@@ -158,17 +201,18 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(int m, long long n, int
       v4.y = pack4(digit<S>(q[4], s), digit<S>(q[5], s), digit<S>(q[6], s), digit<S>(q[7], s));
       v4.z = pack4(digit<S>(q[8], s), digit<S>(q[9], s), digit<S>(q[10], s), digit<S>(q[11], s));
       v4.w = pack4(digit<S>(q[12], s), digit<S>(q[13], s), digit<S>(q[14], s), digit<S>(q[15], s));
-      *reinterpret_cast<uint4*>(sd + ((s - 1) * 32 + lane) * kSlRow + w * 32 + 16 * h) = v4;
+      *reinterpret_cast<uint4*>(sd + ((s - 1) * 32 + lane) * kRow + w * 16 * H + 16 * h) = v4;
     }
   }
   __syncthreads();
-  // copy-out: 16 threads per (slice, row) run of 256 bytes
+  // copy-out: kRB / 16 threads per (slice, row) run of kRB bytes
+  constexpr int kPieces = kRB / 16;
   const size_t off = static_cast<size_t>(rc0 - static_cast<long long>(c) * L);
-  for (int e = threadIdx.x; e < S * 32 * 16; e += blockDim.x) {
-    const int row = e >> 4, piece = e & 15;
+  for (int e = threadIdx.x; e < S * 32 * kPieces; e += blockDim.x) {
+    const int row = e / kPieces, piece = e % kPieces;
     const int s = row / 32 + 1, jj = row - (s - 1) * 32;
     if (j0 + jj >= m) continue;
-    const uint4 v4 = *reinterpret_cast<const uint4*>(sd + row * kSlRow + piece * 16);
+    const uint4 v4 = *reinterpret_cast<const uint4*>(sd + row * kRow + piece * 16);
     const size_t base = (static_cast<size_t>(c) * m + j0 + jj) * S * static_cast<size_t>(L) + off + piece * 16;
     if (out) *reinterpret_cast<uint4*>(out + base + static_cast<size_t>(s - 1) * L) = v4;
     if (out_rev) *reinterpret_cast<uint4*>(out_rev + base + static_cast<size_t>(S - s) * L) = v4;
@@ -256,6 +300,22 @@ bool ozaki_for(int m) {
   return ozaki_enabled() && m >= min_m;
 }
 
+static int slice_halves() {
+  static const int h = [] {
+    const char* e = std::getenv("STGP_OZ_SLICE_H");  // tuning switch: rows per slicing block = 128 H (1 or 2)
+    return e && std::atoi(e) == 2 ? 2 : 1;
+  }();
+  return h;
+}
+
+static bool colmax_rows() {
+  static const bool on = [] {
+    const char* e = std::getenv("STGP_OZ_COLMAX_ROWS");  // A/B switch: 0 = the j-tiled colmax
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 static OzakiState* state(stgp_ctx* ctx) {
   if (!ctx->ozaki) ctx->ozaki = new OzakiState();
   return ctx->ozaki;
@@ -326,18 +386,31 @@ static void cols_product(stgp_ctx* ctx, int m, long long n, const double* A, int
   const dim3 grid(static_cast<unsigned>((n + kSlCols - 1) / kSlCols), (m + 31) / 32);
   // the slicer covers every chunk to its full length L: the padding columns [n, nch L) of the
   // last chunk enter the int8 products and must be zero digits (reused buffers hold old data)
-  const dim3 sgrid(static_cast<unsigned>(static_cast<long long>(nch) * L / kSlCols), (m + 31) / 32);
+  const int H = slice_halves();
+  const dim3 sgrid(static_cast<unsigned>(static_cast<long long>(nch) * L / (128 * H)), (m + 31) / 32);
   oz->maxbits.ensure(static_cast<size_t>(nch) * m);
   auto slice = [&](const double* X, int ldx, const double* f, int8_t* fwd, int8_t* rev, double* sc) {
     STGP_CUDA(cudaMemsetAsync(oz->maxbits.get(), 0, sizeof(unsigned long long) * nch * m, st));
-    colmax_kernel<<<grid, 256, 0, st>>>(m, n, L, X, ldx, f, oz->maxbits.get());
+    if (colmax_rows())
+      colmax_rows_kernel<<<static_cast<unsigned>((n + kMaxRowsPerBlock - 1) / kMaxRowsPerBlock), 256, 0, st>>>(
+          m, n, L, X, ldx, f, oz->maxbits.get());
+    else
+      colmax_kernel<<<grid, 256, 0, st>>>(m, n, L, X, ldx, f, oz->maxbits.get());
     launched(ctx);
     STGP_OZ_SWITCH(S, ({
-                     const int smem = kS * 32 * kSlRow;
-                     STGP_CUDA(cudaFuncSetAttribute(slice_cols_kernel<kS>,
-                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-                     slice_cols_kernel<kS><<<sgrid, 256, smem, st>>>(m, n, L, X, ldx, f, oz->maxbits.get(), fwd, rev,
-                                                                     sc);
+                     if (H == 1) {
+                       const int smem = kS * 32 * sl_row<1>();
+                       STGP_CUDA(cudaFuncSetAttribute(slice_cols_kernel<kS, 1>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                       slice_cols_kernel<kS, 1><<<sgrid, 256, smem, st>>>(m, n, L, X, ldx, f, oz->maxbits.get(), fwd,
+                                                                          rev, sc);
+                     } else {
+                       const int smem = kS * 32 * sl_row<2>();
+                       STGP_CUDA(cudaFuncSetAttribute(slice_cols_kernel<kS, 2>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                       slice_cols_kernel<kS, 2><<<sgrid, 256, smem, st>>>(m, n, L, X, ldx, f, oz->maxbits.get(), fwd,
+                                                                          rev, sc);
+                     }
                    }));
     launched(ctx);
   };
