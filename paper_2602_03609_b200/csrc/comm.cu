@@ -121,6 +121,17 @@ void gather_rows(stgp_ctx* ctx, int32_t* idx, double* dist, long long n, int m_v
   STGP_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+void allgather_cols(stgp_ctx* ctx, double* buf, size_t slab_doubles, long long n_cols, int ld) {
+  if (ctx->world == 1) return;
+  if (ctx->comm) {
+    const ncclResult_t r = ncclAllGather(buf + static_cast<size_t>(ctx->rank) * slab_doubles, buf, slab_doubles,
+                                         ncclDouble, reinterpret_cast<ncclComm_t>(ctx->comm), ctx->stream);
+    if (r != ncclSuccess) throw Error(kInternal, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    return;
+  }
+  allreduce_sum(ctx, buf, static_cast<size_t>(n_cols) * ld);
+}
+
 void shard_rows(const stgp_ctx* ctx, int n, int& begin, int& end) {
   begin = static_cast<int>(static_cast<long long>(n) * ctx->rank / ctx->world);
   end = static_cast<int>(static_cast<long long>(n) * (ctx->rank + 1) / ctx->world);

@@ -188,8 +188,8 @@ __global__ void pad_rows_kernel(const double* L, int M, int ldL, double* Lp) {
 template <bool GEN>
 __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx, const double* zy, const int32_t* ztid,
                                                               int M, int ldm, const double* x, const double* y,
-                                                              const int32_t* tid, int n, DevKernel k, LagTable lt,
-                                                              const double* Lp, int ldL, double* W) {
+                                                              const int32_t* tid, int col0, int n, DevKernel k,
+                                                              LagTable lt, const double* Lp, int ldL, double* W) {
   extern __shared__ double sm[];
   double* ring = sm;                                  // kWStages x [L 64 x kWKS | W 64 x kWKS]
   double* sOut = sm;                                  // [64 cols][65] (aliases the ring)
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
   double* sx = wrow + 2 * 64;                         // [64]
   double* sy = sx + 64;                               // [64]
   int* st = reinterpret_cast<int*>(sy + 64);
-  const int i0 = blockIdx.x * kWB;
+  const int i0 = col0 + blockIdx.x * kWB;  // columns [col0, n), 64 per block
   const int nc = min(kWB, n - i0);
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int grp = lane >> 2, tig = lane & 3, wr = wid >> 1, wc = wid & 1;
@@ -1127,7 +1127,9 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
     lap("setup");
     // W lives in the context between searches: an 8 GB cudaMalloc / cudaFree per call costs 0.1-1 s
     DevBuf<double>& W = ctx->sel_W;
-    W.ensure(static_cast<size_t>(ldm) * n);
+    // column slab of each rank's whitening (a multiple of the 64-column block; world slabs cover n)
+    const int wcols = ctx->world > 1 ? ceil_div(ceil_div(n, ctx->world), kWB) * kWB : n;
+    W.ensure(static_cast<size_t>(ldm) * std::max<long long>(n, static_cast<long long>(wcols) * ctx->world));
     DevBuf<double> resid(n), wnorm(n);
     lap("alloc W");
     STGP_CUDA(cudaMemsetAsync(W.get(), 0, sizeof(double) * ldm * n, st));
@@ -1175,10 +1177,15 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
         ProfRegion prw(ctx, "dr_whiten_seq");
         pad_rows_kernel<<<grid_for(static_cast<long long>(M) * ldL), 256, 0, st>>>(L.get(), M, ldL, Lp.get());
         launched(ctx);
-        wkern<<<ceil_div(n, kWB), kWthreads, kWsmem, st>>>(dzx.get(), dzy.get(), dzt.get(), M, ldm,
-                                                                      ds->x.get(), ds->y.get(), ds->tid.get(), n, k, lt,
-                                                                      Lp.get(), ldL, W.get());
+        // sharded: each rank whitens its slab of wcols columns, then the slabs are all-gathered
+        // (columns are independent, so the gathered W equals one rank's full whitening bit for bit)
+        const int w0 = std::min(n, ctx->rank * wcols), w1 = std::min(n, w0 + wcols);
+        if (w1 > w0)
+          wkern<<<ceil_div(w1 - w0, kWB), kWthreads, kWsmem, st>>>(dzx.get(), dzy.get(), dzt.get(), M, ldm,
+                                                                    ds->x.get(), ds->y.get(), ds->tid.get(), w0, w1, k,
+                                                                    lt, Lp.get(), ldL, W.get());
         launched(ctx);
+        if (ctx->world > 1) allgather_cols(ctx, W.get(), static_cast<size_t>(ldm) * wcols, n, ldm);
         lap("w:whiten_seq");
       }
       ProfRegion prr(ctx, "dr_resid");
