@@ -590,3 +590,10 @@ def zcptn_predict(om: "OracleModel", state, targets, lik_sigma: float, lik_lambd
     d["var_scale"] = vscale
     d["samples"] = np.ascontiguousarray(samples)
     return d
+
+
+def grad_close(g, gr, scale, rtol: float = 1e-8) -> bool:
+    """Per-component gradient parity: |g_k - gr_k| <= rtol * scale_k, scale_k = sum over rows of
+    |row contribution to k| (OracleModel.nll_grad_scale)."""
+    g, gr, scale = np.asarray(g, dtype=np.float64), np.asarray(gr, dtype=np.float64), np.asarray(scale)
+    return bool((np.abs(g - gr) <= rtol * scale).all())

@@ -57,9 +57,9 @@ def test_tiles_match_row_gathers_and_oracle(tmp_path, st, days, m, mv):
     assert np.allclose(ga, gb, rtol=1e-10, atol=1e-10 * np.abs(gb).max())
     th = (0.01, 1.0, 0.5, 20.0, 0.4, 1.5, 0.4, 0.2)
     om = O.OracleModel("vif", case["x"], case["y"], case["t"], th, nbr=case["nbr"], Z=case["Z"])
-    vr, gr = om.nll(case["resp"]), om.nll_grad(case["resp"])
+    vr, (gr, sc) = om.nll(case["resp"]), om.nll_grad_scale(case["resp"])
     assert a["nll"] == pytest.approx(vr, rel=1e-8)
-    assert np.allclose(ga, gr, rtol=1e-8, atol=1e-8 * np.abs(gr).max()), (ga, gr)
+    assert O.grad_close(ga, gr, sc), (ga, gr, sc)
 
 
 def test_ozaki_products_inside_vif_match_oracle(tmp_path):
@@ -71,6 +71,6 @@ def test_ozaki_products_inside_vif_match_oracle(tmp_path):
     assert np.allclose(ga, gb, rtol=1e-9, atol=1e-9 * np.abs(gb).max())
     th = (0.01, 1.0, 0.5, 20.0, 0.4, 1.5, 0.4, 0.2)
     om = O.OracleModel("vif", case["x"], case["y"], case["t"], th, nbr=case["nbr"], Z=case["Z"])
-    vr, gr = om.nll(case["resp"]), om.nll_grad(case["resp"])
+    vr, (gr, sc) = om.nll(case["resp"]), om.nll_grad_scale(case["resp"])
     assert a["nll"] == pytest.approx(vr, rel=1e-8)
-    assert np.allclose(ga, gr, rtol=1e-8, atol=1e-8 * np.abs(gr).max()), (ga, gr)
+    assert O.grad_close(ga, gr, sc), (ga, gr, sc)
