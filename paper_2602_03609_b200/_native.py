@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstgp_b200.so")
+# STGP_LIB selects another build of the same library (the bounds-checked one: `make checks`)
+LIB_PATH = os.environ.get("STGP_LIB") or os.path.join(_HERE, "libstgp_b200.so")
 
 
 class StgpError(RuntimeError):

@@ -33,6 +33,21 @@ struct Error : std::runtime_error {
 
 #define STGP_LAUNCH_CHECK() STGP_CUDA(cudaGetLastError())
 
+// Device-side bounds checks of the checked build (`make checks`: -DSTGP_DEVICE_CHECKS, library
+// libstgp_b200_checks.so, selected with STGP_LIB): a violated index bound traps the kernel, which
+// surfaces as a CUDA error on the next synchronisation.  compute-sanitizer is closed on the GPU pool;
+// the test suite run against the checked build is its substitute (profiles/r02/device_checks.log).
+#ifdef STGP_DEVICE_CHECKS
+#define STGP_DCHECK(cond)    \
+  do {                       \
+    if (!(cond)) __trap();   \
+  } while (0)
+#else
+#define STGP_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+
 // Device memory for DevBuf (engine.cu): the device's memory pool with an unbounded release
 // threshold, so steady-state allocations and frees stay inside the process instead of going to
 // the driver (cudaMalloc / cudaFree calls blocked the host for up to 1.7 s at random on the B200

@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int cnt = nt - t0 + 1 < 4 ? nt - t0 + 1 : 4;
                 const uint64_t db = smem_desc(sbase + S * kTileX + (t0 - 1) * kTileY);
                 // diagonals s + t0 - 2 ..; the first product (s = 1) of the chunk's first K step starts them
+                STGP_DCHECK((s + t0 - 2 + cnt) * kBN <= 512);
                 mma_i8(tmem + (s + t0 - 2) * kBN, da, db, (kb > 0 || s > 1) ? 1u : 0u, idesc_i8(kBN * cnt));
               }
             }

@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
     int nb = -1;
     if (lane < a.m_v) nb = __ldg(&a.nbr[static_cast<size_t>(i) * a.m_v + lane]);
     const int k = __popc(__ballot_sync(kFull, nb >= 0));  // neighbours packed at the front
+    STGP_DCHECK(k <= KS);
     const int pt = lane < k ? nb : (lane == KS ? i : -1);
     double rp = 0.0, zp = 0.0;
     if (pt >= 0) {
@@ -333,10 +334,12 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
     // ---- phase A: covariances over the closure (compact slot k maps to KS) ----
     const int P = (k + 1) * k / 2;
     auto slots = [&](int p, int& sa, int& sb) {
+      STGP_DCHECK(p < NP);
       const int pr = sPair[p];
       const int ca = pr & 0xff;
       sb = pr >> 8;
       sa = ca == k ? KS : ca;
+      STGP_DCHECK(sa < NS && sb < sa);
     };
     for (int p = lane; p < P; p += 32) {
       int sa, sb;
@@ -520,6 +523,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
       for (int p = lane; p < P; p += 32) {
         int sa, sb;
         slots(p, sa, sb);
+        STGP_DCHECK(scls[w][sa] < nc && scls[w][sb] < nc);
         one_pair(sa, sb, stf[w][scls[w][sa] * nc + scls[w][sb]]);
       }
     } else {
@@ -717,15 +721,18 @@ __global__ void __launch_bounds__(kRowWarps * 32) vif_grad_stored_kernel(RowArgs
       for (int q = 0; q < 6; ++q) g[q] = fma(wt, kg[q], g[q]);
     };
     auto slots = [&](int p, int& sa, int& sb) {
+      STGP_DCHECK(p < NP);
       const int pr = sPair[p];
       const int ca = pr & 0xff;
       sb = pr >> 8;
       sa = ca == k ? KS : ca;
+      STGP_DCHECK(sa < NS && sb < sa);
     };
     if (cached) {
       for (int p = lane; p < P; p += 32) {
         int sa, sb;
         slots(p, sa, sb);
+        STGP_DCHECK(scls[w][sa] < nc && scls[w][sb] < nc);
         one_pair(sa, sb, stf[w][scls[w][sa] * nc + scls[w][sb]]);
       }
     } else {

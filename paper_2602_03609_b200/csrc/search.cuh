@@ -90,6 +90,7 @@ __device__ __forceinline__ void topm_emit(const TopM& e, int m_v, int m, int lan
   }
   __syncwarp();
   if (valid) {
+    STGP_DCHECK(rank < m);
     orow[rank] = e.j;
     if (drow) drow[lane] = e.d;
   }
@@ -195,6 +196,7 @@ __device__ __forceinline__ void topl_emit(const TopM (&e)[R], int m_v, int m, in
 #pragma unroll
   for (int r = 0; r < R; ++r)
     if (valid[r]) {
+      STGP_DCHECK(rank[r] < m);
       orow[rank[r]] = e[r].j;
       if (drow) drow[32 * r + lane] = e[r].d;
     }

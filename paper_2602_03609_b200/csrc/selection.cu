@@ -748,6 +748,7 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
     qemit[tid] = i >= 0 ? min(a.m_v, i) : 0;
     // a degenerate query has d = 1 to every predecessor: its list is the m smallest indices
     qm[tid] = (i >= 0 && !a.degen[i]) ? min(a.m_v, i) : 0;
+    STGP_DCHECK(qemit[tid] <= kL);
   }
   for (int g = tid; g < T.G; g += kDrThreads) sAQ[g] = T.A[static_cast<size_t>(qt) * T.G + g];
   __syncthreads();

@@ -92,9 +92,11 @@ __device__ __forceinline__ void load_row_meta(const RowTileArgs& t, int pos, int
 #pragma unroll
   for (int a = 0; a < 31; ++a) {
     const uint16_t v = a < t.m_v ? __ldg(&sl[a]) : static_cast<uint16_t>(0xffff);
+    STGP_DCHECK(v == 0xffff || v < zrow);
     off[a] = static_cast<int>(sizeof(double)) * ((v == 0xffff ? zrow : v) * kCH + c);
     coef[a] = v == 0xffff ? 0.0 : f(a);
   }
+  STGP_DCHECK(__ldg(&sl[t.m_v]) < zrow);
   self_off = static_cast<int>(sizeof(double)) * (__ldg(&sl[t.m_v]) * kCH + c);
 }
 
@@ -115,6 +117,7 @@ __global__ void __launch_bounds__(kTileBlock, 1) tile_vprime_kernel(RowTileArgs 
     const int g = item / t.ntiles, tt = item - g * t.ntiles;
     const int o0 = __ldg(&t.tptr[tt]), nout = __ldg(&t.tptr[tt + 1]) - o0;
     const int u0 = __ldg(&t.uptr[tt]), nU = __ldg(&t.uptr[tt + 1]) - u0;
+    STGP_DCHECK(nU <= ucap && __ldg(&t.tptr[tt + 1]) - __ldg(&t.tptr[tt]) <= kTileRows);
     for (int e = threadIdx.x; e < nU; e += blockDim.x) sU[e] = static_cast<long long>(__ldg(&t.ucol[u0 + e])) * t.ldm;
     const bool live = o < nout;
     int off[31], self_off = 0;
@@ -176,6 +179,7 @@ __global__ void __launch_bounds__(kTileBlock, 1) tile_ef_kernel(RowTileArgs t, i
     const int g = item / t.ntiles, tt = item - g * t.ntiles;
     const int o0 = __ldg(&t.tptr[tt]), nout = __ldg(&t.tptr[tt + 1]) - o0;
     const int u0 = __ldg(&t.uptr[tt]), nU = __ldg(&t.uptr[tt + 1]) - u0;
+    STGP_DCHECK(nU <= ucap && __ldg(&t.tptr[tt + 1]) - __ldg(&t.tptr[tt]) <= kTileRows);
     for (int e = threadIdx.x; e < nU; e += blockDim.x) sU[e] = static_cast<long long>(__ldg(&t.ucol[u0 + e])) * t.ldm;
     if (threadIdx.x < nout) sO[threadIdx.x] = __ldg(&t.out[o0 + threadIdx.x]);
     const bool live = o < nout;
@@ -249,6 +253,7 @@ __global__ void __launch_bounds__(kTileBlock, 1) tile_ga_kernel(RowTileArgs t, i
   for (int tt; (tt = claim(t.next, t.ntiles, &sItem)) >= 0;) {
     const int o0 = __ldg(&t.tptr[tt]), nout = __ldg(&t.tptr[tt + 1]) - o0;
     const int u0 = __ldg(&t.uptr[tt]), nU = __ldg(&t.uptr[tt + 1]) - u0;
+    STGP_DCHECK(nU <= ucap && __ldg(&t.tptr[tt + 1]) - __ldg(&t.tptr[tt]) <= kTileRows);
     for (int e = threadIdx.x; e < nU; e += blockDim.x) sU[e] = static_cast<long long>(__ldg(&t.ucol[u0 + e])) * t.ldm;
     if (threadIdx.x < nout) sO[threadIdx.x] = __ldg(&t.out[o0 + threadIdx.x]);
     const bool live = o < nout;
@@ -260,6 +265,7 @@ __global__ void __launch_bounds__(kTileBlock, 1) tile_ga_kernel(RowTileArgs t, i
 #pragma unroll
       for (int s = 0; s < 31; ++s) {
         const uint16_t v = s < t.m_v ? __ldg(&sl[s]) : static_cast<uint16_t>(0xffff);
+        STGP_DCHECK(v == 0xffff || v < ucap);
         off[s] = static_cast<int>(sizeof(double)) * ((v == 0xffff ? ucap : v) * kCH + c);
       }
       off[31] = static_cast<int>(sizeof(double)) * (__ldg(&sl[t.m_v]) * kCH + c);
