@@ -147,6 +147,7 @@ def bench_config(args, n, world):
 # gradients; KE = 30 flop, KG = 50 flop (device instruction counts of gneiting_eval /
 # gneiting_grad incl. the exp port).
 KE_FLOP, KG_FLOP = 30.0, 50.0
+VIFGRAD_DRAM = 5.407542e9 + 0.379444e9  # vif_grad_stored_kernel, ncu at cfg4 (profiles/r02/v5)
 
 
 def vecchia_flops(nbr_counts):
@@ -396,10 +397,11 @@ def main():
         flops_launch = vif_rows_flops(counts[lo:hi], M)
         step_flops = vif_flops(counts, M)
     elif args.workload == "fitc":
-        # FITC is dense low-rank algebra: the roofline object covers the whole evaluation
-        kname = "FITC evaluation (DMMA GEMM/TRMM over n x M, cross covariance, kernel-gradient pairs)"
-        k_avg = ms_step
-        flops_launch = fitc_flops(hi - lo, M)
+        # FITC's dominant FP64 kernel: the triangular W = L_m^{-1} U (M (M + 1) / 2 FMA per column); the
+        # K, K^{-1} W and W diag(phi) W^T products run on the int8 tensor cores (roofline int8_tensor)
+        kname = "W = L_m^{-1} U: dgemm_kernel<0,0> (DMMA TRMM over the triangle's K range)"
+        k_avg = region_avg("W_trmm")
+        flops_launch = float(M) * (M + 1) * (hi - lo)
         step_flops = fitc_flops(n, M)
     else:
         kname = "vecchia_rows_kernel<grad>"
@@ -409,20 +411,24 @@ def main():
     achieved = flops_launch / (k_avg * 1e-3) / 1e12
     # DRAM bytes of the row pass from one ncu --set full capture per kernel (cfg4, N = 1):
     # dram__bytes_read.sum + dram__bytes_write.sum, profiles/r01/rows_{build,grad}_full_ncu.txt
-    traffic = (14.263361e9 + 5.968408e9 + 24.170873e9 + 0.283e9 + 5.41e9 + 0.34e9) if (
+    traffic = (14.260330e9 + 5.761680e9 + 24.167864e9 + 0.286370e9 + VIFGRAD_DRAM) if (
         args.workload == "vif" and (args.stations, args.days) == (10000, 110) and world == 1) else None
     breakdown = {k: round(ms_ / max(c_, 1), 3) for k, (ms_, c_) in sorted(prof.items(), key=lambda kv: -kv[1][0])}
     roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
             "frac": achieved / fp64_peak, "traffic": traffic,
-            "traffic_source": ("ncu dram__bytes_read+write: vecchia_rows_kernel<build> 20.23 GB + tile_ga_kernel 24.45 GB "
-                               "+ vif_grad_stored_kernel 5.75 GB (profiles/r01/v13_ncu_summary.txt, "
-                               "tiles_ncu_summary.txt)") if traffic else None,
+            "traffic_source": ("ncu --set full dram__bytes_read+write, one capture each at cfg4: "
+                               "vecchia_rows_kernel<build> 20.02 GB (profiles/r02/v5/full_vecchia_rows_kernel.txt) + "
+                               "tile_ga_kernel 24.45 GB (profiles/r02/full_tile_ga.txt) + vif_grad_stored_kernel "
+                               f"{VIFGRAD_DRAM / 1e9:.2f} GB (profiles/r02/v5/full_vif_grad_stored_kernel.txt)")
+            if traffic else None,
             "kernel": kname, "kernel_ms": k_avg,
             "kernel_share": k_avg / ms_step, "flop_per_launch": flops_launch,
             "peak_source": (f"measured in-run: max of DMMA m8n8k4 ({dmma_peak:.1f}) and DFMA ({dfma_peak:.1f}) "
                             "throughput microbenchmarks (MEASURED_PEAKS.json has no FP64 entry)"),
-            "step_canonical_flop": step_flops, "step_tflops": step_flops / (ms_step * 1e-3) / 1e12,
-            "step_frac": step_flops / (ms_step * 1e-3) / 1e12 / fp64_peak,
+            # whole step in canonical FP64 flops, counting the products that run as int8 Ozaki emulation
+            # as FP64 FMAs: an FP64-equivalent rate, which can exceed the FP64 peak (FITC does)
+            "step_canonical_flop": step_flops, "step_fp64_equiv_tflops": step_flops / (ms_step * 1e-3) / 1e12,
+            "step_fp64_equiv_frac": step_flops / (ms_step * 1e-3) / 1e12 / fp64_peak,
             "phase_ms": breakdown}
     # the FP64 products that run on the int8 tensor cores (Ozaki slicing, csrc/ozaki.cu): X = K^-1 V'
     # (FITC: K^-1 W), K = S S^T and V'F^T (FITC: W diag(phi) W^T), each S(S+1)/2 int8 MACs per FP64 FMA
