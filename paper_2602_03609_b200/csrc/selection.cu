@@ -594,6 +594,13 @@ constexpr int kHK = 64;        // halves per staged chunk
 constexpr int kHS = kHK + 8;   // smem row stride (halves): conflict-free 32-bit fragment loads
 static_assert(2 * kQT * kHS * 2 <= static_cast<int>(sizeof(double) * 2 * kQT * kKS), "half stage fits a ring slot");
 
+__device__ __forceinline__ void ldsm_x4(const __half* p, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(a));
+}
+
 __device__ __forceinline__ void hmma_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                            uint32_t b0, uint32_t b1) {
   asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
@@ -601,9 +608,12 @@ __device__ __forceinline__ void hmma_16816(float (&c)[4], uint32_t a0, uint32_t 
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+// one_time: every query and candidate of the tile pair share one time each, so the temporal
+// factors (pe1, pb1) are the pair's for every (i, j) -- no per-pair lag-table lookups.
 template <int kL>
 __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* qidx, const int* cidx, const int* qm,
-                                     const double (*topd)[kL], const int (*topj)[kL]) {
+                                     const double (*topd)[kL], const int (*topj)[kL], bool one_time, double pe1,
+                                     double pb1) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int grp = lane >> 2, tig = lane & 3, wr = wid >> 1, wc = wid & 1;
   float hc[4][4];
@@ -641,20 +651,18 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
     cp_async_commit();
     const __half* hQ = reinterpret_cast<const __half*>(ring + static_cast<size_t>(ch % kStages) * kDrStageDoubles);
     const __half* hC = hQ + kQT * kHS;
+    // fragments by ldmatrix: one x4 for the 16 x 16 A block, two x4 for the four 8-candidate B blocks
+    // (rows of 144 bytes: the eight row addresses of each 8 x 8 matrix fall in distinct bank groups)
+    const __half* pa = hQ + (16 * wr + (lane & 15)) * kHS + (lane >> 4) * 8;
+    const __half* pb = hC + (32 * wc + (lane >> 4) * 8 + (lane & 7)) * kHS + ((lane >> 3) & 1) * 8;
 #pragma unroll
     for (int ks = 0; ks < kHK; ks += 16) {
-      const int r0 = 16 * wr + grp;
-      const uint32_t a0 = *reinterpret_cast<const uint32_t*>(hQ + r0 * kHS + ks + 2 * tig);
-      const uint32_t a1 = *reinterpret_cast<const uint32_t*>(hQ + (r0 + 8) * kHS + ks + 2 * tig);
-      const uint32_t a2 = *reinterpret_cast<const uint32_t*>(hQ + r0 * kHS + ks + 8 + 2 * tig);
-      const uint32_t a3 = *reinterpret_cast<const uint32_t*>(hQ + (r0 + 8) * kHS + ks + 8 + 2 * tig);
+      uint32_t a0, a1, a2, a3, b[8];
+      ldsm_x4(pa + ks, a0, a1, a2, a3);
+      ldsm_x4(pb + ks, b[0], b[1], b[2], b[3]);
+      ldsm_x4(pb + 16 * kHS + ks, b[4], b[5], b[6], b[7]);
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int cc = 32 * wc + 8 * v + grp;
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(hC + cc * kHS + ks + 2 * tig);
-        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(hC + cc * kHS + ks + 8 + 2 * tig);
-        hmma_16816(hc[v], a0, a1, a2, a3, b0, b1);
-      }
+      for (int v = 0; v < 4; ++v) hmma_16816(hc[v], a0, a1, a2, a3, b[2 * v], b[2 * v + 1]);
     }
   }
   cp_async_wait<0>();
@@ -665,7 +673,7 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
   const float cf = static_cast<float>(a.k.c), s1f = static_cast<float>(a.k.s1);
   int iq[2];
   float xq[2], yq[2];
-  double rq[2], wq[2], dwq[2];
+  double rsq[2], wq[2], dwq[2];  // rsq: 1 / sqrt(r_i)
   int tq[2], mq[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -677,7 +685,7 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
       xq[h] = static_cast<float>(a.x[i]);
       yq[h] = static_cast<float>(a.y[i]);
       tq[h] = a.tid[i];
-      rq[h] = a.resid[i];
+      rsq[h] = 1.0 / sqrt(a.resid[i]);
       wq[h] = a.wnorm[i];
       dwq[h] = m > 0 ? topd[qq][m - 1] : 0.0;
     }
@@ -692,7 +700,9 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
       const bool dj = a.degen[j] != 0;
       const float xj = static_cast<float>(a.x[j]), yj = static_cast<float>(a.y[j]);
       const int tj = a.tid[j];
-      const double rj = a.resid[j], wj = a.wnorm[j];
+      // 1 / sqrt(r_i r_j) as a product of rounded reciprocal roots: a few ulp below the exact value at
+      // most, far inside the bound's (1 + 1e-12) margin
+      const double rsj = 1.0 / sqrt(a.resid[j]), wj = a.wnorm[j];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int i = iq[h], m = mq[h];
@@ -702,8 +712,8 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
           if (lex_less(1.0, j, dw, topj[16 * wr + grp + 8 * h][m - 1])) surv = 1;
           continue;
         }
-        double pe, pb;
-        a.lt.get2(tq[h], tj, pe, pb);
+        double pe = pe1, pb = pb1;
+        if (!one_time) a.lt.get2(tq[h], tj, pe, pb);
         const float dx = xq[h] - xj, dy = yq[h] - yj;
         const float xm = cf * sqrtf(dx * dx + dy * dy) * static_cast<float>(pb);
         const float ex = __expf(-xm);
@@ -711,15 +721,24 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
         const double kf = static_cast<double>(s1f * static_cast<float>(pe) * mat);
         const double err = 3e-3 * wq[h] * wj + 1e-5 * (wq[h] + wj) + 1e-5 * fabs(kf) + 1e-30;
         const double ub =
-            (fabs(kf - static_cast<double>(hc[v][2 * h + e2]) * kUnscale) + err) / sqrt(rq[h] * rj) * (1.0 + 1e-12);
+            (fabs(kf - static_cast<double>(hc[v][2 * h + e2]) * kUnscale) + err) * rsq[h] * rsj * (1.0 + 1e-12);
         if (!((1.0 - ub) - 1e-12 > dw * dw)) surv = 1;
       }
     }
   return __syncthreads_or(surv) != 0;
 }
 
+// diagnostics (STGP_DR_STATS): SM cycles per search phase, measured by thread 0 between the phase
+// barriers, summed over CTAs into stats[50 + phase]
+__device__ __forceinline__ void phase_clock(const DrArgs& a, long long& t, int slot) {
+  if (!a.stats || threadIdx.x != 0) return;
+  const long long now = clock64();
+  atomicAdd(&a.stats[50 + slot], static_cast<unsigned long long>(now - t));
+  t = now;
+}
+
 template <bool GEN, int LR>  // GEN: general nu; LR: list slots per lane (m_v <= 32 LR)
-__global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
+__global__ void __launch_bounds__(kDrThreads, 2) knn_dr_kernel(DrArgs a) {  // 2 CTAs per SM (128 registers)
   constexpr int kL = 32 * LR;
   extern __shared__ double sm[];
   // the staging ring and the distance tile are never live together
@@ -793,6 +812,7 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
     const int s_last = phase == 0 ? min(2 * kSeed, 2 * R) : 2 * R;
     bool stop = false;
     for (int s0 = s_first; s0 <= s_last && !stop; s0 += 32) {
+      long long tclk = a.stats ? clock64() : 0;
       // current worst threshold over the tile's queries (inf while any list is short)
       {
         double dm = 0.0;
@@ -854,6 +874,7 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
         }
       }
       __syncthreads();
+      phase_clock(a, tclk, 0);  // tile selection
       const int nsurv = s_nsurv;
       if (nsurv < 0) {
         stop = true;
@@ -895,6 +916,7 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
             }
           }
           const int any = __syncthreads_or(live);
+          phase_clock(a, tclk, 1);  // per-query live test
           if (!any) {
             if (a.stats && tid == 0) {
               atomicAdd(&a.stats[0], ~0ull);  // -1: moved from evaluated to pruned
@@ -906,10 +928,17 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
           }
         }
         const int cp0 = T.off[ct], cn = T.off[ct + 1] - cp0;
+        // single-time query and candidate tiles (the common case: buckets are days): one lag-table
+        // entry serves every pair of the tile pair
+        const bool one_time = tminQ == tmaxQ && T.tmin[ct] == T.tmax[ct];
+        double pe1 = 1.0, pb1 = 1.0;
+        if (one_time) a.lt.get2(tminQ, T.tmin[ct], pe1, pb1);
         if (tid < kCT) cidx[tid] = tid < cn ? T.sp[cp0 + tid] : -1;
         __syncthreads();
         if (a.W16 && phase == 1 && a.M > 0) {  // certified half-precision filter (seeds run exactly)
-          if (!half_filter_survives(a, ring, qidx, cidx, qm, topd, topj)) {
+          const bool fs = half_filter_survives(a, ring, qidx, cidx, qm, topd, topj, one_time, pe1, pb1);
+          phase_clock(a, tclk, 2);  // half-precision filter
+          if (!fs) {
             if (a.stats && tid == 0) atomicAdd(&a.stats[47], 1ull);
             continue;
           }
@@ -964,6 +993,7 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
         }
         // epilogue: d_r for the thread's 16 pairs (sd aliases the staging ring)
         __syncthreads();
+        phase_clock(a, tclk, 3);  // exact Gram (staging + DMMA)
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
@@ -977,8 +1007,8 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
                 if (a.degen[i] || a.degen[j]) {
                   dd = 1.0;
                 } else {
-                  double pe, pb;
-                  a.lt.get2(a.tid[i], a.tid[j], pe, pb);
+                  double pe = pe1, pb = pb1;  // the same table entry as a per-pair lookup
+                  if (!one_time) a.lt.get2(a.tid[i], a.tid[j], pe, pb);
                   TF f;
                   f.pow_mE = pe;
                   f.pow_mbh = pb;
@@ -992,6 +1022,7 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
               sd[qq][cc] = dd;
             }
         __syncthreads();
+        phase_clock(a, tclk, 4);  // d_r epilogue
         // merge: warp wid handles queries wid, wid + 8, ...
         bool inserted = false;
         for (int qq = wid; qq < kQT; qq += kDrThreads / 32) {
@@ -1026,6 +1057,7 @@ __global__ void __launch_bounds__(kDrThreads) knn_dr_kernel(DrArgs a) {
           if (tid == 0 && any) atomicAdd(&a.stats[48 + phase], 1ull);
         }
         __syncthreads();
+        phase_clock(a, tclk, 5);  // list merge
       }
     }
     if (stop) break;
@@ -1420,8 +1452,8 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
       lap("groups");
       DevBuf<unsigned long long> stats;
       if (std::getenv("STGP_DR_STATS")) {  // diagnostics: tile pairs evaluated / pruned
-        stats.alloc(50);
-        STGP_CUDA(cudaMemsetAsync(stats.get(), 0, 50 * 8, st));
+        stats.alloc(64);
+        STGP_CUDA(cudaMemsetAsync(stats.get(), 0, 64 * 8, st));
         a.stats = stats.get();
       }
       ProfRegion pr(ctx, "knn_dr");
@@ -1454,8 +1486,8 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
                   bstart[static_cast<size_t>(b1)]);
       lap("knn");
       if (a.stats) {
-        unsigned long long h[50];
-        STGP_CUDA(cudaMemcpyAsync(h, a.stats, 50 * 8, cudaMemcpyDeviceToHost, st));
+        unsigned long long h[64];
+        STGP_CUDA(cudaMemcpyAsync(h, a.stats, 64 * 8, cudaMemcpyDeviceToHost, st));
         STGP_CUDA(cudaStreamSynchronize(st));
         std::fprintf(stderr,
                      "[stgp] d_r tiles (%d query tiles, %d groups): evaluated %llu pruned %llu; half filter skipped "
@@ -1464,6 +1496,12 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
         for (int lg = 0; lg < 16; ++lg)
           std::fprintf(stderr, "[stgp]   lag %2d: evaluated %llu pruned %llu stops %llu\n", lg, h[2 + lg], h[18 + lg],
                        h[34 + lg]);
+        const char* names[6] = {"tile selection", "live test", "half filter", "exact Gram", "d_r epilogue", "merge"};
+        double tot = 0.0;
+        for (int q = 0; q < 6; ++q) tot += static_cast<double>(h[50 + q]);
+        for (int q = 0; q < 6; ++q)
+          std::fprintf(stderr, "[stgp]   phase %-14s %6.1f%% of CTA cycles\n", names[q],
+                       100.0 * static_cast<double>(h[50 + q]) / std::max(tot, 1.0));
       }
     }
     if (std::getenv("STGP_SPIN_SYNC")) {
