@@ -608,12 +608,44 @@ __device__ __forceinline__ void hmma_16816(float (&c)[4], uint32_t a0, uint32_t 
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+// diagnostics (STGP_DR_STATS): SM cycles per search phase, measured by thread 0 between the phase
+// barriers, summed over CTAs into stats[50 + phase]
+__device__ __forceinline__ void phase_clock(const DrArgs& a, long long& t, int slot) {
+  if (!a.stats || threadIdx.x != 0) return;
+  const long long now = clock64();
+  atomicAdd(&a.stats[50 + slot], static_cast<unsigned long long>(now - t));
+  t = now;
+}
+
+// Per-point data of a 64-row tile staged in shared memory (query tile once per CTA, candidate tile
+// per tested pair): the pair tests and the d_r epilogue read these instead of scattered global loads.
+struct TilePts {
+  double x[kQT], y[kQT], r[kQT], rs[kQT], w[kQT];  // coordinates, residual r, 1 / sqrt(r), |w|
+  int t[kQT], deg[kQT];                            // time id, degenerate flag
+};
+__device__ __forceinline__ void load_tile_pts(const DrArgs& a, int slot, int i, TilePts& P) {
+  if (i < 0) {
+    P.x[slot] = P.y[slot] = P.r[slot] = P.rs[slot] = P.w[slot] = 0.0;
+    P.t[slot] = 0;
+    P.deg[slot] = 1;
+    return;
+  }
+  P.x[slot] = a.x[i];
+  P.y[slot] = a.y[i];
+  const double r = a.resid[i];
+  P.r[slot] = r;
+  P.rs[slot] = r > 0.0 ? 1.0 / sqrt(r) : 0.0;
+  P.w[slot] = a.wnorm ? a.wnorm[i] : 0.0;  // set only with the fp16 filter (M > 0)
+  P.t[slot] = a.tid[i];
+  P.deg[slot] = a.degen[i];
+}
+
 // one_time: every query and candidate of the tile pair share one time each, so the temporal
 // factors (pe1, pb1) are the pair's for every (i, j) -- no per-pair lag-table lookups.
 template <int kL>
 __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* qidx, const int* cidx, const int* qm,
                                      const double (*topd)[kL], const int (*topj)[kL], bool one_time, double pe1,
-                                     double pb1) {
+                                     double pb1, const TilePts& QP, const TilePts& CP) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int grp = lane >> 2, tig = lane & 3, wr = wid >> 1, wc = wid & 1;
   float hc[4][4];
@@ -621,6 +653,7 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
   for (int v = 0; v < 4; ++v)
 #pragma unroll
     for (int e = 0; e < 4; ++e) hc[v][e] = 0.f;
+  long long tclk_f = a.stats ? clock64() : 0;
   const int nhc = a.ld16 / kHK;
   constexpr int kHPieces = 2 * kQT * (kHK / 8);  // 16-byte pieces per stage
   static_assert(kHPieces % kDrThreads == 0, "half staging split");
@@ -666,6 +699,10 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
     }
   }
   cp_async_wait<0>();
+  if (a.stats) {  // diagnostics: the fp16 Gram part of the filter (slot 6); the pair test follows
+    __syncthreads();
+    phase_clock(a, tclk_f, 6);
+  }
   // pair test: can (i, j) still enter i's list?  k(i, j) in single precision with the fast exp:
   // |k_f - k| <= 1e-5 |k_f| + 1e-30 covers its ~10 roundings and the 2-ulp __expf (rel. ~1.3e-6).
   int surv = a.k.nu_code == kNuGeneral ? 1 : 0;  // no single-precision general Matern: all go exact
@@ -682,11 +719,11 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
     iq[h] = i;
     mq[h] = m;
     if (i >= 0) {
-      xq[h] = static_cast<float>(a.x[i]);
-      yq[h] = static_cast<float>(a.y[i]);
-      tq[h] = a.tid[i];
-      rsq[h] = 1.0 / sqrt(a.resid[i]);
-      wq[h] = a.wnorm[i];
+      xq[h] = static_cast<float>(QP.x[qq]);
+      yq[h] = static_cast<float>(QP.y[qq]);
+      tq[h] = QP.t[qq];
+      rsq[h] = QP.rs[qq];
+      wq[h] = QP.w[qq];
       dwq[h] = m > 0 ? topd[qq][m - 1] : 0.0;
     }
   }
@@ -697,12 +734,12 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
       const int cc = 32 * wc + 8 * v + 2 * tig + e2;
       const int j = cidx[cc];
       if (j < 0 || surv) continue;
-      const bool dj = a.degen[j] != 0;
-      const float xj = static_cast<float>(a.x[j]), yj = static_cast<float>(a.y[j]);
-      const int tj = a.tid[j];
+      const bool dj = CP.deg[cc] != 0;
+      const float xj = static_cast<float>(CP.x[cc]), yj = static_cast<float>(CP.y[cc]);
+      const int tj = CP.t[cc];
       // 1 / sqrt(r_i r_j) as a product of rounded reciprocal roots: a few ulp below the exact value at
       // most, far inside the bound's (1 + 1e-12) margin
-      const double rsj = 1.0 / sqrt(a.resid[j]), wj = a.wnorm[j];
+      const double rsj = CP.rs[cc], wj = CP.w[cc];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int i = iq[h], m = mq[h];
@@ -728,15 +765,6 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
   return __syncthreads_or(surv) != 0;
 }
 
-// diagnostics (STGP_DR_STATS): SM cycles per search phase, measured by thread 0 between the phase
-// barriers, summed over CTAs into stats[50 + phase]
-__device__ __forceinline__ void phase_clock(const DrArgs& a, long long& t, int slot) {
-  if (!a.stats || threadIdx.x != 0) return;
-  const long long now = clock64();
-  atomicAdd(&a.stats[50 + slot], static_cast<unsigned long long>(now - t));
-  t = now;
-}
-
 template <bool GEN, int LR>  // GEN: general nu; LR: list slots per lane (m_v <= 32 LR)
 __global__ void __launch_bounds__(kDrThreads, 2) knn_dr_kernel(DrArgs a) {  // 2 CTAs per SM (128 registers)
   constexpr int kL = 32 * LR;
@@ -747,6 +775,7 @@ __global__ void __launch_bounds__(kDrThreads, 2) knn_dr_kernel(DrArgs a) {  // 2
   double (*topd)[kL] = reinterpret_cast<double (*)[kL]>(sm + kStages * kDrStageDoubles);
   int (*topj)[kL] = reinterpret_cast<int (*)[kL]>(sm + kStages * kDrStageDoubles + kQT * kL);
   __shared__ int qidx[kQT], cidx[kCT], qm[kQT], qemit[kQT];
+  __shared__ TilePts sQP, sCP;
   __shared__ double s_dmax[kDrThreads / 32];
   __shared__ int s_surv[32], s_nsurv;
   __shared__ double s_d;
@@ -768,6 +797,7 @@ __global__ void __launch_bounds__(kDrThreads, 2) knn_dr_kernel(DrArgs a) {  // 2
     // a degenerate query has d = 1 to every predecessor: its list is the m smallest indices
     qm[tid] = (i >= 0 && !a.degen[i]) ? min(a.m_v, i) : 0;
     STGP_DCHECK(qemit[tid] <= kL);
+    load_tile_pts(a, tid, i, sQP);
   }
   for (int g = tid; g < T.G; g += kDrThreads) sAQ[g] = T.A[static_cast<size_t>(qt) * T.G + g];
   __syncthreads();
@@ -894,14 +924,13 @@ __global__ void __launch_bounds__(kDrThreads, 2) knn_dr_kernel(DrArgs a) {  // 2
               if (!(dq < 1.0)) {
                 live = 1;
               } else {
-                const int i = qidx[qq];
-                const int ti = a.tid[i], tc0 = T.tmin[ct], tc1 = T.tmax[ct];
+                const int ti = sQP.t[qq], tc0 = T.tmin[ct], tc1 = T.tmax[ct];
                 double pe_min, pb0, pe0, pb_max;
                 if (tc1 >= ti) pe_min = 1.0; else a.lt.get2(ti, tc1, pe_min, pb0);
                 a.lt.get2(ti, tc0, pe0, pb_max);
                 double mat = 1.0;
                 if (a.k.nu_code != kNuGeneral) {
-                  const double xi = a.x[i], yi = a.y[i];
+                  const double xi = sQP.x[qq], yi = sQP.y[qq];
                   const double dx = fmax(0.0, fmax(T.bx0[ct] - xi, xi - T.bx1[ct]));
                   const double dy = fmax(0.0, fmax(T.by0[ct] - yi, yi - T.by1[ct]));
                   const double xm = a.k.c * sqrt(dx * dx + dy * dy) * (1.0 - 1e-12) * pb_max * (1.0 - 1e-12);
@@ -910,7 +939,7 @@ __global__ void __launch_bounds__(kDrThreads, 2) knn_dr_kernel(DrArgs a) {  // 2
                 double wt = 0.0;
                 const double* AC = T.A + static_cast<size_t>(ct) * T.G;
                 for (int g = 0; g < T.G; ++g) wt += sAQ[g] * AC[g];
-                const double ci = (a.s1 * pe_min * mat / sqrt(a.resid[i] * T.rmin[ct]) + wt) * (1.0 + 1e-11);
+                const double ci = (a.s1 * pe_min * mat / sqrt(sQP.r[qq] * T.rmin[ct]) + wt) * (1.0 + 1e-11);
                 live = !(ci < 1.0 && (1.0 - ci) - 1e-12 > dq * dq);
               }
             }
@@ -933,10 +962,14 @@ __global__ void __launch_bounds__(kDrThreads, 2) knn_dr_kernel(DrArgs a) {  // 2
         const bool one_time = tminQ == tmaxQ && T.tmin[ct] == T.tmax[ct];
         double pe1 = 1.0, pb1 = 1.0;
         if (one_time) a.lt.get2(tminQ, T.tmin[ct], pe1, pb1);
-        if (tid < kCT) cidx[tid] = tid < cn ? T.sp[cp0 + tid] : -1;
+        if (tid < kCT) {
+          const int j = tid < cn ? T.sp[cp0 + tid] : -1;
+          cidx[tid] = j;
+          load_tile_pts(a, tid, j, sCP);
+        }
         __syncthreads();
         if (a.W16 && phase == 1 && a.M > 0) {  // certified half-precision filter (seeds run exactly)
-          const bool fs = half_filter_survives(a, ring, qidx, cidx, qm, topd, topj, one_time, pe1, pb1);
+          const bool fs = half_filter_survives(a, ring, qidx, cidx, qm, topd, topj, one_time, pe1, pb1, sQP, sCP);
           phase_clock(a, tclk, 2);  // half-precision filter
           if (!fs) {
             if (a.stats && tid == 0) atomicAdd(&a.stats[47], 1ull);
@@ -1004,18 +1037,18 @@ __global__ void __launch_bounds__(kDrThreads, 2) knn_dr_kernel(DrArgs a) {  // 2
               const int i = qidx[qq], j = cidx[cc];
               double dd = __longlong_as_double(0x7ff0000000000000LL);
               if (i >= 0 && j >= 0 && j < i) {
-                if (a.degen[i] || a.degen[j]) {
+                if (sQP.deg[qq] || sCP.deg[cc]) {
                   dd = 1.0;
                 } else {
                   double pe = pe1, pb = pb1;  // the same table entry as a per-pair lookup
-                  if (!one_time) a.lt.get2(a.tid[i], a.tid[j], pe, pb);
+                  if (!one_time) a.lt.get2(sQP.t[qq], sCP.t[cc], pe, pb);
                   TF f;
                   f.pow_mE = pe;
                   f.pow_mbh = pb;
-                  double rho = gneiting_eval<GEN>(a.k, spatial_dist(a.x[i], a.y[i], a.x[j], a.y[j]), f);
+                  double rho = gneiting_eval<GEN>(a.k, spatial_dist(sQP.x[qq], sQP.y[qq], sCP.x[cc], sCP.y[cc]), f);
                   if (a.M > 0) rho = __dsub_rn(rho, acc[u][v][h]);
                   const double rad =
-                      __dsub_rn(1.0, __ddiv_rn(fabs(rho), __dsqrt_rn(__dmul_rn(a.resid[i], a.resid[j]))));
+                      __dsub_rn(1.0, __ddiv_rn(fabs(rho), __dsqrt_rn(__dmul_rn(sQP.r[qq], sCP.r[cc]))));
                   dd = __dsqrt_rn(rad < 0.0 ? 0.0 : rad);
                 }
               }
@@ -1496,10 +1529,11 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
         for (int lg = 0; lg < 16; ++lg)
           std::fprintf(stderr, "[stgp]   lag %2d: evaluated %llu pruned %llu stops %llu\n", lg, h[2 + lg], h[18 + lg],
                        h[34 + lg]);
-        const char* names[6] = {"tile selection", "live test", "half filter", "exact Gram", "d_r epilogue", "merge"};
+        const char* names[7] = {"tile selection", "live test",    "half filter", "exact Gram",
+                                "d_r epilogue",   "merge",        "  of which fp16 Gram"};
         double tot = 0.0;
         for (int q = 0; q < 6; ++q) tot += static_cast<double>(h[50 + q]);
-        for (int q = 0; q < 6; ++q)
+        for (int q = 0; q < 7; ++q)
           std::fprintf(stderr, "[stgp]   phase %-14s %6.1f%% of CTA cycles\n", names[q],
                        100.0 * static_cast<double>(h[50 + q]) / std::max(tot, 1.0));
       }
