@@ -539,18 +539,28 @@ struct DrArgs {
 //                                    + sum_g A_Q[g] A_C[g]
 // (T(u) and Matern are decreasing; h_min = box-to-box distance; degenerate rows excluded: they sit
 // at d = 1).
-__device__ __forceinline__ double tile_cmax(const DrArgs& a, int tminQ, int tmaxQ, double qx0, double qx1,
-                                            double qy0, double qy1, const double* AQ, double rQ, int ct) {
+// The (query tile, candidate tile) pieces of the bound: the temporal factors at the smallest lag
+// (pe_min) and at the largest (pb_max), and the block bound wt of |w_i . w_j| / sqrt(r_i r_j).
+__device__ __forceinline__ void tile_pair_terms(const DrArgs& a, int tminQ, int tmaxQ, const double* AQ, int ct,
+                                                double& pe_min, double& pb_max, double& wt) {
   const DrTiles& T = a.T;
   // lags: C's times precede or equal Q's (time-sorted rows, j < i)
   const int tc0 = T.tmin[ct], tc1 = T.tmax[ct];
-  double pe_min, pb_dummy, pe_dummy, pb_max;
+  double pb_dummy, pe_dummy;
   if (tc1 >= tminQ) {  // time ranges touch: u_min = 0
     pe_min = 1.0;
   } else {
     a.lt.get2(tminQ, tc1, pe_min, pb_dummy);
   }
   a.lt.get2(tmaxQ, tc0, pe_dummy, pb_max);
+  wt = 0.0;
+  const double* AC = T.A + static_cast<size_t>(ct) * T.G;
+  for (int g = 0; g < T.G; ++g) wt += AQ[g] * AC[g];
+}
+
+__device__ __forceinline__ double tile_cmax(const DrArgs& a, double qx0, double qx1, double qy0, double qy1,
+                                            double rQ, int ct, double pe_min, double pb_max, double wt) {
+  const DrTiles& T = a.T;
   double mat = 1.0;
   if (a.k.nu_code != kNuGeneral) {  // general nu: the bound 1 (correlations are <= 1)
     const double dx = fmax(0.0, fmax(T.bx0[ct] - qx1, qx0 - T.bx1[ct]));
@@ -559,9 +569,6 @@ __device__ __forceinline__ double tile_cmax(const DrArgs& a, int tminQ, int tmax
     const double xm = a.k.c * hmin * pb_max * (1.0 - 1e-12);
     mat = matern_from_exp(xm, exp(-xm), a.k.nu_code);
   }
-  double wt = 0.0;
-  const double* AC = T.A + static_cast<size_t>(ct) * T.G;
-  for (int g = 0; g < T.G; ++g) wt += AQ[g] * AC[g];
   return (a.s1 * pe_min * mat / sqrt(rQ * T.rmin[ct]) + wt) * (1.0 + 1e-11);
 }
 
@@ -778,6 +785,7 @@ __global__ void __launch_bounds__(kDrThreads, 2) knn_dr_kernel(DrArgs a) {  // 2
   __shared__ TilePts sQP, sCP;
   __shared__ double s_dmax[kDrThreads / 32];
   __shared__ int s_surv[32], s_nsurv;
+  __shared__ double s_wt[32], s_pemin[32], s_pbmax[32];  // tile_pair_terms of each surviving tile
   __shared__ double s_d;
   __shared__ double sAQ[kMaxGroups];
   const DrTiles& T = a.T;
@@ -877,15 +885,23 @@ __global__ void __launch_bounds__(kDrThreads, 2) knn_dr_kernel(DrArgs a) {  // 2
         const int ct = p + off;
         bool take = !stop_b && s <= s_last && ct >= t0 && ct < t1 && T.imin[ct] < imaxQ;
         int pruned = 0;
+        double pe_min = 1.0, pb_max = 1.0, wt = 0.0;
+        if (take && phase == 1 && can_prune) tile_pair_terms(a, tminQ, tmaxQ, sAQ, ct, pe_min, pb_max, wt);
         if (take && phase == 1 && can_prune && d < 1.0) {
-          const double cmax = tile_cmax(a, tminQ, tmaxQ, qx0, qx1, qy0, qy1, sAQ, rQ, ct);
+          const double cmax = tile_cmax(a, qx0, qx1, qy0, qy1, rQ, ct, pe_min, pb_max, wt);
           if (cmax < 1.0 && (1.0 - cmax) - 1e-12 > d * d) {
             take = false;
             pruned = 1;
           }
         }
         const unsigned mk = __ballot_sync(kFull, take);
-        if (take) s_surv[__popc(mk & ((1u << lane) - 1))] = ct;
+        if (take) {
+          const int pos = __popc(mk & ((1u << lane) - 1));
+          s_surv[pos] = ct;
+          s_wt[pos] = wt;
+          s_pemin[pos] = pe_min;
+          s_pbmax[pos] = pb_max;
+        }
         if (lane == 0) {
           s_nsurv = stop_b ? -1 : __popc(mk);
           if (a.stats) {
@@ -924,10 +940,13 @@ __global__ void __launch_bounds__(kDrThreads, 2) knn_dr_kernel(DrArgs a) {  // 2
               if (!(dq < 1.0)) {
                 live = 1;
               } else {
-                const int ti = sQP.t[qq], tc0 = T.tmin[ct], tc1 = T.tmax[ct];
-                double pe_min, pb0, pe0, pb_max;
-                if (tc1 >= ti) pe_min = 1.0; else a.lt.get2(ti, tc1, pe_min, pb0);
-                a.lt.get2(ti, tc0, pe0, pb_max);
+                double pe_min = s_pemin[sv], pb_max = s_pbmax[sv];  // the query tile's, exact when it has
+                if (tminQ != tmaxQ) {                               // one time; else each row's own
+                  const int ti = sQP.t[qq], tc0 = T.tmin[ct], tc1 = T.tmax[ct];
+                  double pb0, pe0;
+                  if (tc1 >= ti) pe_min = 1.0; else a.lt.get2(ti, tc1, pe_min, pb0);
+                  a.lt.get2(ti, tc0, pe0, pb_max);
+                }
                 double mat = 1.0;
                 if (a.k.nu_code != kNuGeneral) {
                   const double xi = sQP.x[qq], yi = sQP.y[qq];
@@ -936,10 +955,7 @@ __global__ void __launch_bounds__(kDrThreads, 2) knn_dr_kernel(DrArgs a) {  // 2
                   const double xm = a.k.c * sqrt(dx * dx + dy * dy) * (1.0 - 1e-12) * pb_max * (1.0 - 1e-12);
                   mat = matern_from_exp(xm, exp(-xm), a.k.nu_code);
                 }
-                double wt = 0.0;
-                const double* AC = T.A + static_cast<size_t>(ct) * T.G;
-                for (int g = 0; g < T.G; ++g) wt += sAQ[g] * AC[g];
-                const double ci = (a.s1 * pe_min * mat / sqrt(sQP.r[qq] * T.rmin[ct]) + wt) * (1.0 + 1e-11);
+                const double ci = (a.s1 * pe_min * mat / sqrt(sQP.r[qq] * T.rmin[ct]) + s_wt[sv]) * (1.0 + 1e-11);
                 live = !(ci < 1.0 && (1.0 - ci) - 1e-12 > dq * dq);
               }
             }
