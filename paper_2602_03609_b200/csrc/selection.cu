@@ -716,8 +716,8 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
   constexpr double kUnscale = 1.0 / (kW16Scale * kW16Scale);
   const float cf = static_cast<float>(a.k.c), s1f = static_cast<float>(a.k.s1);
   int iq[2];
-  float xq[2], yq[2];
-  double rsq[2], wq[2], dwq[2];  // rsq: 1 / sqrt(r_i)
+  float xq[2], yq[2], rsq[2], wq[2], dwq2[2];  // rsq: 1 / sqrt(r_i); dwq2: current worst d^2
+  double dwq[2];
   int tq[2], mq[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -729,9 +729,10 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
       xq[h] = static_cast<float>(QP.x[qq]);
       yq[h] = static_cast<float>(QP.y[qq]);
       tq[h] = QP.t[qq];
-      rsq[h] = QP.rs[qq];
-      wq[h] = QP.w[qq];
+      rsq[h] = static_cast<float>(QP.rs[qq]);
+      wq[h] = static_cast<float>(QP.w[qq]);
       dwq[h] = m > 0 ? topd[qq][m - 1] : 0.0;
+      dwq2[h] = static_cast<float>(fmin(dwq[h], 1.0) * fmin(dwq[h], 1.0));
     }
   }
 #pragma unroll
@@ -746,7 +747,7 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
       const int tj = CP.t[cc];
       // 1 / sqrt(r_i r_j) as a product of rounded reciprocal roots: a few ulp below the exact value at
       // most, far inside the bound's (1 + 1e-12) margin
-      const double rsj = CP.rs[cc], wj = CP.w[cc];
+      const float rsj = static_cast<float>(CP.rs[cc]), wj = static_cast<float>(CP.w[cc]);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int i = iq[h], m = mq[h];
@@ -762,11 +763,15 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
         const float xm = cf * sqrtf(dx * dx + dy * dy) * static_cast<float>(pb);
         const float ex = __expf(-xm);
         const float mat = a.k.nu_code == 0 ? ex : (a.k.nu_code == 1 ? (1.f + xm) * ex : (1.f + xm + xm * xm * (1.f / 3.f)) * ex);
-        const double kf = static_cast<double>(s1f * static_cast<float>(pe) * mat);
-        const double err = 3e-3 * wq[h] * wj + 1e-5 * (wq[h] + wj) + 1e-5 * fabs(kf) + 1e-30;
-        const double ub =
-            (fabs(kf - static_cast<double>(hc[v][2 * h + e2]) * kUnscale) + err) * rsq[h] * rsj * (1.0 + 1e-12);
-        if (!((1.0 - ub) - 1e-12 > dw * dw)) surv = 1;
+        // the bound in single precision: the difference kf - g loses at most ~2^-23 (|kf| + |g|)
+        // (covered by the 1e-6 (|kf| + |g|) term), the products and sums ~10 roundings of 2^-24
+        // (the 4e-6 relative margin), the final comparison the 1e-6 absolute one (d^2 <= 1)
+        const float kf = s1f * static_cast<float>(pe) * mat;
+        const float g = hc[v][2 * h + e2] * static_cast<float>(kUnscale);
+        const float err = 3e-3f * wq[h] * wj + 1e-5f * (wq[h] + wj) + 1e-5f * fabsf(kf) +
+                          1e-6f * (fabsf(kf) + fabsf(g)) + 1e-30f;
+        const float ub = ((fabsf(kf - g) + err) * rsq[h] * rsj) * (1.0f + 4e-6f);
+        if (!((1.0f - ub) - 1e-6f > dwq2[h])) surv = 1;
       }
     }
   return __syncthreads_or(surv) != 0;
