@@ -1087,12 +1087,16 @@ int stgp_correlation_neighbors(stgp_dataset* ds, const stgp_params* theta, int m
     Params p;
     std::memcpy(&p, theta, sizeof(p));
     validate_params(p);
-    // The spatial-tile search with an empty inducing set is also the exact d_c search (selection.cu,
-    // STGP_DC_SPATIAL=1; identical sets).  Without a Gram per tile its 64 x 64 evaluation is less
-    // selective than the per-query time-block pruning of knn_kernel<0>: 61 vs 70 ms on the device at
-    // cfg4, slower end to end with the tile set-up, so knn_kernel<0> stays the default.
+    // The spatial-tile search with an empty inducing set is also the exact d_c search (selection.cu;
+    // identical sets).  Its box-distance pruning pays where the equal-time blocks are large: every
+    // query of knn_kernel<0> scans its whole block.  cfg4 (10k rows per day): 52 vs 71 ms kernel,
+    // 0.062 vs 0.071 s end to end; cfg2 (1k rows per day): 9.0 vs 3.7 ms.  So the spatial search
+    // is taken for time-sorted data with >= 4096 rows per distinct time on average;
+    // STGP_DC_SPATIAL=0/1 forces either.
     const char* sp = std::getenv("STGP_DC_SPATIAL");
-    if (sp && sp[0] == '1')
+    const bool big_blocks = ds->time_sorted && !ds->Tdata.empty() &&
+                            static_cast<double>(ds->n) / static_cast<double>(ds->Tdata.size()) >= 4096.0;
+    if (sp ? sp[0] == '1' : big_blocks)
       *out = spatial_search(ds, p, std::vector<double>(), m_v, STGP_METRIC_DC);
     else
       *out = run_search(ds, STGP_METRIC_DC, &p, m_v, 1.0, 1.0);
