@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
                                                               const int32_t* tid, int col0, int n, DevKernel k,
                                                               LagTable lt, const double* Lp, int ldL, double* W) {
   extern __shared__ double sm[];
+  __shared__ double sRcp[64];                         // rounded reciprocals of the diagonal block's pivots
   double* ring = sm;                                  // kWStages x [L 64 x kWKS | W 64 x kWKS]
   double* sOut = sm;                                  // [64 cols][65] (aliases the ring)
   double* sD = sm + kWStages * kWStageDoubles;        // [64][65]
@@ -292,6 +293,7 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
       const int rr = e / 64, cc = e % 64;
       sD[rr * 65 + cc] = (rr < rb && cc <= rr) ? Lp[static_cast<size_t>(r0 + rr) * ldL + r0 + cc] : 0.0;
     }
+    if (t < rb) sRcp[t] = __drcp_rn(Lp[static_cast<size_t>(r0 + t) * ldL + r0 + t]);  // RN(1 / L_rr)
     __syncthreads();
     // diagonal block: the columns are independent forward substitutions, so warp w solves columns
     // 8w..8w+7 alone (lanes hold rows lane, lane + 32; lanes 0..7 divide, one column each): no
@@ -320,7 +322,14 @@ __global__ void __launch_bounds__(kWthreads) whiten_seq_kernel(const double* zx,
         }
         __syncwarp();
         if (lane < 8) {  // lane q divides column cb + q's row cl and writes the result in place
-          const double w = __ddiv_rn(xw[lane], sD[cl * 65 + cl]);
+          // x / L_cc correctly rounded from the rounded reciprocal y: q0 = RN(x y) is within an ulp
+          // of x / L, r = x - q0 L is exact (fma), and RN(q0 + r y) = RN(x / L) (Markstein); r = 0
+          // means q0 is the exact quotient (and keeps the sign of a zero x).  Bit-identical to
+          // __ddiv_rn at a quarter of its latency on the wavefront's critical path.
+          const double x = xw[lane], d = sD[cl * 65 + cl], y = sRcp[cl];
+          const double q0 = __dmul_rn(x, y);
+          const double r = __fma_rn(-q0, d, x);
+          const double w = r == 0.0 ? q0 : __fma_rn(r, y, q0);
           xq[lane] = w;
           sOut[(cb + lane) * 65 + cl] = w;
         }
