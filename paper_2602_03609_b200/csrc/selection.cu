@@ -661,7 +661,7 @@ __device__ __forceinline__ void load_tile_pts(const DrArgs& a, int slot, int i, 
 template <int kL>
 __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* qidx, const int* cidx, const int* qm,
                                      const double (*topd)[kL], const int (*topj)[kL], bool one_time, double pe1,
-                                     double pb1, const TilePts& QP, const TilePts& CP) {
+                                     double pb1, const TilePts& QP, const TilePts& CP, const int* qlive) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int grp = lane >> 2, tig = lane & 3, wr = wid >> 1, wc = wid & 1;
   float hc[4][4];
@@ -731,7 +731,8 @@ __device__ bool half_filter_survives(const DrArgs& a, double* ring, const int* q
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int qq = 16 * wr + grp + 8 * h;
-    const int i = qidx[qq], m = qm[qq];
+    const int i = qidx[qq];
+    const int m = qlive[qq] ? qm[qq] : 0;  // a query the live test excluded takes none of the tile
     iq[h] = i;
     mq[h] = m;
     if (i >= 0) {
@@ -800,6 +801,7 @@ __global__ void __launch_bounds__(kDrThreads, 2) knn_dr_kernel(DrArgs a) {  // 2
   __shared__ double s_dmax[kDrThreads / 32];
   __shared__ int s_surv[32], s_nsurv;
   __shared__ double s_wt[32], s_pemin[32], s_pbmax[32];  // tile_pair_terms of each surviving tile
+  __shared__ int s_qlive[kQT];  // per-query live test of the current candidate tile (1: may take one)
   __shared__ double s_d;
   __shared__ double sAQ[kMaxGroups];
   const DrTiles& T = a.T;
@@ -942,6 +944,7 @@ __global__ void __launch_bounds__(kDrThreads, 2) knn_dr_kernel(DrArgs a) {  // 2
       }
       for (int sv = 0; sv < nsurv; ++sv) {
         const int ct = s_surv[sv];
+        if (tid < kQT) s_qlive[tid] = 1;  // (the live test below narrows it; visible after the next barrier)
         if (phase == 1 && can_prune) {
           // per-query re-test with each row's own threshold, time, point-to-box distance and r
           // (the tile-level test above used the worst of 64 of each): a valid bound per pair, the
@@ -974,6 +977,7 @@ __global__ void __launch_bounds__(kDrThreads, 2) knn_dr_kernel(DrArgs a) {  // 2
               }
             }
           }
+          if (tid < kQT) s_qlive[tid] = live;
           const int any = __syncthreads_or(live);
           phase_clock(a, tclk, 1);  // per-query live test
           if (!any) {
@@ -999,7 +1003,7 @@ __global__ void __launch_bounds__(kDrThreads, 2) knn_dr_kernel(DrArgs a) {  // 2
         }
         __syncthreads();
         if (a.W16 && phase == 1 && a.M > 0) {  // certified half-precision filter (seeds run exactly)
-          const bool fs = half_filter_survives(a, ring, qidx, cidx, qm, topd, topj, one_time, pe1, pb1, sQP, sCP);
+          const bool fs = half_filter_survives(a, ring, qidx, cidx, qm, topd, topj, one_time, pe1, pb1, sQP, sCP, s_qlive);
           phase_clock(a, tclk, 2);  // half-precision filter
           if (!fs) {
             if (a.stats && tid == 0) atomicAdd(&a.stats[47], 1ull);
