@@ -116,6 +116,10 @@ struct stgp_dataset {
   stgp::DevBuf<double> resp, X;
   int p = 0;
   bool has_resp = false;
+  // spatial-tile search meta (selection.cu), computed on first use: time buckets and bounding box
+  bool tile_meta = false;
+  std::vector<int> tile_bstart;
+  double tile_x0 = 0, tile_x1 = 0, tile_y0 = 0, tile_y1 = 0;
 };
 
 struct stgp_neighbors {

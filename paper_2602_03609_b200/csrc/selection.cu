@@ -425,6 +425,32 @@ struct DrTiles {
   double *A, *Apre, *rpre;
 };
 
+// (bucket << 32 | Morton(x, y)) sort keys and the identity permutation of the spatial tiles; bstart
+// holds the nbucket + 1 bucket starts (the Morton part is 0 for unsorted data: index order)
+__device__ __forceinline__ uint32_t spread16(uint32_t v) {
+  v &= 0xffff;
+  v = (v | (v << 8)) & 0x00ff00ffu;
+  v = (v | (v << 4)) & 0x0f0f0f0fu;
+  v = (v | (v << 2)) & 0x33333333u;
+  v = (v | (v << 1)) & 0x55555555u;
+  return v;
+}
+__global__ void tile_keys_kernel(int n, const double* x, const double* y, const int* bstart, int nbucket, bool morton,
+                                 double x0, double y0, double sx, double sy, uint64_t* keys, int32_t* iota) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int lo = 0, hi = nbucket;  // bucket b with bstart[b] <= i < bstart[b + 1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (bstart[mid] <= i) lo = mid; else hi = mid;
+    }
+    const uint32_t mk = morton ? (spread16(static_cast<uint32_t>((x[i] - x0) * sx)) |
+                                  (spread16(static_cast<uint32_t>((y[i] - y0) * sy)) << 1))
+                               : 0u;
+    keys[i] = (static_cast<uint64_t>(lo) << 32) | mk;
+    iota[i] = i;
+  }
+}
+
 __global__ void tile_stats_kernel(DrTiles T, const double* x, const double* y, const double* resid,
                                   const int32_t* degen, const int32_t* tid, double s1) {
   const int tile = blockIdx.x;
@@ -1338,58 +1364,51 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
       // the Morton code of (x, y), cut into tiles of <= 64 rows; one index-order bucket when the rows
       // are not time sorted (no pruning: plain exact brute force over predecessors).
       const bool ts = ds->time_sorted;
-      std::vector<int> bstart{0};
-      if (ts) {
-        int cnt = 0;
-        for (int i = 0; i < n; ++i) {
-          if (i > 0 && ds->htid[static_cast<size_t>(i)] != ds->htid[static_cast<size_t>(i - 1)] && cnt >= kQT) {
-            bstart.push_back(i);
-            cnt = 0;
+      if (!ds->tile_meta) {  // per dataset (immutable): bucket starts and bounding box
+        std::vector<int>& bs = ds->tile_bstart;
+        bs.assign(1, 0);
+        if (ts) {
+          int cnt = 0;
+          for (int i = 0; i < n; ++i) {
+            if (i > 0 && ds->htid[static_cast<size_t>(i)] != ds->htid[static_cast<size_t>(i - 1)] && cnt >= kQT) {
+              bs.push_back(i);
+              cnt = 0;
+            }
+            ++cnt;
           }
-          ++cnt;
         }
-      }
-      bstart.push_back(n);
-      const int nbucket = static_cast<int>(bstart.size()) - 1;
-      double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
-      for (int i = 0; i < n; ++i) {
-        x0 = std::min(x0, ds->hx[i]);
-        x1 = std::max(x1, ds->hx[i]);
-        y0 = std::min(y0, ds->hy[i]);
-        y1 = std::max(y1, ds->hy[i]);
-      }
-      const double sx = x1 > x0 ? 65535.0 / (x1 - x0) : 0.0, sy = y1 > y0 ? 65535.0 / (y1 - y0) : 0.0;
-      auto spread = [](uint32_t v) {
-        v &= 0xffff;
-        v = (v | (v << 8)) & 0x00ff00ffu;
-        v = (v | (v << 4)) & 0x0f0f0f0fu;
-        v = (v | (v << 2)) & 0x33333333u;
-        v = (v | (v << 1)) & 0x55555555u;
-        return v;
-      };
-      // rows sorted by (bucket, Morton key) on the device: a stable radix sort keeps index order
-      // within equal keys
-      std::vector<uint64_t> key64(static_cast<size_t>(n));
-      {
-        int bb = 0;
+        bs.push_back(n);
+        double bx0 = INFINITY, bx1 = -INFINITY, by0 = INFINITY, by1 = -INFINITY;
         for (int i = 0; i < n; ++i) {
-          while (i >= bstart[static_cast<size_t>(bb) + 1]) ++bb;
-          const uint32_t mk = ts ? (spread(static_cast<uint32_t>((ds->hx[i] - x0) * sx)) |
-                                    (spread(static_cast<uint32_t>((ds->hy[i] - y0) * sy)) << 1))
-                                 : 0u;
-          key64[static_cast<size_t>(i)] = (static_cast<uint64_t>(bb) << 32) | mk;
+          bx0 = std::min(bx0, ds->hx[i]);
+          bx1 = std::max(bx1, ds->hx[i]);
+          by0 = std::min(by0, ds->hy[i]);
+          by1 = std::max(by1, ds->hy[i]);
         }
+        ds->tile_x0 = bx0;
+        ds->tile_x1 = bx1;
+        ds->tile_y0 = by0;
+        ds->tile_y1 = by1;
+        ds->tile_meta = true;
       }
+      const std::vector<int>& bstart = ds->tile_bstart;
+      const int nbucket = static_cast<int>(bstart.size()) - 1;
+      const double x0 = ds->tile_x0, x1 = ds->tile_x1, y0 = ds->tile_y0, y1 = ds->tile_y1;
+      const double sx = x1 > x0 ? 65535.0 / (x1 - x0) : 0.0, sy = y1 > y0 ? 65535.0 / (y1 - y0) : 0.0;
+      // rows sorted by (bucket, Morton key) on the device: a stable radix sort keeps index order
+      // within equal keys; the keys are formed on the device (the host loop cost ~7 ms at cfg4)
+      std::unique_ptr<uint64_t[]> key64(new uint64_t[static_cast<size_t>(n)]);  // filled by the download below
       lap("tiles:keys");
       DevBuf<int32_t> d_sp;
       DevBuf<uint64_t> d_keys_sorted;
       {
-        DevBuf<uint64_t> d_keys;
-        DevBuf<int32_t> d_iota;
-        d_keys.upload(key64.data(), key64.size(), st);
-        std::vector<int32_t> iota(static_cast<size_t>(n));
-        for (int i = 0; i < n; ++i) iota[static_cast<size_t>(i)] = i;
-        d_iota.upload(iota.data(), iota.size(), st);
+        DevBuf<uint64_t> d_keys(static_cast<size_t>(n));
+        DevBuf<int32_t> d_iota(static_cast<size_t>(n)), d_bstart;
+        d_bstart.upload(bstart.data(), bstart.size(), st);
+        tile_keys_kernel<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, st>>>(n, ds->x.get(), ds->y.get(), d_bstart.get(),
+                                                                           nbucket, ts, x0, y0, sx, sy, d_keys.get(),
+                                                                           d_iota.get());
+        launched(ctx);
         lap("tiles:upload");
         d_sp.alloc(static_cast<size_t>(n));
         d_keys_sorted.alloc(static_cast<size_t>(n));
@@ -1403,7 +1422,7 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
                                         n, 0, std::min(64, endbit), st);
         launched(ctx);
         lap("tiles:sort");
-        d_keys_sorted.download(key64.data(), key64.size(), st);  // sorted keys: tile anchors
+        d_keys_sorted.download(key64.get(), static_cast<size_t>(n), st);  // sorted keys: tile anchors
         STGP_CUDA(cudaStreamSynchronize(st));
       }
       std::vector<int32_t> toff, tbucket, btile0;

@@ -13,7 +13,7 @@ ds = S.SpaceTimeDataset(x, y, t, ctx=ctx)
 ctx.fp64_peak_tflops()
 ind = S.sts_kmeanspp(ds, 1000, 20260203)
 ctx.profile(True)
-for rep in range(3):
+for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 3):
     t0 = time.perf_counter()
     nb = S.residual_neighbors(ds, S.synth.THETA_T3, ind, 30)
     dt = time.perf_counter() - t0
