@@ -124,6 +124,23 @@ def test_dr_empty_inducing_equals_dc(S):
     assert (a == b).all()
 
 
+@pytest.mark.parametrize("spatial", ["0", "1"])
+def test_dc_both_search_kernels(S, monkeypatch, spatial):
+    # the d_c search runs on the time-block kernel or on the spatial-tile kernel (the default where
+    # equal-time blocks average >= 4096 rows, e.g. cfg4); both must return the oracle's sets and
+    # distances bit for bit, here on the cfg4 geometry with 4500 rows per day
+    monkeypatch.setenv("STGP_DC_SPATIAL", spatial)
+    x, y, t, _ = S.synth.station_day(4500, 3, box=(4.6e6, 2.9e6), theta=S.synth.THETA_T3, seed=33)
+    perm = O.order_observations(t, 33)
+    x, y, t = x[perm], y[perm], t[perm]
+    ds = S.SpaceTimeDataset(x, y, t)
+    nb = S.correlation_neighbors(ds, S.synth.THETA_T3, 30)
+    ref, rdist = O.dc_neighbors(x, y, t, S.synth.THETA_T3, 30, with_dist=True)
+    assert (nb.indices() == ref).all(), np.argwhere(nb.indices() != ref)[:5]
+    ok = ~np.isnan(rdist)
+    assert _bits(nb.distances()[ok], rdist[ok])
+
+
 def test_dr_spatial_pruning_geometry(S):
     # cfg4 geometry (Table 3 theta, 4600 x 2900 km box): spatial tiles, box-distance and
     # block-norm pruning and the early time stop are all active; exactness against the oracle
