@@ -311,7 +311,7 @@ def main():
         nn_s = time.perf_counter() - t0
         knn_ms = ctx.profile_get("knn_dr")[0] + ctx.profile_get("dr_whiten")[0]
         warm = []
-        for _ in range(3):  # warm repeats (identical sets)
+        for _ in range(5):  # warm repeats (identical sets); the median is reported
             t0 = time.perf_counter()
             nb = S.residual_neighbors(ds, theta, ind, args.m_v)
             warm.append(time.perf_counter() - t0)
@@ -334,7 +334,7 @@ def main():
         nn_s = time.perf_counter() - t0
         knn_ms = ctx.profile_get("knn_dc")[0] + ctx.profile_get("knn_dr")[0] + ctx.profile_get("dr_whiten")[0]
         warm = []
-        for _ in range(3):  # warm repeats (identical sets)
+        for _ in range(5):  # warm repeats (identical sets); the median is reported
             t0 = time.perf_counter()
             nb = S.correlation_neighbors(ds, theta, args.m_v)
             warm.append(time.perf_counter() - t0)
