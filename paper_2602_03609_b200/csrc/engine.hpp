@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -116,7 +117,9 @@ struct stgp_dataset {
   stgp::DevBuf<double> resp, X;
   int p = 0;
   bool has_resp = false;
-  // spatial-tile search meta (selection.cu), computed on first use: time buckets and bounding box
+  // spatial-tile search meta (selection.cu), computed on first use under tile_mu: time buckets and
+  // bounding box
+  std::mutex tile_mu;
   bool tile_meta = false;
   std::vector<int> tile_bstart;
   double tile_x0 = 0, tile_x1 = 0, tile_y0 = 0, tile_y1 = 0;

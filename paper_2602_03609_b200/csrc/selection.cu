@@ -1364,6 +1364,7 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
       // the Morton code of (x, y), cut into tiles of <= 64 rows; one index-order bucket when the rows
       // are not time sorted (no pruning: plain exact brute force over predecessors).
       const bool ts = ds->time_sorted;
+      std::unique_lock<std::mutex> meta_lock(ds->tile_mu);
       if (!ds->tile_meta) {  // per dataset (immutable): bucket starts and bounding box
         std::vector<int>& bs = ds->tile_bstart;
         bs.assign(1, 0);
@@ -1391,6 +1392,7 @@ stgp_neighbors* spatial_search(stgp_dataset* ds, const Params& p, const std::vec
         ds->tile_y1 = by1;
         ds->tile_meta = true;
       }
+      meta_lock.unlock();  // written once, read-only from here on
       const std::vector<int>& bstart = ds->tile_bstart;
       const int nbucket = static_cast<int>(bstart.size()) - 1;
       const double x0 = ds->tile_x0, x1 = ds->tile_x1, y0 = ds->tile_y0, y1 = ds->tile_y1;
