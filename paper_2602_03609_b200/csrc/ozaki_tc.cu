@@ -456,13 +456,18 @@ void dispatch(stgp_ctx* ctx, int S, const CUtensorMap& tx, const CUtensorMap& ty
 // shapes (tests/test_gpu_ozaki.py timing cases): rows form 5.12 / 5.39 / 6.03 ms and column form
 // 18.99 / 20.96 / 20.97 ms at CL = 1 / 2 / 4 -- the kernel is not bound by L2 operand traffic, and the
 // cluster-wide stage release couples the CTAs' pipelines.
-int cluster_size() {
-  static const int cl = [] {
+// X-tile multicast cluster size per product form (STGP_OZAKI_CLUSTER=1|2|4 overrides all).  Measured at
+// cfg4 (A/B, one box): the rows form (X = K^-1 V') and the symmetric column form (K) run best with
+// pairs (24.8 -> 23.6 and 23.5 -> 22.9 ms), the general column form (V'F^T) with quads (30.0 -> 29.0 ms).
+enum class TcForm { kRows, kColsSym, kCols };
+int cluster_size(TcForm f) {
+  static const int env = [] {
     const char* e = std::getenv("STGP_OZAKI_CLUSTER");
-    const int v = e ? std::atoi(e) : 1;
-    return v == 1 || v == 2 || v == 4 ? v : 1;
+    const int v = e ? std::atoi(e) : 0;
+    return v == 1 || v == 2 || v == 4 ? v : 0;
   }();
-  return cl;
+  if (env) return env;
+  return f == TcForm::kCols ? 4 : 2;
 }
 
 void run(stgp_ctx* ctx, int S, int CL, const CUtensorMap& tx, const CUtensorMap& ty, const TcArgs& a) {
@@ -492,7 +497,7 @@ void ozaki_tc_rows(stgp_ctx* ctx, OzakiTcState*& st, int S, int kp, long long nx
   if (kp % kBK) throw Error(kInternal, "ozaki_tc_rows: kp must be a multiple of 32");
   OzakiTcState* s = tc_state(st);
   const long long ldk = static_cast<long long>(S) * kp;
-  const int CL = cluster_size();
+  const int CL = cluster_size(TcForm::kRows);
   const CUtensorMap tx = make_map(xd, kp, S, nx, 1, kp, ldk, nx * ldk, kBM / CL);
   const CUtensorMap ty = make_map(yd, kp, S, ny, 1, kp, ldk, static_cast<long long>(ny) * ldk, kBN);
   const int tiles_x = static_cast<int>((nx + kBM - 1) / kBM), tiles_y = (ny + kBN - 1) / kBN;
@@ -530,7 +535,7 @@ void ozaki_tc_cols(stgp_ctx* ctx, OzakiTcState*& st, int S, int L, int nch, int 
   if (L % kBK) throw Error(kInternal, "ozaki_tc_cols: L must be a multiple of 32");
   OzakiTcState* s = tc_state(st);
   const long long rs = static_cast<long long>(S) * L;
-  const int CL = cluster_size();
+  const int CL = cluster_size(symmetric ? TcForm::kColsSym : TcForm::kCols);
   const CUtensorMap tx = make_map(xd, L, S, m, nch, L, rs, static_cast<long long>(m) * rs, kBM / CL);
   const CUtensorMap ty = make_map(yd, L, S, m, nch, L, rs, static_cast<long long>(m) * rs, kBN);
   const int tiles_x = (m + kBM - 1) / kBM, tiles_y = (m + kBN - 1) / kBN;
