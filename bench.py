@@ -173,6 +173,14 @@ def vif_rows_flops(nbr_counts, M):
     return float(np.sum(2 * ((ck + k + 2) * M + k ** 3 / 6 + 2 * k ** 2) + ck * (KE_FLOP + KG_FLOP)))
 
 
+def vif_build_rows_flops(nbr_counts, M):
+    """canonical work of the VIF build row kernel (vecchia_rows_kernel<build>): closure Gram c_k M FMA,
+    Cholesky k^3/6 and one solve k^2 FMA, and c_k covariance evaluations (KE)."""
+    k = nbr_counts.astype(np.float64)
+    ck = (k + 1) * (k + 2) / 2
+    return float(np.sum(2 * (ck * M + k ** 3 / 6 + k ** 2) + ck * KE_FLOP))
+
+
 def fitc_flops(n, M):
     """canonical FP64 work of one FITC NLL+grad: W = L_m^{-1} U, K = I + W Lambda^{-1} W^T (symmetric),
     K^{-1} W, W diag(phi) W^T (symmetric), omega = L_m^{-T} omega' -> 3 n M^2 FMA, plus n M KE and KG."""
@@ -391,10 +399,11 @@ def main():
         return ms_ / max(cnt_, 1)
 
     if args.workload == "vif":
-        kname = ("VIF row pass: vecchia_rows_kernel<build> (closure Gram by DMMA, Cholesky) + "
-                 "tile_ga_kernel (Ga over tile-staged closure columns) + vif_grad_stored_kernel (Phi_i, KG)")
-        k_avg = region_avg("rows") + region_avg("g_ga") + region_avg("rows_vifgrad")
-        flops_launch = vif_rows_flops(counts[lo:hi], M)
+        # the dominant kernel of the step (15% of it): the closure rows of the build
+        kname = ("vecchia_rows_kernel<build>: closure Gram W_cl^T W_cl on DMMA, closure covariances, register "
+                 "Cholesky, A and D per row")
+        k_avg = region_avg("rows")
+        flops_launch = vif_build_rows_flops(counts[lo:hi], M)
         step_flops = vif_flops(counts, M)
     elif args.workload == "fitc":
         # FITC's dominant FP64 kernel: the triangular W = L_m^{-1} U (M (M + 1) / 2 FMA per column); the
@@ -411,16 +420,13 @@ def main():
     achieved = flops_launch / (k_avg * 1e-3) / 1e12
     # DRAM bytes of the row pass from one ncu --set full capture per kernel (cfg4, N = 1):
     # dram__bytes_read.sum + dram__bytes_write.sum, profiles/r01/rows_{build,grad}_full_ncu.txt
-    traffic = (14.260330e9 + 5.761680e9 + 24.167864e9 + 0.286370e9 + VIFGRAD_DRAM) if (
-        args.workload == "vif" and (args.stations, args.days) == (10000, 110) and world == 1) else None
+    cfg4_1 = args.workload == "vif" and (args.stations, args.days) == (10000, 110) and world == 1
+    traffic = (14.260330e9 + 5.761680e9) if cfg4_1 else None
     breakdown = {k: round(ms_ / max(c_, 1), 3) for k, (ms_, c_) in sorted(prof.items(), key=lambda kv: -kv[1][0])}
     roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
             "frac": achieved / fp64_peak, "traffic": traffic,
-            "traffic_source": ("ncu --set full dram__bytes_read+write, one capture each at cfg4: "
-                               "vecchia_rows_kernel<build> 20.02 GB (profiles/r02/v5/full_vecchia_rows_kernel.txt) + "
-                               "tile_ga_kernel 24.45 GB (profiles/r02/full_tile_ga.txt) + vif_grad_stored_kernel "
-                               f"{VIFGRAD_DRAM / 1e9:.2f} GB (profiles/r02/v5/full_vif_grad_stored_kernel.txt)")
-            if traffic else None,
+            "traffic_source": ("ncu --set full dram__bytes_read+write of vecchia_rows_kernel<build> at cfg4 "
+                               "(profiles/r02/v5/full_vecchia_rows_kernel.txt)") if traffic else None,
             "kernel": kname, "kernel_ms": k_avg,
             "kernel_share": k_avg / ms_step, "flop_per_launch": flops_launch,
             "peak_source": (f"measured in-run: max of DMMA m8n8k4 ({dmma_peak:.1f}) and DFMA ({dfma_peak:.1f}) "
@@ -430,6 +436,14 @@ def main():
             "step_canonical_flop": step_flops, "step_fp64_equiv_tflops": step_flops / (ms_step * 1e-3) / 1e12,
             "step_fp64_equiv_frac": step_flops / (ms_step * 1e-3) / 1e12 / fp64_peak,
             "phase_ms": breakdown}
+    if args.workload == "vif":
+        # the whole closure-row pass of an evaluation: build rows + Ga (tile SDDMM) + gradient rows
+        rp_ms = region_avg("rows") + region_avg("g_ga") + region_avg("rows_vifgrad")
+        rp_flops = vif_rows_flops(counts[lo:hi], M)
+        roof["row_pass"] = {
+            "kernels": "vecchia_rows_kernel<build> + tile_ga_kernel + vif_grad_stored_kernel", "kernel_ms": rp_ms,
+            "achieved": rp_flops / (rp_ms * 1e-3) / 1e12, "frac": rp_flops / (rp_ms * 1e-3) / 1e12 / fp64_peak,
+            "traffic": (14.260330e9 + 5.761680e9 + 24.167864e9 + 0.286370e9 + VIFGRAD_DRAM) if cfg4_1 else None}
     # the FP64 products that run on the int8 tensor cores (Ozaki slicing, csrc/ozaki.cu): X = K^-1 V'
     # (FITC: K^-1 W), K = S S^T and V'F^T (FITC: W diag(phi) W^T), each S(S+1)/2 int8 MACs per FP64 FMA
     # (S = 6 slices for the row form, 7 for the long reductions)
