@@ -452,10 +452,6 @@ void dispatch(stgp_ctx* ctx, int S, const CUtensorMap& tx, const CUtensorMap& ty
   }
 }
 
-// cluster size of the X multicast (STGP_OZAKI_CLUSTER: 1, 2 or 4; default 1).  Measured at the cfg4
-// shapes (tests/test_gpu_ozaki.py timing cases): rows form 5.12 / 5.39 / 6.03 ms and column form
-// 18.99 / 20.96 / 20.97 ms at CL = 1 / 2 / 4 -- the kernel is not bound by L2 operand traffic, and the
-// cluster-wide stage release couples the CTAs' pipelines.
 // X-tile multicast cluster size per product form (STGP_OZAKI_CLUSTER=1|2|4 overrides all).  Measured at
 // cfg4 (A/B, one box): the rows form (X = K^-1 V') and the symmetric column form (K) run best with
 // pairs (24.8 -> 23.6 and 23.5 -> 22.9 ms), the general column form (V'F^T) with quads (30.0 -> 29.0 ms).
