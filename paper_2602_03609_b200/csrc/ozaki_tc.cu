@@ -152,12 +152,15 @@ __device__ __forceinline__ void chunk_range(const TcArgs& a, int g, int& c0, int
   c1 = static_cast<int>(static_cast<long long>(a.nchunks) * (g + 1) / a.groups);
 }
 
-// CL > 1: clusters of CL CTAs along the Y tiles share one X tile, each CTA loading 128 / CL of its rows
-// and multicasting them to the whole cluster (half the operand bytes per MMA at CL = 4); the stages are
-// released by every CTA's MMA commit (multicast arrive), items are cluster items (x, y group, group).
-template <int S, int CL>
+// Clusters of CX x CY CTAs (rank r = rx CY + ry) compute CX X tiles x CY Y tiles.  The CY CTAs of one
+// X tile (same rx) each load 128 / CY of its rows and multicast them to the others; the CX CTAs of one
+// Y tile (same ry) each load 64 / CX of its rows likewise.  A stage slot is written by the CTA's X
+// group and Y group (CX + CY - 1 CTAs), so each CTA's MMA commit arrives on the empty barrier of every
+// CTA of both groups.  Items are cluster items (x group, y group, split group).
+template <int S, int CX, int CY>
 __global__ void __launch_bounds__(kThreads, 1)
     ozaki_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy, TcArgs a) {
+  constexpr int CL = CX * CY;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte aligned stage buffers: [stage][X slices S x 4 KB | Y slices S x 2 KB]
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -170,12 +173,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = CL > 1 ? static_cast<int>(cluster_rank()) : 0;
+  const int rx = rank / CY, ry = rank % CY;
   const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
-  constexpr uint16_t kMask = static_cast<uint16_t>((1u << CL) - 1);
+  // multicast masks: the X group (same rx) and the Y group (same ry); their union releases the stages
+  uint16_t mask_x = 0, mask_y = 0;
+  for (int j = 0; j < CY; ++j) mask_x |= static_cast<uint16_t>(1u << (rx * CY + j));
+  for (int i = 0; i < CX; ++i) mask_y |= static_cast<uint16_t>(1u << (i * CY + ry));
+  const uint16_t mask_xy = static_cast<uint16_t>(mask_x | mask_y);
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], CL);
+      mbar_init(&empty[i], CX + CY - 1);
     }
     mbar_init(tmem_full, 1);
     mbar_init(tmem_empty, 4);
@@ -202,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int it = cid; it < a.nitems; it += ncl) {
         const int4 job = a.items[it];
-        const int yt = job.y * CL + rank;
+        const int xt = job.x * CX + rx, yt = job.y * CY + ry;
         int c0, c1;
         chunk_range(a, job.z, c0, c1);
         for (int c = c0; c < c1; ++c)
@@ -212,16 +220,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_expect_tx(&full[stage], kStageBytes);
 #pragma unroll
             for (int s = 1; s <= S; ++s) {
-              if (CL == 1)
-                tma_load4(&tmx, st + (s - 1) * kTileX, &full[stage], kb * kBK, a.x_rev ? S - s : s - 1, job.x * kBM, c);
+              if (CY == 1)
+                tma_load4(&tmx, st + (s - 1) * kTileX, &full[stage], kb * kBK, a.x_rev ? S - s : s - 1, xt * kBM, c);
               else
-                tma_load4_mc(&tmx, st + (s - 1) * kTileX + rank * (kTileX / CL), &full[stage], kb * kBK,
-                             a.x_rev ? S - s : s - 1, job.x * kBM + rank * (kBM / CL), c, kMask);
+                tma_load4_mc(&tmx, st + (s - 1) * kTileX + ry * (kTileX / CY), &full[stage], kb * kBK,
+                             a.x_rev ? S - s : s - 1, xt * kBM + ry * (kBM / CY), c, mask_x);
             }
 #pragma unroll
-            for (int t = 1; t <= S; ++t)
-              tma_load4(&tmy, st + S * kTileX + (t - 1) * kTileY, &full[stage], kb * kBK, a.y_rev ? S - t : t - 1,
-                        yt * kBN, c);
+            for (int t = 1; t <= S; ++t) {
+              if (CX == 1)
+                tma_load4(&tmy, st + S * kTileX + (t - 1) * kTileY, &full[stage], kb * kBK, a.y_rev ? S - t : t - 1,
+                          yt * kBN, c);
+              else
+                tma_load4_mc(&tmy, st + S * kTileX + (t - 1) * kTileY + rx * (kTileY / CX), &full[stage], kb * kBK,
+                             a.y_rev ? S - t : t - 1, yt * kBN + rx * (kBN / CX), c, mask_y);
+            }
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1;
@@ -263,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             if (CL == 1) mma_commit(&empty[stage]);  // frees the stage once these MMAs have read it
-            else mma_commit_mc(&empty[stage], kMask);  // in every CTA of the cluster (their X pieces)
+            else mma_commit_mc(&empty[stage], mask_xy);  // in every CTA that writes into this CTA's stages
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1;
@@ -283,8 +296,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int4 job = a.items[it];
       int c0, c1;
       chunk_range(a, job.z, c0, c1);
-      const int x = job.x * kBM + quarter * 32 + lane;
-      const int y0 = (job.y * CL + rank) * kBN;
+      const int x = (job.x * CX + rx) * kBM + quarter * 32 + lane;
+      const int y0 = (job.y * CY + ry) * kBN;
       double acc[kBN];
 #pragma unroll
       for (int e = 0; e < kBN; ++e) acc[e] = 0.0;
@@ -396,13 +409,14 @@ CUtensorMap make_map(const int8_t* base, long long kext, int S, long long rows, 
   return m;
 }
 
-template <int S, int CL>
+template <int S, int CX, int CY>
 void launch_tc(stgp_ctx* ctx, const CUtensorMap& tx, const CUtensorMap& ty, const TcArgs& a) {
+  constexpr int CL = CX * CY;
   // at least 116 KB so that one CTA holds an SM: it owns all 512 TMEM columns
   constexpr int smem = std::max(kStages * S * (kTileX + kTileY) + 1024 + 256, 116 * 1024);
   static int max_clusters = 0;
   if (max_clusters == 0) {
-    STGP_CUDA(cudaFuncSetAttribute(ozaki_tc_kernel<S, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    STGP_CUDA(cudaFuncSetAttribute(ozaki_tc_kernel<S, CX, CY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     max_clusters = ctx->num_sms / CL;
     if (CL > 1) {
       cudaLaunchConfig_t q{};
@@ -417,7 +431,8 @@ void launch_tc(stgp_ctx* ctx, const CUtensorMap& tx, const CUtensorMap& ty, cons
       q.attrs = at;
       q.numAttrs = 1;
       int mc = 0;
-      if (cudaOccupancyMaxActiveClusters(&mc, ozaki_tc_kernel<S, CL>, &q) == cudaSuccess && mc > 0) max_clusters = mc;
+      if (cudaOccupancyMaxActiveClusters(&mc, ozaki_tc_kernel<S, CX, CY>, &q) == cudaSuccess && mc > 0)
+        max_clusters = mc;
       (void)cudaGetLastError();
     }
   }
@@ -434,42 +449,61 @@ void launch_tc(stgp_ctx* ctx, const CUtensorMap& tx, const CUtensorMap& ty, cons
   cfg.stream = ctx->stream;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  STGP_CUDA(cudaLaunchKernelEx(&cfg, ozaki_tc_kernel<S, CL>, tx, ty, a));
+  STGP_CUDA(cudaLaunchKernelEx(&cfg, ozaki_tc_kernel<S, CX, CY>, tx, ty, a));
   launched(ctx);
 }
 
-template <int CL>
+template <int CX, int CY>
 void dispatch(stgp_ctx* ctx, int S, const CUtensorMap& tx, const CUtensorMap& ty, const TcArgs& a) {
   switch (S) {
-    case 2: launch_tc<2, CL>(ctx, tx, ty, a); break;
-    case 3: launch_tc<3, CL>(ctx, tx, ty, a); break;
-    case 4: launch_tc<4, CL>(ctx, tx, ty, a); break;
-    case 5: launch_tc<5, CL>(ctx, tx, ty, a); break;
-    case 6: launch_tc<6, CL>(ctx, tx, ty, a); break;
-    case 7: launch_tc<7, CL>(ctx, tx, ty, a); break;
-    case 8: launch_tc<8, CL>(ctx, tx, ty, a); break;
+    case 2: launch_tc<2, CX, CY>(ctx, tx, ty, a); break;
+    case 3: launch_tc<3, CX, CY>(ctx, tx, ty, a); break;
+    case 4: launch_tc<4, CX, CY>(ctx, tx, ty, a); break;
+    case 5: launch_tc<5, CX, CY>(ctx, tx, ty, a); break;
+    case 6: launch_tc<6, CX, CY>(ctx, tx, ty, a); break;
+    case 7: launch_tc<7, CX, CY>(ctx, tx, ty, a); break;
+    case 8: launch_tc<8, CX, CY>(ctx, tx, ty, a); break;
     default: throw Error(kConfig, "ozaki_tc: slice count must lie in [2, 8]");
   }
 }
 
-// X-tile multicast cluster size per product form (STGP_OZAKI_CLUSTER=1|2|4 overrides all).  Measured at
+// Cluster shape per product form: CY CTAs share (multicast) an X tile, CX CTAs a Y tile.
+// STGP_OZAKI_CLUSTER=1|2|4 sets CY and STGP_OZAKI_CLUSTER_X=1|2 sets CX for every form.  Measured at
 // cfg4 (A/B, one box): the rows form (X = K^-1 V') and the symmetric column form (K) run best with
-// pairs (24.8 -> 23.6 and 23.5 -> 22.9 ms), the general column form (V'F^T) with quads (30.0 -> 29.0 ms).
+// CY = 2 (24.8 -> 23.6 and 23.5 -> 22.9 ms), the general column form (V'F^T) with CY = 4 (30.0 -> 29.0 ms).
 enum class TcForm { kRows, kColsSym, kCols };
-int cluster_size(TcForm f) {
-  static const int env = [] {
+struct TcCluster {
+  int cx, cy;
+};
+TcCluster cluster_shape(TcForm f) {
+  static const int env_y = [] {
     const char* e = std::getenv("STGP_OZAKI_CLUSTER");
     const int v = e ? std::atoi(e) : 0;
     return v == 1 || v == 2 || v == 4 ? v : 0;
   }();
-  if (env) return env;
-  return f == TcForm::kCols ? 4 : 2;
+  static const int env_x = [] {
+    const char* e = std::getenv("STGP_OZAKI_CLUSTER_X");
+    const int v = e ? std::atoi(e) : 0;
+    return v == 1 || v == 2 ? v : 0;
+  }();
+  TcCluster c{1, f == TcForm::kCols ? 4 : 2};
+  if (env_y) c.cy = env_y;
+  if (env_x) c.cx = env_x;
+  if (c.cx * c.cy > 4) c.cy = 4 / c.cx;  // instantiated shapes: 1x1, 1x2, 1x4, 2x1, 2x2
+  return c;
 }
 
-void run(stgp_ctx* ctx, int S, int CL, const CUtensorMap& tx, const CUtensorMap& ty, const TcArgs& a) {
-  if (CL == 4) dispatch<4>(ctx, S, tx, ty, a);
-  else if (CL == 2) dispatch<2>(ctx, S, tx, ty, a);
-  else dispatch<1>(ctx, S, tx, ty, a);
+void run(stgp_ctx* ctx, int S, TcCluster c, const CUtensorMap& tx, const CUtensorMap& ty, const TcArgs& a) {
+  if (c.cx == 2) {
+    if (c.cy == 2) dispatch<2, 2>(ctx, S, tx, ty, a);
+    else dispatch<2, 1>(ctx, S, tx, ty, a);
+  } else if (c.cy == 4) {
+    dispatch<1, 4>(ctx, S, tx, ty, a);
+  } else if (c.cy == 2) {
+    dispatch<1, 2>(ctx, S, tx, ty, a);
+  } else {
+    dispatch<1, 1>(ctx, S, tx, ty, a);
+  }
 }
 
 }  // namespace
@@ -493,15 +527,15 @@ void ozaki_tc_rows(stgp_ctx* ctx, OzakiTcState*& st, int S, int kp, long long nx
   if (kp % kBK) throw Error(kInternal, "ozaki_tc_rows: kp must be a multiple of 32");
   OzakiTcState* s = tc_state(st);
   const long long ldk = static_cast<long long>(S) * kp;
-  const int CL = cluster_size(TcForm::kRows);
-  const CUtensorMap tx = make_map(xd, kp, S, nx, 1, kp, ldk, nx * ldk, kBM / CL);
-  const CUtensorMap ty = make_map(yd, kp, S, ny, 1, kp, ldk, static_cast<long long>(ny) * ldk, kBN);
+  const TcCluster cs = cluster_shape(TcForm::kRows);
+  const CUtensorMap tx = make_map(xd, kp, S, nx, 1, kp, ldk, nx * ldk, kBM / cs.cy);
+  const CUtensorMap ty = make_map(yd, kp, S, ny, 1, kp, ldk, static_cast<long long>(ny) * ldk, kBN / cs.cx);
   const int tiles_x = static_cast<int>((nx + kBM - 1) / kBM), tiles_y = (ny + kBN - 1) / kBN;
-  const int groups_y = (tiles_y + CL - 1) / CL;
+  const int groups_x = (tiles_x + cs.cx - 1) / cs.cx, groups_y = (tiles_y + cs.cy - 1) / cs.cy;
   std::vector<int4> items;
-  items.reserve(static_cast<size_t>(tiles_x) * groups_y);
-  for (int bx = 0; bx < tiles_x; ++bx)  // Y groups fastest: the clusters in flight share one X block in L2
-    for (int gy = 0; gy < groups_y; ++gy) items.push_back(make_int4(bx, gy, 0, 0));
+  items.reserve(static_cast<size_t>(groups_x) * groups_y);
+  for (int gx = 0; gx < groups_x; ++gx)  // Y groups fastest: the clusters in flight share one X block in L2
+    for (int gy = 0; gy < groups_y; ++gy) items.push_back(make_int4(gx, gy, 0, 0));
   s->items.upload(items.data(), items.size(), ctx->stream);
   TcArgs a{};
   a.S = S;
@@ -519,7 +553,7 @@ void ozaki_tc_rows(stgp_ctx* ctx, OzakiTcState*& st, int S, int kp, long long nx
   a.sy = sy;
   a.out = out;
   a.ldo = ldo;
-  run(ctx, S, CL, tx, ty, a);
+  run(ctx, S, cs, tx, ty, a);
 }
 
 // cols form: C[x ldc + y] = sum_c (sx[c m + x] sy[c m + y]) sum_d 2^-7d sum_{s+t=d} X_s,c[x] . Y_t,c[y];
@@ -531,15 +565,16 @@ void ozaki_tc_cols(stgp_ctx* ctx, OzakiTcState*& st, int S, int L, int nch, int 
   if (L % kBK) throw Error(kInternal, "ozaki_tc_cols: L must be a multiple of 32");
   OzakiTcState* s = tc_state(st);
   const long long rs = static_cast<long long>(S) * L;
-  const int CL = cluster_size(symmetric ? TcForm::kColsSym : TcForm::kCols);
-  const CUtensorMap tx = make_map(xd, L, S, m, nch, L, rs, static_cast<long long>(m) * rs, kBM / CL);
-  const CUtensorMap ty = make_map(yd, L, S, m, nch, L, rs, static_cast<long long>(m) * rs, kBN);
+  const TcCluster cs = cluster_shape(symmetric ? TcForm::kColsSym : TcForm::kCols);
+  const int CL = cs.cx * cs.cy;
+  const CUtensorMap tx = make_map(xd, L, S, m, nch, L, rs, static_cast<long long>(m) * rs, kBM / cs.cy);
+  const CUtensorMap ty = make_map(yd, L, S, m, nch, L, rs, static_cast<long long>(m) * rs, kBN / cs.cx);
   const int tiles_x = (m + kBM - 1) / kBM, tiles_y = (m + kBN - 1) / kBN;
-  const int groups_y = (tiles_y + CL - 1) / CL;
-  std::vector<int2> tiles;  // (x tile, y group): kept when one of its y tiles reaches the lower triangle
-  for (int bx = 0; bx < tiles_x; ++bx)
+  const int groups_x = (tiles_x + cs.cx - 1) / cs.cx, groups_y = (tiles_y + cs.cy - 1) / cs.cy;
+  std::vector<int2> tiles;  // (x group, y group): kept when one of its tiles reaches the lower triangle
+  for (int gx = 0; gx < groups_x; ++gx)
     for (int gy = 0; gy < groups_y; ++gy)
-      if (!symmetric || gy * CL * kBN < (bx + 1) * kBM) tiles.push_back(make_int2(bx, gy));
+      if (!symmetric || gy * cs.cy * kBN < (gx + 1) * cs.cx * kBM) tiles.push_back(make_int2(gx, gy));
   // split the chunks of each tile over G clusters so the work items fill whole waves of the SMs
   const int nt = static_cast<int>(tiles.size());
   const int slots = std::max(1, ctx->num_sms / CL);
@@ -582,7 +617,7 @@ void ozaki_tc_cols(stgp_ctx* ctx, OzakiTcState*& st, int S, int L, int nch, int 
     a.out = C;
     a.ldo = ldc;
   }
-  run(ctx, S, CL, tx, ty, a);
+  run(ctx, S, cs, tx, ty, a);
   if (G > 1) {
     reduce_groups_kernel<<<grid_for(static_cast<long long>(m) * m, 256), 256, 0, ctx->stream>>>(
         m, m, G, s->part.get(), ldp, a.part_stride, C, ldc);
