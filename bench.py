@@ -406,9 +406,9 @@ def main():
         flops_launch = vif_build_rows_flops(counts[lo:hi], M)
         step_flops = vif_flops(counts, M)
     elif args.workload == "fitc":
-        # FITC's dominant FP64 kernel: the triangular W = L_m^{-1} U (M (M + 1) / 2 FMA per column); the
-        # K, K^{-1} W and W diag(phi) W^T products run on the int8 tensor cores (roofline int8_tensor)
-        kname = "W = L_m^{-1} U: dgemm_kernel<0,0> (DMMA TRMM over the triangle's K range)"
+        # FITC is n M^2 products throughout, all on the int8 tensor cores (the int8_tensor object below
+        # becomes the line's roofline); W = L_m^{-1} U is kept here as its FP64-equivalent rate
+        kname = "W = L_m^{-1} U (triangle-cut Ozaki rows form on ozaki_tc_kernel), FP64-equivalent"
         k_avg = region_avg("W_trmm")
         flops_launch = float(M) * (M + 1) * (hi - lo)
         step_flops = fitc_flops(n, M)
@@ -445,8 +445,9 @@ def main():
             "achieved": rp_flops / (rp_ms * 1e-3) / 1e12, "frac": rp_flops / (rp_ms * 1e-3) / 1e12 / fp64_peak,
             "traffic": (14.260330e9 + 5.761680e9 + 24.167864e9 + 0.286370e9 + VIFGRAD_DRAM) if cfg4_1 else None}
     # the FP64 products that run on the int8 tensor cores (Ozaki slicing, csrc/ozaki.cu): X = K^-1 V'
-    # (FITC: K^-1 W), K = S S^T and V'F^T (FITC: W diag(phi) W^T), each S(S+1)/2 int8 MACs per FP64 FMA
-    # (S = 6 slices for the row form, 7 for the long reductions)
+    # (FITC: K^-1 W), K = S S^T and V'F^T (FITC: W diag(phi) W^T), and the triangular W = L_m^-1 U and
+    # omega = L_m^-T omega', each S(S+1)/2 int8 MACs per FP64 FMA (S = 6 slices for the row form, 7 for
+    # the long reductions and the triangular products)
     # per evaluation: the region total over the evaluations profiled (timed steps and e2e steps alike)
     oz_ms = prof.get("oz_imma", (0.0, 0))[0] / max(prof.get("K_gemm_chol", (0.0, 1))[1], 1)
     if args.workload in ("vif", "fitc") and oz_ms > 0:
@@ -456,8 +457,12 @@ def main():
         ldm = (M + 15) // 16 * 16
         # X (rows form, full) and V'F^T (full), K = S S^T symmetric: its lower half (the kernel computes only
         # the tiles that reach the lower triangle and mirrors)
-        pr_, pc_ = s_rows * (s_rows + 1) / 2, s_cols * (s_cols + 1) / 2
+        s_tri = int(os.environ.get("STGP_OZAKI_S_TRMM", s_all or 7))
+        pr_, pc_, pt_ = s_rows * (s_rows + 1) / 2, s_cols * (s_cols + 1) / 2, s_tri * (s_tri + 1) / 2
         int8_ops = 2.0 * (pr_ + pc_) * ldm * ldm * (hi - lo) + pc_ * ldm * (ldm + 1) * (hi - lo)
+        if os.environ.get("STGP_OZAKI_TRMM", "1") != "0":
+            # two triangular products, M (M + 1) / 2 FMA per column each (algorithmic: the triangle)
+            int8_ops += 2 * 2.0 * pt_ * ldm * (ldm + 1) / 2 * (hi - lo)
         int8_peak = 2.0 * peaks().get("bf16_tflops", 1669.7)
         roof["int8_tensor"] = {
             "bound": "tensor", "achieved": int8_ops / (oz_ms * 1e-3) / 1e12, "peak": int8_peak, "unit": "TOPS",
@@ -465,6 +470,15 @@ def main():
             "kernel": "ozaki_tc_kernel: hand-written tcgen05.mma kind::i8 (TMA, per-diagonal TMEM accumulators, "
                       "FP64 epilogue) over the Ozaki slices",
             "peak_source": "2 x measured dense bf16 (MEASURED_PEAKS.json burst; B200 int8:bf16 dense = 2:1)"}
+        if args.workload == "fitc":
+            # FITC's dominant kernel is the tcgen05 product kernel: it becomes the line's roofline object
+            fp64_view = {k_: roof.pop(k_) for k_ in ("bound", "achieved", "peak", "unit", "frac", "traffic",
+                                                      "traffic_source", "kernel", "kernel_ms", "kernel_share",
+                                                      "flop_per_launch", "peak_source")}
+            roof.update(roof.pop("int8_tensor"))
+            roof["traffic"] = None
+            roof["kernel_share"] = oz_ms / ms_step
+            roof["W_trmm_fp64_equiv"] = fp64_view
     line = {"metric": METRIC, "value": 1e3 / ms_step, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",

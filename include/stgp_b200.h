@@ -249,14 +249,20 @@ int stgp_debug_dmma_peak(stgp_ctx* ctx, double* tflops);
 /* Names of the profiled regions recorded so far, newline separated (truncated to cap-1 bytes). */
 int stgp_ctx_profile_names(stgp_ctx* ctx, char* buf, int cap);
 /* FP64 product C[r][j] = sum_c A[r][c] B[j][c] (row-major host arrays, n x k, m x k -> n x m)
- * through the int8 Ozaki path (emulated = 1) or cuBLAS DGEMM (emulated = 0); *ms = device time
+ * through the int8 Ozaki path (emulated = 1) or the DMMA GEMM (emulated = 0); *ms = device time
  * of the product (inputs resident). */
 int stgp_debug_gemm_rows(stgp_ctx* ctx, int emulated, long long n, int m, int k, const double* A_host,
                          const double* B_host, double* C_host, double* ms);
 /* FP64 product C[j][i] = sum_r A[j + r m] B[i + r m] (column-major m x n host arrays -> m x m,
- * row-major C) through the int8 Ozaki path (emulated = 1) or cuBLAS DGEMM (emulated = 0). */
+ * row-major C) through the int8 Ozaki path (emulated = 1) or the DMMA GEMM (emulated = 0). */
 int stgp_debug_gemm_cols(stgp_ctx* ctx, int emulated, int m, long long n, const double* A_host,
                          const double* B_host, double* C_host, double* ms);
+/* Triangular product C = op(T) B (the W = L_m^-1 U and omega = L_m^-T omega' shape): T m x m lower
+ * triangular, B m x n, C m x n, all column-major host arrays; op(T) = T^T when transpose.  mode 0: the
+ * DMMA TRMM; 1: the int8 Ozaki rows form with each Y group's K range cut to the triangle; 2: the same
+ * over the full K range.  *ms = device time of the product (inputs resident). */
+int stgp_debug_trmm(stgp_ctx* ctx, int mode, int transpose, int m, long long n, const double* T_host,
+                    const double* B_host, double* C_host, double* ms);
 /* device Gneiting covariance / kernel gradient of (h, u) pairs with live factors; grad6_out may be
    NULL (covariances only).  A general nu (outside {0.5, 1.5, 2.5}) evaluates covariances through the
    Bessel-K Matern and returns STGP_ERR_NUMERIC when a gradient is requested (covariance.cpp:79-87). */

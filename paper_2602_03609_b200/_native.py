@@ -93,6 +93,7 @@ _SIGS = {
     "stgp_fit": [_P, _P, _P, C.c_int, _P, _P, C.POINTER(Params), _P, _D, C.POINTER(C.c_int), _P, C.c_int,
                  C.POINTER(C.c_int)],
     "stgp_debug_gemm_rows": [_P, C.c_int, C.c_longlong, C.c_int, C.c_int, _P, _P, _P, _D],
+    "stgp_debug_trmm": [_P, C.c_int, C.c_int, C.c_int, C.c_longlong, _P, _P, _P, _D],
     "stgp_debug_gemm_cols": [_P, C.c_int, C.c_int, C.c_longlong, _P, _P, _P, _D],
     "stgp_ctx_profile_names": [_P, C.c_char_p, C.c_int],
     "stgp_ctx_profile": [_P, C.c_int],

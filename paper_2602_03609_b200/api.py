@@ -122,6 +122,18 @@ class Context:
         N.call("stgp_debug_gemm_rows", self.h, int(emulated), n, m, k, _ptr(A), _ptr(B), _ptr(C_), C.byref(ms))
         return C_, ms.value
 
+    def trmm(self, T, B, transpose: bool = False, mode: int = 1):
+        """C = op(T) B for lower-triangular T (m x m) and B (m x n): mode 0 the DMMA TRMM, 1 the int8
+        Ozaki rows form with the triangle's K ranges, 2 the same over the full K range; returns
+        (C, device ms)."""
+        T = np.asfortranarray(T, dtype=np.float64)
+        B = np.asfortranarray(B, dtype=np.float64)
+        m, n = B.shape
+        C_ = np.zeros((m, n), order="F")
+        ms = C.c_double(0.0)
+        N.call("stgp_debug_trmm", self.h, int(mode), int(transpose), m, n, _ptr(T), _ptr(B), _ptr(C_), C.byref(ms))
+        return C_, ms.value
+
     def gemm_cols(self, A, B=None, emulated: bool = True):
         """C = A^T B (A, B: n x m, i.e. m x n column-major), C[j][i] = sum_r A[r, j] B[r, i]; the
         int8 Ozaki path for the long reduction or the DMMA GEMM.  B None: A^T A."""

@@ -779,6 +779,39 @@ int stgp_debug_gemm_rows(stgp_ctx* ctx, int emulated, long long n, int m, int k,
   });
 }
 
+int stgp_debug_trmm(stgp_ctx* ctx, int mode, int transpose, int m, long long n, const double* T_host,
+                    const double* B_host, double* C_host, double* ms) {
+  return guarded([&] {
+    if (!ctx || m <= 0 || m % 4 || n < 0 || mode < 0 || mode > 2 || !T_host || !B_host || !C_host)
+      config_error("stgp_debug_trmm: bad argument");
+    const size_t nb = static_cast<size_t>(m) * n;
+    DevBuf<double> T, B, C(std::max<size_t>(nb, 1));
+    T.upload(T_host, static_cast<size_t>(m) * m, ctx->stream);
+    B.upload(B_host, nb, ctx->stream);
+    auto run = [&] {
+      if (mode == 0)
+        dev_trmm_left(ctx, T.get(), m, m, B.get(), m, n, transpose != 0, C.get(), m);
+      else
+        ozaki_trmm_left(ctx, T.get(), m, m, B.get(), m, n, transpose != 0, C.get(), m, mode == 1);
+    };
+    run();
+    cudaEvent_t e0, e1;
+    STGP_CUDA(cudaEventCreate(&e0));
+    STGP_CUDA(cudaEventCreate(&e1));
+    STGP_CUDA(cudaEventRecord(e0, ctx->stream));
+    run();
+    STGP_CUDA(cudaEventRecord(e1, ctx->stream));
+    STGP_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    STGP_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (ms) *ms = t;
+    C.download(C_host, nb, ctx->stream);
+    STGP_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int stgp_debug_gemm_cols(stgp_ctx* ctx, int emulated, int m, long long n, const double* A_host,
                          const double* B_host, double* C_host, double* ms) {
   return guarded([&] {

@@ -247,7 +247,7 @@ void fitc_nll_grad(stgp_structure* s, double* nll, double* grad) {
         L.work1.get() + own);
     launched(ctx);
     ProfRegion pr(ctx, "f_omega_trmm_upair");
-    dev_trmm_left(ctx, L.Lminv.get(), ldm, ldm, L.work1.get() + own, ldm, nown, true, L.work2.get() + own, ldm);
+    lr_trmm(ctx, L.Lminv.get(), ldm, L.work1.get() + own, nown, true, L.work2.get() + own);
     std::vector<double> gu = upair_grad(s, L.work2.get(), rb, re);
     for (int q = 0; q < 6; ++q) g[1 + q] += gu[q];
   }

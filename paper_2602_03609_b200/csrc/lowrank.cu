@@ -668,8 +668,8 @@ void build_cross(stgp_structure* s, int c0, int c1, bool /*keep_U*/) {
     launched(ctx);
   }
   ProfRegion pr(ctx, "W_trmm");
-  dev_trmm_left(ctx, L.Lminv.get(), L.ldm, L.ldm, L.U.get() + static_cast<size_t>(c0) * L.ldm, L.ldm, c1 - c0, false,
-                L.W.get() + static_cast<size_t>(c0) * L.ldm, L.ldm);
+  lr_trmm(ctx, L.Lminv.get(), L.ldm, L.U.get() + static_cast<size_t>(c0) * L.ldm, c1 - c0, false,
+          L.W.get() + static_cast<size_t>(c0) * L.ldm);
 }
 
 void compute_halo(stgp_structure* s) {
@@ -773,6 +773,13 @@ double dev_sum_log(stgp_ctx* ctx, const double* v, long long n, Reducer& red) {
 }
 // Ws <- L_m^{-T} Ws L_m^{-1} with the basis' explicit inverse factor
 void transform_wsig(stgp_ctx* ctx, const double* Lminv, int ldm, double* Ws) { dev_congruence_t(ctx, Lminv, ldm, ldm, Ws); }
+
+void lr_trmm(stgp_ctx* ctx, const double* Lminv, int ldm, const double* B, long long ncols, bool transpose, double* C) {
+  if (ozaki_for(ldm) && ozaki_trmm_enabled())
+    ozaki_trmm_left(ctx, Lminv, ldm, ldm, B, ldm, ncols, transpose, C, ldm);
+  else
+    dev_trmm_left(ctx, Lminv, ldm, ldm, B, ldm, ncols, transpose, C, ldm);
+}
 std::vector<double> upair_grad(stgp_structure* s, const double* Om, int c0, int c1) {
   stgp_ctx* ctx = s->ds->ctx;
   const int ub = std::max(1, std::min(c1 - c0, ctx->num_sms * 8));
@@ -1020,7 +1027,7 @@ static void vif_grad(stgp_structure* s, double* nll_out, double* grad) {
                        L.work2.get());
     ph.reset(new ProfRegion(ctx, "g_omega_trmm"));
     L.work3.ensure(total);
-    dev_trmm_left(ctx, L.Lminv.get(), ldm, ldm, L.work2.get() + halo, ldm, re - hb, true, L.work3.get() + halo, ldm);
+    lr_trmm(ctx, L.Lminv.get(), ldm, L.work2.get() + halo, re - hb, true, L.work3.get() + halo);
   }
   // U-pair (this shard's omega) and Sigma_m-pair (rank 0) kernel gradients, then one all-reduce
   std::vector<double> g(7, 0.0);

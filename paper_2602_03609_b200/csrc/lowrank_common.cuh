@@ -32,6 +32,9 @@ double dev_sum(stgp_ctx* ctx, const double* v, long long n, Reducer& red);
 double dev_sum_log(stgp_ctx* ctx, const double* v, long long n, Reducer& red);
 // wsig = L_m^{-T} wsig' L_m^{-1} in place
 void transform_wsig(stgp_ctx* ctx, const double* Lminv, int ldm, double* Ws);
+// C = op(L_m^{-1}) B over ncols columns (ldm): the n x M^2 triangular products W = L_m^{-1} U and
+// omega = L_m^{-T} omega' -- the tcgen05 Ozaki rows form at M >= STGP_OZAKI_MIN_M, else the DMMA TRMM
+void lr_trmm(stgp_ctx* ctx, const double* Lminv, int ldm, const double* B, long long ncols, bool transpose, double* C);
 // sum_{j,i} Om(j,i) dk(z_j, p_i) and the Sigma_m-pair sum (6 components each)
 std::vector<double> upair_grad(stgp_structure* s, const double* Om, int c0, int c1);
 void add_identity(stgp_ctx* ctx, double* A, int ld);

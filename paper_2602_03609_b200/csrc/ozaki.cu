@@ -250,6 +250,7 @@ struct OzakiState {
   OzakiTcState* tc = nullptr;  // the tcgen05 kernel's work lists
   DevBuf<int8_t> As, Bs;
   DevBuf<double> sA, sB, colf, colf2;
+  DevBuf<double> Tt;  // transposed triangular factor (ozaki_trmm_left)
   DevBuf<int8_t> keep;  // forward digits of the last ozaki_syrk_keep operand (V' D^{-1/2})
   DevBuf<double> keep_s;
   uint64_t keep_tag = 0;
@@ -321,11 +322,10 @@ static OzakiState* state(stgp_ctx* ctx) {
   return ctx->ozaki;
 }
 
-void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, int lda, const double* B, int ldb,
-                     double* C, int ldc) {
+static void rows_product(stgp_ctx* ctx, int S, long long n, int m, int k, const double* A, int lda, const double* B,
+                         int ldb, double* C, int ldc, int tri = 0) {
   if (n <= 0 || m <= 0) return;
   if (m % 4 || ldc % 4) config_error("ozaki_gemm_rows: m and ldc must be multiples of 4");
-  const int S = slices_for("STGP_OZAKI_S_ROWS", 6);
   const int kp = (k + 31) / 32 * 32;  // slice stride: whole 32-byte K steps of the tcgen05 kernel
   if (static_cast<long long>(S) * kp * 127 * 127 >= (1LL << 31)) config_error("ozaki: k too large for exact int32");
   OzakiState* oz = state(ctx);
@@ -348,8 +348,55 @@ void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, 
     launched(ctx);
     ProfRegion pr(ctx, "oz_imma");
     ozaki_tc_rows(ctx, oz->tc, S, kp, nr, m, oz->As.get(), false, oz->sA.get(), oz->Bs.get(), true, oz->sB.get(),
-                  C + r0 * ldc, ldc);
+                  C + r0 * ldc, ldc, tri);
   }
+}
+
+void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, int lda, const double* B, int ldb,
+                     double* C, int ldc) {
+  rows_product(ctx, slices_for("STGP_OZAKI_S_ROWS", 6), n, m, k, A, lda, B, ldb, C, ldc);
+}
+
+// 32 x 32 tiles through shared memory (the M x M triangular factor, once per product)
+__global__ void transpose_kernel(int n, const double* __restrict__ T, int ldt, double* __restrict__ out) {
+  __shared__ double t[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = bx + threadIdx.x, j = by + r;
+    t[r][threadIdx.x] = (i < n && j < n) ? T[static_cast<size_t>(j) * ldt + i] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = by + threadIdx.x, j = bx + r;
+    if (i < n && j < n) out[static_cast<size_t>(j) * n + i] = t[threadIdx.x][r];
+  }
+}
+
+bool ozaki_trmm_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("STGP_OZAKI_TRMM");  // A/B switch: 0 = the DMMA TRMM
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
+void ozaki_trmm_left(stgp_ctx* ctx, const double* T, int ldt, int n, const double* B, int ldb, long long ncols,
+                     bool transpose, double* C, int ldc, bool skip) {
+  // C(:, r) = op(T) B(:, r): row r of the rows form is column r of B, the B operand's row j is row j
+  // of op(T) -- column j of T (transpose) or row j of T, transposed once into scratch
+  OzakiState* oz = state(ctx);
+  const double* rowsT = T;
+  int ldr = ldt;
+  if (!transpose) {
+    oz->Tt.ensure(static_cast<size_t>(n) * n);
+    transpose_kernel<<<dim3((n + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, ctx->stream>>>(n, T, ldt, oz->Tt.get());
+    launched(ctx);
+    rowsT = oz->Tt.get();
+    ldr = n;
+  }
+  // rows of T^T (columns of T) vanish before the diagonal, rows of T beyond it
+  rows_product(ctx, slices_for("STGP_OZAKI_S_TRMM", 7), ncols, n, n, B, ldb, rowsT, ldr, C, ldc,
+               skip ? (transpose ? 2 : 1) : 0);
 }
 
 // Column-form product C[j ldc + i] = sum_r (fA_r A[j + r lda]) (fB_r B[i + r ldb]) with optional

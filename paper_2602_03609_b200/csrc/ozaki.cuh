@@ -15,6 +15,11 @@ int ozaki_slices();
 // m and ldc multiples of 4)
 void ozaki_gemm_rows(stgp_ctx* ctx, long long n, int m, int k, const double* A, int lda, const double* B, int ldb,
                      double* C, int ldc);
+// C = op(T) B for T lower triangular n x n (column-major, ldt) and B n x ncols (ldb): the rows form
+// with the rows of op(T) as its per-row-scaled operand (n and ldc multiples of 4)
+bool ozaki_trmm_enabled();
+void ozaki_trmm_left(stgp_ctx* ctx, const double* T, int ldt, int n, const double* B, int ldb, long long ncols,
+                     bool transpose, double* C, int ldc, bool skip = true);
 // C[j * ldc + i] = sum_{r < n} A[j + r * lda] * B[i + r * ldb] / colD[r]  for i, j < m: A B^T of two
 // m x n column-major matrices, each column scaled by colD[r]^{-1/2} when colD is given (the long
 // reduction over n runs in exact int32 chunks)
@@ -34,7 +39,8 @@ void ozaki_release(stgp_ctx* ctx);
 struct OzakiTcState;
 void ozaki_tc_release(OzakiTcState* s);
 void ozaki_tc_rows(stgp_ctx* ctx, OzakiTcState*& st, int S, int kp, long long nx, int ny, const int8_t* xd, bool x_rev,
-                   const double* sx, const int8_t* yd, bool y_rev, const double* sy, double* out, long long ldo);
+                   const double* sx, const int8_t* yd, bool y_rev, const double* sy, double* out, long long ldo,
+                   int tri = 0);
 void ozaki_tc_cols(stgp_ctx* ctx, OzakiTcState*& st, int S, int L, int nch, int m, const int8_t* xd, bool x_rev,
                    const double* sx, const int8_t* yd, bool y_rev, const double* sy, bool symmetric, double* C,
                    long long ldc);

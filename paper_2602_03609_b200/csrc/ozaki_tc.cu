@@ -48,7 +48,7 @@ struct TcArgs {
   int x_rev, y_rev;       // slice s (1-based) sits at slice coordinate rev ? S - s : s - 1
   int cols;               // 0: rows form (one chunk, write), 1: cols form (accumulate over chunks)
   int nitems;
-  const int4* items;      // (tile x, tile y, group, -)
+  const int4* items;      // (x group, y group, split group, K-step range kb0 | kb1 << 16 or 0 = all)
   const double* sx;       // scales: rows form sx[x]; cols form sx[c nx + x]
   const double* sy;
   double* out;            // out[x ldo + y] (+ group * part_stride in the cols form with groups > 1)
@@ -213,8 +213,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int xt = job.x * CX + rx, yt = job.y * CY + ry;
         int c0, c1;
         chunk_range(a, job.z, c0, c1);
+        const int kb0 = job.w & 0xffff, kb1 = job.w ? job.w >> 16 : a.kblocks;
         for (int c = c0; c < c1; ++c)
-          for (int kb = 0; kb < a.kblocks; ++kb) {
+          for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
             unsigned char* st = smem + stage * kStageBytes;
             mbar_expect_tx(&full[stage], kStageBytes);
@@ -251,11 +252,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int4 job = a.items[it];
         int c0, c1;
         chunk_range(a, job.z, c0, c1);
+        const int kb0 = job.w & 0xffff, kb1 = job.w ? job.w >> 16 : a.kblocks;
         for (int c = c0; c < c1; ++c) {
           mbar_wait(tmem_empty, te_phase ^ 1);  // the epilogue has read the previous accumulators
           te_phase ^= 1;
           tc_fence_after();
-          for (int kb = 0; kb < a.kblocks; ++kb) {
+          for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const uint32_t sbase = smem_u32(smem + stage * kStageBytes);
@@ -272,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint64_t db = smem_desc(sbase + S * kTileX + (t0 - 1) * kTileY);
                 // diagonals s + t0 - 2 ..; the first product (s = 1) of the chunk's first K step starts them
                 STGP_DCHECK((s + t0 - 2 + cnt) * kBN <= 512);
-                mma_i8(tmem + (s + t0 - 2) * kBN, da, db, (kb > 0 || s > 1) ? 1u : 0u, idesc_i8(kBN * cnt));
+                mma_i8(tmem + (s + t0 - 2) * kBN, da, db, (kb > kb0 || s > 1) ? 1u : 0u, idesc_i8(kBN * cnt));
               }
             }
             if (CL == 1) mma_commit(&empty[stage]);  // frees the stage once these MMAs have read it
@@ -521,9 +523,12 @@ static OzakiTcState* tc_state(OzakiTcState*& s) {
 }
 
 // rows form: out[x ldo + y] = sx[x] sy[y] sum_d 2^-7d sum_{s+t=d} X_s[x] . Y_t[y]; X digits at
-// xd[x ldk + slot(s) kp + k], Y digits likewise (ldk = S kp, kp a multiple of 32)
+// xd[x ldk + slot(s) kp + k], Y digits likewise (ldk = S kp, kp a multiple of 32).  tri: the Y rows are
+// those of a triangular factor -- row y vanishes beyond k = y (1, lower) or before it (2, upper) -- and
+// each Y group's K loop stops (starts) at the group's last (first) row: half the int8 work.
 void ozaki_tc_rows(stgp_ctx* ctx, OzakiTcState*& st, int S, int kp, long long nx, int ny, const int8_t* xd, bool x_rev,
-                   const double* sx, const int8_t* yd, bool y_rev, const double* sy, double* out, long long ldo) {
+                   const double* sx, const int8_t* yd, bool y_rev, const double* sy, double* out, long long ldo,
+                   int tri) {
   if (kp % kBK) throw Error(kInternal, "ozaki_tc_rows: kp must be a multiple of 32");
   OzakiTcState* s = tc_state(st);
   const long long ldk = static_cast<long long>(S) * kp;
@@ -532,14 +537,28 @@ void ozaki_tc_rows(stgp_ctx* ctx, OzakiTcState*& st, int S, int kp, long long nx
   const CUtensorMap ty = make_map(yd, kp, S, ny, 1, kp, ldk, static_cast<long long>(ny) * ldk, kBN / cs.cx);
   const int tiles_x = static_cast<int>((nx + kBM - 1) / kBM), tiles_y = (ny + kBN - 1) / kBN;
   const int groups_x = (tiles_x + cs.cx - 1) / cs.cx, groups_y = (tiles_y + cs.cy - 1) / cs.cy;
+  const int kblocks = kp / kBK;
+  std::vector<int> krange(groups_y, 0);
+  for (int gy = 0; tri && gy < groups_y; ++gy) {
+    const int y0 = gy * cs.cy * kBN, y1 = std::min(ny, (gy + 1) * cs.cy * kBN);  // rows [y0, y1)
+    const int kb0 = tri == 2 ? y0 / kBK : 0;
+    const int kb1 = tri == 1 ? std::min(kblocks, (y1 + kBK - 1) / kBK) : kblocks;
+    krange[gy] = kb0 | (kb1 << 16);
+  }
   std::vector<int4> items;
   items.reserve(static_cast<size_t>(groups_x) * groups_y);
-  for (int gx = 0; gx < groups_x; ++gx)  // Y groups fastest: the clusters in flight share one X block in L2
-    for (int gy = 0; gy < groups_y; ++gy) items.push_back(make_int4(gx, gy, 0, 0));
+  // Y groups fastest: the clusters in flight share one X block in L2.  With triangle-cut K ranges the
+  // items differ in cost; the Y order is rotated by the X group so that the clusters' strided shares
+  // (item cid + t * clusters) mix short and long items instead of repeating the same Y groups.
+  for (int gx = 0; gx < groups_x; ++gx)
+    for (int j = 0; j < groups_y; ++j) {
+      const int gy = tri ? (j + gx) % groups_y : j;
+      items.push_back(make_int4(gx, gy, 0, krange[gy]));
+    }
   s->items.upload(items.data(), items.size(), ctx->stream);
   TcArgs a{};
   a.S = S;
-  a.kblocks = kp / kBK;
+  a.kblocks = kblocks;
   a.nx = static_cast<int>(nx);
   a.ny = ny;
   a.nchunks = 1;

@@ -62,6 +62,50 @@ def test_ozaki_cfg4_shape_timing(ctx):
     print(f"ozaki {ms_e:.2f} ms vs DGEMM {ms_d:.2f} ms at n={n}")
 
 
+TRMM_SLICES = 7  # csrc/ozaki.cu slices_for("STGP_OZAKI_S_TRMM", 7)
+TRMM_TOL = 2.0 ** -(7 * TRMM_SLICES - 3)
+
+
+@pytest.mark.parametrize("transpose", [False, True])
+@pytest.mark.parametrize("m,n", [(212, 1500), (912, 600)])
+def test_ozaki_trmm(ctx, m, n, transpose):
+    # W = L^{-1} U / omega = L^{-T} omega' shapes: T the inverse Cholesky factor of an ill-conditioned
+    # SPD matrix (rows of very different magnitude, cancelling signs), B with columns over many binades
+    rng = np.random.default_rng(m + n + transpose)
+    P = rng.random((m, 2))
+    Kc = np.exp(-np.sqrt(((P[:, None, :] - P[None, :, :]) ** 2).sum(-1)) / 0.3) + 1e-6 * np.eye(m)
+    T = np.tril(np.linalg.inv(np.linalg.cholesky(Kc)))
+    B = rng.standard_normal((m, n)) * np.exp2(rng.integers(-20, 20, size=(1, n)))
+    B[:, 5] = 0.0
+    C1, _ = ctx.trmm(T, B, transpose, mode=1)
+    C2, _ = ctx.trmm(T, B, transpose, mode=2)
+    assert np.array_equal(C1, C2)  # the skipped K steps hold only zero digits: the int32 sums are identical
+    assert (C1[:, 5] == 0.0).all()
+    opT = T.T if transpose else T
+    cols = list(range(0, n, max(1, n // 40)))
+    ref = np.array([[math.fsum(opT[j] * B[:, r]) for r in cols] for j in range(m)])
+    scale = np.abs(opT).max(axis=1)[:, None] * np.abs(B[:, cols]).max(axis=0)[None, :] * m
+    err = np.abs(C1[:, cols] - ref)
+    assert (err <= TRMM_TOL * scale).all(), (err / np.maximum(scale, 1e-300)).max()
+    D, _ = ctx.trmm(T, B, transpose, mode=0)
+    full = np.abs(opT).max(axis=1)[:, None] * np.abs(B).max(axis=0)[None, :] * m
+    assert (np.abs(C1 - D) <= 2 * TRMM_TOL * full).all()
+
+
+def test_ozaki_trmm_cfg4_timing(ctx):
+    # the cfg4 shape (M = 912) over 200k columns: triangle-cut int8 product vs the DMMA TRMM
+    rng = np.random.default_rng(3)
+    m, n = 912, 200000
+    T = np.tril(rng.standard_normal((m, m))) + m * np.eye(m)
+    B = rng.standard_normal((m, n))
+    C1, ms1 = ctx.trmm(T, B, False, mode=1)
+    _, ms2 = ctx.trmm(T, B, False, mode=2)
+    D, ms0 = ctx.trmm(T, B, False, mode=0)
+    full = np.abs(T).max(axis=1)[:, None] * np.abs(B).max(axis=0)[None, :] * m
+    assert (np.abs(C1 - D) <= 2 * TRMM_TOL * full).all()
+    print(f"trmm ozaki {ms1:.2f} ms (full K {ms2:.2f}) vs DMMA {ms0:.2f} ms at n={n}")
+
+
 @pytest.mark.parametrize("n,m", [(1000, 40), (300001, 96)])
 def test_ozaki_long_reduction(ctx, n, m):
     # C = A^T B over n rows in exact int32 chunks (the K = S S^T and V' F^T shapes), per-chunk scales
