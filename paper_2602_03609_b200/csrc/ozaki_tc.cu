@@ -145,7 +145,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
         "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// exact int32 -> double without the quarter-rate I2F.F64: 2^52 + 2^31 + v has v + 2^31 as its low word
+__device__ __forceinline__ double i32_to_f64(int v) {
+  return __hiloint2double(0x43300000, v ^ static_cast<int>(0x80000000u)) - 4503601774854144.0;  // 2^52 + 2^31
+}
 
 __device__ __forceinline__ void chunk_range(const TcArgs& a, int g, int& c0, int& c1) {
   c0 = static_cast<int>(static_cast<long long>(a.nchunks) * g / a.groups);
@@ -300,6 +309,56 @@ __global__ void __launch_bounds__(kThreads, 1)
       chunk_range(a, job.z, c0, c1);
       const int x = (job.x * CX + rx) * kBM + quarter * 32 + lane;
       const int y0 = (job.y * CY + ry) * kBN;
+      if (!a.cols) {
+        // rows form (one chunk, written once): per 8 columns the S diagonals are read with one wait,
+        // combined, scaled and stored; the accumulators are released as soon as the last read lands.
+        // Same operations and order as the column form's combine (bit-identical results).
+        mbar_wait(tmem_full, tf_phase);
+        tf_phase ^= 1;
+        tc_fence_after();
+        const double sxv = x < a.nx ? a.sx[x] : 0.0;
+        double* o = a.out + static_cast<long long>(x) * a.ldo + y0;
+        const int ny = min(kBN, a.ny - y0);
+        const bool vec = ny == kBN && (reinterpret_cast<uintptr_t>(o) & 15) == 0;
+#pragma unroll
+        for (int q = 0; q < kBN / 8; ++q) {
+          int v[S][8];
+#pragma unroll
+          for (int d = 0; d < S; ++d) tmem_ld8(lane_addr + d * kBN + q * 8, v[d]);
+          tmem_wait_ld();
+          if (q == kBN / 8 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tmem_empty);
+          }
+          double sq[8];
+          double w = 0x1p-14;
+#pragma unroll
+          for (int d = 0; d < S - 1; ++d) w *= 0x1p-7;  // 2^-7(S+1)
+#pragma unroll
+          for (int d = S - 1; d >= 0; --d) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) sq[e] = d == S - 1 ? i32_to_f64(v[d][e]) * w : fma(i32_to_f64(v[d][e]), w, sq[e]);
+            w *= 128.0;
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int y = y0 + q * 8 + e;
+            sq[e] = sq[e] * sxv * (y < a.ny ? __ldg(&a.sy[y]) : 0.0);
+          }
+          if (x < a.nx) {
+            if (vec) {
+#pragma unroll
+              for (int e = 0; e < 8; e += 2) *reinterpret_cast<double2*>(o + q * 8 + e) = make_double2(sq[e], sq[e + 1]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                if (q * 8 + e < ny) o[q * 8 + e] = sq[e];
+            }
+          }
+        }
+        continue;
+      }
       double acc[kBN];
 #pragma unroll
       for (int e = 0; e < kBN; ++e) acc[e] = 0.0;
