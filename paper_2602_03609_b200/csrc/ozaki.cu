@@ -165,13 +165,16 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(int m, long long n, int
                                                          int lda, const double* __restrict__ colD,
                                                          const unsigned long long* __restrict__ maxbits,
                                                          int8_t* __restrict__ out, int8_t* __restrict__ out_rev,
-                                                         double* __restrict__ scale) {
+                                                         double* __restrict__ scale, int jfast) {
   constexpr int kRB = 128 * H, kRow = sl_row<H>();
   extern __shared__ __align__(16) unsigned char sd[];  // S * 32 * kRow bytes
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const long long rc0 = static_cast<long long>(blockIdx.x) * kRB;
+  // jfast: the 32-row segments j vary fastest over consecutive blocks (the resident blocks read whole
+  // source rows r) instead of the row blocks
+  const unsigned bx = jfast ? blockIdx.y : blockIdx.x, by = jfast ? blockIdx.x : blockIdx.y;
+  const long long rc0 = static_cast<long long>(bx) * kRB;
   const long long rb = rc0 + w * 16 * H;
-  const int j0 = blockIdx.y * 32, j = j0 + lane;
+  const int j0 = by * 32, j = j0 + lane;
   const int c = static_cast<int>(rc0 / L);
   double inv = 0.0;
   if (j < m) {
@@ -309,6 +312,16 @@ static int slice_halves() {
   return h;
 }
 
+static int slice_jfast() {
+  static const int v = [] {
+    // block order of the column slicer: j segments fastest (default; cfg4 evaluation 270.0 -> 268.5 ms
+    // although the slicer itself takes the same 5.8 ms either way) or row blocks fastest (0)
+    const char* e = std::getenv("STGP_OZ_SLICE_JFAST");
+    return e && std::atoi(e) == 0 ? 0 : 1;
+  }();
+  return v;
+}
+
 static bool colmax_rows() {
   static const bool on = [] {
     const char* e = std::getenv("STGP_OZ_COLMAX_ROWS");  // A/B switch: 0 = the j-tiled colmax
@@ -400,9 +413,10 @@ void ozaki_trmm_left(stgp_ctx* ctx, const double* T, int ldt, int n, const doubl
 }
 
 // Column-form product C[j ldc + i] = sum_r (fA_r A[j + r lda]) (fB_r B[i + r ldb]) with optional
-// per-column factors fA, fB (device vectors).  same: A == B with fA == fB (one slicing pass writes
-// both digit orders).  keep: the forward digits of A go to the context's kept buffer (tag);
-// kept: A's digits are taken from there instead of slicing A.
+// per-column factors fA, fB (device vectors).  same: A == B with fA == fB (one slicing pass; the
+// tcgen05 kernel loads every slice by its coordinate, so X and Y read the same digits).  keep: the
+// digits of A go to the context's kept buffer (tag); kept: A's digits are taken from there instead of
+// slicing A.
 static void cols_product(stgp_ctx* ctx, int m, long long n, const double* A, int lda, const double* fA, const double* B,
                          int ldb, const double* fB, bool same, uint64_t keep_tag, bool use_kept, double* C, int ldc) {
   const int S = slices_for("STGP_OZAKI_S_COLS", 7);
@@ -428,13 +442,17 @@ static void cols_product(stgp_ctx* ctx, int m, long long n, const double* A, int
     Aslices = oz->As.get();
     sA = oz->sA.get();
   }
-  oz->Bs.ensure(sl);
-  oz->sB.ensure(static_cast<size_t>(nch) * m);
+  if (!same) {
+    oz->Bs.ensure(sl);
+    oz->sB.ensure(static_cast<size_t>(nch) * m);
+  }
   const dim3 grid(static_cast<unsigned>((n + kSlCols - 1) / kSlCols), (m + 31) / 32);
   // the slicer covers every chunk to its full length L: the padding columns [n, nch L) of the
   // last chunk enter the int8 products and must be zero digits (reused buffers hold old data)
   const int H = slice_halves();
-  const dim3 sgrid(static_cast<unsigned>(static_cast<long long>(nch) * L / (128 * H)), (m + 31) / 32);
+  const int jf = slice_jfast();
+  const unsigned nrb = static_cast<unsigned>(static_cast<long long>(nch) * L / (128 * H)), njb = (m + 31) / 32;
+  const dim3 sgrid(jf ? njb : nrb, jf ? nrb : njb);
   oz->maxbits.ensure(static_cast<size_t>(nch) * m);
   auto slice = [&](const double* X, int ldx, const double* f, int8_t* fwd, int8_t* rev, double* sc) {
     STGP_CUDA(cudaMemsetAsync(oz->maxbits.get(), 0, sizeof(unsigned long long) * nch * m, st));
@@ -450,19 +468,19 @@ static void cols_product(stgp_ctx* ctx, int m, long long n, const double* A, int
                        STGP_CUDA(cudaFuncSetAttribute(slice_cols_kernel<kS, 1>,
                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
                        slice_cols_kernel<kS, 1><<<sgrid, 256, smem, st>>>(m, n, L, X, ldx, f, oz->maxbits.get(), fwd,
-                                                                          rev, sc);
+                                                                          rev, sc, jf);
                      } else {
                        const int smem = kS * 32 * sl_row<2>();
                        STGP_CUDA(cudaFuncSetAttribute(slice_cols_kernel<kS, 2>,
                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
                        slice_cols_kernel<kS, 2><<<sgrid, 256, smem, st>>>(m, n, L, X, ldx, f, oz->maxbits.get(), fwd,
-                                                                          rev, sc);
+                                                                          rev, sc, jf);
                      }
                    }));
     launched(ctx);
   };
-  if (!use_kept) slice(A, lda, fA, Aslices, same ? oz->Bs.get() : nullptr, sA);
-  if (!same) slice(B, ldb, fB, nullptr, oz->Bs.get(), oz->sB.get());
+  if (!use_kept) slice(A, lda, fA, Aslices, nullptr, sA);
+  if (!same) slice(B, ldb, fB, oz->Bs.get(), nullptr, oz->sB.get());
   if (keep_tag != 0) {
     oz->keep_tag = keep_tag;
     oz->keep_m = m;
@@ -470,7 +488,8 @@ static void cols_product(stgp_ctx* ctx, int m, long long n, const double* A, int
   }
   const double* sB = same ? sA : oz->sB.get();
   ProfRegion pr(ctx, "oz_imma");
-  ozaki_tc_cols(ctx, oz->tc, S, L, nch, m, Aslices, false, sA, oz->Bs.get(), true, sB, same, C, ldc);
+  ozaki_tc_cols(ctx, oz->tc, S, L, nch, m, Aslices, false, sA, same ? Aslices : oz->Bs.get(), false, sB, same, C,
+                ldc);
 }
 
 // per-column factor vector 1 / sqrt(D) (inverse) or sqrt(D)
