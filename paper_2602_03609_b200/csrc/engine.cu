@@ -515,6 +515,15 @@ static int launch_row_kernel(stgp_ctx* ctx, K kern, int static_blocks, RowArgs& 
   return blocks;
 }
 
+// Vecchia gradient in two kernels (factor pass, pair pass); STGP_VGRAD_SPLIT=0 runs the fused kernel
+static bool vgrad_split() {
+  static const bool on = [] {
+    const char* e = std::getenv("STGP_VGRAD_SPLIT");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 // Launch the per-row kernel in the given mode; returns the 8 reduced partials.
 std::vector<double> run_rows(stgp_structure* s, int mode, const double* W, int ldw, double nugget) {
   RowArgs a = row_args(s, W, ldw, nugget);
@@ -565,6 +574,32 @@ std::vector<double> run_rows_args(stgp_structure* s, int mode, RowArgs& a) {
         }
       } else if (mode == kModeBuild) { if (hw) { STGP_ROWS_KS(kModeBuild, true) } else { STGP_ROWS_KS(kModeBuild, false) } }
       else if (mode == kModeNll) { if (hw) { STGP_ROWS_KS(kModeNll, true) } else { STGP_ROWS_KS(kModeNll, false) } }
+      else if (mode == kModeGrad && !hw && vgrad_split()) {
+        // two passes: factors + pair weights (registers of the Cholesky), then the pair loop at higher
+        // occupancy; the second kernel's block partials follow the first's in the reducer
+        s->pairw.ensure(static_cast<size_t>(s->n) * kPairW);
+        a.pairw = s->pairw.get();
+        s->red.ensure(2 * ctx->num_sms * 16, 8);  // both passes' partials (no reallocation in between)
+        a.part = s->red.part.get();
+        STGP_ROWS_KS(kModeGrad, false)
+        RowArgs a2 = a;
+        auto pass2 = [&](auto kern) {
+          int per_sm = 0;
+          STGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowWarps * 32, 0));
+          const int b2 = std::max(1, std::min({ceil_div(std::max(rows, 1), kRowWarps), std::max(per_sm, 1) * ctx->num_sms,
+                                               ctx->num_sms * 16}));
+          a2.part = s->red.part.get() + static_cast<size_t>(blocks) * 8;
+          kern<<<b2, kRowWarps * 32, 0, ctx->stream>>>(a2);
+          ++ctx->launches;
+          blocks += b2;
+        };
+        switch (ks) {
+          case 8: pass2(vecchia_pair_grad_kernel<8>); break;
+          case 16: pass2(vecchia_pair_grad_kernel<16>); break;
+          case 24: pass2(vecchia_pair_grad_kernel<24>); break;
+          default: pass2(vecchia_pair_grad_kernel<31>); break;
+        }
+      }
       else if (mode == kModeGrad) { if (hw) { STGP_ROWS_KS(kModeGrad, true) } else { STGP_ROWS_KS(kModeGrad, false) } }
       else { STGP_ROWS_KS(kModeVifGrad, true) }
 #undef STGP_ROWS_KS

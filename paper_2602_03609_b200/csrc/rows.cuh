@@ -140,7 +140,11 @@ struct RowArgs {
   const double* Lfac_in;
   const double* A_in;
   const double* Ga_in;  // optional: Ga from the tiled SDDMM (tiles.cu tile_ga), n x 32, self at 31
+  // Vecchia gradient in two passes: the factor pass writes each row's pair weights here (a~, w~ per
+  // slot, c_d, c_u, w_d; kPairW doubles per row) and vecchia_pair_grad_kernel runs the pair loop
+  double* pairw;
 };
+constexpr int kPairW = 68;
 
 template <int KS>
 constexpr int lfac_stride() {
@@ -484,6 +488,21 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
     if (a.u_out && lane == 0) a.u_out[i] = u;
     if (lane == 0) row_acc(a, tot, i, 0, log(D) + u * u / D);
     if (!TWO) continue;
+    if (MODE == kModeGrad && a.pairw) {  // two-pass gradient: hand the pair weights to the pair kernel
+      double* pw = a.pairw + static_cast<size_t>(i) * kPairW;
+      pw[lane] = lane < k ? -Aval : (lane == KS ? 1.0 : 0.0);
+      pw[32 + lane] = wval;
+      const double cd = 0.5 * (1.0 / D - u * u / (D * D)), cu = u / D;
+      const double s1n = 1.0 + aa, s2n = -aw;
+      const double wd = cd * s1n - cu * s2n;
+      if (lane == 0) {
+        pw[64] = cd;
+        pw[65] = cu;
+        pw[66] = wd;
+        row_acc(a, tot, i, 1, wd);
+      }
+      continue;
+    }
     // ---- phase D: gradient over closure pairs ----
     sAw[w][0][lane] = lane < k ? -Aval : (lane == KS ? 1.0 : 0.0);  // a~
     sAw[w][1][lane] = wval;                                          // w~ or Rv (0 at i)
@@ -548,6 +567,100 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
     __syncwarp();
   }
   // deterministic block reduction: warps in order
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sred[w][q] = tot[q];
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    double s = 0.0;
+    for (int ww = 0; ww < kRowWarps; ++ww) s += sred[ww][threadIdx.x];
+    a.part[static_cast<size_t>(blockIdx.x) * 8 + threadIdx.x] = s;
+  }
+}
+
+// Second pass of the two-pass Vecchia gradient: the closure-pair loop of phase D above with the pair
+// weights the factor pass stored (same pair order, arithmetic and per-row sums), at the occupancy of a
+// kernel without the register Cholesky.  Per-block partials of q = 2..7 into a.part.
+template <int KS>
+__global__ void __launch_bounds__(kRowWarps * 32, 6) vecchia_pair_grad_kernel(RowArgs a) {
+  constexpr int NS = KS + 1;
+  constexpr int NP = NS * (NS - 1) / 2;
+  __shared__ uint16_t sPair[NP];
+  __shared__ double sx[kRowWarps][32], sy[kRowWarps][32], sAw[kRowWarps][2][32];
+  __shared__ int st[kRowWarps][32];
+  __shared__ double sred[kRowWarps][8];
+  __shared__ TF stf[kRowWarps][kMaxCls * kMaxCls];
+  __shared__ int scls[kRowWarps][32], sctid[kRowWarps][kMaxCls];
+  for (int p = threadIdx.x; p < NP; p += blockDim.x) {
+    int aa = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * static_cast<float>(p))) * 0.5f);
+    while (aa * (aa - 1) / 2 > p) --aa;
+    while ((aa + 1) * aa / 2 <= p) ++aa;
+    sPair[p] = static_cast<uint16_t>(aa | ((p - aa * (aa - 1) / 2) << 8));
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double tot[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) tot[q] = 0.0;
+  const MaternPoly mpol = matern_poly(a.k.nu_code);
+  const int gw = blockIdx.x * kRowWarps + w, nw = gridDim.x * kRowWarps;
+  const int nrows = a.row_end - a.row_begin;
+  for (int kr = gw; kr < nrows; kr += nw) {
+    const int i = a.order ? __ldg(&a.order[kr]) : a.row_begin + kr;
+    int nb = -1;
+    if (lane < a.m_v) nb = __ldg(&a.nbr[static_cast<size_t>(i) * a.m_v + lane]);
+    const int k = __popc(__ballot_sync(kFull, nb >= 0));
+    const int pt = lane < k ? nb : (lane == KS ? i : -1);
+    if (pt >= 0) {
+      sx[w][lane] = __ldg(&a.x[pt]);
+      sy[w][lane] = __ldg(&a.y[pt]);
+      st[w][lane] = __ldg(&a.tid[pt]);
+    }
+    const double* pw = a.pairw + static_cast<size_t>(i) * kPairW;
+    sAw[w][0][lane] = __ldg(&pw[lane]);
+    sAw[w][1][lane] = __ldg(&pw[32 + lane]);
+    const double cd = __ldg(&pw[64]), cu = __ldg(&pw[65]), wd = __ldg(&pw[66]);
+    __syncwarp();
+    const int nc = closure_time_classes(a.lt, pt, pt >= 0 ? st[w][lane] : -1, lane, scls[w], sctid[w], stf[w]);
+    const int P = (k + 1) * k / 2;
+    auto slots = [&](int p, int& sa, int& sb) {
+      const int pr = sPair[p];
+      const int ca = pr & 0xff;
+      sb = pr >> 8;
+      sa = ca == k ? KS : ca;
+    };
+    double g[6] = {0, 0, 0, 0, 0, 0};
+    auto one_pair = [&](int sa, int sb, const TF& f) {
+      const double dx = sx[w][sa] - sx[w][sb], dy = sy[w][sa] - sy[w][sb];
+      double kg[6];
+      gneiting_grad_bf(a.k, mpol, a.inv_c, fma(dx, dx, dy * dy), f, kg);
+      const double ta = sAw[w][0][sa], tb = sAw[w][0][sb], wa = sAw[w][1][sa], wb = sAw[w][1][sb];
+      const double wt = cd * (2.0 * ta * tb) - cu * (wa * tb + wb * ta);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) g[q] = fma(wt, kg[q], g[q]);
+    };
+    if (nc) {
+      for (int p = lane; p < P; p += 32) {
+        int sa, sb;
+        slots(p, sa, sb);
+        one_pair(sa, sb, stf[w][scls[w][sa] * nc + scls[w][sb]]);
+      }
+    } else {
+      for (int p = lane; p < P; p += 32) {
+        int sa, sb;
+        slots(p, sa, sb);
+        one_pair(sa, sb, a.lt.get(st[w][sa], st[w][sb]));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) g[q] += __shfl_xor_sync(kFull, g[q], o);
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < 6; ++q) tot[2 + q] += g[q] + wd * a.g00[q];
+    __syncwarp();
+  }
   if (lane == 0)
 #pragma unroll
     for (int q = 0; q < 8; ++q) sred[w][q] = tot[q];

@@ -69,6 +69,7 @@ struct stgp_structure {
   stgp::Reducer red;
   stgp::DevBuf<int> fail;
   stgp::DevBuf<double> r, ywork, Xwork, betaw, u, scratch, row_part;
+  stgp::DevBuf<double> pairw;  // two-pass Vecchia gradient: per-row pair weights (rows.cuh kPairW)
   stgp::DevBuf<double> zcol;  // ldw zeros (fragment source of empty closure slots)
   int zcol_n = 0;
   stgp::LowRank lr;
