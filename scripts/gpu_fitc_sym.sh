@@ -1,0 +1,10 @@
+# FITC W diag(phi) W^T from one triangle of tiles: parity tests + A/B
+make -C paper_2602_03609_b200/csrc -q || echo "stale build"
+timeout -s KILL 900 python -m pytest -q -x tests/test_gpu_ozaki.py tests/test_gpu_configs.py tests/test_gpu_lowrank.py tests/test_gpu_general_nu.py tests/test_gpu_predict.py 2>&1 | tail -2
+for r in 1 2; do
+for cfg in "STGP_FITC_SYM_S=0" "STGP_XX=0"; do
+  env $cfg timeout -s KILL 900 python bench.py --workload fitc --steps 3 --warmup 3 2>/dev/null | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); p=d['roofline']['phase_ms']
+print('fitc [$cfg]', round(d['ms_per_step'],1), d['nll'], d['grad'][:3], {k: round(v,2) for k,v in p.items()})"
+done
+done
