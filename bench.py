@@ -459,7 +459,11 @@ def main():
         # the tiles that reach the lower triangle and mirrors)
         s_tri = int(os.environ.get("STGP_OZAKI_S_TRMM", s_all or 7))
         pr_, pc_, pt_ = s_rows * (s_rows + 1) / 2, s_cols * (s_cols + 1) / 2, s_tri * (s_tri + 1) / 2
-        int8_ops = 2.0 * (pr_ + pc_) * ldm * ldm * (hi - lo) + pc_ * ldm * (ldm + 1) * (hi - lo)
+        if args.workload == "fitc" and os.environ.get("STGP_FITC_SYM_S", "1") != "0":
+            # W diag(phi) W^T is symmetric and computed on one triangle of tiles, like K
+            int8_ops = 2.0 * pr_ * ldm * ldm * (hi - lo) + 2 * pc_ * ldm * (ldm + 1) * (hi - lo)
+        else:
+            int8_ops = 2.0 * (pr_ + pc_) * ldm * ldm * (hi - lo) + pc_ * ldm * (ldm + 1) * (hi - lo)
         if os.environ.get("STGP_OZAKI_TRMM", "1") != "0":
             # two triangular products, M (M + 1) / 2 FMA per column each (algorithmic: the triangle)
             int8_ops += 2 * 2.0 * pt_ * ldm * (ldm + 1) / 2 * (hi - lo)

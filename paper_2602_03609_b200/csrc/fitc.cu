@@ -6,6 +6,8 @@
 //   omega = L_m^{-T} [ K^{-1} W Lambda^{-1} - (W alpha) alpha^T - W diag(2 phi) ],
 //   wsig  = L_m^{-T} [ -(I - K^{-1})/2 + (W alpha)(W alpha)^T / 2 + W diag(phi) W^T ] L_m^{-1},
 // which removes the reference's n x M^2 GEMMs for G1 and W2.
+#include <cstdlib>
+
 #include "comm.hpp"
 #include "dense.cuh"
 #include "lowrank_common.cuh"
@@ -153,6 +155,16 @@ void fitc_build(stgp_structure* s) {
 }
 
 // shared prefix of NLL and gradient (own rows): rl, v = W rl (summed), kv = K^{-1} v, t = W^T kv
+// W diag(phi) W^T from the tiles of one triangle, mirrored (STGP_FITC_SYM_S=0: all tiles, then the
+// lower triangle copied up)
+static bool sym_S() {
+  static const bool on = [] {
+    const char* e = std::getenv("STGP_FITC_SYM_S");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 static double fitc_core(stgp_structure* s, double*& rl, double*& kv, double*& t) {
   stgp_ctx* ctx = s->ds->ctx;
   LowRank& L = s->lr;
@@ -207,25 +219,28 @@ void fitc_nll_grad(stgp_structure* s, double* nll, double* grad) {
   L.Kinv.ensure(mm);
   dev_chol_inverse(ctx, L.Mc.get(), ldm, ldm, L.Kinv.get());
   if (nown > 0) {
-    ProfRegion pr(ctx, "f_KW_gemm");
-    if (ozaki_for(ldm))  // K^{-1} symmetric: KW_i = K^{-1} W_i row by row
-      ozaki_gemm_rows(ctx, nown, ldm, ldm, L.W.get() + own, ldm, L.Kinv.get(), ldm, L.work1.get() + own, ldm);
-    else
-      dev_gemm(ctx, false, false, ldm, nown, ldm, 1.0, L.Kinv.get(), ldm, L.W.get() + own, ldm, 0.0,
-               L.work1.get() + own, ldm);
-    col_dot_kernel<<<grid_for(static_cast<long long>(nown) * 32), 256, 0, st>>>(nown, ldm, L.W.get() + own,
-                                                                               L.work1.get() + own, hsq + rb);
-    launched(ctx);
-    fitc_alpha_phi_kernel<<<grid_for(nown), 256, 0, st>>>(nown, s->r.get() + rb, L.lambda.get() + rb, t + rb, hsq + rb,
-                                                          alpha + rb, phi + rb);
-    launched(ctx);
-    dev_gemv(ctx, false, ldm, nown, 1.0, L.W.get() + own, ldm, alpha + rb, 0.0, wa);
+    {
+      ProfRegion pr(ctx, "f_KW_gemm");
+      if (ozaki_for(ldm))  // K^{-1} symmetric: KW_i = K^{-1} W_i row by row
+        ozaki_gemm_rows(ctx, nown, ldm, ldm, L.W.get() + own, ldm, L.Kinv.get(), ldm, L.work1.get() + own, ldm);
+      else
+        dev_gemm(ctx, false, false, ldm, nown, ldm, 1.0, L.Kinv.get(), ldm, L.W.get() + own, ldm, 0.0,
+                 L.work1.get() + own, ldm);
+      col_dot_kernel<<<grid_for(static_cast<long long>(nown) * 32), 256, 0, st>>>(nown, ldm, L.W.get() + own,
+                                                                                 L.work1.get() + own, hsq + rb);
+      launched(ctx);
+      fitc_alpha_phi_kernel<<<grid_for(nown), 256, 0, st>>>(nown, s->r.get() + rb, L.lambda.get() + rb, t + rb,
+                                                            hsq + rb, alpha + rb, phi + rb);
+      launched(ctx);
+      dev_gemv(ctx, false, ldm, nown, 1.0, L.W.get() + own, ldm, alpha + rb, 0.0, wa);
+    }
     // S = W diag(phi) W^T (symmetric: lower blocks only)
     ProfRegion prs(ctx, "f_S_gemm");
     scale_cols(ctx, L.W.get() + own, ldm, nown, phi + rb, false, L.work2.get() + own);
     if (ozaki_for(ldm)) {  // S(i, j) = sum_r W(i, r) phi_r W(j, r); mirrored lower triangle
       // (W Lambda^{-1/2}) digits kept from K: S = (W Lambda^{-1/2}) (W diag(phi) Lambda^{1/2})^T
-      if (!ozaki_gemm_kept(ctx, ldm, nown, L.work2.get() + own, ldm, L.lambda.get() + rb, S, ldm, s->uid))
+      if (!ozaki_gemm_kept(ctx, ldm, nown, L.work2.get() + own, ldm, L.lambda.get() + rb, S, ldm, s->uid,
+                           sym_S()))
         ozaki_gemm_cols(ctx, ldm, nown, L.work2.get() + own, ldm, L.W.get() + own, ldm, S, ldm);
       dev_symmetrize_lower(ctx, S, ldm, ldm);
     } else
