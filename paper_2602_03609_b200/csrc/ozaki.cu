@@ -418,7 +418,8 @@ void ozaki_trmm_left(stgp_ctx* ctx, const double* T, int ldt, int n, const doubl
 // digits of A go to the context's kept buffer (tag); kept: A's digits are taken from there instead of
 // slicing A.
 static void cols_product(stgp_ctx* ctx, int m, long long n, const double* A, int lda, const double* fA, const double* B,
-                         int ldb, const double* fB, bool same, uint64_t keep_tag, bool use_kept, double* C, int ldc) {
+                         int ldb, const double* fB, bool same, uint64_t keep_tag, bool use_kept, double* C, int ldc,
+                         bool symmetric = false) {
   const int S = slices_for("STGP_OZAKI_S_COLS", 7);
   OzakiState* oz = state(ctx);
   cudaStream_t st = ctx->stream;
@@ -488,8 +489,8 @@ static void cols_product(stgp_ctx* ctx, int m, long long n, const double* A, int
   }
   const double* sB = same ? sA : oz->sB.get();
   ProfRegion pr(ctx, "oz_imma");
-  ozaki_tc_cols(ctx, oz->tc, S, L, nch, m, Aslices, false, sA, same ? Aslices : oz->Bs.get(), false, sB, same, C,
-                ldc);
+  ozaki_tc_cols(ctx, oz->tc, S, L, nch, m, Aslices, false, sA, same ? Aslices : oz->Bs.get(), false, sB,
+                same || symmetric, C, ldc);
 }
 
 // per-column factor vector 1 / sqrt(D) (inverse) or sqrt(D)
@@ -516,11 +517,11 @@ void ozaki_syrk_keep(stgp_ctx* ctx, int m, long long n, const double* A, int lda
 }
 
 bool ozaki_gemm_kept(stgp_ctx* ctx, int m, long long n, const double* B, int ldb, const double* D, double* C, int ldc,
-                     uint64_t tag) {
+                     uint64_t tag, bool symmetric) {
   OzakiState* oz = state(ctx);
   if (m <= 0 || tag == 0 || oz->keep_tag != tag || oz->keep_m != m || oz->keep_n != n) return false;
   const double* f = col_factors(ctx, oz->colf2, D, n, false);
-  cols_product(ctx, m, n, nullptr, 0, nullptr, B, ldb, f, false, 0, true, C, ldc);
+  cols_product(ctx, m, n, nullptr, 0, nullptr, B, ldb, f, false, 0, true, C, ldc, symmetric);
   return true;
 }
 
