@@ -236,15 +236,19 @@ void fitc_nll_grad(stgp_structure* s, double* nll, double* grad) {
     }
     // S = W diag(phi) W^T (symmetric: lower blocks only)
     ProfRegion prs(ctx, "f_S_gemm");
-    scale_cols(ctx, L.W.get() + own, ldm, nown, phi + rb, false, L.work2.get() + own);
     if (ozaki_for(ldm)) {  // S(i, j) = sum_r W(i, r) phi_r W(j, r); mirrored lower triangle
-      // (W Lambda^{-1/2}) digits kept from K: S = (W Lambda^{-1/2}) (W diag(phi) Lambda^{1/2})^T
-      if (!ozaki_gemm_kept(ctx, ldm, nown, L.work2.get() + own, ldm, L.lambda.get() + rb, S, ldm, s->uid,
-                           sym_S()))
+      // (W Lambda^{-1/2}) digits kept from K: S = (W Lambda^{-1/2}) (W diag(phi Lambda^{1/2}))^T, the column
+      // factors applied by the slicer
+      if (!ozaki_gemm_kept(ctx, ldm, nown, L.W.get() + own, ldm, L.lambda.get() + rb, S, ldm, s->uid, sym_S(),
+                           phi + rb)) {
+        scale_cols(ctx, L.W.get() + own, ldm, nown, phi + rb, false, L.work2.get() + own);
         ozaki_gemm_cols(ctx, ldm, nown, L.work2.get() + own, ldm, L.W.get() + own, ldm, S, ldm);
+      }
       dev_symmetrize_lower(ctx, S, ldm, ldm);
-    } else
+    } else {
+      scale_cols(ctx, L.W.get() + own, ldm, nown, phi + rb, false, L.work2.get() + own);
       dev_gemm_sym_blocked(ctx, ldm, nown, 1.0, L.W.get() + own, ldm, L.work2.get() + own, ldm, S, ldm, 4);
+    }
     Reducer rr;
     phisum[0] = dev_sum(ctx, phi + rb, nown, rr);
   }

@@ -516,11 +516,26 @@ void ozaki_syrk_keep(stgp_ctx* ctx, int m, long long n, const double* A, int lda
   cols_product(ctx, m, n, A, lda, f, A, lda, f, true, tag, false, C, ldc);
 }
 
+__global__ void sqrt_mul_vec_kernel(long long n, const double* __restrict__ d, const double* __restrict__ g,
+                                    double* __restrict__ f) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    f[i] = sqrt(d[i]) * g[i];
+}
+
 bool ozaki_gemm_kept(stgp_ctx* ctx, int m, long long n, const double* B, int ldb, const double* D, double* C, int ldc,
-                     uint64_t tag, bool symmetric) {
+                     uint64_t tag, bool symmetric, const double* colmul) {
   OzakiState* oz = state(ctx);
   if (m <= 0 || tag == 0 || oz->keep_tag != tag || oz->keep_m != m || oz->keep_n != n) return false;
-  const double* f = col_factors(ctx, oz->colf2, D, n, false);
+  const double* f;
+  if (colmul) {
+    oz->colf2.ensure(static_cast<size_t>(n));
+    sqrt_mul_vec_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(n, D, colmul, oz->colf2.get());
+    launched(ctx);
+    f = oz->colf2.get();
+  } else {
+    f = col_factors(ctx, oz->colf2, D, n, false);
+  }
   cols_product(ctx, m, n, nullptr, 0, nullptr, B, ldb, f, false, 0, true, C, ldc, symmetric);
   return true;
 }

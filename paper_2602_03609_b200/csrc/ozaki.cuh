@@ -30,11 +30,12 @@ void ozaki_gemm_cols(stgp_ctx* ctx, int m, long long n, const double* A, int lda
 // ozaki_gemm_kept then forms C[j ldc + i] = sum_r A[j, r] B[i, r] = (A D^{-1/2})(B D^{1/2})^T from
 // them, slicing only B (false when the kept digits belong to another tag or shape).  symmetric: the
 // product is known to be symmetric (FITC's W diag(phi) W^T): only the tiles reaching one triangle
-// are computed and the other is mirrored.
+// are computed and the other is mirrored.  colmul: an extra per-column factor of B (B(:, r) colmul_r),
+// applied inside the slicer instead of in a separate pass over B.
 void ozaki_syrk_keep(stgp_ctx* ctx, int m, long long n, const double* A, int lda, const double* D, double* C, int ldc,
                      uint64_t tag);
 bool ozaki_gemm_kept(stgp_ctx* ctx, int m, long long n, const double* B, int ldb, const double* D, double* C, int ldc,
-                     uint64_t tag, bool symmetric = false);
+                     uint64_t tag, bool symmetric = false, const double* colmul = nullptr);
 void ozaki_release(stgp_ctx* ctx);
 
 // the hand-written tcgen05 kernel behind the products (ozaki_tc.cu)
