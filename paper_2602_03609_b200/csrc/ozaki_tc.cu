@@ -34,7 +34,15 @@ namespace {
 constexpr int kBM = 128;     // X rows per tile = TMEM lanes = MMA M
 constexpr int kBN = 64;      // Y rows per tile = MMA N = TMEM columns per diagonal
 constexpr int kBK = 32;      // int8 K per stage (one MMA K step, one 32-byte swizzle row)
-constexpr int kStages = 4;
+// pipeline depth: as many S * 6 KB stages as fit in 220 KB of shared memory, at most STGP_TC_STAGES_MAX
+#ifndef STGP_TC_STAGES_MAX
+#define STGP_TC_STAGES_MAX 4
+#endif
+template <int S>
+constexpr int stages_for() {
+  constexpr int fit = (220 * 1024) / (S * (128 * 32 + 64 * 32));
+  return fit < STGP_TC_STAGES_MAX ? fit : STGP_TC_STAGES_MAX;
+}
 constexpr int kThreads = 192;
 constexpr int kTileX = kBM * kBK;  // bytes of one X slice tile
 constexpr int kTileY = kBN * kBK;
@@ -174,6 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // 1024-byte aligned stage buffers: [stage][X slices S x 4 KB | Y slices S x 2 KB]
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int kStageBytes = S * (kTileX + kTileY);
+  constexpr int kStages = stages_for<S>();
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
   uint64_t* tmem_full = empty + kStages;
@@ -474,7 +483,7 @@ template <int S, int CX, int CY>
 void launch_tc(stgp_ctx* ctx, const CUtensorMap& tx, const CUtensorMap& ty, const TcArgs& a) {
   constexpr int CL = CX * CY;
   // at least 116 KB so that one CTA holds an SM: it owns all 512 TMEM columns
-  constexpr int smem = std::max(kStages * S * (kTileX + kTileY) + 1024 + 256, 116 * 1024);
+  constexpr int smem = std::max(stages_for<S>() * S * (kTileX + kTileY) + 1024 + 256, 116 * 1024);
   static int max_clusters = 0;
   if (max_clusters == 0) {
     STGP_CUDA(cudaFuncSetAttribute(ozaki_tc_kernel<S, CX, CY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
