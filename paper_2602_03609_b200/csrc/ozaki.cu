@@ -167,7 +167,8 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(int m, long long n, int
                                                          int8_t* __restrict__ out, int8_t* __restrict__ out_rev,
                                                          double* __restrict__ scale, int jfast) {
   constexpr int kRB = 128 * H, kRow = sl_row<H>();
-  extern __shared__ __align__(16) unsigned char sd[];  // S * 32 * kRow bytes
+  extern __shared__ __align__(16) unsigned char sd[];  // S * 32 * kRow digit bytes, then kRB x 32 doubles
+  double* sa = reinterpret_cast<double*>(sd + S * 32 * kRow);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   // jfast: the 32-row segments j vary fastest over consecutive blocks (the resident blocks read whole
   // source rows r) instead of the row blocks
@@ -176,6 +177,18 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(int m, long long n, int
   const long long rb = rc0 + w * 16 * H;
   const int j0 = by * 32, j = j0 + lane;
   const int c = static_cast<int>(rc0 / L);
+  // the block's kRB x 32 source tile in flight at once: 16-byte cp.async pieces (two doubles; m is a
+  // multiple of 4, so a piece is wholly inside or outside), zero-filled beyond n and m
+  for (int e = threadIdx.x; e < kRB * 16; e += blockDim.x) {
+    const int row = e >> 4, piece = e & 15;
+    const long long r = rc0 + row;
+    const int jj = j0 + 2 * piece;
+    const bool ok = r < n && jj < m;
+    const double* src = ok ? A + r * lda + jj : A;
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(sa + row * 32 + 2 * piece));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
   double inv = 0.0;
   if (j < m) {
     const double mx = __longlong_as_double(static_cast<long long>(maxbits[static_cast<size_t>(c) * m + j]));
@@ -184,6 +197,8 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(int m, long long n, int
     if (rc0 % L == 0 && w == 0) scale[static_cast<size_t>(c) * m + j] = ldexp(1.0, e);
     inv = ldexp(1.0, -e);
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
 #pragma unroll
   for (int h = 0; h < H; ++h) {
     Fixed q[16];
@@ -192,7 +207,7 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(int m, long long n, int
       const long long r = rb + 16 * h + u;
       double v = 0.0;
       if (j < m && r < n) {
-        const double a = A[r * lda + j];
+        const double a = sa[(r - rc0) * 32 + lane];
         v = (colD ? a * __ldg(&colD[r]) : a) * inv;  // exact power-of-two scale
       }
       q[u] = fixed_point<S>(v);
@@ -465,13 +480,13 @@ static void cols_product(stgp_ctx* ctx, int m, long long n, const double* A, int
     launched(ctx);
     STGP_OZ_SWITCH(S, ({
                      if (H == 1) {
-                       const int smem = kS * 32 * sl_row<1>();
+                       const int smem = kS * 32 * sl_row<1>() + 128 * 32 * 8;
                        STGP_CUDA(cudaFuncSetAttribute(slice_cols_kernel<kS, 1>,
                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
                        slice_cols_kernel<kS, 1><<<sgrid, 256, smem, st>>>(m, n, L, X, ldx, f, oz->maxbits.get(), fwd,
                                                                           rev, sc, jf);
                      } else {
-                       const int smem = kS * 32 * sl_row<2>();
+                       const int smem = kS * 32 * sl_row<2>() + 256 * 32 * 8;
                        STGP_CUDA(cudaFuncSetAttribute(slice_cols_kernel<kS, 2>,
                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
                        slice_cols_kernel<kS, 2><<<sgrid, 256, smem, st>>>(m, n, L, X, ldx, f, oz->maxbits.get(), fwd,
