@@ -1,0 +1,15 @@
+# temporal factors per inducing-time class staged in shared memory (U and the U-pair gradient)
+make -C paper_2602_03609_b200/csrc -q || echo "stale build"
+timeout -s KILL 900 python -m pytest -q -x tests/test_gpu_lowrank.py tests/test_gpu_configs.py tests/test_gpu_many_times.py tests/test_gpu_general_nu.py tests/test_gpu_predict.py tests/test_gpu_shards.py 2>&1 | tail -2
+for r in 1 2; do
+for lib in paper_2602_03609_b200/libstgp_b200.so paper_2602_03609_b200/libstgp_b200_prev.so; do
+  STGP_LIB=$lib timeout -s KILL 600 python bench.py --steps 5 --warmup 3 2>/dev/null | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); p=d['roofline']['phase_ms']
+print('vif $lib', round(d['ms_per_step'],2), d['nll'], d['grad'][:2], {k: round(v,2) for k,v in p.items() if k in ('U_cross_cov','g_upair_sigma')})"
+done
+done
+for lib in paper_2602_03609_b200/libstgp_b200.so paper_2602_03609_b200/libstgp_b200_prev.so; do
+  STGP_LIB=$lib timeout -s KILL 900 python bench.py --workload fitc --steps 3 --warmup 3 2>/dev/null | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); p=d['roofline']['phase_ms']
+print('fitc $lib', round(d['ms_per_step'],1), d['nll'], d['grad'][:2], {k: round(v,2) for k,v in p.items() if k in ('U_cross_cov','f_omega_trmm_upair')})"
+done
