@@ -6,6 +6,7 @@
 //   omega = L_m^{-T} [ K^{-1} W Lambda^{-1} - (W alpha) alpha^T - W diag(2 phi) ],
 //   wsig  = L_m^{-T} [ -(I - K^{-1})/2 + (W alpha)(W alpha)^T / 2 + W diag(phi) W^T ] L_m^{-1},
 // which removes the reference's n x M^2 GEMMs for G1 and W2.
+#include <algorithm>
 #include <cstdlib>
 
 #include "comm.hpp"
@@ -74,13 +75,20 @@ __global__ void fitc_alpha_phi_kernel(int n, const double* r, const double* lamb
 }
 
 // omega'(:, i) = KW(:, i) / lambda_i - walpha * alpha_i - 2 phi_i W(:, i)   (in place into KW)
-__global__ void fitc_omega_kernel(long long total, int ldm, const double* lambda, const double* alpha, const double* phi,
+// a block per column i (no 64-bit index division per element), two rows j per thread and step
+__global__ void fitc_omega_kernel(long long ncols, int ldm, const double* lambda, const double* alpha, const double* phi,
                                   const double* walpha, const double* W, double* KW) {
-  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long i = e / ldm;
-    const int j = static_cast<int>(e % ldm);
-    KW[e] = KW[e] / lambda[i] - walpha[j] * alpha[i] - 2.0 * phi[i] * W[e];
+  for (long long i = blockIdx.x; i < ncols; i += gridDim.x) {
+    const double lam = lambda[i], al = alpha[i], ph2 = 2.0 * phi[i];
+    const double2* w2 = reinterpret_cast<const double2*>(W + i * ldm);
+    double2* k2 = reinterpret_cast<double2*>(KW + i * ldm);
+    for (int j2 = threadIdx.x; j2 < ldm / 2; j2 += blockDim.x) {
+      const double2 w = w2[j2];
+      double2 k = k2[j2];
+      k.x = k.x / lam - walpha[2 * j2] * al - ph2 * w.x;
+      k.y = k.y / lam - walpha[2 * j2 + 1] * al - ph2 * w.y;
+      k2[j2] = k;
+    }
   }
 }
 
@@ -261,9 +269,8 @@ void fitc_nll_grad(stgp_structure* s, double* nll, double* grad) {
   std::vector<double> g(7, 0.0);
   if (nown > 0) {
     // omega' (in place of KW), omega = L_m^{-T} omega'
-    fitc_omega_kernel<<<grid_for(static_cast<long long>(ldm) * nown), 256, 0, st>>>(
-        static_cast<long long>(ldm) * nown, ldm, L.lambda.get() + rb, alpha + rb, phi + rb, wa, L.W.get() + own,
-        L.work1.get() + own);
+    fitc_omega_kernel<<<static_cast<int>(std::min<long long>(nown, ctx->num_sms * 16LL)), 256, 0, st>>>(
+        nown, ldm, L.lambda.get() + rb, alpha + rb, phi + rb, wa, L.W.get() + own, L.work1.get() + own);
     launched(ctx);
     ProfRegion pr(ctx, "f_omega_trmm_upair");
     lr_trmm(ctx, L.Lminv.get(), ldm, L.work1.get() + own, nown, true, L.work2.get() + own);
