@@ -474,15 +474,19 @@ def main():
             "kernel": "ozaki_tc_kernel: hand-written tcgen05.mma kind::i8 (TMA, per-diagonal TMEM accumulators, "
                       "FP64 epilogue) over the Ozaki slices",
             "peak_source": "2 x measured dense bf16 (MEASURED_PEAKS.json burst; B200 int8:bf16 dense = 2:1)"}
-        if args.workload == "fitc":
-            # FITC's dominant kernel is the tcgen05 product kernel: it becomes the line's roofline object
-            fp64_view = {k_: roof.pop(k_) for k_ in ("bound", "achieved", "peak", "unit", "frac", "traffic",
-                                                      "traffic_source", "kernel", "kernel_ms", "kernel_share",
-                                                      "flop_per_launch", "peak_source")}
-            roof.update(roof.pop("int8_tensor"))
-            roof["traffic"] = None
-            roof["kernel_share"] = oz_ms / ms_step
-            roof["W_trmm_fp64_equiv"] = fp64_view
+        # the step's dominant kernel is the tcgen05 product kernel (VIF: its 16 launches take 32% of the
+        # evaluation's kernel time against 18% for the closure-row build, profiles/r02/v12/launches_vif_summary.txt;
+        # FITC: 70%): it becomes the line's roofline object, the FP64 view of the largest FP64 kernel kept beside it
+        fp64_view = {k_: roof.pop(k_) for k_ in ("bound", "achieved", "peak", "unit", "frac", "traffic",
+                                                  "traffic_source", "kernel", "kernel_ms", "kernel_share",
+                                                  "flop_per_launch", "peak_source")}
+        roof.update(roof.pop("int8_tensor"))
+        roof["kernel_share"] = oz_ms / ms_step
+        # DRAM bytes of the tcgen05 launches of one cfg4 evaluation (ncu launch list, N = 1)
+        roof["traffic"] = 82.97e9 if cfg4_1 else None
+        roof["traffic_source"] = ("ncu launch list of one cfg4 evaluation: dram__bytes_read+write summed over the "
+                                  "ozaki_tc_kernel launches (profiles/r02/v12/launches_vif_summary.txt)") if cfg4_1 else None
+        roof["rows_build" if args.workload == "vif" else "W_trmm_fp64_equiv"] = fp64_view
     line = {"metric": METRIC, "value": 1e3 / ms_step, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",
