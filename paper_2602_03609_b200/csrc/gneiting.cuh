@@ -304,6 +304,14 @@ __device__ __forceinline__ void gneiting_grad_bf(const DevKernel& k, const Mater
   g[5] = -f.log_T * base * M;
 }
 
+// Covariance from the squared distance with the branch-free pieces (closed-form Matern only): within a
+// few ulp of gneiting_eval; for the likelihood-gradient passes, where only the 1e-8 tolerance applies.
+__device__ __forceinline__ double gneiting_eval_bf(const DevKernel& k, const MaternPoly& mp, double s, const TF& f) {
+  const double x = k.c * sqrt_nr(s) * f.pow_mbh;
+  const double e = exp_nonpos(-x);
+  return k.s1 * f.pow_mE * (fma(fma(mp.m2, x, mp.m1), x, 1.0) * e);
+}
+
 // Temporal-factor table indexed by time-id pairs (host-computed with glibc).
 struct TFTable {
   const TF* tab;  // nT * nT

@@ -153,6 +153,14 @@ constexpr int lfac_stride() {
 
 enum RowMode { kModeBuild = 0, kModeNll = 1, kModeGrad = 2, kModeVifGrad = 3 };
 
+// The Vecchia gradient mode evaluates its closure covariances with the branch-free sqrt / exp
+// (gneiting_eval_bf, ~ulp from the correctly rounded path); compile with -DSTGP_FAST_COV=0 for the
+// correctly rounded covariances there too.
+#ifndef STGP_FAST_COV
+#define STGP_FAST_COV 1
+#endif
+__device__ __forceinline__ constexpr bool fast_cov() { return STGP_FAST_COV != 0; }
+
 __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
@@ -359,7 +367,14 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
       TF f;
       f.pow_mE = pe;
       f.pow_mbh = pb;
-      double v = gneiting_eval<GEN>(a.k, spatial_dist(sx[w][sa], sy[w][sa], sx[w][sb], sy[w][sb]), f);
+      double v;
+      if (MODE == kModeGrad && fast_cov()) {
+        // likelihood-gradient evaluations (1e-8 parity): the branch-free sqrt / exp of the pair gradient
+        const double dx = sx[w][sa] - sx[w][sb], dy = sy[w][sa] - sy[w][sb];
+        v = gneiting_eval_bf(a.k, matern_poly(a.k.nu_code), fma(dx, dx, dy * dy), f);
+      } else {
+        v = gneiting_eval<GEN>(a.k, spatial_dist(sx[w][sa], sy[w][sa], sx[w][sb], sy[w][sb]), f);
+      }
       if (HAS_W) v = __dsub_rn(v, C[sa * LD + sb]);  // each pair slot is owned by one lane
       C[sa * LD + sb] = v;
       C[sb * LD + sa] = v;
