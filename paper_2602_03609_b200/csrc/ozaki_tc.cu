@@ -556,8 +556,14 @@ TcCluster cluster_shape(TcForm f) {
     const int v = e ? std::atoi(e) : 0;
     return v == 1 || v == 2 ? v : 0;
   }();
+  // per-form overrides (tuning): STGP_OZAKI_CLUSTER_ROWS / _SYM / _COLS set CY for one form
+  static const int env_form[3] = {
+      [] { const char* e = std::getenv("STGP_OZAKI_CLUSTER_ROWS"); const int v = e ? std::atoi(e) : 0; return v == 1 || v == 2 || v == 4 ? v : 0; }(),
+      [] { const char* e = std::getenv("STGP_OZAKI_CLUSTER_SYM"); const int v = e ? std::atoi(e) : 0; return v == 1 || v == 2 || v == 4 ? v : 0; }(),
+      [] { const char* e = std::getenv("STGP_OZAKI_CLUSTER_COLS"); const int v = e ? std::atoi(e) : 0; return v == 1 || v == 2 || v == 4 ? v : 0; }()};
   TcCluster c{1, f == TcForm::kCols ? 4 : 2};
   if (env_y) c.cy = env_y;
+  if (env_form[static_cast<int>(f)]) c.cy = env_form[static_cast<int>(f)];
   if (env_x) c.cx = env_x;
   if (c.cx * c.cy > 4) c.cy = 4 / c.cx;  // instantiated shapes: 1x1, 1x2, 1x4, 2x1, 2x2
   return c;
