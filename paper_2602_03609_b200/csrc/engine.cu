@@ -395,7 +395,8 @@ void Reducer::ensure(int blocks, int width) {
   out.ensure(static_cast<size_t>(width));
 }
 std::vector<double> Reducer::finish(stgp_ctx* ctx, int blocks, int width) {
-  reduce_parts_kernel<<<1, 32, 0, ctx->stream>>>(part.get(), blocks, width, out.get());
+  if (width < 1 || width > 8) throw Error(kInternal, "Reducer: width must lie in [1, 8]");
+  reduce_parts_kernel<<<1, 32 * width, 0, ctx->stream>>>(part.get(), blocks, width, out.get());
   ++ctx->launches;
   STGP_LAUNCH_CHECK();
   std::vector<double> h(static_cast<size_t>(width));

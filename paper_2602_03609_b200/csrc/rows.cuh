@@ -915,17 +915,33 @@ static __global__ void __launch_bounds__(256) row_part_reduce_kernel(const doubl
 }
 
 // Sum per-block partials in a fixed order: out[q] = sum_b part[b][q] (compensated).
+// Compensated (Kahan) sum of the per-block partials, one warp per column: lane l sums blocks l, l + 32,
+// ... in order, then lane 0 sums the 32 lane sums and their compensations in lane order (fixed order:
+// deterministic; the dependent add chain is 1/32 of the one-thread loop's).
 static __global__ void reduce_parts_kernel(const double* part, int nblocks, int width, double* out) {
-  const int q = threadIdx.x;
+  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (q >= width) return;
   double s = 0.0, c = 0.0;
-  for (int b = 0; b < nblocks; ++b) {
+  for (int b = lane; b < nblocks; b += 32) {
     const double y = part[static_cast<size_t>(b) * width + q] - c;
     const double t = s + y;
     c = (t - s) - y;
     s = t;
   }
-  out[q] = s;
+  __shared__ double ls[8][32], lc[8][32];
+  ls[q][lane] = s;
+  lc[q][lane] = c;
+  __syncwarp();
+  if (lane == 0) {
+    double S = 0.0, C = 0.0;
+    for (int l = 0; l < 64; ++l) {
+      const double y = (l < 32 ? ls[q][l] : -lc[q][l - 32]) - C;
+      const double t = S + y;
+      C = (t - S) - y;
+      S = t;
+    }
+    out[q] = S;
+  }
 }
 
 }  // namespace stgp
