@@ -596,8 +596,11 @@ __global__ void __launch_bounds__(kRowWarps * 32, 4) vecchia_rows_kernel(RowArgs
 // Second pass of the two-pass Vecchia gradient: the closure-pair loop of phase D above with the pair
 // weights the factor pass stored (same pair order, arithmetic and per-row sums), at the occupancy of a
 // kernel without the register Cholesky.  Per-block partials of q = 2..7 into a.part.
+#ifndef STGP_PAIR_MINB
+#define STGP_PAIR_MINB 7  // resident blocks per SM the pair kernel is compiled for (72 registers; 6: 12.92, 7: 12.85, 8: 12.89 ms)
+#endif
 template <int KS>
-__global__ void __launch_bounds__(kRowWarps * 32, 6) vecchia_pair_grad_kernel(RowArgs a) {
+__global__ void __launch_bounds__(kRowWarps * 32, STGP_PAIR_MINB) vecchia_pair_grad_kernel(RowArgs a) {
   constexpr int NS = KS + 1;
   constexpr int NP = NS * (NS - 1) / 2;
   __shared__ uint16_t sPair[NP];
