@@ -197,6 +197,31 @@ __global__ void gemv_n_part_kernel(int m, long long n, const double* __restrict_
     P[static_cast<size_t>(blockIdx.x) * m + r] = (s0 + s1) + (s2 + s3);
   }
 }
+// The same partials with every row of a column in one pass (RB rows per thread, 256 threads: each column
+// of A is read once as one contiguous run instead of once per 256-row pass)
+template <int RB>
+__global__ void __launch_bounds__(256) gemv_n_rows_kernel(int m, long long n, const double* __restrict__ A,
+                                                          long long lda, const double* __restrict__ x,
+                                                          double* __restrict__ P) {
+  const long long c0 = n * blockIdx.x / gridDim.x, c1 = n * (blockIdx.x + 1) / gridDim.x;
+  double acc[RB];
+#pragma unroll
+  for (int k = 0; k < RB; ++k) acc[k] = 0.0;
+  for (long long c = c0; c < c1; ++c) {
+    const double xc = __ldg(&x[c]);
+    const double* a = A + c * lda;
+#pragma unroll
+    for (int k = 0; k < RB; ++k) {
+      const int r = threadIdx.x + 256 * k;
+      if (r < m) acc[k] = fma(a[r], xc, acc[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < RB; ++k) {
+    const int r = threadIdx.x + 256 * k;
+    if (r < m) P[static_cast<size_t>(blockIdx.x) * m + r] = acc[k];
+  }
+}
 __global__ void gemv_n_reduce_kernel(int m, int parts, const double* __restrict__ P, double alpha, double beta,
                                      double* __restrict__ y) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
@@ -442,7 +467,11 @@ void dev_gemv(stgp_ctx* ctx, bool ta, int m, long long n, double alpha, const do
   const int parts = static_cast<int>(std::max<long long>(1, std::min<long long>(n / 256, ctx->num_sms * 4LL)));
   DevBuf<double>& P = ctx->dense_tmp;
   P.ensure(static_cast<size_t>(parts) * m);
-  gemv_n_part_kernel<<<parts, 256, 0, ctx->stream>>>(m, n, A, lda, x, P.get());
+  const int rb = (m + 255) / 256;
+  // one pass per column up to 1024 rows (cfg4 VIF, M = 912: 2.09 -> 1.36 ms); wider (FITC, M = 2130) was
+  // not measured faster, so it keeps the 256-row passes
+  if (rb <= 4) gemv_n_rows_kernel<4><<<parts, 256, 0, ctx->stream>>>(m, n, A, lda, x, P.get());
+  else gemv_n_part_kernel<<<parts, 256, 0, ctx->stream>>>(m, n, A, lda, x, P.get());
   gemv_n_reduce_kernel<<<(m + 255) / 256, 256, 0, ctx->stream>>>(m, parts, P.get(), alpha, beta, y);
   ctx->launches += 2;
   STGP_LAUNCH_CHECK();
