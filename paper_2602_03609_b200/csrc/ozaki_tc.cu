@@ -38,9 +38,9 @@ constexpr int kBK = 32;      // int8 K per stage (one MMA K step, one 32-byte sw
 #ifndef STGP_TC_STAGES_MAX
 #define STGP_TC_STAGES_MAX 4
 #endif
-template <int S>
+template <int S, int BN = 64>
 constexpr int stages_for() {
-  constexpr int fit = (220 * 1024) / (S * (128 * 32 + 64 * 32));
+  constexpr int fit = (220 * 1024) / (S * (128 * 32 + BN * 32));
   return fit < STGP_TC_STAGES_MAX ? fit : STGP_TC_STAGES_MAX;
 }
 constexpr int kThreads = 192;
@@ -174,20 +174,26 @@ __device__ __forceinline__ void chunk_range(const TcArgs& a, int g, int& c0, int
 // Y tile (same ry) each load 64 / CX of its rows likewise.  A stage slot is written by the CTA's X
 // group and Y group (CX + CY - 1 CTAs), so each CTA's MMA commit arrives on the empty barrier of every
 // CTA of both groups.  Items are cluster items (x group, y group, split group).
-template <int S, int CX, int CY>
+// BN: Y rows per tile (64, or 32 with two TMEM accumulator sets so that the epilogue of one item
+// overlaps the MMAs of the next: S * 32 * 2 <= 512 columns).
+template <int S, int CX, int CY, int BN = kBN>
 __global__ void __launch_bounds__(kThreads, 1)
     ozaki_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy, TcArgs a) {
   constexpr int CL = CX * CY;
+  constexpr int kTY = BN * kBK;                 // bytes of one Y slice tile
+  constexpr int NSET = BN == kBN ? 1 : 2;       // TMEM accumulator sets
+  constexpr int kTPer = 256 / BN;               // Y slices per MMA (N <= 256)
+  static_assert(NSET * S * BN <= 512, "TMEM columns");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte aligned stage buffers: [stage][X slices S x 4 KB | Y slices S x 2 KB]
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int kStageBytes = S * (kTileX + kTileY);
-  constexpr int kStages = stages_for<S>();
+  constexpr int kStageBytes = S * (kTileX + kTY);
+  constexpr int kStages = stages_for<S, BN>();
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
-  uint64_t* tmem_full = empty + kStages;
-  uint64_t* tmem_empty = tmem_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+  uint64_t* tmem_full = empty + kStages;   // [2]
+  uint64_t* tmem_empty = tmem_full + 2;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = CL > 1 ? static_cast<int>(cluster_rank()) : 0;
@@ -203,8 +209,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], CX + CY - 1);
     }
-    mbar_init(tmem_full, 1);
-    mbar_init(tmem_empty, 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tmem_full[i], 1);
+      mbar_init(&tmem_empty[i], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {  // TMEM: 512 columns (S diagonals x 64)
@@ -248,11 +256,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int t = 1; t <= S; ++t) {
               if (CX == 1)
-                tma_load4(&tmy, st + S * kTileX + (t - 1) * kTileY, &full[stage], kb * kBK, a.y_rev ? S - t : t - 1,
-                          yt * kBN, c);
+                tma_load4(&tmy, st + S * kTileX + (t - 1) * kTY, &full[stage], kb * kBK, a.y_rev ? S - t : t - 1,
+                          yt * BN, c);
               else
-                tma_load4_mc(&tmy, st + S * kTileX + (t - 1) * kTileY + rx * (kTileY / CX), &full[stage], kb * kBK,
-                             a.y_rev ? S - t : t - 1, yt * kBN + rx * (kBN / CX), c, mask_y);
+                tma_load4_mc(&tmy, st + S * kTileX + (t - 1) * kTY + rx * (kTY / CX), &full[stage], kb * kBK,
+                             a.y_rev ? S - t : t - 1, yt * BN + rx * (BN / CX), c, mask_y);
             }
             if (++stage == kStages) {
               stage = 0;
@@ -265,16 +273,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- MMA issuer ----
     if (lane == 0) {
       int stage = 0;
-      uint32_t phase = 0, te_phase = 0;
+      uint32_t phase = 0, acc_n = 0;  // acc_n: accumulations issued (set = acc_n % NSET)
       for (int it = cid; it < a.nitems; it += ncl) {
         const int4 job = a.items[it];
         int c0, c1;
         chunk_range(a, job.z, c0, c1);
         const int kb0 = job.w & 0xffff, kb1 = job.w ? job.w >> 16 : a.kblocks;
-        for (int c = c0; c < c1; ++c) {
-          mbar_wait(tmem_empty, te_phase ^ 1);  // the epilogue has read the previous accumulators
-          te_phase ^= 1;
+        for (int c = c0; c < c1; ++c, ++acc_n) {
+          const int set = NSET == 1 ? 0 : static_cast<int>(acc_n & 1);
+          const uint32_t sph = NSET == 1 ? (acc_n & 1) : ((acc_n >> 1) & 1);
+          mbar_wait(&tmem_empty[set], sph ^ 1);  // the epilogue has read this set's previous accumulators
           tc_fence_after();
+          const uint32_t tset = tmem + static_cast<uint32_t>(set * S * BN);
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
@@ -287,12 +297,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t da = smem_desc(sbase + (s - 1) * kTileX);
               const int nt = S + 1 - s;
 #pragma unroll
-              for (int t0 = 1; t0 <= nt; t0 += 4) {
-                const int cnt = nt - t0 + 1 < 4 ? nt - t0 + 1 : 4;
-                const uint64_t db = smem_desc(sbase + S * kTileX + (t0 - 1) * kTileY);
+              for (int t0 = 1; t0 <= nt; t0 += kTPer) {
+                const int cnt = nt - t0 + 1 < kTPer ? nt - t0 + 1 : kTPer;
+                const uint64_t db = smem_desc(sbase + S * kTileX + (t0 - 1) * kTY);
                 // diagonals s + t0 - 2 ..; the first product (s = 1) of the chunk's first K step starts them
-                STGP_DCHECK((s + t0 - 2 + cnt) * kBN <= 512);
-                mma_i8(tmem + (s + t0 - 2) * kBN, da, db, (kb > kb0 || s > 1) ? 1u : 0u, idesc_i8(kBN * cnt));
+                STGP_DCHECK(set * S * BN + (s + t0 - 2 + cnt) * BN <= 512);
+                mma_i8(tset + (s + t0 - 2) * BN, da, db, (kb > kb0 || s > 1) ? 1u : 0u, idesc_i8(BN * cnt));
               }
             }
             if (CL == 1) mma_commit(&empty[stage]);  // frees the stage once these MMAs have read it
@@ -302,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               phase ^= 1;
             }
           }
-          mma_commit(tmem_full);
+          mma_commit(&tmem_full[set]);
         }
       }
     }
@@ -311,34 +321,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- epilogue: warps 2..5, TMEM lanes 32 (warp % 4) .. + 31 ----
     const int quarter = warp & 3;
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    uint32_t tf_phase = 0;
+    uint32_t acc_n = 0;  // accumulations consumed, as issued
     for (int it = cid; it < a.nitems; it += ncl) {
       const int4 job = a.items[it];
       int c0, c1;
       chunk_range(a, job.z, c0, c1);
       const int x = (job.x * CX + rx) * kBM + quarter * 32 + lane;
-      const int y0 = (job.y * CY + ry) * kBN;
+      const int y0 = (job.y * CY + ry) * BN;
       if (!a.cols) {
         // rows form (one chunk, written once): per 8 columns the S diagonals are read with one wait,
         // combined, scaled and stored; the accumulators are released as soon as the last read lands.
         // Same operations and order as the column form's combine (bit-identical results).
-        mbar_wait(tmem_full, tf_phase);
-        tf_phase ^= 1;
+        const int set = NSET == 1 ? 0 : static_cast<int>(acc_n & 1);
+        mbar_wait(&tmem_full[set], NSET == 1 ? (acc_n & 1) : ((acc_n >> 1) & 1));
+        ++acc_n;
         tc_fence_after();
+        const uint32_t lset = lane_addr + static_cast<uint32_t>(set * S * BN);
         const double sxv = x < a.nx ? a.sx[x] : 0.0;
         double* o = a.out + static_cast<long long>(x) * a.ldo + y0;
-        const int ny = min(kBN, a.ny - y0);
-        const bool vec = ny == kBN && (reinterpret_cast<uintptr_t>(o) & 15) == 0;
+        const int ny = min(BN, a.ny - y0);
+        const bool vec = ny == BN && (reinterpret_cast<uintptr_t>(o) & 15) == 0;
 #pragma unroll
-        for (int q = 0; q < kBN / 8; ++q) {
+        for (int q = 0; q < BN / 8; ++q) {
           int v[S][8];
 #pragma unroll
-          for (int d = 0; d < S; ++d) tmem_ld8(lane_addr + d * kBN + q * 8, v[d]);
+          for (int d = 0; d < S; ++d) tmem_ld8(lset + d * BN + q * 8, v[d]);
           tmem_wait_ld();
-          if (q == kBN / 8 - 1) {
+          if (q == BN / 8 - 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(tmem_empty);
+            if (lane == 0) mbar_arrive(&tmem_empty[set]);
           }
           double sq[8];
           double w = 0x1p-14;
@@ -368,16 +380,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         continue;
       }
-      double acc[kBN];
+      double acc[BN];
 #pragma unroll
-      for (int e = 0; e < kBN; ++e) acc[e] = 0.0;
+      for (int e = 0; e < BN; ++e) acc[e] = 0.0;
       for (int c = c0; c < c1; ++c) {
-        mbar_wait(tmem_full, tf_phase);
-        tf_phase ^= 1;
+        const int set = NSET == 1 ? 0 : static_cast<int>(acc_n & 1);
+        mbar_wait(&tmem_full[set], NSET == 1 ? (acc_n & 1) : ((acc_n >> 1) & 1));
+        ++acc_n;
         tc_fence_after();
+        const uint32_t lset = lane_addr + static_cast<uint32_t>(set * S * BN);
         const double sxv = x < a.nx ? a.sx[static_cast<size_t>(a.cols ? c : 0) * a.nx + x] : 0.0;
 #pragma unroll
-        for (int q = 0; q < kBN / 16; ++q) {
+        for (int q = 0; q < BN / 16; ++q) {
           // smallest diagonal first: exact products by powers of two, one rounding per add
           double sq[16];
           double w = 0x1p-14;
@@ -386,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int d = S - 1; d >= 0; --d) {
             int v[16];
-            tmem_ld16(lane_addr + d * kBN + q * 16, v);
+            tmem_ld16(lset + d * BN + q * 16, v);
             tmem_wait_ld();
 #pragma unroll
             for (int e = 0; e < 16; ++e) sq[e] = d == S - 1 ? static_cast<double>(v[e]) * w : fma(static_cast<double>(v[e]), w, sq[e]);
@@ -402,17 +416,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tmem_empty);
+        if (lane == 0) mbar_arrive(&tmem_empty[set]);
       }
       if (x < a.nx) {
         double* o = a.out + (a.cols && a.groups > 1 ? job.z * a.part_stride : 0) + static_cast<long long>(x) * a.ldo + y0;
-        const int ny = min(kBN, a.ny - y0);
-        if (ny == kBN && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+        const int ny = min(BN, a.ny - y0);
+        if (ny == BN && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
 #pragma unroll
-          for (int e = 0; e < kBN; e += 2) *reinterpret_cast<double2*>(o + e) = make_double2(acc[e], acc[e + 1]);
+          for (int e = 0; e < BN; e += 2) *reinterpret_cast<double2*>(o + e) = make_double2(acc[e], acc[e + 1]);
         } else {
 #pragma unroll
-          for (int e = 0; e < kBN; ++e)
+          for (int e = 0; e < BN; ++e)
             if (e < ny) o[e] = acc[e];
         }
       }
@@ -479,14 +493,14 @@ CUtensorMap make_map(const int8_t* base, long long kext, int S, long long rows, 
   return m;
 }
 
-template <int S, int CX, int CY>
+template <int S, int CX, int CY, int BN = kBN>
 void launch_tc(stgp_ctx* ctx, const CUtensorMap& tx, const CUtensorMap& ty, const TcArgs& a) {
   constexpr int CL = CX * CY;
   // at least 116 KB so that one CTA holds an SM: it owns all 512 TMEM columns
-  constexpr int smem = std::max(stages_for<S>() * S * (kTileX + kTileY) + 1024 + 256, 116 * 1024);
+  constexpr int smem = std::max(stages_for<S, BN>() * S * (kTileX + BN * kBK) + 1024 + 256, 116 * 1024);
   static int max_clusters = 0;
   if (max_clusters == 0) {
-    STGP_CUDA(cudaFuncSetAttribute(ozaki_tc_kernel<S, CX, CY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    STGP_CUDA(cudaFuncSetAttribute(ozaki_tc_kernel<S, CX, CY, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     max_clusters = ctx->num_sms / CL;
     if (CL > 1) {
       cudaLaunchConfig_t q{};
@@ -501,7 +515,7 @@ void launch_tc(stgp_ctx* ctx, const CUtensorMap& tx, const CUtensorMap& ty, cons
       q.attrs = at;
       q.numAttrs = 1;
       int mc = 0;
-      if (cudaOccupancyMaxActiveClusters(&mc, ozaki_tc_kernel<S, CX, CY>, &q) == cudaSuccess && mc > 0)
+      if (cudaOccupancyMaxActiveClusters(&mc, ozaki_tc_kernel<S, CX, CY, BN>, &q) == cudaSuccess && mc > 0)
         max_clusters = mc;
       (void)cudaGetLastError();
     }
@@ -519,20 +533,20 @@ void launch_tc(stgp_ctx* ctx, const CUtensorMap& tx, const CUtensorMap& ty, cons
   cfg.stream = ctx->stream;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  STGP_CUDA(cudaLaunchKernelEx(&cfg, ozaki_tc_kernel<S, CX, CY>, tx, ty, a));
+  STGP_CUDA(cudaLaunchKernelEx(&cfg, ozaki_tc_kernel<S, CX, CY, BN>, tx, ty, a));
   launched(ctx);
 }
 
-template <int CX, int CY>
+template <int CX, int CY, int BN = kBN>
 void dispatch(stgp_ctx* ctx, int S, const CUtensorMap& tx, const CUtensorMap& ty, const TcArgs& a) {
   switch (S) {
-    case 2: launch_tc<2, CX, CY>(ctx, tx, ty, a); break;
-    case 3: launch_tc<3, CX, CY>(ctx, tx, ty, a); break;
-    case 4: launch_tc<4, CX, CY>(ctx, tx, ty, a); break;
-    case 5: launch_tc<5, CX, CY>(ctx, tx, ty, a); break;
-    case 6: launch_tc<6, CX, CY>(ctx, tx, ty, a); break;
-    case 7: launch_tc<7, CX, CY>(ctx, tx, ty, a); break;
-    case 8: launch_tc<8, CX, CY>(ctx, tx, ty, a); break;
+    case 2: launch_tc<2, CX, CY, BN>(ctx, tx, ty, a); break;
+    case 3: launch_tc<3, CX, CY, BN>(ctx, tx, ty, a); break;
+    case 4: launch_tc<4, CX, CY, BN>(ctx, tx, ty, a); break;
+    case 5: launch_tc<5, CX, CY, BN>(ctx, tx, ty, a); break;
+    case 6: launch_tc<6, CX, CY, BN>(ctx, tx, ty, a); break;
+    case 7: launch_tc<7, CX, CY, BN>(ctx, tx, ty, a); break;
+    case 8: launch_tc<8, CX, CY, BN>(ctx, tx, ty, a); break;
     default: throw Error(kConfig, "ozaki_tc: slice count must lie in [2, 8]");
   }
 }
@@ -569,7 +583,14 @@ TcCluster cluster_shape(TcForm f) {
   return c;
 }
 
-void run(stgp_ctx* ctx, int S, TcCluster c, const CUtensorMap& tx, const CUtensorMap& ty, const TcArgs& a) {
+void run(stgp_ctx* ctx, int S, TcCluster c, const CUtensorMap& tx, const CUtensorMap& ty, const TcArgs& a,
+         int bn = kBN) {
+  if (bn == 32) {  // rows form with two TMEM sets (1-D clusters only)
+    if (c.cy == 4) dispatch<1, 4, 32>(ctx, S, tx, ty, a);
+    else if (c.cy == 2) dispatch<1, 2, 32>(ctx, S, tx, ty, a);
+    else dispatch<1, 1, 32>(ctx, S, tx, ty, a);
+    return;
+  }
   if (c.cx == 2) {
     if (c.cy == 2) dispatch<2, 2>(ctx, S, tx, ty, a);
     else dispatch<2, 1>(ctx, S, tx, ty, a);
@@ -607,14 +628,20 @@ void ozaki_tc_rows(stgp_ctx* ctx, OzakiTcState*& st, int S, int kp, long long nx
   OzakiTcState* s = tc_state(st);
   const long long ldk = static_cast<long long>(S) * kp;
   const TcCluster cs = cluster_shape(TcForm::kRows);
+  // Y tiles of 32 rows with two TMEM accumulator sets (STGP_OZAKI_ROWS_BN=32; 1-D clusters) or of 64
+  static const int env_bn = [] {
+    const char* e = std::getenv("STGP_OZAKI_ROWS_BN");
+    return e && std::atoi(e) == 32 ? 32 : kBN;
+  }();
+  const int bn = cs.cx == 1 ? env_bn : kBN;
   const CUtensorMap tx = make_map(xd, kp, S, nx, 1, kp, ldk, nx * ldk, kBM / cs.cy);
-  const CUtensorMap ty = make_map(yd, kp, S, ny, 1, kp, ldk, static_cast<long long>(ny) * ldk, kBN / cs.cx);
-  const int tiles_x = static_cast<int>((nx + kBM - 1) / kBM), tiles_y = (ny + kBN - 1) / kBN;
+  const CUtensorMap ty = make_map(yd, kp, S, ny, 1, kp, ldk, static_cast<long long>(ny) * ldk, bn / cs.cx);
+  const int tiles_x = static_cast<int>((nx + kBM - 1) / kBM), tiles_y = (ny + bn - 1) / bn;
   const int groups_x = (tiles_x + cs.cx - 1) / cs.cx, groups_y = (tiles_y + cs.cy - 1) / cs.cy;
   const int kblocks = kp / kBK;
   std::vector<int> krange(groups_y, 0);
   for (int gy = 0; tri && gy < groups_y; ++gy) {
-    const int y0 = gy * cs.cy * kBN, y1 = std::min(ny, (gy + 1) * cs.cy * kBN);  // rows [y0, y1)
+    const int y0 = gy * cs.cy * bn, y1 = std::min(ny, (gy + 1) * cs.cy * bn);  // rows [y0, y1)
     const int kb0 = tri == 2 ? y0 / kBK : 0;
     const int kb1 = tri == 1 ? std::min(kblocks, (y1 + kBK - 1) / kBK) : kblocks;
     krange[gy] = kb0 | (kb1 << 16);
@@ -646,7 +673,7 @@ void ozaki_tc_rows(stgp_ctx* ctx, OzakiTcState*& st, int S, int kp, long long nx
   a.sy = sy;
   a.out = out;
   a.ldo = ldo;
-  run(ctx, S, cs, tx, ty, a);
+  run(ctx, S, cs, tx, ty, a, bn);
 }
 
 // cols form: C[x ldc + y] = sum_c (sx[c m + x] sy[c m + y]) sum_d 2^-7d sum_{s+t=d} X_s,c[x] . Y_t,c[y];
